@@ -1,0 +1,197 @@
+/* mgnn.h -- C ABI of the B200 halo feature pipeline of arXiv 2410.22697
+ * ("MassiveGNN": continuous prefetch + eviction for distributed GNN minibatch
+ * training).  PAPER.md line refs are "P:n"; readings "R#n" are listed in
+ * DESIGN.md §Readings.
+ *
+ * One mgnn_ctx lives in one process and drives one GPU.  It hosts one or more
+ * partitions p ("trainers"), each with its own CSR, feature table
+ * (the KVStore), prefetch buffer BUF_p and scoreboards S_E, S_A
+ * (P:111).  The unit of work is a WINDOW: `n_steps` consecutive global steps
+ * t0..t0+n_steps-1 for every hosted partition ("instances" m = lp*n_steps+w).
+ * A window may contain an eviction step (t % Delta == 0, R#14) only as its
+ * last step, so buffer membership is constant inside it and the result is
+ * bit-identical to running PREFETCH_WITH_EVICTION (Alg.2) step by step.
+ *
+ * Every call returns mgnn_status and never aborts.  EINVAL leaves the state
+ * unchanged.  CUDA errors are sticky: the ctx is poisoned and every later call
+ * returns MGNN_ECUDA (mgnn_last_error explains).  A ctx belongs to one host
+ * thread; its device work is ordered on the stream the caller passes, so pass
+ * the same stream to every call (or order streams with events).
+ * All device memory is owned by the library; window outputs are exposed as
+ * device pointers valid until the same window slot is sampled again.
+ */
+#ifndef MGNN_H
+#define MGNN_H
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MGNN_API __attribute__((visibility("default")))
+#else
+#define MGNN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mgnn_ctx_s* mgnn_ctx;
+typedef void* mgnn_stream;  /* a cudaStream_t (0 = legacy default stream) */
+
+typedef enum {
+    MGNN_OK = 0,
+    MGNN_EINVAL = 1,    /* bad argument; no state change */
+    MGNN_ENOMEM = 2,    /* device allocation failed */
+    MGNN_ECUDA = 3,     /* CUDA error (sticky) */
+    MGNN_ESTATE = 5,    /* call-order violation (e.g. gather before sample) */
+    MGNN_EOVERFLOW = 6  /* a device-side size exceeded its arena bound (sticky) */
+} mgnn_status;
+
+#define MGNN_MAX_LAYERS 8
+#define MGNN_MAX_FANOUT 32
+#define MGNN_IPC_HANDLE_BYTES 64
+
+/* One partition p of G(V, E) (first-level partitioning).  Host memory,
+ * read during mgnn_partition_load only; the caller keeps ownership.
+ * V_p^l = [part_bounds[p], part_bounds[p+1]) (R#9). */
+typedef struct {
+    int32_t part_id;            /* p, 0 <= p < n_parts of the ctx */
+    const int64_t* indptr;      /* [n_local+1], indptr[0] == 0: local rows of the symmetric CSR */
+    const int32_t* cols;        /* [indptr[n_local]] global neighbour ids; each row strictly
+                                   ascending, no self loops (simple graph) */
+    const int32_t* train_ids;   /* [n_train] sorted, distinct, local training seeds */
+    int64_t n_train;
+} mgnn_partition_desc;
+
+/* Prefetcher policy (Table 1; Eq.1). */
+typedef struct {
+    float gamma;     /* decay rate gamma, 0 < gamma <= 1 */
+    float alpha;     /* eviction threshold alpha >= 0 (use mgnn_alpha_default for Eq.1, R#13) */
+    float theta_r;   /* replacement eligibility S_A >= theta_r (R#17) */
+    int32_t delta;   /* eviction interval Delta in steps; 0 = prefetch without eviction */
+    uint32_t f_bp;   /* f_p^h in basis points, 0..10000; |BUF| = ceil(f*|V_p^h|) (R#11) */
+} mgnn_policy;
+
+/* Per-instance counters (int64), layout of mgnn_counts_read rows. */
+enum {
+    MGNN_C_NODES = 0,      /* |F_L| (unique sampled nodes incl. seeds, R#23) */
+    MGNN_C_LOCAL = 1,      /* |F_L ∩ V_p^l|  (Alg.2 l.2) */
+    MGNN_C_HIT = 2,        /* |Hits|         (Alg.2 l.4) */
+    MGNN_C_MISS = 3,       /* |Misses|       (Alg.2 l.5) */
+    MGNN_C_EVICTED = 4,    /* k of the eviction round ending at this step (Alg.2 l.14) */
+    MGNN_C_REFILLED = 5,   /* = k (constant |BUF|) */
+    MGNN_C_ROWS_FETCHED = 6, /* remote rows this step = misses + refills */
+    MGNN_C_N = 8
+};
+
+/* Device view of one window slot.  Instance m = lp*n_steps + w holds global
+ * step t0+w of local partition lp.  All pointers are DEVICE pointers. */
+typedef struct {
+    int32_t n_inst, n_steps, n_parts_local, n_layers;
+    uint64_t step0;
+    int64_t rows_stride;        /* rows between consecutive instances in X / frontier */
+    int64_t pitch;              /* floats per X row (feat_dim rounded up to 4) */
+    const float* X;             /* [n_inst][rows_stride][pitch]: X[m][i] = feature row of F_L[i] (R#24) */
+    const int32_t* frontier;    /* [n_inst][rows_stride]: F_L as global ids (F_0 = seeds) */
+    const int64_t* hop_size;    /* [n_inst][MGNN_MAX_LAYERS+1]: |F_i|, i = 0..L */
+    const int64_t* offsets[MGNN_MAX_LAYERS];  /* hop i: [n_inst][off_stride[i]]: CSR offsets over F_i */
+    const int32_t* cols[MGNN_MAX_LAYERS];     /* hop i: [n_inst][col_stride[i]]: sampled neighbour as
+                                                 its POSITION in F_{i+1} (DGL block layout) */
+    int64_t off_stride[MGNN_MAX_LAYERS];
+    int64_t col_stride[MGNN_MAX_LAYERS];
+    const int64_t* counts;      /* [n_inst][MGNN_C_N] */
+} mgnn_window;
+
+/* Eq.1 with initial S_E = 1: alpha = gamma^Delta as the iterated fp32
+ * product (R#13).  Pure host function. */
+MGNN_API float mgnn_alpha_default(float gamma, int32_t delta);
+
+/* Create a context on CUDA device `device` for a graph of n_global nodes cut
+ * into n_parts contiguous ranges part_bounds[0..n_parts] (host array), with
+ * feat_dim-wide fp32 features synthesised from feat_seed (R#4; the synthetic
+ * stand-in for the dataset's node features). */
+MGNN_API mgnn_status mgnn_ctx_create(int32_t device, int32_t n_parts, int64_t n_global, const int64_t* part_bounds,
+                            int32_t feat_dim, uint64_t feat_seed, mgnn_ctx* out);
+MGNN_API void mgnn_destroy(mgnn_ctx ctx);
+MGNN_API const char* mgnn_last_error(mgnn_ctx ctx);
+
+/* Load partition p onto the device (synchronous, one-time):
+ * validates the CSR, builds V_p^h (sorted halo ids), deg_in (R#10), the
+ * local-rank relabelling of the CSR, the train seeds and the feature table.
+ * *local_index receives the partition's index lp among this ctx's partitions. */
+MGNN_API mgnn_status mgnn_partition_load(mgnn_ctx ctx, const mgnn_partition_desc* desc, int32_t* local_index);
+
+/* Feature tables of partitions hosted by OTHER processes (multi-GPU): export
+ * writes a CUDA IPC handle (MGNN_IPC_HANDLE_BYTES) of local partition p's
+ * table; import maps partition p's table from another process's handle so
+ * that miss / refill rows are read directly over NVLink (peer loads inside
+ * the gather kernels).  Tables of partitions in the same ctx need nothing. */
+MGNN_API mgnn_status mgnn_table_export(mgnn_ctx ctx, int32_t part_id, void* handle_out);
+MGNN_API mgnn_status mgnn_table_import(mgnn_ctx ctx, int32_t part_id, const void* handle);
+
+/* INITIALIZE_PREFETCHER (Alg.1) for every hosted partition:
+ * BUF = top ceil(f*|V_p^h|) halo nodes by (deg_in desc, id asc), rows fetched
+ * from their owners, S_E = 1, S_A = -1 (buffered) / 0 (other halo).  Needs
+ * every partition's table (local or imported), else ESTATE. */
+MGNN_API mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* policy, mgnn_stream stream);
+
+/* Sampler configuration and window arenas: fanouts in GNN-layer order, input
+ * layer first (R#2; hop i draws fanouts[n_layers-1-i]), batch size B, run seed
+ * of the counter-based Philox streams (R#4), and the largest window. */
+MGNN_API mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_layers, int32_t batch,
+                                uint64_t run_seed, int32_t max_window);
+
+/* NeighborSampler (Alg.2 l.1) for steps t0..t0+n_steps-1 of every hosted
+ * partition into window slot `slot` (0 or 1).  Seeds are the step's slice of
+ * the partition's epoch order (R#8) when seeds == NULL; otherwise seeds holds
+ * [n_parts_local][n_steps][batch] ids (the first seed_counts[lp*n_steps+w] of
+ * each row used), in host memory if seeds_on_host (copied inside the call,
+ * use pinned memory to keep it async) else device memory.  Uses no buffer
+ * state, so it may run ahead of the scoring of earlier windows. */
+MGNN_API mgnn_status mgnn_sample(mgnn_ctx ctx, int32_t slot, uint64_t t0, int32_t n_steps, const int32_t* seeds,
+                        const int32_t* seed_counts, int32_t seeds_on_host, mgnn_stream stream);
+
+/* Alg.2 l.2-5, l.10-11, l.21-22 for the window in `slot`: classify every node
+ * of F_L (local / hit / miss), gather its feature row into X (local table,
+ * BUF row, or the owner's table over NVLink for misses), record hits, tally
+ * S_A += 1 per miss, relabel the block columns to frontier positions. */
+MGNN_API mgnn_status mgnn_lookup_gather(mgnn_ctx ctx, int32_t slot, mgnn_stream stream);
+
+/* Alg.2 l.6-9 (decay of unused BUF entries, once per step of the window) and,
+ * if the window's last step is a multiple of Delta, EVICT_AND_REPLACE
+ * (l.12-19, l.25-34) with the swap of P:224 and the refill of the k new rows. */
+MGNN_API mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stream);
+
+/* Device view of a window slot (valid after mgnn_sample of that slot). */
+MGNN_API mgnn_status mgnn_window_get(mgnn_ctx ctx, int32_t slot, mgnn_window* out);
+
+/* Copy the window's counters ([n_inst][MGNN_C_N] int64) to host memory and
+ * synchronise `stream`. */
+MGNN_API mgnn_status mgnn_counts_read(mgnn_ctx ctx, int32_t slot, int64_t* host_counts, mgnn_stream stream);
+
+/* Host copies of local partition lp's prefetcher state (synchronous):
+ * node_ids[cap] (BUF in slot order), se[cap], sa[n_halo] and slot_of[n_halo]
+ * in halo-index (ascending id) order, rows[cap][feat_dim] (may be NULL). */
+MGNN_API mgnn_status mgnn_buffer_snapshot(mgnn_ctx ctx, int32_t lp, int32_t* node_ids, float* se, float* sa,
+                                 int32_t* slot_of, float* rows);
+/* Sizes of local partition lp: [0]=part_id [1]=n_local [2]=n_halo [3]=cap [4]=n_train. */
+MGNN_API mgnn_status mgnn_part_info(mgnn_ctx ctx, int32_t lp, int64_t* info5);
+/* Halo ids (sorted) and deg_in of local partition lp (synchronous). */
+MGNN_API mgnn_status mgnn_halo_get(mgnn_ctx ctx, int32_t lp, int32_t* halo_ids, int32_t* deg_in);
+/* Feature table row of a node hosted here (synchronous; tests). */
+MGNN_API mgnn_status mgnn_table_row(mgnn_ctx ctx, int64_t node, float* out);
+
+/* Kernel launches issued by this ctx since creation (bench evidence). */
+MGNN_API int64_t mgnn_launch_count(mgnn_ctx ctx);
+
+/* Optional CUDA-event timing of the gather kernel (the dominant HBM kernel):
+ * when enabled, each mgnn_lookup_gather brackets its gather launch with events
+ * on the caller's stream; read returns the summed milliseconds, the number of
+ * launches timed and the algorithmic bytes they moved (2 * rows * feat_dim * 4),
+ * and resets them (synchronises the events). */
+MGNN_API mgnn_status mgnn_profile_enable(mgnn_ctx ctx, int32_t enable);
+MGNN_API mgnn_status mgnn_profile_read(mgnn_ctx ctx, double* ms, int64_t* launches, int64_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

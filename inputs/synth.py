@@ -158,7 +158,9 @@ def generate(cfg: GraphConfig, cache_dir: Optional[str] = "/tmp/mgnn_inputs") ->
     train_mask = rng.random(n) < cfg.train_frac
     g = Graph(n, indptr, cols, train_mask)
     if path:
-        np.savez(path, indptr=indptr, cols=cols, train_mask=train_mask)
+        tmp = f"{path}.{os.getpid()}.tmp.npz"
+        np.savez(tmp, indptr=indptr, cols=cols, train_mask=train_mask)
+        os.replace(tmp, path)
     return g
 
 

@@ -1,0 +1,91 @@
+"""ctypes binding of libmgnn.so (include/mgnn.h).  Argument marshalling only."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmgnn.so")
+
+MAX_LAYERS = 8
+IPC_HANDLE_BYTES = 64
+C_NODES, C_LOCAL, C_HIT, C_MISS, C_EVICTED, C_REFILLED, C_ROWS_FETCHED, C_N = 0, 1, 2, 3, 4, 5, 6, 8
+STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 5: "ESTATE", 6: "EOVERFLOW"}
+
+# every symbol include/mgnn.h declares (checked by tests/test_abi.py)
+SYMBOLS = [
+    "mgnn_alpha_default", "mgnn_ctx_create", "mgnn_destroy", "mgnn_last_error", "mgnn_partition_load",
+    "mgnn_table_export", "mgnn_table_import", "mgnn_buffer_init", "mgnn_sampler_config", "mgnn_sample",
+    "mgnn_lookup_gather", "mgnn_score_evict_refill", "mgnn_window_get", "mgnn_counts_read",
+    "mgnn_buffer_snapshot", "mgnn_part_info", "mgnn_halo_get", "mgnn_table_row", "mgnn_launch_count",
+    "mgnn_profile_enable", "mgnn_profile_read",
+]
+
+
+class PartitionDesc(C.Structure):
+    _fields_ = [("part_id", C.c_int32), ("indptr", C.c_void_p), ("cols", C.c_void_p),
+                ("train_ids", C.c_void_p), ("n_train", C.c_int64)]
+
+
+class Policy(C.Structure):
+    _fields_ = [("gamma", C.c_float), ("alpha", C.c_float), ("theta_r", C.c_float),
+                ("delta", C.c_int32), ("f_bp", C.c_uint32)]
+
+
+class Window(C.Structure):
+    _fields_ = [("n_inst", C.c_int32), ("n_steps", C.c_int32), ("n_parts_local", C.c_int32),
+                ("n_layers", C.c_int32), ("step0", C.c_uint64), ("rows_stride", C.c_int64),
+                ("pitch", C.c_int64), ("X", C.c_void_p), ("frontier", C.c_void_p), ("hop_size", C.c_void_p),
+                ("offsets", C.c_void_p * MAX_LAYERS), ("cols", C.c_void_p * MAX_LAYERS),
+                ("off_stride", C.c_int64 * MAX_LAYERS), ("col_stride", C.c_int64 * MAX_LAYERS),
+                ("counts", C.c_void_p)]
+
+
+class MgnnError(RuntimeError):
+    def __init__(self, fn: str, status: int, msg: str):
+        super().__init__(f"{fn}: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libmgnn.so; raises if it is missing (no fallback of any kind)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libmgnn.so not built at {path}: run python -m paper_2410_22697_b200.build")
+    L = C.CDLL(path)
+    P, I32, I64, U32, U64, F32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_float
+    S = C.c_int
+    sig = {
+        "mgnn_alpha_default": (F32, [F32, I32]),
+        "mgnn_ctx_create": (S, [I32, I32, I64, P, I32, U64, P]),
+        "mgnn_destroy": (None, [P]),
+        "mgnn_last_error": (C.c_char_p, [P]),
+        "mgnn_partition_load": (S, [P, P, P]),
+        "mgnn_table_export": (S, [P, I32, P]),
+        "mgnn_table_import": (S, [P, I32, P]),
+        "mgnn_buffer_init": (S, [P, P, P]),
+        "mgnn_sampler_config": (S, [P, P, I32, I32, U64, I32]),
+        "mgnn_sample": (S, [P, I32, U64, I32, P, P, I32, P]),
+        "mgnn_lookup_gather": (S, [P, I32, P]),
+        "mgnn_score_evict_refill": (S, [P, I32, P]),
+        "mgnn_window_get": (S, [P, I32, P]),
+        "mgnn_counts_read": (S, [P, I32, P, P]),
+        "mgnn_buffer_snapshot": (S, [P, I32, P, P, P, P, P]),
+        "mgnn_part_info": (S, [P, I32, P]),
+        "mgnn_halo_get": (S, [P, I32, P, P]),
+        "mgnn_table_row": (S, [P, I64, P]),
+        "mgnn_launch_count": (I64, [P]),
+        "mgnn_profile_enable": (S, [P, I32]),
+        "mgnn_profile_read": (S, [P, P, P, P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L

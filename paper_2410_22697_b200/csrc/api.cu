@@ -1,0 +1,945 @@
+// api.cu -- the C ABI of include/mgnn.h: context, partition load, buffer
+// init, window arenas and the three per-window calls.  Host code only
+// marshals sizes/pointers and launches the kernels of sample.cu, gather.cu,
+// score.cu, sort.cu and load.cu; every step of the path runs on the GPU.
+#include <atomic>
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mgnn.h"
+#include "launch.h"
+
+namespace mgnn {
+static std::atomic<long long> g_launches{0};
+static const bool g_debug_sync = [] {
+    const char* e = getenv("MGNN_DEBUG_SYNC");
+    return e && e[0] == '1';
+}();
+void count_launches(long long n, const char* who) {
+    g_launches.fetch_add(n, std::memory_order_relaxed);
+    if (g_debug_sync) {
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) fprintf(stderr, "[mgnn] %s failed: %s\n", who, cudaGetErrorString(e));
+    }
+}
+long long launches_total() { return g_launches.load(); }
+}  // namespace mgnn
+
+using namespace mgnn;
+
+namespace {
+
+struct Part {
+    int32_t part_id = -1;
+    int64_t lo = 0, n_local = 0, n_h = 0, h_below = 0, nnz = 0, n_train = 0, cap = 0, nbatch = 1;
+    int32_t perm_slots = 0;
+    int64_t* indptr = nullptr;
+    int32_t* cols_rank = nullptr;
+    int32_t* halo = nullptr;
+    int32_t* deg_in = nullptr;
+    int32_t* train = nullptr;
+    float* table = nullptr;
+    float* rows = nullptr;
+    float* se = nullptr;
+    float* sa = nullptr;
+    int32_t* slot_of = nullptr;
+    int32_t* slot_h = nullptr;
+    unsigned long long* hitmask = nullptr;
+    int32_t* perm = nullptr;
+    std::vector<int64_t> perm_epoch;     // epoch held by each perm slot (-1 none)
+    // sort buffers: E (cap) / R (n_h) for eviction; R also serves buffer init; P (n_train) for epoch orders
+    unsigned long long *ek = nullptr, *ekt = nullptr, *rk = nullptr, *rkt = nullptr, *pk = nullptr, *pkt = nullptr;
+    uint32_t *ev = nullptr, *evt = nullptr, *rv = nullptr, *rvt = nullptr, *pvt = nullptr;
+};
+
+struct Win {
+    bool alloc = false, sampled = false, gathered = false, scored = false;
+    int32_t n_steps = 0;
+    uint64_t step0 = 0;
+    int32_t* fr_rank = nullptr;
+    int32_t* fr_gid = nullptr;
+    int64_t* hop_size = nullptr;
+    int64_t* off[kMaxLayers] = {};
+    int32_t* cols[kMaxLayers] = {};
+    float* X = nullptr;
+    int32_t* pos_of = nullptr;
+    uint32_t* nb = nullptr;
+    char* zero = nullptr;           // [scan scratch | counts | fb], zeroed per window
+    size_t zero_bytes = 0;
+    unsigned long long* status = nullptr;
+    int32_t* tilectr = nullptr;
+    long long* counts = nullptr;
+    uint32_t* fb = nullptr;
+    int32_t* ext_seeds = nullptr;
+    int32_t* ext_counts = nullptr;
+    // scratch sub-regions
+    Scratch sc_count[kMaxLayers], sc_compact[kMaxLayers];
+};
+
+}  // namespace
+
+struct mgnn_ctx_s {
+    int device = 0;
+    int32_t P = 0;
+    int64_t n_global = 0;
+    std::vector<int64_t> bounds;
+    int32_t D = 0, pitch = 0;
+    uint64_t feat_seed = 0;
+    std::vector<Part> parts;
+    std::vector<int32_t> lp_of;          // part id -> local index or -1
+    std::vector<const float*> tables;    // device-accessible table per partition
+    std::vector<void*> ipc_opened;
+    int64_t* d_bounds = nullptr;
+    const float** d_tables = nullptr;
+    PartDev* d_parts = nullptr;
+    int32_t* d_err = nullptr;
+    long long* d_gathered = nullptr;
+    // policy
+    bool buffer_ready = false;
+    mgnn_policy pol{};
+    // eviction scratch
+    SortSeg* d_evsegs = nullptr;
+    long long* d_sel_n = nullptr;
+    char* ev_zero = nullptr;
+    size_t ev_zero_bytes = 0;
+    Scratch ev_sc{};
+    int64_t ev_tiles = 1;
+    uint32_t* hist = nullptr;
+    size_t hist_words = 0;
+    // sampler
+    bool configured = false;
+    int32_t L = 0, batch = 0, max_window = 0;
+    int32_t fan[kMaxLayers] = {}, k_hop[kMaxLayers] = {};
+    uint64_t run_seed = 0;
+    int64_t ucap = 0, vp_max = 0, bm_words = 0;
+    int64_t fcap[kMaxLayers + 1] = {}, ecap[kMaxLayers] = {};
+    Win win[2];
+    SortSeg* d_permsegs = nullptr;       // [n_lp][max perm slots]
+    int32_t perm_slots_max = 0;
+    long long* d_perm_n = nullptr;       // [n_lp]
+    // ordering of windows through the buffer
+    bool seq_started = false;
+    uint64_t next_step = 0;
+    // status
+    int sticky = MGNN_OK;
+    std::string err;
+    // profiling
+    bool prof = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
+    double prof_ms = 0.0;
+    long long prof_launches = 0;
+};
+
+namespace {
+
+mgnn_status fail(mgnn_ctx c, mgnn_status st, const std::string& msg) {
+    if (c) {
+        c->err = msg;
+        if (st == MGNN_ECUDA || st == MGNN_EOVERFLOW) c->sticky = st;
+    }
+    return st;
+}
+
+#define CK(call)                                                                                     \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess)                                                                       \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? MGNN_ENOMEM : MGNN_ECUDA,            \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                        \
+    } while (0)
+
+#define CKL()                                                                                        \
+    do {                                                                                             \
+        cudaError_t e_ = cudaGetLastError();                                                         \
+        if (e_ != cudaSuccess) return fail(ctx, MGNN_ECUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define GUARD()                                                                                      \
+    do {                                                                                             \
+        if (!ctx) return MGNN_EINVAL;                                                                \
+        if (ctx->sticky) return (mgnn_status)ctx->sticky;                                            \
+        if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, MGNN_ECUDA, "cudaSetDevice"); \
+    } while (0)
+
+template <class T>
+cudaError_t dalloc(T** p, size_t n) {
+    if (n == 0) n = 1;
+    return cudaMalloc((void**)p, n * sizeof(T));
+}
+
+template <class T>
+void dfree(T*& p) {
+    if (p) cudaFree((void*)p);
+    p = nullptr;
+}
+
+inline int64_t sat_mul(int64_t a, int64_t b, int64_t cap) {
+    if (a == 0 || b == 0) return 0;
+    if (a > cap / b) return cap;
+    int64_t r = a * b;
+    return r > cap ? cap : r;
+}
+
+void fill_partdev(const mgnn_ctx_s* c, const Part& p, PartDev* d) {
+    memset(d, 0, sizeof(*d));
+    d->part_id = p.part_id;
+    d->lo = p.lo;
+    d->n_local = p.n_local;
+    d->n_h = p.n_h;
+    d->h_below = p.h_below;
+    d->vp = p.n_local + p.n_h;
+    d->n_train = p.n_train;
+    d->cap = p.cap;
+    d->nbatch = p.nbatch;
+    d->perm_slots = p.perm_slots;
+    d->indptr = p.indptr;
+    d->cols_rank = p.cols_rank;
+    d->halo_ids = p.halo;
+    d->deg_in = p.deg_in;
+    d->train_ids = p.train;
+    d->table = p.table;
+    d->rows = p.rows;
+    d->se = p.se;
+    d->sa = p.sa;
+    d->slot_of = p.slot_of;
+    d->slot_h = p.slot_h;
+    d->hitmask = p.hitmask;
+    d->perm = p.perm;
+    (void)c;
+}
+
+mgnn_status upload_parts(mgnn_ctx ctx) {
+    std::vector<PartDev> h(ctx->parts.size());
+    for (size_t i = 0; i < ctx->parts.size(); ++i) fill_partdev(ctx, ctx->parts[i], &h[i]);
+    dfree(ctx->d_parts);
+    CK(dalloc(&ctx->d_parts, h.size()));
+    CK(cudaMemcpy(ctx->d_parts, h.data(), h.size() * sizeof(PartDev), cudaMemcpyHostToDevice));
+    return MGNN_OK;
+}
+
+mgnn_status upload_tables(mgnn_ctx ctx) {
+    CK(cudaMemcpy((void*)ctx->d_tables, ctx->tables.data(), ctx->P * sizeof(float*), cudaMemcpyHostToDevice));
+    return MGNN_OK;
+}
+
+WorldDev world_of(mgnn_ctx ctx) {
+    WorldDev w;
+    w.n_parts = ctx->P;
+    w.pitch = ctx->pitch;
+    w.bounds = ctx->d_bounds;
+    w.tables = ctx->d_tables;
+    return w;
+}
+
+void free_win(Win& w) {
+    dfree(w.fr_rank);
+    dfree(w.fr_gid);
+    dfree(w.hop_size);
+    for (int i = 0; i < kMaxLayers; ++i) {
+        dfree(w.off[i]);
+        dfree(w.cols[i]);
+    }
+    dfree(w.X);
+    dfree(w.pos_of);
+    dfree(w.nb);
+    dfree(w.zero);
+    dfree(w.ext_seeds);
+    dfree(w.ext_counts);
+    w = Win();
+}
+
+void free_buffer(Part& p) {
+    dfree(p.rows); dfree(p.se); dfree(p.sa); dfree(p.slot_of); dfree(p.slot_h); dfree(p.hitmask);
+    dfree(p.ek); dfree(p.ekt); dfree(p.ev); dfree(p.evt); dfree(p.rk); dfree(p.rkt); dfree(p.rv); dfree(p.rvt);
+}
+
+void free_perm(Part& p) {
+    dfree(p.perm); dfree(p.pk); dfree(p.pkt); dfree(p.pvt);
+    p.perm_epoch.clear();
+    p.perm_slots = 0;
+}
+
+WinDev win_dev(mgnn_ctx ctx, Win& w) {
+    WinDev d;
+    memset(&d, 0, sizeof(d));
+    d.n_steps = w.n_steps;
+    d.n_inst = (int32_t)ctx->parts.size() * w.n_steps;
+    d.L = ctx->L;
+    d.batch = ctx->batch;
+    d.pitch = ctx->pitch;
+    d.feat_dim = ctx->D;
+    d.step0 = w.step0;
+    d.seed_lo = (uint32_t)ctx->run_seed;
+    d.seed_hi = (uint32_t)(ctx->run_seed >> 32);
+    for (int i = 0; i < ctx->L; ++i) {
+        d.k_hop[i] = ctx->k_hop[i];
+        d.off_stride[i] = ctx->fcap[i] + 1;
+        d.col_stride[i] = ctx->ecap[i];
+        d.off[i] = w.off[i];
+        d.cols[i] = w.cols[i];
+    }
+    d.ucap = ctx->ucap;
+    d.vp_stride = ctx->vp_max;
+    d.bm_words = ctx->bm_words;
+    d.fr_rank = w.fr_rank;
+    d.fr_gid = w.fr_gid;
+    d.hop_size = w.hop_size;
+    d.X = w.X;
+    d.counts = w.counts;
+    d.pos_of = w.pos_of;
+    d.fb = w.fb;
+    d.nb = w.nb;
+    d.parts = ctx->d_parts;
+    d.err = ctx->d_err;
+    d.gathered_rows = ctx->d_gathered;
+    return d;
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+float mgnn_alpha_default(float gamma, int32_t delta) {
+    float a = 1.0f;
+    for (int32_t i = 0; i < delta; ++i) a = a * gamma;   // Eq.1, iterated fp32 (R#13)
+    return a;
+}
+
+mgnn_status mgnn_ctx_create(int32_t device, int32_t n_parts, int64_t n_global, const int64_t* bounds,
+                            int32_t feat_dim, uint64_t feat_seed, mgnn_ctx* out) {
+    if (!out || !bounds || n_parts < 1 || n_global < 0 || n_global >= (1ll << 31) || feat_dim < 0) return MGNN_EINVAL;
+    if (bounds[0] != 0 || bounds[n_parts] != n_global) return MGNN_EINVAL;
+    for (int q = 0; q < n_parts; ++q)
+        if (bounds[q + 1] < bounds[q]) return MGNN_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return MGNN_ECUDA;
+    if (cudaSetDevice(device) != cudaSuccess) return MGNN_ECUDA;
+    mgnn_ctx ctx = new mgnn_ctx_s();
+    ctx->device = device;
+    ctx->P = n_parts;
+    ctx->n_global = n_global;
+    ctx->bounds.assign(bounds, bounds + n_parts + 1);
+    ctx->D = feat_dim;
+    ctx->pitch = ((feat_dim + 3) / 4) * 4;
+    if (ctx->pitch == 0) ctx->pitch = 4;
+    ctx->feat_seed = feat_seed;
+    ctx->lp_of.assign(n_parts, -1);
+    ctx->tables.assign(n_parts, nullptr);
+    mgnn_status st = MGNN_OK;
+    auto chk = [&](cudaError_t e) { if (e != cudaSuccess && st == MGNN_OK) st = MGNN_ECUDA; };
+    chk(dalloc(&ctx->d_bounds, n_parts + 1));
+    chk(cudaMemcpy(ctx->d_bounds, bounds, (n_parts + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    chk(dalloc((float***)&ctx->d_tables, n_parts));
+    chk(cudaMemset((void*)ctx->d_tables, 0, n_parts * sizeof(float*)));
+    chk(dalloc(&ctx->d_err, 1));
+    chk(cudaMemset(ctx->d_err, 0, sizeof(int32_t)));
+    chk(dalloc(&ctx->d_gathered, 1));
+    chk(cudaMemset(ctx->d_gathered, 0, sizeof(long long)));
+    if (st != MGNN_OK) {
+        mgnn_destroy(ctx);
+        return st;
+    }
+    *out = ctx;
+    return MGNN_OK;
+}
+
+void mgnn_destroy(mgnn_ctx ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    for (auto& w : ctx->win) free_win(w);
+    for (auto& p : ctx->parts) {
+        free_buffer(p);
+        free_perm(p);
+        dfree(p.indptr); dfree(p.cols_rank); dfree(p.halo); dfree(p.deg_in); dfree(p.train); dfree(p.table);
+    }
+    for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
+    for (auto& e : ctx->prof_ev) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    dfree(ctx->d_bounds);
+    dfree(ctx->d_tables);
+    dfree(ctx->d_parts);
+    dfree(ctx->d_err);
+    dfree(ctx->d_gathered);
+    dfree(ctx->d_evsegs);
+    dfree(ctx->d_sel_n);
+    dfree(ctx->ev_zero);
+    dfree(ctx->hist);
+    dfree(ctx->d_permsegs);
+    dfree(ctx->d_perm_n);
+    delete ctx;
+}
+
+const char* mgnn_last_error(mgnn_ctx ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+int64_t mgnn_launch_count(mgnn_ctx ctx) {
+    (void)ctx;
+    return launches_total();
+}
+
+// ------------------------------------------------------------------ partition load (A1)
+mgnn_status mgnn_partition_load(mgnn_ctx ctx, const mgnn_partition_desc* d, int32_t* local_index) {
+    GUARD();
+    if (!d || d->part_id < 0 || d->part_id >= ctx->P) return fail(ctx, MGNN_EINVAL, "bad part_id");
+    if (ctx->lp_of[d->part_id] >= 0) return fail(ctx, MGNN_EINVAL, "partition already loaded");
+    if (ctx->configured || ctx->buffer_ready) return fail(ctx, MGNN_ESTATE, "load after buffer_init/sampler_config");
+    const int64_t lo = ctx->bounds[d->part_id], hi = ctx->bounds[d->part_id + 1], nl = hi - lo;
+    if (!d->indptr || (nl > 0 && d->indptr[0] != 0)) return fail(ctx, MGNN_EINVAL, "indptr[0] != 0");
+    for (int64_t r = 0; r < nl; ++r) {
+        if (d->indptr[r + 1] < d->indptr[r]) return fail(ctx, MGNN_EINVAL, "indptr not monotone");
+        for (int64_t e = d->indptr[r]; e < d->indptr[r + 1]; ++e) {
+            const int32_t c = d->cols[e];
+            if (c < 0 || c >= ctx->n_global) return fail(ctx, MGNN_EINVAL, "column out of range");
+            if (c == lo + r) return fail(ctx, MGNN_EINVAL, "self loop");
+            if (e > d->indptr[r] && d->cols[e - 1] >= c) return fail(ctx, MGNN_EINVAL, "row not strictly ascending");
+        }
+    }
+    if (d->n_train < 0 || (d->n_train > 0 && !d->train_ids)) return fail(ctx, MGNN_EINVAL, "train ids");
+    for (int64_t i = 0; i < d->n_train; ++i) {
+        if (d->train_ids[i] < lo || d->train_ids[i] >= hi) return fail(ctx, MGNN_EINVAL, "train id not local");
+        if (i > 0 && d->train_ids[i - 1] >= d->train_ids[i]) return fail(ctx, MGNN_EINVAL, "train ids not sorted");
+    }
+    const int64_t nnz = nl > 0 ? d->indptr[nl] : 0;
+    Part p;
+    p.part_id = d->part_id;
+    p.lo = lo;
+    p.n_local = nl;
+    p.nnz = nnz;
+    p.n_train = d->n_train;
+    cudaStream_t s = 0;
+    int32_t* cols_g = nullptr;
+    uint32_t* bm = nullptr;
+    int32_t* gmap = nullptr;
+    unsigned long long* status = nullptr;
+    long long* d_n = nullptr;
+    const int64_t words = (ctx->n_global + 31) / 32;
+    const int64_t halo_max = std::min<int64_t>(nnz, ctx->n_global - nl);
+    const int64_t tiles = (words + 1023) / 1024 + 1;
+    CK(dalloc(&p.indptr, nl + 1));
+    CK(cudaMemcpy(p.indptr, d->indptr, (nl + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CK(dalloc(&cols_g, nnz));
+    if (nnz) CK(cudaMemcpy(cols_g, d->cols, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CK(dalloc(&bm, words));
+    CK(cudaMemset(bm, 0, std::max<int64_t>(words, 1) * sizeof(uint32_t)));
+    CK(dalloc(&status, tiles + 1));
+    CK(cudaMemset(status, 0, (tiles + 1) * sizeof(unsigned long long)));
+    CK(dalloc(&d_n, 2));
+    CK(cudaMemset(d_n, 0, 2 * sizeof(long long)));
+    CK(dalloc(&p.halo, halo_max));
+    launch_mark_halo(cols_g, nnz, lo, hi, bm, s);
+    Scratch sc{status + 1, (int32_t*)status};
+    launch_bitmap_to_ids(bm, words, p.halo, d_n, sc, s);
+    CKL();
+    long long nh = 0;
+    CK(cudaMemcpy(&nh, d_n, sizeof(long long), cudaMemcpyDeviceToHost));
+    p.n_h = nh;
+    launch_lower_bound(p.halo, nh, lo, d_n + 1, s);
+    long long hb = 0;
+    CK(cudaMemcpy(&hb, d_n + 1, sizeof(long long), cudaMemcpyDeviceToHost));
+    p.h_below = hb;
+    CK(dalloc(&gmap, ctx->n_global));
+    launch_halo_index(p.halo, nh, gmap, s);
+    CK(dalloc(&p.deg_in, nh));
+    CK(cudaMemset(p.deg_in, 0, std::max<int64_t>(nh, 1) * sizeof(int32_t)));
+    CK(dalloc(&p.cols_rank, nnz));
+    launch_deg_rank(cols_g, nnz, lo, nl, hb, gmap, p.deg_in, p.cols_rank, s);
+    CK(dalloc(&p.train, d->n_train));
+    if (d->n_train) CK(cudaMemcpy(p.train, d->train_ids, d->n_train * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CK(dalloc(&p.table, std::max<int64_t>(nl, 1) * ctx->pitch));
+    launch_features(p.table, lo, nl, ctx->D, ctx->pitch, ctx->feat_seed, s);
+    CKL();
+    CK(cudaDeviceSynchronize());
+    dfree(cols_g);
+    dfree(bm);
+    dfree(gmap);
+    dfree(status);
+    dfree(d_n);
+    const int32_t lp = (int32_t)ctx->parts.size();
+    ctx->tables[p.part_id] = p.table;
+    ctx->lp_of[p.part_id] = lp;
+    ctx->parts.push_back(p);
+    mgnn_status st = upload_tables(ctx);
+    if (st) return st;
+    st = upload_parts(ctx);
+    if (st) return st;
+    if (local_index) *local_index = lp;
+    return MGNN_OK;
+}
+
+mgnn_status mgnn_table_export(mgnn_ctx ctx, int32_t part_id, void* handle_out) {
+    GUARD();
+    if (part_id < 0 || part_id >= ctx->P || ctx->lp_of[part_id] < 0 || !handle_out)
+        return fail(ctx, MGNN_EINVAL, "export: partition not hosted here");
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, (void*)ctx->parts[ctx->lp_of[part_id]].table));
+    static_assert(sizeof(h) == MGNN_IPC_HANDLE_BYTES, "ipc handle size");
+    memcpy(handle_out, &h, sizeof(h));
+    return MGNN_OK;
+}
+
+mgnn_status mgnn_table_import(mgnn_ctx ctx, int32_t part_id, const void* handle) {
+    GUARD();
+    if (part_id < 0 || part_id >= ctx->P || ctx->lp_of[part_id] >= 0 || !handle)
+        return fail(ctx, MGNN_EINVAL, "import: bad partition");
+    if (ctx->tables[part_id]) return fail(ctx, MGNN_EINVAL, "import: already imported");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->ipc_opened.push_back(ptr);
+    ctx->tables[part_id] = (const float*)ptr;
+    return upload_tables(ctx);
+}
+
+mgnn_status mgnn_part_info(mgnn_ctx ctx, int32_t lp, int64_t* info) {
+    if (!ctx || !info || lp < 0 || lp >= (int32_t)ctx->parts.size()) return MGNN_EINVAL;
+    const Part& p = ctx->parts[lp];
+    info[0] = p.part_id;
+    info[1] = p.n_local;
+    info[2] = p.n_h;
+    info[3] = p.cap;
+    info[4] = p.n_train;
+    return MGNN_OK;
+}
+
+mgnn_status mgnn_halo_get(mgnn_ctx ctx, int32_t lp, int32_t* halo_ids, int32_t* deg_in) {
+    GUARD();
+    if (lp < 0 || lp >= (int32_t)ctx->parts.size()) return fail(ctx, MGNN_EINVAL, "bad lp");
+    const Part& p = ctx->parts[lp];
+    if (halo_ids && p.n_h) CK(cudaMemcpy(halo_ids, p.halo, p.n_h * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (deg_in && p.n_h) CK(cudaMemcpy(deg_in, p.deg_in, p.n_h * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    return MGNN_OK;
+}
+
+mgnn_status mgnn_table_row(mgnn_ctx ctx, int64_t node, float* out) {
+    GUARD();
+    if (node < 0 || node >= ctx->n_global || !out) return fail(ctx, MGNN_EINVAL, "bad node");
+    int q = 0;
+    while (!(ctx->bounds[q] <= node && node < ctx->bounds[q + 1])) ++q;
+    if (ctx->lp_of[q] < 0) return fail(ctx, MGNN_EINVAL, "node not hosted here");
+    const Part& p = ctx->parts[ctx->lp_of[q]];
+    if (ctx->D)
+        CK(cudaMemcpy(out, p.table + (node - p.lo) * ctx->pitch, ctx->D * sizeof(float), cudaMemcpyDeviceToHost));
+    return MGNN_OK;
+}
+
+// ------------------------------------------------------------------ INITIALIZE_PREFETCHER (A2)
+mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream stream) {
+    GUARD();
+    if (!pol || !(pol->gamma > 0.0f && pol->gamma <= 1.0f) || !(pol->alpha >= 0.0f) || pol->alpha != pol->alpha ||
+        pol->alpha > 3.4e38f || pol->theta_r != pol->theta_r || pol->delta < 0 || pol->f_bp > 10000u)
+        return fail(ctx, MGNN_EINVAL, "invalid policy");
+    if (ctx->parts.empty()) return fail(ctx, MGNN_ESTATE, "no partition loaded");
+    for (int q = 0; q < ctx->P; ++q)
+        if (!ctx->tables[q]) return fail(ctx, MGNN_ESTATE, "feature table of partition " + std::to_string(q) + " missing");
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(cudaStreamSynchronize(s));
+    int64_t cap_max = 0, nh_max = 0;
+    for (auto& p : ctx->parts) {
+        free_buffer(p);
+        p.cap = ((int64_t)pol->f_bp * p.n_h + 9999) / 10000;   // ceil(f |V_p^h|) (R#11)
+        CK(dalloc(&p.rows, p.cap * ctx->pitch));
+        CK(dalloc(&p.se, p.cap));
+        CK(dalloc(&p.sa, p.n_h));
+        CK(dalloc(&p.slot_of, p.n_h));
+        CK(dalloc(&p.slot_h, p.cap));
+        CK(dalloc(&p.hitmask, p.cap));
+        CK(dalloc(&p.ek, p.cap)); CK(dalloc(&p.ekt, p.cap)); CK(dalloc(&p.ev, p.cap)); CK(dalloc(&p.evt, p.cap));
+        CK(dalloc(&p.rk, p.n_h)); CK(dalloc(&p.rkt, p.n_h)); CK(dalloc(&p.rv, p.n_h)); CK(dalloc(&p.rvt, p.n_h));
+        cap_max = std::max(cap_max, p.cap);
+        nh_max = std::max(nh_max, p.n_h);
+    }
+    mgnn_status st = upload_parts(ctx);
+    if (st) return st;
+    const int n_lp = (int)ctx->parts.size();
+    // eviction / init sort segments: 2*lp = E (slots), 2*lp+1 = R (halo)
+    std::vector<SortSeg> segs(2 * n_lp);
+    dfree(ctx->d_sel_n);
+    CK(dalloc(&ctx->d_sel_n, 2 * n_lp));
+    CK(cudaMemset(ctx->d_sel_n, 0, 2 * n_lp * sizeof(long long)));
+    for (int lp = 0; lp < n_lp; ++lp) {
+        Part& p = ctx->parts[lp];
+        segs[2 * lp] = SortSeg{p.ek, p.ev, p.ekt, p.evt, ctx->d_sel_n + 2 * lp};
+        segs[2 * lp + 1] = SortSeg{p.rk, p.rv, p.rkt, p.rvt, ctx->d_sel_n + 2 * lp + 1};
+    }
+    dfree(ctx->d_evsegs);
+    CK(dalloc(&ctx->d_evsegs, segs.size()));
+    CK(cudaMemcpy(ctx->d_evsegs, segs.data(), segs.size() * sizeof(SortSeg), cudaMemcpyHostToDevice));
+    const int64_t n_sort_max = std::max<int64_t>(std::max(cap_max, nh_max), 1);
+    ctx->ev_tiles = (n_sort_max + 2047) / 2048;
+    dfree(ctx->ev_zero);
+    ctx->ev_zero_bytes = (size_t)(2 * n_lp) * (ctx->ev_tiles * 8 + 4) + 64;
+    CK(dalloc((char**)&ctx->ev_zero, ctx->ev_zero_bytes));
+    ctx->ev_sc.tilectr = (int32_t*)ctx->ev_zero;
+    ctx->ev_sc.status = (unsigned long long*)(ctx->ev_zero + ((2 * n_lp * 4 + 63) / 64) * 64);
+    ctx->ev_zero_bytes = ((2 * n_lp * 4 + 63) / 64) * 64 + (size_t)(2 * n_lp) * ctx->ev_tiles * 8;
+    size_t hw = radix_hist_words(2 * n_lp, n_sort_max);
+    if (ctx->configured) {
+        for (auto& p : ctx->parts) hw = std::max(hw, radix_hist_words(1, std::max<int64_t>(p.n_train, 1)));
+    }
+    if (hw > ctx->hist_words) {
+        dfree(ctx->hist);
+        CK(dalloc(&ctx->hist, hw));
+        ctx->hist_words = hw;
+    }
+    WorldDev G = world_of(ctx);
+    for (int lp = 0; lp < n_lp; ++lp) {
+        Part& p = ctx->parts[lp];
+        // order V_p^h by (deg_in desc, id asc) (R#10) and take the first cap
+        launch_init_keys(ctx->d_parts + lp, p.n_h, ctx->d_evsegs + 2 * lp + 1, ctx->d_sel_n + 2 * lp + 1, s);
+        radix_sort_pairs(ctx->d_evsegs + 2 * lp + 1, 1, std::max<int64_t>(p.n_h, 1), 32, ctx->hist, s);
+        launch_init_fill(ctx->d_parts + lp, p.n_h, p.cap, p.rv, s);
+        launch_rows_from_owners(ctx->d_parts + lp, p.cap, G, s);
+        CKL();
+    }
+    CK(cudaStreamSynchronize(s));
+    ctx->pol = *pol;
+    ctx->buffer_ready = true;
+    ctx->seq_started = false;
+    for (auto& w : ctx->win) w.sampled = w.gathered = w.scored = false;
+    return MGNN_OK;
+}
+
+// ------------------------------------------------------------------ sampler configuration
+mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_layers, int32_t batch,
+                                uint64_t run_seed, int32_t max_window) {
+    GUARD();
+    if (!fanouts || n_layers < 1 || n_layers > kMaxLayers || batch < 1 || max_window < 1 || max_window > 64)
+        return fail(ctx, MGNN_EINVAL, "bad sampler config");
+    for (int i = 0; i < n_layers; ++i)
+        if (fanouts[i] < 1 || fanouts[i] > MGNN_MAX_FANOUT) return fail(ctx, MGNN_EINVAL, "fanout must be 1..32");
+    if (ctx->parts.empty()) return fail(ctx, MGNN_ESTATE, "no partition loaded");
+    CK(cudaDeviceSynchronize());
+    for (auto& w : ctx->win) free_win(w);
+    for (auto& p : ctx->parts) free_perm(p);
+    ctx->configured = false;
+    ctx->L = n_layers;
+    ctx->batch = batch;
+    ctx->run_seed = run_seed;
+    ctx->max_window = max_window;
+    for (int i = 0; i < n_layers; ++i) {
+        ctx->fan[i] = fanouts[i];
+        ctx->k_hop[i] = fanouts[n_layers - 1 - i];   // hop 0 (seeds) draws the last layer's fanout (R#2)
+    }
+    ctx->vp_max = 1;
+    for (auto& p : ctx->parts) ctx->vp_max = std::max(ctx->vp_max, p.n_local + p.n_h);
+    ctx->bm_words = (ctx->vp_max + 31) / 32;
+    const int64_t big = (int64_t)1 << 40;
+    ctx->fcap[0] = std::min<int64_t>(batch, ctx->vp_max);
+    for (int i = 0; i < n_layers; ++i) {
+        ctx->ecap[i] = std::max<int64_t>(sat_mul(ctx->fcap[i], ctx->k_hop[i], big), 1);
+        ctx->fcap[i + 1] = std::min<int64_t>(sat_mul(ctx->fcap[i], 1 + ctx->k_hop[i], big), ctx->vp_max);
+    }
+    ctx->ucap = ctx->fcap[n_layers];
+    const int n_lp = (int)ctx->parts.size();
+    const int64_t M = (int64_t)n_lp * max_window;
+    for (auto& w : ctx->win) {
+        CK(dalloc(&w.fr_rank, M * ctx->ucap));
+        CK(dalloc(&w.fr_gid, M * ctx->ucap));
+        CK(dalloc(&w.hop_size, M * (kMaxLayers + 1)));
+        CK(cudaMemset(w.hop_size, 0, M * (kMaxLayers + 1) * sizeof(int64_t)));
+        for (int i = 0; i < n_layers; ++i) {
+            CK(dalloc(&w.off[i], M * (ctx->fcap[i] + 1)));
+            CK(dalloc(&w.cols[i], M * ctx->ecap[i]));
+        }
+        CK(dalloc(&w.X, (size_t)M * ctx->ucap * ctx->pitch));
+        CK(dalloc(&w.pos_of, M * ctx->vp_max));
+        CK(dalloc(&w.nb, M * ctx->bm_words));
+        CK(cudaMemset(w.nb, 0, M * ctx->bm_words * sizeof(uint32_t)));
+        CK(dalloc(&w.ext_seeds, M * batch));
+        CK(dalloc(&w.ext_counts, M));
+        // zero region: [tile counters | status words | counts | fb]
+        size_t ctr_words = (size_t)(2 * n_layers) * M;                  // int32
+        size_t st_words = 0;
+        for (int i = 0; i < n_layers; ++i)
+            st_words += (size_t)M * (scan_tiles_count(ctx->fcap[i]) + 1) + (size_t)M * (scan_tiles_words(ctx->bm_words) + 1);
+        size_t off_ctr = 0;
+        size_t off_st = ((ctr_words * 4 + 255) / 256) * 256;
+        size_t off_cnt = off_st + ((st_words * 8 + 255) / 256) * 256;
+        size_t off_fb = off_cnt + (((size_t)M * 8 * 8 + 255) / 256) * 256;
+        size_t total = off_fb + (size_t)M * ctx->bm_words * 4;
+        CK(dalloc(&w.zero, total));
+        CK(cudaMemset(w.zero, 0, total));
+        w.zero_bytes = total;
+        w.tilectr = (int32_t*)(w.zero + off_ctr);
+        w.status = (unsigned long long*)(w.zero + off_st);
+        w.counts = (long long*)(w.zero + off_cnt);
+        w.fb = (uint32_t*)(w.zero + off_fb);
+        size_t so = 0;
+        for (int i = 0; i < n_layers; ++i) {
+            int64_t tc = scan_tiles_count(ctx->fcap[i]);
+            w.sc_count[i] = Scratch{w.status + so, w.tilectr + (size_t)(2 * i) * M};
+            so += (size_t)M * (tc < 1 ? 1 : tc);
+            int64_t tw = scan_tiles_words(ctx->bm_words);
+            w.sc_compact[i] = Scratch{w.status + so, w.tilectr + (size_t)(2 * i + 1) * M};
+            so += (size_t)M * (tw < 1 ? 1 : tw);
+        }
+        w.alloc = true;
+    }
+    // epoch orders: ring of perm slots per partition
+    ctx->perm_slots_max = 1;
+    for (auto& p : ctx->parts) {
+        p.nbatch = p.n_train > 0 ? (p.n_train + batch - 1) / batch : 1;
+        p.perm_slots = (int32_t)((max_window + p.nbatch - 1) / p.nbatch + 1);
+        ctx->perm_slots_max = std::max(ctx->perm_slots_max, p.perm_slots);
+        p.perm_epoch.assign(p.perm_slots, -1);
+        CK(dalloc(&p.perm, (int64_t)p.perm_slots * std::max<int64_t>(p.n_train, 1)));
+        CK(dalloc(&p.pk, p.n_train)); CK(dalloc(&p.pkt, p.n_train)); CK(dalloc(&p.pvt, p.n_train));
+    }
+    std::vector<SortSeg> ps((size_t)n_lp * ctx->perm_slots_max);
+    dfree(ctx->d_perm_n);
+    CK(dalloc(&ctx->d_perm_n, n_lp));
+    std::vector<long long> pn(n_lp);
+    for (int lp = 0; lp < n_lp; ++lp) {
+        Part& p = ctx->parts[lp];
+        pn[lp] = p.n_train;
+        for (int k = 0; k < p.perm_slots; ++k)
+            ps[(size_t)lp * ctx->perm_slots_max + k] =
+                SortSeg{p.pk, (uint32_t*)(p.perm + (int64_t)k * p.n_train), p.pkt, p.pvt, ctx->d_perm_n + lp};
+    }
+    CK(cudaMemcpy(ctx->d_perm_n, pn.data(), n_lp * sizeof(long long), cudaMemcpyHostToDevice));
+    dfree(ctx->d_permsegs);
+    CK(dalloc(&ctx->d_permsegs, ps.size()));
+    CK(cudaMemcpy(ctx->d_permsegs, ps.data(), ps.size() * sizeof(SortSeg), cudaMemcpyHostToDevice));
+    size_t hw = 0;
+    for (auto& p : ctx->parts) hw = std::max(hw, radix_hist_words(1, std::max<int64_t>(p.n_train, 1)));
+    if (hw > ctx->hist_words) {
+        dfree(ctx->hist);
+        CK(dalloc(&ctx->hist, hw));
+        ctx->hist_words = hw;
+    }
+    mgnn_status st = upload_parts(ctx);
+    if (st) return st;
+    ctx->configured = true;
+    return MGNN_OK;
+}
+
+// ------------------------------------------------------------------ mgnn_sample (A3-A5)
+mgnn_status mgnn_sample(mgnn_ctx ctx, int32_t slot, uint64_t t0, int32_t n_steps, const int32_t* seeds,
+                        const int32_t* seed_counts, int32_t seeds_on_host, mgnn_stream stream) {
+    GUARD();
+    if (!ctx->configured || !ctx->buffer_ready) return fail(ctx, MGNN_ESTATE, "sample before buffer_init/sampler_config");
+    if (slot < 0 || slot > 1 || t0 < 1 || n_steps < 1 || n_steps > ctx->max_window)
+        return fail(ctx, MGNN_EINVAL, "bad window");
+    const int32_t delta = ctx->pol.delta;
+    if (delta > 0) {
+        for (uint64_t t = t0; t + 1 < t0 + (uint64_t)n_steps; ++t)
+            if (t % (uint64_t)delta == 0) return fail(ctx, MGNN_EINVAL, "eviction step inside window (only last allowed)");
+    }
+    Win& w = ctx->win[slot];
+    if (w.sampled && !w.scored && w.gathered) return fail(ctx, MGNN_ESTATE, "slot gathered but not scored");
+    const int n_lp = (int)ctx->parts.size();
+    const int64_t M = (int64_t)n_lp * n_steps;
+    if (seeds && seeds_on_host) {
+        if (!seed_counts) return fail(ctx, MGNN_EINVAL, "seed_counts missing");
+        for (int64_t m = 0; m < M; ++m)
+            if (seed_counts[m] < 1 || seed_counts[m] > ctx->batch) return fail(ctx, MGNN_EINVAL, "seed count");
+    }
+    if (!seeds)
+        for (auto& p : ctx->parts)
+            if (p.n_train < 1) return fail(ctx, MGNN_EINVAL, "partition without train ids needs external seeds");
+    cudaStream_t s = (cudaStream_t)stream;
+    // epoch orders needed by this window (R#8)
+    if (!seeds) {
+        for (int lp = 0; lp < n_lp; ++lp) {
+            Part& p = ctx->parts[lp];
+            const int64_t e0 = (int64_t)((t0 - 1) / (uint64_t)p.nbatch);
+            const int64_t e1 = (int64_t)((t0 + n_steps - 2) / (uint64_t)p.nbatch);
+            for (int64_t e = e0; e <= e1; ++e) {
+                const int k = (int)(e % p.perm_slots);
+                if (p.perm_epoch[k] == e) continue;
+                const SortSeg* seg = ctx->d_permsegs + (size_t)lp * ctx->perm_slots_max + k;
+                launch_perm_keys(ctx->d_parts + lp, p.n_train, (uint64_t)e, (uint32_t)ctx->run_seed,
+                                 (uint32_t)(ctx->run_seed >> 32), seg, s);
+                radix_sort_pairs(seg, 1, p.n_train, 64, ctx->hist, s);
+                p.perm_epoch[k] = e;
+            }
+        }
+    } else {
+        const cudaMemcpyKind kind = seeds_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        CK(cudaMemcpyAsync(w.ext_seeds, seeds, M * ctx->batch * sizeof(int32_t), kind, s));
+        CK(cudaMemcpyAsync(w.ext_counts, seed_counts, M * sizeof(int32_t), kind, s));
+    }
+    CK(cudaMemsetAsync(w.zero, 0, w.zero_bytes, s));
+    w.n_steps = n_steps;
+    w.step0 = t0;
+    WinDev wd = win_dev(ctx, w);
+    wd.n_inst = (int32_t)M;
+    if (seeds) {
+        wd.ext_seeds = w.ext_seeds;
+        wd.ext_counts = w.ext_counts;
+    }
+    launch_seeds(wd, s);
+    for (int i = 0; i < ctx->L; ++i) {
+        // per-hop scratch strides follow the max window; scans index by instance < M
+        Scratch scc = w.sc_count[i], scp = w.sc_compact[i];
+        launch_count_scan(wd, i, ctx->fcap[i], scc, s);
+        launch_sample(wd, i, ctx->fcap[i], s);
+        launch_compact(wd, i, scp, s);
+    }
+    launch_relabel(wd, s);
+    CKL();
+    w.sampled = true;
+    w.gathered = w.scored = false;
+    return MGNN_OK;
+}
+
+// ------------------------------------------------------------------ mgnn_lookup_gather (A6-A8, A10)
+mgnn_status mgnn_lookup_gather(mgnn_ctx ctx, int32_t slot, mgnn_stream stream) {
+    GUARD();
+    if (slot < 0 || slot > 1) return fail(ctx, MGNN_EINVAL, "bad slot");
+    Win& w = ctx->win[slot];
+    if (!w.sampled || w.gathered) return fail(ctx, MGNN_ESTATE, "gather needs a freshly sampled window");
+    Win& other = ctx->win[slot ^ 1];
+    if (other.gathered && !other.scored) return fail(ctx, MGNN_ESTATE, "previous window not scored");
+    if (ctx->seq_started && w.step0 != ctx->next_step)
+        return fail(ctx, MGNN_ESTATE, "windows must be gathered in step order");
+    cudaStream_t s = (cudaStream_t)stream;
+    WinDev wd = win_dev(ctx, w);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->prof) {
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, s));
+    }
+    launch_gather(wd, world_of(ctx), s);
+    CKL();
+    if (ctx->prof) {
+        CK(cudaEventRecord(e1, s));
+        ctx->prof_ev.emplace_back(e0, e1);
+    }
+    w.gathered = true;
+    ctx->seq_started = true;
+    ctx->next_step = w.step0 + (uint64_t)w.n_steps;
+    return MGNN_OK;
+}
+
+// ------------------------------------------------------------------ mgnn_score_evict_refill (A9, A11, A12)
+mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stream) {
+    GUARD();
+    if (slot < 0 || slot > 1) return fail(ctx, MGNN_EINVAL, "bad slot");
+    Win& w = ctx->win[slot];
+    if (!w.gathered || w.scored) return fail(ctx, MGNN_ESTATE, "score needs a gathered window");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int n_lp = (int)ctx->parts.size();
+    int64_t cap_max = 0, nmax = 1;
+    for (auto& p : ctx->parts) {
+        cap_max = std::max(cap_max, p.cap);
+        nmax = std::max(nmax, std::max(p.cap, p.n_h));
+    }
+    launch_decay(ctx->d_parts, n_lp, cap_max, w.n_steps, ctx->pol.gamma, s);
+    const uint64_t t_last = w.step0 + (uint64_t)w.n_steps - 1;
+    if (ctx->pol.delta > 0 && t_last % (uint64_t)ctx->pol.delta == 0) {
+        CK(cudaMemsetAsync(ctx->ev_zero, 0, ctx->ev_zero_bytes, s));
+        launch_select(ctx->d_parts, n_lp, nmax, ctx->pol.alpha, ctx->pol.theta_r, ctx->d_evsegs, ctx->d_sel_n,
+                      ctx->ev_sc, s);
+        radix_sort_pairs(ctx->d_evsegs, 2 * n_lp, nmax, 64, ctx->hist, s);
+        launch_swap_refill(ctx->d_parts, n_lp, cap_max, ctx->d_evsegs, world_of(ctx), w.counts, 8, w.n_steps, s);
+    }
+    CKL();
+    w.scored = true;
+    return MGNN_OK;
+}
+
+// ------------------------------------------------------------------ views / readback
+mgnn_status mgnn_window_get(mgnn_ctx ctx, int32_t slot, mgnn_window* out) {
+    GUARD();
+    if (slot < 0 || slot > 1 || !out) return fail(ctx, MGNN_EINVAL, "bad slot");
+    Win& w = ctx->win[slot];
+    if (!w.sampled) return fail(ctx, MGNN_ESTATE, "slot not sampled");
+    memset(out, 0, sizeof(*out));
+    out->n_steps = w.n_steps;
+    out->n_parts_local = (int32_t)ctx->parts.size();
+    out->n_inst = out->n_steps * out->n_parts_local;
+    out->n_layers = ctx->L;
+    out->step0 = w.step0;
+    out->rows_stride = ctx->ucap;
+    out->pitch = ctx->pitch;
+    out->X = w.X;
+    out->frontier = w.fr_gid;
+    out->hop_size = w.hop_size;
+    for (int i = 0; i < ctx->L; ++i) {
+        out->offsets[i] = w.off[i];
+        out->cols[i] = w.cols[i];
+        out->off_stride[i] = ctx->fcap[i] + 1;
+        out->col_stride[i] = ctx->ecap[i];
+    }
+    out->counts = (const int64_t*)w.counts;
+    return MGNN_OK;
+}
+
+mgnn_status mgnn_counts_read(mgnn_ctx ctx, int32_t slot, int64_t* host_counts, mgnn_stream stream) {
+    GUARD();
+    if (slot < 0 || slot > 1 || !host_counts) return fail(ctx, MGNN_EINVAL, "bad slot");
+    Win& w = ctx->win[slot];
+    if (!w.sampled) return fail(ctx, MGNN_ESTATE, "slot not sampled");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t M = (int64_t)ctx->parts.size() * w.n_steps;
+    int32_t err = 0;
+    CK(cudaMemcpyAsync(host_counts, w.counts, M * 8 * sizeof(long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&err, ctx->d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (err) {
+        ctx->sticky = MGNN_EINVAL;
+        return fail(ctx, MGNN_EINVAL, "invalid external seeds (not local or duplicated)");
+    }
+    return MGNN_OK;
+}
+
+mgnn_status mgnn_buffer_snapshot(mgnn_ctx ctx, int32_t lp, int32_t* node_ids, float* se, float* sa, int32_t* slot_of,
+                                 float* rows) {
+    GUARD();
+    if (lp < 0 || lp >= (int32_t)ctx->parts.size()) return fail(ctx, MGNN_EINVAL, "bad lp");
+    if (!ctx->buffer_ready) return fail(ctx, MGNN_ESTATE, "buffer not initialised");
+    CK(cudaDeviceSynchronize());
+    const Part& p = ctx->parts[lp];
+    std::vector<int32_t> sh(p.cap), halo(p.n_h);
+    if (p.cap) CK(cudaMemcpy(sh.data(), p.slot_h, p.cap * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (p.n_h) CK(cudaMemcpy(halo.data(), p.halo, p.n_h * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (node_ids)
+        for (int64_t s = 0; s < p.cap; ++s) node_ids[s] = halo[sh[s]];
+    if (se && p.cap) CK(cudaMemcpy(se, p.se, p.cap * sizeof(float), cudaMemcpyDeviceToHost));
+    if (sa && p.n_h) CK(cudaMemcpy(sa, p.sa, p.n_h * sizeof(float), cudaMemcpyDeviceToHost));
+    if (slot_of && p.n_h) CK(cudaMemcpy(slot_of, p.slot_of, p.n_h * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (rows && p.cap && ctx->D)
+        CK(cudaMemcpy2D(rows, ctx->D * sizeof(float), p.rows, ctx->pitch * sizeof(float), ctx->D * sizeof(float), p.cap,
+                        cudaMemcpyDeviceToHost));
+    return MGNN_OK;
+}
+
+// ------------------------------------------------------------------ profiling
+mgnn_status mgnn_profile_enable(mgnn_ctx ctx, int32_t enable) {
+    if (!ctx) return MGNN_EINVAL;
+    ctx->prof = enable != 0;
+    return MGNN_OK;
+}
+
+mgnn_status mgnn_profile_read(mgnn_ctx ctx, double* ms, int64_t* launches, int64_t* bytes) {
+    GUARD();
+    double tot = 0.0;
+    for (auto& e : ctx->prof_ev) {
+        CK(cudaEventSynchronize(e.second));
+        float x = 0.0f;
+        CK(cudaEventElapsedTime(&x, e.first, e.second));
+        tot += x;
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+    }
+    const long long n = (long long)ctx->prof_ev.size();
+    ctx->prof_ev.clear();
+    long long rows = 0;
+    CK(cudaMemcpy(&rows, ctx->d_gathered, sizeof(long long), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(ctx->d_gathered, 0, sizeof(long long)));
+    if (ms) *ms = tot;
+    if (launches) *launches = n;
+    if (bytes) *bytes = 2ll * rows * ctx->D * (long long)sizeof(float);
+    return MGNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// launch.h -- host-side launch wrappers shared by the .cu units of libmgnn.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace mgnn {
+
+constexpr int kMaxLayers = MGNN_MAX_LAYERS;
+
+// Kernel launches issued by the library (process-wide; bench evidence).
+// With MGNN_DEBUG_SYNC=1 in the environment every launcher synchronises and
+// reports the first failing kernel by name (debug aid, never on by default).
+void count_launches(long long n, const char* who);
+long long launches_total();
+
+// ------------------------------------------------------------------ window (device view)
+struct WinDev {
+    int32_t n_inst, n_steps, L, batch, pitch, feat_dim;
+    uint64_t step0;
+    uint32_t seed_lo, seed_hi;           // run seed (Philox key, R#4)
+    int32_t k_hop[kMaxLayers];           // fanout drawn at hop i (R#2)
+    int64_t ucap;                        // rows per instance (X, frontier)
+    int64_t off_stride[kMaxLayers];      // offsets row stride per hop (>= fcap_i + 1)
+    int64_t col_stride[kMaxLayers];      // cols stride per hop (= ecap_i)
+    int64_t vp_stride;                   // pos_of stride (>= max vp)
+    int64_t bm_words;                    // bitmap words per instance
+    int32_t* fr_rank;                    // [M][ucap]
+    int32_t* fr_gid;                     // [M][ucap]
+    int64_t* hop_size;                   // [M][kMaxLayers+1]
+    int64_t* off[kMaxLayers];
+    int32_t* cols[kMaxLayers];
+    float* X;                            // [M][ucap][pitch]
+    long long* counts;                   // [M][8]
+    int32_t* pos_of;                     // [M][vp_stride]
+    uint32_t* fb;                        // [M][bm_words] frontier membership
+    uint32_t* nb;                        // [M][bm_words] new-node candidates
+    const int32_t* ext_seeds;            // [M][batch] or nullptr
+    const int32_t* ext_counts;           // [M]
+    const PartDev* parts;                // [n_parts_local]
+    int32_t* err;                        // device error word
+    long long* gathered_rows;            // profiling counter
+};
+
+// Segment of a radix sort (device array of these).
+struct SortSeg {
+    unsigned long long* keys;    // primary (result ends here after an even number of passes)
+    uint32_t* vals;
+    unsigned long long* keys_tmp;
+    uint32_t* vals_tmp;
+    const long long* n;          // device element count
+};
+
+struct Scratch {          // zeroed look-back status words + tile counters
+    unsigned long long* status;
+    int32_t* tilectr;
+};
+
+// sample.cu
+void launch_seeds(const WinDev& w, cudaStream_t s);
+void launch_count_scan(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s);
+void launch_sample(const WinDev& w, int hop, int64_t fcap, cudaStream_t s);
+void launch_compact(const WinDev& w, int hop, Scratch sc, cudaStream_t s);
+void launch_relabel(const WinDev& w, cudaStream_t s);
+int64_t scan_tiles_count(int64_t fcap);   // tiles used by count_scan for fcap items
+int64_t scan_tiles_words(int64_t words);  // tiles used by compact for `words`
+
+// gather.cu
+void launch_gather(const WinDev& w, const WorldDev& world, cudaStream_t s);
+
+// score.cu
+void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, float gamma, cudaStream_t s);
+void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, float theta_r, const SortSeg* segs,
+                   long long* n_out, Scratch sc, cudaStream_t s);
+void launch_swap_refill(const PartDev* parts, int n_lp, int64_t cap_max, const SortSeg* segs, const WorldDev& world,
+                        long long* counts, int64_t inst_stride_counts, int n_steps, cudaStream_t s);
+void launch_init_keys(const PartDev* pd_dev, int64_t n_h, const SortSeg* seg, long long* n_dev, cudaStream_t s);
+void launch_init_fill(const PartDev* pd_dev, int64_t n_h, int64_t cap, const uint32_t* order, cudaStream_t s);
+void launch_rows_from_owners(const PartDev* pd_dev, int64_t cap, const WorldDev& world, cudaStream_t s);
+void launch_perm_keys(const PartDev* pd_dev, int64_t n_train, uint64_t epoch, uint32_t seed_lo, uint32_t seed_hi,
+                      const SortSeg* seg, cudaStream_t s);
+
+// sort.cu: stable LSD radix sort of (u64 key, u32 value) pairs over `bits` low key bits
+// (bits multiple of 16), each segment independently; n_max bounds every segment.
+void radix_sort_pairs(const SortSeg* segs_dev, int n_seg, int64_t n_max, int bits, uint32_t* hist_scratch,
+                      cudaStream_t s);
+size_t radix_hist_words(int n_seg, int64_t n_max);
+
+// load.cu
+void launch_mark_halo(const int32_t* cols, int64_t nnz, int64_t lo, int64_t hi, uint32_t* bm, cudaStream_t s);
+void launch_bitmap_to_ids(const uint32_t* bm, int64_t nwords, int32_t* out, long long* out_n, Scratch sc,
+                          cudaStream_t s);
+void launch_lower_bound(const int32_t* arr, int64_t n, int64_t v, long long* out, cudaStream_t s);
+void launch_halo_index(const int32_t* halo, int64_t n_h, int32_t* gmap, cudaStream_t s);
+void launch_deg_rank(const int32_t* cols, int64_t nnz, int64_t lo, int64_t n_local, int64_t h_below,
+                     const int32_t* gmap, int32_t* deg_in, int32_t* cols_rank, cudaStream_t s);
+void launch_features(float* table, int64_t lo, int64_t n_rows, int32_t dim, int32_t pitch, uint64_t feat_seed,
+                     cudaStream_t s);
+
+}  // namespace mgnn

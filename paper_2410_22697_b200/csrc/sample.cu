@@ -1,0 +1,290 @@
+// sample.cu -- NeighborSampler of Alg.2 l.1 (uniform fixed
+// fanout without replacement) for a window of minibatch instances.
+//
+// Work unit: instance m = (local partition lp, window step w).  All kernels
+// run every instance of the window side by side (gridDim.y = instances), so
+// one launch per stage serves W steps x P_local partitions.
+//
+// Per hop i (K1/K2):
+//   k_count_scan : deg-capped counts min(deg, k_i) of F_i, exclusive offsets
+//                  by a single-pass decoupled look-back scan;
+//   k_sample     : warp per frontier node, lane j draws u_j = Philox(node,
+//                  (i<<16)|j, step, (p<<8)|1) (R#4), r_j = mulhi(u_j, t_j+1)
+//                  (R#5), Floyd resolution by k shuffles (R#6); writes the
+//                  neighbour's local rank and marks it in the new-node bitmap
+//                  unless it is already in F_i;
+//   k_compact    : the bitmap in rank order IS the ascending-id order, so a
+//                  popcount scan appends sorted_unique(cols_i) \ F_i to the
+//                  frontier (R#7) and records every node's frontier position.
+// After the last hop k_relabel rewrites the sampled columns as positions in
+// F_{i+1} (the DGL block layout the consumer indexes X with).
+#include "launch.h"
+
+namespace mgnn {
+
+constexpr int kThreads = 256;
+constexpr int kScanItems = 8;                         // count scan: items per thread
+constexpr int kScanTile = kThreads * kScanItems;      // 2048 frontier nodes per tile
+constexpr int kWordItems = 4;                         // compact: bitmap words per thread
+constexpr int kWordTile = kThreads * kWordItems;      // 1024 words = 32768 ranks per tile
+
+int64_t scan_tiles_count(int64_t fcap) { return (fcap + kScanTile - 1) / kScanTile; }
+int64_t scan_tiles_words(int64_t words) { return (words + kWordTile - 1) / kWordTile; }
+
+static inline unsigned grid_x_for(int64_t items_per_inst, int items_per_block, int n_inst) {
+    // enough blocks to cover one instance, but about 16 resident blocks per SM overall
+    int64_t need = (items_per_inst + items_per_block - 1) / items_per_block;
+    int64_t target = (148 * 16 + n_inst - 1) / n_inst;
+    int64_t g = need < target ? need : target;
+    return (unsigned)(g < 1 ? 1 : g);
+}
+
+// ------------------------------------------------------------------ seeds: F_0 (R#8)
+__global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
+    const int m = blockIdx.y;
+    const int lp = m / W.n_steps, w = m % W.n_steps;
+    const PartDev& pd = W.parts[lp];
+    const uint64_t t = W.step0 + (uint64_t)w;
+    const int32_t* src;
+    int64_t n0;
+    if (W.ext_seeds) {
+        src = W.ext_seeds + (int64_t)m * W.batch;
+        n0 = W.ext_counts[m];
+        if (n0 < 1 || n0 > W.batch) {
+            if (threadIdx.x == 0 && blockIdx.x == 0) atomicOr(W.err, 1);
+            n0 = 0;
+        }
+    } else {
+        const int64_t e = (int64_t)((t - 1) / (uint64_t)pd.nbatch), b = (int64_t)((t - 1) % (uint64_t)pd.nbatch);
+        const int32_t* perm = pd.perm + (int64_t)(e % pd.perm_slots) * pd.n_train;
+        const int64_t s0 = b * W.batch;
+        n0 = pd.n_train - s0 < W.batch ? pd.n_train - s0 : W.batch;
+        src = perm + s0;
+    }
+    int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
+    int32_t* pos = W.pos_of + (int64_t)m * W.vp_stride;
+    uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n0; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t gid = src[j];
+        int64_t row = gid - pd.lo;
+        if (row < 0 || row >= pd.n_local) {      // external seed not owned by this partition
+            atomicOr(W.err, 1);
+            row = 0;
+        }
+        const int32_t r = (int32_t)(pd.h_below + row);
+        fr[j] = r;
+        W.fr_gid[(int64_t)m * W.ucap + j] = (int32_t)gid;   // F_0 readable right after sampling
+        pos[r] = (int32_t)j;
+        const uint32_t bit = 1u << (r & 31);
+        if (atomicOr(&fb[r >> 5], bit) & bit) atomicOr(W.err, 2);   // duplicate seed
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) W.hop_size[(int64_t)m * (kMaxLayers + 1)] = n0;
+}
+
+// ------------------------------------------------------------------ counts + offsets (single-pass scan)
+__global__ void __launch_bounds__(kThreads) k_count_scan(WinDev W, int hop, Scratch sc, int64_t tiles_max) {
+    __shared__ long long sm[8];
+    __shared__ int tslot;
+    __shared__ long long prefix_sh;
+    const int m = blockIdx.y;
+    const PartDev& pd = W.parts[m / W.n_steps];
+    const int64_t nF = W.hop_size[(int64_t)m * (kMaxLayers + 1) + hop];
+    const int64_t ntiles = (nF + kScanTile - 1) / kScanTile;
+    const int tile = claim_tile(sc.tilectr + m, &tslot);
+    if (tile >= ntiles) {
+        if (tile == 0 && threadIdx.x == 0) W.off[hop][(int64_t)m * W.off_stride[hop]] = 0;   // empty F_i
+        return;
+    }
+    const int k = W.k_hop[hop];
+    const int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
+    int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
+    const int64_t f0 = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    int cnt[kScanItems];
+    long long sum = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        const int64_t f = f0 + i;
+        int c = 0;
+        if (f < nF) {
+            const int64_t row = (int64_t)fr[f] - pd.h_below;
+            if (row >= 0 && row < pd.n_local) {       // halo frontier nodes are leaves (R#1)
+                const int64_t d = pd.indptr[row + 1] - pd.indptr[row];
+                c = (int)(d < k ? d : k);             // |sample| = min(deg, k) (R#3)
+            }
+        }
+        cnt[i] = c;
+        sum += c;
+    }
+    long long agg;
+    long long excl = block_excl_scan256(sum, sm, &agg);
+    if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
+                                                                     (unsigned long long)agg);
+    __syncthreads();
+    long long run = prefix_sh + excl;
+    if (tile == 0 && threadIdx.x == 0) off[0] = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        const int64_t f = f0 + i;
+        run += cnt[i];
+        if (f < nF) {
+            MGNN_CHECK(f + 1 < W.off_stride[hop], "off f=%lld", (long long)f);
+            off[f + 1] = run;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ sampling (warp per frontier node)
+__global__ void __launch_bounds__(kThreads) k_sample(WinDev W, int hop) {
+    const int m = blockIdx.y;
+    const int lp = m / W.n_steps, w = m % W.n_steps;
+    const PartDev& pd = W.parts[lp];
+    const uint32_t step = (uint32_t)(W.step0 + (uint64_t)w);
+    const int64_t nF = W.hop_size[(int64_t)m * (kMaxLayers + 1) + hop];
+    const int k = W.k_hop[hop];
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (kThreads / 32);
+    const int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
+    const int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
+    int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop];
+    const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
+    uint32_t* nb = W.nb + (int64_t)m * W.bm_words;
+    const uint32_t c1 = (uint32_t)hop << 16;
+    const uint32_t c3 = ((uint32_t)pd.part_id << 8) | kStreamSample;
+    const int64_t h_below = pd.h_below, n_local = pd.n_local, lo = pd.lo;
+    const int64_t* __restrict__ indptr = pd.indptr;
+    const int32_t* __restrict__ crank = pd.cols_rank;
+    for (int64_t f = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); f < nF; f += nwarps) {
+        const int64_t row = (int64_t)fr[f] - h_below;
+        if (row < 0 || row >= n_local) continue;
+        const int64_t b0 = indptr[row];
+        const int64_t d = indptr[row + 1] - b0;
+        const int64_t o = off[f];
+        int32_t c = -1;
+        int j = lane;
+        if (d <= k) {                                    // whole neighbourhood in CSR order (R#3)
+            if (lane < d) c = crank[b0 + lane];
+        } else {
+            uint32_t r = 0, t = 0;
+            if (lane < k) {
+                const u4 u = philox4x32_10(u4{(uint32_t)(lo + row), c1 | (uint32_t)lane, step, c3}, W.seed_lo,
+                                           W.seed_hi);
+                t = (uint32_t)(d - k + lane);
+                r = __umulhi(u.x, t + 1u);               // floor(u (t+1) / 2^32)
+            }
+            bool coll = false;                           // Floyd: pos_j = r_j unless already chosen, else t_j
+            for (int jj = 0; jj < k; ++jj) {
+                const uint32_t pj = __shfl_sync(kFull, coll ? t : r, jj);
+                if (lane > jj && r == pj) coll = true;
+            }
+            if (lane < k) c = crank[b0 + (coll ? t : r)];
+        }
+        if (c >= 0) {
+            MGNN_CHECK(o + j < W.col_stride[hop] && c < pd.vp, "cols o=%lld j=%d c=%d", (long long)o, j, c);
+            cols[o + j] = c;
+            const uint32_t bit = 1u << (c & 31);
+            if (!(fb[c >> 5] & bit)) atomicOr(&nb[c >> 5], bit);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ bitmap -> sorted new frontier nodes
+__global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch sc, int64_t tiles_max) {
+    __shared__ long long sm[8];
+    __shared__ int tslot;
+    __shared__ long long prefix_sh;
+    const int m = blockIdx.y;
+    const PartDev& pd = W.parts[m / W.n_steps];
+    const int64_t nwords = (pd.vp + 31) >> 5;
+    const int64_t ntiles = (nwords + kWordTile - 1) / kWordTile;
+    const int tile = claim_tile(sc.tilectr + m, &tslot);
+    if (tile >= ntiles) return;
+    uint32_t* nb = W.nb + (int64_t)m * W.bm_words;
+    uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
+    const int64_t w0 = (int64_t)tile * kWordTile + (int64_t)threadIdx.x * kWordItems;
+    uint32_t bits[kWordItems];
+    long long cnt = 0;
+#pragma unroll
+    for (int i = 0; i < kWordItems; ++i) {
+        bits[i] = (w0 + i < nwords) ? nb[w0 + i] : 0u;
+        cnt += __popc(bits[i]);
+    }
+    long long agg;
+    long long excl = block_excl_scan256(cnt, sm, &agg);
+    int64_t* hs = W.hop_size + (int64_t)m * (kMaxLayers + 1);
+    if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
+                                                                     (unsigned long long)agg);
+    __syncthreads();
+    const int64_t nF = hs[hop];
+    int64_t pos = nF + prefix_sh + excl;
+    int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
+    int32_t* posof = W.pos_of + (int64_t)m * W.vp_stride;
+#pragma unroll
+    for (int i = 0; i < kWordItems; ++i) {
+        uint32_t b = bits[i];
+        if (b) {
+            fb[w0 + i] |= b;
+            nb[w0 + i] = 0u;
+        }
+        while (b) {
+            const int bi = __ffs(b) - 1;
+            b &= b - 1;
+            const int32_t r = (int32_t)((w0 + i) * 32 + bi);
+            MGNN_CHECK(pos < W.ucap && r < pd.vp, "compact pos=%lld r=%d", (long long)pos, r);
+            fr[pos] = r;
+            posof[r] = (int32_t)pos;
+            ++pos;
+        }
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) hs[hop + 1] = nF + prefix_sh + agg;
+}
+
+// ------------------------------------------------------------------ cols: rank -> position in F_{i+1}
+__global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
+    const int m = blockIdx.y;
+    const int32_t* posof = W.pos_of + (int64_t)m * W.vp_stride;
+    const int64_t* hs = W.hop_size + (int64_t)m * (kMaxLayers + 1);
+    const int64_t stride = (int64_t)gridDim.x * kThreads;
+    for (int hop = 0; hop < W.L; ++hop) {
+        const int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
+        int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop];
+        const int64_t E = off[hs[hop]];
+        for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < E; e += stride) cols[e] = posof[cols[e]];
+    }
+}
+
+// ------------------------------------------------------------------ launchers
+void launch_seeds(const WinDev& w, cudaStream_t s) {
+    dim3 grid(grid_x_for(w.batch, kThreads, w.n_inst), w.n_inst);
+    k_seeds<<<grid, kThreads, 0, s>>>(w);
+    count_launches(1, __func__);
+}
+
+void launch_count_scan(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s) {
+    const int64_t tiles = scan_tiles_count(fcap);
+    dim3 grid((unsigned)(tiles < 1 ? 1 : tiles), w.n_inst);
+    k_count_scan<<<grid, kThreads, 0, s>>>(w, hop, sc, tiles < 1 ? 1 : tiles);
+    count_launches(1, __func__);
+}
+
+void launch_sample(const WinDev& w, int hop, int64_t fcap, cudaStream_t s) {
+    dim3 grid(grid_x_for(fcap, kThreads / 32, w.n_inst), w.n_inst);
+    k_sample<<<grid, kThreads, 0, s>>>(w, hop);
+    count_launches(1, __func__);
+}
+
+void launch_compact(const WinDev& w, int hop, Scratch sc, cudaStream_t s) {
+    const int64_t tiles = scan_tiles_words(w.bm_words);
+    dim3 grid((unsigned)(tiles < 1 ? 1 : tiles), w.n_inst);
+    k_compact<<<grid, kThreads, 0, s>>>(w, hop, sc, tiles < 1 ? 1 : tiles);
+    count_launches(1, __func__);
+}
+
+void launch_relabel(const WinDev& w, cudaStream_t s) {
+    int64_t e_max = 0;
+    for (int i = 0; i < w.L; ++i) e_max = w.col_stride[i] > e_max ? w.col_stride[i] : e_max;
+    dim3 grid(grid_x_for(e_max, kThreads, w.n_inst), w.n_inst);
+    k_relabel<<<grid, kThreads, 0, s>>>(w);
+    count_launches(1, __func__);
+}
+
+}  // namespace mgnn

@@ -1,0 +1,258 @@
+// score.cu -- scoreboards and buffer maintenance (§3.2, Alg.2 l.6-9,
+// l.12-19, EVICT_AND_REPLACE l.25-34; Alg.1 INITIALIZE_PREFETCHER).
+//
+// fp32 throughout with explicit round-to-nearest intrinsics and no FTZ
+// (DESIGN R#12), so every score is bit-identical to the step-by-step oracle.
+#include "launch.h"
+
+namespace mgnn {
+
+constexpr int kSThreads = 256;
+
+static inline unsigned blocks_for(int64_t n, int per_block) {
+    int64_t b = (n + per_block - 1) / per_block;
+    if (b > 148 * 8) b = 148 * 8;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+// ------------------------------------------------------------------ decay (Alg.2 l.6-9)
+// Slot s was hit at popc(mask) of the window's n_steps steps; each other step
+// multiplies S_E by gamma once (the same sequence of RN products the paper's
+// per-step loop performs: only *gamma ever touches S_E between rounds).
+__global__ void __launch_bounds__(kSThreads) k_decay(const PartDev* __restrict__ parts, int n_steps, float gamma) {
+    const PartDev& pd = parts[blockIdx.y];
+    for (int64_t s = (int64_t)blockIdx.x * kSThreads + threadIdx.x; s < pd.cap; s += (int64_t)gridDim.x * kSThreads) {
+        const unsigned long long mask = pd.hitmask[s];
+        const int unused = n_steps - __popcll(mask);
+        float v = pd.se[s];
+        for (int i = 0; i < unused; ++i) v = __fmul_rn(v, gamma);
+        pd.se[s] = v;
+        if (mask) pd.hitmask[s] = 0ull;
+    }
+}
+
+void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, float gamma, cudaStream_t s) {
+    if (cap_max < 1) return;
+    dim3 grid(blocks_for(cap_max, kSThreads), n_lp);
+    k_decay<<<grid, kSThreads, 0, s>>>(parts, n_steps, gamma);
+    count_launches(1, __func__);
+}
+
+// ------------------------------------------------------------------ candidate selection
+// Segment 2*lp   : E = {slots s : S_E[s] < alpha}                       (R#16)
+//                  key = (S_E bits << 32) | node id   -> ascending = (S_E asc, id asc)
+// Segment 2*lp+1 : R = {halo h : not buffered, S_A[h] >= theta_r}     (R#17)
+//                  key = (~S_A bits << 32) | ~deg_in  -> ascending = (S_A desc, deg_in desc);
+//                  items enter in halo order (= id asc) and the sort is stable (R#18).
+// Scores here are >= +0, so their IEEE bit patterns order like the values.
+// Order-preserving compaction by a decoupled look-back scan.
+__global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict__ parts, float alpha, float theta_r,
+                                                      const SortSeg* __restrict__ segs, long long* __restrict__ n_out,
+                                                      Scratch sc, int64_t tiles_max) {
+    __shared__ long long sm[8];
+    __shared__ int tslot;
+    __shared__ long long prefix_sh;
+    const int sg = blockIdx.y;
+    const PartDev& pd = parts[sg >> 1];
+    const bool isE = (sg & 1) == 0;
+    const int64_t n = isE ? pd.cap : pd.n_h;
+    const int64_t tile_items = kSThreads * 8;
+    const int64_t ntiles = (n + tile_items - 1) / tile_items;
+    const int tile = claim_tile(sc.tilectr + sg, &tslot);
+    if (tile >= ntiles) {
+        if (ntiles == 0 && tile == 0 && threadIdx.x == 0) n_out[sg] = 0;
+        return;
+    }
+    const int64_t i0 = (int64_t)tile * tile_items + (int64_t)threadIdx.x * 8;
+    unsigned flags = 0;
+    long long cnt = 0;
+    for (int i = 0; i < 8; ++i) {
+        const int64_t x = i0 + i;
+        bool pf = false;
+        if (x < n) pf = isE ? (pd.se[x] < alpha) : (pd.slot_of[x] < 0 && pd.sa[x] >= theta_r);
+        flags |= (unsigned)pf << i;
+        cnt += pf;
+    }
+    long long agg;
+    long long excl = block_excl_scan256(cnt, sm, &agg);
+    if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)sg * tiles_max, tile,
+                                                                     (unsigned long long)agg);
+    __syncthreads();
+    int64_t pos = prefix_sh + excl;
+    const SortSeg out = segs[sg];
+    for (int i = 0; i < 8; ++i) {
+        if (!((flags >> i) & 1u)) continue;
+        const int64_t x = i0 + i;
+        unsigned long long key;
+        if (isE) {
+            const uint32_t node = (uint32_t)pd.halo_ids[pd.slot_h[x]];
+            key = ((unsigned long long)__float_as_uint(pd.se[x]) << 32) | node;
+        } else {
+            key = ((unsigned long long)(~__float_as_uint(pd.sa[x])) << 32) | (uint32_t)(~(uint32_t)pd.deg_in[x]);
+        }
+        MGNN_CHECK(pos < n, "select pos=%lld n=%lld sg=%d", (long long)pos, (long long)n, sg);
+        out.keys[pos] = key;
+        out.vals[pos] = (uint32_t)x;
+        ++pos;
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) n_out[sg] = prefix_sh + agg;
+}
+
+void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, float theta_r, const SortSeg* segs,
+                   long long* n_out, Scratch sc, cudaStream_t s) {
+    int64_t tiles = (n_max + kSThreads * 8 - 1) / (kSThreads * 8);
+    if (tiles < 1) tiles = 1;
+    dim3 grid((unsigned)tiles, 2 * n_lp);
+    k_select<<<grid, kSThreads, 0, s>>>(parts, alpha, theta_r, segs, n_out, sc, tiles);
+    count_launches(1, __func__);
+}
+
+// ------------------------------------------------------------------ swap + refill
+// Pair i (i < k = min(|E|, |R|), R#19): slot s = E[i], evicted e, replacement r = R[i]:
+//   S_A[e] <- S_E[s]; slot_of[e] <- -1; BUF[s] <- r; S_E[s] <- S_A[r]; S_A[r] <- -1
+// then the row of r is copied from its owner's table into the slot.
+// E and R are disjoint (buffered vs. not), so pairs never conflict.
+__global__ void __launch_bounds__(kSThreads) k_swap_refill(const PartDev* __restrict__ parts,
+                                                           const SortSeg* __restrict__ segs, WorldDev G,
+                                                           long long* counts, int64_t counts_stride, int n_steps) {
+    const int lp = blockIdx.y;
+    const PartDev& pd = parts[lp];
+    const SortSeg E = segs[2 * lp], R = segs[2 * lp + 1];
+    const long long nE = *E.n, nR = *R.n;
+    const long long k = nE < nR ? nE : nR;
+    const int lane = threadIdx.x & 31;
+    const int pitch = G.pitch;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        long long* cn = counts + ((int64_t)lp * n_steps + (n_steps - 1)) * counts_stride;
+        cn[4] = k;
+        cn[5] = k;
+        cn[6] += k;
+    }
+    const int64_t nwarps = (int64_t)gridDim.x * (kSThreads / 32);
+    for (int64_t i = (int64_t)blockIdx.x * (kSThreads / 32) + (threadIdx.x >> 5); i < k; i += nwarps) {
+        const int32_t s = (int32_t)E.vals[i];
+        const int32_t r = (int32_t)R.vals[i];
+#ifdef MGNN_CHECKS
+        if (s < 0 || s >= pd.cap || r < 0 || r >= pd.n_h || k > pd.cap) {
+            if (lane == 0)
+                printf("swap lp=%d i=%lld k=%lld nE=%lld nR=%lld s=%d r=%d cap=%lld nh=%lld\n", lp, (long long)i, k,
+                       nE, nR, s, r, (long long)pd.cap, (long long)pd.n_h);
+            __trap();
+        }
+#endif
+        if (lane == 0) {
+            const int32_t e = pd.slot_h[s];
+            const float se_s = pd.se[s];
+            const float sa_r = pd.sa[r];
+            pd.sa[e] = se_s;
+            pd.slot_of[e] = -1;
+            pd.slot_h[s] = r;
+            pd.slot_of[r] = s;
+            pd.se[s] = sa_r;
+            pd.sa[r] = -1.0f;
+        }
+        const int32_t gid = pd.halo_ids[r];
+        const int q = owner_of(G.bounds, G.n_parts, gid);
+        const float* src = G.tables[q] + ((int64_t)gid - G.bounds[q]) * pitch;
+        float* dst = pd.rows + (int64_t)s * pitch;
+        for (int c = lane * 4; c < pitch; c += 128)
+            *reinterpret_cast<float4*>(dst + c) = __ldg(reinterpret_cast<const float4*>(src + c));
+    }
+}
+
+void launch_swap_refill(const PartDev* parts, int n_lp, int64_t cap_max, const SortSeg* segs, const WorldDev& world,
+                        long long* counts, int64_t counts_stride, int n_steps, cudaStream_t s) {
+    dim3 grid(blocks_for(cap_max < 1 ? 1 : cap_max, kSThreads / 32), n_lp);
+    k_swap_refill<<<grid, kSThreads, 0, s>>>(parts, segs, world, counts, counts_stride, n_steps);
+    count_launches(1, __func__);
+}
+
+// ------------------------------------------------------------------ INITIALIZE_PREFETCHER
+// keys = ~deg_in (ascending = degree desc), values = halo index in id order.
+__global__ void k_init_keys(const PartDev* __restrict__ pdp, const SortSeg* __restrict__ seg, long long* n_dev) {
+    const PartDev& pd = *pdp;
+    const SortSeg sg = *seg;
+    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < pd.n_h; h += (int64_t)gridDim.x * blockDim.x) {
+        sg.keys[h] = (unsigned long long)(~(uint32_t)pd.deg_in[h]);
+        sg.vals[h] = (uint32_t)h;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = pd.n_h;
+}
+
+void launch_init_keys(const PartDev* pd_dev, int64_t n_h, const SortSeg* seg, long long* n_dev, cudaStream_t s) {
+    k_init_keys<<<blocks_for(n_h < 1 ? 1 : n_h, kSThreads), kSThreads, 0, s>>>(pd_dev, seg, n_dev);
+    count_launches(1, __func__);
+}
+
+// S_A = 0 for every halo node, then for the top-cap: slot s <- order[s], S_E = 1, S_A = -1.
+__global__ void k_init_reset(const PartDev* __restrict__ pdp) {
+    const PartDev& pd = *pdp;
+    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < pd.n_h; h += (int64_t)gridDim.x * blockDim.x) {
+        pd.sa[h] = 0.0f;
+        pd.slot_of[h] = -1;
+    }
+}
+
+__global__ void k_init_slots(const PartDev* __restrict__ pdp, const uint32_t* __restrict__ order) {
+    const PartDev& pd = *pdp;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < pd.cap; s += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t h = (int32_t)order[s];
+        pd.slot_h[s] = h;
+        pd.slot_of[h] = (int32_t)s;
+        pd.se[s] = 1.0f;
+        pd.sa[h] = -1.0f;
+        pd.hitmask[s] = 0ull;
+    }
+}
+
+void launch_init_fill(const PartDev* pd_dev, int64_t n_h, int64_t cap, const uint32_t* order, cudaStream_t s) {
+    k_init_reset<<<blocks_for(n_h < 1 ? 1 : n_h, kSThreads), kSThreads, 0, s>>>(pd_dev);
+    k_init_slots<<<blocks_for(cap < 1 ? 1 : cap, kSThreads), kSThreads, 0, s>>>(pd_dev, order);
+    count_launches(2, __func__);
+}
+
+// BUF rows of every slot from the owners' tables (the init "RPC").
+__global__ void k_rows_from_owners(const PartDev* __restrict__ pdp, WorldDev G) {
+    const PartDev& pd = *pdp;
+    const int lane = threadIdx.x & 31;
+    const int pitch = G.pitch;
+    for (int64_t s = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); s < pd.cap;
+         s += (int64_t)gridDim.x * (blockDim.x / 32)) {
+        const int32_t gid = pd.halo_ids[pd.slot_h[s]];
+        const int q = owner_of(G.bounds, G.n_parts, gid);
+        const float* src = G.tables[q] + ((int64_t)gid - G.bounds[q]) * pitch;
+        float* dst = pd.rows + s * pitch;
+        for (int c = lane * 4; c < pitch; c += 128)
+            *reinterpret_cast<float4*>(dst + c) = __ldg(reinterpret_cast<const float4*>(src + c));
+    }
+}
+
+void launch_rows_from_owners(const PartDev* pd_dev, int64_t cap, const WorldDev& world, cudaStream_t s) {
+    if (cap < 1) return;
+    k_rows_from_owners<<<blocks_for(cap, kSThreads / 32), kSThreads, 0, s>>>(pd_dev, world);
+    count_launches(1, __func__);
+}
+
+// ------------------------------------------------------------------ epoch order keys (R#8)
+__global__ void k_perm_keys(const PartDev* __restrict__ pdp, uint64_t epoch, uint32_t k0, uint32_t k1,
+                            const SortSeg* __restrict__ seg) {
+    const PartDev& pd = *pdp;
+    const SortSeg sg = *seg;
+    const uint32_t c3 = ((uint32_t)pd.part_id << 8) | kStreamShuffle;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pd.n_train;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t id = (uint32_t)pd.train_ids[i];
+        const u4 o = philox4x32_10(u4{id, (uint32_t)epoch, 0u, c3}, k0, k1);
+        sg.keys[i] = ((unsigned long long)o.x << 32) | o.y;
+        sg.vals[i] = id;
+    }
+}
+
+void launch_perm_keys(const PartDev* pd_dev, int64_t n_train, uint64_t epoch, uint32_t seed_lo, uint32_t seed_hi,
+                      const SortSeg* seg, cudaStream_t s) {
+    k_perm_keys<<<blocks_for(n_train < 1 ? 1 : n_train, kSThreads), kSThreads, 0, s>>>(pd_dev, epoch, seed_lo, seed_hi,
+                                                                                       seg);
+    count_launches(1, __func__);
+}
+
+}  // namespace mgnn

@@ -1,0 +1,88 @@
+"""GPU (libmgnn.so, sm_100a) vs CPU oracle parity -- bit-exact (-m gpu).
+
+Every comparison is element by element on the same seeded inputs; scores
+are compared as fp32 bit patterns (0 ULP, BASELINE.json north_star).
+"""
+import numpy as np
+import pytest
+
+from inputs import synth
+from tests.parity_util import run_parity
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    return synth.generate(synth.CONFIGS["cfg1"])
+
+
+def test_cfg1_per_step(cfg1):
+    """configs[0]: 10k nodes, 2 partitions, [10,25], B=256, f=0.25 -- one step per window."""
+    st = run_parity(cfg1, 2, 64, [10, 25], 256, 2500, 0.9, 4, 1.0, [1] * 12)
+    assert st["hits"] > 0 and st["misses"] > 0 and st["evicted"] > 0
+
+
+@pytest.mark.parametrize("wins", [[4, 4, 4, 4], [2, 2, 4, 3, 1, 4], [8, 8, 8]])
+def test_cfg1_windows(cfg1, wins):
+    """Window batching (several steps per launch) is bit-identical to the per-step oracle."""
+    delta = 8 if wins[0] == 8 else 4
+    st = run_parity(cfg1, 2, 64, [10, 25], 256, 2500, 0.9, delta, 1.0, wins)
+    assert st["evicted"] > 0
+
+
+@pytest.mark.parametrize("delta,gamma,theta,f_bp", [
+    (1, 0.5, 0.0, 2500), (3, 0.95, 1.0, 2500), (16, 1.0, 1.0, 2500), (2, 0.5, 1.0, 10000),
+    (2, 0.5, 1.0, 0), (0, 0.95, 1.0, 2500), (3, 0.95, 0.0, 5000), (1, 0.95, 1.0, 1),
+])
+def test_cfg1_policy_grid(cfg1, delta, gamma, theta, f_bp):
+    wins = [delta] * 6 if delta > 0 else [5, 5]
+    st = run_parity(cfg1, 2, 64, [10, 25], 256, f_bp, gamma, delta, theta, wins)
+    if f_bp == 0:
+        assert st["hits"] == 0
+    if f_bp == 10000:
+        assert st["misses"] == 0
+
+
+def test_cfg1_three_hops_and_partitions(cfg1):
+    run_parity(cfg1, 3, 64, [5, 10, 15], 128, 3500, 0.95, 4, 1.0, [4, 4, 4])
+
+
+def test_alpha_zero_never_evicts(cfg1):
+    st = run_parity(cfg1, 2, 64, [10, 25], 256, 2500, 0.5, 2, 1.0, [2] * 4, alpha=0.0)
+    assert st["evicted"] == 0
+
+
+def test_full_fanout_small_graph_edge_cases():
+    """fanout >= max degree, batch > n_train (single partial batch per epoch), epochs wrap in a window,
+    odd feature width (D=7 -> pitch 8), a partition without halo nodes (P=1)."""
+    g = synth.random_graph(40, 0.15, 3, train_frac=0.5)
+    run_parity(g, 2, 7, [32, 32], 64, 5000, 0.9, 3, 1.0, [3, 3, 3])
+    run_parity(g, 2, 7, [2, 3], 3, 5000, 0.9, 5, 0.0, [5, 5, 5, 5])
+    run_parity(g, 1, 4, [3, 3], 4, 5000, 0.9, 2, 1.0, [2, 2])
+
+
+def test_external_seeds(cfg1):
+    rng = np.random.default_rng(5)
+    cache = {}
+
+    def seeds(pid, step):
+        key = (pid, step)
+        if key not in cache:
+            lo, hi = pid * 5000, (pid + 1) * 5000
+            n = int(rng.integers(1, 200))
+            cache[key] = np.sort(rng.choice(np.arange(lo, hi), n, replace=False)).astype(np.int32)[::-1].copy()
+        return cache[key]
+
+    run_parity(cfg1, 2, 64, [10, 25], 256, 2500, 0.9, 4, 1.0, [4, 4], ext_seeds=seeds)
+
+
+@pytest.mark.slow
+def test_arxiv_full_size_bench_config():
+    """configs[1] at full size in the bench launch configuration: P=2 on one GPU, [10,25], B=1000,
+    f=0.25, gamma=0.995, Delta=32 (paper's GPU optimum for 2 partitions), 32-step windows."""
+    g = synth.generate(synth.CONFIGS["arxiv"])
+    st = run_parity(g, 2, 128, [10, 25], 1000, 2500, 0.995, 32, 1.0, [32, 32, 32], sample_every=7,
+                    check_x_rows=4096)
+    assert st["evicted"] > 0
