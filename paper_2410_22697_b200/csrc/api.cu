@@ -49,7 +49,8 @@ struct Part {
     int32_t* slot_h = nullptr;
     unsigned long long* hitmask = nullptr;
     int32_t* perm = nullptr;
-    std::vector<int64_t> perm_epoch;     // epoch held by each perm slot (-1 none)
+    int32_t perm_chunk = 1;              // G: epoch orders generated per sort call
+    int64_t chunk_loaded[2] = {-1, -1};  // chunk id c (epochs [cG, cG+G)) held by ring half c % 2
     // sort buffers: E (cap) / R (n_h) for eviction; R also serves buffer init; P (n_train) for epoch orders
     unsigned long long *ek = nullptr, *ekt = nullptr, *rk = nullptr, *rkt = nullptr, *pk = nullptr, *pkt = nullptr;
     uint32_t *ev = nullptr, *evt = nullptr, *rv = nullptr, *rvt = nullptr, *pvt = nullptr;
@@ -107,8 +108,8 @@ struct mgnn_ctx_s {
     size_t ev_zero_bytes = 0;
     Scratch ev_sc{};
     int64_t ev_tiles = 1;
-    uint32_t* hist = nullptr;
-    size_t hist_words = 0;
+    void* sort_scr = nullptr;            // radix sort scratch (histograms + look-back words)
+    size_t sort_scr_bytes = 0;
     // sampler
     bool configured = false;
     int32_t L = 0, batch = 0, max_window = 0;
@@ -258,8 +259,18 @@ void free_buffer(Part& p) {
 
 void free_perm(Part& p) {
     dfree(p.perm); dfree(p.pk); dfree(p.pkt); dfree(p.pvt);
-    p.perm_epoch.clear();
+    p.chunk_loaded[0] = p.chunk_loaded[1] = -1;
     p.perm_slots = 0;
+}
+
+mgnn_status ensure_sort_scratch(mgnn_ctx ctx, size_t bytes) {
+    if (bytes <= ctx->sort_scr_bytes) return MGNN_OK;
+    if (ctx->sort_scr) cudaFree(ctx->sort_scr);
+    ctx->sort_scr = nullptr;
+    ctx->sort_scr_bytes = 0;
+    CK(cudaMalloc(&ctx->sort_scr, bytes));
+    ctx->sort_scr_bytes = bytes;
+    return MGNN_OK;
 }
 
 WinDev win_dev(mgnn_ctx ctx, Win& w) {
@@ -370,7 +381,7 @@ void mgnn_destroy(mgnn_ctx ctx) {
     dfree(ctx->d_evsegs);
     dfree(ctx->d_sel_n);
     dfree(ctx->ev_zero);
-    dfree(ctx->hist);
+    if (ctx->sort_scr) cudaFree(ctx->sort_scr);
     dfree(ctx->d_permsegs);
     dfree(ctx->d_perm_n);
     delete ctx;
@@ -579,21 +590,17 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
     ctx->ev_sc.tilectr = (int32_t*)ctx->ev_zero;
     ctx->ev_sc.status = (unsigned long long*)(ctx->ev_zero + ((2 * n_lp * 4 + 63) / 64) * 64);
     ctx->ev_zero_bytes = ((2 * n_lp * 4 + 63) / 64) * 64 + (size_t)(2 * n_lp) * ctx->ev_tiles * 8;
-    size_t hw = radix_hist_words(2 * n_lp, n_sort_max);
-    if (ctx->configured) {
-        for (auto& p : ctx->parts) hw = std::max(hw, radix_hist_words(1, std::max<int64_t>(p.n_train, 1)));
-    }
-    if (hw > ctx->hist_words) {
-        dfree(ctx->hist);
-        CK(dalloc(&ctx->hist, hw));
-        ctx->hist_words = hw;
+    {
+        mgnn_status st2 = ensure_sort_scratch(ctx, std::max(radix_scratch_bytes(2 * n_lp, n_sort_max, 64),
+                                                             radix_scratch_bytes(1, std::max<int64_t>(nh_max, 1), 32)));
+        if (st2) return st2;
     }
     WorldDev G = world_of(ctx);
     for (int lp = 0; lp < n_lp; ++lp) {
         Part& p = ctx->parts[lp];
         // order V_p^h by (deg_in desc, id asc) (R#10) and take the first cap
         launch_init_keys(ctx->d_parts + lp, p.n_h, ctx->d_evsegs + 2 * lp + 1, ctx->d_sel_n + 2 * lp + 1, s);
-        radix_sort_pairs(ctx->d_evsegs + 2 * lp + 1, 1, std::max<int64_t>(p.n_h, 1), 32, ctx->hist, s);
+        radix_sort_pairs(ctx->d_evsegs + 2 * lp + 1, 1, std::max<int64_t>(p.n_h, 1), 32, ctx->sort_scr, s);
         launch_init_fill(ctx->d_parts + lp, p.n_h, p.cap, p.rv, s);
         launch_rows_from_owners(ctx->d_parts + lp, p.cap, G, s);
         CKL();
@@ -682,15 +689,24 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
         }
         w.alloc = true;
     }
-    // epoch orders: ring of perm slots per partition
+    // epoch orders (R#8): a ring of 2G orders per partition, generated G epochs per sort call
+    // (G >= the epochs one window can span, so a window's epochs live in at most two ring halves).
     ctx->perm_slots_max = 1;
+    size_t scr = 0;
     for (auto& p : ctx->parts) {
         p.nbatch = p.n_train > 0 ? (p.n_train + batch - 1) / batch : 1;
-        p.perm_slots = (int32_t)((max_window + p.nbatch - 1) / p.nbatch + 1);
+        p.perm_chunk = (int32_t)std::max<int64_t>(8, (max_window + p.nbatch - 1) / p.nbatch + 1);
+        p.perm_slots = 2 * p.perm_chunk;
         ctx->perm_slots_max = std::max(ctx->perm_slots_max, p.perm_slots);
-        p.perm_epoch.assign(p.perm_slots, -1);
-        CK(dalloc(&p.perm, (int64_t)p.perm_slots * std::max<int64_t>(p.n_train, 1)));
-        CK(dalloc(&p.pk, p.n_train)); CK(dalloc(&p.pkt, p.n_train)); CK(dalloc(&p.pvt, p.n_train));
+        p.chunk_loaded[0] = p.chunk_loaded[1] = -1;
+        const int64_t nt = std::max<int64_t>(p.n_train, 1);
+        CK(dalloc(&p.perm, (int64_t)p.perm_slots * nt));
+        CK(dalloc(&p.pk, p.perm_chunk * nt)); CK(dalloc(&p.pkt, p.perm_chunk * nt)); CK(dalloc(&p.pvt, p.perm_chunk * nt));
+        scr = std::max(scr, radix_scratch_bytes(p.perm_chunk, nt, 64));
+    }
+    {
+        mgnn_status st2 = ensure_sort_scratch(ctx, scr);
+        if (st2) return st2;
     }
     std::vector<SortSeg> ps((size_t)n_lp * ctx->perm_slots_max);
     dfree(ctx->d_perm_n);
@@ -699,21 +715,17 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
     for (int lp = 0; lp < n_lp; ++lp) {
         Part& p = ctx->parts[lp];
         pn[lp] = p.n_train;
-        for (int k = 0; k < p.perm_slots; ++k)
+        for (int k = 0; k < p.perm_slots; ++k) {   // slot k = half k / G, epoch-in-chunk j = k % G
+            const int64_t j = k % p.perm_chunk;
             ps[(size_t)lp * ctx->perm_slots_max + k] =
-                SortSeg{p.pk, (uint32_t*)(p.perm + (int64_t)k * p.n_train), p.pkt, p.pvt, ctx->d_perm_n + lp};
+                SortSeg{p.pk + j * p.n_train, (uint32_t*)(p.perm + (int64_t)k * p.n_train), p.pkt + j * p.n_train,
+                        p.pvt + j * p.n_train, ctx->d_perm_n + lp};
+        }
     }
     CK(cudaMemcpy(ctx->d_perm_n, pn.data(), n_lp * sizeof(long long), cudaMemcpyHostToDevice));
     dfree(ctx->d_permsegs);
     CK(dalloc(&ctx->d_permsegs, ps.size()));
     CK(cudaMemcpy(ctx->d_permsegs, ps.data(), ps.size() * sizeof(SortSeg), cudaMemcpyHostToDevice));
-    size_t hw = 0;
-    for (auto& p : ctx->parts) hw = std::max(hw, radix_hist_words(1, std::max<int64_t>(p.n_train, 1)));
-    if (hw > ctx->hist_words) {
-        dfree(ctx->hist);
-        CK(dalloc(&ctx->hist, hw));
-        ctx->hist_words = hw;
-    }
     mgnn_status st = upload_parts(ctx);
     if (st) return st;
     ctx->configured = true;
@@ -751,14 +763,14 @@ mgnn_status mgnn_sample(mgnn_ctx ctx, int32_t slot, uint64_t t0, int32_t n_steps
             Part& p = ctx->parts[lp];
             const int64_t e0 = (int64_t)((t0 - 1) / (uint64_t)p.nbatch);
             const int64_t e1 = (int64_t)((t0 + n_steps - 2) / (uint64_t)p.nbatch);
-            for (int64_t e = e0; e <= e1; ++e) {
-                const int k = (int)(e % p.perm_slots);
-                if (p.perm_epoch[k] == e) continue;
-                const SortSeg* seg = ctx->d_permsegs + (size_t)lp * ctx->perm_slots_max + k;
-                launch_perm_keys(ctx->d_parts + lp, p.n_train, (uint64_t)e, (uint32_t)ctx->run_seed,
-                                 (uint32_t)(ctx->run_seed >> 32), seg, s);
-                radix_sort_pairs(seg, 1, p.n_train, 64, ctx->hist, s);
-                p.perm_epoch[k] = e;
+            const int64_t G = p.perm_chunk;
+            for (int64_t c = e0 / G; c <= e1 / G; ++c) {     // epoch e lives in ring slot e % 2G
+                if (p.chunk_loaded[c % 2] == c) continue;
+                const SortSeg* segs = ctx->d_permsegs + (size_t)lp * ctx->perm_slots_max + (c % 2) * G;
+                launch_perm_keys(ctx->d_parts + lp, p.n_train, (uint64_t)(c * G), (int)G, (uint32_t)ctx->run_seed,
+                                 (uint32_t)(ctx->run_seed >> 32), segs, s);
+                radix_sort_pairs(segs, (int)G, p.n_train, 64, ctx->sort_scr, s);
+                p.chunk_loaded[c % 2] = c;
             }
         }
     } else {
@@ -839,7 +851,7 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
         CK(cudaMemsetAsync(ctx->ev_zero, 0, ctx->ev_zero_bytes, s));
         launch_select(ctx->d_parts, n_lp, nmax, ctx->pol.alpha, ctx->pol.theta_r, ctx->d_evsegs, ctx->d_sel_n,
                       ctx->ev_sc, s);
-        radix_sort_pairs(ctx->d_evsegs, 2 * n_lp, nmax, 64, ctx->hist, s);
+        radix_sort_pairs(ctx->d_evsegs, 2 * n_lp, nmax, 64, ctx->sort_scr, s);
         launch_swap_refill(ctx->d_parts, n_lp, cap_max, ctx->d_evsegs, world_of(ctx), w.counts, 8, w.n_steps, s);
     }
     CKL();

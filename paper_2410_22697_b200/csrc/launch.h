@@ -78,14 +78,14 @@ void launch_swap_refill(const PartDev* parts, int n_lp, int64_t cap_max, const S
 void launch_init_keys(const PartDev* pd_dev, int64_t n_h, const SortSeg* seg, long long* n_dev, cudaStream_t s);
 void launch_init_fill(const PartDev* pd_dev, int64_t n_h, int64_t cap, const uint32_t* order, cudaStream_t s);
 void launch_rows_from_owners(const PartDev* pd_dev, int64_t cap, const WorldDev& world, cudaStream_t s);
-void launch_perm_keys(const PartDev* pd_dev, int64_t n_train, uint64_t epoch, uint32_t seed_lo, uint32_t seed_hi,
-                      const SortSeg* seg, cudaStream_t s);
+// keys of n_epochs consecutive epoch orders (epoch0 ...) into segments segs[0..n_epochs)
+void launch_perm_keys(const PartDev* pd_dev, int64_t n_train, uint64_t epoch0, int n_epochs, uint32_t seed_lo,
+                      uint32_t seed_hi, const SortSeg* segs, cudaStream_t s);
 
 // sort.cu: stable LSD radix sort of (u64 key, u32 value) pairs over `bits` low key bits
 // (bits multiple of 16), each segment independently; n_max bounds every segment.
-void radix_sort_pairs(const SortSeg* segs_dev, int n_seg, int64_t n_max, int bits, uint32_t* hist_scratch,
-                      cudaStream_t s);
-size_t radix_hist_words(int n_seg, int64_t n_max);
+void radix_sort_pairs(const SortSeg* segs_dev, int n_seg, int64_t n_max, int bits, void* scratch, cudaStream_t s);
+size_t radix_scratch_bytes(int n_seg, int64_t n_max, int bits);
 
 // load.cu
 void launch_mark_halo(const int32_t* cols, int64_t nnz, int64_t lo, int64_t hi, uint32_t* bm, cudaStream_t s);

@@ -234,24 +234,26 @@ void launch_rows_from_owners(const PartDev* pd_dev, int64_t cap, const WorldDev&
 }
 
 // ------------------------------------------------------------------ epoch order keys (R#8)
-__global__ void k_perm_keys(const PartDev* __restrict__ pdp, uint64_t epoch, uint32_t k0, uint32_t k1,
-                            const SortSeg* __restrict__ seg) {
+__global__ void k_perm_keys(const PartDev* __restrict__ pdp, uint64_t epoch0, int n_epochs, uint32_t k0, uint32_t k1,
+                            const SortSeg* __restrict__ segs) {
     const PartDev& pd = *pdp;
-    const SortSeg sg = *seg;
     const uint32_t c3 = ((uint32_t)pd.part_id << 8) | kStreamShuffle;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pd.n_train;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = pd.n_train, total = n * n_epochs;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = x / n, i = x - j * n;
+        const SortSeg& sg = segs[j];
         const uint32_t id = (uint32_t)pd.train_ids[i];
-        const u4 o = philox4x32_10(u4{id, (uint32_t)epoch, 0u, c3}, k0, k1);
+        const u4 o = philox4x32_10(u4{id, (uint32_t)(epoch0 + j), 0u, c3}, k0, k1);
         sg.keys[i] = ((unsigned long long)o.x << 32) | o.y;
         sg.vals[i] = id;
     }
 }
 
-void launch_perm_keys(const PartDev* pd_dev, int64_t n_train, uint64_t epoch, uint32_t seed_lo, uint32_t seed_hi,
-                      const SortSeg* seg, cudaStream_t s) {
-    k_perm_keys<<<blocks_for(n_train < 1 ? 1 : n_train, kSThreads), kSThreads, 0, s>>>(pd_dev, epoch, seed_lo, seed_hi,
-                                                                                       seg);
+void launch_perm_keys(const PartDev* pd_dev, int64_t n_train, uint64_t epoch0, int n_epochs, uint32_t seed_lo,
+                      uint32_t seed_hi, const SortSeg* segs, cudaStream_t s) {
+    const int64_t total = n_train * n_epochs;
+    k_perm_keys<<<blocks_for(total < 1 ? 1 : total, kSThreads), kSThreads, 0, s>>>(pd_dev, epoch0, n_epochs, seed_lo,
+                                                                                   seed_hi, segs);
     count_launches(1, __func__);
 }
 
