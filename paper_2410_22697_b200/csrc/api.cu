@@ -35,6 +35,7 @@ namespace {
 struct Part {
     int32_t part_id = -1;
     int64_t lo = 0, n_local = 0, n_h = 0, h_below = 0, nnz = 0, n_train = 0, cap = 0, nbatch = 1;
+    int32_t max_deg_in = 0;
     int32_t perm_slots = 0;
     int64_t* indptr = nullptr;
     int32_t* cols_rank = nullptr;
@@ -103,6 +104,8 @@ struct mgnn_ctx_s {
     mgnn_policy pol{};
     // eviction scratch
     SortSeg* d_evsegs = nullptr;
+    SortSeg* d_initsegs = nullptr;
+    int32_t ev_passes = 8;
     long long* d_sel_n = nullptr;
     char* ev_zero = nullptr;
     size_t ev_zero_bytes = 0;
@@ -379,6 +382,7 @@ void mgnn_destroy(mgnn_ctx ctx) {
     dfree(ctx->d_err);
     dfree(ctx->d_gathered);
     dfree(ctx->d_evsegs);
+    dfree(ctx->d_initsegs);
     dfree(ctx->d_sel_n);
     dfree(ctx->ev_zero);
     if (ctx->sort_scr) cudaFree(ctx->sort_scr);
@@ -460,6 +464,11 @@ mgnn_status mgnn_partition_load(mgnn_ctx ctx, const mgnn_partition_desc* d, int3
     CK(cudaMemset(p.deg_in, 0, std::max<int64_t>(nh, 1) * sizeof(int32_t)));
     CK(dalloc(&p.cols_rank, nnz));
     launch_deg_rank(cols_g, nnz, lo, nl, hb, gmap, p.deg_in, p.cols_rank, s);
+    {   // max in-partition degree: sets the number of degree digits the replacement sort needs
+        std::vector<int32_t> deg(nh);
+        if (nh) CK(cudaMemcpy(deg.data(), p.deg_in, nh * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        for (int32_t x : deg) p.max_deg_in = std::max(p.max_deg_in, x);
+    }
     CK(dalloc(&p.train, d->n_train));
     if (d->n_train) CK(cudaMemcpy(p.train, d->train_ids, d->n_train * sizeof(int32_t), cudaMemcpyHostToDevice));
     CK(dalloc(&p.table, std::max<int64_t>(nl, 1) * ctx->pitch));
@@ -570,18 +579,31 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
     if (st) return st;
     const int n_lp = (int)ctx->parts.size();
     // eviction / init sort segments: 2*lp = E (slots), 2*lp+1 = R (halo)
-    std::vector<SortSeg> segs(2 * n_lp);
+    std::vector<SortSeg> segs(2 * n_lp), initsegs(n_lp);
+    ctx->ev_passes = 2;
     dfree(ctx->d_sel_n);
     CK(dalloc(&ctx->d_sel_n, 2 * n_lp));
     CK(cudaMemset(ctx->d_sel_n, 0, 2 * n_lp * sizeof(long long)));
     for (int lp = 0; lp < n_lp; ++lp) {
         Part& p = ctx->parts[lp];
-        segs[2 * lp] = SortSeg{p.ek, p.ev, p.ekt, p.evt, ctx->d_sel_n + 2 * lp};
-        segs[2 * lp + 1] = SortSeg{p.rk, p.rv, p.rkt, p.rvt, ctx->d_sel_n + 2 * lp + 1};
+        // E: key = S_E bits << 32, items in id order -> digits of the high word only
+        segs[2 * lp] = make_seg(p.ek, p.ev, p.ekt, p.evt, ctx->d_sel_n + 2 * lp, {32, 40, 48, 56});
+        // R: key = ~S_A bits << 32 | ~deg_in: the low word needs only the bytes max(deg_in) occupies
+        // (bytes above max(deg_in) are the constant 0xFF of ~deg_in; an even digit count is kept so the
+        // result lands in the primary buffers)
+        segs[2 * lp + 1] = p.max_deg_in < (1 << 16)
+                               ? make_seg(p.rk, p.rv, p.rkt, p.rvt, ctx->d_sel_n + 2 * lp + 1, {0, 8, 32, 40, 48, 56})
+                               : make_seg(p.rk, p.rv, p.rkt, p.rvt, ctx->d_sel_n + 2 * lp + 1,
+                                          {0, 8, 16, 24, 32, 40, 48, 56});
+        ctx->ev_passes = std::max(ctx->ev_passes, std::max(segs[2 * lp].npass, segs[2 * lp + 1].npass));
+        initsegs[lp] = make_seg(p.rk, p.rv, p.rkt, p.rvt, ctx->d_sel_n + 2 * lp + 1, {0, 8, 16, 24});
     }
     dfree(ctx->d_evsegs);
     CK(dalloc(&ctx->d_evsegs, segs.size()));
     CK(cudaMemcpy(ctx->d_evsegs, segs.data(), segs.size() * sizeof(SortSeg), cudaMemcpyHostToDevice));
+    dfree(ctx->d_initsegs);
+    CK(dalloc(&ctx->d_initsegs, initsegs.size()));
+    CK(cudaMemcpy(ctx->d_initsegs, initsegs.data(), initsegs.size() * sizeof(SortSeg), cudaMemcpyHostToDevice));
     const int64_t n_sort_max = std::max<int64_t>(std::max(cap_max, nh_max), 1);
     ctx->ev_tiles = (n_sort_max + 2047) / 2048;
     dfree(ctx->ev_zero);
@@ -591,16 +613,16 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
     ctx->ev_sc.status = (unsigned long long*)(ctx->ev_zero + ((2 * n_lp * 4 + 63) / 64) * 64);
     ctx->ev_zero_bytes = ((2 * n_lp * 4 + 63) / 64) * 64 + (size_t)(2 * n_lp) * ctx->ev_tiles * 8;
     {
-        mgnn_status st2 = ensure_sort_scratch(ctx, std::max(radix_scratch_bytes(2 * n_lp, n_sort_max, 64),
-                                                             radix_scratch_bytes(1, std::max<int64_t>(nh_max, 1), 32)));
+        mgnn_status st2 = ensure_sort_scratch(ctx, std::max(radix_scratch_bytes(2 * n_lp, n_sort_max, 8),
+                                                             radix_scratch_bytes(1, std::max<int64_t>(nh_max, 1), 4)));
         if (st2) return st2;
     }
     WorldDev G = world_of(ctx);
     for (int lp = 0; lp < n_lp; ++lp) {
         Part& p = ctx->parts[lp];
         // order V_p^h by (deg_in desc, id asc) (R#10) and take the first cap
-        launch_init_keys(ctx->d_parts + lp, p.n_h, ctx->d_evsegs + 2 * lp + 1, ctx->d_sel_n + 2 * lp + 1, s);
-        radix_sort_pairs(ctx->d_evsegs + 2 * lp + 1, 1, std::max<int64_t>(p.n_h, 1), 32, ctx->sort_scr, s);
+        launch_init_keys(ctx->d_parts + lp, p.n_h, ctx->d_initsegs + lp, ctx->d_sel_n + 2 * lp + 1, s);
+        radix_sort_pairs(ctx->d_initsegs + lp, 1, std::max<int64_t>(p.n_h, 1), 4, ctx->sort_scr, s);
         launch_init_fill(ctx->d_parts + lp, p.n_h, p.cap, p.rv, s);
         launch_rows_from_owners(ctx->d_parts + lp, p.cap, G, s);
         CKL();
@@ -702,7 +724,7 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
         const int64_t nt = std::max<int64_t>(p.n_train, 1);
         CK(dalloc(&p.perm, (int64_t)p.perm_slots * nt));
         CK(dalloc(&p.pk, p.perm_chunk * nt)); CK(dalloc(&p.pkt, p.perm_chunk * nt)); CK(dalloc(&p.pvt, p.perm_chunk * nt));
-        scr = std::max(scr, radix_scratch_bytes(p.perm_chunk, nt, 64));
+        scr = std::max(scr, radix_scratch_bytes(p.perm_chunk, nt, 8));
     }
     {
         mgnn_status st2 = ensure_sort_scratch(ctx, scr);
@@ -718,8 +740,8 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
         for (int k = 0; k < p.perm_slots; ++k) {   // slot k = half k / G, epoch-in-chunk j = k % G
             const int64_t j = k % p.perm_chunk;
             ps[(size_t)lp * ctx->perm_slots_max + k] =
-                SortSeg{p.pk + j * p.n_train, (uint32_t*)(p.perm + (int64_t)k * p.n_train), p.pkt + j * p.n_train,
-                        p.pvt + j * p.n_train, ctx->d_perm_n + lp};
+                make_seg(p.pk + j * p.n_train, (uint32_t*)(p.perm + (int64_t)k * p.n_train), p.pkt + j * p.n_train,
+                         p.pvt + j * p.n_train, ctx->d_perm_n + lp, {0, 8, 16, 24, 32, 40, 48, 56});
         }
     }
     CK(cudaMemcpy(ctx->d_perm_n, pn.data(), n_lp * sizeof(long long), cudaMemcpyHostToDevice));
@@ -769,7 +791,7 @@ mgnn_status mgnn_sample(mgnn_ctx ctx, int32_t slot, uint64_t t0, int32_t n_steps
                 const SortSeg* segs = ctx->d_permsegs + (size_t)lp * ctx->perm_slots_max + (c % 2) * G;
                 launch_perm_keys(ctx->d_parts + lp, p.n_train, (uint64_t)(c * G), (int)G, (uint32_t)ctx->run_seed,
                                  (uint32_t)(ctx->run_seed >> 32), segs, s);
-                radix_sort_pairs(segs, (int)G, p.n_train, 64, ctx->sort_scr, s);
+                radix_sort_pairs(segs, (int)G, p.n_train, 8, ctx->sort_scr, s);
                 p.chunk_loaded[c % 2] = c;
             }
         }
@@ -791,8 +813,7 @@ mgnn_status mgnn_sample(mgnn_ctx ctx, int32_t slot, uint64_t t0, int32_t n_steps
     for (int i = 0; i < ctx->L; ++i) {
         // per-hop scratch strides follow the max window; scans index by instance < M
         Scratch scc = w.sc_count[i], scp = w.sc_compact[i];
-        launch_count_scan(wd, i, ctx->fcap[i], scc, s);
-        launch_sample(wd, i, ctx->fcap[i], s);
+        launch_hop(wd, i, ctx->fcap[i], scc, s);
         launch_compact(wd, i, scp, s);
     }
     launch_relabel(wd, s);
@@ -851,7 +872,7 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
         CK(cudaMemsetAsync(ctx->ev_zero, 0, ctx->ev_zero_bytes, s));
         launch_select(ctx->d_parts, n_lp, nmax, ctx->pol.alpha, ctx->pol.theta_r, ctx->d_evsegs, ctx->d_sel_n,
                       ctx->ev_sc, s);
-        radix_sort_pairs(ctx->d_evsegs, 2 * n_lp, nmax, 64, ctx->sort_scr, s);
+        radix_sort_pairs(ctx->d_evsegs, 2 * n_lp, nmax, ctx->ev_passes, ctx->sort_scr, s);
         launch_swap_refill(ctx->d_parts, n_lp, cap_max, ctx->d_evsegs, world_of(ctx), w.counts, 8, w.n_steps, s);
     }
     CKL();

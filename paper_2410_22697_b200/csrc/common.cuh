@@ -8,6 +8,9 @@
 #ifndef MGNN_MAX_LAYERS
 #define MGNN_MAX_LAYERS 8
 #endif
+#ifndef MGNN_MAX_FANOUT
+#define MGNN_MAX_FANOUT 32
+#endif
 
 // Device bounds checks, compiled in with -DMGNN_CHECKS (debug builds only).
 #ifdef MGNN_CHECKS

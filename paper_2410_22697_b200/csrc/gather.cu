@@ -1,29 +1,33 @@
 // gather.cu -- classify + feature gather (Alg.2 l.2-5, l.10-11, l.21-22).
 //
-// One warp per node of F_L, every instance of the window at once:
+// Every instance of the window at once (gridDim.y = instances).  A warp takes
+// 32 consecutive nodes of F_L: lane i classifies node f0+i in parallel
 //   local  (u in V_p^l)           -> row of the partition's own table   (l.10)
 //   hit    (u in V_p^h, in BUF)   -> BUF row of its slot                 (l.11)
 //   miss   (u in V_p^h, not BUF)  -> row of the OWNER's table, read over
 //                                    NVLink peer memory when the owner is
 //                                    another GPU (the RPC of l.22, fused into
 //                                    the gather: no request/response exchange)
-// The class is a range test on the node's local rank plus one slot_of load
-// (the compact O(|V_p^h|) S_A of P:228, indexed directly instead of by binary
-// search).  Hits set bit w of the slot's hit mask (decay bookkeeping, l.6-9);
-// misses add 1 to S_A (l.21).  Every add is +1.0f, so the result does not
-// depend on the order of the atomics (bit-exact vs. sequential steps).
-// Rows move as 16-byte vectors, coalesced per warp; X stores stream past L2.
+// -- a range test on the node's local rank plus one slot_of load (the compact
+// O(|V_p^h|) S_A of P:228, indexed directly instead of by binary search) --
+// then the warp copies the 32 rows with several 16-byte loads in flight per
+// lane (source pointers broadcast by shuffles), so no row waits on the
+// classification of the next.  Hits set bit w of the slot's hit mask (decay
+// bookkeeping, l.6-9); misses add 1.0f to S_A (l.21): every operand is 1.0f,
+// so the result does not depend on the order of the atomics.  X stores are
+// streaming (evict-first) so the window's output does not flush the tables
+// out of L2.
 #include "launch.h"
 
 namespace mgnn {
 
 constexpr int kGThreads = 256;
+constexpr int kGWarps = kGThreads / 32;
 
-__device__ __forceinline__ float4 ld_row(const float* p) {
-    return __ldg(reinterpret_cast<const float4*>(p));
-}
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void stcs4(float* p, float4 v) { __stcs(reinterpret_cast<float4*>(p), v); }
 
-__global__ void __launch_bounds__(kGThreads) k_gather(WinDev W, WorldDev G) {
+__global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
     __shared__ unsigned long long cnt_sh[3];
     const int m = blockIdx.y;
     const int lp = m / W.n_steps, w = m % W.n_steps;
@@ -33,44 +37,91 @@ __global__ void __launch_bounds__(kGThreads) k_gather(WinDev W, WorldDev G) {
     const int64_t U = W.hop_size[(int64_t)m * (kMaxLayers + 1) + W.L];
     const int lane = threadIdx.x & 31;
     const int pitch = W.pitch;
-    const int64_t nwarps = (int64_t)gridDim.x * (kGThreads / 32);
+    const int q = pitch >> 2;                      // float4 per row
     const int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
     int32_t* fgid = W.fr_gid + (int64_t)m * W.ucap;
     float* X = W.X + (int64_t)m * W.ucap * pitch;
     const int64_t h_below = pd.h_below, n_local = pd.n_local, lo = pd.lo;
     const unsigned long long wbit = 1ull << w;
     unsigned n_loc = 0, n_hit = 0, n_miss = 0;
-    for (int64_t f = (int64_t)blockIdx.x * (kGThreads / 32) + (threadIdx.x >> 5); f < U; f += nwarps) {
-        const int64_t r = fr[f];
-        const float* src;
-        int32_t gid;
-        if (r >= h_below && r < h_below + n_local) {
-            gid = (int32_t)(lo + (r - h_below));
-            src = pd.table + (r - h_below) * pitch;
-            ++n_loc;
-        } else {
-            const int64_t h = r < h_below ? r : r - n_local;
-            gid = pd.halo_ids[h];
-            const int32_t s = pd.slot_of[h];
-            if (s >= 0) {
-                src = pd.rows + (int64_t)s * pitch;
-                if (lane == 0) atomicOr(&pd.hitmask[s], wbit);
-                ++n_hit;
+    const int64_t stride = (int64_t)gridDim.x * kGWarps * 32;
+    for (int64_t f0 = ((int64_t)blockIdx.x * kGWarps + (threadIdx.x >> 5)) * 32; f0 < U; f0 += stride) {
+        // ---- classify 32 nodes, one per lane
+        const int64_t f = f0 + lane;
+        const bool valid = f < U;
+        const float* src = nullptr;
+        int cls = 3;
+        if (valid) {
+            const int64_t r = fr[f];
+            int32_t gid;
+            if (r >= h_below && r < h_below + n_local) {
+                gid = (int32_t)(lo + (r - h_below));
+                src = pd.table + (r - h_below) * pitch;
+                cls = 0;
             } else {
-                const int q = owner_of(G.bounds, G.n_parts, gid);
-                src = G.tables[q] + ((int64_t)gid - G.bounds[q]) * pitch;
-                if (lane == 0) atomicAdd(&pd.sa[h], 1.0f);
-                ++n_miss;
+                const int64_t h = r < h_below ? r : r - n_local;
+                gid = pd.halo_ids[h];
+                const int32_t s = pd.slot_of[h];
+                if (s >= 0) {
+                    src = pd.rows + (int64_t)s * pitch;
+                    atomicOr(&pd.hitmask[s], wbit);
+                    cls = 1;
+                } else {
+                    const int qo = owner_of(G.bounds, G.n_parts, gid);
+                    src = G.tables[qo] + ((int64_t)gid - G.bounds[qo]) * pitch;
+                    atomicAdd(&pd.sa[h], 1.0f);
+                    cls = 2;
+                }
+            }
+            fgid[f] = gid;
+        }
+        n_loc += __popc(__ballot_sync(kFull, cls == 0));
+        n_hit += __popc(__ballot_sync(kFull, cls == 1));
+        n_miss += __popc(__ballot_sync(kFull, cls == 2));
+        const int nrows = (int)(U - f0 < 32 ? U - f0 : 32);
+        float* Xw = X + f0 * pitch;
+        // ---- copy the rows, several independent 16-B loads in flight per lane
+        if (q >= 32) {
+            for (int j = 0; j < nrows; j += 4) {
+                const float* s0 = (const float*)__shfl_sync(kFull, (unsigned long long)src, j);
+                const float* s1 = (const float*)__shfl_sync(kFull, (unsigned long long)src, (j + 1) & 31);
+                const float* s2 = (const float*)__shfl_sync(kFull, (unsigned long long)src, (j + 2) & 31);
+                const float* s3 = (const float*)__shfl_sync(kFull, (unsigned long long)src, (j + 3) & 31);
+                for (int c = lane * 4; c < pitch; c += 128) {
+                    float4 v0 = ldg4(s0 + c), v1, v2, v3;
+                    if (j + 1 < nrows) v1 = ldg4(s1 + c);
+                    if (j + 2 < nrows) v2 = ldg4(s2 + c);
+                    if (j + 3 < nrows) v3 = ldg4(s3 + c);
+                    stcs4(Xw + (int64_t)j * pitch + c, v0);
+                    if (j + 1 < nrows) stcs4(Xw + (int64_t)(j + 1) * pitch + c, v1);
+                    if (j + 2 < nrows) stcs4(Xw + (int64_t)(j + 2) * pitch + c, v2);
+                    if (j + 3 < nrows) stcs4(Xw + (int64_t)(j + 3) * pitch + c, v3);
+                }
+            }
+        } else {
+            // q < 32 float4 per row: 32/q rows side by side per warp instruction
+            const int per = 32 / q;
+            const int sub = lane / q, ch = lane - sub * q;
+            const bool act = sub < per;
+            for (int j = 0; j < nrows; j += 4 * per) {
+                float4 v[4];
+                int row[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    row[u] = j + u * per + sub;
+                    const float* s = (const float*)__shfl_sync(kFull, (unsigned long long)src, row[u] & 31);
+                    if (act && row[u] < nrows) v[u] = ldg4(s + ch * 4);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (act && row[u] < nrows) stcs4(Xw + (int64_t)row[u] * pitch + ch * 4, v[u]);
             }
         }
-        if (lane == 0) fgid[f] = gid;
-        float* dst = X + f * pitch;
-        for (int c = lane * 4; c < pitch; c += 128) __stcs(reinterpret_cast<float4*>(dst + c), ld_row(src + c));
     }
     if (lane == 0) {
-        if (n_loc) atomicAdd(&cnt_sh[0], n_loc);
-        if (n_hit) atomicAdd(&cnt_sh[1], n_hit);
-        if (n_miss) atomicAdd(&cnt_sh[2], n_miss);
+        if (n_loc) atomicAdd(&cnt_sh[0], (unsigned long long)n_loc);
+        if (n_hit) atomicAdd(&cnt_sh[1], (unsigned long long)n_hit);
+        if (n_miss) atomicAdd(&cnt_sh[2], (unsigned long long)n_miss);
     }
     __syncthreads();
     long long* cn = W.counts + (int64_t)m * 8;
@@ -88,8 +139,9 @@ __global__ void __launch_bounds__(kGThreads) k_gather(WinDev W, WorldDev G) {
 }
 
 void launch_gather(const WinDev& w, const WorldDev& world, cudaStream_t s) {
-    int64_t target = (148 * 8 + w.n_inst - 1) / w.n_inst;   // ~8 resident 256-thread blocks per SM in total
-    int64_t need = (w.ucap + 7) / 8;
+    // one wave of 4 resident 256-thread blocks per SM in total (64 registers per thread)
+    int64_t target = (148 * 4 + w.n_inst - 1) / w.n_inst;
+    int64_t need = (w.ucap + kGWarps * 32 - 1) / (kGWarps * 32);
     unsigned gx = (unsigned)(need < target ? need : target);
     if (gx < 1) gx = 1;
     dim3 grid(gx, w.n_inst);

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <initializer_list>
+
 #include "common.cuh"
 
 namespace mgnn {
@@ -50,7 +52,19 @@ struct SortSeg {
     unsigned long long* keys_tmp;
     uint32_t* vals_tmp;
     const long long* n;          // device element count
+    int32_t npass;               // even number of 8-bit digit passes for this segment
+    uint8_t shift[8];            // bit offset of each pass's digit, least significant first
 };
+
+// Digit schedule: the key bytes that can differ, least significant first.  The caller
+// guarantees every other byte is constant and passes an EVEN number of shifts (so the
+// sorted data ends in the primary buffers).
+inline SortSeg make_seg(unsigned long long* k, uint32_t* v, unsigned long long* kt, uint32_t* vt, const long long* n,
+                        std::initializer_list<int> shifts) {
+    SortSeg s{k, v, kt, vt, n, 0, {0, 0, 0, 0, 0, 0, 0, 0}};
+    for (int sh : shifts) s.shift[s.npass++] = (uint8_t)sh;
+    return s;
+}
 
 struct Scratch {          // zeroed look-back status words + tile counters
     unsigned long long* status;
@@ -59,8 +73,7 @@ struct Scratch {          // zeroed look-back status words + tile counters
 
 // sample.cu
 void launch_seeds(const WinDev& w, cudaStream_t s);
-void launch_count_scan(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s);
-void launch_sample(const WinDev& w, int hop, int64_t fcap, cudaStream_t s);
+void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s);
 void launch_compact(const WinDev& w, int hop, Scratch sc, cudaStream_t s);
 void launch_relabel(const WinDev& w, cudaStream_t s);
 int64_t scan_tiles_count(int64_t fcap);   // tiles used by count_scan for fcap items
@@ -82,10 +95,10 @@ void launch_rows_from_owners(const PartDev* pd_dev, int64_t cap, const WorldDev&
 void launch_perm_keys(const PartDev* pd_dev, int64_t n_train, uint64_t epoch0, int n_epochs, uint32_t seed_lo,
                       uint32_t seed_hi, const SortSeg* segs, cudaStream_t s);
 
-// sort.cu: stable LSD radix sort of (u64 key, u32 value) pairs over `bits` low key bits
-// (bits multiple of 16), each segment independently; n_max bounds every segment.
-void radix_sort_pairs(const SortSeg* segs_dev, int n_seg, int64_t n_max, int bits, void* scratch, cudaStream_t s);
-size_t radix_scratch_bytes(int n_seg, int64_t n_max, int bits);
+// sort.cu: stable LSD radix sort of (u64 key, u32 value) pairs, each segment with its own digit
+// schedule (SortSeg::shift, at most max_passes); n_max bounds every segment's length.
+void radix_sort_pairs(const SortSeg* segs_dev, int n_seg, int64_t n_max, int max_passes, void* scratch, cudaStream_t s);
+size_t radix_scratch_bytes(int n_seg, int64_t n_max, int max_passes);
 
 // load.cu
 void launch_mark_halo(const int32_t* cols, int64_t nnz, int64_t lo, int64_t hi, uint32_t* bm, cudaStream_t s);

@@ -5,17 +5,19 @@
 // run every instance of the window side by side (gridDim.y = instances), so
 // one launch per stage serves W steps x P_local partitions.
 //
-// Per hop i (DESIGN.md "Kernels", K1/K2):
-//   k_count_scan : deg-capped counts min(deg, k_i) of F_i, exclusive offsets
-//                  by a single-pass decoupled look-back scan;
-//   k_sample     : warp per frontier node, lane j draws u_j = Philox(node,
-//                  (i<<16)|j, step, (p<<8)|1) (R#4), r_j = mulhi(u_j, t_j+1)
-//                  (R#5), Floyd resolution by k shuffles (R#6); writes the
-//                  neighbour's local rank and marks it in the new-node bitmap
-//                  unless it is already in F_i;
-//   k_compact    : the bitmap in rank order IS the ascending-id order, so a
-//                  popcount scan appends sorted_unique(cols_i) \ F_i to the
-//                  frontier (R#7) and records every node's frontier position.
+// Per hop i (DESIGN.md §7, K1/K2):
+//   k_hop     : thread per frontier node x of F_i (a tile of 256 per block):
+//               count min(deg, k_i) (halo nodes: 0, R#1), exclusive offsets by
+//               a block scan + decoupled look-back across tiles; then groups
+//               of G = pow2 >= k_i lanes take the warp's nodes 32/G at a time:
+//               lane j draws u_j = Philox(x, (i<<16)|j, step, (p<<8)|1) (R#4),
+//               r_j = mulhi(u_j, t_j+1) (R#5), Floyd resolution by k_i
+//               in-group shuffles (R#6).  Every neighbour's local rank is
+//               written in slot order and marked in the new-node bitmap
+//               unless already in F_i.
+//   k_compact : the bitmap in rank order IS the ascending-id order, so a
+//               popcount scan appends sorted_unique(cols_i) \ F_i to the
+//               frontier (R#7) and records every node's frontier position.
 // After the last hop k_relabel rewrites the sampled columns as positions in
 // F_{i+1} (the DGL block layout the consumer indexes X with).
 #include "launch.h"
@@ -23,12 +25,10 @@
 namespace mgnn {
 
 constexpr int kThreads = 256;
-constexpr int kScanItems = 8;                         // count scan: items per thread
-constexpr int kScanTile = kThreads * kScanItems;      // 2048 frontier nodes per tile
-constexpr int kWordItems = 4;                         // compact: bitmap words per thread
-constexpr int kWordTile = kThreads * kWordItems;      // 1024 words = 32768 ranks per tile
+constexpr int kHopTile = kThreads;     // frontier nodes per k_hop tile
+constexpr int kWordTile = kThreads;    // bitmap words per k_compact tile (one per thread)
 
-int64_t scan_tiles_count(int64_t fcap) { return (fcap + kScanTile - 1) / kScanTile; }
+int64_t scan_tiles_count(int64_t fcap) { return (fcap + kHopTile - 1) / kHopTile; }
 int64_t scan_tiles_words(int64_t words) { return (words + kWordTile - 1) / kWordTile; }
 
 static inline unsigned grid_x_for(int64_t items_per_inst, int items_per_block, int n_inst) {
@@ -81,106 +81,85 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
     if (blockIdx.x == 0 && threadIdx.x == 0) W.hop_size[(int64_t)m * (kMaxLayers + 1)] = n0;
 }
 
-// ------------------------------------------------------------------ counts + offsets (single-pass scan)
-__global__ void __launch_bounds__(kThreads) k_count_scan(WinDev W, int hop, Scratch sc, int64_t tiles_max) {
+// ------------------------------------------------------------------ one hop: counts, offsets, samples
+__global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max) {
     __shared__ long long sm[8];
     __shared__ int tslot;
     __shared__ long long prefix_sh;
     const int m = blockIdx.y;
-    const PartDev& pd = W.parts[m / W.n_steps];
+    const int lp = m / W.n_steps, w = m % W.n_steps;
+    const PartDev& pd = W.parts[lp];
     const int64_t nF = W.hop_size[(int64_t)m * (kMaxLayers + 1) + hop];
-    const int64_t ntiles = (nF + kScanTile - 1) / kScanTile;
+    const int64_t ntiles = (nF + kHopTile - 1) / kHopTile;
     const int tile = claim_tile(sc.tilectr + m, &tslot);
+    int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
     if (tile >= ntiles) {
-        if (tile == 0 && threadIdx.x == 0) W.off[hop][(int64_t)m * W.off_stride[hop]] = 0;   // empty F_i
+        if (tile == 0 && threadIdx.x == 0) off[0] = 0;   // empty F_i
         return;
     }
     const int k = W.k_hop[hop];
-    const int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
-    int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
-    const int64_t f0 = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
-    int cnt[kScanItems];
-    long long sum = 0;
-#pragma unroll
-    for (int i = 0; i < kScanItems; ++i) {
-        const int64_t f = f0 + i;
-        int c = 0;
-        if (f < nF) {
-            const int64_t row = (int64_t)fr[f] - pd.h_below;
-            if (row >= 0 && row < pd.n_local) {       // halo frontier nodes are leaves (R#1)
-                const int64_t d = pd.indptr[row + 1] - pd.indptr[row];
-                c = (int)(d < k ? d : k);             // |sample| = min(deg, k) (R#3)
-            }
+    const int64_t f = (int64_t)tile * kHopTile + threadIdx.x;
+    const int64_t h_below = pd.h_below, n_local = pd.n_local;
+    int64_t row = -1, b0 = 0, d = 0;
+    if (f < nF) {
+        row = (int64_t)W.fr_rank[(int64_t)m * W.ucap + f] - h_below;
+        if (row >= 0 && row < n_local) {               // halo frontier nodes are leaves (R#1)
+            b0 = pd.indptr[row];
+            d = pd.indptr[row + 1] - b0;
+        } else {
+            row = -1;
         }
-        cnt[i] = c;
-        sum += c;
     }
+    const int cnt = (int)(d < k ? d : k);              // |sample| = min(deg, k) (R#3)
     long long agg;
-    long long excl = block_excl_scan256(sum, sm, &agg);
-    if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
-                                                                     (unsigned long long)agg);
+    const long long excl = block_excl_scan256(cnt, sm, &agg);
+    if (threadIdx.x == 0)
+        prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile, (unsigned long long)agg);
     __syncthreads();
-    long long run = prefix_sh + excl;
+    const int64_t o = prefix_sh + excl;
     if (tile == 0 && threadIdx.x == 0) off[0] = 0;
-#pragma unroll
-    for (int i = 0; i < kScanItems; ++i) {
-        const int64_t f = f0 + i;
-        run += cnt[i];
-        if (f < nF) {
-            MGNN_CHECK(f + 1 < W.off_stride[hop], "off f=%lld", (long long)f);
-            off[f + 1] = run;
-        }
+    if (f < nF) {
+        MGNN_CHECK(f + 1 < W.off_stride[hop], "off f=%lld", (long long)f);
+        off[f + 1] = o + cnt;
     }
-}
-
-// ------------------------------------------------------------------ sampling (warp per frontier node)
-__global__ void __launch_bounds__(kThreads) k_sample(WinDev W, int hop) {
-    const int m = blockIdx.y;
-    const int lp = m / W.n_steps, w = m % W.n_steps;
-    const PartDev& pd = W.parts[lp];
-    const uint32_t step = (uint32_t)(W.step0 + (uint64_t)w);
-    const int64_t nF = W.hop_size[(int64_t)m * (kMaxLayers + 1) + hop];
-    const int k = W.k_hop[hop];
-    const int lane = threadIdx.x & 31;
-    const int64_t nwarps = (int64_t)gridDim.x * (kThreads / 32);
-    const int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
-    const int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
+    // ---- sampling: G lanes per node (G = power of two >= k), 32/G nodes of the warp side by side;
+    // lane j of a group draws slot j, Floyd collisions resolved by k shuffles inside the group.
     int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop];
     const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
     uint32_t* nb = W.nb + (int64_t)m * W.bm_words;
+    const int lane = threadIdx.x & 31;
+    const int G = k <= 8 ? 8 : (k <= 16 ? 16 : 32);
+    const int per = 32 / G;
+    const int gi = lane / G, gl = lane & (G - 1), gbase = lane & ~(G - 1);
     const uint32_t c1 = (uint32_t)hop << 16;
     const uint32_t c3 = ((uint32_t)pd.part_id << 8) | kStreamSample;
-    const int64_t h_below = pd.h_below, n_local = pd.n_local, lo = pd.lo;
-    const int64_t* __restrict__ indptr = pd.indptr;
-    const int32_t* __restrict__ crank = pd.cols_rank;
-    for (int64_t f = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); f < nF; f += nwarps) {
-        const int64_t row = (int64_t)fr[f] - h_below;
-        if (row < 0 || row >= n_local) continue;
-        const int64_t b0 = indptr[row];
-        const int64_t d = indptr[row + 1] - b0;
-        const int64_t o = off[f];
-        int32_t c = -1;
-        int j = lane;
-        if (d <= k) {                                    // whole neighbourhood in CSR order (R#3)
-            if (lane < d) c = crank[b0 + lane];
-        } else {
-            uint32_t r = 0, t = 0;
-            if (lane < k) {
-                const u4 u = philox4x32_10(u4{(uint32_t)(lo + row), c1 | (uint32_t)lane, step, c3}, W.seed_lo,
-                                           W.seed_hi);
-                t = (uint32_t)(d - k + lane);
-                r = __umulhi(u.x, t + 1u);               // floor(u (t+1) / 2^32)
-            }
-            bool coll = false;                           // Floyd: pos_j = r_j unless already chosen, else t_j
-            for (int jj = 0; jj < k; ++jj) {
-                const uint32_t pj = __shfl_sync(kFull, coll ? t : r, jj);
-                if (lane > jj && r == pj) coll = true;
-            }
-            if (lane < k) c = crank[b0 + (coll ? t : r)];
+    const uint32_t step = (uint32_t)(W.step0 + (uint64_t)w);
+    const int64_t lo = pd.lo;
+    for (int base = 0; base < 32; base += per) {
+        const int srcl = base + gi;                    // the node of this group = thread srcl's node
+        const long long n_row = __shfl_sync(kFull, (long long)row, srcl);
+        const long long n_b0 = __shfl_sync(kFull, (long long)b0, srcl);
+        const long long n_d = __shfl_sync(kFull, (long long)d, srcl);
+        const long long n_o = __shfl_sync(kFull, (long long)o, srcl);
+        const bool active = n_row >= 0 && n_d > 0;
+        const bool whole = n_d <= k;                   // whole neighbourhood in CSR order (R#3)
+        uint32_t r = 0, t = 0;
+        if (active && !whole && gl < k) {
+            const u4 u = philox4x32_10(u4{(uint32_t)(lo + n_row), c1 | (uint32_t)gl, step, c3}, W.seed_lo,
+                                       W.seed_hi);
+            t = (uint32_t)(n_d - k + gl);
+            r = __umulhi(u.x, t + 1u);                 // floor(u (t+1) / 2^32)
         }
-        if (c >= 0) {
-            MGNN_CHECK(o + j < W.col_stride[hop] && c < pd.vp, "cols o=%lld j=%d c=%d", (long long)o, j, c);
-            cols[o + j] = c;
+        bool coll = false;                             // Floyd: pos_j = r_j unless already chosen, else t_j
+        for (int jj = 0; jj < k; ++jj) {
+            const uint32_t pj = __shfl_sync(kFull, coll ? t : r, gbase + jj);
+            if (gl > jj && r == pj) coll = true;
+        }
+        if (active && gl < (whole ? (int)n_d : k)) {
+            const uint32_t pos = whole ? (uint32_t)gl : (coll ? t : r);
+            const int32_t c = pd.cols_rank[n_b0 + pos];
+            MGNN_CHECK(n_o + gl < W.col_stride[hop] && c < pd.vp, "cols o=%lld j=%d c=%d", n_o, gl, c);
+            cols[n_o + gl] = c;
             const uint32_t bit = 1u << (c & 31);
             if (!(fb[c >> 5] & bit)) atomicOr(&nb[c >> 5], bit);
         }
@@ -200,40 +179,30 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
     if (tile >= ntiles) return;
     uint32_t* nb = W.nb + (int64_t)m * W.bm_words;
     uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
-    const int64_t w0 = (int64_t)tile * kWordTile + (int64_t)threadIdx.x * kWordItems;
-    uint32_t bits[kWordItems];
-    long long cnt = 0;
-#pragma unroll
-    for (int i = 0; i < kWordItems; ++i) {
-        bits[i] = (w0 + i < nwords) ? nb[w0 + i] : 0u;
-        cnt += __popc(bits[i]);
-    }
+    const int64_t wd = (int64_t)tile * kWordTile + threadIdx.x;
+    uint32_t b = (wd < nwords) ? nb[wd] : 0u;
     long long agg;
-    long long excl = block_excl_scan256(cnt, sm, &agg);
+    const long long excl = block_excl_scan256(__popc(b), sm, &agg);
     int64_t* hs = W.hop_size + (int64_t)m * (kMaxLayers + 1);
     if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
                                                                      (unsigned long long)agg);
     __syncthreads();
     const int64_t nF = hs[hop];
     int64_t pos = nF + prefix_sh + excl;
+    if (b) {
+        fb[wd] |= b;
+        nb[wd] = 0u;
+    }
     int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
     int32_t* posof = W.pos_of + (int64_t)m * W.vp_stride;
-#pragma unroll
-    for (int i = 0; i < kWordItems; ++i) {
-        uint32_t b = bits[i];
-        if (b) {
-            fb[w0 + i] |= b;
-            nb[w0 + i] = 0u;
-        }
-        while (b) {
-            const int bi = __ffs(b) - 1;
-            b &= b - 1;
-            const int32_t r = (int32_t)((w0 + i) * 32 + bi);
-            MGNN_CHECK(pos < W.ucap && r < pd.vp, "compact pos=%lld r=%d", (long long)pos, r);
-            fr[pos] = r;
-            posof[r] = (int32_t)pos;
-            ++pos;
-        }
+    while (b) {
+        const int bi = __ffs(b) - 1;
+        b &= b - 1;
+        const int32_t r = (int32_t)(wd * 32 + bi);
+        MGNN_CHECK(pos < W.ucap && r < pd.vp, "compact pos=%lld r=%d", (long long)pos, r);
+        fr[pos] = r;
+        posof[r] = (int32_t)pos;
+        ++pos;
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) hs[hop + 1] = nF + prefix_sh + agg;
 }
@@ -259,16 +228,10 @@ void launch_seeds(const WinDev& w, cudaStream_t s) {
     count_launches(1, __func__);
 }
 
-void launch_count_scan(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s) {
+void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s) {
     const int64_t tiles = scan_tiles_count(fcap);
     dim3 grid((unsigned)(tiles < 1 ? 1 : tiles), w.n_inst);
-    k_count_scan<<<grid, kThreads, 0, s>>>(w, hop, sc, tiles < 1 ? 1 : tiles);
-    count_launches(1, __func__);
-}
-
-void launch_sample(const WinDev& w, int hop, int64_t fcap, cudaStream_t s) {
-    dim3 grid(grid_x_for(fcap, kThreads / 32, w.n_inst), w.n_inst);
-    k_sample<<<grid, kThreads, 0, s>>>(w, hop);
+    k_hop<<<grid, kThreads, 0, s>>>(w, hop, sc, tiles < 1 ? 1 : tiles);
     count_launches(1, __func__);
 }
 

@@ -40,7 +40,7 @@ void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, 
 
 // ------------------------------------------------------------------ candidate selection
 // Segment 2*lp   : E = {slots s : S_E[s] < alpha}                       (R#16)
-//                  key = (S_E bits << 32) | node id   -> ascending = (S_E asc, id asc)
+//                  scanned in halo (= id) order, key = S_E bits << 32 -> stable ascending = (S_E asc, id asc)
 // Segment 2*lp+1 : R = {halo h : not buffered, S_A[h] >= theta_r}     (R#17)
 //                  key = (~S_A bits << 32) | ~deg_in  -> ascending = (S_A desc, deg_in desc);
 //                  items enter in halo order (= id asc) and the sort is stable (R#18).
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict_
     const int sg = blockIdx.y;
     const PartDev& pd = parts[sg >> 1];
     const bool isE = (sg & 1) == 0;
-    const int64_t n = isE ? pd.cap : pd.n_h;
+    const int64_t n = pd.n_h;
     const int64_t tile_items = kSThreads * 8;
     const int64_t ntiles = (n + tile_items - 1) / tile_items;
     const int tile = claim_tile(sc.tilectr + sg, &tslot);
@@ -69,7 +69,10 @@ __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict_
     for (int i = 0; i < 8; ++i) {
         const int64_t x = i0 + i;
         bool pf = false;
-        if (x < n) pf = isE ? (pd.se[x] < alpha) : (pd.slot_of[x] < 0 && pd.sa[x] >= theta_r);
+        if (x < n) {
+            const int32_t s = pd.slot_of[x];
+            pf = isE ? (s >= 0 && pd.se[s] < alpha) : (s < 0 && pd.sa[x] >= theta_r);
+        }
         flags |= (unsigned)pf << i;
         cnt += pf;
     }
@@ -84,15 +87,17 @@ __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict_
         if (!((flags >> i) & 1u)) continue;
         const int64_t x = i0 + i;
         unsigned long long key;
+        uint32_t val;
         if (isE) {
-            const uint32_t node = (uint32_t)pd.halo_ids[pd.slot_h[x]];
-            key = ((unsigned long long)__float_as_uint(pd.se[x]) << 32) | node;
+            val = (uint32_t)pd.slot_of[x];
+            key = (unsigned long long)__float_as_uint(pd.se[val]) << 32;
         } else {
+            val = (uint32_t)x;
             key = ((unsigned long long)(~__float_as_uint(pd.sa[x])) << 32) | (uint32_t)(~(uint32_t)pd.deg_in[x]);
         }
-        MGNN_CHECK(pos < n, "select pos=%lld n=%lld sg=%d", (long long)pos, (long long)n, sg);
+        MGNN_CHECK(pos < (isE ? pd.cap : n), "select pos=%lld n=%lld sg=%d", (long long)pos, (long long)n, sg);
         out.keys[pos] = key;
-        out.vals[pos] = (uint32_t)x;
+        out.vals[pos] = val;
         ++pos;
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) n_out[sg] = prefix_sh + agg;

@@ -30,8 +30,8 @@ static inline int64_t sort_tiles(int64_t n_max) {
 //   bins   u32 [n_seg][passes][256]            digit histograms -> bin offsets
 //   ctr    i32 [n_seg][passes]                 dynamic tile ids
 //   status u32 [n_seg][passes][tiles][256]     look-back words: [31:30] flag, [29:0] count
-size_t radix_scratch_bytes(int n_seg, int64_t n_max, int bits) {
-    const int64_t passes = bits / 8, tiles = sort_tiles(n_max);
+size_t radix_scratch_bytes(int n_seg, int64_t n_max, int max_passes) {
+    const int64_t passes = max_passes, tiles = sort_tiles(n_max);
     size_t b = (size_t)n_seg * passes * kRadix * 4;
     b += (size_t)n_seg * passes * 4;
     b = (b + 255) / 256 * 256;
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const SortSeg* __res
             const int64_t idx = base + (int64_t)i * kSortThreads + threadIdx.x;
             if (idx < n) {
                 const unsigned long long k = sg.keys[idx];
-                for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(unsigned)(k >> (8 * p)) & 0xFF], 1u);
+                for (int p = 0; p < sg.npass; ++p) atomicAdd(&h[p][(unsigned)(k >> sg.shift[p]) & 0xFF], 1u);
             }
         }
     }
@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortSeg* __res
     __shared__ int tslot;
     const int s = blockIdx.y;
     const SortSeg sg = segs[s];
+    if (p >= sg.npass) return;                 // this segment's schedule has fewer digits
     const int64_t n = *sg.n;
     const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
     const int tile = claim_tile(scr.ctr + s * passes + p, &tslot);
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortSeg* __res
     uint32_t* vout = parity ? sg.vals : sg.vals_tmp;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const int shift = 8 * p;
+    const int shift = sg.shift[p];
     const int64_t base = (int64_t)tile * kSortTile;
     run[threadIdx.x] = 0;
     for (int w = 0; w < 8; ++w) wc[w][threadIdx.x] = 0;
@@ -188,11 +189,12 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortSeg* __res
     }
 }
 
-void radix_sort_pairs(const SortSeg* segs_dev, int n_seg, int64_t n_max, int bits, void* scratch, cudaStream_t s) {
+void radix_sort_pairs(const SortSeg* segs_dev, int n_seg, int64_t n_max, int max_passes, void* scratch,
+                      cudaStream_t s) {
     if (n_seg < 1) return;
-    const int passes = bits / 8;
+    const int passes = max_passes;
     const int64_t tiles = sort_tiles(n_max);
-    cudaMemsetAsync(scratch, 0, radix_scratch_bytes(n_seg, n_max, bits), s);
+    cudaMemsetAsync(scratch, 0, radix_scratch_bytes(n_seg, n_max, max_passes), s);
     const SortScr scr = carve(scratch, n_seg, passes);
     dim3 grid((unsigned)tiles, (unsigned)n_seg);
     k_sort_hist<<<grid, kSortThreads, 0, s>>>(segs_dev, passes, scr);
