@@ -25,10 +25,10 @@
 namespace mgnn {
 
 constexpr int kThreads = 256;
-constexpr int kHopTile = kThreads;     // frontier nodes per k_hop tile
+constexpr int kHopTileMin = 64;        // frontier nodes per k_hop tile: 64 or 256
 constexpr int kWordTile = kThreads;    // bitmap words per k_compact tile (one per thread)
 
-int64_t scan_tiles_count(int64_t fcap) { return (fcap + kHopTile - 1) / kHopTile; }
+int64_t scan_tiles_count(int64_t fcap) { return (fcap + kHopTileMin - 1) / kHopTileMin; }
 int64_t scan_tiles_words(int64_t words) { return (words + kWordTile - 1) / kWordTile; }
 
 static inline unsigned grid_x_for(int64_t items_per_inst, int items_per_block, int n_inst) {
@@ -82,15 +82,17 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
 }
 
 // ------------------------------------------------------------------ one hop: counts, offsets, samples
-__global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max) {
+// T = frontier nodes per tile (64 or 256; small tiles give small hops enough blocks).
+__global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max, int T) {
     __shared__ long long sm[8];
     __shared__ int tslot;
     __shared__ long long prefix_sh;
+    __shared__ long long s_row[kThreads], s_b0[kThreads], s_d[kThreads], s_o[kThreads];
     const int m = blockIdx.y;
     const int lp = m / W.n_steps, w = m % W.n_steps;
     const PartDev& pd = W.parts[lp];
     const int64_t nF = W.hop_size[(int64_t)m * (kMaxLayers + 1) + hop];
-    const int64_t ntiles = (nF + kHopTile - 1) / kHopTile;
+    const int64_t ntiles = (nF + T - 1) / T;
     const int tile = claim_tile(sc.tilectr + m, &tslot);
     int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
     if (tile >= ntiles) {
@@ -98,10 +100,11 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
         return;
     }
     const int k = W.k_hop[hop];
-    const int64_t f = (int64_t)tile * kHopTile + threadIdx.x;
+    const int64_t f = (int64_t)tile * T + threadIdx.x;
+    const bool mine = threadIdx.x < T && f < nF;
     const int64_t h_below = pd.h_below, n_local = pd.n_local;
     int64_t row = -1, b0 = 0, d = 0;
-    if (f < nF) {
+    if (mine) {
         row = (int64_t)W.fr_rank[(int64_t)m * W.ucap + f] - h_below;
         if (row >= 0 && row < n_local) {               // halo frontier nodes are leaves (R#1)
             b0 = pd.indptr[row];
@@ -118,16 +121,23 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
     __syncthreads();
     const int64_t o = prefix_sh + excl;
     if (tile == 0 && threadIdx.x == 0) off[0] = 0;
-    if (f < nF) {
+    if (mine) {
         MGNN_CHECK(f + 1 < W.off_stride[hop], "off f=%lld", (long long)f);
         off[f + 1] = o + cnt;
     }
-    // ---- sampling: G lanes per node (G = power of two >= k), 32/G nodes of the warp side by side;
+    if (threadIdx.x < T) {
+        s_row[threadIdx.x] = cnt > 0 ? row : -1;
+        s_b0[threadIdx.x] = b0;
+        s_d[threadIdx.x] = d;
+        s_o[threadIdx.x] = o;
+    }
+    __syncthreads();
+    // ---- sampling: G lanes per node (G = power of two >= k), 8 * 32/G nodes of the tile side by side;
     // lane j of a group draws slot j, Floyd collisions resolved by k shuffles inside the group.
     int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop];
     const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
     uint32_t* nb = W.nb + (int64_t)m * W.bm_words;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int G = k <= 8 ? 8 : (k <= 16 ? 16 : 32);
     const int per = 32 / G;
     const int gi = lane / G, gl = lane & (G - 1), gbase = lane & ~(G - 1);
@@ -135,25 +145,27 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
     const uint32_t c3 = ((uint32_t)pd.part_id << 8) | kStreamSample;
     const uint32_t step = (uint32_t)(W.step0 + (uint64_t)w);
     const int64_t lo = pd.lo;
-    for (int base = 0; base < 32; base += per) {
-        const int srcl = base + gi;                    // the node of this group = thread srcl's node
-        const long long n_row = __shfl_sync(kFull, (long long)row, srcl);
-        const long long n_b0 = __shfl_sync(kFull, (long long)b0, srcl);
-        const long long n_d = __shfl_sync(kFull, (long long)d, srcl);
-        const long long n_o = __shfl_sync(kFull, (long long)o, srcl);
-        const bool active = n_row >= 0 && n_d > 0;
+    for (int base = warp * per; base < T; base += 8 * per) {
+        const int idx = base + gi;                     // this group's node in the tile
+        const long long n_row = s_row[idx];
+        const long long n_b0 = s_b0[idx];
+        const long long n_d = s_d[idx];
+        const long long n_o = s_o[idx];
+        const bool active = n_row >= 0;
         const bool whole = n_d <= k;                   // whole neighbourhood in CSR order (R#3)
         uint32_t r = 0, t = 0;
-        if (active && !whole && gl < k) {
-            const u4 u = philox4x32_10(u4{(uint32_t)(lo + n_row), c1 | (uint32_t)gl, step, c3}, W.seed_lo,
-                                       W.seed_hi);
-            t = (uint32_t)(n_d - k + gl);
-            r = __umulhi(u.x, t + 1u);                 // floor(u (t+1) / 2^32)
-        }
-        bool coll = false;                             // Floyd: pos_j = r_j unless already chosen, else t_j
-        for (int jj = 0; jj < k; ++jj) {
-            const uint32_t pj = __shfl_sync(kFull, coll ? t : r, gbase + jj);
-            if (gl > jj && r == pj) coll = true;
+        bool coll = false;
+        if (__any_sync(kFull, active && !whole)) {     // some group draws: Philox + Floyd
+            if (active && !whole && gl < k) {
+                const u4 u = philox4x32_10(u4{(uint32_t)(lo + n_row), c1 | (uint32_t)gl, step, c3}, W.seed_lo,
+                                           W.seed_hi);
+                t = (uint32_t)(n_d - k + gl);
+                r = __umulhi(u.x, t + 1u);             // floor(u (t+1) / 2^32)
+            }
+            for (int jj = 0; jj < k; ++jj) {           // Floyd: pos_j = r_j unless already chosen, else t_j
+                const uint32_t pj = __shfl_sync(kFull, coll ? t : r, gbase + jj);
+                if (gl > jj && r == pj) coll = true;
+            }
         }
         if (active && gl < (whole ? (int)n_d : k)) {
             const uint32_t pos = whole ? (uint32_t)gl : (coll ? t : r);
@@ -229,9 +241,13 @@ void launch_seeds(const WinDev& w, cudaStream_t s) {
 }
 
 void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s) {
-    const int64_t tiles = scan_tiles_count(fcap);
-    dim3 grid((unsigned)(tiles < 1 ? 1 : tiles), w.n_inst);
-    k_hop<<<grid, kThreads, 0, s>>>(w, hop, sc, tiles < 1 ? 1 : tiles);
+    // small hops (e.g. the seeds) use 64-node tiles so the launch still fills the GPU
+    const int T = (fcap * (int64_t)w.n_inst) / 256 < 148 * 4 ? 64 : 256;
+    const int64_t tiles_max = scan_tiles_count(fcap);          // scratch stride (64-node tiles)
+    int64_t tiles = (fcap + T - 1) / T;
+    if (tiles < 1) tiles = 1;
+    dim3 grid((unsigned)tiles, w.n_inst);
+    k_hop<<<grid, kThreads, 0, s>>>(w, hop, sc, tiles_max < 1 ? 1 : tiles_max, T);
     count_launches(1, __func__);
 }
 
