@@ -111,8 +111,10 @@ struct mgnn_ctx_s {
     size_t ev_zero_bytes = 0;
     Scratch ev_sc{};
     int64_t ev_tiles = 1;
-    void* sort_scr = nullptr;            // radix sort scratch (histograms + look-back words)
+    void* sort_scr = nullptr;            // radix sort scratch of init / eviction (buffer stream)
     size_t sort_scr_bytes = 0;
+    void* perm_scr = nullptr;            // radix sort scratch of epoch orders (sampling stream), so
+    size_t perm_scr_bytes = 0;           // mgnn_sample may run concurrently with gather/score
     // sampler
     bool configured = false;
     int32_t L = 0, batch = 0, max_window = 0;
@@ -266,13 +268,13 @@ void free_perm(Part& p) {
     p.perm_slots = 0;
 }
 
-mgnn_status ensure_sort_scratch(mgnn_ctx ctx, size_t bytes) {
-    if (bytes <= ctx->sort_scr_bytes) return MGNN_OK;
-    if (ctx->sort_scr) cudaFree(ctx->sort_scr);
-    ctx->sort_scr = nullptr;
-    ctx->sort_scr_bytes = 0;
-    CK(cudaMalloc(&ctx->sort_scr, bytes));
-    ctx->sort_scr_bytes = bytes;
+mgnn_status ensure_scratch(mgnn_ctx ctx, void** p, size_t* have, size_t bytes) {
+    if (bytes <= *have) return MGNN_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *have = 0;
+    CK(cudaMalloc(p, bytes));
+    *have = bytes;
     return MGNN_OK;
 }
 
@@ -386,6 +388,7 @@ void mgnn_destroy(mgnn_ctx ctx) {
     dfree(ctx->d_sel_n);
     dfree(ctx->ev_zero);
     if (ctx->sort_scr) cudaFree(ctx->sort_scr);
+    if (ctx->perm_scr) cudaFree(ctx->perm_scr);
     dfree(ctx->d_permsegs);
     dfree(ctx->d_perm_n);
     delete ctx;
@@ -613,7 +616,8 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
     ctx->ev_sc.status = (unsigned long long*)(ctx->ev_zero + ((2 * n_lp * 4 + 63) / 64) * 64);
     ctx->ev_zero_bytes = ((2 * n_lp * 4 + 63) / 64) * 64 + (size_t)(2 * n_lp) * ctx->ev_tiles * 8;
     {
-        mgnn_status st2 = ensure_sort_scratch(ctx, std::max(radix_scratch_bytes(2 * n_lp, n_sort_max, 8),
+        mgnn_status st2 = ensure_scratch(ctx, &ctx->sort_scr, &ctx->sort_scr_bytes,
+                                         std::max(radix_scratch_bytes(2 * n_lp, n_sort_max, 8),
                                                              radix_scratch_bytes(1, std::max<int64_t>(nh_max, 1), 4)));
         if (st2) return st2;
     }
@@ -727,7 +731,7 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
         scr = std::max(scr, radix_scratch_bytes(p.perm_chunk, nt, 8));
     }
     {
-        mgnn_status st2 = ensure_sort_scratch(ctx, scr);
+        mgnn_status st2 = ensure_scratch(ctx, &ctx->perm_scr, &ctx->perm_scr_bytes, scr);
         if (st2) return st2;
     }
     std::vector<SortSeg> ps((size_t)n_lp * ctx->perm_slots_max);
@@ -791,7 +795,7 @@ mgnn_status mgnn_sample(mgnn_ctx ctx, int32_t slot, uint64_t t0, int32_t n_steps
                 const SortSeg* segs = ctx->d_permsegs + (size_t)lp * ctx->perm_slots_max + (c % 2) * G;
                 launch_perm_keys(ctx->d_parts + lp, p.n_train, (uint64_t)(c * G), (int)G, (uint32_t)ctx->run_seed,
                                  (uint32_t)(ctx->run_seed >> 32), segs, s);
-                radix_sort_pairs(segs, (int)G, p.n_train, 8, ctx->sort_scr, s);
+                radix_sort_pairs(segs, (int)G, p.n_train, 8, ctx->perm_scr, s);
                 p.chunk_loaded[c % 2] = c;
             }
         }

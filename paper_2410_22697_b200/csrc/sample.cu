@@ -9,11 +9,13 @@
 //   k_hop     : thread per frontier node x of F_i (a tile of 256 per block):
 //               count min(deg, k_i) (halo nodes: 0, R#1), exclusive offsets by
 //               a block scan + decoupled look-back across tiles; then groups
-//               of G = pow2 >= k_i lanes take the warp's nodes 32/G at a time:
-//               lane j draws u_j = Philox(x, (i<<16)|j, step, (p<<8)|1) (R#4),
-//               r_j = mulhi(u_j, t_j+1) (R#5), Floyd resolution by k_i
-//               in-group shuffles (R#6).  Every neighbour's local rank is
-//               written in slot order and marked in the new-node bitmap
+//               of G = pow2 >= k_i lanes take the tile's nodes 32/G per warp
+//               at a time: lane j draws u_j = Philox(x, (i<<16)|j, step,
+//               (p<<8)|1) (R#4), r_j = mulhi(u_j, t_j+1) (R#5), Floyd
+//               resolution by k_i in-group shuffles (R#6), and stages the
+//               CSR index in shared memory; finally all threads of the block
+//               load the neighbours' local ranks in parallel, write them in
+//               slot order (coalesced) and mark them in the new-node bitmap
 //               unless already in F_i.
 //   k_compact : the bitmap in rank order IS the ascending-id order, so a
 //               popcount scan appends sorted_unique(cols_i) \ F_i to the
@@ -88,93 +90,108 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
     __shared__ int tslot;
     __shared__ long long prefix_sh;
     __shared__ long long s_row[kThreads], s_b0[kThreads], s_d[kThreads], s_o[kThreads];
+    extern __shared__ __align__(16) unsigned char dyn_smem[];
     const int m = blockIdx.y;
     const int lp = m / W.n_steps, w = m % W.n_steps;
     const PartDev& pd = W.parts[lp];
     const int64_t nF = W.hop_size[(int64_t)m * (kMaxLayers + 1) + hop];
     const int64_t ntiles = (nF + T - 1) / T;
-    const int tile = claim_tile(sc.tilectr + m, &tslot);
     int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
-    if (tile >= ntiles) {
-        if (tile == 0 && threadIdx.x == 0) off[0] = 0;   // empty F_i
-        return;
-    }
-    const int k = W.k_hop[hop];
-    const int64_t f = (int64_t)tile * T + threadIdx.x;
-    const bool mine = threadIdx.x < T && f < nF;
-    const int64_t h_below = pd.h_below, n_local = pd.n_local;
-    int64_t row = -1, b0 = 0, d = 0;
-    if (mine) {
-        row = (int64_t)W.fr_rank[(int64_t)m * W.ucap + f] - h_below;
-        if (row >= 0 && row < n_local) {               // halo frontier nodes are leaves (R#1)
-            b0 = pd.indptr[row];
-            d = pd.indptr[row + 1] - b0;
-        } else {
-            row = -1;
+    // persistent: blocks claim tiles in order until the instance's frontier is exhausted
+    for (;;) {
+        const int tile = claim_tile(sc.tilectr + m, &tslot);
+        if (tile >= ntiles) {
+            if (tile == 0 && threadIdx.x == 0) off[0] = 0;   // empty F_i
+            break;
         }
-    }
-    const int cnt = (int)(d < k ? d : k);              // |sample| = min(deg, k) (R#3)
-    long long agg;
-    const long long excl = block_excl_scan256(cnt, sm, &agg);
-    if (threadIdx.x == 0)
-        prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile, (unsigned long long)agg);
-    __syncthreads();
-    const int64_t o = prefix_sh + excl;
-    if (tile == 0 && threadIdx.x == 0) off[0] = 0;
-    if (mine) {
-        MGNN_CHECK(f + 1 < W.off_stride[hop], "off f=%lld", (long long)f);
-        off[f + 1] = o + cnt;
-    }
-    if (threadIdx.x < T) {
-        s_row[threadIdx.x] = cnt > 0 ? row : -1;
-        s_b0[threadIdx.x] = b0;
-        s_d[threadIdx.x] = d;
-        s_o[threadIdx.x] = o;
-    }
-    __syncthreads();
-    // ---- sampling: G lanes per node (G = power of two >= k), 8 * 32/G nodes of the tile side by side;
-    // lane j of a group draws slot j, Floyd collisions resolved by k shuffles inside the group.
-    int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop];
-    const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
-    uint32_t* nb = W.nb + (int64_t)m * W.bm_words;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int G = k <= 8 ? 8 : (k <= 16 ? 16 : 32);
-    const int per = 32 / G;
-    const int gi = lane / G, gl = lane & (G - 1), gbase = lane & ~(G - 1);
-    const uint32_t c1 = (uint32_t)hop << 16;
-    const uint32_t c3 = ((uint32_t)pd.part_id << 8) | kStreamSample;
-    const uint32_t step = (uint32_t)(W.step0 + (uint64_t)w);
-    const int64_t lo = pd.lo;
-    for (int base = warp * per; base < T; base += 8 * per) {
-        const int idx = base + gi;                     // this group's node in the tile
-        const long long n_row = s_row[idx];
-        const long long n_b0 = s_b0[idx];
-        const long long n_d = s_d[idx];
-        const long long n_o = s_o[idx];
-        const bool active = n_row >= 0;
-        const bool whole = n_d <= k;                   // whole neighbourhood in CSR order (R#3)
-        uint32_t r = 0, t = 0;
-        bool coll = false;
-        if (__any_sync(kFull, active && !whole)) {     // some group draws: Philox + Floyd
-            if (active && !whole && gl < k) {
-                const u4 u = philox4x32_10(u4{(uint32_t)(lo + n_row), c1 | (uint32_t)gl, step, c3}, W.seed_lo,
-                                           W.seed_hi);
-                t = (uint32_t)(n_d - k + gl);
-                r = __umulhi(u.x, t + 1u);             // floor(u (t+1) / 2^32)
-            }
-            for (int jj = 0; jj < k; ++jj) {           // Floyd: pos_j = r_j unless already chosen, else t_j
-                const uint32_t pj = __shfl_sync(kFull, coll ? t : r, gbase + jj);
-                if (gl > jj && r == pj) coll = true;
+        const int k = W.k_hop[hop];
+        const int64_t f = (int64_t)tile * T + threadIdx.x;
+        const bool mine = threadIdx.x < T && f < nF;
+        const int64_t h_below = pd.h_below, n_local = pd.n_local;
+        int64_t row = -1, b0 = 0, d = 0;
+        if (mine) {
+            row = (int64_t)W.fr_rank[(int64_t)m * W.ucap + f] - h_below;
+            if (row >= 0 && row < n_local) {               // halo frontier nodes are leaves (R#1)
+                b0 = pd.indptr[row];
+                d = pd.indptr[row + 1] - b0;
+            } else {
+                row = -1;
             }
         }
-        if (active && gl < (whole ? (int)n_d : k)) {
-            const uint32_t pos = whole ? (uint32_t)gl : (coll ? t : r);
-            const int32_t c = pd.cols_rank[n_b0 + pos];
-            MGNN_CHECK(n_o + gl < W.col_stride[hop] && c < pd.vp, "cols o=%lld j=%d c=%d", n_o, gl, c);
-            cols[n_o + gl] = c;
+        const int cnt = (int)(d < k ? d : k);              // |sample| = min(deg, k) (R#3)
+        long long agg;
+        const long long excl = block_excl_scan256(cnt, sm, &agg);
+        if (threadIdx.x == 0)
+            prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile, (unsigned long long)agg);
+        __syncthreads();
+        const int64_t o = prefix_sh + excl;
+        if (tile == 0 && threadIdx.x == 0) off[0] = 0;
+        if (mine) {
+            MGNN_CHECK(f + 1 < W.off_stride[hop], "off f=%lld", (long long)f);
+            off[f + 1] = o + cnt;
+        }
+        if (threadIdx.x < T) {
+            s_row[threadIdx.x] = cnt > 0 ? row : -1;
+            s_b0[threadIdx.x] = b0;
+            s_d[threadIdx.x] = d;
+            s_o[threadIdx.x] = o;
+        }
+        __syncthreads();
+        // ---- phase A: positions.  k lanes per node, 8 * floor(32/k) nodes of the tile side by side;
+        // lane j of a group draws slot j, Floyd collisions resolved by k shuffles inside the group.
+        // Only CSR indices are produced here (no global loads), staged in shared memory.
+        long long* sidx = reinterpret_cast<long long*>(dyn_smem);   // [T * k] CSR index of each sample of the tile
+        const long long o_tile = prefix_sh;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int G = k;                                   // one lane per slot; 32/k nodes per warp step
+        const int per = 32 / G;
+        const int gi = lane / G, gl = lane - gi * G, gbase = gi * G;
+        const uint32_t c1 = (uint32_t)hop << 16;
+        const uint32_t c3 = ((uint32_t)pd.part_id << 8) | kStreamSample;
+        const uint32_t step = (uint32_t)(W.step0 + (uint64_t)w);
+        const int64_t lo = pd.lo;
+        for (int base = warp * per; base < T; base += 8 * per) {
+            const int idx = base + gi;                     // this group's node in the tile
+            const bool ingroup = gi < per && idx < T;      // lanes past per*k idle
+            const long long n_row = ingroup ? s_row[idx] : -1;
+            const long long n_d = ingroup ? s_d[idx] : 0;
+            const bool active = n_row >= 0;
+            const bool whole = n_d <= k;                   // whole neighbourhood in CSR order (R#3)
+            uint32_t r = 0, t = 0;
+            bool coll = false;
+            if (__any_sync(kFull, active && !whole)) {     // some group draws: Philox + Floyd
+                if (active && !whole && gl < k) {
+                    const u4 u = philox4x32_10(u4{(uint32_t)(lo + n_row), c1 | (uint32_t)gl, step, c3}, W.seed_lo,
+                                               W.seed_hi);
+                    t = (uint32_t)(n_d - k + gl);
+                    r = __umulhi(u.x, t + 1u);             // floor(u (t+1) / 2^32)
+                }
+                for (int jj = 0; jj < k; ++jj) {           // Floyd: pos_j = r_j unless already chosen, else t_j
+                    const uint32_t pj = __shfl_sync(kFull, coll ? t : r, (gbase + jj) & 31);
+                    if (gl > jj && r == pj) coll = true;
+                }
+            }
+            if (active && gl < (whole ? (int)n_d : k)) {
+                const uint32_t pos = whole ? (uint32_t)gl : (coll ? t : r);
+                sidx[s_o[idx] - o_tile + gl] = s_b0[idx] + pos;
+            }
+        }
+        __syncthreads();
+        // ---- phase B: every sample of the tile in parallel: neighbour rank, coalesced column write, and
+        // the new-node mark unless the neighbour is already in F_i.
+        int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop] + o_tile;
+        const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
+        uint32_t* nb = W.nb + (int64_t)m * W.bm_words;
+        const int32_t* __restrict__ crank = pd.cols_rank;
+    #pragma unroll 4
+        for (int e = threadIdx.x; e < (int)agg; e += kThreads) {
+            const int32_t c = crank[sidx[e]];
+            MGNN_CHECK(o_tile + e < W.col_stride[hop] && c < pd.vp, "cols o=%lld c=%d", o_tile + e, c);
+            cols[e] = c;
             const uint32_t bit = 1u << (c & 31);
             if (!(fb[c >> 5] & bit)) atomicOr(&nb[c >> 5], bit);
         }
+        __syncthreads();
     }
 }
 
@@ -244,10 +261,19 @@ void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t
     // small hops (e.g. the seeds) use 64-node tiles so the launch still fills the GPU
     const int T = (fcap * (int64_t)w.n_inst) / 256 < 148 * 4 ? 64 : 256;
     const int64_t tiles_max = scan_tiles_count(fcap);          // scratch stride (64-node tiles)
+    // persistent blocks (~5 resident per SM in total); each loops over claimed tiles
     int64_t tiles = (fcap + T - 1) / T;
+    const int64_t target = (148 * 5 + w.n_inst - 1) / w.n_inst;
+    if (tiles > target) tiles = target;
     if (tiles < 1) tiles = 1;
     dim3 grid((unsigned)tiles, w.n_inst);
-    k_hop<<<grid, kThreads, 0, s>>>(w, hop, sc, tiles_max < 1 ? 1 : tiles_max, T);
+    const size_t smem = (size_t)T * w.k_hop[hop] * sizeof(long long);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_hop, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * MGNN_MAX_FANOUT * 8);
+        attr_set = true;
+    }
+    k_hop<<<grid, kThreads, smem, s>>>(w, hop, sc, tiles_max < 1 ? 1 : tiles_max, T);
     count_launches(1, __func__);
 }
 
