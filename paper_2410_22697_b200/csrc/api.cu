@@ -49,6 +49,7 @@ struct Part {
     int32_t* slot_of = nullptr;
     int32_t* slot_h = nullptr;
     unsigned long long* hitmask = nullptr;
+    int32_t* rank_deg = nullptr;
     int32_t* perm = nullptr;
     int32_t perm_chunk = 1;              // G: epoch orders generated per sort call
     int64_t chunk_loaded[2] = {-1, -1};  // chunk id c (epochs [cG, cG+G)) held by ring half c % 2
@@ -105,11 +106,13 @@ struct mgnn_ctx_s {
     // eviction scratch
     SortSeg* d_evsegs = nullptr;
     SortSeg* d_initsegs = nullptr;
+    bool force_sort_path = false;        // MGNN_EVICT_SORT=1: always use the full radix-sort eviction path
     int32_t ev_passes = 8;
     long long* d_sel_n = nullptr;
     char* ev_zero = nullptr;
     size_t ev_zero_bytes = 0;
     Scratch ev_sc{};
+    EvScratch ev_ev{};
     int64_t ev_tiles = 1;
     void* sort_scr = nullptr;            // radix sort scratch of init / eviction (buffer stream)
     size_t sort_scr_bytes = 0;
@@ -213,6 +216,7 @@ void fill_partdev(const mgnn_ctx_s* c, const Part& p, PartDev* d) {
     d->slot_of = p.slot_of;
     d->slot_h = p.slot_h;
     d->hitmask = p.hitmask;
+    d->rank_deg = p.rank_deg;
     d->perm = p.perm;
     (void)c;
 }
@@ -258,7 +262,7 @@ void free_win(Win& w) {
 }
 
 void free_buffer(Part& p) {
-    dfree(p.rows); dfree(p.se); dfree(p.sa); dfree(p.slot_of); dfree(p.slot_h); dfree(p.hitmask);
+    dfree(p.rows); dfree(p.se); dfree(p.sa); dfree(p.slot_of); dfree(p.slot_h); dfree(p.hitmask); dfree(p.rank_deg);
     dfree(p.ek); dfree(p.ekt); dfree(p.ev); dfree(p.evt); dfree(p.rk); dfree(p.rkt); dfree(p.rv); dfree(p.rvt);
 }
 
@@ -344,6 +348,10 @@ mgnn_status mgnn_ctx_create(int32_t device, int32_t n_parts, int64_t n_global, c
     if (ctx->pitch == 0) ctx->pitch = 4;
     ctx->feat_seed = feat_seed;
     ctx->lp_of.assign(n_parts, -1);
+    {
+        const char* e = getenv("MGNN_EVICT_SORT");
+        ctx->force_sort_path = e && e[0] == '1';
+    }
     ctx->tables.assign(n_parts, nullptr);
     mgnn_status st = MGNN_OK;
     auto chk = [&](cudaError_t e) { if (e != cudaSuccess && st == MGNN_OK) st = MGNN_ECUDA; };
@@ -573,6 +581,7 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
         CK(dalloc(&p.slot_of, p.n_h));
         CK(dalloc(&p.slot_h, p.cap));
         CK(dalloc(&p.hitmask, p.cap));
+        CK(dalloc(&p.rank_deg, p.n_h));
         CK(dalloc(&p.ek, p.cap)); CK(dalloc(&p.ekt, p.cap)); CK(dalloc(&p.ev, p.cap)); CK(dalloc(&p.evt, p.cap));
         CK(dalloc(&p.rk, p.n_h)); CK(dalloc(&p.rkt, p.n_h)); CK(dalloc(&p.rv, p.n_h)); CK(dalloc(&p.rvt, p.n_h));
         cap_max = std::max(cap_max, p.cap);
@@ -591,10 +600,10 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
         Part& p = ctx->parts[lp];
         // E: key = S_E bits << 32, items in id order -> digits of the high word only
         segs[2 * lp] = make_seg(p.ek, p.ev, p.ekt, p.evt, ctx->d_sel_n + 2 * lp, {32, 40, 48, 56});
-        // R: key = ~S_A bits << 32 | ~deg_in: the low word needs only the bytes max(deg_in) occupies
-        // (bytes above max(deg_in) are the constant 0xFF of ~deg_in; an even digit count is kept so the
+        // R: key = ~S_A bits << 32 | rank_deg (unique): the low word needs only the bytes n_h occupies
+        // (low word = rank_deg < n_h: bytes above it are zero; an even digit count is kept so the
         // result lands in the primary buffers)
-        segs[2 * lp + 1] = p.max_deg_in < (1 << 16)
+        segs[2 * lp + 1] = p.n_h <= (1 << 16)
                                ? make_seg(p.rk, p.rv, p.rkt, p.rvt, ctx->d_sel_n + 2 * lp + 1, {0, 8, 32, 40, 48, 56})
                                : make_seg(p.rk, p.rv, p.rkt, p.rvt, ctx->d_sel_n + 2 * lp + 1,
                                           {0, 8, 16, 24, 32, 40, 48, 56});
@@ -610,11 +619,23 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
     const int64_t n_sort_max = std::max<int64_t>(std::max(cap_max, nh_max), 1);
     ctx->ev_tiles = (n_sort_max + 2047) / 2048;
     dfree(ctx->ev_zero);
-    ctx->ev_zero_bytes = (size_t)(2 * n_lp) * (ctx->ev_tiles * 8 + 4) + 64;
-    CK(dalloc((char**)&ctx->ev_zero, ctx->ev_zero_bytes));
-    ctx->ev_sc.tilectr = (int32_t*)ctx->ev_zero;
-    ctx->ev_sc.status = (unsigned long long*)(ctx->ev_zero + ((2 * n_lp * 4 + 63) / 64) * 64);
-    ctx->ev_zero_bytes = ((2 * n_lp * 4 + 63) / 64) * 64 + (size_t)(2 * n_lp) * ctx->ev_tiles * 8;
+    {   // eviction-round scratch, zeroed per round: [tile ctrs | look-back words | hist | ticket | thr | n_cand]
+        auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+        const size_t nseg = 2 * (size_t)n_lp;
+        const size_t o_st = up(nseg * 4);
+        const size_t o_hist = o_st + up(nseg * ctx->ev_tiles * 8);
+        const size_t o_tk = o_hist + up(nseg * 4096 * 4);
+        const size_t o_thr = o_tk + 256;
+        const size_t o_nc = o_thr + up(nseg * 16);
+        ctx->ev_zero_bytes = o_nc + up(nseg * 8);
+        CK(dalloc((char**)&ctx->ev_zero, ctx->ev_zero_bytes));
+        ctx->ev_sc.tilectr = (int32_t*)ctx->ev_zero;
+        ctx->ev_sc.status = (unsigned long long*)(ctx->ev_zero + o_st);
+        ctx->ev_ev.hist = (uint32_t*)(ctx->ev_zero + o_hist);
+        ctx->ev_ev.ticket = (unsigned*)(ctx->ev_zero + o_tk);
+        ctx->ev_ev.thr = (long long*)(ctx->ev_zero + o_thr);
+        ctx->ev_ev.n_cand = (unsigned long long*)(ctx->ev_zero + o_nc);
+    }
     {
         mgnn_status st2 = ensure_scratch(ctx, &ctx->sort_scr, &ctx->sort_scr_bytes,
                                          std::max(radix_scratch_bytes(2 * n_lp, n_sort_max, 8),
@@ -875,8 +896,11 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
     if (ctx->pol.delta > 0 && t_last % (uint64_t)ctx->pol.delta == 0) {
         CK(cudaMemsetAsync(ctx->ev_zero, 0, ctx->ev_zero_bytes, s));
         launch_select(ctx->d_parts, n_lp, nmax, ctx->pol.alpha, ctx->pol.theta_r, ctx->d_evsegs, ctx->d_sel_n,
-                      ctx->ev_sc, s);
-        radix_sort_pairs(ctx->d_evsegs, 2 * n_lp, nmax, ctx->ev_passes, ctx->sort_scr, s);
+                      ctx->ev_sc, ctx->ev_ev, s);
+        if (cap_max <= kEvMax && !ctx->force_sort_path)
+            launch_cand_rank(ctx->d_evsegs, n_lp, nmax, ctx->ev_ev, s);     // K winners in order, no sort
+        else
+            radix_sort_pairs(ctx->d_evsegs, 2 * n_lp, nmax, ctx->ev_passes, ctx->sort_scr, s);
         launch_swap_refill(ctx->d_parts, n_lp, cap_max, ctx->d_evsegs, world_of(ctx), w.counts, 8, w.n_steps, s);
     }
     CKL();

@@ -78,6 +78,7 @@ struct PartDev {
     int32_t* slot_of;          // [n_h] slot or -1
     int32_t* slot_h;           // [cap] halo index in slot
     unsigned long long* hitmask;  // [cap] bit w = hit at window step w
+    int32_t* rank_deg;         // [n_h] position in the (deg_in desc, id asc) order (replacement tie-break)
     int32_t* perm;             // [perm_slots][n_train] epoch orders
 };
 

@@ -71,6 +71,13 @@ struct Scratch {          // zeroed look-back status words + tile counters
     int32_t* tilectr;
 };
 
+struct EvScratch {        // eviction-round scratch, zeroed per round
+    uint32_t* hist;                 // [2*n_lp][4096] histogram of key >> 52
+    unsigned* ticket;               // last-block detection of k_select
+    long long* thr;                 // [2*n_lp][2] = {K, threshold digit T (-1: none)}
+    unsigned long long* n_cand;     // [2*n_lp] candidates appended by k_cand
+};
+
 // sample.cu
 void launch_seeds(const WinDev& w, cudaStream_t s);
 void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s);
@@ -85,9 +92,13 @@ void launch_gather(const WinDev& w, const WorldDev& world, cudaStream_t s);
 // score.cu
 void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, float gamma, cudaStream_t s);
 void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, float theta_r, const SortSeg* segs,
-                   long long* n_out, Scratch sc, cudaStream_t s);
+                   long long* n_out, Scratch sc, EvScratch ev, cudaStream_t s);
+// small-buffer path: candidates below the threshold digit, ranked by counting into sorted order
+void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, cudaStream_t s);
 void launch_swap_refill(const PartDev* parts, int n_lp, int64_t cap_max, const SortSeg* segs, const WorldDev& world,
                         long long* counts, int64_t inst_stride_counts, int n_steps, cudaStream_t s);
+// |BUF| up to which the candidate-rank path (no sort) is used for eviction rounds
+constexpr int kEvMax = 65536;
 void launch_init_keys(const PartDev* pd_dev, int64_t n_h, const SortSeg* seg, long long* n_dev, cudaStream_t s);
 void launch_init_fill(const PartDev* pd_dev, int64_t n_h, int64_t cap, const uint32_t* order, cudaStream_t s);
 void launch_rows_from_owners(const PartDev* pd_dev, int64_t cap, const WorldDev& world, cudaStream_t s);

@@ -3,11 +3,27 @@
 //
 // fp32 throughout with explicit round-to-nearest intrinsics and no FTZ
 // (DESIGN R#12), so every score is bit-identical to the step-by-step oracle.
+//
+// Eviction round (every Delta steps, R#14):
+//   k_select  order-preserving compaction of E = {buffered, S_E < alpha} and
+//             R = {not buffered, S_A >= theta_r} with UNIQUE 64-bit keys
+//               E: S_E bits << 32 | node id             -> ascending = (S_E asc, id asc)      (R#16)
+//               R: ~S_A bits << 32 | rank_deg            -> ascending = (S_A desc, deg_in desc, id asc) (R#18)
+//             (rank_deg = position in the static (deg_in desc, id asc) order of the buffer init),
+//             plus a histogram of the top 12 key bits; the last block computes K = min(|E|, |R|)
+//             (R#19) and, per list, the threshold digit T below which the K smallest keys lie.
+//   small |BUF| (<= kEvMax):
+//   k_cand    compacts the candidates (digit <= T) -- typically a few hundred;
+//   k_rank    ranks every candidate by counting smaller candidate keys (keys are unique, so the
+//             rank IS the sorted position) and writes the K winners in order: no sort at all.
+//   large |BUF|: the onesweep radix sort of both lists (sort.cu).
+//   k_swap_refill  pair i = (E[i], R[i]): swap of P:224, refill from the owner's table.
 #include "launch.h"
 
 namespace mgnn {
 
 constexpr int kSThreads = 256;
+constexpr int kDig = 4096;            // 12-bit top-of-key histogram
 
 static inline unsigned blocks_for(int64_t n, int per_block) {
     int64_t b = (n + per_block - 1) / per_block;
@@ -39,19 +55,17 @@ void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, 
 }
 
 // ------------------------------------------------------------------ candidate selection
-// Segment 2*lp   : E = {slots s : S_E[s] < alpha}                       (R#16)
-//                  scanned in halo (= id) order, key = S_E bits << 32 -> stable ascending = (S_E asc, id asc)
-// Segment 2*lp+1 : R = {halo h : not buffered, S_A[h] >= theta_r}     (R#17)
-//                  key = (~S_A bits << 32) | ~deg_in  -> ascending = (S_A desc, deg_in desc);
-//                  items enter in halo order (= id asc) and the sort is stable (R#18).
-// Scores here are >= +0, so their IEEE bit patterns order like the values.
-// Order-preserving compaction by a decoupled look-back scan.
+// Segment 2*lp = E, 2*lp+1 = R; both scanned in halo (= id) order.  Scores here are >= +0, so
+// their IEEE bit patterns order like the values.  Order-preserving compaction by a decoupled
+// look-back scan; warp-aggregated histogram of key >> 52; the last block to finish (ticket)
+// derives K and the per-list threshold digits into ev.thr[sg] = {K, T}.
 __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict__ parts, float alpha, float theta_r,
                                                       const SortSeg* __restrict__ segs, long long* __restrict__ n_out,
-                                                      Scratch sc, int64_t tiles_max) {
+                                                      Scratch sc, int64_t tiles_max, EvScratch ev) {
     __shared__ long long sm[8];
     __shared__ int tslot;
     __shared__ long long prefix_sh;
+    __shared__ int last_sh;
     const int sg = blockIdx.y;
     const PartDev& pd = parts[sg >> 1];
     const bool isE = (sg & 1) == 0;
@@ -59,57 +73,165 @@ __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict_
     const int64_t tile_items = kSThreads * 8;
     const int64_t ntiles = (n + tile_items - 1) / tile_items;
     const int tile = claim_tile(sc.tilectr + sg, &tslot);
-    if (tile >= ntiles) {
-        if (ntiles == 0 && tile == 0 && threadIdx.x == 0) n_out[sg] = 0;
-        return;
-    }
-    const int64_t i0 = (int64_t)tile * tile_items + (int64_t)threadIdx.x * 8;
-    unsigned flags = 0;
-    long long cnt = 0;
-    for (int i = 0; i < 8; ++i) {
-        const int64_t x = i0 + i;
-        bool pf = false;
-        if (x < n) {
-            const int32_t s = pd.slot_of[x];
-            pf = isE ? (s >= 0 && pd.se[s] < alpha) : (s < 0 && pd.sa[x] >= theta_r);
+    if (tile < ntiles) {
+        const int64_t i0 = (int64_t)tile * tile_items + (int64_t)threadIdx.x * 8;
+        unsigned flags = 0;
+        long long cnt = 0;
+        for (int i = 0; i < 8; ++i) {
+            const int64_t x = i0 + i;
+            bool pf = false;
+            if (x < n) {
+                const int32_t s = pd.slot_of[x];
+                pf = isE ? (s >= 0 && pd.se[s] < alpha) : (s < 0 && pd.sa[x] >= theta_r);
+            }
+            flags |= (unsigned)pf << i;
+            cnt += pf;
         }
-        flags |= (unsigned)pf << i;
-        cnt += pf;
+        long long agg;
+        long long excl = block_excl_scan256(cnt, sm, &agg);
+        if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)sg * tiles_max, tile,
+                                                                         (unsigned long long)agg);
+        __syncthreads();
+        int64_t pos = prefix_sh + excl;
+        const SortSeg out = segs[sg];
+        uint32_t* hist = ev.hist + (size_t)sg * kDig;
+        for (int i = 0; i < 8; ++i) {
+            const int64_t x = i0 + i;
+            unsigned d = 0xFFFFFFFFu;
+            if ((flags >> i) & 1u) {
+                unsigned long long key;
+                uint32_t val;
+                if (isE) {
+                    val = (uint32_t)pd.slot_of[x];
+                    key = ((unsigned long long)__float_as_uint(pd.se[val]) << 32) | (uint32_t)pd.halo_ids[x];
+                } else {
+                    val = (uint32_t)x;
+                    key = ((unsigned long long)(~__float_as_uint(pd.sa[x])) << 32) | (uint32_t)pd.rank_deg[x];
+                }
+                MGNN_CHECK(pos < (isE ? pd.cap : n), "select pos=%lld n=%lld sg=%d", (long long)pos, (long long)n, sg);
+                out.keys[pos] = key;
+                out.vals[pos] = val;
+                ++pos;
+                d = (unsigned)(key >> 52);
+            }
+            const unsigned peers = __match_any_sync(kFull, d);
+            if (d != 0xFFFFFFFFu && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[d], (unsigned)__popc(peers));
+        }
+        if (tile == ntiles - 1 && threadIdx.x == 0) n_out[sg] = prefix_sh + agg;
+    } else if (ntiles == 0 && tile == 0 && threadIdx.x == 0) {
+        n_out[sg] = 0;
     }
-    long long agg;
-    long long excl = block_excl_scan256(cnt, sm, &agg);
-    if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)sg * tiles_max, tile,
-                                                                     (unsigned long long)agg);
+    // ---- last block: K per partition and threshold digits
+    __threadfence();
     __syncthreads();
-    int64_t pos = prefix_sh + excl;
-    const SortSeg out = segs[sg];
-    for (int i = 0; i < 8; ++i) {
-        if (!((flags >> i) & 1u)) continue;
-        const int64_t x = i0 + i;
-        unsigned long long key;
-        uint32_t val;
-        if (isE) {
-            val = (uint32_t)pd.slot_of[x];
-            key = (unsigned long long)__float_as_uint(pd.se[val]) << 32;
-        } else {
-            val = (uint32_t)x;
-            key = ((unsigned long long)(~__float_as_uint(pd.sa[x])) << 32) | (uint32_t)(~(uint32_t)pd.deg_in[x]);
+    if (threadIdx.x == 0) last_sh = (atomicAdd(ev.ticket, 1u) == gridDim.x * gridDim.y - 1);
+    __syncthreads();
+    if (!last_sh) return;
+    __threadfence();
+    for (int g = 0; g < (int)gridDim.y; ++g) {
+        const long long nE = *(volatile long long*)&n_out[g & ~1], nR = *(volatile long long*)&n_out[g | 1];
+        const long long K = nE < nR ? nE : nR;
+        // smallest digit T with #(digit <= T) >= K
+        const volatile uint32_t* hist = ev.hist + (size_t)g * kDig;
+        long long local = 0;
+        for (int j = 0; j < kDig / kSThreads; ++j) local += hist[threadIdx.x * (kDig / kSThreads) + j];
+        long long tot;
+        long long run = block_excl_scan256(local, sm, &tot);
+        if (threadIdx.x == 0) {
+            ev.thr[2 * g] = K;
+            ev.thr[2 * g + 1] = -1;
         }
-        MGNN_CHECK(pos < (isE ? pd.cap : n), "select pos=%lld n=%lld sg=%d", (long long)pos, (long long)n, sg);
-        out.keys[pos] = key;
-        out.vals[pos] = val;
-        ++pos;
+        __syncthreads();
+        if (K > 0 && run < K && K <= run + local) {
+            for (int j = 0; j < kDig / kSThreads; ++j) {
+                run += hist[threadIdx.x * (kDig / kSThreads) + j];
+                if (run >= K) {
+                    ev.thr[2 * g + 1] = threadIdx.x * (kDig / kSThreads) + j;
+                    break;
+                }
+            }
+        }
+        __syncthreads();
     }
-    if (tile == ntiles - 1 && threadIdx.x == 0) n_out[sg] = prefix_sh + agg;
 }
 
 void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, float theta_r, const SortSeg* segs,
-                   long long* n_out, Scratch sc, cudaStream_t s) {
+                   long long* n_out, Scratch sc, EvScratch ev, cudaStream_t s) {
     int64_t tiles = (n_max + kSThreads * 8 - 1) / (kSThreads * 8);
     if (tiles < 1) tiles = 1;
     dim3 grid((unsigned)tiles, 2 * n_lp);
-    k_select<<<grid, kSThreads, 0, s>>>(parts, alpha, theta_r, segs, n_out, sc, tiles);
+    k_select<<<grid, kSThreads, 0, s>>>(parts, alpha, theta_r, segs, n_out, sc, tiles, ev);
     count_launches(1, __func__);
+}
+
+// ------------------------------------------------------------------ candidates: key >> 52 <= T
+__global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ segs, EvScratch ev) {
+    const int sg = blockIdx.y;
+    const SortSeg S = segs[sg];
+    const long long n = *S.n;
+    const long long T = ev.thr[2 * sg + 1];
+    if (T < 0) return;
+    const int lane = threadIdx.x & 31;
+    const long long stride = (long long)gridDim.x * kSThreads;
+    for (long long i0 = (long long)blockIdx.x * kSThreads + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+        const long long i = i0 + lane;
+        unsigned long long k = 0;
+        bool c = false;
+        if (i < n) {
+            k = S.keys[i];
+            c = (long long)(k >> 52) <= T;
+        }
+        const unsigned ball = __ballot_sync(kFull, c);
+        if (!ball) continue;
+        // warp-aggregated append (order irrelevant: keys are unique)
+        unsigned long long base = 0;
+        const int leader = __ffs(ball) - 1;
+        if (lane == leader) base = atomicAdd(&ev.n_cand[sg], (unsigned long long)__popc(ball));
+        base = __shfl_sync(kFull, base, leader);
+        if (c) {
+            const unsigned long long p = base + __popc(ball & ((1u << lane) - 1u));
+            S.keys_tmp[p] = k;
+            S.vals_tmp[p] = S.vals[i];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ rank by counting (unique keys)
+__global__ void __launch_bounds__(kSThreads) k_rank(const SortSeg* __restrict__ segs, EvScratch ev) {
+    __shared__ unsigned long long tile_k[2048];
+    const int sg = blockIdx.y;
+    const SortSeg S = segs[sg];
+    const long long T = ev.thr[2 * sg + 1];
+    if (T < 0) return;
+    const long long nc = (long long)ev.n_cand[sg];
+    const long long K = ev.thr[2 * sg];
+    const long long first = (long long)blockIdx.x * kSThreads;
+    if (first >= nc) return;
+    const long long c = first + threadIdx.x;
+    const unsigned long long mine = c < nc ? S.keys_tmp[c] : ~0ull;
+    long long rank = 0;
+    for (long long t0 = 0; t0 < nc; t0 += 2048) {
+        const int m = (int)(nc - t0 < 2048 ? nc - t0 : 2048);
+        __syncthreads();
+        for (int j = threadIdx.x; j < m; j += kSThreads) tile_k[j] = S.keys_tmp[t0 + j];
+        __syncthreads();
+        int r = 0;
+#pragma unroll 8
+        for (int j = 0; j < m; ++j) r += tile_k[j] < mine;
+        rank += r;
+    }
+    if (c < nc && rank < K) {
+        S.keys[rank] = mine;          // the K winners, in order, replace the list
+        S.vals[rank] = S.vals_tmp[c];
+    }
+}
+
+void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, cudaStream_t s) {
+    dim3 g1(blocks_for(n_max, kSThreads) > 64 ? 64 : blocks_for(n_max, kSThreads), 2 * n_lp);
+    k_cand<<<g1, kSThreads, 0, s>>>(segs, ev);
+    dim3 g2((unsigned)((n_max + kSThreads - 1) / kSThreads), 2 * n_lp);
+    k_rank<<<g2, kSThreads, 0, s>>>(segs, ev);
+    count_launches(2, __func__);
 }
 
 // ------------------------------------------------------------------ swap + refill
@@ -137,14 +259,8 @@ __global__ void __launch_bounds__(kSThreads) k_swap_refill(const PartDev* __rest
     for (int64_t i = (int64_t)blockIdx.x * (kSThreads / 32) + (threadIdx.x >> 5); i < k; i += nwarps) {
         const int32_t s = (int32_t)E.vals[i];
         const int32_t r = (int32_t)R.vals[i];
-#ifdef MGNN_CHECKS
-        if (s < 0 || s >= pd.cap || r < 0 || r >= pd.n_h || k > pd.cap) {
-            if (lane == 0)
-                printf("swap lp=%d i=%lld k=%lld nE=%lld nR=%lld s=%d r=%d cap=%lld nh=%lld\n", lp, (long long)i, k,
-                       nE, nR, s, r, (long long)pd.cap, (long long)pd.n_h);
-            __trap();
-        }
-#endif
+        MGNN_CHECK(s >= 0 && s < pd.cap && r >= 0 && r < pd.n_h, "swap lp=%d i=%lld s=%d r=%d", lp, (long long)i, s,
+                   r);
         if (lane == 0) {
             const int32_t e = pd.slot_h[s];
             const float se_s = pd.se[s];
@@ -189,12 +305,14 @@ void launch_init_keys(const PartDev* pd_dev, int64_t n_h, const SortSeg* seg, lo
     count_launches(1, __func__);
 }
 
-// S_A = 0 for every halo node, then for the top-cap: slot s <- order[s], S_E = 1, S_A = -1.
-__global__ void k_init_reset(const PartDev* __restrict__ pdp) {
+// S_A = 0 for every halo node and rank_deg[order[i]] = i; then for the top-cap: slot s <- order[s],
+// S_E = 1, S_A = -1.
+__global__ void k_init_reset(const PartDev* __restrict__ pdp, const uint32_t* __restrict__ order) {
     const PartDev& pd = *pdp;
     for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < pd.n_h; h += (int64_t)gridDim.x * blockDim.x) {
         pd.sa[h] = 0.0f;
         pd.slot_of[h] = -1;
+        pd.rank_deg[order[h]] = (int32_t)h;
     }
 }
 
@@ -211,7 +329,7 @@ __global__ void k_init_slots(const PartDev* __restrict__ pdp, const uint32_t* __
 }
 
 void launch_init_fill(const PartDev* pd_dev, int64_t n_h, int64_t cap, const uint32_t* order, cudaStream_t s) {
-    k_init_reset<<<blocks_for(n_h < 1 ? 1 : n_h, kSThreads), kSThreads, 0, s>>>(pd_dev);
+    k_init_reset<<<blocks_for(n_h < 1 ? 1 : n_h, kSThreads), kSThreads, 0, s>>>(pd_dev, order);
     k_init_slots<<<blocks_for(cap < 1 ? 1 : cap, kSThreads), kSThreads, 0, s>>>(pd_dev, order);
     count_launches(2, __func__);
 }

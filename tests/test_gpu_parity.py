@@ -86,3 +86,11 @@ def test_arxiv_full_size_bench_config():
     st = run_parity(g, 2, 128, [10, 25], 1000, 2500, 0.995, 32, 1.0, [32, 32, 32], sample_every=7,
                     check_x_rows=4096)
     assert st["evicted"] > 0
+
+
+@pytest.mark.parametrize("wins", [[4, 4, 4, 4], [8, 8, 8]])
+def test_cfg1_full_sort_eviction_path(cfg1, monkeypatch, wins):
+    """The large-buffer eviction path (full radix sort of E and R) gives the same result."""
+    monkeypatch.setenv("MGNN_EVICT_SORT", "1")
+    st = run_parity(cfg1, 2, 64, [10, 25], 256, 2500, 0.9, wins[0], 1.0, wins)
+    assert st["evicted"] > 0

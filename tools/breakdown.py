@@ -1,0 +1,61 @@
+"""Per-call GPU time of one window (serial, no overlap): sample / lookup_gather / score_evict_refill.
+
+    python tools/breakdown.py [--windows 10]
+Uses the bench workload (arxiv-shaped, 2 partitions, 32-step windows) and CUDA events on one stream.
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from inputs import synth  # noqa: E402
+from paper_2410_22697_b200 import pipeline as PL  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--windows", type=int, default=12)
+    ap.add_argument("--config", default="arxiv")
+    ap.add_argument("--parts", type=int, default=2)
+    a = ap.parse_args()
+    cfg = synth.CONFIGS[a.config]
+    P = a.parts
+    f_bp, gamma, delta = bench.policy_for(P)
+    g = synth.generate(cfg)
+    parts = synth.partition(g, P)
+    ctx = PL.build_context(0, parts, cfg.feat_dim, synth.FEAT_SEED)
+    ctx.buffer_init(gamma, PL.alpha_default(gamma, delta), 1.0, delta, f_bp)
+    W = min(32, delta)
+    ctx.sampler_config(cfg.fanouts, cfg.batch, synth.RUN_SEED, W)
+    s = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    t, slot = 1, 0
+    acc = {"sample": [], "gather": [], "score": []}
+    for i in range(a.windows + 3):
+        flush.zero_()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record(s)
+        ctx.sample(slot, t, W, stream=s)
+        e[1].record(s)
+        ctx.lookup_gather(slot, s)
+        e[2].record(s)
+        ctx.score(slot, s)
+        e[3].record(s)
+        torch.cuda.synchronize()
+        if i >= 3:
+            acc["sample"].append(e[0].elapsed_time(e[1]))
+            acc["gather"].append(e[1].elapsed_time(e[2]))
+            acc["score"].append(e[2].elapsed_time(e[3]))
+        t += W
+        slot ^= 1
+    for k, v in acc.items():
+        print(f"{k:8s} mean {1e3 * sum(v) / len(v):8.1f} us   min {1e3 * min(v):8.1f} us")
+
+
+if __name__ == "__main__":
+    main()
