@@ -27,6 +27,8 @@ constexpr int kGWarps = kGThreads / 32;
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ void stcs4(float* p, float4 v) { __stcs(reinterpret_cast<float4*>(p), v); }
 
+// WIDE: rows of >= 32 float4 (D >= 128, one or more 16-B chunks per lane); else 32/q rows per warp step.
+template <bool WIDE>
 __global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
     __shared__ unsigned long long cnt_sh[3];
     const int m = blockIdx.y;
@@ -81,21 +83,26 @@ __global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
         const int nrows = (int)(U - f0 < 32 ? U - f0 : 32);
         float* Xw = X + f0 * pitch;
         // ---- copy the rows, several independent 16-B loads in flight per lane
-        if (q >= 32) {
-            for (int j = 0; j < nrows; j += 4) {
-                const float* s0 = (const float*)__shfl_sync(kFull, (unsigned long long)src, j);
-                const float* s1 = (const float*)__shfl_sync(kFull, (unsigned long long)src, (j + 1) & 31);
-                const float* s2 = (const float*)__shfl_sync(kFull, (unsigned long long)src, (j + 2) & 31);
-                const float* s3 = (const float*)__shfl_sync(kFull, (unsigned long long)src, (j + 3) & 31);
-                for (int c = lane * 4; c < pitch; c += 128) {
-                    float4 v0 = ldg4(s0 + c), v1, v2, v3;
-                    if (j + 1 < nrows) v1 = ldg4(s1 + c);
-                    if (j + 2 < nrows) v2 = ldg4(s2 + c);
-                    if (j + 3 < nrows) v3 = ldg4(s3 + c);
-                    stcs4(Xw + (int64_t)j * pitch + c, v0);
-                    if (j + 1 < nrows) stcs4(Xw + (int64_t)(j + 1) * pitch + c, v1);
-                    if (j + 2 < nrows) stcs4(Xw + (int64_t)(j + 2) * pitch + c, v2);
-                    if (j + 3 < nrows) stcs4(Xw + (int64_t)(j + 3) * pitch + c, v3);
+        if (WIDE) {
+            constexpr int R = 8;                       // rows in flight per lane
+            if (nrows == 32) {
+#pragma unroll 1
+                for (int j = 0; j < 32; j += R) {
+                    const float* s[R];
+#pragma unroll
+                    for (int u = 0; u < R; ++u) s[u] = (const float*)__shfl_sync(kFull, (unsigned long long)src, j + u);
+                    for (int c = lane * 4; c < pitch; c += 128) {
+                        float4 v[R];
+#pragma unroll
+                        for (int u = 0; u < R; ++u) v[u] = ldg4(s[u] + c);
+#pragma unroll
+                        for (int u = 0; u < R; ++u) stcs4(Xw + (int64_t)(j + u) * pitch + c, v[u]);
+                    }
+                }
+            } else {
+                for (int j = 0; j < nrows; ++j) {
+                    const float* s = (const float*)__shfl_sync(kFull, (unsigned long long)src, j);
+                    for (int c = lane * 4; c < pitch; c += 128) stcs4(Xw + (int64_t)j * pitch + c, ldg4(s + c));
                 }
             }
         } else {
@@ -139,13 +146,17 @@ __global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
 }
 
 void launch_gather(const WinDev& w, const WorldDev& world, cudaStream_t s) {
-    // one wave of 4 resident 256-thread blocks per SM in total (64 registers per thread)
-    int64_t target = (148 * 4 + w.n_inst - 1) / w.n_inst;
+    // exactly one wave of 4 resident 256-thread blocks per SM in total (64 registers per thread):
+    // floor, so no second, nearly empty wave leaves SMs idle at the tail
+    int64_t target = (148 * 4) / w.n_inst;
     int64_t need = (w.ucap + kGWarps * 32 - 1) / (kGWarps * 32);
     unsigned gx = (unsigned)(need < target ? need : target);
     if (gx < 1) gx = 1;
     dim3 grid(gx, w.n_inst);
-    k_gather<<<grid, kGThreads, 0, s>>>(w, world);
+    if (w.pitch >= 128)
+        k_gather<true><<<grid, kGThreads, 0, s>>>(w, world);
+    else
+        k_gather<false><<<grid, kGThreads, 0, s>>>(w, world);
     count_launches(1, __func__);
 }
 

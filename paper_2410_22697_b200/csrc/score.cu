@@ -57,15 +57,13 @@ void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, 
 // ------------------------------------------------------------------ candidate selection
 // Segment 2*lp = E, 2*lp+1 = R; both scanned in halo (= id) order.  Scores here are >= +0, so
 // their IEEE bit patterns order like the values.  Order-preserving compaction by a decoupled
-// look-back scan; warp-aggregated histogram of key >> 52; the last block to finish (ticket)
-// derives K and the per-list threshold digits into ev.thr[sg] = {K, T}.
+// look-back scan, plus a warp-aggregated histogram of key >> 52 per list.
 __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict__ parts, float alpha, float theta_r,
                                                       const SortSeg* __restrict__ segs, long long* __restrict__ n_out,
                                                       Scratch sc, int64_t tiles_max, EvScratch ev) {
     __shared__ long long sm[8];
     __shared__ int tslot;
     __shared__ long long prefix_sh;
-    __shared__ int last_sh;
     const int sg = blockIdx.y;
     const PartDev& pd = parts[sg >> 1];
     const bool isE = (sg & 1) == 0;
@@ -121,38 +119,6 @@ __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict_
     } else if (ntiles == 0 && tile == 0 && threadIdx.x == 0) {
         n_out[sg] = 0;
     }
-    // ---- last block: K per partition and threshold digits
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last_sh = (atomicAdd(ev.ticket, 1u) == gridDim.x * gridDim.y - 1);
-    __syncthreads();
-    if (!last_sh) return;
-    __threadfence();
-    for (int g = 0; g < (int)gridDim.y; ++g) {
-        const long long nE = *(volatile long long*)&n_out[g & ~1], nR = *(volatile long long*)&n_out[g | 1];
-        const long long K = nE < nR ? nE : nR;
-        // smallest digit T with #(digit <= T) >= K
-        const volatile uint32_t* hist = ev.hist + (size_t)g * kDig;
-        long long local = 0;
-        for (int j = 0; j < kDig / kSThreads; ++j) local += hist[threadIdx.x * (kDig / kSThreads) + j];
-        long long tot;
-        long long run = block_excl_scan256(local, sm, &tot);
-        if (threadIdx.x == 0) {
-            ev.thr[2 * g] = K;
-            ev.thr[2 * g + 1] = -1;
-        }
-        __syncthreads();
-        if (K > 0 && run < K && K <= run + local) {
-            for (int j = 0; j < kDig / kSThreads; ++j) {
-                run += hist[threadIdx.x * (kDig / kSThreads) + j];
-                if (run >= K) {
-                    ev.thr[2 * g + 1] = threadIdx.x * (kDig / kSThreads) + j;
-                    break;
-                }
-            }
-        }
-        __syncthreads();
-    }
 }
 
 void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, float theta_r, const SortSeg* segs,
@@ -165,11 +131,41 @@ void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, f
 }
 
 // ------------------------------------------------------------------ candidates: key >> 52 <= T
+// Every block derives K = min(|E|, |R|) of its partition and the threshold digit T of its list
+// (smallest T with #(digit <= T) >= K) from the histogram; block 0 records {K, T} for k_rank.
 __global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ segs, EvScratch ev) {
+    __shared__ long long sm[8];
+    __shared__ long long T_sh;
     const int sg = blockIdx.y;
     const SortSeg S = segs[sg];
     const long long n = *S.n;
-    const long long T = ev.thr[2 * sg + 1];
+    const long long nE = *segs[sg & ~1].n, nR = *segs[sg | 1].n;
+    const long long K = nE < nR ? nE : nR;
+    {
+        const uint32_t* hist = ev.hist + (size_t)sg * kDig;
+        constexpr int per = kDig / kSThreads;
+        long long local = 0;
+        for (int j = 0; j < per; ++j) local += hist[threadIdx.x * per + j];
+        long long tot;
+        long long run = block_excl_scan256(local, sm, &tot);
+        if (threadIdx.x == 0) T_sh = -1;
+        __syncthreads();
+        if (K > 0 && run < K && K <= run + local) {
+            for (int j = 0; j < per; ++j) {
+                run += hist[threadIdx.x * per + j];
+                if (run >= K) {
+                    T_sh = threadIdx.x * per + j;
+                    break;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    const long long T = T_sh;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ev.thr[2 * sg] = K;
+        ev.thr[2 * sg + 1] = T;
+    }
     if (T < 0) return;
     const int lane = threadIdx.x & 31;
     const long long stride = (long long)gridDim.x * kSThreads;

@@ -57,5 +57,46 @@ def main():
         print(f"{k:8s} mean {1e3 * sum(v) / len(v):8.1f} us   min {1e3 * min(v):8.1f} us")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--timeline" not in sys.argv:
     main()
+
+
+def timeline(windows=6):
+    """Pipelined (two-stream) iterations: event timestamps after each call, relative to iteration start."""
+    cfg = synth.CONFIGS["arxiv"]
+    P = 2
+    f_bp, gamma, delta = bench.policy_for(P)
+    g = synth.generate(cfg)
+    parts = synth.partition(g, P)
+    ctx = PL.build_context(0, parts, cfg.feat_dim, synth.FEAT_SEED)
+    ctx.buffer_init(gamma, PL.alpha_default(gamma, delta), 1.0, delta, f_bp)
+    W = 32
+    ctx.sampler_config(cfg.fanouts, cfg.batch, synth.RUN_SEED, W)
+    sA, sB = torch.cuda.Stream(), torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    t, slot = 1, 0
+    ctx.sample(0, t, W, stream=sA)
+    torch.cuda.synchronize()
+    for i in range(windows + 4):
+        flush.zero_()
+        torch.cuda.synchronize()
+        ev = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "sampleA", "gatherB", "scoreB", "end")}
+        ev["start"].record(sB)
+        sA.wait_event(ev["start"])
+        ctx.sample(slot ^ 1, t + W, W, stream=sA)
+        ev["sampleA"].record(sA)
+        ctx.lookup_gather(slot, sB)
+        ev["gatherB"].record(sB)
+        ctx.score(slot, sB)
+        ev["scoreB"].record(sB)
+        sB.wait_stream(sA)
+        ev["end"].record(sB)
+        torch.cuda.synchronize()
+        if i >= 4:
+            print("  ".join(f"{k} {1e3 * ev['start'].elapsed_time(e):7.1f}" for k, e in ev.items() if k != "start"))
+        t += W
+        slot ^= 1
+
+
+if __name__ == "__main__" and "--timeline" in sys.argv:
+    timeline()
