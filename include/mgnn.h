@@ -191,6 +191,11 @@ MGNN_API int64_t mgnn_launch_count(mgnn_ctx ctx);
 MGNN_API mgnn_status mgnn_profile_enable(mgnn_ctx ctx, int32_t enable);
 MGNN_API mgnn_status mgnn_profile_read(mgnn_ctx ctx, double* ms, int64_t* launches, int64_t* bytes);
 
+/* Process-wide per-launcher timing (diagnostics): enable = 1 clears and starts recording an
+ * event after every kernel launcher (time since the previous event on the same stream is
+ * attributed to it); enable = 0 stops, synchronises and writes a text table into report. */
+MGNN_API mgnn_status mgnn_profile_kernels(int32_t enable, char* report, int64_t report_len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,7 @@ SYMBOLS = [
     "mgnn_table_export", "mgnn_table_import", "mgnn_buffer_init", "mgnn_sampler_config", "mgnn_sample",
     "mgnn_lookup_gather", "mgnn_score_evict_refill", "mgnn_window_get", "mgnn_counts_read",
     "mgnn_buffer_snapshot", "mgnn_part_info", "mgnn_halo_get", "mgnn_table_row", "mgnn_launch_count",
-    "mgnn_profile_enable", "mgnn_profile_read",
+    "mgnn_profile_enable", "mgnn_profile_read", "mgnn_profile_kernels",
 ]
 
 
@@ -82,6 +82,7 @@ def load(path: str = LIB_PATH):
         "mgnn_launch_count": (I64, [P]),
         "mgnn_profile_enable": (S, [P, I32]),
         "mgnn_profile_read": (S, [P, P, P, P]),
+        "mgnn_profile_kernels": (S, [I32, P, I64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -18,11 +18,31 @@ static const bool g_debug_sync = [] {
     const char* e = getenv("MGNN_DEBUG_SYNC");
     return e && e[0] == '1';
 }();
-void count_launches(long long n, const char* who) {
+struct ProfRec {
+    const char* who;
+    cudaEvent_t a, b;
+};
+static bool g_kprof = false;
+static std::vector<ProfRec> g_kprof_recs;
+static std::vector<std::pair<cudaStream_t, cudaEvent_t>> g_kprof_last;
+
+void count_launches(long long n, const char* who, cudaStream_t s) {
     g_launches.fetch_add(n, std::memory_order_relaxed);
     if (g_debug_sync) {
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) fprintf(stderr, "[mgnn] %s failed: %s\n", who, cudaGetErrorString(e));
+    }
+    if (g_kprof) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        cudaEventRecord(e, s);
+        for (auto& pl : g_kprof_last)
+            if (pl.first == s) {
+                g_kprof_recs.push_back(ProfRec{who, pl.second, e});
+                pl.second = e;
+                return;
+            }
+        g_kprof_last.emplace_back(s, e);
     }
 }
 long long launches_total() { return g_launches.load(); }
@@ -975,6 +995,43 @@ mgnn_status mgnn_buffer_snapshot(mgnn_ctx ctx, int32_t lp, int32_t* node_ids, fl
 }
 
 // ------------------------------------------------------------------ profiling
+mgnn_status mgnn_profile_kernels(int32_t enable, char* report, int64_t report_len) {
+    if (!enable && report && report_len > 0) {
+        std::vector<std::pair<std::string, std::pair<double, long long>>> agg;
+        for (auto& r : g_kprof_recs) {
+            float ms = 0.0f;
+            if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) continue;
+            bool found = false;
+            for (auto& a : agg)
+                if (a.first == r.who) {
+                    a.second.first += ms;
+                    a.second.second += 1;
+                    found = true;
+                }
+            if (!found) agg.push_back({r.who, {ms, 1}});
+        }
+        std::string out;
+        for (auto& a : agg) {
+            char line[256];
+            snprintf(line, sizeof(line), "%-28s %10.3f ms %8lld calls %9.2f us/call\n", a.first.c_str(), a.second.first,
+                     a.second.second, 1e3 * a.second.first / (double)a.second.second);
+            out += line;
+        }
+        snprintf(report, (size_t)report_len, "%s", out.c_str());
+    }
+    if (!enable || enable) {
+        std::vector<cudaEvent_t> all;
+        for (auto& r : g_kprof_recs) all.push_back(r.b);
+        for (auto& l : g_kprof_last) all.push_back(l.second);
+        cudaDeviceSynchronize();
+        for (cudaEvent_t e : all) cudaEventDestroy(e);
+        g_kprof_recs.clear();
+        g_kprof_last.clear();
+    }
+    g_kprof = enable != 0;
+    return MGNN_OK;
+}
+
 mgnn_status mgnn_profile_enable(mgnn_ctx ctx, int32_t enable) {
     if (!ctx) return MGNN_EINVAL;
     ctx->prof = enable != 0;

@@ -157,7 +157,7 @@ void launch_gather(const WinDev& w, const WorldDev& world, cudaStream_t s) {
         k_gather<true><<<grid, kGThreads, 0, s>>>(w, world);
     else
         k_gather<false><<<grid, kGThreads, 0, s>>>(w, world);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 }  // namespace mgnn

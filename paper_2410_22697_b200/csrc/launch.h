@@ -14,7 +14,9 @@ constexpr int kMaxLayers = MGNN_MAX_LAYERS;
 // Kernel launches issued by the library (process-wide; bench evidence).
 // With MGNN_DEBUG_SYNC=1 in the environment every launcher synchronises and
 // reports the first failing kernel by name (debug aid, never on by default).
-void count_launches(long long n, const char* who);
+// With per-kernel profiling on (mgnn_profile_kernels), an event is recorded after every launcher
+// and the time since the previous event on the same stream is attributed to that launcher.
+void count_launches(long long n, const char* who, cudaStream_t s);
 long long launches_total();
 
 // ------------------------------------------------------------------ window (device view)

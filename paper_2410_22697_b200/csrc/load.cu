@@ -30,7 +30,7 @@ __global__ void k_mark_halo(const int32_t* __restrict__ cols, int64_t nnz, int64
 void launch_mark_halo(const int32_t* cols, int64_t nnz, int64_t lo, int64_t hi, uint32_t* bm, cudaStream_t s) {
     if (nnz < 1) return;
     k_mark_halo<<<lblocks(nnz), kLThreads, 0, s>>>(cols, nnz, lo, hi, bm);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 // Bitmap -> ascending ids (decoupled look-back over popcounts, 4 words per thread).
@@ -71,7 +71,7 @@ void launch_bitmap_to_ids(const uint32_t* bm, int64_t nwords, int32_t* out, long
     int64_t tiles = (nwords + kLThreads * 4 - 1) / (kLThreads * 4);
     if (tiles < 1) tiles = 1;
     k_bitmap_to_ids<<<(unsigned)tiles, kLThreads, 0, s>>>(bm, nwords, out, out_n, sc);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 __global__ void k_lower_bound(const int32_t* __restrict__ arr, int64_t n, int64_t v, long long* out) {
@@ -85,7 +85,7 @@ __global__ void k_lower_bound(const int32_t* __restrict__ arr, int64_t n, int64_
 
 void launch_lower_bound(const int32_t* arr, int64_t n, int64_t v, long long* out, cudaStream_t s) {
     k_lower_bound<<<1, 1, 0, s>>>(arr, n, v, out);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 __global__ void k_halo_index(const int32_t* __restrict__ halo, int64_t n_h, int32_t* __restrict__ gmap) {
@@ -96,7 +96,7 @@ __global__ void k_halo_index(const int32_t* __restrict__ halo, int64_t n_h, int3
 void launch_halo_index(const int32_t* halo, int64_t n_h, int32_t* gmap, cudaStream_t s) {
     if (n_h < 1) return;
     k_halo_index<<<lblocks(n_h), kLThreads, 0, s>>>(halo, n_h, gmap);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 __global__ void k_deg_rank(const int32_t* __restrict__ cols, int64_t nnz, int64_t lo, int64_t n_local, int64_t h_below,
@@ -120,7 +120,7 @@ void launch_deg_rank(const int32_t* cols, int64_t nnz, int64_t lo, int64_t n_loc
                      const int32_t* gmap, int32_t* deg_in, int32_t* cols_rank, cudaStream_t s) {
     if (nnz < 1) return;
     k_deg_rank<<<lblocks(nnz), kLThreads, 0, s>>>(cols, nnz, lo, n_local, h_below, gmap, deg_in, cols_rank);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 // Feature value (R#4): ((Philox(node, c/4, 0, 3; feat_seed).c%4 >> 8) - 2^23) * 2^-23, exact in fp32.
@@ -149,7 +149,7 @@ void launch_features(float* table, int64_t lo, int64_t n_rows, int32_t dim, int3
     if (n_rows < 1 || pitch < 4) return;
     k_features<<<lblocks(n_rows * (pitch / 4)), kLThreads, 0, s>>>(table, lo, n_rows, dim, pitch, (uint32_t)feat_seed,
                                                                    (uint32_t)(feat_seed >> 32));
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 }  // namespace mgnn

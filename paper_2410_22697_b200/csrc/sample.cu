@@ -98,13 +98,18 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
     const int64_t ntiles = (nF + T - 1) / T;
     int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
     // persistent: blocks claim tiles in order until the instance's frontier is exhausted
+    // lane groups for the draws: k lanes per node, floor(32/k) nodes per warp step (hop constants)
+    const int k = W.k_hop[hop];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int G = k;
+    const int per = 32 / G;
+    const int gi = lane / G, gl = lane - gi * G, gbase = gi * G;
     for (;;) {
         const int tile = claim_tile(sc.tilectr + m, &tslot);
         if (tile >= ntiles) {
             if (tile == 0 && threadIdx.x == 0) off[0] = 0;   // empty F_i
             break;
         }
-        const int k = W.k_hop[hop];
         const int64_t f = (int64_t)tile * T + threadIdx.x;
         const bool mine = threadIdx.x < T && f < nF;
         const int64_t h_below = pd.h_below, n_local = pd.n_local;
@@ -142,10 +147,6 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
         // Only CSR indices are produced here (no global loads), staged in shared memory.
         long long* sidx = reinterpret_cast<long long*>(dyn_smem);   // [T * k] CSR index of each sample of the tile
         const long long o_tile = prefix_sh;
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        const int G = k;                                   // one lane per slot; 32/k nodes per warp step
-        const int per = 32 / G;
-        const int gi = lane / G, gl = lane - gi * G, gbase = gi * G;
         const uint32_t c1 = (uint32_t)hop << 16;
         const uint32_t c3 = ((uint32_t)pd.part_id << 8) | kStreamSample;
         const uint32_t step = (uint32_t)(W.step0 + (uint64_t)w);
@@ -179,15 +180,34 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
         __syncthreads();
         // ---- phase B: every sample of the tile in parallel: neighbour rank, coalesced column write, and
         // the new-node mark unless the neighbour is already in F_i.
-        int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop] + o_tile;
-        const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
-        uint32_t* nb = W.nb + (int64_t)m * W.bm_words;
+        // B1: all neighbour ranks of the tile (independent loads) into shared memory, over sidx
+        int32_t* __restrict__ cols = W.cols[hop] + (int64_t)m * W.col_stride[hop] + o_tile;
+        const uint32_t* __restrict__ fb = W.fb + (int64_t)m * W.bm_words;
+        uint32_t* __restrict__ nb = W.nb + (int64_t)m * W.bm_words;
         const int32_t* __restrict__ crank = pd.cols_rank;
-    #pragma unroll 4
-        for (int e = threadIdx.x; e < (int)agg; e += kThreads) {
-            const int32_t c = crank[sidx[e]];
-            MGNN_CHECK(o_tile + e < W.col_stride[hop] && c < pd.vp, "cols o=%lld c=%d", o_tile + e, c);
-            cols[e] = c;
+        int32_t creg[8];
+        int nmine = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = threadIdx.x + u * kThreads;
+            if (e < (int)agg) creg[u] = crank[sidx[e]], nmine = u + 1;
+        }
+        for (int e = threadIdx.x + 8 * kThreads; e < (int)agg; e += kThreads) cols[e] = crank[sidx[e]];
+        __syncthreads();
+        // B2: coalesced column writes and new-node marks (fire-and-forget reductions)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (u < nmine) {
+                const int e = threadIdx.x + u * kThreads;
+                const int32_t c = creg[u];
+                MGNN_CHECK(o_tile + e < W.col_stride[hop] && c < pd.vp, "cols o=%lld c=%d", o_tile + e, c);
+                cols[e] = c;
+                const uint32_t bit = 1u << (c & 31);
+                if (!(fb[c >> 5] & bit)) atomicOr(&nb[c >> 5], bit);
+            }
+        }
+        for (int e = threadIdx.x + 8 * kThreads; e < (int)agg; e += kThreads) {
+            const int32_t c = cols[e];
             const uint32_t bit = 1u << (c & 31);
             if (!(fb[c >> 5] & bit)) atomicOr(&nb[c >> 5], bit);
         }
@@ -196,6 +216,7 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
 }
 
 // ------------------------------------------------------------------ bitmap -> sorted new frontier nodes
+// Persistent blocks: each claims the instance's word tiles in order until exhausted.
 __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch sc, int64_t tiles_max) {
     __shared__ long long sm[8];
     __shared__ int tslot;
@@ -204,36 +225,39 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
     const PartDev& pd = W.parts[m / W.n_steps];
     const int64_t nwords = (pd.vp + 31) >> 5;
     const int64_t ntiles = (nwords + kWordTile - 1) / kWordTile;
-    const int tile = claim_tile(sc.tilectr + m, &tslot);
-    if (tile >= ntiles) return;
-    uint32_t* nb = W.nb + (int64_t)m * W.bm_words;
-    uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
-    const int64_t wd = (int64_t)tile * kWordTile + threadIdx.x;
-    uint32_t b = (wd < nwords) ? nb[wd] : 0u;
-    long long agg;
-    const long long excl = block_excl_scan256(__popc(b), sm, &agg);
+    uint32_t* __restrict__ nb = W.nb + (int64_t)m * W.bm_words;
+    uint32_t* __restrict__ fb = W.fb + (int64_t)m * W.bm_words;
     int64_t* hs = W.hop_size + (int64_t)m * (kMaxLayers + 1);
-    if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
-                                                                     (unsigned long long)agg);
-    __syncthreads();
-    const int64_t nF = hs[hop];
-    int64_t pos = nF + prefix_sh + excl;
-    if (b) {
-        fb[wd] |= b;
-        nb[wd] = 0u;
+    int32_t* __restrict__ fr = W.fr_rank + (int64_t)m * W.ucap;
+    int32_t* __restrict__ posof = W.pos_of + (int64_t)m * W.vp_stride;
+    for (;;) {
+        const int tile = claim_tile(sc.tilectr + m, &tslot);
+        if (tile >= ntiles) break;
+        const int64_t wd = (int64_t)tile * kWordTile + threadIdx.x;
+        uint32_t b = (wd < nwords) ? nb[wd] : 0u;
+        long long agg;
+        const long long excl = block_excl_scan256(__popc(b), sm, &agg);
+        if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
+                                                                         (unsigned long long)agg);
+        __syncthreads();
+        const int64_t nF = hs[hop];
+        int64_t pos = nF + prefix_sh + excl;
+        if (b) {
+            fb[wd] |= b;
+            nb[wd] = 0u;
+        }
+        while (b) {
+            const int bi = __ffs(b) - 1;
+            b &= b - 1;
+            const int32_t r = (int32_t)(wd * 32 + bi);
+            MGNN_CHECK(pos < W.ucap && r < pd.vp, "compact pos=%lld r=%d", (long long)pos, r);
+            fr[pos] = r;
+            posof[r] = (int32_t)pos;
+            ++pos;
+        }
+        if (tile == ntiles - 1 && threadIdx.x == 0) hs[hop + 1] = nF + prefix_sh + agg;
+        __syncthreads();
     }
-    int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
-    int32_t* posof = W.pos_of + (int64_t)m * W.vp_stride;
-    while (b) {
-        const int bi = __ffs(b) - 1;
-        b &= b - 1;
-        const int32_t r = (int32_t)(wd * 32 + bi);
-        MGNN_CHECK(pos < W.ucap && r < pd.vp, "compact pos=%lld r=%d", (long long)pos, r);
-        fr[pos] = r;
-        posof[r] = (int32_t)pos;
-        ++pos;
-    }
-    if (tile == ntiles - 1 && threadIdx.x == 0) hs[hop + 1] = nF + prefix_sh + agg;
 }
 
 // ------------------------------------------------------------------ cols: rank -> position in F_{i+1}
@@ -254,7 +278,7 @@ __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
 void launch_seeds(const WinDev& w, cudaStream_t s) {
     dim3 grid(grid_x_for(w.batch, kThreads, w.n_inst), w.n_inst);
     k_seeds<<<grid, kThreads, 0, s>>>(w);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s) {
@@ -274,14 +298,17 @@ void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t
         attr_set = true;
     }
     k_hop<<<grid, kThreads, smem, s>>>(w, hop, sc, tiles_max < 1 ? 1 : tiles_max, T);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 void launch_compact(const WinDev& w, int hop, Scratch sc, cudaStream_t s) {
     const int64_t tiles = scan_tiles_words(w.bm_words);
-    dim3 grid((unsigned)(tiles < 1 ? 1 : tiles), w.n_inst);
+    int64_t gx = tiles;
+    const int64_t target = (148 * 6 + w.n_inst - 1) / w.n_inst;   // persistent: ~6 blocks per SM in total
+    if (gx > target) gx = target;
+    dim3 grid((unsigned)(gx < 1 ? 1 : gx), w.n_inst);
     k_compact<<<grid, kThreads, 0, s>>>(w, hop, sc, tiles < 1 ? 1 : tiles);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 void launch_relabel(const WinDev& w, cudaStream_t s) {
@@ -289,7 +316,7 @@ void launch_relabel(const WinDev& w, cudaStream_t s) {
     for (int i = 0; i < w.L; ++i) e_max = w.col_stride[i] > e_max ? w.col_stride[i] : e_max;
     dim3 grid(grid_x_for(e_max, kThreads, w.n_inst), w.n_inst);
     k_relabel<<<grid, kThreads, 0, s>>>(w);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 }  // namespace mgnn

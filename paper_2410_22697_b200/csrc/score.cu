@@ -51,7 +51,7 @@ void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, 
     if (cap_max < 1) return;
     dim3 grid(blocks_for(cap_max, kSThreads), n_lp);
     k_decay<<<grid, kSThreads, 0, s>>>(parts, n_steps, gamma);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 // ------------------------------------------------------------------ candidate selection
@@ -127,7 +127,7 @@ void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, f
     if (tiles < 1) tiles = 1;
     dim3 grid((unsigned)tiles, 2 * n_lp);
     k_select<<<grid, kSThreads, 0, s>>>(parts, alpha, theta_r, segs, n_out, sc, tiles, ev);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 // ------------------------------------------------------------------ candidates: key >> 52 <= T
@@ -227,7 +227,7 @@ void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev
     k_cand<<<g1, kSThreads, 0, s>>>(segs, ev);
     dim3 g2((unsigned)((n_max + kSThreads - 1) / kSThreads), 2 * n_lp);
     k_rank<<<g2, kSThreads, 0, s>>>(segs, ev);
-    count_launches(2, __func__);
+    count_launches(2, __func__, s);
 }
 
 // ------------------------------------------------------------------ swap + refill
@@ -281,7 +281,7 @@ void launch_swap_refill(const PartDev* parts, int n_lp, int64_t cap_max, const S
                         long long* counts, int64_t counts_stride, int n_steps, cudaStream_t s) {
     dim3 grid(blocks_for(cap_max < 1 ? 1 : cap_max, kSThreads / 32), n_lp);
     k_swap_refill<<<grid, kSThreads, 0, s>>>(parts, segs, world, counts, counts_stride, n_steps);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 // ------------------------------------------------------------------ INITIALIZE_PREFETCHER
@@ -298,7 +298,7 @@ __global__ void k_init_keys(const PartDev* __restrict__ pdp, const SortSeg* __re
 
 void launch_init_keys(const PartDev* pd_dev, int64_t n_h, const SortSeg* seg, long long* n_dev, cudaStream_t s) {
     k_init_keys<<<blocks_for(n_h < 1 ? 1 : n_h, kSThreads), kSThreads, 0, s>>>(pd_dev, seg, n_dev);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 // S_A = 0 for every halo node and rank_deg[order[i]] = i; then for the top-cap: slot s <- order[s],
@@ -327,7 +327,7 @@ __global__ void k_init_slots(const PartDev* __restrict__ pdp, const uint32_t* __
 void launch_init_fill(const PartDev* pd_dev, int64_t n_h, int64_t cap, const uint32_t* order, cudaStream_t s) {
     k_init_reset<<<blocks_for(n_h < 1 ? 1 : n_h, kSThreads), kSThreads, 0, s>>>(pd_dev, order);
     k_init_slots<<<blocks_for(cap < 1 ? 1 : cap, kSThreads), kSThreads, 0, s>>>(pd_dev, order);
-    count_launches(2, __func__);
+    count_launches(2, __func__, s);
 }
 
 // BUF rows of every slot from the owners' tables (the init "RPC").
@@ -349,7 +349,7 @@ __global__ void k_rows_from_owners(const PartDev* __restrict__ pdp, WorldDev G) 
 void launch_rows_from_owners(const PartDev* pd_dev, int64_t cap, const WorldDev& world, cudaStream_t s) {
     if (cap < 1) return;
     k_rows_from_owners<<<blocks_for(cap, kSThreads / 32), kSThreads, 0, s>>>(pd_dev, world);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 // ------------------------------------------------------------------ epoch order keys (R#8)
@@ -373,7 +373,7 @@ void launch_perm_keys(const PartDev* pd_dev, int64_t n_train, uint64_t epoch0, i
     const int64_t total = n_train * n_epochs;
     k_perm_keys<<<blocks_for(total < 1 ? 1 : total, kSThreads), kSThreads, 0, s>>>(pd_dev, epoch0, n_epochs, seed_lo,
                                                                                    seed_hi, segs);
-    count_launches(1, __func__);
+    count_launches(1, __func__, s);
 }
 
 }  // namespace mgnn

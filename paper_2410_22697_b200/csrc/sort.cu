@@ -200,7 +200,7 @@ void radix_sort_pairs(const SortSeg* segs_dev, int n_seg, int64_t n_max, int max
     k_sort_hist<<<grid, kSortThreads, 0, s>>>(segs_dev, passes, scr);
     k_sort_binscan<<<dim3(1, n_seg), kSortThreads, 0, s>>>(passes, scr);
     for (int p = 0; p < passes; ++p) k_sort_pass<<<grid, kSortThreads, 0, s>>>(segs_dev, passes, p, tiles, scr);
-    count_launches(2 + passes, __func__);
+    count_launches(2 + passes, __func__, s);
 }
 
 }  // namespace mgnn

@@ -36,7 +36,7 @@ def assert_bits_equal(a, b, what):
 def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, gamma: float, delta: int,
                theta_r: float, windows, run_seed: int = synth.RUN_SEED, feat_seed: int = synth.FEAT_SEED,
                alpha=None, hosted=None, sample_every: int = 1, check_x_rows: int = 0, ext_seeds=None,
-               device: int = 0):
+               device: int = 0, exchange: bool = False):
     """windows: list of window lengths run back to back from step 1."""
     from paper_2410_22697_b200 import pipeline as PL
 
@@ -47,6 +47,8 @@ def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, g
     for p in W.parts:
         p.buffer_init(gamma, alpha, theta_r, delta, f_bp)
     ctx = PL.build_context(device, parts, D, feat_seed, hosted)
+    if exchange:                      # multi-process: map the other ranks' tables (CUDA IPC, NVLink)
+        PL.exchange_tables(ctx)
     ctx.buffer_init(gamma, alpha, theta_r, delta, f_bp)
     ctx.sampler_config(fanouts, batch, run_seed, max(windows))
     lps = {pid: lp for lp, pid in enumerate(ctx.parts)}
@@ -121,6 +123,11 @@ def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, g
             assert_bits_equal(gs["rows"], os_["rows"], f"BUF rows p{pid} after t{t + wlen - 1}")
         t += wlen
         slot ^= 1
+    if exchange:                      # peers may still read our tables until every rank is done
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize()
+        dist.barrier()
     ctx.close()
     W.close()
     return stats

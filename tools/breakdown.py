@@ -36,7 +36,12 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     t, slot = 1, 0
     acc = {"sample": [], "gather": [], "score": []}
+    import ctypes
+    from paper_2410_22697_b200 import _lib
+    L = _lib.load()
     for i in range(a.windows + 3):
+        if i == 3:
+            L.mgnn_profile_kernels(1, None, 0)
         flush.zero_()
         e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         e[0].record(s)
@@ -53,8 +58,12 @@ def main():
             acc["score"].append(e[2].elapsed_time(e[3]))
         t += W
         slot ^= 1
+    buf = ctypes.create_string_buffer(1 << 16)
+    L.mgnn_profile_kernels(0, buf, len(buf))
     for k, v in acc.items():
         print(f"{k:8s} mean {1e3 * sum(v) / len(v):8.1f} us   min {1e3 * min(v):8.1f} us")
+    print(f"per launcher over {a.windows} windows (time since the previous launcher on the stream):")
+    print(buf.value.decode())
 
 
 if __name__ == "__main__" and "--timeline" not in sys.argv:
