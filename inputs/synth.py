@@ -110,6 +110,12 @@ def _raw_edges(rng: np.random.Generator, m: int, n: int, mu: float):
     return u, v
 
 
+def _unique_sorted(x: np.ndarray) -> np.ndarray:
+    """Sorted unique int64 keys (torch's multithreaded CPU sort; identical result to np.unique)."""
+    import torch
+    return torch.unique(torch.from_numpy(x), sorted=True).numpy()
+
+
 def generate(cfg: GraphConfig, cache_dir: Optional[str] = "/tmp/mgnn_inputs") -> Graph:
     """Deterministic planted-block R-MAT graph for `cfg` (see module doc)."""
     key = hashlib.sha1(repr(dataclasses.astuple(cfg)).encode() + b"v2").hexdigest()[:12]
@@ -144,7 +150,7 @@ def generate(cfg: GraphConfig, cache_dir: Optional[str] = "/tmp/mgnn_inputs") ->
             parts.append(u * n + v)
             parts.append(v * n + u)
             left -= c
-        new_keys = np.unique(np.concatenate(parts))
+        new_keys = _unique_sorted(np.concatenate(parts))
         gained = new_keys.shape[0] - keys.shape[0]
         keys = new_keys
         if keys.shape[0] >= 0.98 * target or gained <= 0:

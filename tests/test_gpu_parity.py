@@ -94,3 +94,23 @@ def test_cfg1_full_sort_eviction_path(cfg1, monkeypatch, wins):
     monkeypatch.setenv("MGNN_EVICT_SORT", "1")
     st = run_parity(cfg1, 2, 64, [10, 25], 256, 2500, 0.9, wins[0], 1.0, wins)
     assert st["evicted"] > 0
+
+
+@pytest.mark.slow
+def test_reddit_full_size_wide_rows():
+    """configs[2] at full size: 602-dim features (pitch 604, the multi-chunk row path), ~113M edges,
+    P=2 with the paper's GPU optimum for 2 partitions (f=0.35, gamma=0.995, Delta=32)."""
+    g = synth.generate(synth.CONFIGS["reddit"])
+    st = run_parity(g, 2, 602, [10, 25], 1000, 3500, 0.995, 8, 1.0, [8, 8, 8], sample_every=5,
+                    check_x_rows=2048)
+    assert st["misses"] > 0 and st["evicted"] > 0
+
+
+@pytest.mark.slow
+def test_products_full_size_three_hops():
+    """configs[3] at full size: 2.45M nodes, ~123M edges, 100-dim rows (25 float4 per row, the narrow
+    path), fanout [5,10,15] (three hops), batch 2000, P=2 (f=0.5, gamma=0.995, Delta=32)."""
+    g = synth.generate(synth.CONFIGS["products"])
+    st = run_parity(g, 2, 100, [5, 10, 15], 2000, 5000, 0.995, 8, 1.0, [8, 8, 8], sample_every=5,
+                    check_x_rows=2048)
+    assert st["misses"] > 0 and st["evicted"] > 0
