@@ -59,6 +59,9 @@ CONFIGS = {
     "reddit": GraphConfig("reddit", 232_965, 114_615_892, 602, 0.05, 0.659, [10, 25], 1000),
     "products": GraphConfig("products", 2_449_029, 2 * 61_859_140, 100, 0.2, 0.080, [5, 10, 15], 2000),
     "papers": GraphConfig("papers", 111_059_956, 2 * 1_615_685_872, 128, 0.15, 0.0109, [5, 10, 15], 2000),
+    # 1/32-scale papers100M shape (same degree, dims, train fraction, fanout) for routine parity runs
+    "papers_s32": GraphConfig("papers_s32", 111_059_956 // 32, 2 * 1_615_685_872 // 32, 128, 0.15, 0.0109,
+                              [5, 10, 15], 2000),
 }
 
 

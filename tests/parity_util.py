@@ -84,9 +84,18 @@ def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, g
                 op = W.parts[pid]
                 op.step(run_seed, step, fanouts, batch,
                         seeds=None if ext_seeds is None else np.asarray(ext_seeds(pid, step), np.int32))
+                m = lp * wlen + w
+                oc = op.counts()
+                gc = counts[m]
+                got = [gc[0], gc[1], gc[2], gc[3], gc[4], gc[6]]
+                want = [oc["n_nodes"], oc["n_local"], oc["n_hit"], oc["n_miss"], oc["n_evicted"], oc["rows_fetched"]]
+                assert got == want, (pid, step, got, want)      # counts: every step
+                stats["steps"] += 1
+                stats["hits"] += oc["n_hit"]
+                stats["misses"] += oc["n_miss"]
+                stats["evicted"] += oc["n_evicted"]
                 if (step - 1) % sample_every:
                     continue
-                m = lp * wlen + w
                 inst = ctx.instance(slot, m, with_x=True)
                 hs = op.hop_sizes()
                 assert_bits_equal(inst["hop_size"], np.array(hs, np.int64), f"hop sizes p{pid} t{step}")
@@ -104,15 +113,6 @@ def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, g
                     assert_bits_equal(inst["X"][sel], X[sel], f"X p{pid} t{step}")
                 else:
                     assert_bits_equal(inst["X"], X, f"X p{pid} t{step}")
-                oc = op.counts()
-                gc = counts[m]
-                got = [gc[0], gc[1], gc[2], gc[3], gc[4], gc[6]]
-                want = [oc["n_nodes"], oc["n_local"], oc["n_hit"], oc["n_miss"], oc["n_evicted"], oc["rows_fetched"]]
-                assert got == want, (pid, step, got, want)
-                stats["steps"] += 1
-                stats["hits"] += oc["n_hit"]
-                stats["misses"] += oc["n_miss"]
-                stats["evicted"] += oc["n_evicted"]
         for pid, lp in lps.items():
             gs = ctx.snapshot(lp, rows=True)
             os_ = W.parts[pid].buffer_state(rows=True)

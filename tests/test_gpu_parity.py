@@ -3,6 +3,8 @@
 Every comparison is element by element on the same seeded inputs; scores
 are compared as fp32 bit patterns (0 ULP, BASELINE.json north_star).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -114,3 +116,24 @@ def test_products_full_size_three_hops():
     st = run_parity(g, 2, 100, [5, 10, 15], 2000, 5000, 0.995, 8, 1.0, [8, 8, 8], sample_every=5,
                     check_x_rows=2048)
     assert st["misses"] > 0 and st["evicted"] > 0
+
+
+@pytest.mark.slow
+def test_papers_shape_eight_partitions_one_gpu():
+    """configs[4] shape at 1/32 scale (3.47M nodes, ~101M edges, 128-d, [5,10,15], batch 2000)
+    across 8 partitions hosted by ONE context (8 trainers per GPU), the paper's papers setting
+    (f=0.5, gamma=0.9995) with a short Delta so that rounds occur."""
+    g = synth.generate(synth.CONFIGS["papers_s32"])
+    st = run_parity(g, 8, 128, [5, 10, 15], 2000, 5000, 0.99, 4, 1.0, [4, 4, 4], sample_every=3,
+                    check_x_rows=1024)
+    assert st["misses"] > 0 and st["evicted"] > 0
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(os.environ.get("MGNN_PAPERS_FULL") != "1", reason="set MGNN_PAPERS_FULL=1 (~15 min, ~150 GB)")
+def test_papers_full_size_eight_partitions():
+    """configs[4] at full size: 111M nodes, ~3.23B directed edges, 8 partitions on one GPU."""
+    g = synth.generate(synth.CONFIGS["papers"])
+    st = run_parity(g, 8, 128, [5, 10, 15], 2000, 5000, 0.9995, 4, 1.0, [4, 4], sample_every=4,
+                    check_x_rows=512)
+    assert st["misses"] > 0
