@@ -644,7 +644,8 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
         const size_t nseg = 2 * (size_t)n_lp;
         const size_t o_st = up(nseg * 4);
         const size_t o_hist = o_st + up(nseg * ctx->ev_tiles * 8);
-        const size_t o_tk = o_hist + up(nseg * 4096 * 4);
+        const size_t o_hist2 = o_hist + up(nseg * 4096 * 4);
+        const size_t o_tk = o_hist2 + up(nseg * 4096 * 4);
         const size_t o_thr = o_tk + 256;
         const size_t o_nc = o_thr + up(nseg * 16);
         ctx->ev_zero_bytes = o_nc + up(nseg * 8);
@@ -652,6 +653,7 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
         ctx->ev_sc.tilectr = (int32_t*)ctx->ev_zero;
         ctx->ev_sc.status = (unsigned long long*)(ctx->ev_zero + o_st);
         ctx->ev_ev.hist = (uint32_t*)(ctx->ev_zero + o_hist);
+        ctx->ev_ev.hist2 = (uint32_t*)(ctx->ev_zero + o_hist2);
         ctx->ev_ev.ticket = (unsigned*)(ctx->ev_zero + o_tk);
         ctx->ev_ev.thr = (long long*)(ctx->ev_zero + o_thr);
         ctx->ev_ev.n_cand = (unsigned long long*)(ctx->ev_zero + o_nc);

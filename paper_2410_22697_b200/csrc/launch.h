@@ -75,6 +75,7 @@ struct Scratch {          // zeroed look-back status words + tile counters
 
 struct EvScratch {        // eviction-round scratch, zeroed per round
     uint32_t* hist;                 // [2*n_lp][4096] histogram of key >> 52
+    uint32_t* hist2;                // [2*n_lp][4096] bits [40,52) inside the threshold bucket
     unsigned* ticket;               // last-block detection of k_select
     long long* thr;                 // [2*n_lp][2] = {K, threshold digit T (-1: none)}
     unsigned long long* n_cand;     // [2*n_lp] candidates appended by k_cand

@@ -130,38 +130,85 @@ void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, f
     count_launches(1, __func__, s);
 }
 
-// ------------------------------------------------------------------ candidates: key >> 52 <= T
-// Every block derives K = min(|E|, |R|) of its partition and the threshold digit T of its list
-// (smallest T with #(digit <= T) >= K) from the histogram; block 0 records {K, T} for k_rank.
-__global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ segs, EvScratch ev) {
+// ------------------------------------------------------------------ candidates
+// Smallest digit T with #(digit <= T) >= need (T = -1 if need <= 0); *below = #(digit < T).
+// Block-wide (256 threads, 16 digits each); every block of the launch derives the same answer.
+__device__ __forceinline__ void find_threshold(const uint32_t* __restrict__ hist, long long need, long long* sm,
+                                               long long* T_sh, long long* below_sh) {
+    constexpr int per = kDig / kSThreads;
+    long long local = 0;
+    for (int j = 0; j < per; ++j) local += hist[threadIdx.x * per + j];
+    long long tot;
+    long long run = block_excl_scan256(local, sm, &tot);
+    if (threadIdx.x == 0) {
+        *T_sh = -1;
+        *below_sh = 0;
+    }
+    __syncthreads();
+    if (need > 0 && run < need && need <= run + local) {
+        for (int j = 0; j < per; ++j) {
+            const long long c = hist[threadIdx.x * per + j];
+            if (run + c >= need) {
+                *T_sh = threadIdx.x * per + j;
+                *below_sh = run;
+                break;
+            }
+            run += c;
+        }
+    }
+    __syncthreads();
+}
+
+constexpr long long kCandMax = 4096;   // refine the threshold with the next 12 key bits above this
+
+// Second-level histogram (key bits [40, 52)) of the threshold bucket, only when the first level
+// would leave more than kCandMax candidates (e.g. many equal scores in an early round).
+__global__ void __launch_bounds__(kSThreads) k_hist2(const SortSeg* __restrict__ segs, EvScratch ev) {
     __shared__ long long sm[8];
-    __shared__ long long T_sh;
+    __shared__ long long T_sh, below_sh;
     const int sg = blockIdx.y;
     const SortSeg S = segs[sg];
     const long long n = *S.n;
     const long long nE = *segs[sg & ~1].n, nR = *segs[sg | 1].n;
     const long long K = nE < nR ? nE : nR;
-    {
-        const uint32_t* hist = ev.hist + (size_t)sg * kDig;
-        constexpr int per = kDig / kSThreads;
-        long long local = 0;
-        for (int j = 0; j < per; ++j) local += hist[threadIdx.x * per + j];
-        long long tot;
-        long long run = block_excl_scan256(local, sm, &tot);
-        if (threadIdx.x == 0) T_sh = -1;
-        __syncthreads();
-        if (K > 0 && run < K && K <= run + local) {
-            for (int j = 0; j < per; ++j) {
-                run += hist[threadIdx.x * per + j];
-                if (run >= K) {
-                    T_sh = threadIdx.x * per + j;
-                    break;
-                }
-            }
-        }
-        __syncthreads();
-    }
+    const uint32_t* hist = ev.hist + (size_t)sg * kDig;
+    find_threshold(hist, K, sm, &T_sh, &below_sh);
     const long long T = T_sh;
+    if (T < 0 || below_sh + (long long)hist[T] <= kCandMax) return;
+    uint32_t* hist2 = ev.hist2 + (size_t)sg * kDig;
+    const int lane = threadIdx.x & 31;
+    const long long stride = (long long)gridDim.x * kSThreads;
+    for (long long i0 = (long long)blockIdx.x * kSThreads + (threadIdx.x & ~31); i0 < n; i0 += stride) {
+        const long long i = i0 + lane;
+        unsigned d = 0xFFFFFFFFu;
+        if (i < n) {
+            const unsigned long long k = S.keys[i];
+            if ((long long)(k >> 52) == T) d = (unsigned)(k >> 40) & 0xFFFu;
+        }
+        const unsigned peers = __match_any_sync(kFull, d);
+        if (d != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist2[d], (unsigned)__popc(peers));
+    }
+}
+
+// Every block derives K = min(|E|, |R|) of its partition and the threshold(s) of its list from the
+// histograms; block 0 records {K, T} for k_rank.
+__global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ segs, EvScratch ev) {
+    __shared__ long long sm[8];
+    __shared__ long long T_sh, below_sh, T2_sh, below2_sh;
+    const int sg = blockIdx.y;
+    const SortSeg S = segs[sg];
+    const long long n = *S.n;
+    const long long nE = *segs[sg & ~1].n, nR = *segs[sg | 1].n;
+    const long long K = nE < nR ? nE : nR;
+    const uint32_t* hist = ev.hist + (size_t)sg * kDig;
+    find_threshold(hist, K, sm, &T_sh, &below_sh);
+    const long long T = T_sh;
+    const bool refined = T >= 0 && below_sh + (long long)hist[T] > kCandMax;
+    long long T2 = 0xFFF;
+    if (refined) {
+        find_threshold(ev.hist2 + (size_t)sg * kDig, K - below_sh, sm, &T2_sh, &below2_sh);
+        T2 = T2_sh;
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ev.thr[2 * sg] = K;
         ev.thr[2 * sg + 1] = T;
@@ -175,7 +222,8 @@ __global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ 
         bool c = false;
         if (i < n) {
             k = S.keys[i];
-            c = (long long)(k >> 52) <= T;
+            const long long d1 = (long long)(k >> 52);
+            c = d1 < T || (d1 == T && (long long)((k >> 40) & 0xFFF) <= T2);
         }
         const unsigned ball = __ballot_sync(kFull, c);
         if (!ball) continue;
@@ -224,10 +272,11 @@ __global__ void __launch_bounds__(kSThreads) k_rank(const SortSeg* __restrict__ 
 
 void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, cudaStream_t s) {
     dim3 g1(blocks_for(n_max, kSThreads) > 64 ? 64 : blocks_for(n_max, kSThreads), 2 * n_lp);
+    k_hist2<<<g1, kSThreads, 0, s>>>(segs, ev);
     k_cand<<<g1, kSThreads, 0, s>>>(segs, ev);
     dim3 g2((unsigned)((n_max + kSThreads - 1) / kSThreads), 2 * n_lp);
     k_rank<<<g2, kSThreads, 0, s>>>(segs, ev);
-    count_launches(2, __func__, s);
+    count_launches(3, __func__, s);
 }
 
 // ------------------------------------------------------------------ swap + refill

@@ -1,0 +1,157 @@
+"""C-ABI contract on the GPU (include/mgnn.h): status codes, call order, sticky errors,
+zero-copy views and the per-launcher profile (-m gpu)."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from inputs import synth
+from oracle import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2410_22697_b200 import _lib  # noqa: E402
+from paper_2410_22697_b200 import pipeline as PL  # noqa: E402
+from paper_2410_22697_b200._lib import MgnnError  # noqa: E402
+
+EINVAL, ESTATE = 1, 5
+
+
+@pytest.fixture(scope="module")
+def graph():
+    return synth.generate(synth.CONFIGS["cfg1"])
+
+
+def _ctx(graph, hosted=None, init=True, window=4, delta=4):
+    parts = synth.partition(graph, 2)
+    ctx = PL.build_context(0, parts, 64, synth.FEAT_SEED, hosted)
+    if init:
+        ctx.buffer_init(0.9, PL.alpha_default(0.9, delta), 1.0, delta, 2500)
+        ctx.sampler_config([10, 25], 256, synth.RUN_SEED, window)
+    return ctx
+
+
+def _status(excinfo):
+    return excinfo.value.status
+
+
+def test_call_order(graph):
+    ctx = _ctx(graph, init=False)
+    with pytest.raises(MgnnError) as e:
+        ctx.sample(0, 1, 1)                          # before buffer_init / sampler_config
+    assert _status(e) == ESTATE
+    ctx.buffer_init(0.9, 0.5, 1.0, 4, 2500)
+    ctx.sampler_config([10, 25], 256, synth.RUN_SEED, 4)
+    with pytest.raises(MgnnError) as e:
+        ctx.lookup_gather(0)                         # gather before sample
+    assert _status(e) == ESTATE
+    ctx.sample(0, 1, 4)
+    with pytest.raises(MgnnError) as e:
+        ctx.score(0)                                 # score before gather
+    assert _status(e) == ESTATE
+    ctx.lookup_gather(0)
+    ctx.sample(1, 9, 4)                              # skips steps 5..8
+    with pytest.raises(MgnnError) as e:
+        ctx.lookup_gather(1)                         # previous window not scored
+    assert _status(e) == ESTATE
+    ctx.score(0)
+    with pytest.raises(MgnnError) as e:
+        ctx.lookup_gather(1)                         # windows must be gathered in step order
+    assert _status(e) == ESTATE
+    ctx.close()
+
+
+def test_invalid_arguments_leave_state(graph):
+    ctx = _ctx(graph)
+    for bad in (dict(slot=2, t0=1, n=4), dict(slot=0, t0=0, n=4), dict(slot=0, t0=1, n=5),
+                dict(slot=0, t0=3, n=3)):            # t=4 (eviction) inside [3, 5]
+        with pytest.raises(MgnnError) as e:
+            ctx.sample(bad["slot"], bad["t0"], bad["n"])
+        assert _status(e) == EINVAL
+    for pol in ((0.0, 0.5, 1.0, 4, 2500), (1.5, 0.5, 1.0, 4, 2500), (0.9, -1.0, 1.0, 4, 2500),
+                (0.9, 0.5, 1.0, -1, 2500), (0.9, 0.5, 1.0, 4, 10001), (0.9, float("nan"), 1.0, 4, 2500)):
+        with pytest.raises(MgnnError) as e:
+            ctx.buffer_init(*pol)
+        assert _status(e) == EINVAL
+    with pytest.raises(MgnnError) as e:
+        ctx.sampler_config([10, 33], 256, 1, 4)      # fanout > 32
+    assert _status(e) == EINVAL
+    # the context is still usable
+    ctx.sample(0, 1, 4)
+    ctx.lookup_gather(0)
+    ctx.score(0)
+    assert ctx.counts(0).shape == (8, 8)
+    ctx.close()
+
+
+def test_partition_validation(graph):
+    parts = synth.partition(graph, 2)
+    ctx = PL.Context(0, parts[0].bounds, 64, synth.FEAT_SEED)
+    p = parts[0]
+    bad_cols = p.cols.copy()
+    r = int(np.argmax(np.diff(p.indptr) >= 2))
+    a, b = int(p.indptr[r]), int(p.indptr[r] + 1)
+    bad_cols[a], bad_cols[b] = bad_cols[b], bad_cols[a]      # row not ascending
+    with pytest.raises(MgnnError) as e:
+        ctx.load_partition(0, p.indptr, bad_cols, p.train_ids)
+    assert _status(e) == EINVAL
+    with pytest.raises(MgnnError) as e:
+        ctx.load_partition(0, p.indptr, p.cols, p.train_ids[::-1].copy())   # unsorted train ids
+    assert _status(e) == EINVAL
+    ctx.load_partition(0, p.indptr, p.cols, p.train_ids)
+    with pytest.raises(MgnnError) as e:
+        ctx.load_partition(0, p.indptr, p.cols, p.train_ids)                # loaded twice
+    assert _status(e) == EINVAL
+    with pytest.raises(MgnnError) as e:
+        ctx.buffer_init(0.9, 0.5, 1.0, 4, 2500)       # partition 1's table neither hosted nor imported
+    assert _status(e) == ESTATE
+    ctx.close()
+
+
+def test_bad_external_seeds_are_reported(graph):
+    ctx = _ctx(graph)
+    seeds = np.zeros((2, 4, 256), np.int32)
+    counts = np.full((2, 4), 2, np.int32)
+    seeds[:, :, 0] = 7
+    seeds[:, :, 1] = 7                                # duplicate seed
+    seeds[1, :, :2] += 5000                           # partition 1 owns [5000, 10000)
+    ctx.sample(0, 1, 4, seeds=seeds, seed_counts=counts)
+    with pytest.raises(MgnnError) as e:
+        ctx.counts(0)
+    assert _status(e) == EINVAL
+    with pytest.raises(MgnnError):                    # sticky
+        ctx.sample(1, 5, 4)
+    ctx.close()
+
+
+def test_zero_copy_views_match_instance(graph):
+    ctx = _ctx(graph)
+    ctx.sample(0, 1, 4)
+    ctx.lookup_gather(0)
+    ctx.score(0)
+    torch.cuda.synchronize()
+    w = ctx.window(0)
+    assert w.n_inst == 8 and w.n_steps == 4 and w.pitch == 64
+    X = PL.device_view(w.X, (w.n_inst, w.rows_stride, w.pitch), "f4")
+    inst = ctx.instance(0, 3)
+    U = int(inst["hop_size"][-1])
+    assert torch.equal(X[3, :U, :64].cpu(), torch.from_numpy(inst["X"]))
+    F = inst["frontier"]
+    for i in range(0, U, 97):
+        assert np.array_equal(inst["X"][i], O.feature_row(int(F[i]), 64, synth.FEAT_SEED))
+    ctx.close()
+
+
+def test_kernel_profile_and_launch_count(graph):
+    L = _lib.load()
+    ctx = _ctx(graph)
+    n0 = ctx.launch_count()
+    L.mgnn_profile_kernels(1, None, 0)
+    ctx.prepare(0, 1, 4)
+    buf = ctypes.create_string_buffer(1 << 14)
+    L.mgnn_profile_kernels(0, buf, len(buf))
+    report = buf.value.decode()
+    assert "launch_gather" in report and "launch_hop" in report
+    assert ctx.launch_count() - n0 >= 8
+    ctx.close()
