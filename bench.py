@@ -152,7 +152,6 @@ def run_reference(args):
     parts = synth.partition(g, P)
     # each reference "step" = the same 32 x (partitions on one GPU) minibatches, bounded by time
     per_step = WINDOW * PARTS_PER_GPU
-    _, _, _ = oracle_rate(parts, P, f_bp, gamma, delta, 0.0, min_steps=max(1, args.warmup))
     from oracle import oracle as O
     W = O.World(parts, CFG.feat_dim, synth.FEAT_SEED)
     alpha = O.alpha_default(gamma, delta)

@@ -6,7 +6,8 @@
 // one launch per stage serves W steps x P_local partitions.
 //
 // Per hop i (K1/K2):
-//   k_hop     : thread per frontier node x of F_i (a tile of 256 per block):
+//   k_hop     : (hop 0 first writes F_0 = the step's seeds, R#8)
+//               thread per frontier node x of F_i (a tile of 64/256 per block):
 //               count min(deg, k_i) (halo nodes: 0, R#1), exclusive offsets by
 //               a block scan + decoupled look-back across tiles; then groups
 //               of G = pow2 >= k_i lanes take the tile's nodes 32/G per warp
@@ -41,48 +42,6 @@ static inline unsigned grid_x_for(int64_t items_per_inst, int items_per_block, i
     return (unsigned)(g < 1 ? 1 : g);
 }
 
-// ------------------------------------------------------------------ seeds: F_0 (R#8)
-__global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
-    const int m = blockIdx.y;
-    const int lp = m / W.n_steps, w = m % W.n_steps;
-    const PartDev& pd = W.parts[lp];
-    const uint64_t t = W.step0 + (uint64_t)w;
-    const int32_t* src;
-    int64_t n0;
-    if (W.ext_seeds) {
-        src = W.ext_seeds + (int64_t)m * W.batch;
-        n0 = W.ext_counts[m];
-        if (n0 < 1 || n0 > W.batch) {
-            if (threadIdx.x == 0 && blockIdx.x == 0) atomicOr(W.err, 1);
-            n0 = 0;
-        }
-    } else {
-        const int64_t e = (int64_t)((t - 1) / (uint64_t)pd.nbatch), b = (int64_t)((t - 1) % (uint64_t)pd.nbatch);
-        const int32_t* perm = pd.perm + (int64_t)(e % pd.perm_slots) * pd.n_train;
-        const int64_t s0 = b * W.batch;
-        n0 = pd.n_train - s0 < W.batch ? pd.n_train - s0 : W.batch;
-        src = perm + s0;
-    }
-    int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
-    int32_t* pos = W.pos_of + (int64_t)m * W.vp_stride;
-    uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n0; j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t gid = src[j];
-        int64_t row = gid - pd.lo;
-        if (row < 0 || row >= pd.n_local) {      // external seed not owned by this partition
-            atomicOr(W.err, 1);
-            row = 0;
-        }
-        const int32_t r = (int32_t)(pd.h_below + row);
-        fr[j] = r;
-        W.fr_gid[(int64_t)m * W.ucap + j] = (int32_t)gid;   // F_0 readable right after sampling
-        pos[r] = (int32_t)j;
-        const uint32_t bit = 1u << (r & 31);
-        if (atomicOr(&fb[r >> 5], bit) & bit) atomicOr(W.err, 2);   // duplicate seed
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) W.hop_size[(int64_t)m * (kMaxLayers + 1)] = n0;
-}
-
 // ------------------------------------------------------------------ one hop: counts, offsets, samples
 // T = frontier nodes per tile (64 or 256; small tiles give small hops enough blocks).
 __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max, int T) {
@@ -94,7 +53,28 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
     const int m = blockIdx.y;
     const int lp = m / W.n_steps, w = m % W.n_steps;
     const PartDev& pd = W.parts[lp];
-    const int64_t nF = W.hop_size[(int64_t)m * (kMaxLayers + 1) + hop];
+    // hop 0 also materialises F_0 = the step's seeds (R#8): epoch-order slice or external seeds
+    const int32_t* seed_src = nullptr;
+    int64_t nF;
+    if (hop == 0) {
+        if (W.ext_seeds) {
+            seed_src = W.ext_seeds + (int64_t)m * W.batch;
+            nF = W.ext_counts[m];
+            if (nF < 1 || nF > W.batch) {
+                if (threadIdx.x == 0 && blockIdx.x == 0) atomicOr(W.err, 1);
+                nF = 0;
+            }
+        } else {
+            const uint64_t t = W.step0 + (uint64_t)w;
+            const int64_t e = (int64_t)((t - 1) / (uint64_t)pd.nbatch), b = (int64_t)((t - 1) % (uint64_t)pd.nbatch);
+            const int64_t s0 = b * W.batch;
+            seed_src = pd.perm + (int64_t)(e % pd.perm_slots) * pd.n_train + s0;
+            nF = pd.n_train - s0 < W.batch ? pd.n_train - s0 : W.batch;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) W.hop_size[(int64_t)m * (kMaxLayers + 1)] = nF;
+    } else {
+        nF = W.hop_size[(int64_t)m * (kMaxLayers + 1) + hop];
+    }
     const int64_t ntiles = (nF + T - 1) / T;
     int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
     // persistent: blocks claim tiles in order until the instance's frontier is exhausted
@@ -114,7 +94,22 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
         const bool mine = threadIdx.x < T && f < nF;
         const int64_t h_below = pd.h_below, n_local = pd.n_local;
         int64_t row = -1, b0 = 0, d = 0;
-        if (mine) {
+        if (mine && hop == 0) {                            // seed: local rank, frontier bitmap, position
+            const int64_t gid = seed_src[f];
+            row = gid - pd.lo;
+            if (row < 0 || row >= n_local) {               // external seed not owned by this partition
+                atomicOr(W.err, 1);
+                row = 0;
+            }
+            const int32_t r = (int32_t)(h_below + row);
+            W.fr_rank[(int64_t)m * W.ucap + f] = r;
+            W.fr_gid[(int64_t)m * W.ucap + f] = (int32_t)gid;
+            W.pos_of[(int64_t)m * W.vp_stride + r] = (int32_t)f;
+            const uint32_t bit = 1u << (r & 31);
+            if (atomicOr(&W.fb[(int64_t)m * W.bm_words + (r >> 5)], bit) & bit) atomicOr(W.err, 2);   // duplicate
+            b0 = pd.indptr[row];
+            d = pd.indptr[row + 1] - b0;
+        } else if (mine) {
             row = (int64_t)W.fr_rank[(int64_t)m * W.ucap + f] - h_below;
             if (row >= 0 && row < n_local) {               // halo frontier nodes are leaves (R#1)
                 b0 = pd.indptr[row];
@@ -234,7 +229,10 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
         const int tile = claim_tile(sc.tilectr + m, &tslot);
         if (tile >= ntiles) break;
         const int64_t wd = (int64_t)tile * kWordTile + threadIdx.x;
-        uint32_t b = (wd < nwords) ? nb[wd] : 0u;
+        // new nodes = marked and not already in F_i (a seed may be marked by a sample drawn
+        // before its own frontier bit was set in the fused seed/hop-0 kernel)
+        const uint32_t nbw = (wd < nwords) ? nb[wd] : 0u;
+        uint32_t b = nbw ? (nbw & ~fb[wd]) : 0u;
         long long agg;
         const long long excl = block_excl_scan256(__popc(b), sm, &agg);
         if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
@@ -242,7 +240,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
         __syncthreads();
         const int64_t nF = hs[hop];
         int64_t pos = nF + prefix_sh + excl;
-        if (b) {
+        if (nbw) {
             fb[wd] |= b;
             nb[wd] = 0u;
         }
@@ -275,12 +273,6 @@ __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
 }
 
 // ------------------------------------------------------------------ launchers
-void launch_seeds(const WinDev& w, cudaStream_t s) {
-    dim3 grid(grid_x_for(w.batch, kThreads, w.n_inst), w.n_inst);
-    k_seeds<<<grid, kThreads, 0, s>>>(w);
-    count_launches(1, __func__, s);
-}
-
 void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s) {
     // small hops (e.g. the seeds) use 64-node tiles so the launch still fills the GPU
     const int T = (fcap * (int64_t)w.n_inst) / 256 < 148 * 4 ? 64 : 256;
