@@ -84,8 +84,16 @@ class ClockSampler:
             import pynvml
             import torch
             pynvml.nvmlInit()
-            bus = torch.cuda.get_device_properties(self.idx).pci_bus_id
-            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            pr = torch.cuda.get_device_properties(self.idx)
+            want = (int(pr.pci_domain_id), int(pr.pci_bus_id), int(pr.pci_device_id))
+            for i in range(pynvml.nvmlDeviceGetCount()):        # match the CUDA device by PCI location
+                h = pynvml.nvmlDeviceGetHandleByIndex(i)
+                pci = pynvml.nvmlDeviceGetPciInfo(h)
+                if (int(pci.domain), int(pci.bus), int(pci.device)) == want:
+                    self.h = h
+                    break
+            if self.h is None:
+                raise RuntimeError("no NVML device matches the CUDA device")
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.nv = pynvml
             self.t = threading.Thread(target=self._run, daemon=True)

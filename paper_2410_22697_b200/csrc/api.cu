@@ -2,6 +2,7 @@
 // init, window arenas and the three per-window calls.  Host code only
 // marshals sizes/pointers and launches the kernels of sample.cu, gather.cu,
 // score.cu, sort.cu and load.cu; every step of the path runs on the GPU.
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cstdio>
@@ -1020,10 +1021,15 @@ mgnn_status mgnn_profile_kernels(int32_t enable, char* report, int64_t report_le
         }
         snprintf(report, (size_t)report_len, "%s", out.c_str());
     }
-    if (!enable || enable) {
+    {   // every event exactly once: each record's start is the previous record's end (or a stream's first event)
         std::vector<cudaEvent_t> all;
-        for (auto& r : g_kprof_recs) all.push_back(r.b);
+        for (auto& r : g_kprof_recs) {
+            all.push_back(r.a);
+            all.push_back(r.b);
+        }
         for (auto& l : g_kprof_last) all.push_back(l.second);
+        std::sort(all.begin(), all.end());
+        all.erase(std::unique(all.begin(), all.end()), all.end());
         cudaDeviceSynchronize();
         for (cudaEvent_t e : all) cudaEventDestroy(e);
         g_kprof_recs.clear();

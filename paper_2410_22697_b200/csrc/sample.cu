@@ -106,7 +106,12 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
             W.fr_gid[(int64_t)m * W.ucap + f] = (int32_t)gid;
             W.pos_of[(int64_t)m * W.vp_stride + r] = (int32_t)f;
             const uint32_t bit = 1u << (r & 31);
-            if (atomicOr(&W.fb[(int64_t)m * W.bm_words + (r >> 5)], bit) & bit) atomicOr(W.err, 2);   // duplicate
+            uint32_t* fbw = &W.fb[(int64_t)m * W.bm_words + (r >> 5)];
+            if (W.ext_seeds) {                             // user seeds: detect duplicates
+                if (atomicOr(fbw, bit) & bit) atomicOr(W.err, 2);
+            } else {                                       // epoch order: distinct by construction
+                atomicOr(fbw, bit);
+            }
             b0 = pd.indptr[row];
             d = pd.indptr[row + 1] - b0;
         } else if (mine) {

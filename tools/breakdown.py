@@ -6,6 +6,7 @@ Uses the bench workload (arxiv-shaped, 2 partitions, 32-step windows) and CUDA e
 import argparse
 import os
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -90,6 +91,7 @@ def timeline(windows=6):
         flush.zero_()
         torch.cuda.synchronize()
         ev = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "sampleA", "gatherB", "scoreB", "end")}
+        h0 = time.perf_counter()
         ev["start"].record(sB)
         sA.wait_event(ev["start"])
         ctx.sample(slot ^ 1, t + W, W, stream=sA)
@@ -100,9 +102,11 @@ def timeline(windows=6):
         ev["scoreB"].record(sB)
         sB.wait_stream(sA)
         ev["end"].record(sB)
+        host_us = 1e6 * (time.perf_counter() - h0)
         torch.cuda.synchronize()
         if i >= 4:
-            print("  ".join(f"{k} {1e3 * ev['start'].elapsed_time(e):7.1f}" for k, e in ev.items() if k != "start"))
+            print("  ".join(f"{k} {1e3 * ev['start'].elapsed_time(e):7.1f}" for k, e in ev.items() if k != "start")
+                  + f"  host_issue {host_us:7.1f}")
         t += W
         slot ^= 1
 
