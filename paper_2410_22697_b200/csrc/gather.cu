@@ -17,6 +17,9 @@
 // so the result does not depend on the order of the atomics.  X stores are
 // streaming (evict-first) so the window's output does not flush the tables
 // out of L2.
+#include <algorithm>
+#include <cstdlib>
+
 #include "launch.h"
 
 namespace mgnn {
@@ -145,6 +148,150 @@ __global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
     }
 }
 
+// ------------------------------------------------------------------ TMA bulk-copy variant
+// Same classification; the rows move through shared memory with the copy engine instead of
+// registers: per warp, two stages of R rows; lane j issues cp.async.bulk (global -> smem,
+// completion counted on the stage's mbarrier) for row j of the next chunk while the current
+// chunk's rows go out with cp.async.bulk smem -> global (bulk_group).  The SM keeps only the
+// classification, so the concurrent sampling kernels get the issue slots and registers.
+constexpr int kTWarps = 4;
+constexpr int kTStageBytes = 8192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(sdst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev G, int R) {
+    extern __shared__ __align__(128) unsigned char tsm[];
+    __shared__ __align__(8) uint64_t bars[kTWarps][2];
+    __shared__ unsigned long long cnt_sh[3];
+    const int m = blockIdx.y;
+    const int lp = m / W.n_steps, w = m % W.n_steps;
+    const PartDev& pd = W.parts[lp];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x < 3) cnt_sh[threadIdx.x] = 0;
+    if (lane == 0) {
+        mbar_init(&bars[warp][0], 1);
+        mbar_init(&bars[warp][1], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    const int64_t U = W.hop_size[(int64_t)m * (kMaxLayers + 1) + W.L];
+    const int pitch = W.pitch;
+    const uint32_t rowb = (uint32_t)pitch * 4u;
+    const int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
+    int32_t* fgid = W.fr_gid + (int64_t)m * W.ucap;
+    float* X = W.X + (int64_t)m * W.ucap * pitch;
+    unsigned char* stage[2] = {tsm + (size_t)warp * 2 * kTStageBytes, tsm + (size_t)warp * 2 * kTStageBytes + kTStageBytes};
+    const int64_t h_below = pd.h_below, n_local = pd.n_local, lo = pd.lo;
+    const unsigned long long wbit = 1ull << w;
+    unsigned n_loc = 0, n_hit = 0, n_miss = 0;
+    const int64_t stride = (int64_t)gridDim.x * kTWarps * R;
+    uint32_t phase[2] = {0u, 0u};
+    // classify chunk starting at f0 (lanes < R) and issue its row loads into stage st
+    auto issue = [&](int64_t f0, int st) -> int {
+        const int64_t f = f0 + lane;
+        const bool valid = lane < R && f < U;
+        const float* src = nullptr;
+        int cls = 3;
+        if (valid) {
+            const int64_t r = fr[f];
+            int32_t gid;
+            if (r >= h_below && r < h_below + n_local) {
+                gid = (int32_t)(lo + (r - h_below));
+                src = pd.table + (r - h_below) * pitch;
+                cls = 0;
+            } else {
+                const int64_t h = r < h_below ? r : r - n_local;
+                gid = pd.halo_ids[h];
+                const int32_t s = pd.slot_of[h];
+                if (s >= 0) {
+                    src = pd.rows + (int64_t)s * pitch;
+                    atomicOr(&pd.hitmask[s], wbit);
+                    cls = 1;
+                } else {
+                    const int qo = owner_of(G.bounds, G.n_parts, gid);
+                    src = G.tables[qo] + ((int64_t)gid - G.bounds[qo]) * pitch;
+                    atomicAdd(&pd.sa[h], 1.0f);
+                    cls = 2;
+                }
+            }
+            fgid[f] = gid;
+        }
+        n_loc += __popc(__ballot_sync(kFull, cls == 0));
+        n_hit += __popc(__ballot_sync(kFull, cls == 1));
+        n_miss += __popc(__ballot_sync(kFull, cls == 2));
+        const int nrows = (int)(U - f0 < R ? U - f0 : R);
+        bulk_wait_read0();                       // stores that last read this stage are done
+        __syncwarp();
+        if (lane == 0) mbar_expect_tx(&bars[warp][st], (uint32_t)nrows * rowb);
+        __syncwarp();
+        if (valid) bulk_load(stage[st] + (size_t)lane * rowb, src, rowb, &bars[warp][st]);
+        return nrows;
+    };
+    int64_t f0 = ((int64_t)blockIdx.x * kTWarps + warp) * R;
+    int st = 0;
+    int nrows = f0 < U ? issue(f0, st) : 0;
+    while (f0 < U) {
+        const int64_t fn = f0 + stride;
+        int nn = 0;
+        if (fn < U) nn = issue(fn, st ^ 1);      // next chunk's loads overlap this chunk's wait
+        mbar_wait(&bars[warp][st], phase[st]);
+        phase[st] ^= 1u;
+        if (lane < nrows) bulk_store(X + (f0 + lane) * pitch, stage[st] + (size_t)lane * rowb, rowb);
+        bulk_commit();
+        f0 = fn;
+        nrows = nn;
+        st ^= 1;
+    }
+    bulk_wait0();
+    if (lane == 0) {
+        if (n_loc) atomicAdd(&cnt_sh[0], (unsigned long long)n_loc);
+        if (n_hit) atomicAdd(&cnt_sh[1], (unsigned long long)n_hit);
+        if (n_miss) atomicAdd(&cnt_sh[2], (unsigned long long)n_miss);
+    }
+    __syncthreads();
+    long long* cn = W.counts + (int64_t)m * 8;
+    if (threadIdx.x == 0) {
+        if (cnt_sh[0]) atomicAdd((unsigned long long*)&cn[1], cnt_sh[0]);
+        if (cnt_sh[1]) atomicAdd((unsigned long long*)&cn[2], cnt_sh[1]);
+        if (cnt_sh[2]) {
+            atomicAdd((unsigned long long*)&cn[3], cnt_sh[2]);
+            atomicAdd((unsigned long long*)&cn[6], cnt_sh[2]);
+        }
+        const unsigned long long rows = cnt_sh[0] + cnt_sh[1] + cnt_sh[2];
+        if (rows && W.gathered_rows) atomicAdd((unsigned long long*)W.gathered_rows, rows);
+        if (blockIdx.x == 0) cn[0] = U;
+    }
+}
+
 void launch_gather(const WinDev& w, const WorldDev& world, cudaStream_t s) {
     // exactly one wave of 4 resident 256-thread blocks per SM in total (64 registers per thread):
     // floor, so no second, nearly empty wave leaves SMs idle at the tail
@@ -152,11 +299,30 @@ void launch_gather(const WinDev& w, const WorldDev& world, cudaStream_t s) {
     int64_t need = (w.ucap + kGWarps * 32 - 1) / (kGWarps * 32);
     unsigned gx = (unsigned)(need < target ? need : target);
     if (gx < 1) gx = 1;
-    dim3 grid(gx, w.n_inst);
-    if (w.pitch >= 128)
-        k_gather<true><<<grid, kGThreads, 0, s>>>(w, world);
-    else
-        k_gather<false><<<grid, kGThreads, 0, s>>>(w, world);
+    static const int use_tma = [] {            // default: TMA bulk copies; MGNN_GATHER=reg forces registers
+        const char* e = getenv("MGNN_GATHER");
+        return e && e[0] == 'r' ? 0 : 1;
+    }();
+    const int R = (int)std::min<int64_t>(32, std::max<int64_t>(1, kTStageBytes / ((int64_t)w.pitch * 4)));
+    if (use_tma && (int64_t)w.pitch * 4 <= kTStageBytes) {
+        const size_t smem = (size_t)kTWarps * 2 * kTStageBytes;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        // ~3 resident 128-thread blocks per SM (64 KB shared each), one wave
+        int64_t tgt = (148 * 3) / w.n_inst;
+        int64_t nd = (w.ucap + kTWarps * R - 1) / (kTWarps * R);
+        unsigned gxt = (unsigned)std::max<int64_t>(1, std::min(nd, tgt));
+        k_gather_tma<<<dim3(gxt, w.n_inst), kTWarps * 32, smem, s>>>(w, world, R);
+    } else {
+        dim3 grid(gx, w.n_inst);
+        if (w.pitch >= 128)
+            k_gather<true><<<grid, kGThreads, 0, s>>>(w, world);
+        else
+            k_gather<false><<<grid, kGThreads, 0, s>>>(w, world);
+    }
     count_launches(1, __func__, s);
 }
 
