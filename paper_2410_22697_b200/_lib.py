@@ -5,7 +5,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmgnn.so")
+LIB_PATH = os.environ.get("MGNN_LIB", os.path.join(HERE, "libmgnn.so"))   # override: A/B builds
 
 MAX_LAYERS = 8
 IPC_HANDLE_BYTES = 64

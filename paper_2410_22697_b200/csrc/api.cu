@@ -857,7 +857,8 @@ mgnn_status mgnn_sample(mgnn_ctx ctx, int32_t slot, uint64_t t0, int32_t n_steps
         wd.ext_seeds = w.ext_seeds;
         wd.ext_counts = w.ext_counts;
     }
-    for (int i = 0; i < ctx->L; ++i) {              // hop 0 also writes F_0 (the seeds)
+    launch_seeds(wd, s);
+    for (int i = 0; i < ctx->L; ++i) {
         // per-hop scratch strides follow the max window; scans index by instance < M
         Scratch scc = w.sc_count[i], scp = w.sc_compact[i];
         launch_hop(wd, i, ctx->fcap[i], scc, s);

@@ -82,6 +82,7 @@ struct EvScratch {        // eviction-round scratch, zeroed per round
 };
 
 // sample.cu
+void launch_seeds(const WinDev& w, cudaStream_t s);
 void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s);
 void launch_compact(const WinDev& w, int hop, Scratch sc, cudaStream_t s);
 void launch_relabel(const WinDev& w, cudaStream_t s);

@@ -6,8 +6,7 @@
 // one launch per stage serves W steps x P_local partitions.
 //
 // Per hop i (K1/K2):
-//   k_hop     : (hop 0 first writes F_0 = the step's seeds, R#8)
-//               thread per frontier node x of F_i (a tile of 64/256 per block):
+//   k_hop     : thread per frontier node x of F_i (a tile of 256 per block):
 //               count min(deg, k_i) (halo nodes: 0, R#1), exclusive offsets by
 //               a block scan + decoupled look-back across tiles; then groups
 //               of G = pow2 >= k_i lanes take the tile's nodes 32/G per warp
@@ -42,6 +41,52 @@ static inline unsigned grid_x_for(int64_t items_per_inst, int items_per_block, i
     return (unsigned)(g < 1 ? 1 : g);
 }
 
+// ------------------------------------------------------------------ seeds: F_0 (R#8)
+__global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
+    const int m = blockIdx.y;
+    const int lp = m / W.n_steps, w = m % W.n_steps;
+    const PartDev& pd = W.parts[lp];
+    const uint64_t t = W.step0 + (uint64_t)w;
+    const int32_t* src;
+    int64_t n0;
+    if (W.ext_seeds) {
+        src = W.ext_seeds + (int64_t)m * W.batch;
+        n0 = W.ext_counts[m];
+        if (n0 < 1 || n0 > W.batch) {
+            if (threadIdx.x == 0 && blockIdx.x == 0) atomicOr(W.err, 1);
+            n0 = 0;
+        }
+    } else {
+        const int64_t e = (int64_t)((t - 1) / (uint64_t)pd.nbatch), b = (int64_t)((t - 1) % (uint64_t)pd.nbatch);
+        const int32_t* perm = pd.perm + (int64_t)(e % pd.perm_slots) * pd.n_train;
+        const int64_t s0 = b * W.batch;
+        n0 = pd.n_train - s0 < W.batch ? pd.n_train - s0 : W.batch;
+        src = perm + s0;
+    }
+    int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
+    int32_t* pos = W.pos_of + (int64_t)m * W.vp_stride;
+    uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n0; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t gid = src[j];
+        int64_t row = gid - pd.lo;
+        if (row < 0 || row >= pd.n_local) {      // external seed not owned by this partition
+            atomicOr(W.err, 1);
+            row = 0;
+        }
+        const int32_t r = (int32_t)(pd.h_below + row);
+        fr[j] = r;
+        W.fr_gid[(int64_t)m * W.ucap + j] = (int32_t)gid;   // F_0 readable right after sampling
+        pos[r] = (int32_t)j;
+        const uint32_t bit = 1u << (r & 31);
+        if (W.ext_seeds) {                                  // user seeds: detect duplicates
+            if (atomicOr(&fb[r >> 5], bit) & bit) atomicOr(W.err, 2);
+        } else {                                            // epoch order: distinct by construction
+            atomicOr(&fb[r >> 5], bit);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) W.hop_size[(int64_t)m * (kMaxLayers + 1)] = n0;
+}
+
 // ------------------------------------------------------------------ one hop: counts, offsets, samples
 // T = frontier nodes per tile (64 or 256; small tiles give small hops enough blocks).
 __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max, int T) {
@@ -53,68 +98,22 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
     const int m = blockIdx.y;
     const int lp = m / W.n_steps, w = m % W.n_steps;
     const PartDev& pd = W.parts[lp];
-    // hop 0 also materialises F_0 = the step's seeds (R#8): epoch-order slice or external seeds
-    const int32_t* seed_src = nullptr;
-    int64_t nF;
-    if (hop == 0) {
-        if (W.ext_seeds) {
-            seed_src = W.ext_seeds + (int64_t)m * W.batch;
-            nF = W.ext_counts[m];
-            if (nF < 1 || nF > W.batch) {
-                if (threadIdx.x == 0 && blockIdx.x == 0) atomicOr(W.err, 1);
-                nF = 0;
-            }
-        } else {
-            const uint64_t t = W.step0 + (uint64_t)w;
-            const int64_t e = (int64_t)((t - 1) / (uint64_t)pd.nbatch), b = (int64_t)((t - 1) % (uint64_t)pd.nbatch);
-            const int64_t s0 = b * W.batch;
-            seed_src = pd.perm + (int64_t)(e % pd.perm_slots) * pd.n_train + s0;
-            nF = pd.n_train - s0 < W.batch ? pd.n_train - s0 : W.batch;
-        }
-        if (blockIdx.x == 0 && threadIdx.x == 0) W.hop_size[(int64_t)m * (kMaxLayers + 1)] = nF;
-    } else {
-        nF = W.hop_size[(int64_t)m * (kMaxLayers + 1) + hop];
-    }
+    const int64_t nF = W.hop_size[(int64_t)m * (kMaxLayers + 1) + hop];
     const int64_t ntiles = (nF + T - 1) / T;
     int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
     // persistent: blocks claim tiles in order until the instance's frontier is exhausted
-    // lane groups for the draws: k lanes per node, floor(32/k) nodes per warp step (hop constants)
-    const int k = W.k_hop[hop];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int G = k;
-    const int per = 32 / G;
-    const int gi = lane / G, gl = lane - gi * G, gbase = gi * G;
     for (;;) {
         const int tile = claim_tile(sc.tilectr + m, &tslot);
         if (tile >= ntiles) {
             if (tile == 0 && threadIdx.x == 0) off[0] = 0;   // empty F_i
             break;
         }
+        const int k = W.k_hop[hop];
         const int64_t f = (int64_t)tile * T + threadIdx.x;
         const bool mine = threadIdx.x < T && f < nF;
         const int64_t h_below = pd.h_below, n_local = pd.n_local;
         int64_t row = -1, b0 = 0, d = 0;
-        if (mine && hop == 0) {                            // seed: local rank, frontier bitmap, position
-            const int64_t gid = seed_src[f];
-            row = gid - pd.lo;
-            if (row < 0 || row >= n_local) {               // external seed not owned by this partition
-                atomicOr(W.err, 1);
-                row = 0;
-            }
-            const int32_t r = (int32_t)(h_below + row);
-            W.fr_rank[(int64_t)m * W.ucap + f] = r;
-            W.fr_gid[(int64_t)m * W.ucap + f] = (int32_t)gid;
-            W.pos_of[(int64_t)m * W.vp_stride + r] = (int32_t)f;
-            const uint32_t bit = 1u << (r & 31);
-            uint32_t* fbw = &W.fb[(int64_t)m * W.bm_words + (r >> 5)];
-            if (W.ext_seeds) {                             // user seeds: detect duplicates
-                if (atomicOr(fbw, bit) & bit) atomicOr(W.err, 2);
-            } else {                                       // epoch order: distinct by construction
-                atomicOr(fbw, bit);
-            }
-            b0 = pd.indptr[row];
-            d = pd.indptr[row + 1] - b0;
-        } else if (mine) {
+        if (mine) {
             row = (int64_t)W.fr_rank[(int64_t)m * W.ucap + f] - h_below;
             if (row >= 0 && row < n_local) {               // halo frontier nodes are leaves (R#1)
                 b0 = pd.indptr[row];
@@ -147,6 +146,10 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
         // Only CSR indices are produced here (no global loads), staged in shared memory.
         long long* sidx = reinterpret_cast<long long*>(dyn_smem);   // [T * k] CSR index of each sample of the tile
         const long long o_tile = prefix_sh;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int G = k;                                   // one lane per slot; 32/k nodes per warp step
+        const int per = 32 / G;
+        const int gi = lane / G, gl = lane - gi * G, gbase = gi * G;
         const uint32_t c1 = (uint32_t)hop << 16;
         const uint32_t c3 = ((uint32_t)pd.part_id << 8) | kStreamSample;
         const uint32_t step = (uint32_t)(W.step0 + (uint64_t)w);
@@ -180,34 +183,15 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
         __syncthreads();
         // ---- phase B: every sample of the tile in parallel: neighbour rank, coalesced column write, and
         // the new-node mark unless the neighbour is already in F_i.
-        // B1: all neighbour ranks of the tile (independent loads) into shared memory, over sidx
-        int32_t* __restrict__ cols = W.cols[hop] + (int64_t)m * W.col_stride[hop] + o_tile;
-        const uint32_t* __restrict__ fb = W.fb + (int64_t)m * W.bm_words;
-        uint32_t* __restrict__ nb = W.nb + (int64_t)m * W.bm_words;
+        int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop] + o_tile;
+        const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
+        uint32_t* nb = W.nb + (int64_t)m * W.bm_words;
         const int32_t* __restrict__ crank = pd.cols_rank;
-        int32_t creg[8];
-        int nmine = 0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int e = threadIdx.x + u * kThreads;
-            if (e < (int)agg) creg[u] = crank[sidx[e]], nmine = u + 1;
-        }
-        for (int e = threadIdx.x + 8 * kThreads; e < (int)agg; e += kThreads) cols[e] = crank[sidx[e]];
-        __syncthreads();
-        // B2: coalesced column writes and new-node marks (fire-and-forget reductions)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            if (u < nmine) {
-                const int e = threadIdx.x + u * kThreads;
-                const int32_t c = creg[u];
-                MGNN_CHECK(o_tile + e < W.col_stride[hop] && c < pd.vp, "cols o=%lld c=%d", o_tile + e, c);
-                cols[e] = c;
-                const uint32_t bit = 1u << (c & 31);
-                if (!(fb[c >> 5] & bit)) atomicOr(&nb[c >> 5], bit);
-            }
-        }
-        for (int e = threadIdx.x + 8 * kThreads; e < (int)agg; e += kThreads) {
-            const int32_t c = cols[e];
+    #pragma unroll 4
+        for (int e = threadIdx.x; e < (int)agg; e += kThreads) {
+            const int32_t c = crank[sidx[e]];
+            MGNN_CHECK(o_tile + e < W.col_stride[hop] && c < pd.vp, "cols o=%lld c=%d", o_tile + e, c);
+            cols[e] = c;
             const uint32_t bit = 1u << (c & 31);
             if (!(fb[c >> 5] & bit)) atomicOr(&nb[c >> 5], bit);
         }
@@ -216,7 +200,6 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
 }
 
 // ------------------------------------------------------------------ bitmap -> sorted new frontier nodes
-// Persistent blocks: each claims the instance's word tiles in order until exhausted.
 __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch sc, int64_t tiles_max) {
     __shared__ long long sm[8];
     __shared__ int tslot;
@@ -225,42 +208,36 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
     const PartDev& pd = W.parts[m / W.n_steps];
     const int64_t nwords = (pd.vp + 31) >> 5;
     const int64_t ntiles = (nwords + kWordTile - 1) / kWordTile;
-    uint32_t* __restrict__ nb = W.nb + (int64_t)m * W.bm_words;
-    uint32_t* __restrict__ fb = W.fb + (int64_t)m * W.bm_words;
+    const int tile = claim_tile(sc.tilectr + m, &tslot);
+    if (tile >= ntiles) return;
+    uint32_t* nb = W.nb + (int64_t)m * W.bm_words;
+    uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
+    const int64_t wd = (int64_t)tile * kWordTile + threadIdx.x;
+    uint32_t b = (wd < nwords) ? nb[wd] : 0u;
+    long long agg;
+    const long long excl = block_excl_scan256(__popc(b), sm, &agg);
     int64_t* hs = W.hop_size + (int64_t)m * (kMaxLayers + 1);
-    int32_t* __restrict__ fr = W.fr_rank + (int64_t)m * W.ucap;
-    int32_t* __restrict__ posof = W.pos_of + (int64_t)m * W.vp_stride;
-    for (;;) {
-        const int tile = claim_tile(sc.tilectr + m, &tslot);
-        if (tile >= ntiles) break;
-        const int64_t wd = (int64_t)tile * kWordTile + threadIdx.x;
-        // new nodes = marked and not already in F_i (a seed may be marked by a sample drawn
-        // before its own frontier bit was set in the fused seed/hop-0 kernel)
-        const uint32_t nbw = (wd < nwords) ? nb[wd] : 0u;
-        uint32_t b = nbw ? (nbw & ~fb[wd]) : 0u;
-        long long agg;
-        const long long excl = block_excl_scan256(__popc(b), sm, &agg);
-        if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
-                                                                         (unsigned long long)agg);
-        __syncthreads();
-        const int64_t nF = hs[hop];
-        int64_t pos = nF + prefix_sh + excl;
-        if (nbw) {
-            fb[wd] |= b;
-            nb[wd] = 0u;
-        }
-        while (b) {
-            const int bi = __ffs(b) - 1;
-            b &= b - 1;
-            const int32_t r = (int32_t)(wd * 32 + bi);
-            MGNN_CHECK(pos < W.ucap && r < pd.vp, "compact pos=%lld r=%d", (long long)pos, r);
-            fr[pos] = r;
-            posof[r] = (int32_t)pos;
-            ++pos;
-        }
-        if (tile == ntiles - 1 && threadIdx.x == 0) hs[hop + 1] = nF + prefix_sh + agg;
-        __syncthreads();
+    if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
+                                                                     (unsigned long long)agg);
+    __syncthreads();
+    const int64_t nF = hs[hop];
+    int64_t pos = nF + prefix_sh + excl;
+    if (b) {
+        fb[wd] |= b;
+        nb[wd] = 0u;
     }
+    int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
+    int32_t* posof = W.pos_of + (int64_t)m * W.vp_stride;
+    while (b) {
+        const int bi = __ffs(b) - 1;
+        b &= b - 1;
+        const int32_t r = (int32_t)(wd * 32 + bi);
+        MGNN_CHECK(pos < W.ucap && r < pd.vp, "compact pos=%lld r=%d", (long long)pos, r);
+        fr[pos] = r;
+        posof[r] = (int32_t)pos;
+        ++pos;
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) hs[hop + 1] = nF + prefix_sh + agg;
 }
 
 // ------------------------------------------------------------------ cols: rank -> position in F_{i+1}
@@ -278,6 +255,12 @@ __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
 }
 
 // ------------------------------------------------------------------ launchers
+void launch_seeds(const WinDev& w, cudaStream_t s) {
+    dim3 grid(grid_x_for(w.batch, kThreads, w.n_inst), w.n_inst);
+    k_seeds<<<grid, kThreads, 0, s>>>(w);
+    count_launches(1, __func__, s);
+}
+
 void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s) {
     // small hops (e.g. the seeds) use 64-node tiles so the launch still fills the GPU
     const int T = (fcap * (int64_t)w.n_inst) / 256 < 148 * 4 ? 64 : 256;
@@ -300,10 +283,7 @@ void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t
 
 void launch_compact(const WinDev& w, int hop, Scratch sc, cudaStream_t s) {
     const int64_t tiles = scan_tiles_words(w.bm_words);
-    int64_t gx = tiles;
-    const int64_t target = (148 * 6 + w.n_inst - 1) / w.n_inst;   // persistent: ~6 blocks per SM in total
-    if (gx > target) gx = target;
-    dim3 grid((unsigned)(gx < 1 ? 1 : gx), w.n_inst);
+    dim3 grid((unsigned)(tiles < 1 ? 1 : tiles), w.n_inst);
     k_compact<<<grid, kThreads, 0, s>>>(w, hop, sc, tiles < 1 ? 1 : tiles);
     count_launches(1, __func__, s);
 }
