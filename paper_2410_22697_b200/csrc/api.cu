@@ -772,7 +772,7 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
         const int64_t nt = std::max<int64_t>(p.n_train, 1);
         CK(dalloc(&p.perm, (int64_t)p.perm_slots * nt));
         CK(dalloc(&p.pk, p.perm_chunk * nt)); CK(dalloc(&p.pkt, p.perm_chunk * nt)); CK(dalloc(&p.pvt, p.perm_chunk * nt));
-        scr = std::max(scr, radix_scratch_bytes(p.perm_chunk, nt, 8));
+        scr = std::max(scr, (size_t)p.perm_chunk * 256 * 2 * sizeof(uint32_t));
     }
     {
         mgnn_status st2 = ensure_scratch(ctx, &ctx->perm_scr, &ctx->perm_scr_bytes, scr);
@@ -837,9 +837,8 @@ mgnn_status mgnn_sample(mgnn_ctx ctx, int32_t slot, uint64_t t0, int32_t n_steps
             for (int64_t c = e0 / G; c <= e1 / G; ++c) {     // epoch e lives in ring slot e % 2G
                 if (p.chunk_loaded[c % 2] == c) continue;
                 const SortSeg* segs = ctx->d_permsegs + (size_t)lp * ctx->perm_slots_max + (c % 2) * G;
-                launch_perm_keys(ctx->d_parts + lp, p.n_train, (uint64_t)(c * G), (int)G, (uint32_t)ctx->run_seed,
-                                 (uint32_t)(ctx->run_seed >> 32), segs, s);
-                radix_sort_pairs(segs, (int)G, p.n_train, 8, ctx->perm_scr, s);
+                launch_perm_build(ctx->d_parts + lp, p.n_train, (uint64_t)(c * G), (int)G, (uint32_t)ctx->run_seed,
+                                  (uint32_t)(ctx->run_seed >> 32), segs, ctx->perm_scr, s);
                 p.chunk_loaded[c % 2] = c;
             }
         }

@@ -105,9 +105,10 @@ constexpr int kEvMax = 65536;
 void launch_init_keys(const PartDev* pd_dev, int64_t n_h, const SortSeg* seg, long long* n_dev, cudaStream_t s);
 void launch_init_fill(const PartDev* pd_dev, int64_t n_h, int64_t cap, const uint32_t* order, cudaStream_t s);
 void launch_rows_from_owners(const PartDev* pd_dev, int64_t cap, const WorldDev& world, cudaStream_t s);
-// keys of n_epochs consecutive epoch orders (epoch0 ...) into segments segs[0..n_epochs)
-void launch_perm_keys(const PartDev* pd_dev, int64_t n_train, uint64_t epoch0, int n_epochs, uint32_t seed_lo,
-                      uint32_t seed_hi, const SortSeg* segs, cudaStream_t s);
+// n_epochs consecutive epoch orders (epoch0 ...) into segs[j].vals; keys / keys_tmp / vals_tmp
+// are work buffers of n_train each; scratch holds 2 * 256 * n_epochs counters (zeroed here)
+void launch_perm_build(const PartDev* pd_dev, int64_t n_train, uint64_t epoch0, int n_epochs, uint32_t seed_lo,
+                       uint32_t seed_hi, const SortSeg* segs, void* scratch, cudaStream_t s);
 
 // sort.cu: stable LSD radix sort of (u64 key, u32 value) pairs, each segment with its own digit
 // schedule (SortSeg::shift, at most max_passes); n_max bounds every segment's length.

@@ -18,6 +18,8 @@
 //             rank IS the sorted position) and writes the K winners in order: no sort at all.
 //   large |BUF|: the onesweep radix sort of both lists (sort.cu).
 //   k_swap_refill  pair i = (E[i], R[i]): swap of P:224, refill from the owner's table.
+#include <algorithm>
+
 #include "launch.h"
 
 namespace mgnn {
@@ -401,28 +403,97 @@ void launch_rows_from_owners(const PartDev* pd_dev, int64_t cap, const WorldDev&
     count_launches(1, __func__, s);
 }
 
-// ------------------------------------------------------------------ epoch order keys (R#8)
+// ------------------------------------------------------------------ epoch orders (R#8)
+// G epoch orders of a partition at once: train ids sorted by (Philox key, id).  MSB bucket
+// scheme instead of an LSD sort: (1) keys + histogram of the top key byte, (2) scatter into the
+// 256 buckets of each epoch, (3) one block per bucket ranks its items by counting smaller
+// (key, index) pairs -- the rank is the sorted position.  Philox keys are uniform, so a bucket
+// holds ~n/256 items; any size stays correct (large buckets are ranked from global memory).
 __global__ void k_perm_keys(const PartDev* __restrict__ pdp, uint64_t epoch0, int n_epochs, uint32_t k0, uint32_t k1,
-                            const SortSeg* __restrict__ segs) {
+                            const SortSeg* __restrict__ segs, uint32_t* __restrict__ hist) {
     const PartDev& pd = *pdp;
     const uint32_t c3 = ((uint32_t)pd.part_id << 8) | kStreamShuffle;
     const int64_t n = pd.n_train, total = n * n_epochs;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = x / n, i = x - j * n;
-        const SortSeg& sg = segs[j];
         const uint32_t id = (uint32_t)pd.train_ids[i];
         const u4 o = philox4x32_10(u4{id, (uint32_t)(epoch0 + j), 0u, c3}, k0, k1);
-        sg.keys[i] = ((unsigned long long)o.x << 32) | o.y;
-        sg.vals[i] = id;
+        const unsigned long long key = ((unsigned long long)o.x << 32) | o.y;
+        segs[j].keys[i] = key;
+        atomicAdd(&hist[j * 256 + (unsigned)(key >> 56)], 1u);
     }
 }
 
-void launch_perm_keys(const PartDev* pd_dev, int64_t n_train, uint64_t epoch0, int n_epochs, uint32_t seed_lo,
-                      uint32_t seed_hi, const SortSeg* segs, cudaStream_t s) {
+// exclusive prefix of the segment's 256 bucket counts, in shared memory (256 threads)
+__device__ __forceinline__ void bucket_starts(const uint32_t* __restrict__ h, uint32_t* start_sh, long long* sm) {
+    long long tot;
+    const long long ex = block_excl_scan256(h[threadIdx.x], sm, &tot);
+    start_sh[threadIdx.x] = (uint32_t)ex;
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_perm_scatter(const PartDev* __restrict__ pdp, int n_epochs,
+                                                      const SortSeg* __restrict__ segs, const uint32_t* __restrict__ hist,
+                                                      uint32_t* __restrict__ cursor) {
+    __shared__ uint32_t start[256];
+    __shared__ long long sm[8];
+    const int64_t n = pdp->n_train;
+    const int j = blockIdx.y;
+    bucket_starts(hist + j * 256, start, sm);
+    const SortSeg sg = segs[j];
+    for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) {
+        const unsigned long long key = sg.keys[i];
+        const unsigned b = (unsigned)(key >> 56);
+        const uint32_t p = start[b] + atomicAdd(&cursor[j * 256 + b], 1u);
+        sg.keys_tmp[p] = key;
+        sg.vals_tmp[p] = (uint32_t)i;         // list index = id order: the tie-break
+    }
+}
+
+__global__ void __launch_bounds__(256) k_perm_rank(const PartDev* __restrict__ pdp, const SortSeg* __restrict__ segs,
+                                                   const uint32_t* __restrict__ hist) {
+    __shared__ uint32_t start[256];
+    __shared__ long long sm[8];
+    __shared__ unsigned long long sk[1024];
+    __shared__ uint32_t si[1024];
+    const int j = blockIdx.y, b = blockIdx.x;
+    bucket_starts(hist + j * 256, start, sm);
+    const SortSeg sg = segs[j];
+    const uint32_t s0 = start[b], cnt = hist[j * 256 + b];
+    const bool in_smem = cnt <= 1024;
+    if (in_smem) {
+        for (uint32_t x = threadIdx.x; x < cnt; x += 256) {
+            sk[x] = sg.keys_tmp[s0 + x];
+            si[x] = sg.vals_tmp[s0 + x];
+        }
+        __syncthreads();
+    }
+    const int32_t* train = pdp->train_ids;
+    for (uint32_t x = threadIdx.x; x < cnt; x += 256) {
+        const unsigned long long k = in_smem ? sk[x] : sg.keys_tmp[s0 + x];
+        const uint32_t i = in_smem ? si[x] : sg.vals_tmp[s0 + x];
+        uint32_t rank = 0;
+        for (uint32_t y = 0; y < cnt; ++y) {
+            const unsigned long long ky = in_smem ? sk[y] : sg.keys_tmp[s0 + y];
+            const uint32_t iy = in_smem ? si[y] : sg.vals_tmp[s0 + y];
+            rank += (ky < k) || (ky == k && iy < i);
+        }
+        sg.vals[s0 + rank] = (uint32_t)train[i];   // vals = the epoch-order slot
+    }
+}
+
+void launch_perm_build(const PartDev* pd_dev, int64_t n_train, uint64_t epoch0, int n_epochs, uint32_t seed_lo,
+                       uint32_t seed_hi, const SortSeg* segs, void* scratch, cudaStream_t s) {
+    uint32_t* hist = (uint32_t*)scratch;
+    uint32_t* cursor = hist + (size_t)n_epochs * 256;
+    cudaMemsetAsync(scratch, 0, (size_t)n_epochs * 256 * 2 * sizeof(uint32_t), s);
     const int64_t total = n_train * n_epochs;
     k_perm_keys<<<blocks_for(total < 1 ? 1 : total, kSThreads), kSThreads, 0, s>>>(pd_dev, epoch0, n_epochs, seed_lo,
-                                                                                   seed_hi, segs);
-    count_launches(1, __func__, s);
+                                                                                   seed_hi, segs, hist);
+    unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_train + 255) / 256, 64));
+    k_perm_scatter<<<dim3(gx, n_epochs), 256, 0, s>>>(pd_dev, n_epochs, segs, hist, cursor);
+    k_perm_rank<<<dim3(256, n_epochs), 256, 0, s>>>(pd_dev, segs, hist);
+    count_launches(3, __func__, s);
 }
 
 }  // namespace mgnn
