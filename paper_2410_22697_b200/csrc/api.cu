@@ -47,6 +47,13 @@ void count_launches(long long n, const char* who, cudaStream_t s) {
     }
 }
 long long launches_total() { return g_launches.load(); }
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("MGNN_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 }  // namespace mgnn
 
 using namespace mgnn;

@@ -169,6 +169,13 @@ __device__ __forceinline__ long long block_excl_scan256(long long v, long long* 
     return wpre + x - v;
 }
 
+// Programmatic dependent launch: a kernel launched with programmatic stream serialization is
+// set up while its predecessor in the stream drains and waits here, before touching any memory
+// the predecessor produces or consumes (a no-op for a normal launch).  Kernels do not trigger
+// their successors early: waiting blocks would hold SM slots the concurrent stream needs
+// (measured: +7% with the implicit trigger at exit, -2% with an early trigger).
+__device__ __forceinline__ void pdl_enter() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Dynamic, in-order tile id for a segment (claimed by thread 0, broadcast).
 __device__ __forceinline__ int claim_tile(int32_t* ctr, int* smem_slot) {
     if (threadIdx.x == 0) *smem_slot = atomicAdd(ctr, 1);

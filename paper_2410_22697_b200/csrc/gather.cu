@@ -33,6 +33,7 @@ __device__ __forceinline__ void stcs4(float* p, float4 v) { __stcs(reinterpret_c
 // WIDE: rows of >= 32 float4 (D >= 128, one or more 16-B chunks per lane); else 32/q rows per warp step.
 template <bool WIDE>
 __global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
+    pdl_enter();
     __shared__ unsigned long long cnt_sh[3];
     const int m = blockIdx.y;
     const int lp = m / W.n_steps, w = m % W.n_steps;
@@ -189,6 +190,7 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev G, int R) {
+    pdl_enter();
     extern __shared__ __align__(128) unsigned char tsm[];
     __shared__ __align__(8) uint64_t bars[kTWarps][2];
     __shared__ unsigned long long cnt_sh[3];
@@ -315,13 +317,13 @@ void launch_gather(const WinDev& w, const WorldDev& world, cudaStream_t s) {
         int64_t tgt = (148 * 3) / w.n_inst;
         int64_t nd = (w.ucap + kTWarps * R - 1) / (kTWarps * R);
         unsigned gxt = (unsigned)std::max<int64_t>(1, std::min(nd, tgt));
-        k_gather_tma<<<dim3(gxt, w.n_inst), kTWarps * 32, smem, s>>>(w, world, R);
+        launch_k(k_gather_tma, dim3(gxt, w.n_inst), dim3(kTWarps * 32), smem, s, w, world, R);
     } else {
         dim3 grid(gx, w.n_inst);
         if (w.pitch >= 128)
-            k_gather<true><<<grid, kGThreads, 0, s>>>(w, world);
+            launch_k(k_gather<true>, grid, dim3(kGThreads), 0, s, w, world);
         else
-            k_gather<false><<<grid, kGThreads, 0, s>>>(w, world);
+            launch_k(k_gather<false>, grid, dim3(kGThreads), 0, s, w, world);
     }
     count_launches(1, __func__, s);
 }

@@ -81,6 +81,24 @@ struct EvScratch {        // eviction-round scratch, zeroed per round
     unsigned long long* n_cand;     // [2*n_lp] candidates appended by k_cand
 };
 
+// Launch with programmatic stream serialization (PDL) unless MGNN_PDL=0; the kernel must call
+// pdl_enter() before its first global-memory access.
+bool pdl_enabled();
+template <typename... P, typename... A>
+inline void launch_k(void (*kern)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // sample.cu
 void launch_seeds(const WinDev& w, cudaStream_t s);
 void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s);

@@ -43,6 +43,7 @@ static inline unsigned grid_x_for(int64_t items_per_inst, int items_per_block, i
 
 // ------------------------------------------------------------------ seeds: F_0 (R#8)
 __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
+    pdl_enter();
     const int m = blockIdx.y;
     const int lp = m / W.n_steps, w = m % W.n_steps;
     const PartDev& pd = W.parts[lp];
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
 // ------------------------------------------------------------------ one hop: counts, offsets, samples
 // T = frontier nodes per tile (64 or 256; small tiles give small hops enough blocks).
 __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max, int T) {
+    pdl_enter();
     __shared__ long long sm[8];
     __shared__ int tslot;
     __shared__ long long prefix_sh;
@@ -201,6 +203,7 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
 
 // ------------------------------------------------------------------ bitmap -> sorted new frontier nodes
 __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch sc, int64_t tiles_max) {
+    pdl_enter();
     __shared__ long long sm[8];
     __shared__ int tslot;
     __shared__ long long prefix_sh;
@@ -242,6 +245,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
 
 // ------------------------------------------------------------------ cols: rank -> position in F_{i+1}
 __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
+    pdl_enter();
     const int m = blockIdx.y;
     const int32_t* posof = W.pos_of + (int64_t)m * W.vp_stride;
     const int64_t* hs = W.hop_size + (int64_t)m * (kMaxLayers + 1);
@@ -257,7 +261,7 @@ __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
 // ------------------------------------------------------------------ launchers
 void launch_seeds(const WinDev& w, cudaStream_t s) {
     dim3 grid(grid_x_for(w.batch, kThreads, w.n_inst), w.n_inst);
-    k_seeds<<<grid, kThreads, 0, s>>>(w);
+    launch_k(k_seeds, grid, dim3(kThreads), 0, s, w);
     count_launches(1, __func__, s);
 }
 
@@ -277,14 +281,14 @@ void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t
         cudaFuncSetAttribute(k_hop, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * MGNN_MAX_FANOUT * 8);
         attr_set = true;
     }
-    k_hop<<<grid, kThreads, smem, s>>>(w, hop, sc, tiles_max < 1 ? 1 : tiles_max, T);
+    launch_k(k_hop, grid, dim3(kThreads), smem, s, w, hop, sc, (int64_t)(tiles_max < 1 ? 1 : tiles_max), T);
     count_launches(1, __func__, s);
 }
 
 void launch_compact(const WinDev& w, int hop, Scratch sc, cudaStream_t s) {
     const int64_t tiles = scan_tiles_words(w.bm_words);
     dim3 grid((unsigned)(tiles < 1 ? 1 : tiles), w.n_inst);
-    k_compact<<<grid, kThreads, 0, s>>>(w, hop, sc, tiles < 1 ? 1 : tiles);
+    launch_k(k_compact, grid, dim3(kThreads), 0, s, w, hop, sc, (int64_t)(tiles < 1 ? 1 : tiles));
     count_launches(1, __func__, s);
 }
 
@@ -292,7 +296,7 @@ void launch_relabel(const WinDev& w, cudaStream_t s) {
     int64_t e_max = 0;
     for (int i = 0; i < w.L; ++i) e_max = w.col_stride[i] > e_max ? w.col_stride[i] : e_max;
     dim3 grid(grid_x_for(e_max, kThreads, w.n_inst), w.n_inst);
-    k_relabel<<<grid, kThreads, 0, s>>>(w);
+    launch_k(k_relabel, grid, dim3(kThreads), 0, s, w);
     count_launches(1, __func__, s);
 }
 

@@ -38,6 +38,7 @@ static inline unsigned blocks_for(int64_t n, int per_block) {
 // multiplies S_E by gamma once (the same sequence of RN products the paper's
 // per-step loop performs: only *gamma ever touches S_E between rounds).
 __global__ void __launch_bounds__(kSThreads) k_decay(const PartDev* __restrict__ parts, int n_steps, float gamma) {
+    pdl_enter();
     const PartDev& pd = parts[blockIdx.y];
     for (int64_t s = (int64_t)blockIdx.x * kSThreads + threadIdx.x; s < pd.cap; s += (int64_t)gridDim.x * kSThreads) {
         const unsigned long long mask = pd.hitmask[s];
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(kSThreads) k_decay(const PartDev* __restrict__
 void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, float gamma, cudaStream_t s) {
     if (cap_max < 1) return;
     dim3 grid(blocks_for(cap_max, kSThreads), n_lp);
-    k_decay<<<grid, kSThreads, 0, s>>>(parts, n_steps, gamma);
+    launch_k(k_decay, grid, dim3(kSThreads), 0, s, parts, n_steps, gamma);
     count_launches(1, __func__, s);
 }
 
@@ -63,6 +64,7 @@ void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, 
 __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict__ parts, float alpha, float theta_r,
                                                       const SortSeg* __restrict__ segs, long long* __restrict__ n_out,
                                                       Scratch sc, int64_t tiles_max, EvScratch ev) {
+    pdl_enter();
     __shared__ long long sm[8];
     __shared__ int tslot;
     __shared__ long long prefix_sh;
@@ -128,7 +130,7 @@ void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, f
     int64_t tiles = (n_max + kSThreads * 8 - 1) / (kSThreads * 8);
     if (tiles < 1) tiles = 1;
     dim3 grid((unsigned)tiles, 2 * n_lp);
-    k_select<<<grid, kSThreads, 0, s>>>(parts, alpha, theta_r, segs, n_out, sc, tiles, ev);
+    launch_k(k_select, grid, dim3(kSThreads), 0, s, parts, alpha, theta_r, segs, n_out, sc, tiles, ev);
     count_launches(1, __func__, s);
 }
 
@@ -166,6 +168,7 @@ constexpr long long kCandMax = 4096;   // refine the threshold with the next 12 
 // Second-level histogram (key bits [40, 52)) of the threshold bucket, only when the first level
 // would leave more than kCandMax candidates (e.g. many equal scores in an early round).
 __global__ void __launch_bounds__(kSThreads) k_hist2(const SortSeg* __restrict__ segs, EvScratch ev) {
+    pdl_enter();
     __shared__ long long sm[8];
     __shared__ long long T_sh, below_sh;
     const int sg = blockIdx.y;
@@ -195,6 +198,7 @@ __global__ void __launch_bounds__(kSThreads) k_hist2(const SortSeg* __restrict__
 // Every block derives K = min(|E|, |R|) of its partition and the threshold(s) of its list from the
 // histograms; block 0 records {K, T} for k_rank.
 __global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ segs, EvScratch ev) {
+    pdl_enter();
     __shared__ long long sm[8];
     __shared__ long long T_sh, below_sh, T2_sh, below2_sh;
     const int sg = blockIdx.y;
@@ -244,6 +248,7 @@ __global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ 
 
 // ------------------------------------------------------------------ rank by counting (unique keys)
 __global__ void __launch_bounds__(kSThreads) k_rank(const SortSeg* __restrict__ segs, EvScratch ev) {
+    pdl_enter();
     __shared__ unsigned long long tile_k[2048];
     const int sg = blockIdx.y;
     const SortSeg S = segs[sg];
@@ -274,10 +279,10 @@ __global__ void __launch_bounds__(kSThreads) k_rank(const SortSeg* __restrict__ 
 
 void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, cudaStream_t s) {
     dim3 g1(blocks_for(n_max, kSThreads) > 64 ? 64 : blocks_for(n_max, kSThreads), 2 * n_lp);
-    k_hist2<<<g1, kSThreads, 0, s>>>(segs, ev);
-    k_cand<<<g1, kSThreads, 0, s>>>(segs, ev);
+    launch_k(k_hist2, g1, dim3(kSThreads), 0, s, segs, ev);
+    launch_k(k_cand, g1, dim3(kSThreads), 0, s, segs, ev);
     dim3 g2((unsigned)((n_max + kSThreads - 1) / kSThreads), 2 * n_lp);
-    k_rank<<<g2, kSThreads, 0, s>>>(segs, ev);
+    launch_k(k_rank, g2, dim3(kSThreads), 0, s, segs, ev);
     count_launches(3, __func__, s);
 }
 
@@ -289,6 +294,7 @@ void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev
 __global__ void __launch_bounds__(kSThreads) k_swap_refill(const PartDev* __restrict__ parts,
                                                            const SortSeg* __restrict__ segs, WorldDev G,
                                                            long long* counts, int64_t counts_stride, int n_steps) {
+    pdl_enter();
     const int lp = blockIdx.y;
     const PartDev& pd = parts[lp];
     const SortSeg E = segs[2 * lp], R = segs[2 * lp + 1];
@@ -331,7 +337,7 @@ __global__ void __launch_bounds__(kSThreads) k_swap_refill(const PartDev* __rest
 void launch_swap_refill(const PartDev* parts, int n_lp, int64_t cap_max, const SortSeg* segs, const WorldDev& world,
                         long long* counts, int64_t counts_stride, int n_steps, cudaStream_t s) {
     dim3 grid(blocks_for(cap_max < 1 ? 1 : cap_max, kSThreads / 32), n_lp);
-    k_swap_refill<<<grid, kSThreads, 0, s>>>(parts, segs, world, counts, counts_stride, n_steps);
+    launch_k(k_swap_refill, grid, dim3(kSThreads), 0, s, parts, segs, world, counts, counts_stride, n_steps);
     count_launches(1, __func__, s);
 }
 
@@ -435,6 +441,7 @@ __device__ __forceinline__ void bucket_starts(const uint32_t* __restrict__ h, ui
 __global__ void __launch_bounds__(256) k_perm_scatter(const PartDev* __restrict__ pdp, int n_epochs,
                                                       const SortSeg* __restrict__ segs, const uint32_t* __restrict__ hist,
                                                       uint32_t* __restrict__ cursor) {
+    pdl_enter();
     __shared__ uint32_t start[256];
     __shared__ long long sm[8];
     const int64_t n = pdp->n_train;
@@ -452,6 +459,7 @@ __global__ void __launch_bounds__(256) k_perm_scatter(const PartDev* __restrict_
 
 __global__ void __launch_bounds__(256) k_perm_rank(const PartDev* __restrict__ pdp, const SortSeg* __restrict__ segs,
                                                    const uint32_t* __restrict__ hist) {
+    pdl_enter();
     __shared__ uint32_t start[256];
     __shared__ long long sm[8];
     __shared__ unsigned long long sk[1024];
@@ -491,8 +499,8 @@ void launch_perm_build(const PartDev* pd_dev, int64_t n_train, uint64_t epoch0, 
     k_perm_keys<<<blocks_for(total < 1 ? 1 : total, kSThreads), kSThreads, 0, s>>>(pd_dev, epoch0, n_epochs, seed_lo,
                                                                                    seed_hi, segs, hist);
     unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n_train + 255) / 256, 64));
-    k_perm_scatter<<<dim3(gx, n_epochs), 256, 0, s>>>(pd_dev, n_epochs, segs, hist, cursor);
-    k_perm_rank<<<dim3(256, n_epochs), 256, 0, s>>>(pd_dev, segs, hist);
+    launch_k(k_perm_scatter, dim3(gx, n_epochs), dim3(256), 0, s, pd_dev, n_epochs, segs, (const uint32_t*)hist, cursor);
+    launch_k(k_perm_rank, dim3(256, n_epochs), dim3(256), 0, s, pd_dev, segs, (const uint32_t*)hist);
     count_launches(3, __func__, s);
 }
 
