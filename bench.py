@@ -16,9 +16,9 @@ Software pipeline (the paper's prepare-ahead, Alg.1 l.9): in timed iteration i
 the sampling of window i+1 runs on a second stream concurrently with the
 classify/gather/score of window i; both streams join at the end of the
 iteration.  Timing: per-iteration CUDA events, L2 flushed (256 MB write)
-between timed iterations, max over ranks.  `e2e` drives the same windows
-through the C ABI with the seeds in pinned HOST memory (H2D inside the call)
-and the per-minibatch counters read back to the host (D2H) every window.
+between timed iterations, max over ranks.  `e2e` drives the same pipeline
+through the C ABI with the seeds in pinned HOST memory (H2D inside mgnn_sample)
+and every window's per-minibatch counters read back to the host (D2H).
 """
 from __future__ import annotations
 
@@ -327,18 +327,36 @@ def main():
         counts_h.append(n0.cpu().pin_memory())
     h2d = n_inst * CFG.batch * 4 + n_inst * 4
     d2h = n_inst * 8 * 8
+    cbuf = [torch.zeros((n_inst, 8), dtype=torch.int64).pin_memory() for _ in range(2)]
+    ev_cnt = [torch.cuda.Event(), torch.cuda.Event()]
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2e_hits = 0
+
+    def sample_host(sl, i):                    # H2D of window i's seeds inside mgnn_sample (stream A)
+        sA.wait_event(ev_done[sl])
+        ctx.sample_ptr(sl, t_e2e + i * WINDOW, WINDOW, seeds_h[i].data_ptr(), counts_h[i].data_ptr(), True, sA)
+        ev_sampled[sl].record(sA)
+
     barrier()
-    ev0.record(stream)
-    for i in range(E2E):
-        ctx.sample_ptr(slot, t_e2e + i * WINDOW, WINDOW, seeds_h[i].data_ptr(), counts_h[i].data_ptr(), True, stream)
-        ctx.lookup_gather(slot, stream)
-        ctx.score(slot, stream)
-        out_counts = ctx.counts(slot, stream)          # D2H of the window's counters + stream sync
-        e2e_hits += int(out_counts[:, 2].sum())
+    ev0.record(sB)
+    sA.wait_event(ev0)
+    sample_host(slot, 0)
+    for i in range(E2E):                       # same two-stream pipeline, host buffers at both ends
+        if i + 1 < E2E:
+            sample_host(slot ^ 1, i + 1)
+        sB.wait_event(ev_sampled[slot])
+        ctx.lookup_gather(slot, sB)
+        ctx.score(slot, sB)
+        ctx.counts_async(slot, cbuf[i % 2].data_ptr(), sB)      # D2H of the window's counters
+        ev_cnt[i % 2].record(sB)
+        ev_done[slot].record(sB)
+        if i >= 1:                             # read the previous window's counters on the host
+            ev_cnt[(i - 1) % 2].synchronize()
+            e2e_hits += int(cbuf[(i - 1) % 2][:, 2].sum())
         slot ^= 1
-    ev1.record(stream)
+    ev1.record(sB)
+    ev_cnt[(E2E - 1) % 2].synchronize()
+    e2e_hits += int(cbuf[(E2E - 1) % 2][:, 2].sum())
     barrier()
     e2e_ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -371,7 +389,9 @@ def main():
             "dtype": "f32", "data": "synthetic", "config": workload(P),
             "hit_rate": hits / max(1, hits + misses),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "steps": E2E, "path": "mgnn_sample(host pinned seeds) + lookup_gather + score + counts_read"},
+                    "steps": E2E, "path": "two-stream pipeline: mgnn_sample(host pinned seeds, H2D) | "
+                                          "lookup_gather + score_evict_refill + counts_read_async (D2H), "
+                                          "host reads each window's counters"},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": "k_gather (classify + feature-row gather)",
                          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",

@@ -167,6 +167,10 @@ MGNN_API mgnn_status mgnn_window_get(mgnn_ctx ctx, int32_t slot, mgnn_window* ou
 /* Copy the window's counters ([n_inst][MGNN_C_N] int64) to host memory and
  * synchronise `stream`. */
 MGNN_API mgnn_status mgnn_counts_read(mgnn_ctx ctx, int32_t slot, int64_t* host_counts, mgnn_stream stream);
+/* Asynchronous variant: enqueues the copy of the window's counters into host_counts (pinned
+ * memory) on `stream` and returns; the caller synchronises (stream or event) before reading
+ * them.  Device-side seed errors are reported by the next mgnn_counts_read. */
+MGNN_API mgnn_status mgnn_counts_read_async(mgnn_ctx ctx, int32_t slot, int64_t* host_counts, mgnn_stream stream);
 
 /* Host copies of local partition lp's prefetcher state (synchronous):
  * node_ids[cap] (BUF in slot order), se[cap], sa[n_halo] and slot_of[n_halo]

@@ -17,6 +17,7 @@ SYMBOLS = [
     "mgnn_alpha_default", "mgnn_ctx_create", "mgnn_destroy", "mgnn_last_error", "mgnn_partition_load",
     "mgnn_table_export", "mgnn_table_import", "mgnn_buffer_init", "mgnn_sampler_config", "mgnn_sample",
     "mgnn_lookup_gather", "mgnn_score_evict_refill", "mgnn_window_get", "mgnn_counts_read",
+    "mgnn_counts_read_async",
     "mgnn_buffer_snapshot", "mgnn_part_info", "mgnn_halo_get", "mgnn_table_row", "mgnn_launch_count",
     "mgnn_profile_enable", "mgnn_profile_read", "mgnn_profile_kernels",
 ]
@@ -75,6 +76,7 @@ def load(path: str = LIB_PATH):
         "mgnn_score_evict_refill": (S, [P, I32, P]),
         "mgnn_window_get": (S, [P, I32, P]),
         "mgnn_counts_read": (S, [P, I32, P, P]),
+        "mgnn_counts_read_async": (S, [P, I32, P, P]),
         "mgnn_buffer_snapshot": (S, [P, I32, P, P, P, P, P]),
         "mgnn_part_info": (S, [P, I32, P]),
         "mgnn_halo_get": (S, [P, I32, P, P]),

@@ -964,6 +964,17 @@ mgnn_status mgnn_window_get(mgnn_ctx ctx, int32_t slot, mgnn_window* out) {
     return MGNN_OK;
 }
 
+mgnn_status mgnn_counts_read_async(mgnn_ctx ctx, int32_t slot, int64_t* host_counts, mgnn_stream stream) {
+    GUARD();
+    if (slot < 0 || slot > 1 || !host_counts) return fail(ctx, MGNN_EINVAL, "bad slot");
+    Win& w = ctx->win[slot];
+    if (!w.sampled) return fail(ctx, MGNN_ESTATE, "slot not sampled");
+    const int64_t M = (int64_t)ctx->parts.size() * w.n_steps;
+    CK(cudaMemcpyAsync(host_counts, w.counts, M * 8 * sizeof(long long), cudaMemcpyDeviceToHost,
+                       (cudaStream_t)stream));
+    return MGNN_OK;
+}
+
 mgnn_status mgnn_counts_read(mgnn_ctx ctx, int32_t slot, int64_t* host_counts, mgnn_stream stream) {
     GUARD();
     if (slot < 0 || slot > 1 || !host_counts) return fail(ctx, MGNN_EINVAL, "bad slot");

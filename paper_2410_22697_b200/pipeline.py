@@ -160,6 +160,11 @@ class Context:
         self._chk("mgnn_counts_read", self.L.mgnn_counts_read(self._h, slot, _ptr(out), _stream(stream)))
         return out
 
+    def counts_async(self, slot: int, host_ptr: int, stream=None):
+        """Enqueue the D2H copy of the window's counters into pinned host memory (no sync)."""
+        self._chk("mgnn_counts_read_async",
+                  self.L.mgnn_counts_read_async(self._h, slot, C.c_void_p(host_ptr), _stream(stream)))
+
     def instance(self, slot: int, m: int, with_x: bool = True) -> Dict[str, np.ndarray]:
         """Host copies of instance m of a window (tests; synchronises)."""
         import torch
