@@ -302,6 +302,7 @@ def main():
     c = ctx.counts(slot ^ 1, stream)            # the last consumed window
     hits += int(c[:, 2].sum())
     misses += int(c[:, 3].sum())
+    peer_rows = int(c[:, 7].sum())              # rows read from another GPU's table over NVLink
     ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = sum(ms)
     mine_ms = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
@@ -401,6 +402,12 @@ def main():
             "clocks": clocks,
             "wall_s_timed_region": wall,
         }
+        if world > 1:
+            nv_bytes = peer_rows * CFG.feat_dim * 4
+            line["nvlink"] = {"peer_rows_per_window": peer_rows, "bytes_per_window": nv_bytes,
+                              "gbs_during_gather": nv_bytes / (g_avg_ms / 1e3) / 1e9 if g_avg_ms > 0 else None,
+                              "note": "miss + refill rows whose owner is on another GPU, read by peer loads "
+                                      "inside k_gather / k_swap_refill (last timed window)"}
         if world == 1 and not args.no_cpu_baseline:
             rate, n_mb, el = oracle_rate(parts, P, f_bp, gamma, delta, args.cpu_budget)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",

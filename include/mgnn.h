@@ -80,6 +80,7 @@ enum {
     MGNN_C_EVICTED = 4,    /* k of the eviction round ending at this step (Alg.2 l.14) */
     MGNN_C_REFILLED = 5,   /* = k (constant |BUF|) */
     MGNN_C_ROWS_FETCHED = 6, /* remote rows this step = misses + refills */
+    MGNN_C_PEER_ROWS = 7,    /* of those, rows read from another GPU's table over NVLink */
     MGNN_C_N = 8
 };
 

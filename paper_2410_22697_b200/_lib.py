@@ -9,7 +9,7 @@ LIB_PATH = os.environ.get("MGNN_LIB", os.path.join(HERE, "libmgnn.so"))   # over
 
 MAX_LAYERS = 8
 IPC_HANDLE_BYTES = 64
-C_NODES, C_LOCAL, C_HIT, C_MISS, C_EVICTED, C_REFILLED, C_ROWS_FETCHED, C_N = 0, 1, 2, 3, 4, 5, 6, 8
+C_NODES, C_LOCAL, C_HIT, C_MISS, C_EVICTED, C_REFILLED, C_ROWS_FETCHED, C_PEER_ROWS, C_N = 0, 1, 2, 3, 4, 5, 6, 7, 8
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 5: "ESTATE", 6: "EOVERFLOW"}
 
 # every symbol include/mgnn.h declares (checked by tests/test_abi.py)

@@ -125,6 +125,7 @@ struct mgnn_ctx_s {
     std::vector<void*> ipc_opened;
     int64_t* d_bounds = nullptr;
     const float** d_tables = nullptr;
+    uint8_t* d_on_peer = nullptr;        // [P]: table imported from another process (NVLink)
     PartDev* d_parts = nullptr;
     int32_t* d_err = nullptr;
     long long* d_gathered = nullptr;
@@ -260,6 +261,9 @@ mgnn_status upload_parts(mgnn_ctx ctx) {
 
 mgnn_status upload_tables(mgnn_ctx ctx) {
     CK(cudaMemcpy((void*)ctx->d_tables, ctx->tables.data(), ctx->P * sizeof(float*), cudaMemcpyHostToDevice));
+    std::vector<uint8_t> peer(ctx->P);
+    for (int q = 0; q < ctx->P; ++q) peer[q] = (ctx->tables[q] && ctx->lp_of[q] < 0) ? 1 : 0;
+    CK(cudaMemcpy(ctx->d_on_peer, peer.data(), ctx->P, cudaMemcpyHostToDevice));
     return MGNN_OK;
 }
 
@@ -269,6 +273,7 @@ WorldDev world_of(mgnn_ctx ctx) {
     w.pitch = ctx->pitch;
     w.bounds = ctx->d_bounds;
     w.tables = ctx->d_tables;
+    w.on_peer = ctx->d_on_peer;
     return w;
 }
 
@@ -387,6 +392,8 @@ mgnn_status mgnn_ctx_create(int32_t device, int32_t n_parts, int64_t n_global, c
     chk(cudaMemcpy(ctx->d_bounds, bounds, (n_parts + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
     chk(dalloc((float***)&ctx->d_tables, n_parts));
     chk(cudaMemset((void*)ctx->d_tables, 0, n_parts * sizeof(float*)));
+    chk(dalloc(&ctx->d_on_peer, n_parts));
+    chk(cudaMemset(ctx->d_on_peer, 0, n_parts));
     chk(dalloc(&ctx->d_err, 1));
     chk(cudaMemset(ctx->d_err, 0, sizeof(int32_t)));
     chk(dalloc(&ctx->d_gathered, 1));
@@ -416,6 +423,7 @@ void mgnn_destroy(mgnn_ctx ctx) {
     }
     dfree(ctx->d_bounds);
     dfree(ctx->d_tables);
+    dfree(ctx->d_on_peer);
     dfree(ctx->d_parts);
     dfree(ctx->d_err);
     dfree(ctx->d_gathered);

@@ -88,6 +88,7 @@ struct WorldDev {
     int32_t pitch;
     const int64_t* bounds;      // [P+1]
     const float* const* tables; // [P] device-accessible pointers (NVLink peer pointers for remote)
+    const uint8_t* on_peer;     // [P] 1 if the table lives on another GPU (rows cross NVLink)
 };
 
 __device__ __forceinline__ int owner_of(const int64_t* __restrict__ bounds, int P, int64_t v) {

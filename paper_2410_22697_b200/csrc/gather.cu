@@ -34,11 +34,11 @@ __device__ __forceinline__ void stcs4(float* p, float4 v) { __stcs(reinterpret_c
 template <bool WIDE>
 __global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
     pdl_enter();
-    __shared__ unsigned long long cnt_sh[3];
+    __shared__ unsigned long long cnt_sh[4];
     const int m = blockIdx.y;
     const int lp = m / W.n_steps, w = m % W.n_steps;
     const PartDev& pd = W.parts[lp];
-    if (threadIdx.x < 3) cnt_sh[threadIdx.x] = 0;
+    if (threadIdx.x < 4) cnt_sh[threadIdx.x] = 0;
     __syncthreads();
     const int64_t U = W.hop_size[(int64_t)m * (kMaxLayers + 1) + W.L];
     const int lane = threadIdx.x & 31;
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
     float* X = W.X + (int64_t)m * W.ucap * pitch;
     const int64_t h_below = pd.h_below, n_local = pd.n_local, lo = pd.lo;
     const unsigned long long wbit = 1ull << w;
-    unsigned n_loc = 0, n_hit = 0, n_miss = 0;
+    unsigned n_loc = 0, n_hit = 0, n_miss = 0, n_peer = 0;
     const int64_t stride = (int64_t)gridDim.x * kGWarps * 32;
     for (int64_t f0 = ((int64_t)blockIdx.x * kGWarps + (threadIdx.x >> 5)) * 32; f0 < U; f0 += stride) {
         // ---- classify 32 nodes, one per lane
@@ -76,14 +76,15 @@ __global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
                     const int qo = owner_of(G.bounds, G.n_parts, gid);
                     src = G.tables[qo] + ((int64_t)gid - G.bounds[qo]) * pitch;
                     atomicAdd(&pd.sa[h], 1.0f);
-                    cls = 2;
+                    cls = G.on_peer[qo] ? 4 : 2;
                 }
             }
             fgid[f] = gid;
         }
         n_loc += __popc(__ballot_sync(kFull, cls == 0));
         n_hit += __popc(__ballot_sync(kFull, cls == 1));
-        n_miss += __popc(__ballot_sync(kFull, cls == 2));
+        n_miss += __popc(__ballot_sync(kFull, cls >= 2 && cls != 3));
+        n_peer += __popc(__ballot_sync(kFull, cls == 4));
         const int nrows = (int)(U - f0 < 32 ? U - f0 : 32);
         float* Xw = X + f0 * pitch;
         // ---- copy the rows, several independent 16-B loads in flight per lane
@@ -133,6 +134,7 @@ __global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
         if (n_loc) atomicAdd(&cnt_sh[0], (unsigned long long)n_loc);
         if (n_hit) atomicAdd(&cnt_sh[1], (unsigned long long)n_hit);
         if (n_miss) atomicAdd(&cnt_sh[2], (unsigned long long)n_miss);
+        if (n_peer) atomicAdd(&cnt_sh[3], (unsigned long long)n_peer);
     }
     __syncthreads();
     long long* cn = W.counts + (int64_t)m * 8;
@@ -143,6 +145,7 @@ __global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
             atomicAdd((unsigned long long*)&cn[3], cnt_sh[2]);
             atomicAdd((unsigned long long*)&cn[6], cnt_sh[2]);
         }
+        if (cnt_sh[3]) atomicAdd((unsigned long long*)&cn[7], cnt_sh[3]);
         const unsigned long long rows = cnt_sh[0] + cnt_sh[1] + cnt_sh[2];
         if (rows && W.gathered_rows) atomicAdd((unsigned long long*)W.gathered_rows, rows);
         if (blockIdx.x == 0) cn[0] = U;
@@ -193,12 +196,12 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
     pdl_enter();
     extern __shared__ __align__(128) unsigned char tsm[];
     __shared__ __align__(8) uint64_t bars[kTWarps][2];
-    __shared__ unsigned long long cnt_sh[3];
+    __shared__ unsigned long long cnt_sh[4];
     const int m = blockIdx.y;
     const int lp = m / W.n_steps, w = m % W.n_steps;
     const PartDev& pd = W.parts[lp];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x < 3) cnt_sh[threadIdx.x] = 0;
+    if (threadIdx.x < 4) cnt_sh[threadIdx.x] = 0;
     if (lane == 0) {
         mbar_init(&bars[warp][0], 1);
         mbar_init(&bars[warp][1], 1);
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
     unsigned char* stage[2] = {tsm + (size_t)warp * 2 * kTStageBytes, tsm + (size_t)warp * 2 * kTStageBytes + kTStageBytes};
     const int64_t h_below = pd.h_below, n_local = pd.n_local, lo = pd.lo;
     const unsigned long long wbit = 1ull << w;
-    unsigned n_loc = 0, n_hit = 0, n_miss = 0;
+    unsigned n_loc = 0, n_hit = 0, n_miss = 0, n_peer = 0;
     const int64_t stride = (int64_t)gridDim.x * kTWarps * R;
     uint32_t phase[2] = {0u, 0u};
     // classify chunk starting at f0 (lanes < R) and issue its row loads into stage st
@@ -242,14 +245,15 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
                     const int qo = owner_of(G.bounds, G.n_parts, gid);
                     src = G.tables[qo] + ((int64_t)gid - G.bounds[qo]) * pitch;
                     atomicAdd(&pd.sa[h], 1.0f);
-                    cls = 2;
+                    cls = G.on_peer[qo] ? 4 : 2;
                 }
             }
             fgid[f] = gid;
         }
         n_loc += __popc(__ballot_sync(kFull, cls == 0));
         n_hit += __popc(__ballot_sync(kFull, cls == 1));
-        n_miss += __popc(__ballot_sync(kFull, cls == 2));
+        n_miss += __popc(__ballot_sync(kFull, cls >= 2 && cls != 3));
+        n_peer += __popc(__ballot_sync(kFull, cls == 4));
         const int nrows = (int)(U - f0 < R ? U - f0 : R);
         bulk_wait_read0();                       // stores that last read this stage are done
         __syncwarp();
@@ -278,6 +282,7 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
         if (n_loc) atomicAdd(&cnt_sh[0], (unsigned long long)n_loc);
         if (n_hit) atomicAdd(&cnt_sh[1], (unsigned long long)n_hit);
         if (n_miss) atomicAdd(&cnt_sh[2], (unsigned long long)n_miss);
+        if (n_peer) atomicAdd(&cnt_sh[3], (unsigned long long)n_peer);
     }
     __syncthreads();
     long long* cn = W.counts + (int64_t)m * 8;
@@ -288,6 +293,7 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
             atomicAdd((unsigned long long*)&cn[3], cnt_sh[2]);
             atomicAdd((unsigned long long*)&cn[6], cnt_sh[2]);
         }
+        if (cnt_sh[3]) atomicAdd((unsigned long long*)&cn[7], cnt_sh[3]);
         const unsigned long long rows = cnt_sh[0] + cnt_sh[1] + cnt_sh[2];
         if (rows && W.gathered_rows) atomicAdd((unsigned long long*)W.gathered_rows, rows);
         if (blockIdx.x == 0) cn[0] = U;

@@ -331,6 +331,8 @@ __global__ void __launch_bounds__(kSThreads) k_swap_refill(const PartDev* __rest
         float* dst = pd.rows + (int64_t)s * pitch;
         for (int c = lane * 4; c < pitch; c += 128)
             *reinterpret_cast<float4*>(dst + c) = __ldg(reinterpret_cast<const float4*>(src + c));
+        if (lane == 0 && G.on_peer[q])
+            atomicAdd((unsigned long long*)(counts + ((int64_t)lp * n_steps + (n_steps - 1)) * counts_stride + 7), 1ull);
     }
 }
 

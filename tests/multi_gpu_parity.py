@@ -40,7 +40,7 @@ def main():
                         [a.delta] * a.windows, hosted=hosted, device=local, exchange=True,
                         sample_every=1 if a.config == "cfg1" else 9, check_x_rows=0 if a.config == "cfg1" else 2048)
         print(f"[rank {rank}] parity ok: {st}", flush=True)
-        assert st["misses"] > 0 and st["evicted"] > 0
+        assert st["misses"] > 0 and st["evicted"] > 0 and st["peer_rows"] > 0
     except Exception as e:  # report, then fail the collective result
         print(f"[rank {rank}] FAILED: {e!r}", flush=True)
         ok.zero_()

@@ -90,6 +90,12 @@ def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, g
                 got = [gc[0], gc[1], gc[2], gc[3], gc[4], gc[6]]
                 want = [oc["n_nodes"], oc["n_local"], oc["n_hit"], oc["n_miss"], oc["n_evicted"], oc["rows_fetched"]]
                 assert got == want, (pid, step, got, want)      # counts: every step
+                # NVLink rows (counts[7]): misses + refills owned by a partition on another GPU
+                refill = gc[5] if w == wlen - 1 else 0
+                assert 0 <= gc[7] <= gc[3] + refill, (pid, step, gc[7])
+                if not exchange:
+                    assert gc[7] == 0, (pid, step, gc[7])
+                stats["peer_rows"] = stats.get("peer_rows", 0) + int(gc[7])
                 stats["steps"] += 1
                 stats["hits"] += oc["n_hit"]
                 stats["misses"] += oc["n_miss"]
