@@ -120,28 +120,40 @@ __device__ __forceinline__ unsigned long long ld_status(const unsigned long long
     return v;
 }
 
-// Called by ONE thread of tile `tile` with the tile's aggregate; returns the
-// exclusive prefix of all earlier tiles of the same segment.  status[] must
-// be zero before the launch; tiles are claimed in order (dynamic tile ids), so
-// every waited-on predecessor is already resident.
+// Called by ALL 32 lanes of one warp of tile `tile` with the tile's aggregate;
+// returns (to every lane) the exclusive prefix of all earlier tiles of the
+// same segment.  The warp inspects 32 predecessors per round (one status load
+// per lane), so a chain of published aggregates costs one L2 round trip per 32
+// tiles instead of one per tile.  status[] must be zero before the launch;
+// tiles are claimed in order (dynamic tile ids), so every waited-on
+// predecessor is already resident.
 __device__ __forceinline__ unsigned long long lookback_exclusive(unsigned long long* status, int tile,
                                                                  unsigned long long agg) {
+    const int lane = threadIdx.x & 31;
     if (tile == 0) {
-        st_status(&status[0], kFlagInc | agg);
+        if (lane == 0) st_status(&status[0], kFlagInc | agg);
         return 0;
     }
-    st_status(&status[tile], kFlagAgg | agg);
+    if (lane == 0) st_status(&status[tile], kFlagAgg | agg);
     unsigned long long excl = 0;
-    int j = tile - 1;
+    int base = tile - 1;                       // lane l looks at tile base - l
     while (true) {
-        unsigned long long s = ld_status(&status[j]);
-        unsigned long long f = s & ~kValMask;
-        if (f == 0) continue;  // predecessor not published yet
-        excl += s & kValMask;
-        if (f == kFlagInc) break;
-        --j;
+        const int j = base - lane;
+        const unsigned long long s = j >= 0 ? ld_status(&status[j]) : kFlagInc;
+        const unsigned long long f = s & ~kValMask;
+        const unsigned inc = __ballot_sync(kFull, f == kFlagInc);
+        const unsigned none = __ballot_sync(kFull, f == 0);
+        const int first = inc ? __ffs(inc) - 1 : 31;          // nearest inclusive predecessor
+        const unsigned need = first == 31 ? kFull : ((2u << first) - 1u);
+        if (none & need) continue;             // a needed predecessor has not published yet
+        unsigned long long v = lane <= first ? (s & kValMask) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+        excl += v;
+        if (inc) break;
+        base -= 32;
     }
-    st_status(&status[tile], kFlagInc | (excl + agg));
+    if (lane == 0) st_status(&status[tile], kFlagInc | (excl + agg));
     return excl;
 }
 

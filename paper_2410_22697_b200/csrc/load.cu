@@ -52,7 +52,10 @@ __global__ void __launch_bounds__(kLThreads) k_bitmap_to_ids(const uint32_t* __r
     }
     long long agg;
     long long excl = block_excl_scan256(cnt, sm, &agg);
-    if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status, tile, (unsigned long long)agg);
+    if (threadIdx.x < 32) {
+            const unsigned long long pv = lookback_exclusive(sc.status, tile, (unsigned long long)agg);
+            if (threadIdx.x == 0) prefix_sh = (long long)pv;
+        }
     __syncthreads();
     int64_t pos = prefix_sh + excl;
     for (int i = 0; i < 4; ++i) {

@@ -90,30 +90,45 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
 
 // ------------------------------------------------------------------ one hop: counts, offsets, samples
 // T = frontier nodes per tile (64 or 256; small tiles give small hops enough blocks).
+// Per tile: (1) thread per node: deg-capped count, block scan -> tile-relative
+// sample offsets; (2) warp 0 resolves the tile's global offset by look-back
+// while warps 1..7 produce the CSR index of every sample (a node with deg <= k
+// takes its whole neighbourhood, R#3; a node with deg > k is drawn by a group
+// of k lanes: Philox + Floyd, R#4-R#6); (3) all threads load the sampled
+// neighbours' ranks, write the columns (coalesced) and mark new nodes.
 __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max, int T) {
     pdl_enter();
     __shared__ long long sm[8];
-    __shared__ int tslot;
+    __shared__ int tslot, n_draw;
     __shared__ long long prefix_sh;
-    __shared__ long long s_row[kThreads], s_b0[kThreads], s_d[kThreads], s_o[kThreads];
+    __shared__ long long s_b0[kThreads];
+    __shared__ int s_row[kThreads], s_d[kThreads], s_o[kThreads], s_draw[kThreads];
     extern __shared__ __align__(16) unsigned char dyn_smem[];
+    long long* sidx = reinterpret_cast<long long*>(dyn_smem);   // [T * k] CSR index of each sample of the tile
     const int m = blockIdx.y;
     const int lp = m / W.n_steps, w = m % W.n_steps;
     const PartDev& pd = W.parts[lp];
     const int64_t nF = W.hop_size[(int64_t)m * (kMaxLayers + 1) + hop];
     const int64_t ntiles = (nF + T - 1) / T;
     int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
+    const int k = W.k_hop[hop];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per = 32 / k;                                // k lanes per drawn node, `per` nodes per warp step
+    const int gi = lane / k, gl = lane - gi * k, gbase = gi * k;
+    const uint32_t c1 = (uint32_t)hop << 16;
+    const uint32_t c3 = ((uint32_t)pd.part_id << 8) | kStreamSample;
+    const uint32_t step = (uint32_t)(W.step0 + (uint64_t)w);
+    const int64_t h_below = pd.h_below, n_local = pd.n_local, lo = pd.lo;
     // persistent: blocks claim tiles in order until the instance's frontier is exhausted
     for (;;) {
+        if (threadIdx.x == 0) n_draw = 0;
         const int tile = claim_tile(sc.tilectr + m, &tslot);
         if (tile >= ntiles) {
             if (tile == 0 && threadIdx.x == 0) off[0] = 0;   // empty F_i
             break;
         }
-        const int k = W.k_hop[hop];
         const int64_t f = (int64_t)tile * T + threadIdx.x;
         const bool mine = threadIdx.x < T && f < nF;
-        const int64_t h_below = pd.h_below, n_local = pd.n_local;
         int64_t row = -1, b0 = 0, d = 0;
         if (mine) {
             row = (int64_t)W.fr_rank[(int64_t)m * W.ucap + f] - h_below;
@@ -126,65 +141,57 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
         }
         const int cnt = (int)(d < k ? d : k);              // |sample| = min(deg, k) (R#3)
         long long agg;
-        const long long excl = block_excl_scan256(cnt, sm, &agg);
-        if (threadIdx.x == 0)
-            prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile, (unsigned long long)agg);
-        __syncthreads();
-        const int64_t o = prefix_sh + excl;
-        if (tile == 0 && threadIdx.x == 0) off[0] = 0;
-        if (mine) {
-            MGNN_CHECK(f + 1 < W.off_stride[hop], "off f=%lld", (long long)f);
-            off[f + 1] = o + cnt;
-        }
-        if (threadIdx.x < T) {
-            s_row[threadIdx.x] = cnt > 0 ? row : -1;
+        const int excl = (int)block_excl_scan256(cnt, sm, &agg);   // tile-relative offset (< T * k)
+        if (threadIdx.x < T) s_o[threadIdx.x] = excl;
+        const bool draw = cnt > 0 && d > k;
+        if (cnt > 0 && !draw)                              // whole neighbourhood in CSR order (R#3)
+            for (int j = 0; j < cnt; ++j) sidx[excl + j] = b0 + j;
+        const unsigned bal = __ballot_sync(kFull, draw);
+        int dbase = 0;
+        if (lane == 0 && bal) dbase = atomicAdd(&n_draw, __popc(bal));
+        dbase = __shfl_sync(kFull, dbase, 0);
+        if (draw) {
+            s_draw[dbase + __popc(bal & ((1u << lane) - 1u))] = threadIdx.x;
+            s_row[threadIdx.x] = (int)row;
             s_b0[threadIdx.x] = b0;
-            s_d[threadIdx.x] = d;
-            s_o[threadIdx.x] = o;
+            s_d[threadIdx.x] = (int)d;
         }
         __syncthreads();
-        // ---- phase A: positions.  k lanes per node, 8 * floor(32/k) nodes of the tile side by side;
-        // lane j of a group draws slot j, Floyd collisions resolved by k shuffles inside the group.
-        // Only CSR indices are produced here (no global loads), staged in shared memory.
-        long long* sidx = reinterpret_cast<long long*>(dyn_smem);   // [T * k] CSR index of each sample of the tile
-        const long long o_tile = prefix_sh;
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        const int G = k;                                   // one lane per slot; 32/k nodes per warp step
-        const int per = 32 / G;
-        const int gi = lane / G, gl = lane - gi * G, gbase = gi * G;
-        const uint32_t c1 = (uint32_t)hop << 16;
-        const uint32_t c3 = ((uint32_t)pd.part_id << 8) | kStreamSample;
-        const uint32_t step = (uint32_t)(W.step0 + (uint64_t)w);
-        const int64_t lo = pd.lo;
-        for (int base = warp * per; base < T; base += 8 * per) {
-            const int idx = base + gi;                     // this group's node in the tile
-            const bool ingroup = gi < per && idx < T;      // lanes past per*k idle
-            const long long n_row = ingroup ? s_row[idx] : -1;
-            const long long n_d = ingroup ? s_d[idx] : 0;
-            const bool active = n_row >= 0;
-            const bool whole = n_d <= k;                   // whole neighbourhood in CSR order (R#3)
-            uint32_t r = 0, t = 0;
-            bool coll = false;
-            if (__any_sync(kFull, active && !whole)) {     // some group draws: Philox + Floyd
-                if (active && !whole && gl < k) {
-                    const u4 u = philox4x32_10(u4{(uint32_t)(lo + n_row), c1 | (uint32_t)gl, step, c3}, W.seed_lo,
-                                               W.seed_hi);
-                    t = (uint32_t)(n_d - k + gl);
+        if (warp == 0) {
+            // global offset of the tile; overlaps with the sample draws of warps 1..7
+            const unsigned long long pv =
+                lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile, (unsigned long long)agg);
+            if (lane == 0) prefix_sh = (long long)pv;
+        } else {
+            // drawn nodes: k lanes per node, lane j draws slot j; Floyd collisions by k in-group shuffles
+            const int nd = n_draw;
+            for (int bd = (warp - 1) * per; bd < nd; bd += 7 * per) {
+                const int di = bd + gi;
+                const bool active = gi < per && di < nd;
+                const int x = active ? s_draw[di] : 0;
+                uint32_t r = 0, t = 0;
+                bool coll = false;
+                if (active) {
+                    const u4 u = philox4x32_10(u4{(uint32_t)(lo + s_row[x]), c1 | (uint32_t)gl, step, c3},
+                                               W.seed_lo, W.seed_hi);
+                    t = (uint32_t)(s_d[x] - k + gl);
                     r = __umulhi(u.x, t + 1u);             // floor(u (t+1) / 2^32)
                 }
                 for (int jj = 0; jj < k; ++jj) {           // Floyd: pos_j = r_j unless already chosen, else t_j
                     const uint32_t pj = __shfl_sync(kFull, coll ? t : r, (gbase + jj) & 31);
                     if (gl > jj && r == pj) coll = true;
                 }
-            }
-            if (active && gl < (whole ? (int)n_d : k)) {
-                const uint32_t pos = whole ? (uint32_t)gl : (coll ? t : r);
-                sidx[s_o[idx] - o_tile + gl] = s_b0[idx] + pos;
+                if (active) sidx[s_o[x] + gl] = s_b0[x] + (coll ? t : r);
             }
         }
         __syncthreads();
-        // ---- phase B: every sample of the tile in parallel: neighbour rank, coalesced column write, and
-        // the new-node mark unless the neighbour is already in F_i.
+        // every sample of the tile in parallel: neighbour rank, coalesced column write, new-node mark
+        const long long o_tile = prefix_sh;
+        if (mine) {
+            MGNN_CHECK(f + 1 < W.off_stride[hop], "off f=%lld", (long long)f);
+            off[f + 1] = o_tile + excl + cnt;
+        }
+        if (tile == 0 && threadIdx.x == 0) off[0] = 0;
         int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop] + o_tile;
         const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
         uint32_t* nb = W.nb + (int64_t)m * W.bm_words;
@@ -220,8 +227,11 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
     long long agg;
     const long long excl = block_excl_scan256(__popc(b), sm, &agg);
     int64_t* hs = W.hop_size + (int64_t)m * (kMaxLayers + 1);
-    if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
+    if (threadIdx.x < 32) {
+            const unsigned long long pv = lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
                                                                      (unsigned long long)agg);
+            if (threadIdx.x == 0) prefix_sh = (long long)pv;
+        }
     __syncthreads();
     const int64_t nF = hs[hop];
     int64_t pos = nF + prefix_sh + excl;
@@ -254,7 +264,17 @@ __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
         const int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
         int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop];
         const int64_t E = off[hs[hop]];
-        for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < E; e += stride) cols[e] = posof[cols[e]];
+        // 4 independent gathers in flight per thread (the posof loads are random L2 reads)
+        for (int64_t e0 = (int64_t)blockIdx.x * kThreads * 4 + threadIdx.x; e0 < E; e0 += stride * 4) {
+            int32_t c[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) c[j] = e0 + j * kThreads < E ? cols[e0 + j * kThreads] : 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) c[j] = posof[c[j]];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (e0 + j * kThreads < E) cols[e0 + j * kThreads] = c[j];
+        }
     }
 }
 
@@ -295,7 +315,7 @@ void launch_compact(const WinDev& w, int hop, Scratch sc, cudaStream_t s) {
 void launch_relabel(const WinDev& w, cudaStream_t s) {
     int64_t e_max = 0;
     for (int i = 0; i < w.L; ++i) e_max = w.col_stride[i] > e_max ? w.col_stride[i] : e_max;
-    dim3 grid(grid_x_for(e_max, kThreads, w.n_inst), w.n_inst);
+    dim3 grid(grid_x_for(e_max, kThreads * 4, w.n_inst), w.n_inst);
     launch_k(k_relabel, grid, dim3(kThreads), 0, s, w);
     count_launches(1, __func__, s);
 }

@@ -91,8 +91,11 @@ __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict_
         }
         long long agg;
         long long excl = block_excl_scan256(cnt, sm, &agg);
-        if (threadIdx.x == 0) prefix_sh = (long long)lookback_exclusive(sc.status + (int64_t)sg * tiles_max, tile,
+        if (threadIdx.x < 32) {
+            const unsigned long long pv = lookback_exclusive(sc.status + (int64_t)sg * tiles_max, tile,
                                                                          (unsigned long long)agg);
+            if (threadIdx.x == 0) prefix_sh = (long long)pv;
+        }
         __syncthreads();
         int64_t pos = prefix_sh + excl;
         const SortSeg out = segs[sg];
