@@ -231,3 +231,30 @@ def describe(g: Graph, parts: List[PartitionInput]) -> dict:
         "max_deg": int(deg.max()) if deg.size else 0, "median_deg": float(np.median(deg)) if deg.size else 0.0,
         "n_train": int(g.train_mask.sum()), "halo_over_local": halo,
     }
+
+
+# ------------------------------------------------------------------ consumer weights (A14)
+HIDDEN = 128                    # GraphSAGE hidden size (SURVEY §8(a) A14: unstated in the paper -> 128)
+N_CLASSES = {"cfg1": 16, "arxiv": 40, "reddit": 41, "products": 47, "papers": 172, "papers_s32": 172}
+SAGE_SEED = GRAPH_SEED + 3
+
+
+def sage_dims(feat_dim: int, n_layers: int, n_classes: int, hidden: int = HIDDEN) -> List[int]:
+    """[D, hidden, ..., hidden, C]: layer widths of an n_layers-deep GraphSAGE."""
+    return [feat_dim] + [hidden] * (n_layers - 1) + [n_classes]
+
+
+def sage_weights(dims: List[int], seed: int = SAGE_SEED):
+    """Random-init fp32 weights, one (W_self, W_neigh, bias) triple per layer in nn.Linear
+    layout [d_out][d_in]: Glorot-uniform matrices, small uniform biases.  Input generation
+    only (the stand-in for a trained model; there are no trained weights to load)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    out = []
+    for l in range(len(dims) - 1):
+        d_in, d_out = dims[l], dims[l + 1]
+        lim = float(np.sqrt(6.0 / (d_in + d_out)))
+        ws = rng.uniform(-lim, lim, (d_out, d_in)).astype(np.float32)
+        wn = rng.uniform(-lim, lim, (d_out, d_in)).astype(np.float32)
+        b = rng.uniform(-0.1, 0.1, d_out).astype(np.float32)
+        out.append((ws, wn, b))
+    return out

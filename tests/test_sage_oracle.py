@@ -1,0 +1,167 @@
+"""Pins of the consumer oracle (oracle/sage.py) against what the
+definition fixes: hand-worked examples, closed forms, special cases and an
+independent formulation through a library primitive (torch sparse CSR matmul).
+CPU only."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from inputs import synth
+from oracle import oracle as O
+from oracle import sage as S
+
+
+def _layer(h, n_dst, off, nbr, ws, wn, b, relu):
+    return S.sage_layer(np.asarray(h, np.float64), n_dst, np.asarray(off), np.asarray(nbr),
+                        np.asarray(ws, np.float64), np.asarray(wn, np.float64), np.asarray(b, np.float64), relu)
+
+
+def test_identity_self_weight_returns_dst_rows():
+    # W_self = I, W_neigh = 0, b = 0, no activation: H^1 = H^0[:n_dst] exactly
+    rng = np.random.default_rng(0)
+    h = rng.standard_normal((6, 4))
+    off = np.array([0, 2, 3, 3])
+    nbr = np.array([4, 5, 1])
+    out = _layer(h, 3, off, nbr, np.eye(4), np.zeros((4, 4)), np.zeros(4), relu=False)
+    assert np.array_equal(out, h[:3])
+
+
+def test_star_neighbour_mean_hand_value():
+    # star: centre (row 0) with sampled leaves rows 1,2,3 of features 1, 2, 6 -> mean 3;
+    # W_neigh = [[1]], W_self = [[0]], b = 0.5 -> 3.5 (hand computed)
+    h = np.array([[10.0], [1.0], [2.0], [6.0]])
+    out = _layer(h, 1, [0, 3], [1, 2, 3], [[0.0]], [[1.0]], [0.5], relu=False)
+    assert out.shape == (1, 1) and out[0, 0] == 3.5
+    # self term only: W_self = [[2]], W_neigh = 0 -> 20
+    out = _layer(h, 1, [0, 3], [1, 2, 3], [[2.0]], [[0.0]], [0.0], relu=False)
+    assert out[0, 0] == 20.0
+
+
+def test_empty_neighbourhood_mean_is_zero():
+    # a destination without sampled neighbours gets W_self x + b (DGL mean of nothing = 0)
+    h = np.array([[1.0, -2.0], [5.0, 7.0]])
+    ws = np.array([[1.0, 1.0], [0.0, 3.0], [2.0, 0.0]])
+    wn = np.full((3, 2), 100.0)
+    out = _layer(h, 1, [0, 0], [], ws, wn, [0.25, 0.0, -1.0], relu=False)
+    assert np.array_equal(out[0], [1.0 - 2.0 + 0.25, -6.0, 2.0 - 1.0])
+
+
+def test_nonsquare_weights_hand_product():
+    # d_in = 2, d_out = 3: pins the orientation W [d_out][d_in] (a transposed operand
+    # cannot even be applied).  dst 0 with neighbours rows 1, 2 (mean [2, 1]).
+    h = np.array([[1.0, 2.0], [3.0, 0.0], [1.0, 2.0]])
+    ws = np.array([[1.0, 0.0], [0.0, 1.0], [1.0, 1.0]])
+    wn = np.array([[0.0, 1.0], [1.0, 0.0], [-1.0, 2.0]])
+    out = _layer(h, 1, [0, 2], [1, 2], ws, wn, [0.0, 0.0, 0.0], relu=False)
+    # self: [1, 2, 3]; neigh: [1, 2, 0]
+    assert np.array_equal(out[0], [2.0, 4.0, 3.0])
+
+
+def test_relu_between_layers_not_after_last():
+    # layer 0 drives every hidden unit negative (W = 0, b = -1) -> ReLU -> 0;
+    # layer 1 then outputs exactly its bias, which is negative (no ReLU on the last layer).
+    X = np.arange(12, dtype=np.float64).reshape(4, 3)
+    blocks = [(np.array([0, 1]), np.array([1])),                  # hop 0: dst F_0 = {0}, nbr pos 1
+              (np.array([0, 1, 2, 4]), np.array([3, 0, 1, 3]))]   # hop 1: dst F_1 = {0, 1, 2}
+    w0 = (np.zeros((5, 3)), np.zeros((5, 3)), np.full(5, -1.0))
+    w1 = (np.ones((2, 5)), np.ones((2, 5)), np.array([-3.0, 0.5]))
+    h1, h2 = S.sage_forward(X, blocks, [w0, w1])
+    assert h1.shape == (3, 5) and np.all(h1 == 0.0)
+    assert np.array_equal(h2, [[-3.0, 0.5]])
+
+
+def test_two_layer_hand_trace_hop_order():
+    # F_2 = 4 nodes with scalar features 1, 2, 4, 8.  hop 1 (used by layer 0): dst F_1 = rows 0..2,
+    # row 0 <- {1, 3}, row 1 <- {0}, row 2 <- {}.  hop 0 (used by layer 1): dst F_0 = row 0 <- {1, 2}.
+    X = np.array([[1.0], [2.0], [4.0], [8.0]])
+    blocks = [(np.array([0, 2]), np.array([1, 2])),
+              (np.array([0, 2, 3, 3]), np.array([1, 3, 0]))]
+    w0 = (np.array([[1.0]]), np.array([[1.0]]), np.array([0.0]))     # h = x + mean
+    w1 = (np.array([[1.0]]), np.array([[10.0]]), np.array([0.0]))    # z = h + 10 mean
+    h1, h2 = S.sage_forward(X, blocks, [w0, w1])
+    # layer 0: row0 = 1 + (2+8)/2 = 6; row1 = 2 + 1 = 3; row2 = 4 + 0 = 4
+    assert np.array_equal(h1[:, 0], [6.0, 3.0, 4.0])
+    # layer 1: row0 = 6 + 10 * (3 + 4) / 2 = 41
+    assert np.array_equal(h2[:, 0], [41.0])
+
+
+def test_constant_features_closed_form():
+    # every input row = c  =>  mean = c for deg > 0 and z = (W_self + W_neigh) c + b
+    rng = np.random.default_rng(3)
+    c = rng.standard_normal(6)
+    h = np.tile(c, (9, 1))
+    off = np.array([0, 3, 5, 5, 8])
+    nbr = np.array([1, 2, 8, 0, 7, 4, 5, 6])
+    ws, wn, b = rng.standard_normal((4, 6)), rng.standard_normal((4, 6)), rng.standard_normal(4)
+    out = _layer(h, 4, off, nbr, ws, wn, b, relu=False)
+    for i in (0, 1, 3):
+        np.testing.assert_allclose(out[i], (ws + wn) @ c + b, rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(out[2], ws @ c + b, rtol=1e-13, atol=1e-13)
+
+
+def test_neighbour_order_invariance():
+    rng = np.random.default_rng(4)
+    h = rng.standard_normal((10, 5))
+    off = np.array([0, 4, 7])
+    nbr = np.array([2, 5, 9, 3, 8, 1, 6])
+    ws, wn, b = rng.standard_normal((3, 5)), rng.standard_normal((3, 5)), rng.standard_normal(3)
+    a = _layer(h, 2, off, nbr, ws, wn, b, relu=True)
+    nbr2 = np.array([3, 9, 2, 5, 6, 8, 1])
+    bb = _layer(h, 2, off, nbr2, ws, wn, b, relu=True)
+    np.testing.assert_allclose(a, bb, rtol=1e-14, atol=1e-14)
+
+
+def _torch_sparse_forward(X, blocks, weights):
+    """Independent formulation: per layer H' = act(H[:n] W_s^T + (D^-1 A) H W_n^T + b) with the
+    row-normalised block adjacency as a torch sparse CSR matrix (library primitive)."""
+    import torch
+    h = torch.as_tensor(np.asarray(X, np.float64))
+    L = len(weights)
+    for l in range(L):
+        off, nbr = blocks[L - 1 - l]
+        n = len(off) - 1
+        deg = np.diff(off).astype(np.float64)
+        vals = np.repeat(np.where(deg > 0, 1.0 / np.maximum(deg, 1.0), 0.0), np.diff(off).astype(np.int64))
+        A = torch.sparse_csr_tensor(torch.as_tensor(np.asarray(off, np.int64)),
+                                    torch.as_tensor(np.asarray(nbr, np.int64)),
+                                    torch.as_tensor(vals), size=(n, h.shape[0]), dtype=torch.float64)
+        ws, wn, b = (torch.as_tensor(np.asarray(a, np.float64)) for a in weights[l])
+        z = h[:n] @ ws.T + (A @ h) @ wn.T + b
+        h = torch.relu(z) if l < L - 1 else z
+    return h.numpy()
+
+
+@pytest.mark.filterwarnings("ignore::UserWarning")
+def test_matches_sparse_matmul_on_sampled_blocks():
+    # real sampled blocks from the C oracle (600-node random graph, 2 partitions, fanout [10,25])
+    g = synth.random_graph(600, 0.02, seed=11)
+    parts = synth.partition(g, 2)
+    D = 12
+    W = O.World(parts, D, synth.FEAT_SEED)
+    p = W.parts[0]
+    p.buffer_init(0.9, float(O.alpha_default(0.9, 4)), 1.0, 4, 2500)
+    fan = [10, 25]
+    dims = synth.sage_dims(D, 2, 7, hidden=9)
+    wts = synth.sage_weights(dims, seed=5)
+    for step in (1, 2, 3):
+        p.step(synth.RUN_SEED, step, fan, 32)
+        F = p.frontier()
+        blocks = []
+        for h in range(2):
+            off, cols = p.hop_block(h)
+            blocks.append((off, S.positions(F, cols)))
+        X = p.features().astype(np.float64)
+        outs = S.sage_forward(X, blocks, wts)
+        ref = _torch_sparse_forward(X, blocks, wts)
+        assert outs[-1].shape == (p.hop_sizes()[0], 7)
+        np.testing.assert_allclose(outs[-1], ref, rtol=1e-12, atol=1e-12)
+    W.close()
+
+
+@pytest.mark.parametrize("dims", [[3, 5, 2], [64, 128, 16]])
+def test_weights_generator_shapes(dims):
+    wts = synth.sage_weights(dims, seed=1)
+    for l, (ws, wn, b) in enumerate(wts):
+        assert ws.shape == (dims[l + 1], dims[l]) and wn.shape == ws.shape and b.shape == (dims[l + 1],)
+        assert ws.dtype == np.float32
