@@ -364,6 +364,67 @@ def main():
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_value = WINDOW * PARTS_PER_GPU * world * E2E / (float(e2e_ms.item()) / 1e3)
 
+    # ---------------- with consumer (A14): the same pipeline plus the GraphSAGE-mean forward of every
+    # minibatch (mgnn_sage_forward, tcgen05 TF32) between gather and score on the buffer stream, with
+    # the sampling of the next window still overlapped on stream A (Alg.1 l.6-9).
+    dims = synth.sage_dims(CFG.feat_dim, len(CFG.fanouts), synth.N_CLASSES[CFG.name])
+    wts = synth.sage_weights(dims)
+    ctx.sage_config(dims, [w_[0] for w_ in wts], [w_[1] for w_ in wts], [w_[2] for w_ in wts])
+    logits = torch.empty((PARTS_PER_GPU * WINDOW, CFG.batch, dims[-1]), dtype=torch.float32, device="cuda")
+    fwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+
+    def consume_fwd(sl, i=None):
+        sB.wait_event(ev_sampled[sl])
+        ctx.lookup_gather(sl, sB)
+        if i is not None:
+            fwd_ev[i][0].record(sB)
+        ctx.sage_forward(sl, logits, sB)
+        if i is not None:
+            fwd_ev[i][1].record(sB)
+        ctx.score(sl, sB)
+        ev_done[sl].record(sB)
+
+    t_c = t_e2e + E2E * WINDOW
+    barrier()
+    sample_async(slot, t_c)
+    for _ in range(args.warmup):
+        sample_async(slot ^ 1, t_c + WINDOW)
+        consume_fwd(slot)
+        t_c += WINDOW
+        slot ^= 1
+    barrier()
+    for i in range(K):
+        flush.zero_()
+        cev[i][0].record(sB)
+        sA.wait_event(cev[i][0])
+        sample_async(slot ^ 1, t_c + WINDOW)
+        consume_fwd(slot, i)
+        sB.wait_stream(sA)
+        cev[i][1].record(sB)
+        t_c += WINDOW
+        slot ^= 1
+    barrier()
+    c_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in cev)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(c_ms, op=dist.ReduceOp.MAX)
+    c_value = mb_total / (float(c_ms.item()) / 1e3)
+    fwd_ms = sum(a.elapsed_time(b) for a, b in fwd_ev) / K
+    # algorithmic work of the last forward (window slot ^ 1): per layer 2 * n_dst * (2 d_in) * d_out
+    # flops (dense part) and the neighbour rows it averages (4 * d_in bytes per sampled edge)
+    wv = ctx.window(slot ^ 1)
+    hs = PL.device_view(wv.hop_size, (wv.n_inst, 9), "i8").cpu().numpy()
+    L_ = len(CFG.fanouts)
+    flops = 0.0
+    agg_bytes = 0.0
+    for l in range(L_):
+        hop = L_ - 1 - l
+        n_dst = hs[:, hop].astype(np.float64)
+        flops += float((2.0 * n_dst * 2 * dims[l] * dims[l + 1]).sum())
+        offs = PL.device_view(wv.offsets[hop], (wv.n_inst, wv.off_stride[hop]), "i8")
+        n_edges = np.array([int(offs[m, int(hs[m, hop])]) for m in range(wv.n_inst)], np.float64)
+        agg_bytes += float((n_edges * dims[l] * 4).sum())
+
     clocks = clk.summary()
     if rank == 0:
         peaks = {}
@@ -401,6 +462,15 @@ def main():
                          "algorithmic_bytes_per_launch": g_bytes},
             "clocks": clocks,
             "wall_s_timed_region": wall,
+            "with_consumer": {
+                "value": c_value, "unit": UNIT, "ms_per_step": float(c_ms.item()) / K,
+                "model": f"GraphSAGE-mean {dims} (random init), forward of every minibatch",
+                "consumer_ms_per_step": fwd_ms, "consumer_launches_per_step": L_,
+                "kernel": "k_sage_layer: neighbour mean -> smem (SW128) + TMA self rows/weights -> "
+                          "tcgen05.mma kind::tf32 (TMEM accumulator) -> bias/ReLU epilogue",
+                "tflops": flops / (fwd_ms / 1e3) / 1e12 if fwd_ms > 0 else None,
+                "agg_gbs": agg_bytes / (fwd_ms / 1e3) / 1e9 if fwd_ms > 0 else None,
+                "dtype": "tf32 x tf32 -> f32"},
         }
         if world > 1:
             nv_bytes = peer_rows * CFG.feat_dim * 4

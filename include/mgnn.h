@@ -162,6 +162,34 @@ MGNN_API mgnn_status mgnn_lookup_gather(mgnn_ctx ctx, int32_t slot, mgnn_stream 
  * (l.12-19, l.25-34) with the swap of P:224 and the refill of the k new rows. */
 MGNN_API mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stream);
 
+/* ------------------------------------------------------------------ A14: the consumer
+ * GraphSAGE-mean forward pass over a prepared window (Alg.1 l.6-7: the trainer
+ * consumes the minibatch "by computing the forward pass" over the sampled blocks; SAGEConv
+ * 'mean' of DGL).  Layer l = 0..L-1 uses the block of hop h = L-1-l (dst = F_h, the
+ * first |F_h| rows of F_{h+1}; neighbours = that hop's cols, positions in F_{h+1}):
+ *     H^{l+1}[i] = act( W_self^l H^l[i] + W_neigh^l mean_{j in N_h(i)} H^l[j] + b^l ),
+ * H^0 = X, act = ReLU for l < L-1 and identity for the last layer, mean over an empty
+ * neighbourhood = 0.  The tensor cores multiply in TF32 with fp32 accumulation.
+ * The weights are copied to the device by mgnn_sage_config (host arrays, caller keeps them). */
+typedef struct {
+    int32_t n_layers;               /* must equal the sampler's n_layers */
+    const int32_t* dims;            /* [n_layers+1]: dims[0] = feat_dim, 1 <= dims[l] <= 256 for l >= 1 */
+    const float* const* w_self;     /* [n_layers] host: [dims[l+1]][dims[l]] row-major (nn.Linear.weight) */
+    const float* const* w_neigh;    /* [n_layers] host: same shapes */
+    const float* const* bias;       /* [n_layers] host: [dims[l+1]] */
+} mgnn_sage_desc;
+
+/* Upload the weights and size the hidden-activation buffers for the current sampler
+ * configuration (call again after mgnn_sampler_config).  EINVAL on bad shapes, ESTATE
+ * before mgnn_sampler_config. */
+MGNN_API mgnn_status mgnn_sage_config(mgnn_ctx ctx, const mgnn_sage_desc* desc);
+/* Forward pass of every instance of the window in `slot` (after mgnn_lookup_gather of that
+ * slot, ordered on `stream`).  logits: DEVICE [n_inst][batch][logits_pitch] fp32, caller-
+ * owned; row i < |F_0| of instance m receives the dims[L] outputs of seed F_0[i]; other rows
+ * and columns are not written.  logits_pitch >= dims[L].  One kernel launch per layer. */
+MGNN_API mgnn_status mgnn_sage_forward(mgnn_ctx ctx, int32_t slot, float* logits, int64_t logits_pitch,
+                                       mgnn_stream stream);
+
 /* Device view of a window slot (valid after mgnn_sample of that slot). */
 MGNN_API mgnn_status mgnn_window_get(mgnn_ctx ctx, int32_t slot, mgnn_window* out);
 

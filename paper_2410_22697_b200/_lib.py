@@ -20,6 +20,7 @@ SYMBOLS = [
     "mgnn_counts_read_async",
     "mgnn_buffer_snapshot", "mgnn_part_info", "mgnn_halo_get", "mgnn_table_row", "mgnn_launch_count",
     "mgnn_profile_enable", "mgnn_profile_read", "mgnn_profile_kernels",
+    "mgnn_sage_config", "mgnn_sage_forward",
 ]
 
 
@@ -40,6 +41,11 @@ class Window(C.Structure):
                 ("offsets", C.c_void_p * MAX_LAYERS), ("cols", C.c_void_p * MAX_LAYERS),
                 ("off_stride", C.c_int64 * MAX_LAYERS), ("col_stride", C.c_int64 * MAX_LAYERS),
                 ("counts", C.c_void_p)]
+
+
+class SageDesc(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("dims", C.c_void_p), ("w_self", C.c_void_p),
+                ("w_neigh", C.c_void_p), ("bias", C.c_void_p)]
 
 
 class MgnnError(RuntimeError):
@@ -85,6 +91,8 @@ def load(path: str = LIB_PATH):
         "mgnn_profile_enable": (S, [P, I32]),
         "mgnn_profile_read": (S, [P, P, P, P]),
         "mgnn_profile_kernels": (S, [I32, P, I64]),
+        "mgnn_sage_config": (S, [P, P]),
+        "mgnn_sage_forward": (S, [P, I32, P, I64, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libmgnn.so")
-UNITS = ["api.cu", "sample.cu", "gather.cu", "score.cu", "sort.cu", "load.cu"]
+UNITS = ["api.cu", "sample.cu", "gather.cu", "score.cu", "sort.cu", "load.cu", "sage.cu"]
 HEADERS = ["common.cuh", "launch.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 EXTRA = os.environ.get("MGNN_NVCC_EXTRA", "").split()

@@ -158,6 +158,20 @@ struct mgnn_ctx_s {
     SortSeg* d_permsegs = nullptr;       // [n_lp][max perm slots]
     int32_t perm_slots_max = 0;
     long long* d_perm_n = nullptr;       // [n_lp]
+    // A14 consumer (GraphSAGE-mean): padded weights [npad][2*kp] = [W_self | W_neigh], bias [npad],
+    // ping-pong hidden buffers, and the TMA tensor maps of every operand (128 B each)
+    struct Sage {
+        bool ready = false;
+        int32_t L = 0;
+        int32_t dims[kMaxLayers + 1] = {};
+        int32_t npad[kMaxLayers] = {}, kp[kMaxLayers] = {};
+        float* w[kMaxLayers] = {};
+        float* b[kMaxLayers] = {};
+        float* h[2] = {};
+        int64_t out_rows[kMaxLayers] = {};        // rows per instance of layer l's output buffer (= fcap[h])
+        alignas(64) unsigned char map_w[kMaxLayers][128];
+        alignas(64) unsigned char map_in[2][kMaxLayers][128];   // [window slot][layer]
+    } sage;
     // ordering of windows through the buffer
     bool seq_started = false;
     uint64_t next_step = 0;
@@ -294,6 +308,16 @@ void free_win(Win& w) {
     w = Win();
 }
 
+void free_sage(mgnn_ctx_s* ctx) {
+    for (int l = 0; l < kMaxLayers; ++l) {
+        dfree(ctx->sage.w[l]);
+        dfree(ctx->sage.b[l]);
+    }
+    dfree(ctx->sage.h[0]);
+    dfree(ctx->sage.h[1]);
+    ctx->sage.ready = false;
+}
+
 void free_buffer(Part& p) {
     dfree(p.rows); dfree(p.se); dfree(p.sa); dfree(p.slot_of); dfree(p.slot_h); dfree(p.hitmask); dfree(p.rank_deg);
     dfree(p.ek); dfree(p.ekt); dfree(p.ev); dfree(p.evt); dfree(p.rk); dfree(p.rkt); dfree(p.rv); dfree(p.rvt);
@@ -411,6 +435,7 @@ void mgnn_destroy(mgnn_ctx ctx) {
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
     for (auto& w : ctx->win) free_win(w);
+    free_sage(ctx);
     for (auto& p : ctx->parts) {
         free_buffer(p);
         free_perm(p);
@@ -709,6 +734,7 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
     if (ctx->parts.empty()) return fail(ctx, MGNN_ESTATE, "no partition loaded");
     CK(cudaDeviceSynchronize());
     for (auto& w : ctx->win) free_win(w);
+    free_sage(ctx);
     for (auto& p : ctx->parts) free_perm(p);
     ctx->configured = false;
     ctx->L = n_layers;
@@ -942,6 +968,126 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
     }
     CKL();
     w.scored = true;
+    return MGNN_OK;
+}
+
+// ------------------------------------------------------------------ A14: GraphSAGE-mean consumer
+mgnn_status mgnn_sage_config(mgnn_ctx ctx, const mgnn_sage_desc* d) {
+    GUARD();
+    if (!ctx->configured) return fail(ctx, MGNN_ESTATE, "sage_config before sampler_config");
+    if (!d || d->n_layers != ctx->L || !d->dims || !d->w_self || !d->w_neigh || !d->bias)
+        return fail(ctx, MGNN_EINVAL, "sage: n_layers must equal the sampler's and all arrays given");
+    if (d->dims[0] != ctx->D) return fail(ctx, MGNN_EINVAL, "sage: dims[0] must equal feat_dim");
+    for (int l = 1; l <= d->n_layers; ++l)
+        if (d->dims[l] < 1 || d->dims[l] > 256) return fail(ctx, MGNN_EINVAL, "sage: dims[l] must be 1..256");
+    for (int l = 0; l < d->n_layers; ++l)
+        if (!d->w_self[l] || !d->w_neigh[l] || !d->bias[l]) return fail(ctx, MGNN_EINVAL, "sage: null weight");
+    CK(cudaDeviceSynchronize());
+    free_sage(ctx);
+    auto& S = ctx->sage;
+    const int L = d->n_layers;
+    S.L = L;
+    for (int l = 0; l <= L; ++l) S.dims[l] = d->dims[l];
+    const int64_t M = (int64_t)ctx->parts.size() * ctx->max_window;
+    int64_t hbytes[2] = {0, 0};
+    for (int l = 0; l < L; ++l) {
+        const int kin = S.dims[l], n = S.dims[l + 1];
+        S.npad[l] = (n + 15) / 16 * 16;
+        S.kp[l] = (kin + 127) / 128 * 128;
+        const int64_t wc = 2 * (int64_t)S.kp[l];
+        std::vector<float> w((size_t)S.npad[l] * wc, 0.0f), b((size_t)S.npad[l], 0.0f);
+        for (int o = 0; o < n; ++o) {
+            for (int k = 0; k < kin; ++k) {
+                w[(size_t)o * wc + k] = d->w_self[l][(size_t)o * kin + k];
+                w[(size_t)o * wc + S.kp[l] + k] = d->w_neigh[l][(size_t)o * kin + k];
+            }
+            b[o] = d->bias[l][o];
+        }
+        CK(dalloc(&S.w[l], w.size()));
+        CK(dalloc(&S.b[l], b.size()));
+        CK(cudaMemcpy(S.w[l], w.data(), w.size() * sizeof(float), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(S.b[l], b.data(), b.size() * sizeof(float), cudaMemcpyHostToDevice));
+        if (!sage_encode_map(S.map_w[l], S.w[l], S.npad[l], wc, wc, S.npad[l]))
+            return fail(ctx, MGNN_ECUDA, "sage: cuTensorMapEncodeTiled (weights) failed");
+        const int hop = L - 1 - l;
+        S.out_rows[l] = ctx->fcap[hop];
+        if (l < L - 1) hbytes[l & 1] = std::max(hbytes[l & 1], M * S.out_rows[l] * S.npad[l]);
+    }
+    for (int i = 0; i < 2; ++i)
+        if (hbytes[i]) CK(dalloc(&S.h[i], hbytes[i]));
+    for (int slot = 0; slot < 2; ++slot)
+        for (int l = 0; l < L; ++l) {
+            const int hop = L - 1 - l;
+            const float* base;
+            int64_t rows, cols, pitch;
+            if (l == 0) {
+                base = ctx->win[slot].X;
+                rows = M * ctx->ucap;
+                cols = pitch = ctx->pitch;
+            } else {
+                base = S.h[(l - 1) & 1];
+                rows = M * ctx->fcap[hop + 1];
+                cols = pitch = S.npad[l - 1];
+            }
+            if (!sage_encode_map(S.map_in[slot][l], base, rows, cols, pitch, 128))
+                return fail(ctx, MGNN_ECUDA, "sage: cuTensorMapEncodeTiled (activations) failed");
+        }
+    S.ready = true;
+    return MGNN_OK;
+}
+
+mgnn_status mgnn_sage_forward(mgnn_ctx ctx, int32_t slot, float* logits, int64_t logits_pitch, mgnn_stream stream) {
+    GUARD();
+    if (slot < 0 || slot > 1 || !logits) return fail(ctx, MGNN_EINVAL, "bad slot / logits");
+    auto& S = ctx->sage;
+    if (!S.ready) return fail(ctx, MGNN_ESTATE, "sage_forward before sage_config");
+    if (logits_pitch < S.dims[S.L]) return fail(ctx, MGNN_EINVAL, "logits_pitch < dims[L]");
+    Win& w = ctx->win[slot];
+    if (!w.gathered) return fail(ctx, MGNN_ESTATE, "sage_forward needs a gathered window");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int L = S.L;
+    const int n_inst = (int)ctx->parts.size() * w.n_steps;
+    for (int l = 0; l < L; ++l) {
+        const int hop = L - 1 - l;
+        SageLayerArgs a;
+        memset(&a, 0, sizeof(a));
+        a.n_inst = n_inst;
+        a.hop = hop;
+        a.k_in = S.dims[l];
+        a.kp = S.kp[l];
+        a.npad = S.npad[l];
+        a.relu = l < L - 1;
+        a.k_hop = ctx->k_hop[hop];
+        a.hop_size = w.hop_size;
+        a.off = w.off[hop];
+        a.off_stride = ctx->fcap[hop] + 1;
+        a.cols = w.cols[hop];
+        a.col_stride = ctx->ecap[hop];
+        if (l == 0) {
+            a.h_in = w.X;
+            a.in_rows = ctx->ucap;
+            a.in_pitch = ctx->pitch;
+        } else {
+            a.h_in = S.h[(l - 1) & 1];
+            a.in_rows = ctx->fcap[hop + 1];
+            a.in_pitch = S.npad[l - 1];
+        }
+        if (l < L - 1) {
+            a.h_out = S.h[l & 1];
+            a.out_rows = S.out_rows[l];
+            a.out_pitch = S.npad[l];
+            a.n_out = S.npad[l];
+        } else {
+            a.h_out = logits;
+            a.out_rows = ctx->batch;
+            a.out_pitch = logits_pitch;
+            a.n_out = S.dims[L];
+        }
+        a.bias = S.b[l];
+        if (!launch_sage_layer(S.map_in[slot][l], S.map_w[l], a, s))
+            return fail(ctx, MGNN_ECUDA, "sage: layer launch configuration failed");
+    }
+    CKL();
     return MGNN_OK;
 }
 

@@ -133,6 +133,35 @@ void launch_perm_build(const PartDev* pd_dev, int64_t n_train, uint64_t epoch0, 
 void radix_sort_pairs(const SortSeg* segs_dev, int n_seg, int64_t n_max, int max_passes, void* scratch, cudaStream_t s);
 size_t radix_scratch_bytes(int n_seg, int64_t n_max, int max_passes);
 
+// sage.cu: GraphSAGE-mean consumer (A14), one launch per layer over every instance of a window
+struct SageLayerArgs {
+    int32_t n_inst;
+    int32_t hop;               // block of hop h: dst F_h, src positions in F_{h+1}
+    int32_t k_in;              // input features (columns of H_in that carry data)
+    int32_t n_panels;          // ceil(k_in / panel width), set by the launcher
+    int32_t kp;                // K offset of W_neigh inside Wcat (k_in rounded up to 128)
+    int32_t npad;              // UMMA N (multiple of 16, <= 256)
+    int32_t n_out;             // columns written per output row (npad for hidden, C for logits)
+    int32_t relu;
+    int32_t k_hop;             // fanout of the hop (max neighbours per dst row)
+    int32_t stages;            // weight-chunk ring depth
+    uint32_t idesc;
+    uint32_t tmem_cols;
+    const int64_t* hop_size;   // [M][kMaxLayers+1]
+    const int64_t* off;        // [M][off_stride]
+    int64_t off_stride;
+    const int32_t* cols;       // [M][col_stride]
+    int64_t col_stride;
+    const float* h_in;         // [M][in_rows][in_pitch]
+    int64_t in_rows, in_pitch;
+    float* h_out;              // [M][out_rows][out_pitch]
+    int64_t out_rows, out_pitch;
+    const float* bias;         // [npad], zero padded
+};
+bool sage_encode_map(void* map_out, const float* base, int64_t rows, int64_t cols, int64_t pitch, int box_rows);
+bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArgs& a, cudaStream_t s);
+size_t sage_smem_bytes(int n_inst, int k_hop);
+
 // load.cu
 void launch_mark_halo(const int32_t* cols, int64_t nnz, int64_t lo, int64_t hi, uint32_t* bm, cudaStream_t s);
 void launch_bitmap_to_ids(const uint32_t* bm, int64_t nwords, int32_t* out, long long* out_n, Scratch sc,

@@ -1,0 +1,420 @@
+// sage.cu -- A14, the GraphSAGE-mean consumer of a prepared window (Alg.1 l.6-7, P:126-137:
+// "the trainer ... computes the forward pass over the sampled blocks"; SAGEConv 'mean' as in
+// DGL, hidden size 128).  One launch per GNN layer covers every instance of the window.
+//
+// Layer l consumes the block of hop h = L-1-l (DGL block layout: dst = F_h = the first |F_h|
+// rows of F_{h+1}; cols = positions in F_{h+1}):
+//     H_out[i] = act( W_self H_in[i] + W_neigh mean_{j in N(i)} H_in[j] + b ),  i < |F_h|
+// act = ReLU except on the last layer; mean over no neighbours = 0 (DGL).
+//
+// Kernel design (sm_100a, tcgen05 + TMEM + TMA): a persistent CTA per SM walks 128-row dst
+// tiles of all instances.  Per tile the K dimension [self | neigh] is processed in panels of
+// 128 input columns:
+//   * warp 8 (one elected lane) loads the self rows of the panel with TMA (SWIZZLE_128B,
+//     K-major, 4 chunks of 128 rows x 32 fp32) and streams the weight chunks W[:, k0:k0+32]
+//     through an mbarrier ring, then issues tcgen05.mma kind::tf32 (M=128, N=Npad, K=8) into
+//     a TMEM accumulator (fp32, Npad columns);
+//   * warps 0-7 compute the neighbour means of the same 128 columns (warp per dst row, one
+//     float4 per lane, 4 neighbour rows in flight) straight into shared memory in the same
+//     swizzled layout, so the aggregation feeds the tensor core without an HBM round trip;
+//   * after the last panel the 8 warps read the accumulator back (tcgen05.ld 32x32b), add the
+//     bias, apply ReLU and store the output rows.
+// Operands are fp32 in memory; the tensor core multiplies them as TF32 (10-bit mantissa) and
+// accumulates in fp32 -- the tolerance of the parity test is derived from that.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "launch.h"
+
+namespace mgnn {
+
+namespace {
+
+constexpr int kAggWarps = 8;                // aggregation / epilogue warps (2 CTAs per SM)
+constexpr int kCtlWarp = kAggWarps;         // TMA + MMA issue warp
+constexpr int kSageThreads = (kAggWarps + 1) * 32;
+constexpr int kTileM = 128;                 // UMMA M (cta_group::1)
+constexpr int kChunkCols = 32;              // fp32 columns per 128-byte swizzle atom row
+constexpr int kPanelChunks = 2;             // 64 input columns per panel
+constexpr int kChunkBytesA = kTileM * 128;  // 16 KB
+constexpr int kMaxStages = 8;
+constexpr int kMaxInst = 1024;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n SW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra SW_%=;\n}\n" ::"r"(
+            su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* sdst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            su32(sdst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(su32(bar))
+        : "memory");
+}
+// Shared-memory matrix descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart (SBO),
+// LBO unused for swizzled K-major (1), descriptor version 1 (sm_100).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void add4(float4& a, const float4 b) {
+    a.x = __fadd_rn(a.x, b.x);
+    a.y = __fadd_rn(a.y, b.y);
+    a.z = __fadd_rn(a.z, b.z);
+    a.w = __fadd_rn(a.w, b.w);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kSageThreads, 2)
+    k_sage_layer(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_w,
+                 SageLayerArgs a) {
+    extern __shared__ __align__(1024) unsigned char dsm[];
+    __shared__ __align__(8) uint64_t bar_self, bar_mma, bar_full[kMaxStages], bar_empty[kMaxStages];
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ int32_t s_off[kTileM + 1];      // tile's CSR offsets, relative to its first edge
+
+    // 1024-byte aligned operand region (SWIZZLE_128B atoms)
+    unsigned char* base = (unsigned char*)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);
+    unsigned char* a_self = base;                                   // kPanelChunks x 16 KB
+    unsigned char* a_neigh = base + kPanelChunks * kChunkBytesA;    // kPanelChunks x 16 KB
+    unsigned char* b_ring = base + 2 * kPanelChunks * kChunkBytesA; // stages x (npad x 128 B)
+    const uint32_t b_stage_bytes = (uint32_t)a.npad * 128u;
+    int32_t* tile_pref = (int32_t*)(b_ring + a.stages * b_stage_bytes);  // [n_inst + 1] tile prefix per instance
+    int32_t* s_cols = tile_pref + ((a.n_inst + 4) & ~3);            // tile's neighbour positions
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == kCtlWarp) {
+        if (lane == 0) {
+            mb_init(&bar_self, 1);
+            mb_init(&bar_mma, 1);
+            for (int s = 0; s < a.stages; ++s) {
+                mb_init(&bar_full[s], 1);
+                mb_init(&bar_empty[s], 1);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&map_in) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+        }
+        __syncwarp();
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base_sh)),
+                     "r"(a.tmem_cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    pdl_enter();
+    // per-instance tile prefix (warp 0): tiles of instance m = ceil(|F_h| / 128)
+    if (warp == 0) {
+        int32_t run = 0;
+        if (lane == 0) tile_pref[0] = 0;
+        for (int m0 = 0; m0 < a.n_inst; m0 += 32) {
+            const int m = m0 + lane;
+            int32_t t = 0;
+            if (m < a.n_inst) t = (int32_t)((a.hop_size[(int64_t)m * (kMaxLayers + 1) + a.hop] + kTileM - 1) / kTileM);
+            int32_t x = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(kFull, x, o);
+                if (lane >= o) x += y;
+            }
+            if (m < a.n_inst) tile_pref[m + 1] = run + x;
+            run += __shfl_sync(kFull, x, 31);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+    const int32_t n_tiles = tile_pref[a.n_inst];
+
+    uint32_t mma_phase = 0;     // completions of bar_mma seen
+    uint32_t self_phase = 0;
+    uint32_t g_cons = 0, g_issued = 0;   // weight chunks consumed / issued (control lane only)
+    bool pending = false;       // an MMA batch (previous panel) may still read A
+
+    // aggregation mapping: 8 lanes per dst row (lane8 = 16-byte unit of a 128-byte chunk row),
+    // 4 rows per warp at a time, kAggWarps * 4 rows per pass
+    const int sub = lane >> 3, lane8 = lane & 7;
+
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        int lo = 0, hi = a.n_inst;   // instance m with tile_pref[m] <= tile < tile_pref[m+1]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (tile_pref[mid] <= tile) lo = mid; else hi = mid;
+        }
+        const int m = lo;
+        const int64_t row0 = (int64_t)(tile - tile_pref[m]) * kTileM;
+        const int64_t n_dst = a.hop_size[(int64_t)m * (kMaxLayers + 1) + a.hop];
+        const int n_rows = (int)(n_dst - row0 < kTileM ? n_dst - row0 : kTileM);
+        const int64_t in_base = (int64_t)m * a.in_rows;
+        const float* h_in = a.h_in + in_base * a.in_pitch;
+
+        // the tile's offsets and neighbour lists -> shared memory (read once, used by every panel)
+        if (warp < kAggWarps) {
+            const int64_t* off = a.off + (int64_t)m * a.off_stride + row0;
+            const int64_t e_begin = __ldg(off);
+            for (int i = threadIdx.x; i <= kTileM; i += kAggWarps * 32)
+                s_off[i] = (int32_t)(__ldg(off + (i <= n_rows ? i : n_rows)) - e_begin);
+            const int64_t n_e = __ldg(off + n_rows) - e_begin;
+            const int32_t* cols = a.cols + (int64_t)m * a.col_stride + e_begin;
+            for (int64_t i = threadIdx.x; i < n_e; i += kAggWarps * 32) s_cols[i] = __ldg(cols + i);
+            named_sync(2, kAggWarps * 32);
+        }
+
+        for (int p = 0; p < a.n_panels; ++p) {
+            const int col0 = p * (kPanelChunks * kChunkCols);
+            const int rem = a.k_in - col0;
+            const int nch = rem >= kPanelChunks * kChunkCols ? kPanelChunks : (rem + kChunkCols - 1) / kChunkCols;
+            // A may be overwritten only after the previous panel's MMAs completed
+            if (pending) {
+                mb_wait(&bar_mma, mma_phase & 1);
+                ++mma_phase;
+                pending = false;
+            }
+            if (warp == kCtlWarp) {
+                if (lane == 0) {
+                    mb_expect_tx(&bar_self, (uint32_t)nch * kChunkBytesA);
+                    for (int j = 0; j < nch; ++j)
+                        tma_load_2d(a_self + j * kChunkBytesA, &map_in, col0 + j * kChunkCols, (int)(in_base + row0),
+                                    &bar_self);
+                }
+                __syncwarp();
+            } else {
+                // neighbour means of panel columns [col0, col0 + 32*nch): lane covers the 16-byte
+                // unit lane8 of each chunk g, i.e. columns col0 + 32 g + 4 lane8 .. +3
+                bool gok[kPanelChunks];
+#pragma unroll
+                for (int g = 0; g < kPanelChunks; ++g) gok[g] = g < nch && col0 + g * kChunkCols + lane8 * 4 < a.in_pitch;
+                for (int r = warp * 4 + sub; r < kTileM; r += kAggWarps * 4) {
+                    float4 acc[kPanelChunks];
+#pragma unroll
+                    for (int g = 0; g < kPanelChunks; ++g) acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    const int e0 = r < n_rows ? s_off[r] : 0, e1 = r < n_rows ? s_off[r + 1] : 0;
+                    const float* hb = h_in + col0 + lane8 * 4;
+                    int e = e0;
+                    for (; e + 4 <= e1; e += 4) {
+                        float4 v[4][kPanelChunks];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const float* pj = hb + (int64_t)s_cols[e + j] * a.in_pitch;
+#pragma unroll
+                            for (int g = 0; g < kPanelChunks; ++g)
+                                if (gok[g]) v[j][g] = ldg4(pj + g * kChunkCols);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+#pragma unroll
+                            for (int g = 0; g < kPanelChunks; ++g)
+                                if (gok[g]) add4(acc[g], v[j][g]);
+                    }
+                    for (; e < e1; ++e) {
+                        const float* p0 = hb + (int64_t)s_cols[e] * a.in_pitch;
+#pragma unroll
+                        for (int g = 0; g < kPanelChunks; ++g)
+                            if (gok[g]) add4(acc[g], ldg4(p0 + g * kChunkCols));
+                    }
+                    const int deg = e1 - e0;
+                    if (deg > 0) {
+                        const float fd = (float)deg;
+#pragma unroll
+                        for (int g = 0; g < kPanelChunks; ++g) {
+                            acc[g].x = __fdiv_rn(acc[g].x, fd);
+                            acc[g].y = __fdiv_rn(acc[g].y, fd);
+                            acc[g].z = __fdiv_rn(acc[g].z, fd);
+                            acc[g].w = __fdiv_rn(acc[g].w, fd);
+                        }
+                    }
+                    // SWIZZLE_128B: 16-byte unit u of row r lives at unit u ^ (r % 8)
+#pragma unroll
+                    for (int g = 0; g < kPanelChunks; ++g)
+                        if (g < nch)
+                            *reinterpret_cast<float4*>(a_neigh + g * kChunkBytesA + r * 128 + ((lane8 ^ (r & 7)) << 4)) =
+                                gok[g] ? acc[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+            tc_fence_before();
+            named_sync(1, kSageThreads);
+            tc_fence_after();
+            if (warp == kCtlWarp && lane == 0) {
+                mb_wait(&bar_self, self_phase & 1);
+                ++self_phase;
+                const int nk = 2 * nch;   // self chunks then neigh chunks
+                for (int kc = 0; kc < nk; ++kc) {
+                    // keep up to `stages` weight chunks in flight
+                    while (g_issued < g_cons + (uint32_t)a.stages && g_issued < g_cons + (uint32_t)(nk - kc)) {
+                        const uint32_t s = g_issued % a.stages;
+                        if (g_issued >= (uint32_t)a.stages) mb_wait(&bar_empty[s], ((g_issued / a.stages) - 1) & 1);
+                        const int kk = kc + (int)(g_issued - g_cons);
+                        const int wcol = kk < nch ? col0 + kk * kChunkCols : a.kp + col0 + (kk - nch) * kChunkCols;
+                        mb_expect_tx(&bar_full[s], b_stage_bytes);
+                        tma_load_2d(b_ring + s * b_stage_bytes, &map_w, wcol, 0, &bar_full[s]);
+                        ++g_issued;
+                    }
+                    const uint32_t s = g_cons % a.stages;
+                    mb_wait(&bar_full[s], (g_cons / a.stages) & 1);
+                    tc_fence_after();
+                    const unsigned char* ab = kc < nch ? a_self + kc * kChunkBytesA : a_neigh + (kc - nch) * kChunkBytesA;
+                    const uint32_t a0 = su32(ab), b0 = su32(b_ring + s * b_stage_bytes);
+#pragma unroll
+                    for (int k = 0; k < kChunkCols / 8; ++k)   // UMMA K = 8 for tf32 (32 bytes)
+                        mma_tf32(tmem, sdesc(a0 + k * 32), sdesc(b0 + k * 32), a.idesc,
+                                 (p > 0 || kc > 0 || k > 0) ? 1u : 0u);
+                    mma_commit(&bar_empty[s]);
+                    ++g_cons;
+                }
+                mma_commit(&bar_mma);
+            }
+            if (warp == kCtlWarp) __syncwarp();
+            pending = true;
+        }
+        // epilogue: TMEM -> registers -> bias, ReLU -> H_out
+        mb_wait(&bar_mma, mma_phase & 1);
+        ++mma_phase;
+        pending = false;
+        tc_fence_after();
+        if (warp < kAggWarps) {
+            const int q = warp & 3;               // TMEM lane quarter this warp may access
+            const int r = q * 32 + lane;
+            const int64_t row = row0 + r;
+            float* out = a.h_out + ((int64_t)m * a.out_rows + row) * a.out_pitch;
+            const bool vec = (a.out_pitch & 3) == 0;
+            for (int c = (warp >> 2) * 8; c < a.npad; c += (kAggWarps / 4) * 8) {
+                float v[8];
+                tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    float x = __fadd_rn(v[i], __ldg(a.bias + c + i));
+                    v[i] = a.relu ? fmaxf(x, 0.0f) : x;
+                }
+                if (row < n_dst) {
+                    if (vec && c + 8 <= a.n_out) {
+                        reinterpret_cast<float4*>(out + c)[0] = make_float4(v[0], v[1], v[2], v[3]);
+                        reinterpret_cast<float4*>(out + c)[1] = make_float4(v[4], v[5], v[6], v[7]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+                            if (c + i < a.n_out) out[c + i] = v[i];
+                    }
+                }
+            }
+        }
+        tc_fence_before();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == kCtlWarp)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols) : "memory");
+}
+
+// ------------------------------------------------------------------ host side
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+bool load_encode() {
+    if (g_encode) return true;
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+        return false;
+    g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    return true;
+}
+}  // namespace
+
+// 2-D fp32 tensor [rows][cols] with row pitch `pitch` floats, box 32 columns x box_rows rows,
+// SWIZZLE_128B (one 128-byte swizzle atom per box row), out-of-bounds elements read as zero.
+bool sage_encode_map(void* map_out, const float* base, int64_t rows, int64_t cols, int64_t pitch, int box_rows) {
+    if (!load_encode()) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)pitch * 4};
+    cuuint32_t box[2] = {(cuuint32_t)kChunkCols, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode((CUtensorMap*)map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// dynamic shared memory of one CTA: alignment slack, A (self + neigh panels), weight ring,
+// tile prefix, the tile's neighbour lists
+static size_t smem_fixed(int n_inst, int k_hop) {
+    return 1024 + 2 * kPanelChunks * kChunkBytesA + (size_t)((n_inst + 4) & ~3) * 4 + (size_t)kTileM * k_hop * 4;
+}
+constexpr size_t kSmemPerCta = 114 * 1024 - 2048;   // two CTAs per SM (228 KB), minus reserved + static
+
+size_t sage_smem_bytes(int n_inst, int k_hop) { return smem_fixed(n_inst, k_hop) + 2 * 32 * 1024; }
+
+bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArgs& args_in, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_sage_layer, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sage_smem_bytes(kMaxInst, MGNN_MAX_FANOUT)) != cudaSuccess)
+            return false;
+        attr = true;
+    }
+    SageLayerArgs a = args_in;
+    a.n_panels = (a.k_in + kPanelChunks * kChunkCols - 1) / (kPanelChunks * kChunkCols);
+    if (a.kp < a.n_panels * kPanelChunks * kChunkCols) return false;
+    if (a.n_inst > kMaxInst || a.npad % 16 || a.npad < 16 || a.npad > 256 || a.k_hop < 1 || a.k_hop > MGNN_MAX_FANOUT)
+        return false;
+    // weight ring: as many chunk stages as fit next to the rest while two CTAs share the SM
+    const int64_t stage = (int64_t)a.npad * 128;
+    const int64_t room = (int64_t)kSmemPerCta - (int64_t)smem_fixed(a.n_inst, a.k_hop);
+    a.stages = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxStages, room / stage));
+    const size_t smem = smem_fixed(a.n_inst, a.k_hop) + (size_t)a.stages * stage;
+    a.tmem_cols = 32;
+    while ((int)a.tmem_cols < a.npad) a.tmem_cols <<= 1;
+    // instruction descriptor: D fp32, A/B tf32, both K-major, N = npad, M = 128
+    a.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(a.npad >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    CUtensorMap mi = *(const CUtensorMap*)map_in, mw = *(const CUtensorMap*)map_w;
+    // two CTAs per SM: one aggregates while the other waits on its MMA / epilogue
+    launch_k(k_sage_layer, dim3(2 * sms), dim3(kSageThreads), smem, s, mi, mw, a);
+    count_launches(1, __func__, s);
+    return true;
+}
+
+}  // namespace mgnn

@@ -13,7 +13,7 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import MgnnError, Policy, PartitionDesc, Window
+from ._lib import MgnnError, Policy, PartitionDesc, SageDesc, Window
 
 
 def _ptr(a: Optional[np.ndarray]):
@@ -147,6 +147,31 @@ class Context:
         self.sample(slot, t0, n_steps, stream=s.value)
         self.lookup_gather(slot, stream=s.value)
         self.score(slot, stream=s.value)
+
+    # ------------------------------------------------------------ A14: GraphSAGE-mean consumer
+    def sage_config(self, dims: Sequence[int], w_self: Sequence[np.ndarray], w_neigh: Sequence[np.ndarray],
+                    bias: Sequence[np.ndarray]):
+        """Upload layer weights (nn.Linear layout [dims[l+1]][dims[l]], fp32) to the library."""
+        L = len(dims) - 1
+        keep = [np.ascontiguousarray(dims, np.int32)]
+        arrs = []
+        for group in (w_self, w_neigh, bias):
+            ptrs = (C.c_void_p * L)()
+            for l in range(L):
+                a = np.ascontiguousarray(group[l], np.float32)
+                keep.append(a)
+                ptrs[l] = a.ctypes.data
+            arrs.append(ptrs)
+        d = SageDesc(L, keep[0].ctypes.data, C.cast(arrs[0], C.c_void_p), C.cast(arrs[1], C.c_void_p),
+                     C.cast(arrs[2], C.c_void_p))
+        self._chk("mgnn_sage_config", self.L.mgnn_sage_config(self._h, C.byref(d)))
+        self.sage_dims = list(dims)
+
+    def sage_forward(self, slot: int, logits, stream=None):
+        """Forward pass of the window in `slot` into logits (torch CUDA tensor [n_inst][batch][pitch])."""
+        assert logits.is_cuda and logits.dtype.itemsize == 4 and logits.is_contiguous()
+        self._chk("mgnn_sage_forward", self.L.mgnn_sage_forward(self._h, slot, C.c_void_p(logits.data_ptr()),
+                                                                logits.shape[-1], _stream(stream)))
 
     # ------------------------------------------------------------ outputs
     def window(self, slot: int) -> Window:
