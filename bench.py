@@ -43,20 +43,53 @@ WINDOW = 32
 PARTS_PER_GPU = 2
 CFG = synth.CONFIGS["arxiv"]
 
+# Measurement policy (f_p in basis points, gamma, Delta) by config and total partitions P: the
+# paper's GPU optima; theta_R = 1.
+POLICY = {
+    "cfg1": {2: (2500, 0.995, 64)},
+    "arxiv": {2: (2500, 0.995, 32), 4: (5000, 0.995, 32), 8: (3500, 0.995, 128)},
+    "reddit": {2: (3500, 0.995, 32), 4: (5000, 0.995, 256), 8: (5000, 0.95, 32)},
+    "products": {2: (5000, 0.995, 32), 4: (5000, 0.995, 32), 8: (5000, 0.9995, 16)},
+    "papers_s32": {8: (5000, 0.9995, 512)},
+}
+# partitions per GPU and window length per config (papers: all 8 partitions on one GPU at N=1,
+# short windows so the statically bounded window arenas fit in HBM)
+LAYOUT = {"cfg1": (2, 32), "arxiv": (2, 32), "reddit": (2, 32), "products": (2, 32), "papers_s32": (8, 8)}
+WORKLOAD_TEXT = {
+    "cfg1": "synthetic 10k-node graph, avg degree 10, 64-d fp32, fanout [10,25], batch 256 (BASELINE.json configs[0])",
+    "arxiv": "ogbn-arxiv-shaped synthetic (169,343 nodes, ~2.33M directed edges, 128-d fp32), "
+             "fanout [10,25], batch 1000 (BASELINE.json configs[1])",
+    "reddit": "Reddit-shaped synthetic (232,965 nodes, ~114.6M directed edges, 602-d fp32), fanout [10,25], "
+              "batch 1000 (BASELINE.json configs[2])",
+    "products": "ogbn-products-shaped synthetic (2,449,029 nodes, ~123.7M directed edges, 100-d fp32), "
+                "fanout [5,10,15], batch 2000 (BASELINE.json configs[3])",
+    "papers_s32": "ogbn-papers100M-shaped synthetic at 1/32 scale (3.47M nodes, ~101M directed edges, 128-d fp32), "
+                  "8 partitions, fanout [5,10,15], batch 2000 (BASELINE.json configs[4], scaled)",
+}
+
+
+def select_config(name: str) -> None:
+    global CFG, WINDOW, PARTS_PER_GPU
+    CFG = synth.CONFIGS[name]
+    PARTS_PER_GPU, WINDOW = LAYOUT[name]
+
 
 def policy_for(P: int):
-    if P <= 2:
-        return 2500, 0.995, 32
-    if P <= 4:
-        return 5000, 0.995, 32
-    return 3500, 0.995, 128
+    table = POLICY[CFG.name]
+    k = min((q for q in table if q >= P), default=max(table))
+    f_bp, gamma, delta = table[k]
+    return f_bp, gamma, delta
+
+
+def window_for(delta: int) -> int:
+    """Steps per window: a window may end on an eviction step but not contain one earlier."""
+    return min(WINDOW, delta) if delta > 0 else WINDOW
 
 
 def workload(P: int) -> dict:
     f_bp, gamma, delta = policy_for(P)
     return {
-        "workload": "ogbn-arxiv-shaped synthetic (169,343 nodes, ~2.33M directed edges, 128-d fp32), "
-                    "fanout [10,25], batch 1000 (BASELINE.json configs[1])",
+        "workload": WORKLOAD_TEXT[CFG.name],
         "partitions": P, "partitions_per_gpu": PARTS_PER_GPU, "f_p": f_bp / 10000, "gamma": gamma, "delta": delta,
         "theta_r": 1.0, "window_steps": WINDOW, "minibatches_per_step_per_gpu": WINDOW * PARTS_PER_GPU,
         "l2": "flushed (256 MB write) between timed windows",
@@ -154,8 +187,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    global WINDOW
     P = PARTS_PER_GPU * args.gpus
     f_bp, gamma, delta = policy_for(P)
+    WINDOW = window_for(delta)
     g = synth.generate(CFG)
     parts = synth.partition(g, P)
     # each reference "step" = the same 32 x (partitions on one GPU) minibatches, bounded by time
@@ -201,7 +236,11 @@ def main():
     ap.add_argument("--impl", default="mgnn", choices=["mgnn", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--config", default="arxiv", choices=sorted(LAYOUT),
+                    help="workload (default: arxiv-shaped, BASELINE.json configs[1])")
     args = ap.parse_args()
+    global WINDOW
+    select_config(args.config)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":
@@ -231,6 +270,7 @@ def main():
             os.close(saved)
     P = PARTS_PER_GPU * world
     f_bp, gamma, delta = policy_for(P)
+    WINDOW = window_for(delta)
     g = synth.generate(CFG)
     parts = synth.partition(g, P)
     hosted = list(range(PARTS_PER_GPU * rank, PARTS_PER_GPU * (rank + 1)))

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kSageThreads, 2)
     __shared__ int32_t s_off[kTileM + 1];      // tile's CSR offsets, relative to its first edge
 
     // 1024-byte aligned operand region (SWIZZLE_128B atoms)
-    unsigned char* base = (unsigned char*)(((uintptr_t)dsm + 1023) & ~(uintptr_t)1023);
+    unsigned char* base = dsm + ((1024u - (su32(dsm) & 1023u)) & 1023u);   // stays in the shared window
     unsigned char* a_self = base;                                   // kPanelChunks x 16 KB
     unsigned char* a_neigh = base + kPanelChunks * kChunkBytesA;    // kPanelChunks x 16 KB
     unsigned char* b_ring = base + 2 * kPanelChunks * kChunkBytesA; // stages x (npad x 128 B)
@@ -216,6 +216,18 @@ __global__ void __launch_bounds__(kSageThreads, 2)
                     for (int j = 0; j < nch; ++j)
                         tma_load_2d(a_self + j * kChunkBytesA, &map_in, col0 + j * kChunkCols, (int)(in_base + row0),
                                     &bar_self);
+                    // the panel's first weight chunks load while the warps aggregate (their stages
+                    // were released by the previous panel's MMAs, complete once bar_mma fired)
+                    const int nk = 2 * nch;
+                    while (g_issued < g_cons + (uint32_t)a.stages && g_issued < g_cons + (uint32_t)nk) {
+                        const uint32_t st = g_issued % a.stages;
+                        if (g_issued >= (uint32_t)a.stages) mb_wait(&bar_empty[st], ((g_issued / a.stages) - 1) & 1);
+                        const int kk = (int)(g_issued - g_cons);
+                        const int wcol = kk < nch ? col0 + kk * kChunkCols : a.kp + col0 + (kk - nch) * kChunkCols;
+                        mb_expect_tx(&bar_full[st], b_stage_bytes);
+                        tma_load_2d(b_ring + st * b_stage_bytes, &map_w, wcol, 0, &bar_full[st]);
+                        ++g_issued;
+                    }
                 }
                 __syncwarp();
             } else {
@@ -321,9 +333,11 @@ __global__ void __launch_bounds__(kSageThreads, 2)
             for (int c = (warp >> 2) * 8; c < a.npad; c += (kAggWarps / 4) * 8) {
                 float v[8];
                 tmem_ld8(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+                const float4 b0 = ldg4(a.bias + c), b1 = ldg4(a.bias + c + 4);
+                const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    float x = __fadd_rn(v[i], __ldg(a.bias + c + i));
+                    float x = __fadd_rn(v[i], bb[i]);
                     v[i] = a.relu ? fmaxf(x, 0.0f) : x;
                 }
                 if (row < n_dst) {
