@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--config", default="arxiv")
     ap.add_argument("--parts", type=int, default=2)
     a = ap.parse_args()
+    bench.select_config(a.config)
     cfg = synth.CONFIGS[a.config]
     P = a.parts
     f_bp, gamma, delta = bench.policy_for(P)
@@ -31,7 +32,7 @@ def main():
     parts = synth.partition(g, P)
     ctx = PL.build_context(0, parts, cfg.feat_dim, synth.FEAT_SEED)
     ctx.buffer_init(gamma, PL.alpha_default(gamma, delta), 1.0, delta, f_bp)
-    W = min(32, delta)
+    W = min(bench.WINDOW, delta)
     ctx.sampler_config(cfg.fanouts, cfg.batch, synth.RUN_SEED, W)
     s = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
