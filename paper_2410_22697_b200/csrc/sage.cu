@@ -40,6 +40,8 @@ constexpr int kChunkCols = 32;              // fp32 columns per 128-byte swizzle
 constexpr int kPanelChunks = 2;             // 64 input columns per panel
 constexpr int kChunkBytesA = kTileM * 128;  // 16 KB
 constexpr int kMaxStages = 8;
+constexpr int kGroups = kAggWarps * 4;      // 8-lane aggregation groups per CTA
+constexpr int kUnroll = 4;                  // neighbour rows in flight per group
 constexpr int kMaxInst = 1024;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -232,55 +234,87 @@ __global__ void __launch_bounds__(kSageThreads, 2)
                 __syncwarp();
             } else {
                 // neighbour means of panel columns [col0, col0 + 32*nch): lane covers the 16-byte
-                // unit lane8 of each chunk g, i.e. columns col0 + 32 g + 4 lane8 .. +3
+                // unit lane8 of each chunk g, i.e. columns col0 + 32 g + 4 lane8 .. +3.
+                // Edge-balanced, deterministic: the tile's edges (grouped by dst row, in CSR order)
+                // are cut at row boundaries into kGroups nearly equal runs; each 8-lane group streams
+                // its run with kUnroll neighbour rows in flight, whatever the degrees, and sums every
+                // row in CSR order (the same order as one row at a time).
                 bool gok[kPanelChunks];
 #pragma unroll
                 for (int g = 0; g < kPanelChunks; ++g) gok[g] = g < nch && col0 + g * kChunkCols + lane8 * 4 < a.in_pitch;
-                for (int r = warp * 4 + sub; r < kTileM; r += kAggWarps * 4) {
+                // rows without neighbours (and rows past the end) are zero
+                for (int i = threadIdx.x; i < nch * kTileM * 8; i += kAggWarps * 32)
+                    reinterpret_cast<float4*>(a_neigh)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                named_sync(2, kAggWarps * 32);
+                const int grp = warp * 4 + sub;
+                const int E = s_off[n_rows];
+                const int t_lo = (int)(((int64_t)grp * E) / kGroups), t_hi = (int)(((int64_t)(grp + 1) * E) / kGroups);
+                // rows r with t_lo <= s_off[r] < t_hi (last group: all remaining rows)
+                int rs = 0, re = n_rows;
+                {
+                    int lo2 = 0, hi2 = n_rows;
+                    while (lo2 < hi2) { const int mid = (lo2 + hi2) >> 1; if (s_off[mid] < t_lo) lo2 = mid + 1; else hi2 = mid; }
+                    rs = lo2;
+                    if (grp + 1 < kGroups) {
+                        lo2 = rs; hi2 = n_rows;
+                        while (lo2 < hi2) { const int mid = (lo2 + hi2) >> 1; if (s_off[mid] < t_hi) lo2 = mid + 1; else hi2 = mid; }
+                        re = lo2;
+                    }
+                }
+                const float* hb = h_in + col0 + lane8 * 4;
+                if (rs < re) {
+                    int r = rs;
+                    int rend = s_off[r + 1];
+                    const int eb = s_off[rs], ee = s_off[re];
                     float4 acc[kPanelChunks];
 #pragma unroll
                     for (int g = 0; g < kPanelChunks; ++g) acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    const int e0 = r < n_rows ? s_off[r] : 0, e1 = r < n_rows ? s_off[r + 1] : 0;
-                    const float* hb = h_in + col0 + lane8 * 4;
-                    int e = e0;
-                    for (; e + 4 <= e1; e += 4) {
-                        float4 v[4][kPanelChunks];
+                    auto flush = [&](int row) {
+                        const int deg = s_off[row + 1] - s_off[row];
+                        if (deg > 0) {
+                            const float fd = (float)deg;
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const float* pj = hb + (int64_t)s_cols[e + j] * a.in_pitch;
+                            for (int g = 0; g < kPanelChunks; ++g) {
+                                if (g < nch && gok[g]) {
+                                    float4 m4;
+                                    m4.x = __fdiv_rn(acc[g].x, fd);
+                                    m4.y = __fdiv_rn(acc[g].y, fd);
+                                    m4.z = __fdiv_rn(acc[g].z, fd);
+                                    m4.w = __fdiv_rn(acc[g].w, fd);
+                                    // SWIZZLE_128B: 16-byte unit u of row r lives at unit u ^ (r % 8)
+                                    *reinterpret_cast<float4*>(a_neigh + g * kChunkBytesA + row * 128 +
+                                                               ((lane8 ^ (row & 7)) << 4)) = m4;
+                                }
+                                acc[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            }
+                        }
+                    };
+                    for (int e = eb; e < ee; e += kUnroll) {
+                        float4 v[kUnroll][kPanelChunks];
 #pragma unroll
-                            for (int g = 0; g < kPanelChunks; ++g)
-                                if (gok[g]) v[j][g] = ldg4(pj + g * kChunkCols);
+                        for (int j = 0; j < kUnroll; ++j) {
+                            if (e + j < ee) {
+                                const float* pj = hb + (int64_t)s_cols[e + j] * a.in_pitch;
+#pragma unroll
+                                for (int g = 0; g < kPanelChunks; ++g)
+                                    if (gok[g]) v[j][g] = ldg4(pj + g * kChunkCols);
+                            }
                         }
 #pragma unroll
-                        for (int j = 0; j < 4; ++j)
+                        for (int j = 0; j < kUnroll; ++j) {
+                            if (e + j < ee) {
+                                while (e + j >= rend) {      // next row of the run (skips empty rows)
+                                    flush(r);
+                                    ++r;
+                                    rend = s_off[r + 1];
+                                }
 #pragma unroll
-                            for (int g = 0; g < kPanelChunks; ++g)
-                                if (gok[g]) add4(acc[g], v[j][g]);
-                    }
-                    for (; e < e1; ++e) {
-                        const float* p0 = hb + (int64_t)s_cols[e] * a.in_pitch;
-#pragma unroll
-                        for (int g = 0; g < kPanelChunks; ++g)
-                            if (gok[g]) add4(acc[g], ldg4(p0 + g * kChunkCols));
-                    }
-                    const int deg = e1 - e0;
-                    if (deg > 0) {
-                        const float fd = (float)deg;
-#pragma unroll
-                        for (int g = 0; g < kPanelChunks; ++g) {
-                            acc[g].x = __fdiv_rn(acc[g].x, fd);
-                            acc[g].y = __fdiv_rn(acc[g].y, fd);
-                            acc[g].z = __fdiv_rn(acc[g].z, fd);
-                            acc[g].w = __fdiv_rn(acc[g].w, fd);
+                                for (int g = 0; g < kPanelChunks; ++g)
+                                    if (gok[g]) add4(acc[g], v[j][g]);
+                            }
                         }
                     }
-                    // SWIZZLE_128B: 16-byte unit u of row r lives at unit u ^ (r % 8)
-#pragma unroll
-                    for (int g = 0; g < kPanelChunks; ++g)
-                        if (g < nch)
-                            *reinterpret_cast<float4*>(a_neigh + g * kChunkBytesA + r * 128 + ((lane8 ^ (r & 7)) << 4)) =
-                                gok[g] ? acc[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    flush(r);
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             }
@@ -405,6 +439,8 @@ bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArg
         if (cudaFuncSetAttribute(k_sage_layer, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sage_smem_bytes(kMaxInst, MGNN_MAX_FANOUT)) != cudaSuccess)
             return false;
+        // the whole unified L1/shared array as shared memory, so two CTAs fit per SM
+        cudaFuncSetAttribute(k_sage_layer, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr = true;
     }
     SageLayerArgs a = args_in;
