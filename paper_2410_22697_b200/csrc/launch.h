@@ -160,7 +160,6 @@ struct SageLayerArgs {
 };
 bool sage_encode_map(void* map_out, const float* base, int64_t rows, int64_t cols, int64_t pitch, int box_rows);
 bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArgs& a, cudaStream_t s);
-size_t sage_smem_bytes(int n_inst, int k_hop);
 
 // load.cu
 void launch_mark_halo(const int32_t* cols, int64_t nnz, int64_t lo, int64_t hi, uint32_t* bm, cudaStream_t s);

@@ -32,16 +32,20 @@ namespace mgnn {
 
 namespace {
 
-constexpr int kAggWarps = 8;                // aggregation / epilogue warps (2 CTAs per SM)
+#ifndef MGNN_SAGE_CTAS
+#define MGNN_SAGE_CTAS 2
+#endif
+constexpr int kCtasPerSm = MGNN_SAGE_CTAS;   // 1: one wide CTA per SM; 2: two narrow CTAs per SM
+constexpr int kAggWarps = kCtasPerSm == 1 ? 24 : 8;   // aggregation / epilogue warps
 constexpr int kCtlWarp = kAggWarps;         // TMA + MMA issue warp
 constexpr int kSageThreads = (kAggWarps + 1) * 32;
 constexpr int kTileM = 128;                 // UMMA M (cta_group::1)
 constexpr int kChunkCols = 32;              // fp32 columns per 128-byte swizzle atom row
-constexpr int kPanelChunks = 2;             // 64 input columns per panel
+constexpr int kPanelChunks = kCtasPerSm == 1 ? 4 : 2;   // 128 / 64 input columns per panel
 constexpr int kChunkBytesA = kTileM * 128;  // 16 KB
 constexpr int kMaxStages = 8;
 constexpr int kGroups = kAggWarps * 4;      // 8-lane aggregation groups per CTA
-constexpr int kUnroll = 4;                  // neighbour rows in flight per group
+constexpr int kUnroll = kCtasPerSm == 1 ? 2 : 4;   // neighbour rows in flight per group
 constexpr int kMaxInst = 1024;
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -107,7 +111,7 @@ __device__ __forceinline__ void add4(float4& a, const float4 b) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kSageThreads, 2)
+__global__ void __launch_bounds__(kSageThreads, kCtasPerSm)
     k_sage_layer(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_w,
                  SageLayerArgs a) {
     extern __shared__ __align__(1024) unsigned char dsm[];
@@ -429,15 +433,16 @@ bool sage_encode_map(void* map_out, const float* base, int64_t rows, int64_t col
 static size_t smem_fixed(int n_inst, int k_hop) {
     return 1024 + 2 * kPanelChunks * kChunkBytesA + (size_t)((n_inst + 4) & ~3) * 4 + (size_t)kTileM * k_hop * 4;
 }
-constexpr size_t kSmemPerCta = 114 * 1024 - 2048;   // two CTAs per SM (228 KB), minus reserved + static
+constexpr size_t kSmemPerCta = (228 * 1024) / kCtasPerSm - 2048;   // per CTA, minus reserved + static
 
-size_t sage_smem_bytes(int n_inst, int k_hop) { return smem_fixed(n_inst, k_hop) + 2 * 32 * 1024; }
 
 bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArgs& args_in, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(k_sage_layer, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sage_smem_bytes(kMaxInst, MGNN_MAX_FANOUT)) != cudaSuccess)
+        int optin = 0, dev0 = 0;
+        cudaGetDevice(&dev0);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev0);
+        if (cudaFuncSetAttribute(k_sage_layer, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024) != cudaSuccess)
             return false;
         // the whole unified L1/shared array as shared memory, so two CTAs fit per SM
         cudaFuncSetAttribute(k_sage_layer, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -450,7 +455,15 @@ bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArg
         return false;
     // weight ring: as many chunk stages as fit next to the rest while two CTAs share the SM
     const int64_t stage = (int64_t)a.npad * 128;
-    const int64_t room = (int64_t)kSmemPerCta - (int64_t)smem_fixed(a.n_inst, a.k_hop);
+    int optin = 0;
+    {
+        int dev0 = 0;
+        cudaGetDevice(&dev0);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev0);
+    }
+    const int64_t cap = std::min<int64_t>((int64_t)kSmemPerCta, (int64_t)optin - 1024);   // 1 KB static
+    const int64_t room = cap - (int64_t)smem_fixed(a.n_inst, a.k_hop);
+    if (room < stage) return false;
     a.stages = (int)std::max<int64_t>(1, std::min<int64_t>(kMaxStages, room / stage));
     const size_t smem = smem_fixed(a.n_inst, a.k_hop) + (size_t)a.stages * stage;
     a.tmem_cols = 32;
@@ -461,8 +474,7 @@ bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArg
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     CUtensorMap mi = *(const CUtensorMap*)map_in, mw = *(const CUtensorMap*)map_w;
-    // two CTAs per SM: one aggregates while the other waits on its MMA / epilogue
-    launch_k(k_sage_layer, dim3(2 * sms), dim3(kSageThreads), smem, s, mi, mw, a);
+    launch_k(k_sage_layer, dim3(kCtasPerSm * sms), dim3(kSageThreads), smem, s, mi, mw, a);
     count_launches(1, __func__, s);
     return true;
 }
