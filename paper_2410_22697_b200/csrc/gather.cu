@@ -192,7 +192,7 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-__global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev G, int R) {
+__global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev G, int R, int stage_bytes) {
     pdl_enter();
     extern __shared__ __align__(128) unsigned char tsm[];
     __shared__ __align__(8) uint64_t bars[kTWarps][2];
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
     const int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
     int32_t* fgid = W.fr_gid + (int64_t)m * W.ucap;
     float* X = W.X + (int64_t)m * W.ucap * pitch;
-    unsigned char* stage[2] = {tsm + (size_t)warp * 2 * kTStageBytes, tsm + (size_t)warp * 2 * kTStageBytes + kTStageBytes};
+    unsigned char* stage[2] = {tsm + (size_t)warp * 2 * stage_bytes, tsm + (size_t)warp * 2 * stage_bytes + stage_bytes};
     const int64_t h_below = pd.h_below, n_local = pd.n_local, lo = pd.lo;
     const unsigned long long wbit = 1ull << w;
     unsigned n_loc = 0, n_hit = 0, n_miss = 0, n_peer = 0;
@@ -311,19 +311,30 @@ void launch_gather(const WinDev& w, const WorldDev& world, cudaStream_t s) {
         const char* e = getenv("MGNN_GATHER");
         return e && e[0] == 'r' ? 0 : 1;
     }();
-    const int R = (int)std::min<int64_t>(32, std::max<int64_t>(1, kTStageBytes / ((int64_t)w.pitch * 4)));
-    if (use_tma && (int64_t)w.pitch * 4 <= kTStageBytes) {
-        const size_t smem = (size_t)kTWarps * 2 * kTStageBytes;
-        static bool attr = false;
-        if (!attr) {
+    // staging per warp: 2 stages of `stage` bytes; `bps` resident blocks per SM (one wave).  The
+    // shared memory left on each SM is what the concurrently running sampling kernels can use.
+    static const int stage = [] {
+        const char* e = getenv("MGNN_GATHER_STAGE");
+        const int v = e ? atoi(e) : kTStageBytes;
+        return v >= 1024 && v <= 32768 ? v : kTStageBytes;
+    }();
+    static const int bps = [] {
+        const char* e = getenv("MGNN_GATHER_BPS");
+        const int v = e ? atoi(e) : 3;
+        return v >= 1 && v <= 8 ? v : 3;
+    }();
+    const int R = (int)std::min<int64_t>(32, std::max<int64_t>(1, stage / ((int64_t)w.pitch * 4)));
+    if (use_tma && (int64_t)w.pitch * 4 <= stage) {
+        const size_t smem = (size_t)kTWarps * 2 * stage;
+        static size_t attr = 0;
+        if (smem > attr) {
             cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
+            attr = smem;
         }
-        // ~3 resident 128-thread blocks per SM (64 KB shared each), one wave
-        int64_t tgt = (148 * 3) / w.n_inst;
+        int64_t tgt = (148 * bps) / w.n_inst;
         int64_t nd = (w.ucap + kTWarps * R - 1) / (kTWarps * R);
         unsigned gxt = (unsigned)std::max<int64_t>(1, std::min(nd, tgt));
-        launch_k(k_gather_tma, dim3(gxt, w.n_inst), dim3(kTWarps * 32), smem, s, w, world, R);
+        launch_k(k_gather_tma, dim3(gxt, w.n_inst), dim3(kTWarps * 32), smem, s, w, world, R, stage);
     } else {
         dim3 grid(gx, w.n_inst);
         if (w.pitch >= 128)
