@@ -97,7 +97,8 @@ struct Win {
     int32_t* cols[kMaxLayers] = {};
     float* X = nullptr;
     int32_t* pos_of = nullptr;
-    uint32_t* nb = nullptr;
+    uint32_t* nb = nullptr;         // [M][L][bm_words] new-node bitmap of each hop (in the zero region)
+    int32_t* wpre = nullptr;        // [M][L][bm_words] frontier position of each word's first new node
     char* zero = nullptr;           // [scan scratch | counts | fb], zeroed per window
     size_t zero_bytes = 0;
     unsigned long long* status = nullptr;
@@ -301,7 +302,7 @@ void free_win(Win& w) {
     }
     dfree(w.X);
     dfree(w.pos_of);
-    dfree(w.nb);
+    dfree(w.wpre);
     dfree(w.zero);
     dfree(w.ext_seeds);
     dfree(w.ext_counts);
@@ -369,6 +370,7 @@ WinDev win_dev(mgnn_ctx ctx, Win& w) {
     d.pos_of = w.pos_of;
     d.fb = w.fb;
     d.nb = w.nb;
+    d.wpre = w.wpre;
     d.parts = ctx->d_parts;
     d.err = ctx->d_err;
     d.gathered_rows = ctx->d_gathered;
@@ -768,11 +770,10 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
         }
         CK(dalloc(&w.X, (size_t)M * ctx->ucap * ctx->pitch));
         CK(dalloc(&w.pos_of, M * ctx->vp_max));
-        CK(dalloc(&w.nb, M * ctx->bm_words));
-        CK(cudaMemset(w.nb, 0, M * ctx->bm_words * sizeof(uint32_t)));
+        CK(dalloc(&w.wpre, M * n_layers * ctx->bm_words));
         CK(dalloc(&w.ext_seeds, M * batch));
         CK(dalloc(&w.ext_counts, M));
-        // zero region: [tile counters | status words | counts | fb]
+        // zero region: [tile counters | status words | counts | fb | per-hop new-node bitmaps]
         size_t ctr_words = (size_t)(2 * n_layers) * M;                  // int32
         size_t st_words = 0;
         for (int i = 0; i < n_layers; ++i)
@@ -781,7 +782,8 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
         size_t off_st = ((ctr_words * 4 + 255) / 256) * 256;
         size_t off_cnt = off_st + ((st_words * 8 + 255) / 256) * 256;
         size_t off_fb = off_cnt + (((size_t)M * 8 * 8 + 255) / 256) * 256;
-        size_t total = off_fb + (size_t)M * ctx->bm_words * 4;
+        size_t off_nb = off_fb + (((size_t)M * ctx->bm_words * 4 + 255) / 256) * 256;
+        size_t total = off_nb + (size_t)M * n_layers * ctx->bm_words * 4;
         CK(dalloc(&w.zero, total));
         CK(cudaMemset(w.zero, 0, total));
         w.zero_bytes = total;
@@ -789,6 +791,7 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
         w.status = (unsigned long long*)(w.zero + off_st);
         w.counts = (long long*)(w.zero + off_cnt);
         w.fb = (uint32_t*)(w.zero + off_fb);
+        w.nb = (uint32_t*)(w.zero + off_nb);
         size_t so = 0;
         for (int i = 0; i < n_layers; ++i) {
             int64_t tc = scan_tiles_count(ctx->fcap[i]);

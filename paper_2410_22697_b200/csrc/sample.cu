@@ -19,9 +19,11 @@
 //               unless already in F_i.
 //   k_compact : the bitmap in rank order IS the ascending-id order, so a
 //               popcount scan appends sorted_unique(cols_i) \ F_i to the
-//               frontier (R#7) and records every node's frontier position.
+//               frontier (R#7) and keeps, per bitmap word, the frontier
+//               position of its first new node.
 // After the last hop k_relabel rewrites the sampled columns as positions in
-// F_{i+1} (the DGL block layout the consumer indexes X with).
+// F_{i+1} (the DGL block layout the consumer indexes X with): a new node's
+// position is its word's position + popc of the lower bits of new_j.
 #include "launch.h"
 
 namespace mgnn {
@@ -194,7 +196,7 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
         if (tile == 0 && threadIdx.x == 0) off[0] = 0;
         int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop] + o_tile;
         const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
-        uint32_t* nb = W.nb + (int64_t)m * W.bm_words;
+        uint32_t* nb = W.nb + ((int64_t)m * W.L + hop) * W.bm_words;
         const int32_t* __restrict__ crank = pd.cols_rank;
     #pragma unroll 4
         for (int e = threadIdx.x; e < (int)agg; e += kThreads) {
@@ -220,7 +222,8 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
     const int64_t ntiles = (nwords + kWordTile - 1) / kWordTile;
     const int tile = claim_tile(sc.tilectr + m, &tslot);
     if (tile >= ntiles) return;
-    uint32_t* nb = W.nb + (int64_t)m * W.bm_words;
+    const uint32_t* nb = W.nb + ((int64_t)m * W.L + hop) * W.bm_words;
+    int32_t* wpre = W.wpre + ((int64_t)m * W.L + hop) * W.bm_words;
     uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
     const int64_t wd = (int64_t)tile * kWordTile + threadIdx.x;
     uint32_t b = (wd < nwords) ? nb[wd] : 0u;
@@ -235,25 +238,38 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
     __syncthreads();
     const int64_t nF = hs[hop];
     int64_t pos = nF + prefix_sh + excl;
-    if (b) {
-        fb[wd] |= b;
-        nb[wd] = 0u;
-    }
+    // new_i keeps its bitmap; with the word's first position it gives every new node's frontier
+    // position as wpre + popc(lower bits) (k_relabel), without a scattered rank -> position table
+    if (wd < nwords) wpre[wd] = (int32_t)pos;
+    if (b) fb[wd] |= b;
     int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
-    int32_t* posof = W.pos_of + (int64_t)m * W.vp_stride;
     while (b) {
         const int bi = __ffs(b) - 1;
         b &= b - 1;
         const int32_t r = (int32_t)(wd * 32 + bi);
         MGNN_CHECK(pos < W.ucap && r < pd.vp, "compact pos=%lld r=%d", (long long)pos, r);
         fr[pos] = r;
-        posof[r] = (int32_t)pos;
         ++pos;
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) hs[hop + 1] = nF + prefix_sh + agg;
 }
 
 // ------------------------------------------------------------------ cols: rank -> position in F_{i+1}
+// A sampled rank c of hop i is either a seed (position from k_seeds' table) or a new node of
+// exactly one hop j <= i; then its position is wpre_j[c/32] + popc(new_j[c/32] & lower bits),
+// since new_j is appended to the frontier in ascending rank order (R#7).
+__device__ __forceinline__ int32_t frontier_pos(const WinDev& W, int m, int hop, const int32_t* __restrict__ posof,
+                                                int32_t c) {
+    const int64_t wd = c >> 5;
+    const uint32_t bit = 1u << (c & 31);
+    for (int j = hop; j >= 0; --j) {
+        const int64_t o = ((int64_t)m * W.L + j) * W.bm_words + wd;
+        const uint32_t b = __ldg(W.nb + o);
+        if (b & bit) return __ldg(W.wpre + o) + __popc(b & (bit - 1u));
+    }
+    return posof[c];
+}
+
 __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
     pdl_enter();
     const int m = blockIdx.y;
@@ -264,13 +280,13 @@ __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
         const int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
         int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop];
         const int64_t E = off[hs[hop]];
-        // 4 independent gathers in flight per thread (the posof loads are random L2 reads)
+        // 4 independent lookups in flight per thread (bitmap / prefix words are L2 reads)
         for (int64_t e0 = (int64_t)blockIdx.x * kThreads * 4 + threadIdx.x; e0 < E; e0 += stride * 4) {
             int32_t c[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) c[j] = e0 + j * kThreads < E ? cols[e0 + j * kThreads] : 0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) c[j] = posof[c[j]];
+            for (int j = 0; j < 4; ++j) c[j] = frontier_pos(W, m, hop, posof, c[j]);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 if (e0 + j * kThreads < E) cols[e0 + j * kThreads] = c[j];
