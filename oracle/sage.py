@@ -71,3 +71,83 @@ def positions(frontier: np.ndarray, cols_global: np.ndarray) -> np.ndarray:
     hold global ids; F_{h+1} is a prefix of F_L, so a position in F_L is a position in F_{h+1})."""
     pos = {int(v): i for i, v in enumerate(frontier)}
     return np.array([pos[int(v)] for v in cols_global], np.int64)
+
+
+# ---------------------------------------------------------------------------------------------
+# Training step (SURVEY §8(f) NEXT-3: "GraphSAGE forward/backward with ncclAllReduce gradients",
+# Alg.1 l.6-8, P:126-137: forward, loss, backward, gradient all-reduce across trainers (DDP),
+# optimizer step).  Loss = mean softmax cross-entropy over the seeds (F_0) of the minibatch; the
+# gradient of a DDP step over P trainers is the average of the trainers' gradients (P:133-137).
+# Written out by hand (chain rule, layer by layer, one destination row at a time), float64.
+
+def sage_forward_cache(X, blocks, weights):
+    """Forward pass keeping what the backward needs: per layer (h_in, mean rows, z)."""
+    L = len(weights)
+    h = np.asarray(X, np.float64)
+    cache = []
+    for l in range(L):
+        off, nbr = blocks[L - 1 - l]
+        n = len(off) - 1
+        ws, wn, b = (np.asarray(a, np.float64) for a in weights[l])
+        mean = np.zeros((n, h.shape[1]))
+        for i in range(n):
+            nb = nbr[off[i]:off[i + 1]]
+            if len(nb):
+                mean[i] = h[nb].sum(axis=0) / len(nb)
+        z = h[:n] @ ws.T + mean @ wn.T + b
+        cache.append((h, mean, z))
+        h = np.maximum(z, 0.0) if l < L - 1 else z
+    return h, cache
+
+
+def softmax_xent(logits, labels):
+    """Mean cross-entropy of rows of logits against integer labels; returns (loss, dlogits)."""
+    z = np.asarray(logits, np.float64)
+    zm = z - z.max(axis=1, keepdims=True)
+    e = np.exp(zm)
+    p = e / e.sum(axis=1, keepdims=True)
+    n = z.shape[0]
+    loss = float(-np.mean(np.log(p[np.arange(n), labels])))
+    d = p.copy()
+    d[np.arange(n), labels] -= 1.0
+    return loss, d / n
+
+
+def sage_backward(blocks, weights, cache, dlogits):
+    """Gradients (dW_self, dW_neigh, db) per layer of the loss whose gradient w.r.t. the
+    logits is dlogits.  Backward of H' = act(H[:n] Ws^T + mean(H[N(i)]) Wn^T + b):
+    dZ = dH' * [Z > 0] (hidden layers), dWs = dZ^T H[:n], dWn = dZ^T mean, db = sum_i dZ_i,
+    dH[i] += dZ_i Ws (i < n), dH[j] += (dZ_i Wn) / |N(i)| for every sampled neighbour j of i."""
+    L = len(weights)
+    grads = [None] * L
+    dh = np.asarray(dlogits, np.float64)
+    for l in range(L - 1, -1, -1):
+        off, nbr = blocks[L - 1 - l]
+        h, mean, z = cache[l]
+        n = len(off) - 1
+        ws, wn, _ = (np.asarray(a, np.float64) for a in weights[l])
+        dz = dh if l == L - 1 else dh * (z > 0.0)
+        grads[l] = (dz.T @ h[:n], dz.T @ mean, dz.sum(axis=0))
+        if l > 0:
+            dh_in = np.zeros_like(h)
+            dh_in[:n] += dz @ ws
+            dmean = dz @ wn
+            for i in range(n):
+                nb = nbr[off[i]:off[i + 1]]
+                for j in nb:
+                    dh_in[j] += dmean[i] / len(nb)
+            dh = dh_in
+    return grads
+
+
+def sage_loss_grads(X, blocks, weights, labels):
+    """(loss, grads) of one minibatch (labels of the seeds F_0, in F_0 order)."""
+    logits, cache = sage_forward_cache(X, blocks, weights)
+    loss, dlog = softmax_xent(logits, labels)
+    return loss, sage_backward(blocks, weights, cache, dlog)
+
+
+def sgd(weights, grads, lr):
+    """W <- W - lr * g for every tensor (plain SGD, the optimizer of the training step)."""
+    return [tuple(np.asarray(w, np.float64) - lr * np.asarray(g, np.float64) for w, g in zip(wl, gl))
+            for wl, gl in zip(weights, grads)]

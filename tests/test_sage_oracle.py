@@ -165,3 +165,99 @@ def test_weights_generator_shapes(dims):
     for l, (ws, wn, b) in enumerate(wts):
         assert ws.shape == (dims[l + 1], dims[l]) and wn.shape == ws.shape and b.shape == (dims[l + 1],)
         assert ws.dtype == np.float32
+
+
+# ------------------------------------------------------------------ training step (NEXT-3)
+def test_xent_closed_forms():
+    # equal logits -> loss = log C and dlogits = (1/C - onehot) / n
+    loss, d = S.softmax_xent(np.zeros((4, 5)), np.array([0, 1, 2, 3]))
+    assert abs(loss - np.log(5.0)) < 1e-15
+    want = np.full((4, 5), 0.2)
+    want[np.arange(4), [0, 1, 2, 3]] -= 1.0
+    np.testing.assert_allclose(d, want / 4, rtol=0, atol=1e-16)
+    # a dominant correct logit -> loss ~ 0, gradient ~ 0
+    z = np.zeros((1, 3))
+    z[0, 2] = 60.0
+    loss, d = S.softmax_xent(z, np.array([2]))
+    assert loss < 1e-25 and np.abs(d).max() < 1e-25
+
+
+def _tiny_problem(seed=0):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((7, 3))
+    blocks = [(np.array([0, 2, 3]), np.array([2, 4, 1])),                       # hop 0: dst F_0 = rows 0, 1
+              (np.array([0, 2, 3, 3, 5, 6]), np.array([5, 6, 0, 1, 6, 2]))]      # hop 1: dst F_1 = rows 0..4
+    wts = synth.sage_weights([3, 4, 3], seed=seed + 1)
+    wts = [tuple(np.asarray(a, np.float64) for a in w) for w in wts]
+    labels = np.array([2, 0])
+    return X, blocks, wts, labels
+
+
+def test_backward_matches_central_differences():
+    X, blocks, wts, labels = _tiny_problem()
+    loss, grads = S.sage_loss_grads(X, blocks, wts, labels)
+    eps = 1e-6
+    worst = 0.0
+    for l in range(2):
+        for t in range(3):
+            g = grads[l][t]
+            it = np.nditer(g, flags=["multi_index"])
+            for _ in it:
+                idx = it.multi_index
+                wp = [list(w) for w in wts]
+                wm = [list(w) for w in wts]
+                wp[l][t] = wts[l][t].copy()
+                wm[l][t] = wts[l][t].copy()
+                wp[l][t][idx] += eps
+                wm[l][t][idx] -= eps
+                lp, _ = S.softmax_xent(S.sage_forward(X, blocks, [tuple(w) for w in wp])[-1], labels)
+                lm, _ = S.softmax_xent(S.sage_forward(X, blocks, [tuple(w) for w in wm])[-1], labels)
+                num = (lp - lm) / (2 * eps)
+                worst = max(worst, abs(num - g[idx]))
+    assert worst < 1e-8, worst
+
+
+@pytest.mark.filterwarnings("ignore::UserWarning")
+def test_backward_matches_torch_autograd_on_sampled_blocks():
+    import torch
+    g = synth.random_graph(600, 0.02, seed=11)
+    parts = synth.partition(g, 2)
+    D = 12
+    W = O.World(parts, D, synth.FEAT_SEED)
+    p = W.parts[1]
+    p.buffer_init(0.9, float(O.alpha_default(0.9, 4)), 1.0, 4, 2500)
+    dims = synth.sage_dims(D, 2, 7, hidden=9)
+    wts = [tuple(np.asarray(a, np.float64) for a in w) for w in synth.sage_weights(dims, seed=5)]
+    rng = np.random.default_rng(2)
+    p.step(synth.RUN_SEED, 1, [10, 25], 32)
+    F = p.frontier()
+    blocks = [(off, S.positions(F, cols)) for off, cols in (p.hop_block(h) for h in range(2))]
+    X = p.features().astype(np.float64)
+    labels = rng.integers(0, 7, size=p.hop_sizes()[0])
+    loss, grads = S.sage_loss_grads(X, blocks, wts, labels)
+    # independent formulation: torch autograd through sparse CSR row-mean matrices
+    tw = [[torch.tensor(a, requires_grad=True) for a in w] for w in wts]
+    h = torch.as_tensor(X)
+    for l in range(2):
+        off, nbr = blocks[1 - l]
+        n = len(off) - 1
+        deg = np.diff(off).astype(np.float64)
+        vals = np.repeat(np.where(deg > 0, 1.0 / np.maximum(deg, 1.0), 0.0), np.diff(off).astype(np.int64))
+        A = torch.sparse_csr_tensor(torch.as_tensor(np.asarray(off, np.int64)), torch.as_tensor(np.asarray(nbr, np.int64)),
+                                    torch.as_tensor(vals), size=(n, h.shape[0]), dtype=torch.float64)
+        z = h[:n] @ tw[l][0].T + (A @ h) @ tw[l][1].T + tw[l][2]
+        h = torch.relu(z) if l == 0 else z
+    tl = torch.nn.functional.cross_entropy(h, torch.as_tensor(labels))
+    tl.backward()
+    assert abs(tl.item() - loss) < 1e-12
+    for l in range(2):
+        for t in range(3):
+            np.testing.assert_allclose(grads[l][t], tw[l][t].grad.numpy(), rtol=1e-10, atol=1e-12)
+    W.close()
+
+
+def test_sgd_step_decreases_loss():
+    X, blocks, wts, labels = _tiny_problem(3)
+    loss0, grads = S.sage_loss_grads(X, blocks, wts, labels)
+    loss1, _ = S.sage_loss_grads(X, blocks, S.sgd(wts, grads, 0.05), labels)
+    assert loss1 < loss0
