@@ -190,6 +190,33 @@ MGNN_API mgnn_status mgnn_sage_config(mgnn_ctx ctx, const mgnn_sage_desc* desc);
 MGNN_API mgnn_status mgnn_sage_forward(mgnn_ctx ctx, int32_t slot, float* logits, int64_t logits_pitch,
                                        mgnn_stream stream);
 
+/* ------------------------------------------------------------------ NEXT-3: a DDP training step
+ * (Alg.1 l.6-8: every trainer runs forward and backward on its
+ * minibatch, gradients are all-reduced across trainers, the replicated model is updated).
+ * One step of the DDP job = window step `step_in_window` of every partition (trainer) hosted
+ * here.  Loss = mean softmax cross-entropy over each trainer's seeds F_0, averaged over the
+ * n_trainers of the whole job (all ranks); gradients accumulate into the ctx's gradient buffer
+ * (mgnn_sage_grads), which the caller all-reduces (sum) across ranks -- e.g. NCCL through
+ * torch.distributed -- before mgnn_sage_sgd.  fp32 weights, TF32 tensor-core GEMMs, fp32
+ * atomics for the gradient reductions (so gradients are reproducible only up to rounding). */
+/* Labels (host int32 [n_global], 0 <= label < dims[L]) and training buffers; after
+ * mgnn_sage_config.  Weights stay those of mgnn_sage_config until mgnn_sage_sgd. */
+MGNN_API mgnn_status mgnn_sage_train_config(mgnn_ctx ctx, const int32_t* labels);
+/* Forward + loss + backward of the instances lp * n_steps + step_in_window of the window in
+ * `slot` (after mgnn_lookup_gather of that slot); gradients ADD to the gradient buffer. */
+MGNN_API mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_window, int32_t n_trainers,
+                                          mgnn_stream stream);
+/* Device pointer and length (floats) of the gradient buffer (the all-reduce operand); its
+ * layout mirrors the padded parameters (per layer [W_self | W_neigh] rows, then the bias). */
+MGNN_API mgnn_status mgnn_sage_grads(mgnn_ctx ctx, float** grads, int64_t* n_floats);
+/* W <- W - lr * g for every parameter, then g <- 0 (plain SGD, ordered on `stream`). */
+MGNN_API mgnn_status mgnn_sage_sgd(mgnn_ctx ctx, float lr, mgnn_stream stream);
+/* Loss accumulated since the last call (sum over steps), copied to the host and reset
+ * (synchronises `stream`). */
+MGNN_API mgnn_status mgnn_sage_loss(mgnn_ctx ctx, float* host_loss, mgnn_stream stream);
+/* Host copies of layer l's current parameters (unpadded, nn.Linear layout; any may be NULL). */
+MGNN_API mgnn_status mgnn_sage_params(mgnn_ctx ctx, int32_t l, float* w_self, float* w_neigh, float* bias);
+
 /* Device view of a window slot (valid after mgnn_sample of that slot). */
 MGNN_API mgnn_status mgnn_window_get(mgnn_ctx ctx, int32_t slot, mgnn_window* out);
 

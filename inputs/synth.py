@@ -258,3 +258,10 @@ def sage_weights(dims: List[int], seed: int = SAGE_SEED):
         b = rng.uniform(-0.1, 0.1, d_out).astype(np.float32)
         out.append((ws, wn, b))
     return out
+
+
+def node_labels(n_nodes: int, n_classes: int, seed: int = SAGE_SEED + 1) -> np.ndarray:
+    """Synthetic class labels (int32 [n_nodes], uniform in [0, n_classes)): the stand-in for the
+    dataset's labels the training step's loss needs (input generation only)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.integers(0, n_classes, size=n_nodes, dtype=np.int64).astype(np.int32)

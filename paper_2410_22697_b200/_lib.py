@@ -20,7 +20,8 @@ SYMBOLS = [
     "mgnn_counts_read_async",
     "mgnn_buffer_snapshot", "mgnn_part_info", "mgnn_halo_get", "mgnn_table_row", "mgnn_launch_count",
     "mgnn_profile_enable", "mgnn_profile_read", "mgnn_profile_kernels",
-    "mgnn_sage_config", "mgnn_sage_forward",
+    "mgnn_sage_config", "mgnn_sage_forward", "mgnn_sage_train_config", "mgnn_sage_train_step",
+    "mgnn_sage_grads", "mgnn_sage_sgd", "mgnn_sage_loss", "mgnn_sage_params",
 ]
 
 
@@ -93,6 +94,12 @@ def load(path: str = LIB_PATH):
         "mgnn_profile_kernels": (S, [I32, P, I64]),
         "mgnn_sage_config": (S, [P, P]),
         "mgnn_sage_forward": (S, [P, I32, P, I64, P]),
+        "mgnn_sage_train_config": (S, [P, P]),
+        "mgnn_sage_train_step": (S, [P, I32, I32, I32, P]),
+        "mgnn_sage_grads": (S, [P, P, P]),
+        "mgnn_sage_sgd": (S, [P, F32, P]),
+        "mgnn_sage_loss": (S, [P, P, P]),
+        "mgnn_sage_params": (S, [P, I32, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

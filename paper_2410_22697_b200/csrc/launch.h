@@ -158,9 +158,85 @@ struct SageLayerArgs {
     float* h_out;              // [M][out_rows][out_pitch]
     int64_t out_rows, out_pitch;
     const float* bias;         // [npad], zero padded
+    int32_t inst0, inst_step;  // kernel instance k is window instance inst0 + k * inst_step
+    float* mean_out;           // optional [M][mean_rows][mean_pitch]: neighbour means (training)
+    int64_t mean_rows, mean_pitch;
 };
 bool sage_encode_map(void* map_out, const float* base, int64_t rows, int64_t cols, int64_t pitch, int box_rows);
 bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArgs& a, cudaStream_t s);
+
+// train.cu: backward of the GraphSAGE-mean consumer (NEXT-3: loss, weight and input gradients)
+struct XentArgs {
+    int32_t n_inst, inst0, inst_step, n_classes;
+    const int64_t* hop_size;   // [M][kMaxLayers+1] (|F_0| = hop_size[m][0])
+    const int32_t* frontier;   // [M][ucap] global ids (F_0 prefix)
+    int64_t ucap;
+    const int32_t* labels;     // [n_global]
+    const float* logits;       // [M][rows][pitch]
+    float* dlogits;            // [M][rows][pitch]
+    int64_t rows, pitch;
+    float scale;               // 1 / (trainers in the DDP step)
+    float* db;                 // [pitch] bias gradient of the last layer (accumulated)
+    float* loss;               // device scalar (accumulated: sum over trainers of mean loss, times scale)
+};
+void launch_xent(const XentArgs& a, cudaStream_t s);
+
+struct MaskArgs {              // dZ = dH * [H > 0] over rows < hop_size[m][hop], column sums -> db
+    int32_t n_inst, inst0, inst_step, hop;
+    const int64_t* hop_size;
+    float* dz;                 // [M][rows][pitch] in place (holds dH on entry)
+    int64_t rows, pitch;
+    const float* h;            // [M][h_rows][h_pitch] layer output H
+    int64_t h_rows, h_pitch;
+    int32_t ncols;             // columns carrying data (npad)
+    float* db;                 // [pitch]
+};
+void launch_relu_mask(const MaskArgs& a, cudaStream_t s);
+
+struct ZeroRowsArgs {          // buf[m][r][*] = 0 for r < hop_size[m][hop]
+    int32_t n_inst, inst0, inst_step, hop;
+    const int64_t* hop_size;
+    float* buf;
+    int64_t rows, pitch;
+};
+void launch_zero_rows(const ZeroRowsArgs& a, cudaStream_t s);
+
+struct WgradArgs {             // dW[npad][2 kp] += dZ^T [H | mean] over the step's rows
+    int32_t n_inst, inst0, inst_step, hop;
+    const int64_t* hop_size;
+    const float* dz;           // [M][dz_rows][dz_pitch]
+    int64_t dz_rows, dz_pitch;
+    const float* h_in;         // [M][in_rows][in_pitch], in_cols columns carry data
+    int64_t in_rows, in_pitch;
+    int32_t in_cols;
+    const float* mean;         // [M][mean_rows][mean_pitch]
+    int64_t mean_rows, mean_pitch;
+    int32_t mean_cols;
+    int32_t kp, npad;
+    float* dw;                 // [npad][2 kp]
+    int32_t ksplit;            // CTAs per (M-tile, N-tile), set by the launcher
+};
+bool launch_wgrad(const WgradArgs& a, cudaStream_t s);
+
+struct DgradArgs {             // dH[i] += dZ_i W_self; dH[j] += dZ_i W_neigh / deg(i) for j in N(i)
+    int32_t n_inst, inst0, inst_step, hop;
+    const int64_t* hop_size;
+    const int64_t* off;
+    int64_t off_stride;
+    const int32_t* cols;
+    int64_t col_stride;
+    int64_t dz_rows;           // rows per instance of dZ
+    int32_t npad_out;          // K of the GEMM (dZ columns)
+    int32_t kp;                // N of each half (input features, padded)
+    int32_t k_in;              // input features with data
+    float* dh;                 // [M][dh_rows][dh_pitch] (zeroed rows < |F_{h+1}|)
+    int64_t dh_rows, dh_pitch;
+};
+bool launch_dgrad(const void* map_dz, const void* map_wt, const DgradArgs& a, cudaStream_t s);
+
+// W <- W - lr * g, g <- 0, and the transposed copy Wt[c][o] = W[o][c] (dgrad operand)
+void launch_sgd(float* w, float* g, int64_t n, float lr, cudaStream_t s);
+void launch_transpose(const float* w, float* wt, int32_t rows, int32_t cols, cudaStream_t s);
 
 // load.cu
 void launch_mark_halo(const int32_t* cols, int64_t nnz, int64_t lo, int64_t hi, uint32_t* bm, cudaStream_t s);

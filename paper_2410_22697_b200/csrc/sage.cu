@@ -27,6 +27,7 @@
 #include <algorithm>
 
 #include "launch.h"
+#include "umma.cuh"
 
 namespace mgnn {
 
@@ -47,67 +48,6 @@ constexpr int kMaxStages = 8;
 constexpr int kGroups = kAggWarps * 4;      // 8-lane aggregation groups per CTA
 constexpr int kUnroll = kCtasPerSm == 1 ? 2 : 4;   // neighbour rows in flight per group
 constexpr int kMaxInst = 1024;
-
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
-}
-__device__ __forceinline__ void mb_expect_tx(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n SW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra SW_%=;\n}\n" ::"r"(
-            su32(b)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* sdst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            su32(sdst)),
-        "l"(map), "r"(c0), "r"(c1), "r"(su32(bar))
-        : "memory");
-}
-// Shared-memory matrix descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart (SBO),
-// LBO unused for swizzled K-major (1), descriptor version 1 (sm_100).
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
-    return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
-           (2ull << 61);
-}
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
-    uint32_t r[8];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-__device__ __forceinline__ void add4(float4& a, const float4 b) {
-    a.x = __fadd_rn(a.x, b.x);
-    a.y = __fadd_rn(a.y, b.y);
-    a.z = __fadd_rn(a.z, b.z);
-    a.w = __fadd_rn(a.w, b.w);
-}
 
 }  // namespace
 
@@ -155,7 +95,9 @@ __global__ void __launch_bounds__(kSageThreads, kCtasPerSm)
         for (int m0 = 0; m0 < a.n_inst; m0 += 32) {
             const int m = m0 + lane;
             int32_t t = 0;
-            if (m < a.n_inst) t = (int32_t)((a.hop_size[(int64_t)m * (kMaxLayers + 1) + a.hop] + kTileM - 1) / kTileM);
+            if (m < a.n_inst)
+                t = (int32_t)((a.hop_size[(int64_t)(a.inst0 + m * a.inst_step) * (kMaxLayers + 1) + a.hop] + kTileM - 1) /
+                              kTileM);
             int32_t x = t;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -187,8 +129,8 @@ __global__ void __launch_bounds__(kSageThreads, kCtasPerSm)
             const int mid = (lo + hi) >> 1;
             if (tile_pref[mid] <= tile) lo = mid; else hi = mid;
         }
-        const int m = lo;
-        const int64_t row0 = (int64_t)(tile - tile_pref[m]) * kTileM;
+        const int m = a.inst0 + lo * a.inst_step;   // window instance
+        const int64_t row0 = (int64_t)(tile - tile_pref[lo]) * kTileM;
         const int64_t n_dst = a.hop_size[(int64_t)m * (kMaxLayers + 1) + a.hop];
         const int n_rows = (int)(n_dst - row0 < kTileM ? n_dst - row0 : kTileM);
         const int64_t in_base = (int64_t)m * a.in_rows;
@@ -325,6 +267,17 @@ __global__ void __launch_bounds__(kSageThreads, kCtasPerSm)
             tc_fence_before();
             named_sync(1, kSageThreads);
             tc_fence_after();
+            if (a.mean_out && warp < kAggWarps) {
+                // training: keep the neighbour means for the weight gradient (read by tcgen05 too)
+                float* mo = a.mean_out + ((int64_t)m * a.mean_rows + row0) * a.mean_pitch + col0;
+                for (int u = threadIdx.x; u < nch * kTileM * 8; u += kAggWarps * 32) {
+                    const int g = u / (kTileM * 8), r = (u >> 3) % kTileM, lu = u & 7;
+                    if (r < n_rows && col0 + g * kChunkCols + lu * 4 < a.mean_pitch)
+                        *reinterpret_cast<float4*>(mo + (int64_t)r * a.mean_pitch + g * kChunkCols + lu * 4) =
+                            *reinterpret_cast<const float4*>(a_neigh + g * kChunkBytesA + r * 128 + ((lu ^ (r & 7)) << 4));
+                }
+                named_sync(2, kAggWarps * 32);
+            }
             if (warp == kCtlWarp && lane == 0) {
                 mb_wait(&bar_self, self_phase & 1);
                 ++self_phase;

@@ -1,0 +1,491 @@
+// train.cu -- backward of the GraphSAGE-mean consumer: one DDP training step per minibatch
+// (Alg.1 l.6-8: every trainer computes the forward
+// pass and the backward pass of its minibatch, gradients are all-reduced across trainers,
+// and the optimizer updates the replicated model).  The forward is k_sage_layer (sage.cu)
+// with the neighbour means kept; here:
+//   k_xent      : softmax cross-entropy of the seeds' logits -> dlogits, loss, bias gradient
+//   k_relu_mask : dZ = dH * [H > 0] (hidden layers) + bias gradient
+//   k_zero_rows : clears a gradient buffer's live rows
+//   k_wgrad     : dW[o][c] += sum_rows dZ[r][o] * [H | mean][r][c]  -- tcgen05 kind::tf32, the
+//                 row-major operands transposed into K-major shared-memory tiles by the CTA's
+//                 threads, split-K over CTAs, partial tiles reduced with red.global.add.v4.f32
+//   k_dgrad     : [dZ W_self | dZ W_neigh] per 128-row tile (tcgen05, K-major, transposed
+//                 weights), epilogue scatters dZ W_neigh / deg to the sampled neighbours
+//   k_sgd, k_transpose : the optimizer step and the dgrad operand layout
+// Gradient reductions use fp32 atomics (order-dependent rounding; the parity bound of the
+// training step is stated in DESIGN.md §7.2).
+#include <algorithm>
+
+#include "launch.h"
+#include "umma.cuh"
+
+namespace mgnn {
+
+namespace {
+
+constexpr int kT = 256;
+
+__device__ __forceinline__ int inst_of(int k, int inst0, int inst_step) { return inst0 + k * inst_step; }
+
+// ------------------------------------------------------------------ loss
+// warp per seed row: softmax over the C logits, cross-entropy against the seed's label
+__global__ void __launch_bounds__(kT) k_xent(XentArgs a) {
+    pdl_enter();
+    __shared__ float s_db[256];
+    __shared__ float s_loss;
+    const int k = blockIdx.y;
+    const int m = inst_of(k, a.inst0, a.inst_step);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int c = threadIdx.x; c < 256; c += kT) s_db[c] = 0.0f;
+    if (threadIdx.x == 0) s_loss = 0.0f;
+    __syncthreads();
+    const int64_t n0 = a.hop_size[(int64_t)m * (kMaxLayers + 1)];
+    const int C = a.n_classes;
+    const float inv = a.scale / (float)(n0 > 0 ? n0 : 1);
+    for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < a.rows; i += (int64_t)gridDim.x * 8) {
+        const float* z = a.logits + ((int64_t)m * a.rows + i) * a.pitch;
+        float* dz = a.dlogits + ((int64_t)m * a.rows + i) * a.pitch;
+        if (i >= n0) {
+            for (int c = lane; c < a.pitch; c += 32) dz[c] = 0.0f;
+            continue;
+        }
+        const int label = a.labels[a.frontier[(int64_t)m * a.ucap + i]];
+        float mx = -INFINITY;
+        for (int c = lane; c < C; c += 32) mx = fmaxf(mx, z[c]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+        float se = 0.0f;
+        for (int c = lane; c < C; c += 32) se += expf(z[c] - mx);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(kFull, se, o);
+        const float lse = logf(se);
+        for (int c = lane; c < a.pitch; c += 32) {
+            float g = 0.0f;
+            if (c < C) {
+                const float p = expf(z[c] - mx - lse);
+                g = (p - (c == label ? 1.0f : 0.0f)) * inv;
+                atomicAdd(&s_db[c], g);
+            }
+            dz[c] = g;
+        }
+        if (lane == 0) atomicAdd(&s_loss, (mx + lse - z[label]) * inv);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < C; c += kT)
+        if (s_db[c] != 0.0f) atomicAdd(&a.db[c], s_db[c]);
+    if (threadIdx.x == 0 && s_loss != 0.0f) atomicAdd(a.loss, s_loss);
+}
+
+// ------------------------------------------------------------------ ReLU backward + bias gradient
+__global__ void __launch_bounds__(kT) k_relu_mask(MaskArgs a) {
+    pdl_enter();
+    __shared__ float s_db[256];
+    const int k = blockIdx.y;
+    const int m = inst_of(k, a.inst0, a.inst_step);
+    for (int c = threadIdx.x; c < 256; c += kT) s_db[c] = 0.0f;
+    __syncthreads();
+    const int64_t n = a.hop_size[(int64_t)m * (kMaxLayers + 1) + a.hop];
+    const int64_t n64 = (n + 63) / 64 * 64;
+    const int q = a.ncols / 4;
+    for (int64_t e = (int64_t)blockIdx.x * kT + threadIdx.x; e < n64 * q; e += (int64_t)gridDim.x * kT) {
+        const int64_t r = e / q;
+        const int c4 = (int)(e - r * q);
+        float4* dz = reinterpret_cast<float4*>(a.dz + ((int64_t)m * a.rows + r) * a.pitch) + c4;
+        if (r >= n) {
+            *dz = make_float4(0.f, 0.f, 0.f, 0.f);
+            continue;
+        }
+        const float4 h = *(reinterpret_cast<const float4*>(a.h + ((int64_t)m * a.h_rows + r) * a.h_pitch) + c4);
+        float4 g = *dz;
+        g.x = h.x > 0.0f ? g.x : 0.0f;
+        g.y = h.y > 0.0f ? g.y : 0.0f;
+        g.z = h.z > 0.0f ? g.z : 0.0f;
+        g.w = h.w > 0.0f ? g.w : 0.0f;
+        *dz = g;
+        if (g.x != 0.0f) atomicAdd(&s_db[4 * c4], g.x);
+        if (g.y != 0.0f) atomicAdd(&s_db[4 * c4 + 1], g.y);
+        if (g.z != 0.0f) atomicAdd(&s_db[4 * c4 + 2], g.z);
+        if (g.w != 0.0f) atomicAdd(&s_db[4 * c4 + 3], g.w);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < a.ncols; c += kT)
+        if (s_db[c] != 0.0f) atomicAdd(&a.db[c], s_db[c]);
+}
+
+__global__ void __launch_bounds__(kT) k_zero_rows(ZeroRowsArgs a) {
+    pdl_enter();
+    const int m = inst_of(blockIdx.y, a.inst0, a.inst_step);
+    const int64_t n = a.hop_size[(int64_t)m * (kMaxLayers + 1) + a.hop];
+    const int64_t n64 = (n + 63) / 64 * 64;
+    const int64_t q = a.pitch / 4;
+    float4* b = reinterpret_cast<float4*>(a.buf + (int64_t)m * a.rows * a.pitch);
+    for (int64_t e = (int64_t)blockIdx.x * kT + threadIdx.x; e < n64 * q; e += (int64_t)gridDim.x * kT)
+        b[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// ------------------------------------------------------------------ weight gradient (tcgen05)
+// dW (M = output features o, N = input columns c) = sum over rows r (the K dimension) of
+// dZ[r][o] * In[r][c].  Both operands are stored row-major with K = rows, i.e. MN-major, which
+// kind::tf32 does not accept (measured: the MMA writes nothing, tools/umma_probe.cu), so the
+// CTA's threads load each 64-row chunk and store it TRANSPOSED into the K-major SWIZZLE_128B
+// layout (operand row = o or c, 128-byte rows of 32 consecutive K values, 16-byte unit u of
+// row x at u ^ (x % 8)); rows past |F_h| and columns past the data read as zero.
+constexpr int kWRows = 64;                       // K rows per chunk
+constexpr int kWRegion = 128 * 128;              // 128 operand rows x 32 K values (fp32): 16 KB
+constexpr int kWStage = 4 * kWRegion;            // A and B, 2 K-regions each: 64 KB
+constexpr int kWMaxInst = 256;
+
+__global__ void __launch_bounds__(128, 1) k_wgrad(WgradArgs a) {
+    extern __shared__ __align__(1024) unsigned char dsm[];
+    __shared__ __align__(8) uint64_t bar_empty[2], bar_done;
+    __shared__ uint32_t tmem_sh;
+    __shared__ int32_t pref[kWMaxInst + 1];
+    unsigned char* base = dsm + ((1024u - (su32(dsm) & 1023u)) & 1023u);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_nt = (2 * a.kp) / 128, n_mt = (a.npad + 127) / 128;
+    const int tile = blockIdx.x % (n_mt * n_nt), ks = blockIdx.x / (n_mt * n_nt);
+    const int mt = tile / n_nt, nt = tile % n_nt;
+    if (warp == 0) {
+        if (lane == 0) {
+            mb_init(&bar_empty[0], 1);
+            mb_init(&bar_empty[1], 1);
+            mb_init(&bar_done, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        tmem_alloc(&tmem_sh, 128);
+    }
+    pdl_enter();
+    if (warp == 1) {     // chunk prefix over the step's instances: ceil(|F_h| / 64) chunks each
+        int32_t run = 0;
+        if (lane == 0) pref[0] = 0;
+        for (int k0 = 0; k0 < a.n_inst; k0 += 32) {
+            const int k = k0 + lane;
+            int32_t t = 0;
+            if (k < a.n_inst)
+                t = (int32_t)((a.hop_size[(int64_t)inst_of(k, a.inst0, a.inst_step) * (kMaxLayers + 1) + a.hop] + kWRows -
+                               1) / kWRows);
+            int32_t x = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(kFull, x, o);
+                if (lane >= o) x += y;
+            }
+            if (k < a.n_inst) pref[k + 1] = run + x;
+            run += __shfl_sync(kFull, x, 31);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_sh;
+    const int total = pref[a.n_inst];
+    const int c_lo = (int)(((int64_t)total * ks) / a.ksplit), c_hi = (int)(((int64_t)total * (ks + 1)) / a.ksplit);
+    const bool neigh = nt * 128 >= a.kp;               // columns of the mean rows
+    const int col0 = neigh ? nt * 128 - a.kp : nt * 128;
+    const float* src_b = neigh ? a.mean : a.h_in;
+    const int64_t b_rows = neigh ? a.mean_rows : a.in_rows, b_pitch = neigh ? a.mean_pitch : a.in_pitch;
+    const int b_cols = neigh ? a.mean_cols : a.in_cols;  // columns carrying data
+    // K-major tf32, M = 128, N = 128
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+    for (int c = c_lo; c < c_hi; ++c) {
+        const int i = c - c_lo, st = i & 1;
+        int lo = 0, hi = a.n_inst;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pref[mid] <= c) lo = mid; else hi = mid;
+        }
+        const int m = inst_of(lo, a.inst0, a.inst_step);
+        const int64_t r0 = (int64_t)(c - pref[lo]) * kWRows;
+        const int64_t n_rows = a.hop_size[(int64_t)m * (kMaxLayers + 1) + a.hop] - r0;
+        if (i >= 2) mb_wait(&bar_empty[st], ((i >> 1) - 1) & 1);   // MMAs of chunk c-2 read this stage
+        unsigned char* sa = base + st * kWStage;
+        unsigned char* sb = sa + 2 * kWRegion;
+        // thread = (operand row x = threadIdx.x, i.e. o or c within the tile); 4 K rows per float4
+        const int x = threadIdx.x;
+        const int o = mt * 128 + x, cc = col0 + x;
+        const float* pa = a.dz + ((int64_t)m * a.dz_rows + r0) * a.dz_pitch + o;
+        const float* pb = src_b + ((int64_t)m * b_rows + r0) * b_pitch + cc;
+        const bool oka = o < a.npad, okb = cc < b_cols;
+#pragma unroll 4
+        for (int k4 = 0; k4 < kWRows / 4; ++k4) {
+            float va[4], vb[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k = k4 * 4 + e;
+                const bool rk = k < n_rows;
+                va[e] = (oka && rk) ? __ldg(pa + (int64_t)k * a.dz_pitch) : 0.0f;
+                vb[e] = (okb && rk) ? __ldg(pb + (int64_t)k * b_pitch) : 0.0f;
+            }
+            const int reg = k4 >> 3, u = k4 & 7;            // 32 K values per region, 8 units of 4
+            const uint32_t off = (uint32_t)(reg * kWRegion + x * 128 + ((u ^ (x & 7)) << 4));
+            *reinterpret_cast<float4*>(sa + off) = make_float4(va[0], va[1], va[2], va[3]);
+            *reinterpret_cast<float4*>(sb + off) = make_float4(vb[0], vb[1], vb[2], vb[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+        if (threadIdx.x == 0) {
+            const uint32_t a0 = su32(sa), b0 = su32(sb);
+#pragma unroll
+            for (int kk = 0; kk < kWRows / 8; ++kk) {      // UMMA K = 8: region kk/4, 32-byte step kk%4
+                const uint32_t ko = (uint32_t)((kk >> 2) * kWRegion + (kk & 3) * 32);
+                mma_tf32(tmem, sdesc(a0 + ko), sdesc(b0 + ko), idesc, (i > 0 || kk > 0) ? 1u : 0u);
+            }
+            mma_commit(&bar_empty[st]);
+        }
+    }
+    if (c_lo < c_hi) {
+        if (threadIdx.x == 0) mma_commit(&bar_done);
+        __syncwarp();
+        mb_wait(&bar_done, 0);
+        tc_fence_after();
+        const int o = mt * 128 + warp * 32 + lane;      // TMEM lane = output feature (M)
+        float* dst = a.dw + (int64_t)o * (2 * a.kp) + nt * 128;
+        for (int c = 0; c < 128; c += 8) {
+            float v[8];
+            tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
+            if (o < a.npad) {
+                red_add4(dst + c, v[0], v[1], v[2], v[3]);
+                red_add4(dst + c + 4, v[4], v[5], v[6], v[7]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) tmem_dealloc(tmem, 128);
+}
+
+// ------------------------------------------------------------------ input gradient (tcgen05, K-major)
+constexpr int kDTile = 128;
+
+__global__ void __launch_bounds__(128, 1)
+    k_dgrad(const __grid_constant__ CUtensorMap map_dz, const __grid_constant__ CUtensorMap map_wt, DgradArgs a,
+            uint32_t tmem_cols) {
+    extern __shared__ __align__(1024) unsigned char dsm[];
+    __shared__ __align__(8) uint64_t bar_full[2], bar_empty[2], bar_done;
+    __shared__ uint32_t tmem_sh;
+    __shared__ int32_t pref[kWMaxInst + 1];
+    unsigned char* base = dsm + ((1024u - (su32(dsm) & 1023u)) & 1023u);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t a_bytes = kDTile * 128, b_bytes = (uint32_t)(2 * a.kp) * 128;
+    const uint32_t stage_bytes = a_bytes + b_bytes;
+    if (warp == 0) {
+        if (lane == 0) {
+            mb_init(&bar_full[0], 1);
+            mb_init(&bar_full[1], 1);
+            mb_init(&bar_empty[0], 1);
+            mb_init(&bar_empty[1], 1);
+            mb_init(&bar_done, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        tmem_alloc(&tmem_sh, tmem_cols);
+    }
+    pdl_enter();
+    if (warp == 1) {
+        int32_t run = 0;
+        if (lane == 0) pref[0] = 0;
+        for (int k0 = 0; k0 < a.n_inst; k0 += 32) {
+            const int k = k0 + lane;
+            int32_t t = 0;
+            if (k < a.n_inst)
+                t = (int32_t)((a.hop_size[(int64_t)inst_of(k, a.inst0, a.inst_step) * (kMaxLayers + 1) + a.hop] + kDTile -
+                               1) / kDTile);
+            int32_t x = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(kFull, x, o);
+                if (lane >= o) x += y;
+            }
+            if (k < a.n_inst) pref[k + 1] = run + x;
+            run += __shfl_sync(kFull, x, 31);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_sh;
+    const int n_tiles = pref[a.n_inst];
+    const int nk = (a.npad_out + 31) / 32;          // K chunks of 32 dZ columns
+    // K-major tf32, M = 128, N = kp per half
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(a.kp >> 3) << 17) | ((128u >> 4) << 24);
+    uint32_t g = 0;        // chunks issued/consumed by this CTA (both stages alternate)
+    uint32_t done_phase = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        int lo = 0, hi = a.n_inst;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pref[mid] <= tile) lo = mid; else hi = mid;
+        }
+        const int m = inst_of(lo, a.inst0, a.inst_step);
+        const int64_t row0 = (int64_t)(tile - pref[lo]) * kDTile;
+        const int64_t n_dst = a.hop_size[(int64_t)m * (kMaxLayers + 1) + a.hop];
+        if (warp == 0 && lane == 0) {
+            auto issue = [&](int j, uint32_t gg) {
+                const int st = gg & 1;
+                if (gg >= 2) mb_wait(&bar_empty[st], ((gg >> 1) - 1) & 1);
+                unsigned char* sa = base + st * stage_bytes;
+                mb_expect_tx(&bar_full[st], stage_bytes);
+                tma_load_2d(sa, &map_dz, j * 32, (int)((int64_t)m * a.dz_rows + row0), &bar_full[st]);
+                tma_load_2d(sa + a_bytes, &map_wt, j * 32, 0, &bar_full[st]);
+                if (a.kp > 128) tma_load_2d(sa + a_bytes + a.kp * 128, &map_wt, j * 32, a.kp, &bar_full[st]);
+            };
+            issue(0, g);
+            for (int j = 0; j < nk; ++j) {
+                const uint32_t gg = g + j;
+                if (j + 1 < nk) issue(j + 1, gg + 1);
+                const int st = gg & 1;
+                mb_wait(&bar_full[st], (gg >> 1) & 1);
+                tc_fence_after();
+                const uint32_t sa = su32(base + st * stage_bytes), sb = sa + a_bytes;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    mma_tf32(tmem, sdesc(sa + k * 32), sdesc(sb + k * 32), idesc, (j > 0 || k > 0) ? 1u : 0u);
+                    mma_tf32(tmem + (uint32_t)a.kp, sdesc(sa + k * 32), sdesc(sb + a.kp * 128 + k * 32), idesc,
+                             (j > 0 || k > 0) ? 1u : 0u);
+                }
+                mma_commit(&bar_empty[st]);
+            }
+            mma_commit(&bar_done);
+        }
+        __syncwarp();
+        g += nk;
+        mb_wait(&bar_done, done_phase & 1);
+        ++done_phase;
+        tc_fence_after();
+        const int r = warp * 32 + lane;
+        const int64_t row = row0 + r;
+        const bool live = row < n_dst;
+        int64_t e0 = 0, e1 = 0;
+        if (live) {
+            e0 = a.off[(int64_t)m * a.off_stride + row];
+            e1 = a.off[(int64_t)m * a.off_stride + row + 1];
+        }
+        const float inv = e1 > e0 ? 1.0f / (float)(e1 - e0) : 0.0f;
+        float* dh_m = a.dh + (int64_t)m * a.dh_rows * a.dh_pitch;
+        const int32_t* nb = a.cols + (int64_t)m * a.col_stride;
+        for (int c = 0; c < a.k_in; c += 8) {
+            float v[8], u[8];
+            tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
+            tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(a.kp + c), u);
+            if (live) {
+                float* d = dh_m + row * a.dh_pitch + c;
+                red_add4(d, v[0], v[1], v[2], v[3]);
+                red_add4(d + 4, v[4], v[5], v[6], v[7]);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) u[i] *= inv;
+                for (int64_t e = e0; e < e1; ++e) {
+                    float* dj = dh_m + (int64_t)nb[e] * a.dh_pitch + c;
+                    red_add4(dj, u[0], u[1], u[2], u[3]);
+                    red_add4(dj + 4, u[4], u[5], u[6], u[7]);
+                }
+            }
+        }
+        tc_fence_before();
+        __syncthreads();      // TMEM is rewritten by the next tile's MMAs
+        tc_fence_after();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) tmem_dealloc(tmem, tmem_cols);
+}
+
+// ------------------------------------------------------------------ optimizer
+__global__ void __launch_bounds__(kT) k_sgd(float* __restrict__ w, float* __restrict__ g, int64_t n, float lr) {
+    pdl_enter();
+    for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
+        w[i] = __fsub_rn(w[i], __fmul_rn(lr, g[i]));
+        g[i] = 0.0f;
+    }
+}
+
+__global__ void __launch_bounds__(kT) k_transpose(const float* __restrict__ w, float* __restrict__ wt, int rows,
+                                                  int cols) {
+    pdl_enter();
+    __shared__ float t[32][33];
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int j = ty; j < 32; j += kT / 32)
+        if (by + j < rows && bx + tx < cols) t[j][tx] = w[(int64_t)(by + j) * cols + bx + tx];
+    __syncthreads();
+    for (int j = ty; j < 32; j += kT / 32)
+        if (bx + j < cols && by + tx < rows) wt[(int64_t)(bx + j) * rows + by + tx] = t[tx][j];
+}
+
+}  // namespace
+
+void launch_xent(const XentArgs& a, cudaStream_t s) {
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((a.rows + 7) / 8, 64));
+    launch_k(k_xent, dim3(gx, a.n_inst), dim3(kT), 0, s, a);
+    count_launches(1, __func__, s);
+}
+
+void launch_relu_mask(const MaskArgs& a, cudaStream_t s) {
+    const int64_t work = ((a.rows + 63) / 64 * 64) * (a.ncols / 4);
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + kT - 1) / kT, 256));
+    launch_k(k_relu_mask, dim3(gx, a.n_inst), dim3(kT), 0, s, a);
+    count_launches(1, __func__, s);
+}
+
+void launch_zero_rows(const ZeroRowsArgs& a, cudaStream_t s) {
+    const int64_t work = a.rows * (a.pitch / 4);
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + kT - 1) / kT, 256));
+    launch_k(k_zero_rows, dim3(gx, a.n_inst), dim3(kT), 0, s, a);
+    count_launches(1, __func__, s);
+}
+
+bool launch_wgrad(const WgradArgs& a_in, cudaStream_t s) {
+    static bool attr = false;
+    const size_t smem = 1024 + 2 * kWStage;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return false;
+        attr = true;
+    }
+    WgradArgs a = a_in;
+    if (a.n_inst > kWMaxInst || a.kp % 128 || a.npad > 256) return false;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int tiles = ((a.npad + 127) / 128) * ((2 * a.kp) / 128);
+    a.ksplit = std::max(1, sms / tiles);
+    launch_k(k_wgrad, dim3(tiles * a.ksplit), dim3(128), smem, s, a);
+    count_launches(1, __func__, s);
+    return true;
+}
+
+bool launch_dgrad(const void* map_dz, const void* map_wt, const DgradArgs& a, cudaStream_t s) {
+    if (a.n_inst > kWMaxInst || a.kp % 32 || a.kp > 256 || a.npad_out > 256) return false;
+    const size_t smem = 1024 + 2 * ((size_t)kDTile * 128 + (size_t)2 * a.kp * 128);
+    static size_t attr = 0;
+    if (smem > attr) {
+        if (cudaFuncSetAttribute(k_dgrad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return false;
+        attr = smem;
+    }
+    uint32_t cols = 32;
+    while ((int)cols < 2 * a.kp) cols <<= 1;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    launch_k(k_dgrad, dim3(sms), dim3(128), smem, s, *(const CUtensorMap*)map_dz, *(const CUtensorMap*)map_wt, a, cols);
+    count_launches(1, __func__, s);
+    return true;
+}
+
+void launch_sgd(float* w, float* g, int64_t n, float lr, cudaStream_t s) {
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kT - 1) / kT, 148 * 8));
+    launch_k(k_sgd, dim3(gx), dim3(kT), 0, s, w, g, n, lr);
+    count_launches(1, __func__, s);
+}
+
+void launch_transpose(const float* w, float* wt, int32_t rows, int32_t cols, cudaStream_t s) {
+    launch_k(k_transpose, dim3((cols + 31) / 32, (rows + 31) / 32), dim3(kT), 0, s, w, wt, rows, cols);
+    count_launches(1, __func__, s);
+}
+
+}  // namespace mgnn

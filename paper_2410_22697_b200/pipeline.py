@@ -173,6 +173,38 @@ class Context:
         self._chk("mgnn_sage_forward", self.L.mgnn_sage_forward(self._h, slot, C.c_void_p(logits.data_ptr()),
                                                                 logits.shape[-1], _stream(stream)))
 
+    # ------------------------------------------------------------ NEXT-3: DDP training step
+    def train_config(self, labels: np.ndarray):
+        lab = np.ascontiguousarray(labels, np.int32)
+        self._chk("mgnn_sage_train_config", self.L.mgnn_sage_train_config(self._h, _ptr(lab)))
+
+    def train_step(self, slot: int, step_in_window: int, n_trainers: int, stream=None):
+        self._chk("mgnn_sage_train_step",
+                  self.L.mgnn_sage_train_step(self._h, slot, step_in_window, n_trainers, _stream(stream)))
+
+    def grads(self):
+        """Zero-copy torch view of the gradient buffer (the all-reduce operand)."""
+        p = C.c_void_p()
+        n = C.c_int64()
+        self._chk("mgnn_sage_grads", self.L.mgnn_sage_grads(self._h, C.byref(p), C.byref(n)))
+        return device_view(p.value, (n.value,), "f4")
+
+    def sgd(self, lr: float, stream=None):
+        self._chk("mgnn_sage_sgd", self.L.mgnn_sage_sgd(self._h, lr, _stream(stream)))
+
+    def loss(self, stream=None) -> float:
+        out = C.c_float()
+        self._chk("mgnn_sage_loss", self.L.mgnn_sage_loss(self._h, C.byref(out), _stream(stream)))
+        return out.value
+
+    def params(self, l: int):
+        d_in, d_out = self.sage_dims[l], self.sage_dims[l + 1]
+        ws = np.zeros((d_out, d_in), np.float32)
+        wn = np.zeros((d_out, d_in), np.float32)
+        b = np.zeros(d_out, np.float32)
+        self._chk("mgnn_sage_params", self.L.mgnn_sage_params(self._h, l, _ptr(ws), _ptr(wn), _ptr(b)))
+        return ws, wn, b
+
     # ------------------------------------------------------------ outputs
     def window(self, slot: int) -> Window:
         w = Window()
