@@ -312,3 +312,22 @@ def exchange_tables(ctx: Context, group=None) -> None:
         for pid, h in d.items():
             if pid not in ctx.parts:
                 ctx.import_table(pid, h)
+
+
+def ddp_step(ctx: Context, slot: int, step_in_window: int, n_trainers: int, lr: float, stream=None,
+             group=None) -> None:
+    """One DDP training step (Alg.1 l.6-8): forward and backward
+    of every local trainer's minibatch (library kernels), sum-all-reduce of the gradient buffer
+    across ranks (NCCL through torch.distributed, on the same stream), then SGD."""
+    import torch
+    import torch.distributed as dist
+    ctx.train_step(slot, step_in_window, n_trainers, stream)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        g = ctx.grads()
+        if stream is not None and not isinstance(stream, int):
+            with torch.cuda.stream(stream):
+                dist.all_reduce(g, group=group)
+        else:
+            dist.all_reduce(g, group=group)
+    ctx.sgd(lr, stream)
+

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--config", default="cfg1")
     ap.add_argument("--delta", type=int, default=4)
     ap.add_argument("--windows", type=int, default=4)
+    ap.add_argument("--train", action="store_true", help="DDP training-step parity (NEXT-3) instead")
     a = ap.parse_args()
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -36,6 +37,14 @@ def main():
     hosted = [2 * rank, 2 * rank + 1]
     ok = torch.ones(1, device="cuda")
     try:
+        if a.train:
+            from tests.train_util import run_train_parity
+            r = run_train_parity(g, P, cfg.feat_dim, cfg.fanouts, cfg.batch, synth.sage_dims(cfg.feat_dim, 2, 16), 3,
+                                 hosted=hosted, device=local, exchange=True)
+            print(f"[rank {rank}] train parity ok: worst error / tolerance {r:.3f}", flush=True)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            dist.destroy_process_group()
+            sys.exit(0 if ok.item() == 1 else 1)
         st = run_parity(g, P, cfg.feat_dim, cfg.fanouts, cfg.batch, 2500, 0.9, a.delta, 1.0,
                         [a.delta] * a.windows, hosted=hosted, device=local, exchange=True,
                         sample_every=1 if a.config == "cfg1" else 9, check_x_rows=0 if a.config == "cfg1" else 2048)

@@ -58,6 +58,66 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
+class FakeTrainCtx:
+    """Stands in for pipeline.Context in ddp_step: CPU gradient buffer, records the call order."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.calls = []
+        self.g = torch.full((6,), float(rank + 1))
+
+    def train_step(self, slot, w, n, stream=None):
+        self.calls.append(("train_step", slot, w, n))
+
+    def grads(self):
+        return self.g
+
+    def sgd(self, lr, stream=None):
+        self.calls.append(("sgd", lr, self.g.tolist()))
+
+
+def _train_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, ROOT)
+    from paper_2410_22697_b200.pipeline import ddp_step
+    ctx = FakeTrainCtx(rank)
+    ddp_step(ctx, 1, 3, 4, 0.5)
+    q.put((rank, ctx.calls))
+    dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_ddp_step():
+    """NEXT-3 host logic: train_step, then the SUM all-reduce of the gradient buffer across ranks,
+    then SGD on the reduced gradients, on every rank."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_train_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, calls in res:
+        assert calls == [("train_step", 1, 3, 4), ("sgd", 0.5, [3.0] * 6)], (rank, calls)
+
+
+@pytest.mark.gpu
+def test_nccl_two_gpus_train_parity():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    port = _free_port()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(ROOT, "tests", "multi_gpu_parity.py"), "--train"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0
+
+
 def test_gloo_two_ranks_table_exchange():
     world = 2
     ctx = mp.get_context("spawn")

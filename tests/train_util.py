@@ -52,7 +52,8 @@ def close(got, ref, what, rows=True, rel=REL):
     return nerr / max(nref, 1e-30)
 
 
-def run_train_parity(g, P, D, fanouts, batch, dims, n_steps, lr=0.05, window=None, device=0):
+def run_train_parity(g, P, D, fanouts, batch, dims, n_steps, lr=0.05, window=None, device=0, hosted=None,
+                     exchange=False):
     """P trainers (partitions) on one GPU, `n_steps` DDP steps of one window: per step compare the
     loss and every gradient with the oracle's average over the P minibatches, then SGD on both
     sides and compare the weights.  Returns the worst (relative gradient error / tolerance)."""
@@ -63,7 +64,10 @@ def run_train_parity(g, P, D, fanouts, batch, dims, n_steps, lr=0.05, window=Non
     W = O.World(parts, D, synth.FEAT_SEED)
     for p in W.parts:
         p.buffer_init(0.95, 0.0, 1.0, 0, 2500)
-    ctx = PL.build_context(device, parts, D, synth.FEAT_SEED)
+    ctx = PL.build_context(device, parts, D, synth.FEAT_SEED, hosted)
+    if exchange:                      # multi-process: map the other ranks' tables (CUDA IPC, NVLink)
+        PL.exchange_tables(ctx)
+    multi = exchange
     ctx.buffer_init(0.95, 0.0, 1.0, 0, 2500)
     window = window or n_steps
     ctx.sampler_config(fanouts, batch, synth.RUN_SEED, window)
@@ -83,9 +87,16 @@ def run_train_parity(g, P, D, fanouts, batch, dims, n_steps, lr=0.05, window=Non
         ctx.lookup_gather(slot)
         for w in range(wl):
             ctx.train_step(slot, w, P)
+            if multi:                 # DDP: sum the ranks' gradient buffers (NCCL) and losses
+                import torch.distributed as dist
+                dist.all_reduce(ctx.grads())
             torch.cuda.synchronize()
             gpu_g = unpack(ctx.grads().cpu().numpy(), dims)
             gpu_loss = ctx.loss()
+            if multi:
+                lt = torch.tensor([gpu_loss], dtype=torch.float64, device="cuda")
+                dist.all_reduce(lt)
+                gpu_loss = float(lt.item())
             ref_g = None
             ref_loss = 0.0
             for pid in range(P):
@@ -114,6 +125,10 @@ def run_train_parity(g, P, D, fanouts, batch, dims, n_steps, lr=0.05, window=Non
         ctx.score(slot)
         t += wl
         slot ^= 1
+    if multi:                         # peers may still read our tables until every rank is done
+        import torch.distributed as dist
+        torch.cuda.synchronize()
+        dist.barrier()
     ctx.close()
     W.close()
     print(f"[train parity] worst gradient error / tolerance {worst:.3f}")
