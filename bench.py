@@ -485,6 +485,67 @@ def main():
         n_edges = np.array([int(offs[m, int(hs[m, hop])]) for m in range(wv.n_inst)], np.float64)
         agg_bytes += float((n_edges * dims[l] * 4).sum())
 
+    # ---------------- with training (NEXT-3): every minibatch trains the model -- forward, loss,
+    # backward, NCCL all-reduce of the gradients across ranks (N > 1), SGD -- on stream C, one
+    # DDP step per window step (the steps of a window are sequential through the weights), while
+    # streams A/B prepare the next windows (Alg.1: prepare(t+1) || train(t)).
+    labels = synth.node_labels(CFG.n_nodes, dims[-1])
+    ctx.train_config(labels)
+    n_trainers = PARTS_PER_GPU * world
+    lr = 0.01
+    ev_trained = [torch.cuda.Event(), torch.cuda.Event()]
+
+    def sample_async_t(sl, tt):
+        sA.wait_event(ev_done[sl])
+        sA.wait_event(ev_trained[sl])
+        ctx.sample(sl, tt, WINDOW, stream=sA)
+        ev_sampled[sl].record(sA)
+
+    def consume_train(sl):
+        sB.wait_event(ev_sampled[sl])
+        ctx.lookup_gather(sl, sB)
+        ev_gathered[sl].record(sB)
+        ctx.score(sl, sB)
+        ev_done[sl].record(sB)
+        sC.wait_event(ev_gathered[sl])
+        for w_ in range(WINDOW):
+            PL.ddp_step(ctx, sl, w_, n_trainers, lr, stream=sC)
+        ev_trained[sl].record(sC)
+
+    KT = max(3, min(K, 6))
+    t_t = t_c                   # the window pending in `slot` (sampled, not yet gathered)
+    barrier()
+    sample_async_t(slot, t_t)
+    for _ in range(args.warmup):
+        sample_async_t(slot ^ 1, t_t + WINDOW)
+        consume_train(slot)
+        t_t += WINDOW
+        slot ^= 1
+    barrier()
+    ctx.loss(sC)
+    t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush.zero_()
+    t0e.record(sB)
+    sA.wait_event(t0e)
+    sC.wait_event(t0e)
+    for i in range(KT):
+        sample_async_t(slot ^ 1, t_t + WINDOW)
+        consume_train(slot)
+        t_t += WINDOW
+        slot ^= 1
+    sB.wait_stream(sA)
+    sB.wait_stream(sC)
+    t1e.record(sB)
+    barrier()
+    tr_ms = torch.tensor([t0e.elapsed_time(t1e)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tr_ms, op=dist.ReduceOp.MAX)
+    tr_value = WINDOW * PARTS_PER_GPU * world * KT / (float(tr_ms.item()) / 1e3)
+    tr_loss_t = torch.tensor([ctx.loss(sC) / (KT * WINDOW)], dtype=torch.float64, device="cuda")
+    if world > 1:                       # each rank holds its trainers' share of the mean loss
+        dist.all_reduce(tr_loss_t)
+    tr_loss = float(tr_loss_t.item())
+
     clocks = clk.summary()
     if rank == 0:
         peaks = {}
@@ -531,6 +592,14 @@ def main():
                           "tcgen05.mma kind::tf32 (TMEM accumulator) -> bias/ReLU epilogue",
                 "tflops": flops / (fwd_ms / 1e3) / 1e12 if fwd_ms > 0 else None,
                 "agg_gbs": agg_bytes / (fwd_ms / 1e3) / 1e9 if fwd_ms > 0 else None,
+                "dtype": "tf32 x tf32 -> f32"},
+            "with_training": {
+                "value": tr_value, "unit": UNIT, "ms_per_step": float(tr_ms.item()) / KT, "steps": KT,
+                "model": f"GraphSAGE-mean {dims}, softmax cross-entropy, SGD lr {lr}",
+                "ddp": f"{n_trainers} trainers; gradient all-reduce " + ("NCCL (torch.distributed)" if world > 1
+                                                                          else "none (one rank)"),
+                "mean_loss_in_timed_steps": tr_loss,
+                "pipeline": "3 streams: sample(w+2) | gather+score(w+1) | DDP steps of window w",
                 "dtype": "tf32 x tf32 -> f32"},
         }
         if world > 1:
