@@ -236,6 +236,7 @@ def main():
     ap.add_argument("--impl", default="mgnn", choices=["mgnn", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-train-graph", action="store_true", help="training steps as eager launches")
     ap.add_argument("--config", default="arxiv", choices=sorted(LAYOUT),
                     help="workload (default: arxiv-shaped, BASELINE.json configs[1])")
     args = ap.parse_args()
@@ -501,6 +502,30 @@ def main():
         ctx.sample(sl, tt, WINDOW, stream=sA)
         ev_sampled[sl].record(sA)
 
+    # The WINDOW DDP steps of a slot are one CUDA graph (captured once per slot, replayed every
+    # window): ~12 launches per step, all device-resident sizes, so the graph is static.
+    graphs = {}
+    use_graph = [not args.no_train_graph]
+
+    def train_window(sl):
+        if use_graph[0]:
+            if sl not in graphs:
+                try:
+                    g_ = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g_, stream=sC):
+                        for w_ in range(WINDOW):
+                            PL.ddp_step(ctx, sl, w_, n_trainers, lr, stream=torch.cuda.current_stream())
+                    graphs[sl] = g_
+                except Exception as e:  # capture unsupported here: stay eager
+                    print(f"[bench] training graph capture failed ({e!r}); eager launches", file=sys.stderr)
+                    use_graph[0] = False
+            if use_graph[0]:
+                with torch.cuda.stream(sC):
+                    graphs[sl].replay()
+                return
+        for w_ in range(WINDOW):
+            PL.ddp_step(ctx, sl, w_, n_trainers, lr, stream=sC)
+
     def consume_train(sl):
         sB.wait_event(ev_sampled[sl])
         ctx.lookup_gather(sl, sB)
@@ -508,8 +533,7 @@ def main():
         ctx.score(sl, sB)
         ev_done[sl].record(sB)
         sC.wait_event(ev_gathered[sl])
-        for w_ in range(WINDOW):
-            PL.ddp_step(ctx, sl, w_, n_trainers, lr, stream=sC)
+        train_window(sl)
         ev_trained[sl].record(sC)
 
     KT = max(3, min(K, 6))
@@ -600,6 +624,7 @@ def main():
                                                                           else "none (one rank)"),
                 "mean_loss_in_timed_steps": tr_loss,
                 "pipeline": "3 streams: sample(w+2) | gather+score(w+1) | DDP steps of window w",
+                "cuda_graph": bool(use_graph[0]),
                 "dtype": "tf32 x tf32 -> f32"},
         }
         if world > 1:

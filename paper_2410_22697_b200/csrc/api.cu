@@ -184,9 +184,10 @@ struct mgnn_ctx_s {
         float* logits = nullptr;                  // [M][rows64][npad_L]
         float* dlogits = nullptr;
         float* dh[kMaxLayers] = {};               // gradient of h[l]: [M][dh_rows[l]][npad[l]]
+        float* dmean = nullptr;                   // dZ W_neigh / deg of the current layer (dgrad -> scatter)
         float* loss = nullptr;                    // device scalar
         int64_t rows64 = 0, dh_rows[kMaxLayers] = {};
-        alignas(64) unsigned char map_dz128[kMaxLayers][128], map_wt[kMaxLayers][128];
+        alignas(64) unsigned char map_dz128[kMaxLayers][128], map_wt[kMaxLayers][128], map_mean128[kMaxLayers][128];
     } sage;
     // ordering of windows through the buffer
     bool seq_started = false;
@@ -335,6 +336,7 @@ void free_sage(mgnn_ctx_s* ctx) {
         dfree(S.dh[l]);
     }
     dfree(S.labels);
+    dfree(S.dmean);
     dfree(S.grads);
     dfree(S.logits);
     dfree(S.dlogits);
@@ -1078,7 +1080,8 @@ mgnn_status mgnn_sage_config(mgnn_ctx ctx, const mgnn_sage_desc* d) {
 namespace {
 // one forward layer over `n_inst` instances inst0, inst0 + inst_step, ... of a window slot
 mgnn_status sage_layer(mgnn_ctx ctx, Win& w, int slot, int l, int n_inst, int inst0, int inst_step, float* out,
-                       int64_t out_rows, int64_t out_pitch, int n_out, float* mean_out, cudaStream_t s) {
+                       int64_t out_rows, int64_t out_pitch, int n_out, float* mean_out, cudaStream_t s,
+                       bool mean_first = false) {
     auto& S = ctx->sage;
     const int L = S.L, hop = L - 1 - l;
     SageLayerArgs a;
@@ -1114,7 +1117,11 @@ mgnn_status sage_layer(mgnn_ctx ctx, Win& w, int slot, int l, int n_inst, int in
     a.mean_out = mean_out;
     a.mean_rows = S.out_rows[l];
     a.mean_pitch = S.kp[l];
-    if (!launch_sage_layer(S.map_in[slot][l], S.map_w[l], a, s))
+    if (mean_first) {          // training: means by k_mean over all SMs, then the GEMM reads them by TMA
+        launch_mean(a, s);
+        a.mean_in = 1;
+    }
+    if (!launch_sage_layer(S.map_in[slot][l], S.map_w[l], mean_first ? S.map_mean128[l] : nullptr, a, s))
         return fail(ctx, MGNN_ECUDA, "sage: layer launch configuration failed");
     return MGNN_OK;
 }
@@ -1167,6 +1174,9 @@ mgnn_status mgnn_sage_train_config(mgnn_ctx ctx, const int32_t* labels) {
         CK(dalloc(&S.dlogits, nl));
         CK(cudaMemset(S.logits, 0, nl * sizeof(float)));
         CK(cudaMemset(S.dlogits, 0, nl * sizeof(float)));
+        int64_t ndm = 1;
+        for (int l = 1; l < L; ++l) ndm = std::max(ndm, M * S.out_rows[l] * S.kp[l]);
+        CK(dalloc(&S.dmean, ndm));
         for (int l = 0; l < L; ++l) {
             const int64_t nm = M * S.out_rows[l] * S.kp[l];
             CK(dalloc(&S.mean[l], nm));
@@ -1184,6 +1194,7 @@ mgnn_status mgnn_sage_train_config(mgnn_ctx ctx, const int32_t* labels) {
             const int64_t dzr = l == L - 1 ? S.rows64 : S.dh_rows[l];
             const int64_t wtr = 2 * (int64_t)S.kp[l];
             if (!sage_encode_map(S.map_dz128[l], dz, M * dzr, S.npad[l], S.npad[l], 128) ||
+                !sage_encode_map(S.map_mean128[l], S.mean[l], M * S.out_rows[l], S.kp[l], S.kp[l], 128) ||
                 !sage_encode_map(S.map_wt[l], S.wt[l], wtr, S.npad[l], S.npad[l], (int)(wtr <= 256 ? wtr : S.kp[l])))
                 return fail(ctx, MGNN_ECUDA, "train: cuTensorMapEncodeTiled failed");
             launch_transpose(S.w[l], S.wt[l], S.npad[l], (int32_t)wtr, 0);
@@ -1211,9 +1222,9 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
     // forward, keeping every layer's output and neighbour means
     for (int l = 0; l < L; ++l) {
         mgnn_status st = l < L - 1 ? sage_layer(ctx, w, slot, l, n_lp, i0, is, S.h[l], S.out_rows[l], S.npad[l],
-                                                S.npad[l], S.mean[l], s)
+                                                S.npad[l], S.mean[l], s, true)
                                    : sage_layer(ctx, w, slot, l, n_lp, i0, is, S.logits, S.rows64, S.npad[l],
-                                                S.npad[l], S.mean[l], s);
+                                                S.npad[l], S.mean[l], s, true);
         if (st) return st;
     }
     // loss: mean cross-entropy per trainer, averaged over the n_trainers of the DDP step
@@ -1315,8 +1326,11 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
             da.dh = S.dh[l - 1];
             da.dh_rows = S.dh_rows[l - 1];
             da.dh_pitch = S.npad[l - 1];
+            da.dmean = S.dmean;
+            da.dmean_rows = S.out_rows[l];
             if (!launch_dgrad(S.map_dz128[l], S.map_wt[l], da, s))
                 return fail(ctx, MGNN_ECUDA, "train: dgrad launch configuration failed");
+            launch_scatter(da, s);
         }
     }
     CKL();
@@ -1337,8 +1351,17 @@ mgnn_status mgnn_sage_sgd(mgnn_ctx ctx, float lr, mgnn_stream stream) {
     auto& S = ctx->sage;
     if (!S.train) return fail(ctx, MGNN_ESTATE, "sgd before train_config");
     cudaStream_t s = (cudaStream_t)stream;
-    launch_sgd(S.params, S.grads, S.n_params, lr, s);
-    for (int l = 0; l < S.L; ++l) launch_transpose(S.w[l], S.wt[l], S.npad[l], 2 * S.kp[l], s);
+    SgdLayers d;
+    memset(&d, 0, sizeof(d));
+    d.n_layers = S.L;
+    for (int l = 0; l < S.L; ++l) {     // the bias follows its layer's block (b_off = w_off + npad * 2 kp)
+        d.w[l] = S.w[l];
+        d.g[l] = S.grads + S.w_off[l];
+        d.wt[l] = S.wt[l];
+        d.rows[l] = S.npad[l];
+        d.cols[l] = 2 * (int64_t)S.kp[l];
+    }
+    launch_sgd_layers(d, lr, s);
     CKL();
     return MGNN_OK;
 }

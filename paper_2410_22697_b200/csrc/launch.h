@@ -161,9 +161,14 @@ struct SageLayerArgs {
     int32_t inst0, inst_step;  // kernel instance k is window instance inst0 + k * inst_step
     float* mean_out;           // optional [M][mean_rows][mean_pitch]: neighbour means (training)
     int64_t mean_rows, mean_pitch;
+    int32_t mean_in;           // 1: the means are already in mean_out (k_mean); TMA them, no aggregation
 };
 bool sage_encode_map(void* map_out, const float* base, int64_t rows, int64_t cols, int64_t pitch, int box_rows);
-bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArgs& a, cudaStream_t s);
+bool launch_sage_layer(const void* map_in, const void* map_w, const void* map_mean, const SageLayerArgs& a,
+                       cudaStream_t s);
+// neighbour means of a layer's dst rows into mean_out (warp per row, all SMs): the training step's
+// forward, whose per-step instance count is too small for the fused aggregation to fill the GPU
+void launch_mean(const SageLayerArgs& a, cudaStream_t s);
 
 // train.cu: backward of the GraphSAGE-mean consumer (NEXT-3: loss, weight and input gradients)
 struct XentArgs {
@@ -231,11 +236,23 @@ struct DgradArgs {             // dH[i] += dZ_i W_self; dH[j] += dZ_i W_neigh / 
     int32_t k_in;              // input features with data
     float* dh;                 // [M][dh_rows][dh_pitch] (zeroed rows < |F_{h+1}|)
     int64_t dh_rows, dh_pitch;
+    float* dmean;              // [M][dmean_rows][kp]: dZ_i W_neigh / deg(i), scattered by k_scatter
+    int64_t dmean_rows;
 };
 bool launch_dgrad(const void* map_dz, const void* map_wt, const DgradArgs& a, cudaStream_t s);
+// dH[j] += dmean[i] for every sampled neighbour j of dst row i (warp per row, vector atomics)
+void launch_scatter(const DgradArgs& a, cudaStream_t s);
 
 // W <- W - lr * g, g <- 0, and the transposed copy Wt[c][o] = W[o][c] (dgrad operand)
 void launch_sgd(float* w, float* g, int64_t n, float lr, cudaStream_t s);
+struct SgdLayers {             // per layer: Wcat [rows][cols] followed by the bias [rows]; Wt [cols][rows]
+    int32_t n_layers;
+    float* w[kMaxLayers];
+    float* g[kMaxLayers];
+    float* wt[kMaxLayers];
+    int64_t rows[kMaxLayers], cols[kMaxLayers];
+};
+void launch_sgd_layers(const SgdLayers& d, float lr, cudaStream_t s);
 void launch_transpose(const float* w, float* wt, int32_t rows, int32_t cols, cudaStream_t s);
 
 // load.cu

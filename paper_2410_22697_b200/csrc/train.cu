@@ -10,7 +10,8 @@
 //                 row-major operands transposed into K-major shared-memory tiles by the CTA's
 //                 threads, split-K over CTAs, partial tiles reduced with red.global.add.v4.f32
 //   k_dgrad     : [dZ W_self | dZ W_neigh] per 128-row tile (tcgen05, K-major, transposed
-//                 weights), epilogue scatters dZ W_neigh / deg to the sampled neighbours
+//                 weights); the epilogue stores dZ W_self into dH and dZ W_neigh / deg into dmean
+//   k_scatter   : dmean rows added to the sampled neighbours' dH rows (warp per row, atomics)
 //   k_sgd, k_transpose : the optimizer step and the dgrad operand layout
 // Gradient reductions use fp32 atomics (order-dependent rounding; the parity bound of the
 // training step is stated in DESIGN.md §7.2).
@@ -359,29 +360,25 @@ __global__ void __launch_bounds__(128, 1)
         const int r = warp * 32 + lane;
         const int64_t row = row0 + r;
         const bool live = row < n_dst;
-        int64_t e0 = 0, e1 = 0;
+        int64_t e0 = 0, e1 = 0;   // the row's neighbours: only their count (mean divisor) is used here
         if (live) {
             e0 = a.off[(int64_t)m * a.off_stride + row];
             e1 = a.off[(int64_t)m * a.off_stride + row + 1];
         }
         const float inv = e1 > e0 ? 1.0f / (float)(e1 - e0) : 0.0f;
-        float* dh_m = a.dh + (int64_t)m * a.dh_rows * a.dh_pitch;
-        const int32_t* nb = a.cols + (int64_t)m * a.col_stride;
+        // dH rows < |F_h| are written here (k_zero_rows cleared them; the scatter adds later);
+        // the neighbour part goes to dmean for k_scatter, which spreads it over all SMs
+        float* d = a.dh + ((int64_t)m * a.dh_rows + row) * a.dh_pitch;
+        float* dm = a.dmean + ((int64_t)m * a.dmean_rows + row) * a.kp;
         for (int c = 0; c < a.k_in; c += 8) {
             float v[8], u[8];
             tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
             tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(a.kp + c), u);
             if (live) {
-                float* d = dh_m + row * a.dh_pitch + c;
-                red_add4(d, v[0], v[1], v[2], v[3]);
-                red_add4(d + 4, v[4], v[5], v[6], v[7]);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) u[i] *= inv;
-                for (int64_t e = e0; e < e1; ++e) {
-                    float* dj = dh_m + (int64_t)nb[e] * a.dh_pitch + c;
-                    red_add4(dj, u[0], u[1], u[2], u[3]);
-                    red_add4(dj + 4, u[4], u[5], u[6], u[7]);
-                }
+                reinterpret_cast<float4*>(d + c)[0] = make_float4(v[0], v[1], v[2], v[3]);
+                reinterpret_cast<float4*>(d + c)[1] = make_float4(v[4], v[5], v[6], v[7]);
+                reinterpret_cast<float4*>(dm + c)[0] = make_float4(u[0] * inv, u[1] * inv, u[2] * inv, u[3] * inv);
+                reinterpret_cast<float4*>(dm + c)[1] = make_float4(u[4] * inv, u[5] * inv, u[6] * inv, u[7] * inv);
             }
         }
         tc_fence_before();
@@ -394,12 +391,104 @@ __global__ void __launch_bounds__(128, 1)
     if (warp == 0) tmem_dealloc(tmem, tmem_cols);
 }
 
+// warp per dst row i: dH[j] += dmean[i] over the row's sampled neighbours j, one 16-byte vector
+// atomic per lane per neighbour (128 columns per warp instruction)
+__global__ void __launch_bounds__(kT) k_scatter(DgradArgs a) {
+    pdl_enter();
+    const int m = inst_of(blockIdx.y, a.inst0, a.inst_step);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n_dst = a.hop_size[(int64_t)m * (kMaxLayers + 1) + a.hop];
+    const int64_t* off = a.off + (int64_t)m * a.off_stride;
+    const int32_t* nb = a.cols + (int64_t)m * a.col_stride;
+    float* dh_m = a.dh + (int64_t)m * a.dh_rows * a.dh_pitch;
+    for (int64_t i = (int64_t)blockIdx.x * (kT / 32) + warp; i < n_dst; i += (int64_t)gridDim.x * (kT / 32)) {
+        const int64_t e0 = off[i], e1 = off[i + 1];
+        if (e0 == e1) continue;
+        const float* dm = a.dmean + ((int64_t)m * a.dmean_rows + i) * a.kp;
+        for (int c = lane * 4; c < a.k_in; c += 128) {
+            const float4 u = *reinterpret_cast<const float4*>(dm + c);
+            for (int64_t e = e0; e < e1; ++e) red_add4(dh_m + (int64_t)nb[e] * a.dh_pitch + c, u.x, u.y, u.z, u.w);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ neighbour means (training forward)
+// warp per dst row: lanes cover 128 columns as float4, 4 neighbour rows in flight
+__global__ void __launch_bounds__(kT) k_mean(SageLayerArgs a) {
+    pdl_enter();
+    const int m = inst_of(blockIdx.y, a.inst0, a.inst_step);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n_dst = a.hop_size[(int64_t)m * (kMaxLayers + 1) + a.hop];
+    const int64_t* off = a.off + (int64_t)m * a.off_stride;
+    const int32_t* nb = a.cols + (int64_t)m * a.col_stride;
+    const float* h = a.h_in + (int64_t)m * a.in_rows * a.in_pitch;
+    for (int64_t i = (int64_t)blockIdx.x * (kT / 32) + warp; i < n_dst; i += (int64_t)gridDim.x * (kT / 32)) {
+        const int64_t e0 = off[i], e1 = off[i + 1];
+        float* mo = a.mean_out + ((int64_t)m * a.mean_rows + i) * a.mean_pitch;
+        const float inv = (float)(e1 - e0);
+        for (int c = lane * 4; c < a.mean_pitch; c += 128) {
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (c < a.k_in) {
+                int64_t e = e0;
+                for (; e + 4 <= e1; e += 4) {
+                    float4 v[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[j] = __ldg(reinterpret_cast<const float4*>(h + (int64_t)nb[e + j] * a.in_pitch + c));
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        acc.x = __fadd_rn(acc.x, v[j].x);
+                        acc.y = __fadd_rn(acc.y, v[j].y);
+                        acc.z = __fadd_rn(acc.z, v[j].z);
+                        acc.w = __fadd_rn(acc.w, v[j].w);
+                    }
+                }
+                for (; e < e1; ++e) {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(h + (int64_t)nb[e] * a.in_pitch + c));
+                    acc.x = __fadd_rn(acc.x, v.x);
+                    acc.y = __fadd_rn(acc.y, v.y);
+                    acc.z = __fadd_rn(acc.z, v.z);
+                    acc.w = __fadd_rn(acc.w, v.w);
+                }
+                if (e1 > e0) {
+                    acc.x = __fdiv_rn(acc.x, inv);
+                    acc.y = __fdiv_rn(acc.y, inv);
+                    acc.z = __fdiv_rn(acc.z, inv);
+                    acc.w = __fdiv_rn(acc.w, inv);
+                }
+            }
+            *reinterpret_cast<float4*>(mo + c) = acc;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ optimizer
 __global__ void __launch_bounds__(kT) k_sgd(float* __restrict__ w, float* __restrict__ g, int64_t n, float lr) {
     pdl_enter();
     for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
         w[i] = __fsub_rn(w[i], __fmul_rn(lr, g[i]));
         g[i] = 0.0f;
+    }
+}
+
+// SGD over every layer's [W_self | W_neigh] block (and bias) in one launch, also refreshing the
+// transposed copy the input-gradient GEMM reads
+__global__ void __launch_bounds__(kT) k_sgd_layers(SgdLayers d, float lr) {
+    pdl_enter();
+    for (int l = 0; l < d.n_layers; ++l) {
+        const int64_t rows = d.rows[l], cols = d.cols[l];
+        float* w = d.w[l];
+        float* g = d.g[l];
+        float* wt = d.wt[l];
+        const int64_t n = rows * cols + rows;          // block then bias (contiguous)
+        for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
+            const float v = __fsub_rn(w[i], __fmul_rn(lr, g[i]));
+            w[i] = v;
+            g[i] = 0.0f;
+            if (i < rows * cols && wt) {
+                const int64_t o = i / cols, c = i - o * cols;
+                wt[c * rows + o] = v;
+            }
+        }
     }
 }
 
@@ -477,9 +566,24 @@ bool launch_dgrad(const void* map_dz, const void* map_wt, const DgradArgs& a, cu
     return true;
 }
 
+void launch_scatter(const DgradArgs& a, cudaStream_t s) {
+    launch_k(k_scatter, dim3(64, a.n_inst), dim3(kT), 0, s, a);
+    count_launches(1, __func__, s);
+}
+
+void launch_mean(const SageLayerArgs& a, cudaStream_t s) {
+    launch_k(k_mean, dim3(128, a.n_inst), dim3(kT), 0, s, a);
+    count_launches(1, __func__, s);
+}
+
 void launch_sgd(float* w, float* g, int64_t n, float lr, cudaStream_t s) {
     const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kT - 1) / kT, 148 * 8));
     launch_k(k_sgd, dim3(gx), dim3(kT), 0, s, w, g, n, lr);
+    count_launches(1, __func__, s);
+}
+
+void launch_sgd_layers(const SgdLayers& d, float lr, cudaStream_t s) {
+    launch_k(k_sgd_layers, dim3(148), dim3(kT), 0, s, d, lr);
     count_launches(1, __func__, s);
 }
 
