@@ -47,3 +47,13 @@ def test_arxiv_window_sampled_instances():
     g = synth.generate(synth.CONFIGS["arxiv"])
     run_sage_parity(g, 2, 128, [10, 25], 1000, synth.sage_dims(128, 2, 40), [32], f_bp=2500, gamma=0.995,
                     delta=32, inst_every=8)
+
+
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_fused_and_split_aggregation(cfg1, split, monkeypatch):
+    """Both forward variants: neighbour means inside the GEMM kernel (MGNN_SAGE_SPLIT=0) and
+    k_mean + TMA-fed GEMM (default)."""
+    monkeypatch.setenv("MGNN_SAGE_SPLIT", split)
+    run_sage_parity(cfg1, 2, 64, [10, 25], 256, synth.sage_dims(64, 2, 16), [3])
+    g = synth.random_graph(900, 0.006, seed=21)
+    run_sage_parity(g, 2, 150, [4, 6], 64, [150, 40, 7], [2])
