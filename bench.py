@@ -612,8 +612,9 @@ def main():
                 "model": f"GraphSAGE-mean {dims} (random init), forward of every minibatch",
                 "consumer_ms_per_step": fwd_ms, "consumer_launches_per_step": L_,
                 "pipeline": "3 streams: sample(w+2) | gather+score(w+1) | forward(w), timed as one span",
-                "kernel": "k_mean (neighbour means, all SMs) + k_sage_layer: TMA self rows / means / weights "
-                          "-> tcgen05.mma kind::tf32 (TMEM accumulator) -> bias/ReLU epilogue",
+                "kernel": "k_mean (neighbour means, all SMs) + k_sage_gemm (warp-specialised: TMA ring of self "
+                          "rows / means / weights -> tcgen05.mma kind::tf32 into 2 TMEM accumulators -> "
+                          "bias/ReLU epilogue warps)",
                 "tflops": flops / (fwd_ms / 1e3) / 1e12 if fwd_ms > 0 else None,
                 "agg_gbs": agg_bytes / (fwd_ms / 1e3) / 1e9 if fwd_ms > 0 else None,
                 "dtype": "tf32 x tf32 -> f32"},

@@ -162,10 +162,14 @@ struct SageLayerArgs {
     float* mean_out;           // optional [M][mean_rows][mean_pitch]: neighbour means (training)
     int64_t mean_rows, mean_pitch;
     int32_t mean_in;           // 1: the means are already in mean_out (k_mean); TMA them, no aggregation
+    int32_t b_resident;        // k_sage_gemm: all weight chunks stay in shared memory (set by the launcher)
 };
 bool sage_encode_map(void* map_out, const float* base, int64_t rows, int64_t cols, int64_t pitch, int box_rows);
 bool launch_sage_layer(const void* map_in, const void* map_w, const void* map_mean, const SageLayerArgs& a,
                        cudaStream_t s);
+// out = act([H_in | mean] Wcat^T + b) with the means precomputed (warp-specialised, TMA + tcgen05)
+bool launch_sage_gemm(const void* map_in, const void* map_w, const void* map_mean, const SageLayerArgs& a,
+                      cudaStream_t s);
 // neighbour means of a layer's dst rows into mean_out (warp per row, all SMs): the training step's
 // forward, whose per-step instance count is too small for the fused aggregation to fill the GPU
 void launch_mean(const SageLayerArgs& a, cudaStream_t s);

@@ -438,4 +438,221 @@ bool launch_sage_layer(const void* map_in, const void* map_w, const void* map_me
     return true;
 }
 
+
+// ------------------------------------------------------------------ TMA-fed warp-specialised GEMM
+// out = act([H_in | mean] Wcat^T + b) when the neighbour means are already in HBM (k_mean): the
+// canonical Blackwell pipeline.  Warp 0 streams (A chunk, weight chunk) pairs through an
+// mbarrier ring with TMA; warp 1 issues tcgen05.mma (M = 128, N = npad, K = 8) into one of two
+// TMEM accumulators; warps 2-17 drain the other accumulator (bias, ReLU, stores) meanwhile, so
+// loads, MMAs and the epilogue of consecutive tiles overlap.  One CTA per SM, persistent.
+constexpr int kGEpiWarps = 16;            // epilogue warps (4 per TMEM lane quarter)
+constexpr int kGThreads = (2 + kGEpiWarps) * 32;   // + TMA warp + MMA warp
+constexpr int kGMaxStages = 8;
+
+__global__ void __launch_bounds__(kGThreads, 1)
+    k_sage_gemm(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_w,
+                const __grid_constant__ CUtensorMap map_mean, SageLayerArgs a) {
+    extern __shared__ __align__(1024) unsigned char dsm[];
+    __shared__ __align__(8) uint64_t full[kGMaxStages], empty[kGMaxStages], tfull[2], tempty[2];
+    __shared__ uint32_t tmem_sh;
+    unsigned char* base = dsm + ((1024u - (su32(dsm) & 1023u)) & 1023u);
+    const uint32_t b_bytes = (uint32_t)a.npad * 128u;
+    const int nch = (a.k_in + kChunkCols - 1) / kChunkCols;   // 32-column chunks per operand half
+    const int nk = 2 * nch;
+    // weights resident in shared memory for the whole kernel when they fit (a.b_resident), else
+    // streamed with each A chunk
+    const uint32_t stage_bytes = kChunkBytesA + (a.b_resident ? 0u : b_bytes);
+    unsigned char* b_res = base + (size_t)a.stages * stage_bytes;
+    int32_t* tile_pref = (int32_t*)(b_res + (a.b_resident ? (size_t)nk * b_bytes : 0));
+    __shared__ __align__(8) uint64_t bfull;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < a.stages; ++i) {
+            mb_init(&full[i], 1);
+            mb_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mb_init(&tfull[i], 1);
+            mb_init(&tempty[i], kGEpiWarps);   // one arrive per epilogue warp
+        }
+        mb_init(&bfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_in) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_mean) : "memory");
+    }
+    if (warp == 1) tmem_alloc(&tmem_sh, a.tmem_cols);    // 2 accumulators of npad columns
+    pdl_enter();
+    if (warp == 2) {
+        int32_t run = 0;
+        if (lane == 0) tile_pref[0] = 0;
+        for (int m0 = 0; m0 < a.n_inst; m0 += 32) {
+            const int m = m0 + lane;
+            int32_t t = 0;
+            if (m < a.n_inst)
+                t = (int32_t)((a.hop_size[(int64_t)(a.inst0 + m * a.inst_step) * (kMaxLayers + 1) + a.hop] + kTileM - 1) /
+                              kTileM);
+            int32_t x = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(kFull, x, o);
+                if (lane >= o) x += y;
+            }
+            if (m < a.n_inst) tile_pref[m + 1] = run + x;
+            run += __shfl_sync(kFull, x, 31);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_sh;
+    const int n_tiles = tile_pref[a.n_inst];
+    auto locate = [&](int tile, int& m, int64_t& row0) {
+        int lo = 0, hi = a.n_inst;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (tile_pref[mid] <= tile) lo = mid; else hi = mid;
+        }
+        m = a.inst0 + lo * a.inst_step;
+        row0 = (int64_t)(tile - tile_pref[lo]) * kTileM;
+    };
+    if (warp == 0) {
+        if (lane == 0) {                         // TMA producer
+            if (a.b_resident && blockIdx.x < n_tiles) {
+                mb_expect_tx(&bfull, (uint32_t)nk * b_bytes);
+                for (int kc = 0; kc < nk; ++kc)
+                    tma_load_2d(b_res + (size_t)kc * b_bytes, &map_w,
+                                kc < nch ? kc * kChunkCols : a.kp + (kc - nch) * kChunkCols, 0, &bfull);
+            }
+            uint32_t g = 0;
+            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+                int m;
+                int64_t row0;
+                locate(tile, m, row0);
+                for (int kc = 0; kc < nk; ++kc, ++g) {
+                    const uint32_t st = g % a.stages;
+                    if (g >= (uint32_t)a.stages) mb_wait(&empty[st], ((g / a.stages) - 1) & 1);
+                    unsigned char* sa = base + st * stage_bytes;
+                    mb_expect_tx(&full[st], stage_bytes);
+                    if (kc < nch)
+                        tma_load_2d(sa, &map_in, kc * kChunkCols, (int)((int64_t)m * a.in_rows + row0), &full[st]);
+                    else
+                        tma_load_2d(sa, &map_mean, (kc - nch) * kChunkCols, (int)((int64_t)m * a.mean_rows + row0),
+                                    &full[st]);
+                    if (!a.b_resident) {
+                        const int wcol = kc < nch ? kc * kChunkCols : a.kp + (kc - nch) * kChunkCols;
+                        tma_load_2d(sa + kChunkBytesA, &map_w, wcol, 0, &full[st]);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {                         // MMA issuer
+            if (a.b_resident && blockIdx.x < n_tiles) mb_wait(&bfull, 0);
+            uint32_t g = 0, t = 0;
+            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+                const uint32_t acc = t & 1;
+                if (t >= 2) mb_wait(&tempty[acc], ((t >> 1) - 1) & 1);   // epilogue drained this accumulator
+                tc_fence_after();
+                const uint32_t d = tmem + acc * (uint32_t)a.npad;
+                for (int kc = 0; kc < nk; ++kc, ++g) {
+                    const uint32_t st = g % a.stages;
+                    mb_wait(&full[st], (g / a.stages) & 1);
+                    tc_fence_after();
+                    const uint32_t a0 = su32(base + st * stage_bytes);
+                    const uint32_t b0 = a.b_resident ? su32(b_res + (size_t)kc * b_bytes) : a0 + kChunkBytesA;
+#pragma unroll
+                    for (int k = 0; k < kChunkCols / 8; ++k)
+                        mma_tf32(d, sdesc(a0 + k * 32), sdesc(b0 + k * 32), a.idesc, (kc > 0 || k > 0) ? 1u : 0u);
+                    mma_commit(&empty[st]);
+                }
+                mma_commit(&tfull[acc]);
+            }
+        }
+    } else {                                     // epilogue warps: lane quarter warp % 4, column groups
+        const int q = warp & 3;
+        const int sub = (warp - 2) >> 2;         // 8-column groups sub, sub + nsub, ...
+        constexpr int nsub = kGEpiWarps / 4;
+        uint32_t t = 0;
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+            int m;
+            int64_t row0;
+            locate(tile, m, row0);
+            const int64_t n_dst = a.hop_size[(int64_t)m * (kMaxLayers + 1) + a.hop];
+            const uint32_t acc = t & 1;
+            mb_wait(&tfull[acc], (t >> 1) & 1);
+            tc_fence_after();
+            const int r = q * 32 + lane;
+            const int64_t row = row0 + r;
+            float* out = a.h_out + ((int64_t)m * a.out_rows + row) * a.out_pitch;
+            const bool vec = (a.out_pitch & 3) == 0;
+            for (int c = sub * 8; c < a.npad; c += nsub * 8) {
+                float v[8];
+                tmem_ld8(tmem + acc * (uint32_t)a.npad + ((uint32_t)(q * 32) << 16) + (uint32_t)c, v);
+                const float4 b0 = ldg4(a.bias + c), b1 = ldg4(a.bias + c + 4);
+                const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float x = __fadd_rn(v[i], bb[i]);
+                    v[i] = a.relu ? fmaxf(x, 0.0f) : x;
+                }
+                if (row < n_dst) {
+                    if (vec && c + 8 <= a.n_out) {
+                        reinterpret_cast<float4*>(out + c)[0] = make_float4(v[0], v[1], v[2], v[3]);
+                        reinterpret_cast<float4*>(out + c)[1] = make_float4(v[4], v[5], v[6], v[7]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+                            if (c + i < a.n_out) out[c + i] = v[i];
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[acc])) : "memory");
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc(tmem, a.tmem_cols);
+}
+
+bool launch_sage_gemm(const void* map_in, const void* map_w, const void* map_mean, const SageLayerArgs& args_in,
+                      cudaStream_t s) {
+    static bool attr = false;
+    int optin = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_sage_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024) != cudaSuccess)
+            return false;
+        attr = true;
+    }
+    SageLayerArgs a = args_in;
+    if (a.n_inst > kMaxInst || a.npad % 16 || a.npad < 16 || a.npad > 256 || !map_mean) return false;
+    const int64_t nk = 2 * (int64_t)((a.k_in + kChunkCols - 1) / kChunkCols);
+    const int64_t w_all = nk * a.npad * 128;                  // every weight chunk of the layer
+    const int64_t fixed = 1024 + (int64_t)((a.n_inst + 4) & ~3) * 4;
+    const int64_t room = (int64_t)optin - 2048 - fixed;
+    // keep the weights resident unless that leaves fewer A chunks in flight than streaming them
+    // (A in flight is what the kernel's throughput follows: measured 132 vs 150 us at 7 vs 6 stages)
+    const int64_t st_res = w_all + 2 * (int64_t)kChunkBytesA <= room
+                               ? std::min<int64_t>(kGMaxStages, (room - w_all) / kChunkBytesA) : 0;
+    const int64_t st_str = std::min<int64_t>(kGMaxStages, room / (kChunkBytesA + (int64_t)a.npad * 128));
+    a.b_resident = st_res >= st_str ? 1 : 0;
+    const int64_t stage = kChunkBytesA + (a.b_resident ? 0 : (int64_t)a.npad * 128);
+    const int64_t ring = room - (a.b_resident ? w_all : 0);
+    a.stages = (int)std::max<int64_t>(2, std::min<int64_t>(kGMaxStages, ring / stage));
+    const size_t smem = (size_t)fixed + (size_t)a.stages * stage + (a.b_resident ? (size_t)w_all : 0);
+    a.tmem_cols = 32;
+    while ((int)a.tmem_cols < 2 * a.npad) a.tmem_cols <<= 1;
+    a.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(a.npad >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
+    CUtensorMap mi = *(const CUtensorMap*)map_in, mw = *(const CUtensorMap*)map_w, mm = *(const CUtensorMap*)map_mean;
+    launch_k(k_sage_gemm, dim3(sms), dim3(kGThreads), smem, s, mi, mw, mm, a);
+    count_launches(1, __func__, s);
+    return true;
+}
+
 }  // namespace mgnn
