@@ -413,7 +413,11 @@ __global__ void __launch_bounds__(kT) k_scatter(DgradArgs a) {
 }
 
 // ------------------------------------------------------------------ neighbour means (training forward)
-// warp per dst row: lanes cover 128 columns as float4, 4 neighbour rows in flight
+// warp per dst row: lanes cover 128 columns as float4, kMeanUnroll neighbour rows in flight
+#ifndef MGNN_MEAN_UNROLL
+#define MGNN_MEAN_UNROLL 4
+#endif
+constexpr int kMeanUnroll = MGNN_MEAN_UNROLL;
 __global__ void __launch_bounds__(kT) k_mean(SageLayerArgs a) {
     pdl_enter();
     const int m = inst_of(blockIdx.y, a.inst0, a.inst_step);
@@ -430,12 +434,13 @@ __global__ void __launch_bounds__(kT) k_mean(SageLayerArgs a) {
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
             if (c < a.k_in) {
                 int64_t e = e0;
-                for (; e + 4 <= e1; e += 4) {
-                    float4 v[4];
+                for (; e + kMeanUnroll <= e1; e += kMeanUnroll) {
+                    float4 v[kMeanUnroll];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) v[j] = __ldg(reinterpret_cast<const float4*>(h + (int64_t)nb[e + j] * a.in_pitch + c));
+                    for (int j = 0; j < kMeanUnroll; ++j)
+                        v[j] = __ldg(reinterpret_cast<const float4*>(h + (int64_t)nb[e + j] * a.in_pitch + c));
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
+                    for (int j = 0; j < kMeanUnroll; ++j) {
                         acc.x = __fadd_rn(acc.x, v[j].x);
                         acc.y = __fadd_rn(acc.y, v[j].y);
                         acc.z = __fadd_rn(acc.z, v[j].z);
