@@ -505,7 +505,9 @@ def main():
     # The WINDOW DDP steps of a slot are one CUDA graph (captured once per slot, replayed every
     # window): ~12 launches per step, all device-resident sizes, so the graph is static.
     graphs = {}
-    use_graph = [not args.no_train_graph]
+    # one rank: graph capture; N > 1 keeps eager launches (the step is GPU-bound either way, and a
+    # graph holding captured NCCL work hung the process teardown)
+    use_graph = [not args.no_train_graph and world == 1]
 
     def train_window(sl):
         if use_graph[0]:
@@ -640,6 +642,8 @@ def main():
                                     "sample": f"{n_mb} minibatches (steps 1..{n_mb // P} of all {P} partitions), "
                                               f"{el:.1f} s, single-threaded C oracle"}
         print(json.dumps(line), flush=True)
+    graphs.clear()
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()                 # peers read our feature tables until everyone is done
     ctx.close()
