@@ -161,6 +161,29 @@ class ClockSampler:
                 "reasons": [n for n, bit in self.REASONS if mask & bit], "samples": len(self.rows), "source": "nvml"}
 
 
+def peer_copy_gbs(src: int, dst: int):
+    """Achievable NVLink bandwidth: 256 MB copy from GPU src to GPU dst (CUDA events, best of 5)."""
+    import torch
+    if src == dst:
+        return None
+    try:
+        a = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{src}")
+        b = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dst}")
+        best = None
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            b.copy_(a, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize(src)
+            torch.cuda.synchronize(dst)
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        return (256 << 20) / (best / 1e3) / 1e9
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------- oracle timings (test infrastructure)
 def oracle_rate(parts, P, f_bp, gamma, delta, budget_s: float, min_steps: int = 8):
     """Oracle (oracle/orc.c, single thread) on the same workload: minibatches/s over a bounded sample."""
@@ -632,10 +655,17 @@ def main():
         }
         if world > 1:
             nv_bytes = peer_rows * CFG.feat_dim * 4
+            gbs = nv_bytes / (g_avg_ms / 1e3) / 1e9 if g_avg_ms > 0 else None
+            peer = peer_copy_gbs(local, (local + 1) % torch.cuda.device_count())
             line["nvlink"] = {"peer_rows_per_window": peer_rows, "bytes_per_window": nv_bytes,
-                              "gbs_during_gather": nv_bytes / (g_avg_ms / 1e3) / 1e9 if g_avg_ms > 0 else None,
+                              "gbs_during_gather": gbs,
+                              "peak_gbs": 900.0, "peak_source": "NVLink 5 nominal per direction per GPU",
+                              "frac": gbs / 900.0 if gbs else None,
+                              "achievable_peer_copy_gbs": peer,
+                              "frac_of_achievable": gbs / peer if (gbs and peer) else None,
                               "note": "miss + refill rows whose owner is on another GPU, read by peer loads "
-                                      "inside k_gather / k_swap_refill (last timed window)"}
+                                      "inside k_gather / k_swap_refill (last timed window); achievable = "
+                                      "256 MB device-to-device copy to the next GPU, best of 5"}
         if world == 1 and not args.no_cpu_baseline:
             rate, n_mb, el = oracle_rate(parts, P, f_bp, gamma, delta, args.cpu_budget)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
