@@ -57,3 +57,10 @@ def test_fused_and_split_aggregation(cfg1, split, monkeypatch):
     run_sage_parity(cfg1, 2, 64, [10, 25], 256, synth.sage_dims(64, 2, 16), [3])
     g = synth.random_graph(900, 0.006, seed=21)
     run_sage_parity(g, 2, 150, [4, 6], 64, [150, 40, 7], [2])
+
+
+def test_reddit_width_features():
+    """D = 602 (Reddit's width: pitch 604, ten 64-column panels / nineteen 32-column chunks, a ragged
+    last chunk), 41 classes, on a small graph."""
+    g = synth.random_graph(700, 0.01, seed=41)
+    run_sage_parity(g, 2, 602, [4, 8], 48, [602, 128, 41], [2])

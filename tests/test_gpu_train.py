@@ -23,3 +23,10 @@ def test_three_layers_wide_input():
     """D = 150 (two 128-column K panels in the weight gradient), 3 layers, 3 trainers."""
     g = synth.random_graph(2000, 0.005, seed=9)
     run_train_parity(g, 3, 150, [3, 4, 5], 48, [150, 48, 40, 10], 2)
+
+
+def test_reddit_width_training():
+    """Training with D = 602: the weight gradient's self/neighbour halves span five 128-column
+    N-tiles each (kp = 640), pitch 604 inputs, 41 classes."""
+    g = synth.random_graph(700, 0.01, seed=43)
+    run_train_parity(g, 2, 602, [4, 8], 48, [602, 128, 41], 2)
