@@ -206,6 +206,46 @@ def oracle_rate(parts, P, f_bp, gamma, delta, budget_s: float, min_steps: int = 
     return n_mb / el, n_mb, el
 
 
+def oracle_rate_threads(parts, P, f_bp, gamma, delta, budget_s: float):
+    """The same oracle with one host thread per partition (the C steps release the GIL; partitions
+    are independent between eviction rounds of their own buffers): SURVEY §8(d)'s P-thread rate."""
+    import threading as th
+    from oracle import oracle as O
+    W = O.World(parts, CFG.feat_dim, synth.FEAT_SEED)
+    alpha = O.alpha_default(gamma, delta)
+    for p in W.parts:
+        p.buffer_init(gamma, alpha, 1.0, delta, f_bp)
+    counts = [0] * len(W.parts)
+    t0 = time.perf_counter()
+
+    def run(i):
+        step = 1
+        while time.perf_counter() - t0 < budget_s or step <= 8:
+            W.parts[i].step(synth.RUN_SEED, step, CFG.fanouts, CFG.batch)
+            counts[i] += 1
+            step += 1
+
+    ts = [th.Thread(target=run, args=(i,)) for i in range(len(W.parts))]
+    for t_ in ts:
+        t_.start()
+    for t_ in ts:
+        t_.join()
+    el = time.perf_counter() - t0
+    n_thr = len(ts)
+    W.close()
+    return sum(counts) / el, n_thr
+
+
+def host_cpu():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -668,9 +708,12 @@ def main():
                                       "256 MB device-to-device copy to the next GPU, best of 5"}
         if world == 1 and not args.no_cpu_baseline:
             rate, n_mb, el = oracle_rate(parts, P, f_bp, gamma, delta, args.cpu_budget)
+            rate_p, n_thr = oracle_rate_threads(parts, P, f_bp, gamma, delta, min(args.cpu_budget, 6.0))
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
                                     "sample": f"{n_mb} minibatches (steps 1..{n_mb // P} of all {P} partitions), "
-                                              f"{el:.1f} s, single-threaded C oracle"}
+                                              f"{el:.1f} s, single-threaded C oracle",
+                                    "value_one_thread_per_partition": rate_p, "threads": n_thr,
+                                    "host_cpu": host_cpu(), "host_nproc": os.cpu_count()}
         print(json.dumps(line), flush=True)
     graphs.clear()
     torch.cuda.synchronize()
