@@ -1331,6 +1331,7 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
         wa.kp = S.kp[l];
         wa.npad = S.npad[l];
         wa.dw = S.grads + S.w_off[l];
+        wa.max_chunks = (int64_t)n_lp * ((S.out_rows[l] + 63) / 64);
         if (!launch_wgrad(wa, s)) return fail(ctx, MGNN_ECUDA, "train: wgrad launch configuration failed");
         if (l > 0) {
             ZeroRowsArgs za;

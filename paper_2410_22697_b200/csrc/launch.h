@@ -223,6 +223,7 @@ struct WgradArgs {             // dW[npad][2 kp] += dZ^T [H | mean] over the ste
     int32_t mean_cols;
     int32_t kp, npad;
     float* dw;                 // [npad][2 kp]
+    int64_t max_chunks;        // upper bound of the step's 64-row chunks (host hint for the K split)
     int32_t ksplit;            // CTAs per (M-tile, N-tile), set by the launcher
 };
 bool launch_wgrad(const WgradArgs& a, cudaStream_t s);
