@@ -65,6 +65,7 @@ def lib():
             "orc_buffer_state": (None, [P, P, P, P, P, P]),
             "orc_totals": (None, [P, P]),
             "orc_evict_and_replace": (I64, [I64, I64, P, P, P, P, P, P, F32, F32, P, P, P]),
+            "orc_set_expand_remote": (None, [P, I32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -192,6 +193,10 @@ class Part:
                                    float(np.float32(theta_r)), int(delta), int(f_bp))
         if rc != 0:
             raise ValueError("orc_buffer_init: invalid policy")
+
+    def set_expand_remote(self, on: bool) -> None:
+        """NEXT-1: sample non-local frontier nodes from their owner's CSR (see orc.h)."""
+        lib().orc_set_expand_remote(self._h, 1 if on else 0)
 
     def epoch_perm(self, run_seed: int, epoch: int, n_train: int) -> np.ndarray:
         out = np.zeros(n_train, np.int32)

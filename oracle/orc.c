@@ -128,6 +128,7 @@ struct orc_part {
     int8_t* cls;
     int64_t counts[ORC_C_N];
     int64_t totals[4];
+    int32_t expand_remote;  /* non-local frontier nodes sampled from their owner's CSR */
 };
 
 /* ---------------------------------------------------------------- helpers */
@@ -473,10 +474,15 @@ int orc_step(orc_part* p, uint64_t run_seed, uint64_t step, const int32_t* fanou
         off[0] = 0;
         for (int64_t f = 0; f < nFi; f++) {
             int32_t x = p->F[f];
-            if (x >= p->lo && x < p->hi) {            /* halo frontier nodes are leaves (R#1) */
-                int64_t row = x - p->lo, b0 = p->indptr[row], d = p->indptr[row + 1] - b0;
+            /* the CSR row of x: local rows; with expand_remote (NEXT-1, DistDGL's sampling through the
+               owner) also every other node, from the owning partition's rows */
+            const orc_part* src = NULL;
+            if (x >= p->lo && x < p->hi) src = p;     /* halo frontier nodes are leaves (R#1) */
+            else if (p->expand_remote) src = w->parts[owner_of(w, x)];
+            if (src) {
+                int64_t row = x - src->lo, b0 = src->indptr[row], d = src->indptr[row + 1] - b0;
                 if (d <= k) {                          /* d <= k: whole neighbourhood (R#3) */
-                    for (int64_t j = 0; j < d; j++) col[ne++] = p->cols[b0 + j];
+                    for (int64_t j = 0; j < d; j++) col[ne++] = src->cols[b0 + j];
                 } else {
                     uint32_t r[32];
                     int64_t pos[32];
@@ -487,7 +493,7 @@ int orc_step(orc_part* p, uint64_t run_seed, uint64_t step, const int32_t* fanou
                         r[j] = orc_range(o[0], (uint32_t)(d - k + j + 1));
                     }
                     orc_floyd(d, k, r, pos);
-                    for (int32_t j = 0; j < k; j++) col[ne++] = p->cols[b0 + pos[j]];
+                    for (int32_t j = 0; j < k; j++) col[ne++] = src->cols[b0 + pos[j]];
                 }
             }
             off[f + 1] = ne;
@@ -517,13 +523,18 @@ int orc_step(orc_part* p, uint64_t run_seed, uint64_t step, const int32_t* fanou
     free(p->cls);
     p->cls = malloc((size_t)(nF ? nF : 1));
     int64_t* miss_h = malloc(sizeof(int64_t) * (size_t)(nF ? nF : 1));
-    int64_t n_local = 0, n_hit = 0, n_miss = 0;
+    int64_t n_local = 0, n_hit = 0, n_miss = 0, n_far = 0;
     memset(p->hitflag, 0, (size_t)(p->cap ? p->cap : 1));
     for (int64_t f = 0; f < nF; f++) {
         int32_t u = p->F[f];
         if (u >= p->lo && u < p->hi) { p->cls[f] = 0; n_local++; continue; }
         int64_t h = bsearch_i32(p->halo, p->n_h, u);     /* binary search into sorted V_p^h */
-        if (h < 0) { free(miss_h); return -1; }          /* cannot happen: sampling is partition-local */
+        if (h < 0) {
+            if (!p->expand_remote) { free(miss_h); return -1; }   /* cannot happen: partition-local sampling */
+            p->cls[f] = 3;          /* a remote node outside V_p^h: a miss, fetched, never buffered or scored */
+            n_far++;
+            continue;
+        }
         int32_t s = p->slot_of[h];
         if (s >= 0) { p->cls[f] = 1; n_hit++; p->hitflag[s] = 1; }
         else { p->cls[f] = 2; miss_h[n_miss++] = h; }
@@ -568,21 +579,23 @@ int orc_step(orc_part* p, uint64_t run_seed, uint64_t step, const int32_t* fanou
 
     /* Alg.2 l.22 / l.18: B^h <- fetched features of Misses. */
     for (int64_t f = 0; f < nF; f++)
-        if (p->cls[f] == 2) kv_fetch(w, p->F[f], p->X + (size_t)f * (size_t)D);
+        if (p->cls[f] >= 2) kv_fetch(w, p->F[f], p->X + (size_t)f * (size_t)D);
     free(miss_h);
 
     p->counts[ORC_C_NODES] = nF;
     p->counts[ORC_C_LOCAL] = n_local;
     p->counts[ORC_C_HIT] = n_hit;
-    p->counts[ORC_C_MISS] = n_miss;
+    p->counts[ORC_C_MISS] = n_miss + n_far;
     p->counts[ORC_C_EVICTED] = k;
     p->counts[ORC_C_REFILLED] = k;
-    p->counts[ORC_C_ROWS_FETCHED] = n_miss + k;
+    p->counts[ORC_C_ROWS_FETCHED] = n_miss + n_far + k;
     p->totals[0] += n_hit;
-    p->totals[1] += n_miss;
+    p->totals[1] += n_miss + n_far;
     p->totals[2] += k;
     return 0;
 }
+
+void orc_set_expand_remote(orc_part* p, int32_t on) { p->expand_remote = on ? 1 : 0; }
 
 /* ---------------------------------------------------------------- getters */
 void orc_counts(const orc_part* p, int64_t* out) { memcpy(out, p->counts, sizeof(p->counts)); }

@@ -76,6 +76,13 @@ int64_t orc_evict_and_replace(int64_t cap, int64_t n_h, int32_t* node_of_slot, f
                               int32_t* slot_of, const int32_t* halo, const int32_t* deg_in, float alpha,
                               float theta_r, int32_t* evicted_out, int32_t* replaced_out, int32_t* slots_out);
 
+/* SURVEY §8(f) NEXT-1 (the alternative to reading R#1): with on != 0, every non-local frontier
+ * node is sampled too, from its owner's CSR row, with the same Philox counter (sampling trainer
+ * p, node, hop, slot, step) -- DistDGL's sampling through the owning server.  Sampled
+ * nodes outside V_p^l and V_p^h are misses (class 3): fetched from the owner, never buffered and
+ * never scored (S_A covers V_p^h only; the dense S_A of P:228 is not modelled). */
+void orc_set_expand_remote(orc_part* p, int32_t on);
+
 /* Results of the last orc_step (valid until the next one). */
 enum { ORC_C_NODES = 0, ORC_C_LOCAL, ORC_C_HIT, ORC_C_MISS, ORC_C_EVICTED, ORC_C_REFILLED,
        ORC_C_ROWS_FETCHED, ORC_C_N };

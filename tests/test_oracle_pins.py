@@ -523,3 +523,75 @@ def test_f0_all_misses_f1_all_hits(delta):
             assert c[want] == c["n_nodes"] - c["n_local"]
             assert c["n_evicted"] == 0
         _run_world(g, 2, [10, 25], 256, f_bp, 0.5, delta, 1.0, 2 * max(delta, 1), check=check)
+
+
+# ------------------------------------------------------------------ NEXT-1: remote expansion
+def test_remote_expansion_path_hand_trace():
+    """Path 0-1-2-3-4, partitions {0,1,2} | {3,4}, seed 2, full fanout, 2 hops.  Local reading
+    (R#1): the halo node 3 is a leaf -> F_2 = [2, 1, 3, 0].  Remote expansion: 3 is sampled from
+    partition 1's row {2, 4} -> F_2 = [2, 1, 3, 0, 4]; 4 is outside V_0^l and V_0^h = {3}: a
+    class-3 miss."""
+    g = synth.from_edges(5, [(0, 1), (1, 2), (2, 3), (3, 4)])
+    for remote, want_F, want_cls in ((False, [2, 1, 3, 0], [0, 0, 2, 0]), (True, [2, 1, 3, 0, 4], [0, 0, 2, 0, 3])):
+        W, _ = world_from(g, 2, bounds=np.array([0, 3, 5]))
+        p = W.parts[0]
+        p.buffer_init(0.9, 0.5, 1.0, 0, 0)
+        p.set_expand_remote(remote)
+        p.step(RUN_SEED, 1, [32, 32], 1, seeds=np.array([2], np.int32))
+        assert p.frontier().tolist() == want_F
+        assert p.classes().tolist() == want_cls
+        off, cols = p.hop_block(1)
+        assert cols[off[2]:off[3]].tolist() == ([2, 4] if remote else [])
+        c = p.counts()
+        assert c["n_local"] == 3 and c["n_hit"] == 0 and c["n_miss"] == (2 if remote else 1)
+        X = p.features()
+        for i, v in enumerate(want_F):
+            assert np.array_equal(X[i], O.feature_row(v, 4, FEAT_SEED))   # far rows fetched too
+        W.close()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_remote_expansion_invariants(seed):
+    """Every frontier node (local, halo or far) draws min(deg, k) distinct true neighbours from the
+    GLOBAL graph; hits + misses = non-local nodes; only halo nodes are tallied."""
+    g = synth.random_graph(24, 0.2, seed)
+    W, _ = world_from(g, 3)
+    for p in W.parts:
+        p.buffer_init(0.9, 0.5, 1.0, 3, 5000)
+        p.set_expand_remote(True)
+    p = W.parts[0]
+    lo, hi = 0, 8
+    halo = set(p.halo()[0].tolist())
+    fan = [2, 3]
+    for t in range(1, 10):
+        p.step(RUN_SEED, t, fan, 3)
+        sizes = p.hop_sizes()
+        F = p.frontier()
+        for i in range(2):
+            k = fan[1 - i]
+            off, cols = p.hop_block(i)
+            for f, x in enumerate(F[:sizes[i]].tolist()):
+                s = cols[off[f]:off[f + 1]].tolist()
+                nbr = g.cols[g.indptr[x]:g.indptr[x + 1]].tolist()
+                assert len(s) == min(len(nbr), k) and len(set(s)) == len(s) and set(s) <= set(nbr)
+        cls = p.classes().tolist()
+        for x, c in zip(F.tolist(), cls):
+            assert c == (0 if lo <= x < hi else (3 if x not in halo else c)) and c in (0, 1, 2, 3)
+        cn = p.counts()
+        assert cn["n_local"] + cn["n_hit"] + cn["n_miss"] == cn["n_nodes"]
+    W.close()
+
+
+def test_remote_expansion_single_partition_is_identity():
+    """P = 1: no remote nodes, so remote expansion changes nothing."""
+    g = synth.random_graph(30, 0.15, 5)
+    outs = []
+    for remote in (False, True):
+        W, _ = world_from(g, 1)
+        p = W.parts[0]
+        p.buffer_init(0.9, 0.5, 1.0, 0, 0)
+        p.set_expand_remote(remote)
+        p.step(RUN_SEED, 3, [3, 4], 5)
+        outs.append((p.frontier().tolist(), [p.hop_block(i)[1].tolist() for i in range(2)]))
+        W.close()
+    assert outs[0] == outs[1]
