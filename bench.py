@@ -42,6 +42,7 @@ UNIT = "minibatches/s"
 WINDOW = 32
 PARTS_PER_GPU = 2
 CFG = synth.CONFIGS["arxiv"]
+REMOTE = False                     # NEXT-1 remote expansion (--remote)
 
 # Measurement policy (f_p in basis points, gamma, Delta) by config and total partitions P: the
 # paper's GPU optima; theta_R = 1.
@@ -192,6 +193,7 @@ def oracle_rate(parts, P, f_bp, gamma, delta, budget_s: float, min_steps: int = 
     alpha = O.alpha_default(gamma, delta)
     for p in W.parts:
         p.buffer_init(gamma, alpha, 1.0, delta, f_bp)
+        p.set_expand_remote(REMOTE)
     t0 = time.perf_counter()
     n_mb, step = 0, 1
     while True:
@@ -215,6 +217,7 @@ def oracle_rate_threads(parts, P, f_bp, gamma, delta, budget_s: float):
     alpha = O.alpha_default(gamma, delta)
     for p in W.parts:
         p.buffer_init(gamma, alpha, 1.0, delta, f_bp)
+        p.set_expand_remote(REMOTE)
     counts = [0] * len(W.parts)
     t0 = time.perf_counter()
 
@@ -300,11 +303,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-train-graph", action="store_true", help="training steps as eager launches")
+    ap.add_argument("--remote", action="store_true",
+                    help="NEXT-1: sample non-local frontier nodes from their owner's CSR (one GPU only)")
     ap.add_argument("--config", default="arxiv", choices=sorted(LAYOUT),
                     help="workload (default: arxiv-shaped, BASELINE.json configs[1])")
     args = ap.parse_args()
-    global WINDOW
+    global WINDOW, REMOTE
     select_config(args.config)
+    REMOTE = args.remote
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":
@@ -343,6 +349,10 @@ def main():
         PL.exchange_tables(ctx)
     alpha = PL.alpha_default(gamma, delta)
     ctx.buffer_init(gamma, alpha, 1.0, delta, f_bp)
+    if args.remote:
+        if world > 1:
+            raise SystemExit("--remote needs every partition in one context (one GPU)")
+        ctx.expand_remote(True)
     ctx.sampler_config(CFG.fanouts, CFG.batch, synth.RUN_SEED, WINDOW)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -658,7 +668,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic", "config": workload(P),
+            "dtype": "f32", "data": "synthetic",
+            "config": dict(workload(P), **({"sampling": "remote expansion (NEXT-1)"} if args.remote else {})),
             "hit_rate": hits / max(1, hits + misses),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": E2E, "path": "two-stream pipeline: mgnn_sample(host pinned seeds, H2D) | "

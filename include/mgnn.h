@@ -141,6 +141,14 @@ MGNN_API mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* policy, m
 MGNN_API mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_layers, int32_t batch,
                                 uint64_t run_seed, int32_t max_window);
 
+/* SURVEY §8(f) NEXT-1, the alternative to reading R#1 (call before mgnn_sampler_config): with
+ * enable != 0 every non-local frontier node is sampled too, from its owner's CSR row, with the
+ * same Philox counter -- DistDGL's sampling through the owning server.  Sampled nodes
+ * outside V_p^l and V_p^h are misses: fetched from the owner's table, never buffered, never
+ * scored (S_A covers V_p^h; the dense S_A of P:228 is not modelled).  Ranks become global ids
+ * (window arenas sized by |V|).  Needs every partition hosted by this context (EINVAL otherwise). */
+MGNN_API mgnn_status mgnn_sampler_expand_remote(mgnn_ctx ctx, int32_t enable);
+
 /* NeighborSampler (Alg.2 l.1) for steps t0..t0+n_steps-1 of every hosted
  * partition into window slot `slot` (0 or 1).  Seeds are the step's slice of
  * the partition's epoch order (R#8) when seeds == NULL; otherwise seeds holds

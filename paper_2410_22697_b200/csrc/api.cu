@@ -67,6 +67,7 @@ struct Part {
     int32_t perm_slots = 0;
     int64_t* indptr = nullptr;
     int32_t* cols_rank = nullptr;
+    int32_t* halo_map = nullptr;         // NEXT-1: [n_global] halo index or -1
     int32_t* halo = nullptr;
     int32_t* deg_in = nullptr;
     int32_t* train = nullptr;
@@ -148,6 +149,10 @@ struct mgnn_ctx_s {
     size_t sort_scr_bytes = 0;
     void* perm_scr = nullptr;            // radix sort scratch of epoch orders (sampling stream), so
     size_t perm_scr_bytes = 0;           // mgnn_sample may run concurrently with gather/score
+    // NEXT-1 remote expansion: global CSR over every partition (all hosted by this context)
+    bool remote = false;
+    int64_t* g_indptr = nullptr;
+    int32_t* g_cols = nullptr;
     // sampler
     bool configured = false;
     int32_t L = 0, batch = 0, max_window = 0;
@@ -278,6 +283,7 @@ void fill_partdev(const mgnn_ctx_s* c, const Part& p, PartDev* d) {
     d->hitmask = p.hitmask;
     d->rank_deg = p.rank_deg;
     d->perm = p.perm;
+    d->halo_map = p.halo_map;
     (void)c;
 }
 
@@ -399,6 +405,10 @@ WinDev win_dev(mgnn_ctx ctx, Win& w) {
     d.parts = ctx->d_parts;
     d.err = ctx->d_err;
     d.gathered_rows = ctx->d_gathered;
+    d.remote = ctx->remote ? 1 : 0;
+    d.n_global = ctx->n_global;
+    d.g_indptr = ctx->g_indptr;
+    d.g_cols = ctx->g_cols;
     return d;
 }
 
@@ -487,6 +497,9 @@ void mgnn_destroy(mgnn_ctx ctx) {
     if (ctx->perm_scr) cudaFree(ctx->perm_scr);
     dfree(ctx->d_permsegs);
     dfree(ctx->d_perm_n);
+    dfree(ctx->g_indptr);
+    dfree(ctx->g_cols);
+    for (auto& p : ctx->parts) dfree(p.halo_map);
     delete ctx;
 }
 
@@ -751,6 +764,43 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
 }
 
 // ------------------------------------------------------------------ sampler configuration
+// ------------------------------------------------------------------ NEXT-1: remote expansion
+mgnn_status mgnn_sampler_expand_remote(mgnn_ctx ctx, int32_t enable) {
+    GUARD();
+    if (ctx->configured) return fail(ctx, MGNN_ESTATE, "expand_remote must precede sampler_config");
+    if (!enable) {
+        ctx->remote = false;
+        return MGNN_OK;
+    }
+    if ((int32_t)ctx->parts.size() != ctx->P)
+        return fail(ctx, MGNN_EINVAL, "remote expansion needs every partition hosted by this context");
+    CK(cudaDeviceSynchronize());
+    if (!ctx->g_indptr) {
+        int64_t nnz = 0;
+        for (auto& p : ctx->parts) nnz += p.nnz;
+        CK(dalloc(&ctx->g_indptr, ctx->n_global + 1));
+        CK(dalloc(&ctx->g_cols, nnz));
+        mgnn_status st = upload_parts(ctx);
+        if (st) return st;
+        int64_t base = 0;
+        for (int32_t q = 0; q < ctx->P; ++q) {          // partitions in id order = global row order
+            const int lp = ctx->lp_of[q];
+            Part& p = ctx->parts[lp];
+            launch_global_csr(ctx->d_parts + lp, p.indptr, p.n_local, p.lo, p.nnz, base, ctx->g_indptr, ctx->g_cols, 0);
+            base += p.nnz;
+        }
+        for (auto& p : ctx->parts) {
+            CK(dalloc(&p.halo_map, ctx->n_global));
+            CK(cudaMemset(p.halo_map, 0xFF, ctx->n_global * sizeof(int32_t)));
+            launch_halo_index(p.halo, p.n_h, p.halo_map, 0);
+        }
+        CKL();
+        CK(cudaDeviceSynchronize());
+    }
+    ctx->remote = true;
+    return upload_parts(ctx);
+}
+
 mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_layers, int32_t batch,
                                 uint64_t run_seed, int32_t max_window) {
     GUARD();
@@ -774,6 +824,7 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
     }
     ctx->vp_max = 1;
     for (auto& p : ctx->parts) ctx->vp_max = std::max(ctx->vp_max, p.n_local + p.n_h);
+    if (ctx->remote) ctx->vp_max = std::max<int64_t>(1, ctx->n_global);   // ranks are global ids (NEXT-1)
     ctx->bm_words = (ctx->vp_max + 31) / 32;
     const int64_t big = (int64_t)1 << 40;
     ctx->fcap[0] = std::min<int64_t>(batch, ctx->vp_max);

@@ -80,6 +80,7 @@ struct PartDev {
     unsigned long long* hitmask;  // [cap] bit w = hit at window step w
     int32_t* rank_deg;         // [n_h] position in the (deg_in desc, id asc) order (replacement tie-break)
     int32_t* perm;             // [perm_slots][n_train] epoch orders
+    const int32_t* halo_map;   // [n_global] halo index or -1 (remote expansion only)
 };
 
 // Global (graph-wide) read-only view: every partition's table (local or peer-mapped).

@@ -31,6 +31,41 @@ __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpre
 __device__ __forceinline__ void stcs4(float* p, float4 v) { __stcs(reinterpret_cast<float4*>(p), v); }
 
 // WIDE: rows of >= 32 float4 (D >= 128, one or more 16-B chunks per lane); else 32/q rows per warp step.
+// Alg.2 l.2-5 for one frontier entry r: local row, buffer hit (hit recorded for the decay) or
+// miss (S_A += 1, row from the owner's table -- over NVLink when it lives on another GPU).
+// Returns the class 0 local, 1 hit, 2 miss, 4 miss from a peer GPU; sets the row and global id.
+// Remote expansion (NEXT-1): ranks are global ids; nodes outside V_p^h are misses, not scored.
+__device__ __forceinline__ int classify(const WinDev& W, const WorldDev& G, const PartDev& pd, int64_t r,
+                                        unsigned long long wbit, const float*& src, int32_t& gid) {
+    const int pitch = W.pitch;
+    const int64_t rank_lo = W.remote ? pd.lo : pd.h_below;
+    if (r >= rank_lo && r < rank_lo + pd.n_local) {
+        gid = (int32_t)(pd.lo + (r - rank_lo));
+        src = pd.table + (r - rank_lo) * pitch;
+        return 0;
+    }
+    int64_t h;
+    if (W.remote) {
+        gid = (int32_t)r;
+        h = pd.halo_map[r];
+    } else {
+        h = r < pd.h_below ? r : r - pd.n_local;
+        gid = pd.halo_ids[h];
+    }
+    if (h >= 0) {
+        const int32_t s = pd.slot_of[h];
+        if (s >= 0) {
+            src = pd.rows + (int64_t)s * pitch;
+            atomicOr(&pd.hitmask[s], wbit);
+            return 1;
+        }
+        atomicAdd(&pd.sa[h], 1.0f);
+    }
+    const int qo = owner_of(G.bounds, G.n_parts, gid);
+    src = G.tables[qo] + ((int64_t)gid - G.bounds[qo]) * pitch;
+    return G.on_peer[qo] ? 4 : 2;
+}
+
 template <bool WIDE>
 __global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
     pdl_enter();
@@ -47,7 +82,6 @@ __global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
     const int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
     int32_t* fgid = W.fr_gid + (int64_t)m * W.ucap;
     float* X = W.X + (int64_t)m * W.ucap * pitch;
-    const int64_t h_below = pd.h_below, n_local = pd.n_local, lo = pd.lo;
     const unsigned long long wbit = 1ull << w;
     unsigned n_loc = 0, n_hit = 0, n_miss = 0, n_peer = 0;
     const int64_t stride = (int64_t)gridDim.x * kGWarps * 32;
@@ -58,27 +92,8 @@ __global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
         const float* src = nullptr;
         int cls = 3;
         if (valid) {
-            const int64_t r = fr[f];
             int32_t gid;
-            if (r >= h_below && r < h_below + n_local) {
-                gid = (int32_t)(lo + (r - h_below));
-                src = pd.table + (r - h_below) * pitch;
-                cls = 0;
-            } else {
-                const int64_t h = r < h_below ? r : r - n_local;
-                gid = pd.halo_ids[h];
-                const int32_t s = pd.slot_of[h];
-                if (s >= 0) {
-                    src = pd.rows + (int64_t)s * pitch;
-                    atomicOr(&pd.hitmask[s], wbit);
-                    cls = 1;
-                } else {
-                    const int qo = owner_of(G.bounds, G.n_parts, gid);
-                    src = G.tables[qo] + ((int64_t)gid - G.bounds[qo]) * pitch;
-                    atomicAdd(&pd.sa[h], 1.0f);
-                    cls = G.on_peer[qo] ? 4 : 2;
-                }
-            }
+            cls = classify(W, G, pd, fr[f], wbit, src, gid);
             fgid[f] = gid;
         }
         n_loc += __popc(__ballot_sync(kFull, cls == 0));
@@ -215,7 +230,6 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
     int32_t* fgid = W.fr_gid + (int64_t)m * W.ucap;
     float* X = W.X + (int64_t)m * W.ucap * pitch;
     unsigned char* stage[2] = {tsm + (size_t)warp * 2 * stage_bytes, tsm + (size_t)warp * 2 * stage_bytes + stage_bytes};
-    const int64_t h_below = pd.h_below, n_local = pd.n_local, lo = pd.lo;
     const unsigned long long wbit = 1ull << w;
     unsigned n_loc = 0, n_hit = 0, n_miss = 0, n_peer = 0;
     const int64_t stride = (int64_t)gridDim.x * kTWarps * R;
@@ -227,27 +241,8 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
         const float* src = nullptr;
         int cls = 3;
         if (valid) {
-            const int64_t r = fr[f];
             int32_t gid;
-            if (r >= h_below && r < h_below + n_local) {
-                gid = (int32_t)(lo + (r - h_below));
-                src = pd.table + (r - h_below) * pitch;
-                cls = 0;
-            } else {
-                const int64_t h = r < h_below ? r : r - n_local;
-                gid = pd.halo_ids[h];
-                const int32_t s = pd.slot_of[h];
-                if (s >= 0) {
-                    src = pd.rows + (int64_t)s * pitch;
-                    atomicOr(&pd.hitmask[s], wbit);
-                    cls = 1;
-                } else {
-                    const int qo = owner_of(G.bounds, G.n_parts, gid);
-                    src = G.tables[qo] + ((int64_t)gid - G.bounds[qo]) * pitch;
-                    atomicAdd(&pd.sa[h], 1.0f);
-                    cls = G.on_peer[qo] ? 4 : 2;
-                }
-            }
+            cls = classify(W, G, pd, fr[f], wbit, src, gid);
             fgid[f] = gid;
         }
         n_loc += __popc(__ballot_sync(kFull, cls == 0));

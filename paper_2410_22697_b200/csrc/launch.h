@@ -46,6 +46,12 @@ struct WinDev {
     const PartDev* parts;                // [n_parts_local]
     int32_t* err;                        // device error word
     long long* gathered_rows;            // profiling counter
+    // NEXT-1 remote expansion: ranks are global ids; every frontier node is sampled from the
+    // global CSR (all partitions hosted by this context)
+    int32_t remote;
+    int64_t n_global;
+    const int64_t* g_indptr;             // [n_global+1]
+    const int32_t* g_cols;               // [nnz] global ids
 };
 
 // Segment of a radix sort (device array of these).
@@ -270,5 +276,7 @@ void launch_deg_rank(const int32_t* cols, int64_t nnz, int64_t lo, int64_t n_loc
                      const int32_t* gmap, int32_t* deg_in, int32_t* cols_rank, cudaStream_t s);
 void launch_features(float* table, int64_t lo, int64_t n_rows, int32_t dim, int32_t pitch, uint64_t feat_seed,
                      cudaStream_t s);
+void launch_global_csr(const PartDev* pd_dev, const int64_t* indptr, int64_t n_local, int64_t lo, int64_t nnz,
+                       int64_t base, int64_t* g_indptr, int32_t* g_cols, cudaStream_t s);
 
 }  // namespace mgnn

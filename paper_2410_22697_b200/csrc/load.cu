@@ -102,6 +102,26 @@ void launch_halo_index(const int32_t* halo, int64_t n_h, int32_t* gmap, cudaStre
     count_launches(1, __func__, s);
 }
 
+// NEXT-1 remote expansion: the global CSR in global ids, assembled from the hosted partitions
+// (rows of partition p at [lo_p, hi_p), its edges at base_p = sum of the earlier partitions' nnz).
+__global__ void k_gcsr_rows(const int64_t* __restrict__ indptr, int64_t n_local, int64_t lo, int64_t base,
+                            int64_t* __restrict__ g_indptr) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= n_local; r += (int64_t)gridDim.x * blockDim.x)
+        g_indptr[lo + r] = base + indptr[r];
+}
+__global__ void k_gcsr_cols(const PartDev* __restrict__ pdp, int64_t nnz, int64_t base, int32_t* __restrict__ g_cols) {
+    const PartDev& pd = *pdp;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+        g_cols[base + e] = rank_to_gid(pd, pd.cols_rank[e]);
+}
+
+void launch_global_csr(const PartDev* pd_dev, const int64_t* indptr, int64_t n_local, int64_t lo, int64_t nnz,
+                       int64_t base, int64_t* g_indptr, int32_t* g_cols, cudaStream_t s) {
+    k_gcsr_rows<<<lblocks(n_local + 1), kLThreads, 0, s>>>(indptr, n_local, lo, base, g_indptr);
+    if (nnz > 0) k_gcsr_cols<<<lblocks(nnz), kLThreads, 0, s>>>(pd_dev, nnz, base, g_cols);
+    count_launches(2, __func__, s);
+}
+
 __global__ void k_deg_rank(const int32_t* __restrict__ cols, int64_t nnz, int64_t lo, int64_t n_local, int64_t h_below,
                            const int32_t* __restrict__ gmap, int32_t* __restrict__ deg_in,
                            int32_t* __restrict__ cols_rank) {

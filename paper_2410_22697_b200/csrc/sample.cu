@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
             atomicOr(W.err, 1);
             row = 0;
         }
-        const int32_t r = (int32_t)(pd.h_below + row);
+        const int32_t r = (int32_t)((W.remote ? pd.lo : pd.h_below) + row);   // rank (= global id when remote)
         fr[j] = r;
         W.fr_gid[(int64_t)m * W.ucap + j] = (int32_t)gid;   // F_0 readable right after sampling
         pos[r] = (int32_t)j;
@@ -133,12 +133,19 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
         const bool mine = threadIdx.x < T && f < nF;
         int64_t row = -1, b0 = 0, d = 0;
         if (mine) {
-            row = (int64_t)W.fr_rank[(int64_t)m * W.ucap + f] - h_below;
-            if (row >= 0 && row < n_local) {               // halo frontier nodes are leaves (R#1)
-                b0 = pd.indptr[row];
-                d = pd.indptr[row + 1] - b0;
+            const int64_t r = W.fr_rank[(int64_t)m * W.ucap + f];
+            if (W.remote) {                                // NEXT-1: every node, from the global CSR
+                row = r - lo;                              // (rank = global id; lo + row = id)
+                b0 = W.g_indptr[r];
+                d = W.g_indptr[r + 1] - b0;
             } else {
-                row = -1;
+                row = r - h_below;
+                if (row >= 0 && row < n_local) {           // halo frontier nodes are leaves (R#1)
+                    b0 = pd.indptr[row];
+                    d = pd.indptr[row + 1] - b0;
+                } else {
+                    row = -1;
+                }
             }
         }
         const int cnt = (int)(d < k ? d : k);              // |sample| = min(deg, k) (R#3)
@@ -197,11 +204,12 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
         int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop] + o_tile;
         const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
         uint32_t* nb = W.nb + ((int64_t)m * W.L + hop) * W.bm_words;
-        const int32_t* __restrict__ crank = pd.cols_rank;
+        const int32_t* __restrict__ crank = W.remote ? W.g_cols : pd.cols_rank;
     #pragma unroll 4
         for (int e = threadIdx.x; e < (int)agg; e += kThreads) {
             const int32_t c = crank[sidx[e]];
-            MGNN_CHECK(o_tile + e < W.col_stride[hop] && c < pd.vp, "cols o=%lld c=%d", o_tile + e, c);
+            MGNN_CHECK(o_tile + e < W.col_stride[hop] && c < (W.remote ? W.n_global : pd.vp), "cols o=%lld c=%d",
+                       o_tile + e, c);
             cols[e] = c;
             const uint32_t bit = 1u << (c & 31);
             if (!(fb[c >> 5] & bit)) atomicOr(&nb[c >> 5], bit);
@@ -218,7 +226,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
     __shared__ long long prefix_sh;
     const int m = blockIdx.y;
     const PartDev& pd = W.parts[m / W.n_steps];
-    const int64_t nwords = (pd.vp + 31) >> 5;
+    const int64_t nwords = ((W.remote ? W.n_global : pd.vp) + 31) >> 5;   // rank space
     const int64_t ntiles = (nwords + kWordTile - 1) / kWordTile;
     const int tile = claim_tile(sc.tilectr + m, &tslot);
     if (tile >= ntiles) return;
@@ -247,7 +255,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
         const int bi = __ffs(b) - 1;
         b &= b - 1;
         const int32_t r = (int32_t)(wd * 32 + bi);
-        MGNN_CHECK(pos < W.ucap && r < pd.vp, "compact pos=%lld r=%d", (long long)pos, r);
+        MGNN_CHECK(pos < W.ucap && r < (W.remote ? W.n_global : pd.vp), "compact pos=%lld r=%d", (long long)pos, r);
         fr[pos] = r;
         ++pos;
     }

@@ -106,6 +106,10 @@ class Context:
         self.delta = delta
         self._chk("mgnn_buffer_init", self.L.mgnn_buffer_init(self._h, C.byref(pol), _stream(stream)))
 
+    def expand_remote(self, enable: bool = True):
+        """NEXT-1: sample non-local frontier nodes from their owner's CSR (before sampler_config)."""
+        self._chk("mgnn_sampler_expand_remote", self.L.mgnn_sampler_expand_remote(self._h, 1 if enable else 0))
+
     def sampler_config(self, fanouts: Sequence[int], batch: int, run_seed: int, max_window: int):
         fo = np.array(fanouts, dtype=np.int32)
         self._chk("mgnn_sampler_config",

@@ -137,3 +137,22 @@ def test_papers_full_size_eight_partitions():
     st = run_parity(g, 8, 128, [5, 10, 15], 2000, 5000, 0.9995, 4, 1.0, [4, 4], sample_every=4,
                     check_x_rows=512)
     assert st["misses"] > 0
+
+
+@pytest.mark.parametrize("wins", [[4, 4, 4], [1, 1, 2, 4]])
+def test_cfg1_remote_expansion(cfg1, wins):
+    """NEXT-1: halo (and farther) frontier nodes sampled from their owner's CSR -- bit-exact
+    blocks, X, counts and buffer state against the oracle's remote expansion."""
+    st = run_parity(cfg1, 2, 64, [10, 25], 256, 2500, 0.9, 4, 1.0, wins, remote=True)
+    assert st["misses"] > 0 and st["evicted"] > 0
+
+
+def test_remote_expansion_three_hops_four_partitions(cfg1):
+    run_parity(cfg1, 4, 64, [5, 10, 15], 128, 3500, 0.95, 4, 1.0, [4, 4], remote=True)
+
+
+def test_arxiv_remote_expansion_window():
+    """configs[1] at full size with remote expansion, the bench's window (32 steps x 2 partitions)."""
+    g = synth.generate(synth.CONFIGS["arxiv"])
+    run_parity(g, 2, 128, [10, 25], 1000, 2500, 0.995, 32, 1.0, [32], sample_every=8, check_x_rows=4096,
+               remote=True)
