@@ -304,7 +304,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-train-graph", action="store_true", help="training steps as eager launches")
     ap.add_argument("--remote", action="store_true",
-                    help="NEXT-1: sample non-local frontier nodes from their owner's CSR (one GPU only)")
+                    help="NEXT-1: sample non-local frontier nodes from their owner's CSR")
     ap.add_argument("--config", default="arxiv", choices=sorted(LAYOUT),
                     help="workload (default: arxiv-shaped, BASELINE.json configs[1])")
     args = ap.parse_args()
@@ -351,7 +351,7 @@ def main():
     ctx.buffer_init(gamma, alpha, 1.0, delta, f_bp)
     if args.remote:
         if world > 1:
-            raise SystemExit("--remote needs every partition in one context (one GPU)")
+            ctx.load_global_csr(g.indptr, g.cols)       # replicated global CSR on every GPU
         ctx.expand_remote(True)
     ctx.sampler_config(CFG.fanouts, CFG.batch, synth.RUN_SEED, WINDOW)
     stream = torch.cuda.current_stream()

@@ -146,8 +146,13 @@ MGNN_API mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, i
  * same Philox counter -- DistDGL's sampling through the owning server.  Sampled nodes
  * outside V_p^l and V_p^h are misses: fetched from the owner's table, never buffered, never
  * scored (S_A covers V_p^h; the dense S_A of P:228 is not modelled).  Ranks become global ids
- * (window arenas sized by |V|).  Needs every partition hosted by this context (EINVAL otherwise). */
+ * (window arenas sized by |V|).  Needs the global CSR: loaded (mgnn_graph_csr_load) or assembled
+ * from every partition hosted by this context (ESTATE otherwise). */
 MGNN_API mgnn_status mgnn_sampler_expand_remote(mgnn_ctx ctx, int32_t enable);
+/* The replicated global CSR for remote expansion across GPUs (host arrays, copied; SURVEY §8(f)
+ * NEXT-1's "replicated CSR"): indptr [n_global+1], cols [indptr[n_global]] global ids, rows as in
+ * mgnn_partition_desc.  Without it, mgnn_sampler_expand_remote needs every partition hosted here. */
+MGNN_API mgnn_status mgnn_graph_csr_load(mgnn_ctx ctx, const int64_t* indptr, const int32_t* cols);
 
 /* NeighborSampler (Alg.2 l.1) for steps t0..t0+n_steps-1 of every hosted
  * partition into window slot `slot` (0 or 1).  Seeds are the step's slice of

@@ -765,6 +765,23 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
 
 // ------------------------------------------------------------------ sampler configuration
 // ------------------------------------------------------------------ NEXT-1: remote expansion
+mgnn_status mgnn_graph_csr_load(mgnn_ctx ctx, const int64_t* indptr, const int32_t* cols) {
+    GUARD();
+    if (!indptr || (!cols && indptr[ctx->n_global] > 0) || indptr[0] != 0)
+        return fail(ctx, MGNN_EINVAL, "global CSR");
+    const int64_t nnz = indptr[ctx->n_global];
+    for (int64_t v = 0; v < ctx->n_global; ++v)
+        if (indptr[v + 1] < indptr[v]) return fail(ctx, MGNN_EINVAL, "global CSR indptr not monotone");
+    CK(cudaDeviceSynchronize());
+    dfree(ctx->g_indptr);
+    dfree(ctx->g_cols);
+    CK(dalloc(&ctx->g_indptr, ctx->n_global + 1));
+    CK(dalloc(&ctx->g_cols, nnz));
+    CK(cudaMemcpy(ctx->g_indptr, indptr, (ctx->n_global + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    if (nnz) CK(cudaMemcpy(ctx->g_cols, cols, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+    return MGNN_OK;
+}
+
 mgnn_status mgnn_sampler_expand_remote(mgnn_ctx ctx, int32_t enable) {
     GUARD();
     if (ctx->configured) return fail(ctx, MGNN_ESTATE, "expand_remote must precede sampler_config");
@@ -772,9 +789,15 @@ mgnn_status mgnn_sampler_expand_remote(mgnn_ctx ctx, int32_t enable) {
         ctx->remote = false;
         return MGNN_OK;
     }
-    if ((int32_t)ctx->parts.size() != ctx->P)
-        return fail(ctx, MGNN_EINVAL, "remote expansion needs every partition hosted by this context");
+    if (!ctx->g_indptr && (int32_t)ctx->parts.size() != ctx->P)
+        return fail(ctx, MGNN_ESTATE, "remote expansion: load the global CSR (mgnn_graph_csr_load) or host every partition");
     CK(cudaDeviceSynchronize());
+    for (auto& p : ctx->parts)
+        if (!p.halo_map) {
+            CK(dalloc(&p.halo_map, ctx->n_global));
+            CK(cudaMemset(p.halo_map, 0xFF, ctx->n_global * sizeof(int32_t)));
+            launch_halo_index(p.halo, p.n_h, p.halo_map, 0);
+        }
     if (!ctx->g_indptr) {
         int64_t nnz = 0;
         for (auto& p : ctx->parts) nnz += p.nnz;
@@ -789,14 +812,9 @@ mgnn_status mgnn_sampler_expand_remote(mgnn_ctx ctx, int32_t enable) {
             launch_global_csr(ctx->d_parts + lp, p.indptr, p.n_local, p.lo, p.nnz, base, ctx->g_indptr, ctx->g_cols, 0);
             base += p.nnz;
         }
-        for (auto& p : ctx->parts) {
-            CK(dalloc(&p.halo_map, ctx->n_global));
-            CK(cudaMemset(p.halo_map, 0xFF, ctx->n_global * sizeof(int32_t)));
-            launch_halo_index(p.halo, p.n_h, p.halo_map, 0);
-        }
-        CKL();
-        CK(cudaDeviceSynchronize());
     }
+    CKL();
+    CK(cudaDeviceSynchronize());
     ctx->remote = true;
     return upload_parts(ctx);
 }

@@ -106,6 +106,12 @@ class Context:
         self.delta = delta
         self._chk("mgnn_buffer_init", self.L.mgnn_buffer_init(self._h, C.byref(pol), _stream(stream)))
 
+    def load_global_csr(self, indptr: np.ndarray, cols: np.ndarray):
+        """Replicated global CSR (NEXT-1 across GPUs)."""
+        ip = np.ascontiguousarray(indptr, dtype=np.int64)
+        cl = np.ascontiguousarray(cols, dtype=np.int32)
+        self._chk("mgnn_graph_csr_load", self.L.mgnn_graph_csr_load(self._h, _ptr(ip), _ptr(cl)))
+
     def expand_remote(self, enable: bool = True):
         """NEXT-1: sample non-local frontier nodes from their owner's CSR (before sampler_config)."""
         self._chk("mgnn_sampler_expand_remote", self.L.mgnn_sampler_expand_remote(self._h, 1 if enable else 0))

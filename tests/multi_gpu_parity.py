@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--delta", type=int, default=4)
     ap.add_argument("--windows", type=int, default=4)
     ap.add_argument("--train", action="store_true", help="DDP training-step parity (NEXT-3) instead")
+    ap.add_argument("--remote", action="store_true", help="NEXT-1 remote expansion (replicated global CSR)")
     a = ap.parse_args()
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -46,7 +47,7 @@ def main():
             dist.destroy_process_group()
             sys.exit(0 if ok.item() == 1 else 1)
         st = run_parity(g, P, cfg.feat_dim, cfg.fanouts, cfg.batch, 2500, 0.9, a.delta, 1.0,
-                        [a.delta] * a.windows, hosted=hosted, device=local, exchange=True,
+                        [a.delta] * a.windows, hosted=hosted, device=local, exchange=True, remote=a.remote,
                         sample_every=1 if a.config == "cfg1" else 9, check_x_rows=0 if a.config == "cfg1" else 2048)
         print(f"[rank {rank}] parity ok: {st}", flush=True)
         assert st["misses"] > 0 and st["evicted"] > 0 and st["peer_rows"] > 0

@@ -49,6 +49,8 @@ def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, g
         p.set_expand_remote(remote)
     ctx = PL.build_context(device, parts, D, feat_seed, hosted)
     if remote:                        # NEXT-1: non-local frontier nodes sampled from their owners
+        if hosted is not None:        # other partitions live elsewhere: replicate the global CSR
+            ctx.load_global_csr(g.indptr, g.cols)
         ctx.expand_remote(True)
     if exchange:                      # multi-process: map the other ranks' tables (CUDA IPC, NVLink)
         PL.exchange_tables(ctx)
