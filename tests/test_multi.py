@@ -145,3 +145,17 @@ def test_nccl_two_gpus_parity():
                        capture_output=True, text=True, timeout=900, cwd=ROOT)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
+
+
+@pytest.mark.gpu
+def test_nccl_two_gpus_remote_expansion_parity():
+    """NEXT-1 across GPUs: replicated global CSR, far rows over NVLink, bit-exact per rank."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    port = _free_port()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(ROOT, "tests", "multi_gpu_parity.py"), "--remote"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0
