@@ -43,6 +43,7 @@ WINDOW = 32
 PARTS_PER_GPU = 2
 CFG = synth.CONFIGS["arxiv"]
 REMOTE = False                     # NEXT-1 remote expansion (--remote)
+DENSE = False                      # NEXT-1 dense S_A (--dense)
 
 # Measurement policy (f_p in basis points, gamma, Delta) by config and total partitions P: the
 # paper's GPU optima; theta_R = 1.
@@ -189,7 +190,7 @@ def peer_copy_gbs(src: int, dst: int):
 def oracle_rate(parts, P, f_bp, gamma, delta, budget_s: float, min_steps: int = 8):
     """Oracle (oracle/orc.c, single thread) on the same workload: minibatches/s over a bounded sample."""
     from oracle import oracle as O
-    W = O.World(parts, CFG.feat_dim, synth.FEAT_SEED)
+    W = O.World(parts, CFG.feat_dim, synth.FEAT_SEED, dense=DENSE)
     alpha = O.alpha_default(gamma, delta)
     for p in W.parts:
         p.buffer_init(gamma, alpha, 1.0, delta, f_bp)
@@ -213,7 +214,7 @@ def oracle_rate_threads(parts, P, f_bp, gamma, delta, budget_s: float):
     are independent between eviction rounds of their own buffers): SURVEY §8(d)'s P-thread rate."""
     import threading as th
     from oracle import oracle as O
-    W = O.World(parts, CFG.feat_dim, synth.FEAT_SEED)
+    W = O.World(parts, CFG.feat_dim, synth.FEAT_SEED, dense=DENSE)
     alpha = O.alpha_default(gamma, delta)
     for p in W.parts:
         p.buffer_init(gamma, alpha, 1.0, delta, f_bp)
@@ -305,12 +306,14 @@ def main():
     ap.add_argument("--no-train-graph", action="store_true", help="training steps as eager launches")
     ap.add_argument("--remote", action="store_true",
                     help="NEXT-1: sample non-local frontier nodes from their owner's CSR")
+    ap.add_argument("--dense", action="store_true", help="NEXT-1: dense S_A (every non-local node scorable)")
     ap.add_argument("--config", default="arxiv", choices=sorted(LAYOUT),
                     help="workload (default: arxiv-shaped, BASELINE.json configs[1])")
     args = ap.parse_args()
-    global WINDOW, REMOTE
+    global WINDOW, REMOTE, DENSE
     select_config(args.config)
     REMOTE = args.remote
+    DENSE = args.dense
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     if args.impl == "reference":
@@ -344,7 +347,7 @@ def main():
     g = synth.generate(CFG)
     parts = synth.partition(g, P)
     hosted = list(range(PARTS_PER_GPU * rank, PARTS_PER_GPU * (rank + 1)))
-    ctx = PL.build_context(local, parts, CFG.feat_dim, synth.FEAT_SEED, hosted)
+    ctx = PL.build_context(local, parts, CFG.feat_dim, synth.FEAT_SEED, hosted, dense=args.dense)
     if world > 1:
         PL.exchange_tables(ctx)
     alpha = PL.alpha_default(gamma, delta)
@@ -669,7 +672,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": dict(workload(P), **({"sampling": "remote expansion (NEXT-1)"} if args.remote else {})),
+            "config": dict(workload(P), **({"sampling": "remote expansion (NEXT-1)"} if args.remote else {}),
+                           **({"scores": "dense S_A (NEXT-1)"} if args.dense else {})),
             "hit_rate": hits / max(1, hits + misses),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": E2E, "path": "two-stream pipeline: mgnn_sample(host pinned seeds, H2D) | "

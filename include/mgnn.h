@@ -153,6 +153,11 @@ MGNN_API mgnn_status mgnn_sampler_expand_remote(mgnn_ctx ctx, int32_t enable);
  * NEXT-1's "replicated CSR"): indptr [n_global+1], cols [indptr[n_global]] global ids, rows as in
  * mgnn_partition_desc.  Without it, mgnn_sampler_expand_remote needs every partition hosted here. */
 MGNN_API mgnn_status mgnn_graph_csr_load(mgnn_ctx ctx, const int64_t* indptr, const int32_t* cols);
+/* NEXT-1's dense S_A ("O(|V|)"), before any mgnn_partition_load: every non-local node is
+ * scorable (halo arrays over V \ V_p^l, deg_in = 0 for nodes without a local neighbour), so the
+ * remote nodes remote expansion reaches are tallied and may enter the buffer by replacement.
+ * |BUF| stays ceil(f * |true halo|); the initial buffer is unchanged. */
+MGNN_API mgnn_status mgnn_ctx_set_dense_scores(mgnn_ctx ctx, int32_t enable);
 
 /* NeighborSampler (Alg.2 l.1) for steps t0..t0+n_steps-1 of every hosted
  * partition into window slot `slot` (0 or 1).  Seeds are the step's slice of

@@ -66,6 +66,7 @@ def lib():
             "orc_totals": (None, [P, P]),
             "orc_evict_and_replace": (I64, [I64, I64, P, P, P, P, P, P, F32, F32, P, P, P]),
             "orc_set_expand_remote": (None, [P, I32]),
+            "orc_world_set_dense": (None, [P, I32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -127,7 +128,7 @@ def evict_and_replace(node_of_slot, se, sa, slot_of, halo, deg_in, alpha, theta_
 class World:
     """All P partitions of one graph, each a trainer with its own prefetcher."""
 
-    def __init__(self, parts_in, feat_dim: int, feat_seed: int):
+    def __init__(self, parts_in, feat_dim: int, feat_seed: int, dense: bool = False):
         L = lib()
         p0 = parts_in[0]
         self.P = p0.n_parts
@@ -136,6 +137,7 @@ class World:
         self._w = L.orc_world_new(self.P, p0.n_global, _p(self.bounds), feat_dim, feat_seed)
         if not self._w:
             raise ValueError("orc_world_new: invalid input")
+        L.orc_world_set_dense(self._w, 1 if dense else 0)   # NEXT-1 dense S_A (orc.h)
         self._keep = []
         self.parts = []
         for pi in parts_in:

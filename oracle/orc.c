@@ -81,6 +81,7 @@ float orc_alpha_default(float gamma, int32_t delta) {
 
 /* ---------------------------------------------------------------- types */
 struct orc_world {
+    int32_t dense;     /* NEXT-1 dense S_A: every non-local node is scorable (set before the partitions) */
     int32_t P;
     int64_t n_global;
     int64_t* bounds;   /* P+1 */
@@ -100,6 +101,7 @@ struct orc_part {
     int32_t* halo;     /* V_p^h sorted ascending */
     int32_t* deg_in;
     int64_t n_h;
+    int64_t n_h_true;  /* |V_p^h| (halo nodes with deg_in > 0): the basis of |BUF| even when dense */
     float* table;      /* local KVStore: n_local x D */
     /* prefetcher */
     int ready;
@@ -217,15 +219,22 @@ orc_part* orc_part_new(orc_world* w, int32_t part_id, const int64_t* indptr, con
     p->train = malloc(sizeof(int32_t) * (size_t)(n_train ? n_train : 1));
     memcpy(p->train, train_ids, sizeof(int32_t) * (size_t)n_train);
 
-    /* V_p^h = {v not in V_p^l : v in N(u), u in V_p^l} (R#9), sorted. */
-    int32_t* tmp = malloc(sizeof(int32_t) * (size_t)(nnz ? nnz : 1));
-    int64_t m = 0;
-    for (int64_t e = 0; e < nnz; e++)
-        if (cols[e] < lo || cols[e] >= hi) tmp[m++] = cols[e];
-    qsort(tmp, (size_t)m, sizeof(int32_t), cmp_i32);
-    int64_t nh = 0;
-    for (int64_t i = 0; i < m; i++)
-        if (i == 0 || tmp[i] != tmp[i - 1]) tmp[nh++] = tmp[i];
+    /* V_p^h = {v not in V_p^l : v in N(u), u in V_p^l} (R#9), sorted.  Dense scores
+       (NEXT-1, P:228's O(|V|) S_A): the scorable set is every non-local node. */
+    int64_t m = 0, nh = 0;
+    int32_t* tmp;
+    if (w->dense) {
+        tmp = malloc(sizeof(int32_t) * (size_t)(w->n_global - nl ? w->n_global - nl : 1));
+        for (int64_t v = 0; v < w->n_global; v++)
+            if (v < lo || v >= hi) tmp[nh++] = (int32_t)v;
+    } else {
+        tmp = malloc(sizeof(int32_t) * (size_t)(nnz ? nnz : 1));
+        for (int64_t e = 0; e < nnz; e++)
+            if (cols[e] < lo || cols[e] >= hi) tmp[m++] = cols[e];
+        qsort(tmp, (size_t)m, sizeof(int32_t), cmp_i32);
+        for (int64_t i = 0; i < m; i++)
+            if (i == 0 || tmp[i] != tmp[i - 1]) tmp[nh++] = tmp[i];
+    }
     p->n_h = nh;
     p->halo = malloc(sizeof(int32_t) * (size_t)(nh ? nh : 1));
     memcpy(p->halo, tmp, sizeof(int32_t) * (size_t)nh);
@@ -234,6 +243,8 @@ orc_part* orc_part_new(orc_world* w, int32_t part_id, const int64_t* indptr, con
     p->deg_in = calloc((size_t)(nh ? nh : 1), sizeof(int32_t));
     for (int64_t e = 0; e < nnz; e++)
         if (cols[e] < lo || cols[e] >= hi) p->deg_in[bsearch_i32(p->halo, nh, cols[e])]++;
+    p->n_h_true = 0;
+    for (int64_t h = 0; h < nh; h++) p->n_h_true += p->deg_in[h] > 0;
 
     /* local KVStore */
     int32_t D = w->D;
@@ -288,9 +299,9 @@ int orc_buffer_init(orc_part* p, float gamma, float alpha, float theta_r, int32_
     for (int32_t q = 0; q < p->w->P; q++)
         if (!p->w->parts[q]) return -1;   /* every owner's KVStore must exist for the init RPC */
     p->gamma = gamma; p->alpha = alpha; p->theta_r = theta_r; p->delta = delta;
-    /* |BUF| = ceil(f * |V_p^h|) in integer basis points (R#11) */
+    /* |BUF| = ceil(f * |V_p^h|) in integer basis points (R#11); the true halo, also when dense */
     int64_t nh = p->n_h;
-    p->cap = ((int64_t)f_bp * nh + 9999) / 10000;
+    p->cap = ((int64_t)f_bp * p->n_h_true + 9999) / 10000;
     free(p->node_of_slot); free(p->se); free(p->sa); free(p->slot_of); free(p->rows); free(p->hitflag);
     int64_t cap = p->cap, D = p->w->D;
     p->node_of_slot = malloc(sizeof(int32_t) * (size_t)(cap ? cap : 1));
@@ -596,6 +607,7 @@ int orc_step(orc_part* p, uint64_t run_seed, uint64_t step, const int32_t* fanou
 }
 
 void orc_set_expand_remote(orc_part* p, int32_t on) { p->expand_remote = on ? 1 : 0; }
+void orc_world_set_dense(orc_world* w, int32_t on) { w->dense = on ? 1 : 0; }
 
 /* ---------------------------------------------------------------- getters */
 void orc_counts(const orc_part* p, int64_t* out) { memcpy(out, p->counts, sizeof(p->counts)); }

@@ -82,6 +82,12 @@ int64_t orc_evict_and_replace(int64_t cap, int64_t n_h, int32_t* node_of_slot, f
  * nodes outside V_p^l and V_p^h are misses (class 3): fetched from the owner, never buffered and
  * never scored (S_A covers V_p^h only; the dense S_A of P:228 is not modelled). */
 void orc_set_expand_remote(orc_part* p, int32_t on);
+/* NEXT-1's dense S_A ("a compact S_A over V_p^h ... or O(|V|)"): with on != 0 (before any
+ * orc_part_new) every non-local node is scorable -- in the halo arrays with deg_in = 0 when it has
+ * no local neighbour -- so remote nodes reached by remote expansion are tallied and can enter
+ * the buffer by replacement.  |BUF| stays ceil(f * |true halo|), and the initial buffer is the
+ * same (true halo nodes rank first by deg_in). */
+void orc_world_set_dense(orc_world* w, int32_t on);
 
 /* Results of the last orc_step (valid until the next one). */
 enum { ORC_C_NODES = 0, ORC_C_LOCAL, ORC_C_HIT, ORC_C_MISS, ORC_C_EVICTED, ORC_C_REFILLED,

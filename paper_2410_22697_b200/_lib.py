@@ -22,7 +22,7 @@ SYMBOLS = [
     "mgnn_profile_enable", "mgnn_profile_read", "mgnn_profile_kernels",
     "mgnn_sage_config", "mgnn_sage_forward", "mgnn_sage_train_config", "mgnn_sage_train_step",
     "mgnn_sage_grads", "mgnn_sage_sgd", "mgnn_sage_loss", "mgnn_sage_params", "mgnn_sampler_expand_remote",
-    "mgnn_graph_csr_load",
+    "mgnn_graph_csr_load", "mgnn_ctx_set_dense_scores",
 ]
 
 
@@ -103,6 +103,7 @@ def load(path: str = LIB_PATH):
         "mgnn_sage_params": (S, [P, I32, P, P, P]),
         "mgnn_sampler_expand_remote": (S, [P, I32]),
         "mgnn_graph_csr_load": (S, [P, P, P]),
+        "mgnn_ctx_set_dense_scores": (S, [P, I32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

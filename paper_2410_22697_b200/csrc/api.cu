@@ -68,6 +68,7 @@ struct Part {
     int64_t* indptr = nullptr;
     int32_t* cols_rank = nullptr;
     int32_t* halo_map = nullptr;         // NEXT-1: [n_global] halo index or -1
+    int64_t n_h_true = 0;                // |V_p^h| (deg_in > 0): the basis of |BUF| also with dense scores
     int32_t* halo = nullptr;
     int32_t* deg_in = nullptr;
     int32_t* train = nullptr;
@@ -151,6 +152,7 @@ struct mgnn_ctx_s {
     size_t perm_scr_bytes = 0;           // mgnn_sample may run concurrently with gather/score
     // NEXT-1 remote expansion: global CSR over every partition (all hosted by this context)
     bool remote = false;
+    bool dense = false;                  // NEXT-1 dense S_A: every non-local node scorable
     int64_t* g_indptr = nullptr;
     int32_t* g_cols = nullptr;
     // sampler
@@ -558,8 +560,16 @@ mgnn_status mgnn_partition_load(mgnn_ctx ctx, const mgnn_partition_desc* d, int3
     CK(cudaMemset(status, 0, (tiles + 1) * sizeof(unsigned long long)));
     CK(dalloc(&d_n, 2));
     CK(cudaMemset(d_n, 0, 2 * sizeof(long long)));
-    CK(dalloc(&p.halo, halo_max));
-    launch_mark_halo(cols_g, nnz, lo, hi, bm, s);
+    const int64_t halo_cap = ctx->dense ? std::max<int64_t>(ctx->n_global - nl, 1) : halo_max;
+    CK(dalloc(&p.halo, halo_cap));
+    if (ctx->dense) {       // NEXT-1 dense S_A: the scorable set is every non-local node
+        std::vector<uint32_t> hb((size_t)words, 0u);
+        for (int64_t v = 0; v < ctx->n_global; ++v)
+            if (v < lo || v >= hi) hb[(size_t)(v >> 5)] |= 1u << (v & 31);
+        if (words) CK(cudaMemcpy(bm, hb.data(), words * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    } else {
+        launch_mark_halo(cols_g, nnz, lo, hi, bm, s);
+    }
     Scratch sc{status + 1, (int32_t*)status};
     launch_bitmap_to_ids(bm, words, p.halo, d_n, sc, s);
     CKL();
@@ -580,6 +590,8 @@ mgnn_status mgnn_partition_load(mgnn_ctx ctx, const mgnn_partition_desc* d, int3
         std::vector<int32_t> deg(nh);
         if (nh) CK(cudaMemcpy(deg.data(), p.deg_in, nh * sizeof(int32_t), cudaMemcpyDeviceToHost));
         for (int32_t x : deg) p.max_deg_in = std::max(p.max_deg_in, x);
+        p.n_h_true = 0;
+        for (int32_t x : deg) p.n_h_true += x > 0;
     }
     CK(dalloc(&p.train, d->n_train));
     if (d->n_train) CK(cudaMemcpy(p.train, d->train_ids, d->n_train * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -675,7 +687,7 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
     int64_t cap_max = 0, nh_max = 0;
     for (auto& p : ctx->parts) {
         free_buffer(p);
-        p.cap = ((int64_t)pol->f_bp * p.n_h + 9999) / 10000;   // ceil(f |V_p^h|) (R#11)
+        p.cap = ((int64_t)pol->f_bp * p.n_h_true + 9999) / 10000;   // ceil(f |V_p^h|) (R#11)
         CK(dalloc(&p.rows, p.cap * ctx->pitch));
         CK(dalloc(&p.se, p.cap));
         CK(dalloc(&p.sa, p.n_h));
@@ -765,6 +777,13 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
 
 // ------------------------------------------------------------------ sampler configuration
 // ------------------------------------------------------------------ NEXT-1: remote expansion
+mgnn_status mgnn_ctx_set_dense_scores(mgnn_ctx ctx, int32_t enable) {
+    GUARD();
+    if (!ctx->parts.empty()) return fail(ctx, MGNN_ESTATE, "dense scores must be chosen before partition_load");
+    ctx->dense = enable != 0;
+    return MGNN_OK;
+}
+
 mgnn_status mgnn_graph_csr_load(mgnn_ctx ctx, const int64_t* indptr, const int32_t* cols) {
     GUARD();
     if (!indptr || (!cols && indptr[ctx->n_global] > 0) || indptr[0] != 0)

@@ -301,10 +301,14 @@ def alpha_default(gamma: float, delta: int) -> float:
     return float(_lib.load().mgnn_alpha_default(gamma, delta))
 
 
-def build_context(device: int, parts_in, feat_dim: int, feat_seed: int, hosted: Optional[Sequence[int]] = None) -> Context:
-    """Context hosting the partitions `hosted` (default: all) of a partitioned graph."""
+def build_context(device: int, parts_in, feat_dim: int, feat_seed: int, hosted: Optional[Sequence[int]] = None,
+                  dense: bool = False) -> Context:
+    """Context hosting the partitions `hosted` (default: all) of a partitioned graph.
+    dense: NEXT-1's dense S_A (every non-local node scorable)."""
     p0 = parts_in[0]
     ctx = Context(device, p0.bounds, feat_dim, feat_seed)
+    if dense:
+        ctx._chk("mgnn_ctx_set_dense_scores", ctx.L.mgnn_ctx_set_dense_scores(ctx._h, 1))
     for pi in parts_in:
         if hosted is None or pi.part_id in hosted:
             ctx.load_partition(pi.part_id, pi.indptr, pi.cols, pi.train_ids)

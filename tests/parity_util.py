@@ -36,18 +36,18 @@ def assert_bits_equal(a, b, what):
 def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, gamma: float, delta: int,
                theta_r: float, windows, run_seed: int = synth.RUN_SEED, feat_seed: int = synth.FEAT_SEED,
                alpha=None, hosted=None, sample_every: int = 1, check_x_rows: int = 0, ext_seeds=None,
-               device: int = 0, exchange: bool = False, remote: bool = False):
+               device: int = 0, exchange: bool = False, remote: bool = False, dense: bool = False):
     """windows: list of window lengths run back to back from step 1."""
     from paper_2410_22697_b200 import pipeline as PL
 
     parts = synth.partition(g, P)
     if alpha is None:
         alpha = float(O.alpha_default(gamma, delta))
-    W = O.World(parts, D, feat_seed)
+    W = O.World(parts, D, feat_seed, dense=dense)
     for p in W.parts:
         p.buffer_init(gamma, alpha, theta_r, delta, f_bp)
         p.set_expand_remote(remote)
-    ctx = PL.build_context(device, parts, D, feat_seed, hosted)
+    ctx = PL.build_context(device, parts, D, feat_seed, hosted, dense=dense)
     if remote:                        # NEXT-1: non-local frontier nodes sampled from their owners
         if hosted is not None:        # other partitions live elsewhere: replicate the global CSR
             ctx.load_global_csr(g.indptr, g.cols)

@@ -156,3 +156,14 @@ def test_arxiv_remote_expansion_window():
     g = synth.generate(synth.CONFIGS["arxiv"])
     run_parity(g, 2, 128, [10, 25], 1000, 2500, 0.995, 32, 1.0, [32], sample_every=8, check_x_rows=4096,
                remote=True)
+
+
+@pytest.mark.parametrize("theta", [1.0, 0.0])
+def test_cfg1_remote_expansion_dense_scores(cfg1, theta):
+    """NEXT-1 with the dense S_A: remote nodes are tallied and may replace buffered ones."""
+    st = run_parity(cfg1, 2, 64, [10, 25], 256, 2500, 0.9, 4, theta, [4, 4, 4], remote=True, dense=True)
+    assert st["misses"] > 0 and st["evicted"] > 0
+
+
+def test_dense_scores_local_sampling(cfg1):
+    run_parity(cfg1, 3, 64, [5, 10, 15], 128, 3500, 0.95, 4, 1.0, [4, 4], dense=True)

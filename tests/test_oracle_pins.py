@@ -595,3 +595,71 @@ def test_remote_expansion_single_partition_is_identity():
         outs.append((p.frontier().tolist(), [p.hop_block(i)[1].tolist() for i in range(2)]))
         W.close()
     assert outs[0] == outs[1]
+
+
+def _path6_world(dense):
+    g = synth.from_edges(6, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5)])
+    W, _ = world_from(g, 2, bounds=np.array([0, 3, 6]))
+    return W
+
+
+def test_dense_scores_far_node_enters_buffer():
+    """Path 0-..-5, partitions {0,1,2} | {3,4,5}, seed 2, full fanout, 2 hops, remote expansion:
+    F = [2, 1, 3, 0, 4].  True halo of p0 = {3} (cap = 1 at f = 1); 4 is remote but scorable with
+    the dense S_A.  alpha = 2 (an explicit override) makes the buffered 3 evictable at the round
+    of step 2, when S_A[4] = 2 >= theta_R: 4 replaces 3 (S_A[3] <- S_E = 1, S_E[slot] <- 2).
+    Step 3 then hits 4 and misses 3.  Without the dense S_A, 4 is an unscored miss forever."""
+    g = synth.from_edges(6, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5)])
+    for dense in (False, True):
+        parts = synth.partition(g, 2, np.array([0, 3, 6]))
+        W = O.World(parts, 4, FEAT_SEED, dense=dense)
+        p = W.parts[0]
+        p.buffer_init(0.9, 2.0, 1.0, 2, 10000)
+        p.set_expand_remote(True)
+        assert p.cap == 1
+        seeds = np.array([2], np.int32)
+        for t in (1, 2):
+            p.step(RUN_SEED, t, [32, 32], 1, seeds=seeds)
+            assert p.frontier().tolist() == [2, 1, 3, 0, 4]
+        st = p.buffer_state()
+        halo = p.halo()[0].tolist()
+        if dense:
+            assert halo == [3, 4, 5]
+            assert st["node_of_slot"].tolist() == [4]
+            assert st["se"].tolist() == [2.0]
+            assert st["sa"].tolist() == [1.0, -1.0, 0.0]
+        else:
+            assert halo == [3] and st["node_of_slot"].tolist() == [3]
+        p.step(RUN_SEED, 3, [32, 32], 1, seeds=seeds)
+        c = p.counts()
+        assert (c["n_hit"], c["n_miss"]) == ((1, 1) if dense else (1, 1))
+        cls = p.classes().tolist()
+        assert cls == ([0, 0, 2, 0, 1] if dense else [0, 0, 1, 0, 3])
+        if dense:
+            assert p.buffer_state()["sa"].tolist() == [2.0, -1.0, 0.0]
+        W.close()
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_dense_scores_without_remote_expansion_is_identity(seed):
+    """Local sampling never reaches nodes outside V_p^h; with theta_R = 1 their S_A (0) never
+    qualifies them, so the dense scoreboard changes nothing on the true halo."""
+    g = synth.random_graph(30, 0.15, seed)
+    res = []
+    for dense in (False, True):
+        W, parts = world_from(g, 3)
+        W.close()
+        W = O.World(parts, 4, FEAT_SEED, dense=dense)
+        p = W.parts[1]
+        p.buffer_init(0.8, float(O.alpha_default(0.8, 2)), 1.0, 2, 5000)
+        out = []
+        for t in range(1, 9):
+            p.step(RUN_SEED, t, [2, 3], 3)
+            out.append((p.frontier().tolist(), p.counts()))
+        st = p.buffer_state()
+        halo = p.halo()[0]
+        true = [i for i, d in enumerate(p.halo()[1].tolist()) if d > 0]
+        res.append((out, st["node_of_slot"].tolist(), st["se"].tolist(), halo[true].tolist(),
+                    st["sa"][true].tolist()))
+        W.close()
+    assert res[0] == res[1]
