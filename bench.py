@@ -307,6 +307,8 @@ def main():
     ap.add_argument("--remote", action="store_true",
                     help="NEXT-1: sample non-local frontier nodes from their owner's CSR")
     ap.add_argument("--dense", action="store_true", help="NEXT-1: dense S_A (every non-local node scorable)")
+    ap.add_argument("--hash-partition", action="store_true",
+                    help="NEXT-4 stress: partitions of a randomly relabelled graph (hash partitioner)")
     ap.add_argument("--config", default="arxiv", choices=sorted(LAYOUT),
                     help="workload (default: arxiv-shaped, BASELINE.json configs[1])")
     args = ap.parse_args()
@@ -345,13 +347,22 @@ def main():
     f_bp, gamma, delta = policy_for(P)
     WINDOW = window_for(delta)
     g = synth.generate(CFG)
+    if args.hash_partition:
+        g = synth.hash_relabel(g)
     parts = synth.partition(g, P)
     hosted = list(range(PARTS_PER_GPU * rank, PARTS_PER_GPU * (rank + 1)))
     ctx = PL.build_context(local, parts, CFG.feat_dim, synth.FEAT_SEED, hosted, dense=args.dense)
     if world > 1:
         PL.exchange_tables(ctx)
     alpha = PL.alpha_default(gamma, delta)
+    # INITIALIZE_PREFETCHER cost ("<1% of overall training"), CUDA events on the init stream
+    i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    i0.record()
     ctx.buffer_init(gamma, alpha, 1.0, delta, f_bp)
+    i1.record()
+    torch.cuda.synchronize()
+    init_ms = i0.elapsed_time(i1)
     if args.remote:
         if world > 1:
             ctx.load_global_csr(g.indptr, g.cols)       # replicated global CSR on every GPU
@@ -673,7 +684,9 @@ def main():
             "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
             "config": dict(workload(P), **({"sampling": "remote expansion (NEXT-1)"} if args.remote else {}),
-                           **({"scores": "dense S_A (NEXT-1)"} if args.dense else {})),
+                           **({"scores": "dense S_A (NEXT-1)"} if args.dense else {}),
+                           **({"partitioner": "hash (random relabel)"} if args.hash_partition else {})),
+            "buffer_init_ms": init_ms,
             "hit_rate": hits / max(1, hits + misses),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": E2E, "path": "two-stream pipeline: mgnn_sample(host pinned seeds, H2D) | "

@@ -217,6 +217,27 @@ def partition(g: Graph, n_parts: int, bounds: Optional[np.ndarray] = None) -> Li
     return out
 
 
+def hash_relabel(g: Graph, seed: int = GRAPH_SEED + 5) -> Graph:
+    """The same graph under a uniformly random relabelling of its ids: contiguous-range partitions of
+    the result are a hash partition of the original (SURVEY §8(f) NEXT-4's worst-case halo stress)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    n = g.n_nodes
+    new_of = rng.permutation(n).astype(np.int64)           # old id -> new id
+    old_of = np.empty(n, np.int64)
+    old_of[new_of] = np.arange(n, dtype=np.int64)
+    deg = np.diff(g.indptr)[old_of]
+    indptr = np.zeros(n + 1, np.int64)
+    np.cumsum(deg, out=indptr[1:])
+    src = np.repeat(np.arange(n, dtype=np.int64), deg)
+    starts = g.indptr[old_of]
+    idx = np.arange(indptr[-1], dtype=np.int64) - np.repeat(indptr[:-1], deg) + np.repeat(starts, deg)
+    cols = new_of[g.cols[idx]]
+    key = src * n + cols                                    # rows ascending after relabelling
+    order = np.argsort(key, kind="stable")
+    cols = cols[order].astype(np.int32)
+    return Graph(n, indptr, cols, g.train_mask[old_of])
+
+
 def describe(g: Graph, parts: List[PartitionInput]) -> dict:
     """Achieved shape statistics reported beside every result."""
     deg = np.diff(g.indptr)

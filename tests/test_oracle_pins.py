@@ -663,3 +663,16 @@ def test_dense_scores_without_remote_expansion_is_identity(seed):
                     st["sa"][true].tolist()))
         W.close()
     assert res[0] == res[1]
+
+
+def test_hash_relabel_is_an_isomorphism():
+    """NEXT-4 stress input: the relabelled graph has exactly the relabelled edge set, ascending rows."""
+    g = synth.random_graph(60, 0.08, 4)
+    h = synth.hash_relabel(g, 11)
+    rng = np.random.Generator(np.random.PCG64(11))
+    new_of = rng.permutation(60)
+    e_g = {(int(new_of[u]), int(new_of[v])) for u in range(60) for v in g.cols[g.indptr[u]:g.indptr[u + 1]]}
+    e_h = {(u, int(v)) for u in range(60) for v in h.cols[h.indptr[u]:h.indptr[u + 1]]}
+    assert e_g == e_h
+    assert all(np.all(np.diff(h.cols[h.indptr[u]:h.indptr[u + 1]]) > 0) for u in range(60))
+    assert sorted(np.nonzero(h.train_mask)[0].tolist()) == sorted(int(new_of[v]) for v in np.nonzero(g.train_mask)[0])
