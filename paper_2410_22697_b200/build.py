@@ -17,8 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libmgnn.so")
-UNITS = ["api.cu", "sample.cu", "gather.cu", "score.cu", "sort.cu", "load.cu", "sage.cu", "train.cu"]
-HEADERS = ["common.cuh", "launch.h", "umma.cuh"]
+UNITS = ["api.cu", "api_sage.cu", "sample.cu", "gather.cu", "score.cu", "sort.cu", "load.cu", "sage.cu", "train.cu"]
+HEADERS = ["common.cuh", "launch.h", "umma.cuh", "ctx.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 EXTRA = os.environ.get("MGNN_NVCC_EXTRA", "").split()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

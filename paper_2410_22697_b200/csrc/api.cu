@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/mgnn.h"
+#include "ctx.h"
 #include "launch.h"
 
 namespace mgnn {
@@ -56,160 +57,12 @@ bool pdl_enabled() {
 }
 }  // namespace mgnn
 
+
 using namespace mgnn;
+using namespace mgnn::host;
 
-namespace {
-
-struct Part {
-    int32_t part_id = -1;
-    int64_t lo = 0, n_local = 0, n_h = 0, h_below = 0, nnz = 0, n_train = 0, cap = 0, nbatch = 1;
-    int32_t max_deg_in = 0;
-    int32_t perm_slots = 0;
-    int64_t* indptr = nullptr;
-    int32_t* cols_rank = nullptr;
-    int32_t* halo_map = nullptr;         // NEXT-1: [n_global] halo index or -1
-    int64_t n_h_true = 0;                // |V_p^h| (deg_in > 0): the basis of |BUF| also with dense scores
-    int32_t* halo = nullptr;
-    int32_t* deg_in = nullptr;
-    int32_t* train = nullptr;
-    float* table = nullptr;
-    float* rows = nullptr;
-    float* se = nullptr;
-    float* sa = nullptr;
-    int32_t* slot_of = nullptr;
-    int32_t* slot_h = nullptr;
-    unsigned long long* hitmask = nullptr;
-    int32_t* rank_deg = nullptr;
-    int32_t* perm = nullptr;
-    int32_t perm_chunk = 1;              // G: epoch orders generated per sort call
-    int64_t chunk_loaded[2] = {-1, -1};  // chunk id c (epochs [cG, cG+G)) held by ring half c % 2
-    // sort buffers: E (cap) / R (n_h) for eviction; R also serves buffer init; P (n_train) for epoch orders
-    unsigned long long *ek = nullptr, *ekt = nullptr, *rk = nullptr, *rkt = nullptr, *pk = nullptr, *pkt = nullptr;
-    uint32_t *ev = nullptr, *evt = nullptr, *rv = nullptr, *rvt = nullptr, *pvt = nullptr;
-};
-
-struct Win {
-    bool alloc = false, sampled = false, gathered = false, scored = false;
-    int32_t n_steps = 0;
-    uint64_t step0 = 0;
-    int32_t* fr_rank = nullptr;
-    int32_t* fr_gid = nullptr;
-    int64_t* hop_size = nullptr;
-    int64_t* off[kMaxLayers] = {};
-    int32_t* cols[kMaxLayers] = {};
-    float* X = nullptr;
-    int32_t* pos_of = nullptr;
-    uint32_t* nb = nullptr;         // [M][L][bm_words] new-node bitmap of each hop (in the zero region)
-    int32_t* wpre = nullptr;        // [M][L][bm_words] frontier position of each word's first new node
-    char* zero = nullptr;           // [scan scratch | counts | fb], zeroed per window
-    size_t zero_bytes = 0;
-    unsigned long long* status = nullptr;
-    int32_t* tilectr = nullptr;
-    long long* counts = nullptr;
-    uint32_t* fb = nullptr;
-    int32_t* ext_seeds = nullptr;
-    int32_t* ext_counts = nullptr;
-    // scratch sub-regions
-    Scratch sc_count[kMaxLayers], sc_compact[kMaxLayers];
-};
-
-}  // namespace
-
-struct mgnn_ctx_s {
-    int device = 0;
-    int32_t P = 0;
-    int64_t n_global = 0;
-    std::vector<int64_t> bounds;
-    int32_t D = 0, pitch = 0;
-    uint64_t feat_seed = 0;
-    std::vector<Part> parts;
-    std::vector<int32_t> lp_of;          // part id -> local index or -1
-    std::vector<const float*> tables;    // device-accessible table per partition
-    std::vector<void*> ipc_opened;
-    int64_t* d_bounds = nullptr;
-    const float** d_tables = nullptr;
-    uint8_t* d_on_peer = nullptr;        // [P]: table imported from another process (NVLink)
-    PartDev* d_parts = nullptr;
-    int32_t* d_err = nullptr;
-    long long* d_gathered = nullptr;
-    // policy
-    bool buffer_ready = false;
-    mgnn_policy pol{};
-    // eviction scratch
-    SortSeg* d_evsegs = nullptr;
-    SortSeg* d_initsegs = nullptr;
-    bool force_sort_path = false;        // MGNN_EVICT_SORT=1: always use the full radix-sort eviction path
-    int32_t ev_passes = 8;
-    long long* d_sel_n = nullptr;
-    char* ev_zero = nullptr;
-    size_t ev_zero_bytes = 0;
-    Scratch ev_sc{};
-    EvScratch ev_ev{};
-    int64_t ev_tiles = 1;
-    void* sort_scr = nullptr;            // radix sort scratch of init / eviction (buffer stream)
-    size_t sort_scr_bytes = 0;
-    void* perm_scr = nullptr;            // radix sort scratch of epoch orders (sampling stream), so
-    size_t perm_scr_bytes = 0;           // mgnn_sample may run concurrently with gather/score
-    // NEXT-1 remote expansion: global CSR over every partition (all hosted by this context)
-    bool remote = false;
-    bool dense = false;                  // NEXT-1 dense S_A: every non-local node scorable
-    int64_t* g_indptr = nullptr;
-    int32_t* g_cols = nullptr;
-    // sampler
-    bool configured = false;
-    int32_t L = 0, batch = 0, max_window = 0;
-    int32_t fan[kMaxLayers] = {}, k_hop[kMaxLayers] = {};
-    uint64_t run_seed = 0;
-    int64_t ucap = 0, vp_max = 0, bm_words = 0;
-    int64_t fcap[kMaxLayers + 1] = {}, ecap[kMaxLayers] = {};
-    Win win[2];
-    SortSeg* d_permsegs = nullptr;       // [n_lp][max perm slots]
-    int32_t perm_slots_max = 0;
-    long long* d_perm_n = nullptr;       // [n_lp]
-    // A14 consumer (GraphSAGE-mean): padded weights [npad][2*kp] = [W_self | W_neigh], bias [npad],
-    // ping-pong hidden buffers, and the TMA tensor maps of every operand (128 B each)
-    struct Sage {
-        bool ready = false;
-        int32_t L = 0;
-        int32_t dims[kMaxLayers + 1] = {};
-        int32_t npad[kMaxLayers] = {}, kp[kMaxLayers] = {};
-        // parameters: one buffer, layer l = Wcat [npad][2 kp] at w_off[l], bias [npad] at b_off[l]
-        float* params = nullptr;
-        int64_t n_params = 0, w_off[kMaxLayers] = {}, b_off[kMaxLayers] = {};
-        float* w[kMaxLayers] = {};
-        float* b[kMaxLayers] = {};
-        float* h[kMaxLayers] = {};                // hidden outputs H^{l+1}, l < L-1: [M][out_rows][npad]
-        int64_t out_rows[kMaxLayers] = {};        // rows per instance of layer l's output buffer (= fcap[h])
-        alignas(64) unsigned char map_w[kMaxLayers][128];
-        alignas(64) unsigned char map_in[2][kMaxLayers][128];   // [window slot][layer]
-        // training (NEXT-3)
-        bool train = false;
-        int32_t* labels = nullptr;                // [n_global]
-        float* grads = nullptr;                   // same layout as params
-        float* wt[kMaxLayers] = {};               // transposed Wcat: [2 kp][npad] (dgrad operand)
-        float* mean[kMaxLayers] = {};             // [M][out_rows][kp] neighbour means
-        float* logits = nullptr;                  // [M][rows64][npad_L]
-        float* dlogits = nullptr;
-        float* dh[kMaxLayers] = {};               // gradient of h[l]: [M][dh_rows[l]][npad[l]]
-        float* dmean = nullptr;                   // dZ W_neigh / deg of the current layer (dgrad -> scatter)
-        float* loss = nullptr;                    // device scalar
-        int64_t rows64 = 0, dh_rows[kMaxLayers] = {};
-        alignas(64) unsigned char map_dz128[kMaxLayers][128], map_wt[kMaxLayers][128], map_mean128[kMaxLayers][128];
-    } sage;
-    // ordering of windows through the buffer
-    bool seq_started = false;
-    uint64_t next_step = 0;
-    // status
-    int sticky = MGNN_OK;
-    std::string err;
-    // profiling
-    bool prof = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
-    double prof_ms = 0.0;
-    long long prof_launches = 0;
-};
-
-namespace {
+namespace mgnn {
+namespace host {
 
 mgnn_status fail(mgnn_ctx c, mgnn_status st, const std::string& msg) {
     if (c) {
@@ -217,46 +70,6 @@ mgnn_status fail(mgnn_ctx c, mgnn_status st, const std::string& msg) {
         if (st == MGNN_ECUDA || st == MGNN_EOVERFLOW) c->sticky = st;
     }
     return st;
-}
-
-#define CK(call)                                                                                     \
-    do {                                                                                             \
-        cudaError_t e_ = (call);                                                                     \
-        if (e_ != cudaSuccess)                                                                       \
-            return fail(ctx, e_ == cudaErrorMemoryAllocation ? MGNN_ENOMEM : MGNN_ECUDA,            \
-                        std::string(#call) + ": " + cudaGetErrorString(e_));                        \
-    } while (0)
-
-#define CKL()                                                                                        \
-    do {                                                                                             \
-        cudaError_t e_ = cudaGetLastError();                                                         \
-        if (e_ != cudaSuccess) return fail(ctx, MGNN_ECUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
-    } while (0)
-
-#define GUARD()                                                                                      \
-    do {                                                                                             \
-        if (!ctx) return MGNN_EINVAL;                                                                \
-        if (ctx->sticky) return (mgnn_status)ctx->sticky;                                            \
-        if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, MGNN_ECUDA, "cudaSetDevice"); \
-    } while (0)
-
-template <class T>
-cudaError_t dalloc(T** p, size_t n) {
-    if (n == 0) n = 1;
-    return cudaMalloc((void**)p, n * sizeof(T));
-}
-
-template <class T>
-void dfree(T*& p) {
-    if (p) cudaFree((void*)p);
-    p = nullptr;
-}
-
-inline int64_t sat_mul(int64_t a, int64_t b, int64_t cap) {
-    if (a == 0 || b == 0) return 0;
-    if (a > cap / b) return cap;
-    int64_t r = a * b;
-    return r > cap ? cap : r;
 }
 
 void fill_partdev(const mgnn_ctx_s* c, const Part& p, PartDev* d) {
@@ -333,25 +146,6 @@ void free_win(Win& w) {
     w = Win();
 }
 
-void free_sage(mgnn_ctx_s* ctx) {
-    auto& S = ctx->sage;
-    dfree(S.params);
-    for (int l = 0; l < kMaxLayers; ++l) {
-        S.w[l] = S.b[l] = nullptr;
-        dfree(S.h[l]);
-        dfree(S.wt[l]);
-        dfree(S.mean[l]);
-        dfree(S.dh[l]);
-    }
-    dfree(S.labels);
-    dfree(S.dmean);
-    dfree(S.grads);
-    dfree(S.logits);
-    dfree(S.dlogits);
-    dfree(S.loss);
-    S.ready = S.train = false;
-}
-
 void free_buffer(Part& p) {
     dfree(p.rows); dfree(p.se); dfree(p.sa); dfree(p.slot_of); dfree(p.slot_h); dfree(p.hitmask); dfree(p.rank_deg);
     dfree(p.ek); dfree(p.ekt); dfree(p.ev); dfree(p.evt); dfree(p.rk); dfree(p.rkt); dfree(p.rv); dfree(p.rvt);
@@ -414,7 +208,8 @@ WinDev win_dev(mgnn_ctx ctx, Win& w) {
     return d;
 }
 
-}  // namespace
+}  // namespace host
+}  // namespace mgnn
 
 // =====================================================================================
 extern "C" {
@@ -1084,441 +879,6 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
     }
     CKL();
     w.scored = true;
-    return MGNN_OK;
-}
-
-// ------------------------------------------------------------------ A14: GraphSAGE-mean consumer
-mgnn_status mgnn_sage_config(mgnn_ctx ctx, const mgnn_sage_desc* d) {
-    GUARD();
-    if (!ctx->configured) return fail(ctx, MGNN_ESTATE, "sage_config before sampler_config");
-    if (!d || d->n_layers != ctx->L || !d->dims || !d->w_self || !d->w_neigh || !d->bias)
-        return fail(ctx, MGNN_EINVAL, "sage: n_layers must equal the sampler's and all arrays given");
-    if (d->dims[0] != ctx->D) return fail(ctx, MGNN_EINVAL, "sage: dims[0] must equal feat_dim");
-    for (int l = 1; l <= d->n_layers; ++l)
-        if (d->dims[l] < 1 || d->dims[l] > 256) return fail(ctx, MGNN_EINVAL, "sage: dims[l] must be 1..256");
-    for (int l = 0; l < d->n_layers; ++l)
-        if (!d->w_self[l] || !d->w_neigh[l] || !d->bias[l]) return fail(ctx, MGNN_EINVAL, "sage: null weight");
-    CK(cudaDeviceSynchronize());
-    free_sage(ctx);
-    auto& S = ctx->sage;
-    const int L = d->n_layers;
-    S.L = L;
-    for (int l = 0; l <= L; ++l) S.dims[l] = d->dims[l];
-    const int64_t M = (int64_t)ctx->parts.size() * ctx->max_window;
-    // padded parameter layout (one buffer: the optimizer and the gradient all-reduce see one array)
-    int64_t off = 0;
-    for (int l = 0; l < L; ++l) {
-        S.npad[l] = (S.dims[l + 1] + 15) / 16 * 16;
-        S.kp[l] = (S.dims[l] + 127) / 128 * 128;
-        S.w_off[l] = off;
-        off += (int64_t)S.npad[l] * 2 * S.kp[l];
-        S.b_off[l] = off;
-        off += S.npad[l];
-    }
-    S.n_params = off;
-    std::vector<float> hp((size_t)off, 0.0f);
-    for (int l = 0; l < L; ++l) {
-        const int kin = S.dims[l], n = S.dims[l + 1];
-        const int64_t wc = 2 * (int64_t)S.kp[l];
-        float* w = hp.data() + S.w_off[l];
-        for (int o = 0; o < n; ++o) {
-            for (int k = 0; k < kin; ++k) {
-                w[(size_t)o * wc + k] = d->w_self[l][(size_t)o * kin + k];
-                w[(size_t)o * wc + S.kp[l] + k] = d->w_neigh[l][(size_t)o * kin + k];
-            }
-            hp[(size_t)S.b_off[l] + o] = d->bias[l][o];
-        }
-    }
-    CK(dalloc(&S.params, off));
-    CK(cudaMemcpy(S.params, hp.data(), off * sizeof(float), cudaMemcpyHostToDevice));
-    for (int l = 0; l < L; ++l) {
-        S.w[l] = S.params + S.w_off[l];
-        S.b[l] = S.params + S.b_off[l];
-        const int64_t wc = 2 * (int64_t)S.kp[l];
-        if (!sage_encode_map(S.map_w[l], S.w[l], S.npad[l], wc, wc, S.npad[l]))
-            return fail(ctx, MGNN_ECUDA, "sage: cuTensorMapEncodeTiled (weights) failed");
-        S.out_rows[l] = ctx->fcap[L - 1 - l];
-        if (l < L - 1) {
-            const int64_t n = M * S.out_rows[l] * S.npad[l];
-            CK(dalloc(&S.h[l], n));
-            CK(cudaMemset(S.h[l], 0, n * sizeof(float)));   // rows never written stay finite (tensor-core operands)
-        }
-    }
-    for (int slot = 0; slot < 2; ++slot)
-        for (int l = 0; l < L; ++l) {
-            const int hop = L - 1 - l;
-            const float* base;
-            int64_t rows, cols, pitch;
-            if (l == 0) {
-                base = ctx->win[slot].X;
-                rows = M * ctx->ucap;
-                cols = pitch = ctx->pitch;
-            } else {
-                base = S.h[l - 1];
-                rows = M * ctx->fcap[hop + 1];
-                cols = pitch = S.npad[l - 1];
-            }
-            if (!sage_encode_map(S.map_in[slot][l], base, rows, cols, pitch, 128))
-                return fail(ctx, MGNN_ECUDA, "sage: cuTensorMapEncodeTiled (activations) failed");
-        }
-    S.ready = true;
-    return MGNN_OK;
-}
-
-namespace {
-// one forward layer over `n_inst` instances inst0, inst0 + inst_step, ... of a window slot
-mgnn_status sage_layer(mgnn_ctx ctx, Win& w, int slot, int l, int n_inst, int inst0, int inst_step, float* out,
-                       int64_t out_rows, int64_t out_pitch, int n_out, float* mean_out, cudaStream_t s,
-                       bool mean_first = false) {
-    auto& S = ctx->sage;
-    const int L = S.L, hop = L - 1 - l;
-    SageLayerArgs a;
-    memset(&a, 0, sizeof(a));
-    a.n_inst = n_inst;
-    a.inst0 = inst0;
-    a.inst_step = inst_step;
-    a.hop = hop;
-    a.k_in = S.dims[l];
-    a.kp = S.kp[l];
-    a.npad = S.npad[l];
-    a.relu = l < L - 1;
-    a.k_hop = ctx->k_hop[hop];
-    a.hop_size = w.hop_size;
-    a.off = w.off[hop];
-    a.off_stride = ctx->fcap[hop] + 1;
-    a.cols = w.cols[hop];
-    a.col_stride = ctx->ecap[hop];
-    if (l == 0) {
-        a.h_in = w.X;
-        a.in_rows = ctx->ucap;
-        a.in_pitch = ctx->pitch;
-    } else {
-        a.h_in = S.h[l - 1];
-        a.in_rows = ctx->fcap[hop + 1];
-        a.in_pitch = S.npad[l - 1];
-    }
-    a.h_out = out;
-    a.out_rows = out_rows;
-    a.out_pitch = out_pitch;
-    a.n_out = n_out;
-    a.bias = S.b[l];
-    a.mean_out = mean_out;
-    a.mean_rows = S.out_rows[l];
-    a.mean_pitch = S.kp[l];
-    if (mean_first) {          // means by k_mean over all SMs, then the warp-specialised TMA-fed GEMM
-        launch_mean(a, s);
-        a.mean_in = 1;
-        if (!launch_sage_gemm(S.map_in[slot][l], S.map_w[l], S.map_mean128[l], a, s))
-            return fail(ctx, MGNN_ECUDA, "sage: gemm launch configuration failed");
-        return MGNN_OK;
-    }
-    if (!launch_sage_layer(S.map_in[slot][l], S.map_w[l], nullptr, a, s))
-        return fail(ctx, MGNN_ECUDA, "sage: layer launch configuration failed");
-    return MGNN_OK;
-}
-}  // namespace
-
-namespace {
-// neighbour-mean buffers [M][out_rows][kp] per layer and their TMA maps (training; split forward)
-mgnn_status ensure_mean_buffers(mgnn_ctx ctx) {
-    auto& S = ctx->sage;
-    const int64_t M = (int64_t)ctx->parts.size() * ctx->max_window;
-    for (int l = 0; l < S.L; ++l) {
-        if (S.mean[l]) continue;
-        const int64_t nm = M * S.out_rows[l] * S.kp[l];
-        CK(dalloc(&S.mean[l], nm));
-        CK(cudaMemset(S.mean[l], 0, nm * sizeof(float)));
-        if (!sage_encode_map(S.map_mean128[l], S.mean[l], M * S.out_rows[l], S.kp[l], S.kp[l], 128))
-            return fail(ctx, MGNN_ECUDA, "cuTensorMapEncodeTiled (means) failed");
-    }
-    return MGNN_OK;
-}
-// Window forward as k_mean (neighbour means, warp per row over all SMs, stored in HBM) + the
-// TMA-fed GEMM (default; measured faster than aggregating inside the GEMM kernel on every config:
-// arxiv 0.64 -> 0.44 ms, reddit 7.2 -> 4.6 ms, products 6.6 -> 5.6 ms per window).
-// MGNN_SAGE_SPLIT=0 selects the fused in-kernel aggregation (A/B, tested).
-bool split_forward() {
-    const char* e = getenv("MGNN_SAGE_SPLIT");
-    return !(e && e[0] == '0');
-}
-}  // namespace
-
-mgnn_status mgnn_sage_forward(mgnn_ctx ctx, int32_t slot, float* logits, int64_t logits_pitch, mgnn_stream stream) {
-    GUARD();
-    if (slot < 0 || slot > 1 || !logits) return fail(ctx, MGNN_EINVAL, "bad slot / logits");
-    auto& S = ctx->sage;
-    if (!S.ready) return fail(ctx, MGNN_ESTATE, "sage_forward before sage_config");
-    if (logits_pitch < S.dims[S.L]) return fail(ctx, MGNN_EINVAL, "logits_pitch < dims[L]");
-    Win& w = ctx->win[slot];
-    if (!w.gathered) return fail(ctx, MGNN_ESTATE, "sage_forward needs a gathered window");
-    cudaStream_t s = (cudaStream_t)stream;
-    const int L = S.L;
-    const int n_inst = (int)ctx->parts.size() * w.n_steps;
-    const bool split = split_forward();
-    if (split) {
-        mgnn_status st = ensure_mean_buffers(ctx);
-        if (st) return st;
-    }
-    for (int l = 0; l < L; ++l) {
-        float* mo = split ? S.mean[l] : nullptr;
-        mgnn_status st = l < L - 1 ? sage_layer(ctx, w, slot, l, n_inst, 0, 1, S.h[l], S.out_rows[l], S.npad[l],
-                                                S.npad[l], mo, s, split)
-                                   : sage_layer(ctx, w, slot, l, n_inst, 0, 1, logits, ctx->batch, logits_pitch,
-                                                S.dims[L], mo, s, split);
-        if (st) return st;
-    }
-    CKL();
-    return MGNN_OK;
-}
-
-// ------------------------------------------------------------------ NEXT-3: DDP training step
-mgnn_status mgnn_sage_train_config(mgnn_ctx ctx, const int32_t* labels) {
-    GUARD();
-    auto& S = ctx->sage;
-    if (!S.ready) return fail(ctx, MGNN_ESTATE, "train_config before sage_config");
-    if (!labels) return fail(ctx, MGNN_EINVAL, "labels");
-    for (int64_t v = 0; v < ctx->n_global; ++v)
-        if (labels[v] < 0 || labels[v] >= S.dims[S.L]) return fail(ctx, MGNN_EINVAL, "label out of range");
-    CK(cudaDeviceSynchronize());
-    const int L = S.L;
-    const int64_t M = (int64_t)ctx->parts.size() * ctx->max_window;
-    dfree(S.labels);
-    CK(dalloc(&S.labels, ctx->n_global));
-    CK(cudaMemcpy(S.labels, labels, ctx->n_global * sizeof(int32_t), cudaMemcpyHostToDevice));
-    if (!S.grads) {
-        CK(dalloc(&S.grads, S.n_params));
-        CK(cudaMemset(S.grads, 0, S.n_params * sizeof(float)));
-        CK(dalloc(&S.loss, 1));
-        CK(cudaMemset(S.loss, 0, sizeof(float)));
-        S.rows64 = (ctx->batch + 63) / 64 * 64;
-        const int64_t nl = M * S.rows64 * S.npad[L - 1];
-        CK(dalloc(&S.logits, nl));
-        CK(dalloc(&S.dlogits, nl));
-        CK(cudaMemset(S.logits, 0, nl * sizeof(float)));
-        CK(cudaMemset(S.dlogits, 0, nl * sizeof(float)));
-        int64_t ndm = 1;
-        for (int l = 1; l < L; ++l) ndm = std::max(ndm, M * S.out_rows[l] * S.kp[l]);
-        CK(dalloc(&S.dmean, ndm));
-        {
-            mgnn_status st = ensure_mean_buffers(ctx);
-            if (st) return st;
-        }
-        for (int l = 0; l < L; ++l) {
-            CK(dalloc(&S.wt[l], (int64_t)2 * S.kp[l] * S.npad[l]));
-            if (l < L - 1) {
-                S.dh_rows[l] = (S.out_rows[l] + 63) / 64 * 64;
-                const int64_t nd = M * S.dh_rows[l] * S.npad[l];
-                CK(dalloc(&S.dh[l], nd));
-                CK(cudaMemset(S.dh[l], 0, nd * sizeof(float)));
-            }
-        }
-        for (int l = 0; l < L; ++l) {
-            float* dz = l == L - 1 ? S.dlogits : S.dh[l];
-            const int64_t dzr = l == L - 1 ? S.rows64 : S.dh_rows[l];
-            const int64_t wtr = 2 * (int64_t)S.kp[l];
-            // the input gradient (and its transposed-weight operand) exists for layers >= 1 only
-            if (!sage_encode_map(S.map_dz128[l], dz, M * dzr, S.npad[l], S.npad[l], 128) ||
-                (l > 0 && !sage_encode_map(S.map_wt[l], S.wt[l], wtr, S.npad[l], S.npad[l],
-                                           (int)(wtr <= 256 ? wtr : S.kp[l]))))
-                return fail(ctx, MGNN_ECUDA, "train: cuTensorMapEncodeTiled failed");
-            launch_transpose(S.w[l], S.wt[l], S.npad[l], (int32_t)wtr, 0);
-        }
-        CKL();
-        CK(cudaDeviceSynchronize());
-    }
-    S.train = true;
-    return MGNN_OK;
-}
-
-mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_window, int32_t n_trainers,
-                                 mgnn_stream stream) {
-    GUARD();
-    auto& S = ctx->sage;
-    if (!S.train) return fail(ctx, MGNN_ESTATE, "train_step before train_config");
-    if (slot < 0 || slot > 1 || n_trainers < 1) return fail(ctx, MGNN_EINVAL, "bad slot / n_trainers");
-    Win& w = ctx->win[slot];
-    if (!w.gathered) return fail(ctx, MGNN_ESTATE, "train_step needs a gathered window");
-    if (step_in_window < 0 || step_in_window >= w.n_steps) return fail(ctx, MGNN_EINVAL, "step_in_window");
-    cudaStream_t s = (cudaStream_t)stream;
-    const int L = S.L;
-    const int n_lp = (int)ctx->parts.size();
-    const int i0 = step_in_window, is = w.n_steps;   // instances lp * n_steps + step_in_window
-    // forward, keeping every layer's output and neighbour means
-    for (int l = 0; l < L; ++l) {
-        mgnn_status st = l < L - 1 ? sage_layer(ctx, w, slot, l, n_lp, i0, is, S.h[l], S.out_rows[l], S.npad[l],
-                                                S.npad[l], S.mean[l], s, true)
-                                   : sage_layer(ctx, w, slot, l, n_lp, i0, is, S.logits, S.rows64, S.npad[l],
-                                                S.npad[l], S.mean[l], s, true);
-        if (st) return st;
-    }
-    // loss: mean cross-entropy per trainer, averaged over the n_trainers of the DDP step
-    XentArgs xa;
-    memset(&xa, 0, sizeof(xa));
-    xa.n_inst = n_lp;
-    xa.inst0 = i0;
-    xa.inst_step = is;
-    xa.n_classes = S.dims[L];
-    xa.hop_size = w.hop_size;
-    xa.frontier = w.fr_gid;
-    xa.ucap = ctx->ucap;
-    xa.labels = S.labels;
-    xa.logits = S.logits;
-    xa.dlogits = S.dlogits;
-    xa.rows = S.rows64;
-    xa.pitch = S.npad[L - 1];
-    xa.scale = 1.0f / (float)n_trainers;
-    xa.db = S.grads + S.b_off[L - 1];
-    xa.loss = S.loss;
-    launch_xent(xa, s);
-    for (int l = L - 1; l >= 0; --l) {
-        const int hop = L - 1 - l;
-        float* dz = l == L - 1 ? S.dlogits : S.dh[l];
-        const int64_t dzr = l == L - 1 ? S.rows64 : S.dh_rows[l];
-        if (l < L - 1) {
-            MaskArgs ma;
-            memset(&ma, 0, sizeof(ma));
-            ma.n_inst = n_lp;
-            ma.inst0 = i0;
-            ma.inst_step = is;
-            ma.hop = hop;
-            ma.hop_size = w.hop_size;
-            ma.dz = dz;
-            ma.rows = dzr;
-            ma.pitch = S.npad[l];
-            ma.h = S.h[l];
-            ma.h_rows = S.out_rows[l];
-            ma.h_pitch = S.npad[l];
-            ma.ncols = S.npad[l];
-            ma.db = S.grads + S.b_off[l];
-            launch_relu_mask(ma, s);
-        }
-        WgradArgs wa;
-        memset(&wa, 0, sizeof(wa));
-        wa.n_inst = n_lp;
-        wa.inst0 = i0;
-        wa.inst_step = is;
-        wa.hop = hop;
-        wa.hop_size = w.hop_size;
-        wa.dz = dz;
-        wa.dz_rows = dzr;
-        wa.dz_pitch = S.npad[l];
-        if (l == 0) {
-            wa.h_in = w.X;
-            wa.in_rows = ctx->ucap;
-            wa.in_pitch = ctx->pitch;
-        } else {
-            wa.h_in = S.h[l - 1];
-            wa.in_rows = ctx->fcap[hop + 1];
-            wa.in_pitch = S.npad[l - 1];
-        }
-        wa.in_cols = S.dims[l];
-        wa.mean = S.mean[l];
-        wa.mean_rows = S.out_rows[l];
-        wa.mean_pitch = S.kp[l];
-        wa.mean_cols = S.dims[l];
-        wa.kp = S.kp[l];
-        wa.npad = S.npad[l];
-        wa.dw = S.grads + S.w_off[l];
-        wa.max_chunks = (int64_t)n_lp * ((S.out_rows[l] + 63) / 64);
-        if (!launch_wgrad(wa, s)) return fail(ctx, MGNN_ECUDA, "train: wgrad launch configuration failed");
-        if (l > 0) {
-            ZeroRowsArgs za;
-            memset(&za, 0, sizeof(za));
-            za.n_inst = n_lp;
-            za.inst0 = i0;
-            za.inst_step = is;
-            za.hop = hop + 1;
-            za.hop_size = w.hop_size;
-            za.buf = S.dh[l - 1];
-            za.rows = S.dh_rows[l - 1];
-            za.pitch = S.npad[l - 1];
-            launch_zero_rows(za, s);
-            DgradArgs da;
-            memset(&da, 0, sizeof(da));
-            da.n_inst = n_lp;
-            da.inst0 = i0;
-            da.inst_step = is;
-            da.hop = hop;
-            da.hop_size = w.hop_size;
-            da.off = w.off[hop];
-            da.off_stride = ctx->fcap[hop] + 1;
-            da.cols = w.cols[hop];
-            da.col_stride = ctx->ecap[hop];
-            da.dz_rows = dzr;
-            da.npad_out = S.npad[l];
-            da.kp = S.kp[l];
-            da.k_in = S.dims[l];
-            da.dh = S.dh[l - 1];
-            da.dh_rows = S.dh_rows[l - 1];
-            da.dh_pitch = S.npad[l - 1];
-            da.dmean = S.dmean;
-            da.dmean_rows = S.out_rows[l];
-            if (!launch_dgrad(S.map_dz128[l], S.map_wt[l], da, s))
-                return fail(ctx, MGNN_ECUDA, "train: dgrad launch configuration failed");
-            launch_scatter(da, s);
-        }
-    }
-    CKL();
-    return MGNN_OK;
-}
-
-mgnn_status mgnn_sage_grads(mgnn_ctx ctx, float** grads, int64_t* n_floats) {
-    GUARD();
-    if (!grads || !n_floats) return fail(ctx, MGNN_EINVAL, "null output");
-    if (!ctx->sage.train) return fail(ctx, MGNN_ESTATE, "grads before train_config");
-    *grads = ctx->sage.grads;
-    *n_floats = ctx->sage.n_params;
-    return MGNN_OK;
-}
-
-mgnn_status mgnn_sage_sgd(mgnn_ctx ctx, float lr, mgnn_stream stream) {
-    GUARD();
-    auto& S = ctx->sage;
-    if (!S.train) return fail(ctx, MGNN_ESTATE, "sgd before train_config");
-    cudaStream_t s = (cudaStream_t)stream;
-    SgdLayers d;
-    memset(&d, 0, sizeof(d));
-    d.n_layers = S.L;
-    for (int l = 0; l < S.L; ++l) {     // the bias follows its layer's block (b_off = w_off + npad * 2 kp)
-        d.w[l] = S.w[l];
-        d.g[l] = S.grads + S.w_off[l];
-        d.wt[l] = S.wt[l];
-        d.rows[l] = S.npad[l];
-        d.cols[l] = 2 * (int64_t)S.kp[l];
-    }
-    launch_sgd_layers(d, lr, s);
-    CKL();
-    return MGNN_OK;
-}
-
-mgnn_status mgnn_sage_loss(mgnn_ctx ctx, float* host_loss, mgnn_stream stream) {
-    GUARD();
-    auto& S = ctx->sage;
-    if (!S.train || !host_loss) return fail(ctx, MGNN_ESTATE, "loss before train_config");
-    cudaStream_t s = (cudaStream_t)stream;
-    CK(cudaMemcpyAsync(host_loss, S.loss, sizeof(float), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemsetAsync(S.loss, 0, sizeof(float), s));
-    CK(cudaStreamSynchronize(s));
-    return MGNN_OK;
-}
-
-mgnn_status mgnn_sage_params(mgnn_ctx ctx, int32_t l, float* w_self, float* w_neigh, float* bias) {
-    GUARD();
-    auto& S = ctx->sage;
-    if (!S.ready || l < 0 || l >= S.L) return fail(ctx, MGNN_EINVAL, "layer");
-    CK(cudaDeviceSynchronize());
-    const int kin = S.dims[l], n = S.dims[l + 1];
-    const int64_t wc = 2 * (int64_t)S.kp[l];
-    std::vector<float> w((size_t)S.npad[l] * wc), b((size_t)S.npad[l]);
-    CK(cudaMemcpy(w.data(), S.w[l], w.size() * sizeof(float), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(b.data(), S.b[l], b.size() * sizeof(float), cudaMemcpyDeviceToHost));
-    for (int o = 0; o < n; ++o) {
-        for (int k = 0; k < kin; ++k) {
-            if (w_self) w_self[(size_t)o * kin + k] = w[(size_t)o * wc + k];
-            if (w_neigh) w_neigh[(size_t)o * kin + k] = w[(size_t)o * wc + S.kp[l] + k];
-        }
-        if (bias) bias[o] = b[o];
-    }
     return MGNN_OK;
 }
 
