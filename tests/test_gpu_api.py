@@ -155,3 +155,59 @@ def test_kernel_profile_and_launch_count(graph):
     assert "launch_gather" in report and "launch_hop" in report
     assert ctx.launch_count() - n0 >= 8
     ctx.close()
+
+
+def test_consumer_training_remote_call_order_and_arguments(graph):
+    """Status codes of the consumer (A14), training (NEXT-3) and remote-expansion (NEXT-1) calls."""
+    ctx = _ctx(graph)
+    dims = synth.sage_dims(64, 2, 16)
+    wts = synth.sage_weights(dims)
+    logits = torch.zeros((8, 256, 16), device="cuda")
+    with pytest.raises(MgnnError) as e:                       # forward before sage_config
+        ctx.sage_forward(0, logits)
+    assert _status(e) == ESTATE
+    with pytest.raises(MgnnError) as e:                       # remote expansion after sampler_config
+        ctx.expand_remote(True)
+    assert _status(e) == ESTATE
+    with pytest.raises(MgnnError) as e:                       # a hidden width above 256
+        ctx.sage_config([64, 300, 16], *[[w[i] for w in synth.sage_weights([64, 300, 16])] for i in range(3)])
+    assert _status(e) == EINVAL
+    with pytest.raises(MgnnError) as e:                       # dims[0] != feat_dim
+        ctx.sage_config([32, 128, 16], *[[w[i] for w in synth.sage_weights([32, 128, 16])] for i in range(3)])
+    assert _status(e) == EINVAL
+    ctx.sage_config(dims, [w[0] for w in wts], [w[1] for w in wts], [w[2] for w in wts])
+    ctx.sample(0, 1, 4)
+    with pytest.raises(MgnnError) as e:                       # forward before the window is gathered
+        ctx.sage_forward(0, logits)
+    assert _status(e) == ESTATE
+    ctx.lookup_gather(0)
+    with pytest.raises(MgnnError) as e:                       # logits pitch below the class count
+        ctx.sage_forward(0, torch.zeros((8, 256, 8), device="cuda"))
+    assert _status(e) == EINVAL
+    ctx.sage_forward(0, logits)
+    with pytest.raises(MgnnError) as e:                       # training step before train_config
+        ctx.train_step(0, 0, 2)
+    assert _status(e) == ESTATE
+    with pytest.raises(MgnnError) as e:                       # a label outside [0, C)
+        ctx.train_config(np.full(graph.n_nodes, 16, np.int32))
+    assert _status(e) == EINVAL
+    ctx.train_config(synth.node_labels(graph.n_nodes, 16))
+    with pytest.raises(MgnnError) as e:                       # step beyond the window
+        ctx.train_step(0, 4, 2)
+    assert _status(e) == EINVAL
+    ctx.train_step(0, 0, 2)
+    ctx.sgd(0.01)
+    assert np.isfinite(ctx.loss())
+    ctx.score(0)
+    ctx.close()
+    # dense scores must precede partition loading; remote expansion needs the global CSR when
+    # other partitions live in other contexts
+    parts = synth.partition(graph, 2)
+    c2 = PL.build_context(0, parts, 64, synth.FEAT_SEED, hosted=[0])
+    with pytest.raises(MgnnError) as e:
+        c2._chk("mgnn_ctx_set_dense_scores", c2.L.mgnn_ctx_set_dense_scores(c2._h, 1))
+    assert _status(e) == ESTATE
+    with pytest.raises(MgnnError) as e:
+        c2.expand_remote(True)
+    assert _status(e) == ESTATE
+    c2.close()
