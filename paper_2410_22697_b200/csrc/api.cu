@@ -657,7 +657,7 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
     ctx->vp_max = 1;
     for (auto& p : ctx->parts) ctx->vp_max = std::max(ctx->vp_max, p.n_local + p.n_h);
     if (ctx->remote) ctx->vp_max = std::max<int64_t>(1, ctx->n_global);   // ranks are global ids (NEXT-1)
-    ctx->bm_words = (ctx->vp_max + 31) / 32;
+    ctx->bm_words = ((ctx->vp_max + 31) / 32 + 3) / 4 * 4;   // multiple of 4: 16-byte bitmap loads
     const int64_t big = (int64_t)1 << 40;
     ctx->fcap[0] = std::min<int64_t>(batch, ctx->vp_max);
     for (int i = 0; i < n_layers; ++i) {

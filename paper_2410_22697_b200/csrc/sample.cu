@@ -30,7 +30,8 @@ namespace mgnn {
 
 constexpr int kThreads = 256;
 constexpr int kHopTileMin = 64;        // frontier nodes per k_hop tile: 64 or 256
-constexpr int kWordTile = kThreads;    // bitmap words per k_compact tile (one per thread)
+constexpr int kCWords = 4;             // bitmap words per k_compact thread (one 16-byte load)
+constexpr int kWordTile = kThreads * kCWords;   // bitmap words per k_compact tile
 
 int64_t scan_tiles_count(int64_t fcap) { return (fcap + kHopTileMin - 1) / kHopTileMin; }
 int64_t scan_tiles_words(int64_t words) { return (words + kWordTile - 1) / kWordTile; }
@@ -233,31 +234,46 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
     const uint32_t* nb = W.nb + ((int64_t)m * W.L + hop) * W.bm_words;
     int32_t* wpre = W.wpre + ((int64_t)m * W.L + hop) * W.bm_words;
     uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
-    const int64_t wd = (int64_t)tile * kWordTile + threadIdx.x;
-    uint32_t b = (wd < nwords) ? nb[wd] : 0u;
+    const int64_t wd0 = (int64_t)tile * kWordTile + (int64_t)threadIdx.x * kCWords;   // 4 consecutive words
+    uint32_t b[kCWords] = {0u, 0u, 0u, 0u};
+    if (wd0 + kCWords <= nwords) {
+        const uint4 v = *reinterpret_cast<const uint4*>(nb + wd0);      // bm_words is a multiple of 4
+        b[0] = v.x; b[1] = v.y; b[2] = v.z; b[3] = v.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < kCWords; ++j) b[j] = wd0 + j < nwords ? nb[wd0 + j] : 0u;
+    }
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < kCWords; ++j) cnt += __popc(b[j]);
     long long agg;
-    const long long excl = block_excl_scan256(__popc(b), sm, &agg);
+    const long long excl = block_excl_scan256(cnt, sm, &agg);
     int64_t* hs = W.hop_size + (int64_t)m * (kMaxLayers + 1);
     if (threadIdx.x < 32) {
-            const unsigned long long pv = lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
-                                                                     (unsigned long long)agg);
-            if (threadIdx.x == 0) prefix_sh = (long long)pv;
-        }
+        const unsigned long long pv = lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
+                                                         (unsigned long long)agg);
+        if (threadIdx.x == 0) prefix_sh = (long long)pv;
+    }
     __syncthreads();
     const int64_t nF = hs[hop];
     int64_t pos = nF + prefix_sh + excl;
-    // new_i keeps its bitmap; with the word's first position it gives every new node's frontier
-    // position as wpre + popc(lower bits) (k_relabel), without a scattered rank -> position table
-    if (wd < nwords) wpre[wd] = (int32_t)pos;
-    if (b) fb[wd] |= b;
     int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
-    while (b) {
-        const int bi = __ffs(b) - 1;
-        b &= b - 1;
-        const int32_t r = (int32_t)(wd * 32 + bi);
-        MGNN_CHECK(pos < W.ucap && r < (W.remote ? W.n_global : pd.vp), "compact pos=%lld r=%d", (long long)pos, r);
-        fr[pos] = r;
-        ++pos;
+#pragma unroll
+    for (int j = 0; j < kCWords; ++j) {
+        const int64_t wd = wd0 + j;
+        uint32_t bb = b[j];
+        // new_i keeps its bitmap; with the word's first position it gives every new node's frontier
+        // position as wpre + popc(lower bits) (k_relabel), without a scattered rank -> position table
+        if (wd < nwords) wpre[wd] = (int32_t)pos;
+        if (bb) fb[wd] |= bb;
+        while (bb) {
+            const int bi = __ffs(bb) - 1;
+            bb &= bb - 1;
+            const int32_t r = (int32_t)(wd * 32 + bi);
+            MGNN_CHECK(pos < W.ucap && r < (W.remote ? W.n_global : pd.vp), "compact pos=%lld r=%d", (long long)pos, r);
+            fr[pos] = r;
+            ++pos;
+        }
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) hs[hop + 1] = nF + prefix_sh + agg;
 }
