@@ -159,12 +159,11 @@ mgnn_status sage_layer(mgnn_ctx ctx, Win& w, int slot, int l, int n_inst, int in
     a.mean_pitch = S.kp[l];
     if (mean_first) {          // means by k_mean over all SMs, then the warp-specialised TMA-fed GEMM
         launch_mean(a, s);
-        a.mean_in = 1;
         if (!launch_sage_gemm(S.map_in[slot][l], S.map_w[l], S.map_mean128[l], a, s))
             return fail(ctx, MGNN_ECUDA, "sage: gemm launch configuration failed");
         return MGNN_OK;
     }
-    if (!launch_sage_layer(S.map_in[slot][l], S.map_w[l], nullptr, a, s))
+    if (!launch_sage_layer(S.map_in[slot][l], S.map_w[l], a, s))
         return fail(ctx, MGNN_ECUDA, "sage: layer launch configuration failed");
     return MGNN_OK;
 }

@@ -167,12 +167,10 @@ struct SageLayerArgs {
     int32_t inst0, inst_step;  // kernel instance k is window instance inst0 + k * inst_step
     float* mean_out;           // optional [M][mean_rows][mean_pitch]: neighbour means (training)
     int64_t mean_rows, mean_pitch;
-    int32_t mean_in;           // 1: the means are already in mean_out (k_mean); TMA them, no aggregation
     int32_t b_resident;        // k_sage_gemm: all weight chunks stay in shared memory (set by the launcher)
 };
 bool sage_encode_map(void* map_out, const float* base, int64_t rows, int64_t cols, int64_t pitch, int box_rows);
-bool launch_sage_layer(const void* map_in, const void* map_w, const void* map_mean, const SageLayerArgs& a,
-                       cudaStream_t s);
+bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArgs& a, cudaStream_t s);
 // out = act([H_in | mean] Wcat^T + b) with the means precomputed (warp-specialised, TMA + tcgen05)
 bool launch_sage_gemm(const void* map_in, const void* map_w, const void* map_mean, const SageLayerArgs& a,
                       cudaStream_t s);
@@ -255,7 +253,6 @@ bool launch_dgrad(const void* map_dz, const void* map_wt, const DgradArgs& a, cu
 void launch_scatter(const DgradArgs& a, cudaStream_t s);
 
 // W <- W - lr * g, g <- 0, and the transposed copy Wt[c][o] = W[o][c] (dgrad operand)
-void launch_sgd(float* w, float* g, int64_t n, float lr, cudaStream_t s);
 struct SgdLayers {             // per layer: Wcat [rows][cols] followed by the bias [rows]; Wt [cols][rows]
     int32_t n_layers;
     float* w[kMaxLayers];

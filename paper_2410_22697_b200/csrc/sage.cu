@@ -53,7 +53,7 @@ constexpr int kMaxInst = 1024;
 
 __global__ void __launch_bounds__(kSageThreads, kCtasPerSm)
     k_sage_layer(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_w,
-                 const __grid_constant__ CUtensorMap map_mean, SageLayerArgs a) {
+                 SageLayerArgs a) {
     extern __shared__ __align__(1024) unsigned char dsm[];
     __shared__ __align__(8) uint64_t bar_self, bar_mma, bar_full[kMaxStages], bar_empty[kMaxStages];
     __shared__ uint32_t tmem_base_sh;
@@ -160,14 +160,10 @@ __global__ void __launch_bounds__(kSageThreads, kCtasPerSm)
             }
             if (warp == kCtlWarp) {
                 if (lane == 0) {
-                    mb_expect_tx(&bar_self, (uint32_t)(a.mean_in ? 2 : 1) * nch * kChunkBytesA);
+                    mb_expect_tx(&bar_self, (uint32_t)nch * kChunkBytesA);
                     for (int j = 0; j < nch; ++j)
                         tma_load_2d(a_self + j * kChunkBytesA, &map_in, col0 + j * kChunkCols, (int)(in_base + row0),
                                     &bar_self);
-                    if (a.mean_in)        // neighbour means precomputed (k_mean): the A_neigh panel by TMA too
-                        for (int j = 0; j < nch; ++j)
-                            tma_load_2d(a_neigh + j * kChunkBytesA, &map_mean, col0 + j * kChunkCols,
-                                        (int)((int64_t)m * a.mean_rows + row0), &bar_self);
                     // the panel's first weight chunks load while the warps aggregate (their stages
                     // were released by the previous panel's MMAs, complete once bar_mma fired)
                     const int nk = 2 * nch;
@@ -182,7 +178,7 @@ __global__ void __launch_bounds__(kSageThreads, kCtasPerSm)
                     }
                 }
                 __syncwarp();
-            } else if (!a.mean_in) {
+            } else {
                 // neighbour means of panel columns [col0, col0 + 32*nch): lane covers the 16-byte
                 // unit lane8 of each chunk g, i.e. columns col0 + 32 g + 4 lane8 .. +3.
                 // Edge-balanced, deterministic: the tile's edges (grouped by dst row, in CSR order)
@@ -271,7 +267,7 @@ __global__ void __launch_bounds__(kSageThreads, kCtasPerSm)
             tc_fence_before();
             named_sync(1, kSageThreads);
             tc_fence_after();
-            if (a.mean_out && !a.mean_in && warp < kAggWarps) {
+            if (a.mean_out && warp < kAggWarps) {
                 // training: keep the neighbour means for the weight gradient (read by tcgen05 too)
                 float* mo = a.mean_out + ((int64_t)m * a.mean_rows + row0) * a.mean_pitch + col0;
                 for (int u = threadIdx.x; u < nch * kTileM * 8; u += kAggWarps * 32) {
@@ -393,8 +389,7 @@ static size_t smem_fixed(int n_inst, int k_hop) {
 constexpr size_t kSmemPerCta = (228 * 1024) / kCtasPerSm - 2048;   // per CTA, minus reserved + static
 
 
-bool launch_sage_layer(const void* map_in, const void* map_w, const void* map_mean, const SageLayerArgs& args_in,
-                       cudaStream_t s) {
+bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArgs& args_in, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         int optin = 0, dev0 = 0;
@@ -432,8 +427,7 @@ bool launch_sage_layer(const void* map_in, const void* map_w, const void* map_me
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     CUtensorMap mi = *(const CUtensorMap*)map_in, mw = *(const CUtensorMap*)map_w;
-    CUtensorMap mm = *(const CUtensorMap*)(map_mean ? map_mean : map_in);
-    launch_k(k_sage_layer, dim3(kCtasPerSm * sms), dim3(kSageThreads), smem, s, mi, mw, mm, a);
+    launch_k(k_sage_layer, dim3(kCtasPerSm * sms), dim3(kSageThreads), smem, s, mi, mw, a);
     count_launches(1, __func__, s);
     return true;
 }

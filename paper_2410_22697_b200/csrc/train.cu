@@ -12,7 +12,7 @@
 //   k_dgrad     : [dZ W_self | dZ W_neigh] per 128-row tile (tcgen05, K-major, transposed
 //                 weights); the epilogue stores dZ W_self into dH and dZ W_neigh / deg into dmean
 //   k_scatter   : dmean rows added to the sampled neighbours' dH rows (warp per row, atomics)
-//   k_sgd, k_transpose : the optimizer step and the dgrad operand layout
+//   k_sgd_layers, k_transpose : the optimizer step and the dgrad operand layout
 // Gradient reductions use fp32 atomics (order-dependent rounding; the parity bound of the
 // training step is stated in DESIGN.md §7.2).
 #include <algorithm>
@@ -467,14 +467,6 @@ __global__ void __launch_bounds__(kT) k_mean(SageLayerArgs a) {
 }
 
 // ------------------------------------------------------------------ optimizer
-__global__ void __launch_bounds__(kT) k_sgd(float* __restrict__ w, float* __restrict__ g, int64_t n, float lr) {
-    pdl_enter();
-    for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
-        w[i] = __fsub_rn(w[i], __fmul_rn(lr, g[i]));
-        g[i] = 0.0f;
-    }
-}
-
 // SGD over every layer's [W_self | W_neigh] block (and bias) in one launch, also refreshing the
 // transposed copy the input-gradient GEMM reads
 __global__ void __launch_bounds__(kT) k_sgd_layers(SgdLayers d, float lr) {
@@ -580,12 +572,6 @@ void launch_scatter(const DgradArgs& a, cudaStream_t s) {
 
 void launch_mean(const SageLayerArgs& a, cudaStream_t s) {
     launch_k(k_mean, dim3(128, a.n_inst), dim3(kT), 0, s, a);
-    count_launches(1, __func__, s);
-}
-
-void launch_sgd(float* w, float* g, int64_t n, float lr, cudaStream_t s) {
-    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kT - 1) / kT, 148 * 8));
-    launch_k(k_sgd, dim3(gx), dim3(kT), 0, s, w, g, n, lr);
     count_launches(1, __func__, s);
 }
 
