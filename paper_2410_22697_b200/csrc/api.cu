@@ -139,7 +139,6 @@ void free_win(Win& w) {
     }
     dfree(w.X);
     dfree(w.pos_of);
-    dfree(w.wpre);
     dfree(w.zero);
     dfree(w.ext_seeds);
     dfree(w.ext_counts);
@@ -197,7 +196,6 @@ WinDev win_dev(mgnn_ctx ctx, Win& w) {
     d.pos_of = w.pos_of;
     d.fb = w.fb;
     d.nb = w.nb;
-    d.wpre = w.wpre;
     d.parts = ctx->d_parts;
     d.err = ctx->d_err;
     d.gathered_rows = ctx->d_gathered;
@@ -678,7 +676,6 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
         }
         CK(dalloc(&w.X, (size_t)M * ctx->ucap * ctx->pitch));
         CK(dalloc(&w.pos_of, M * ctx->vp_max));
-        CK(dalloc(&w.wpre, M * n_layers * ctx->bm_words));
         CK(dalloc(&w.ext_seeds, M * batch));
         CK(dalloc(&w.ext_counts, M));
         // zero region: [tile counters | status words | counts | fb | per-hop new-node bitmaps]
@@ -691,7 +688,7 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
         size_t off_cnt = off_st + ((st_words * 8 + 255) / 256) * 256;
         size_t off_fb = off_cnt + (((size_t)M * 8 * 8 + 255) / 256) * 256;
         size_t off_nb = off_fb + (((size_t)M * ctx->bm_words * 4 + 255) / 256) * 256;
-        size_t total = off_nb + (size_t)M * n_layers * ctx->bm_words * 4;
+        size_t total = off_nb + (size_t)M * n_layers * ctx->bm_words * 8;   // (bits, position) pairs
         CK(dalloc(&w.zero, total));
         CK(cudaMemset(w.zero, 0, total));
         w.zero_bytes = total;

@@ -52,8 +52,7 @@ struct Win {
     int32_t* cols[kMaxLayers] = {};
     float* X = nullptr;
     int32_t* pos_of = nullptr;
-    uint32_t* nb = nullptr;         // [M][L][bm_words] new-node bitmap of each hop (in the zero region)
-    int32_t* wpre = nullptr;        // [M][L][bm_words] frontier position of each word's first new node
+    uint32_t* nb = nullptr;         // [M][L][bm_words][2] new-node bits + word positions (zero region)
     char* zero = nullptr;           // [scan scratch | counts | fb], zeroed per window
     size_t zero_bytes = 0;
     unsigned long long* status = nullptr;

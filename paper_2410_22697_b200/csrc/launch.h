@@ -39,8 +39,8 @@ struct WinDev {
     long long* counts;                   // [M][8]
     int32_t* pos_of;                     // [M][vp_stride]
     uint32_t* fb;                        // [M][bm_words] frontier membership
-    uint32_t* nb;                        // [M][L][bm_words] new-node bitmap of hop i (new_i, R#7)
-    int32_t* wpre;                       // [M][L][bm_words] position in F_{i+1} of word's first new node
+    uint32_t* nb;                        // [M][L][bm_words][2]: new_i bits of hop i (R#7) and the position
+                                         // in F_{i+1} of the word's first new node (one 8-byte pair)
     const int32_t* ext_seeds;            // [M][batch] or nullptr
     const int32_t* ext_counts;           // [M]
     const PartDev* parts;                // [n_parts_local]

@@ -19,8 +19,8 @@
 //               unless already in F_i.
 //   k_compact : the bitmap in rank order IS the ascending-id order, so a
 //               popcount scan appends sorted_unique(cols_i) \ F_i to the
-//               frontier (R#7) and keeps, per bitmap word, the frontier
-//               position of its first new node.
+//               frontier (R#7) and keeps, beside each bitmap word, the
+//               frontier position of its first new node (one 8-byte pair).
 // After the last hop k_relabel rewrites the sampled columns as positions in
 // F_{i+1} (the DGL block layout the consumer indexes X with): a new node's
 // position is its word's position + popc of the lower bits of new_j.
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
         if (tile == 0 && threadIdx.x == 0) off[0] = 0;
         int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop] + o_tile;
         const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
-        uint32_t* nb = W.nb + ((int64_t)m * W.L + hop) * W.bm_words;
+        uint32_t* nb = W.nb + ((int64_t)m * W.L + hop) * W.bm_words * 2;   // (bits, first position) pairs
         const int32_t* __restrict__ crank = W.remote ? W.g_cols : pd.cols_rank;
     #pragma unroll 4
         for (int e = threadIdx.x; e < (int)agg; e += kThreads) {
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
                        o_tile + e, c);
             cols[e] = c;
             const uint32_t bit = 1u << (c & 31);
-            if (!(fb[c >> 5] & bit)) atomicOr(&nb[c >> 5], bit);
+            if (!(fb[c >> 5] & bit)) atomicOr(&nb[2 * (c >> 5)], bit);
         }
         __syncthreads();
     }
@@ -231,17 +231,17 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
     const int64_t ntiles = (nwords + kWordTile - 1) / kWordTile;
     const int tile = claim_tile(sc.tilectr + m, &tslot);
     if (tile >= ntiles) return;
-    const uint32_t* nb = W.nb + ((int64_t)m * W.L + hop) * W.bm_words;
-    int32_t* wpre = W.wpre + ((int64_t)m * W.L + hop) * W.bm_words;
+    uint32_t* nbp = W.nb + ((int64_t)m * W.L + hop) * W.bm_words * 2;   // word w: nbp[2w] bits, nbp[2w+1] position
     uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
     const int64_t wd0 = (int64_t)tile * kWordTile + (int64_t)threadIdx.x * kCWords;   // 4 consecutive words
     uint32_t b[kCWords] = {0u, 0u, 0u, 0u};
-    if (wd0 + kCWords <= nwords) {
-        const uint4 v = *reinterpret_cast<const uint4*>(nb + wd0);      // bm_words is a multiple of 4
-        b[0] = v.x; b[1] = v.y; b[2] = v.z; b[3] = v.w;
+    if (wd0 + kCWords <= nwords) {       // 4 (bits, position) pairs: two 16-byte loads (bm_words % 4 == 0)
+        const uint4 v0 = *reinterpret_cast<const uint4*>(nbp + 2 * wd0);
+        const uint4 v1 = *reinterpret_cast<const uint4*>(nbp + 2 * wd0 + 4);
+        b[0] = v0.x; b[1] = v0.z; b[2] = v1.x; b[3] = v1.z;
     } else {
 #pragma unroll
-        for (int j = 0; j < kCWords; ++j) b[j] = wd0 + j < nwords ? nb[wd0 + j] : 0u;
+        for (int j = 0; j < kCWords; ++j) b[j] = wd0 + j < nwords ? nbp[2 * (wd0 + j)] : 0u;
     }
     int cnt = 0;
 #pragma unroll
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
         uint32_t bb = b[j];
         // new_i keeps its bitmap; with the word's first position it gives every new node's frontier
         // position as wpre + popc(lower bits) (k_relabel), without a scattered rank -> position table
-        if (wd < nwords) wpre[wd] = (int32_t)pos;
+        if (wd < nwords) nbp[2 * wd + 1] = (uint32_t)pos;
         if (bb) fb[wd] |= bb;
         while (bb) {
             const int bi = __ffs(bb) - 1;
@@ -288,8 +288,8 @@ __device__ __forceinline__ int32_t frontier_pos(const WinDev& W, int m, int hop,
     const uint32_t bit = 1u << (c & 31);
     for (int j = hop; j >= 0; --j) {
         const int64_t o = ((int64_t)m * W.L + j) * W.bm_words + wd;
-        const uint32_t b = __ldg(W.nb + o);
-        if (b & bit) return __ldg(W.wpre + o) + __popc(b & (bit - 1u));
+        const uint2 bp = __ldg(reinterpret_cast<const uint2*>(W.nb) + o);   // bits and position: one load
+        if (bp.x & bit) return (int32_t)bp.y + __popc(bp.x & (bit - 1u));
     }
     return posof[c];
 }
