@@ -31,6 +31,12 @@ void free_sage(mgnn_ctx_s* ctx) {
     dfree(S.logits);
     dfree(S.dlogits);
     dfree(S.loss);
+    if (S.side) {
+        cudaStreamDestroy(S.side);
+        for (auto& e : S.ev_fork) cudaEventDestroy(e);
+        cudaEventDestroy(S.ev_join);
+        S.side = nullptr;
+    }
     S.ready = S.train = false;
 }
 
@@ -241,6 +247,9 @@ mgnn_status mgnn_sage_train_config(mgnn_ctx ctx, const int32_t* labels) {
         CK(cudaMemset(S.grads, 0, S.n_params * sizeof(float)));
         CK(dalloc(&S.loss, 1));
         CK(cudaMemset(S.loss, 0, sizeof(float)));
+        CK(cudaStreamCreateWithFlags(&S.side, cudaStreamNonBlocking));
+        for (auto& e : S.ev_fork) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&S.ev_join, cudaEventDisableTiming));
         S.rows64 = (ctx->batch + 63) / 64 * 64;
         const int64_t nl = M * S.rows64 * S.npad[L - 1];
         CK(dalloc(&S.logits, nl));
@@ -371,7 +380,11 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
         wa.npad = S.npad[l];
         wa.dw = S.grads + S.w_off[l];
         wa.max_chunks = (int64_t)n_lp * ((S.out_rows[l] + 63) / 64);
-        if (!launch_wgrad(wa, s)) return fail(ctx, MGNN_ECUDA, "train: wgrad launch configuration failed");
+        // the weight gradient only reads dZ, H and the means: it runs on the side stream while the
+        // input gradient and the next layer's mask proceed on `s` (joined before returning)
+        CK(cudaEventRecord(S.ev_fork[l], s));
+        CK(cudaStreamWaitEvent(S.side, S.ev_fork[l], 0));
+        if (!launch_wgrad(wa, S.side)) return fail(ctx, MGNN_ECUDA, "train: wgrad launch configuration failed");
         if (l > 0) {
             ZeroRowsArgs za;
             memset(&za, 0, sizeof(za));
@@ -409,6 +422,8 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
             launch_scatter(da, s);
         }
     }
+    CK(cudaEventRecord(S.ev_join, S.side));
+    CK(cudaStreamWaitEvent(s, S.ev_join, 0));
     CKL();
     return MGNN_OK;
 }
