@@ -19,6 +19,17 @@
  * the same stream to every call (or order streams with events).
  * All device memory is owned by the library; window outputs are exposed as
  * device pointers valid until the same window slot is sampled again.
+ *
+ * Typical sequence (one process per GPU; examples/train_ddp.py):
+ *   mgnn_ctx_create -> mgnn_partition_load (each hosted partition)
+ *   [multi-GPU: mgnn_table_export / mgnn_table_import of every other partition]
+ *   mgnn_buffer_init -> mgnn_sampler_config
+ *   per window w (two slots, so sampling runs ahead):
+ *     mgnn_sample(slot w%2)               -- stream A, may run one window ahead
+ *     mgnn_lookup_gather(slot)            -- stream B: X feature-ready (the measured path)
+ *     [mgnn_sage_forward or, per step, mgnn_sage_train_step + all-reduce + mgnn_sage_sgd]
+ *     mgnn_score_evict_refill(slot)       -- stream B: decay, eviction round at t % Delta == 0
+ *     mgnn_counts_read[_async](slot)      -- hits / misses / rows fetched per minibatch
  */
 #ifndef MGNN_H
 #define MGNN_H
