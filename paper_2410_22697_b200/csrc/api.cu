@@ -837,7 +837,12 @@ mgnn_status mgnn_lookup_gather(mgnn_ctx ctx, int32_t slot, mgnn_stream stream) {
         CK(cudaEventCreate(&e1));
         CK(cudaEventRecord(e0, s));
     }
-    launch_gather(wd, world_of(ctx), s);
+    // the tables this GPU's gathers read (hosted partitions; peers' misses are few) fit in L2?
+    int64_t table_bytes = 0;
+    for (auto& p : ctx->parts) table_bytes += p.n_local * (int64_t)ctx->pitch * 4;
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device);
+    launch_gather(wd, world_of(ctx), table_bytes <= (int64_t)l2 * 3 / 4, s);
     CKL();
     if (ctx->prof) {
         CK(cudaEventRecord(e1, s));

@@ -115,7 +115,7 @@ int64_t scan_tiles_count(int64_t fcap);   // tiles used by count_scan for fcap i
 int64_t scan_tiles_words(int64_t words);  // tiles used by compact for `words`
 
 // gather.cu
-void launch_gather(const WinDev& w, const WorldDev& world, cudaStream_t s);
+void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, cudaStream_t s);
 
 // score.cu
 void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, float gamma, cudaStream_t s);
