@@ -167,3 +167,13 @@ def test_cfg1_remote_expansion_dense_scores(cfg1, theta):
 
 def test_dense_scores_local_sampling(cfg1):
     run_parity(cfg1, 3, 64, [5, 10, 15], 128, 3500, 0.95, 4, 1.0, [4, 4], dense=True)
+
+
+@pytest.mark.slow
+def test_products_remote_expansion_dense_scores_window():
+    """configs[3] at full size (2.45M nodes, 124M edges, 3 hops) with remote expansion and the dense
+    S_A: one 32-step window x 2 partitions, sampled instances checked element by element."""
+    g = synth.generate(synth.CONFIGS["products"])
+    st = run_parity(g, 2, 100, [5, 10, 15], 2000, 5000, 0.995, 32, 1.0, [32], sample_every=16, check_x_rows=1024,
+                    remote=True, dense=True)
+    assert st["hits"] > 0 and st["misses"] > 0
