@@ -203,6 +203,10 @@ WinDev win_dev(mgnn_ctx ctx, Win& w) {
     d.n_global = ctx->n_global;
     d.g_indptr = ctx->g_indptr;
     d.g_cols = ctx->g_cols;
+    int64_t nnz_max = ctx->remote ? ctx->g_nnz : 0;
+    if (!ctx->remote)
+        for (auto& p : ctx->parts) nnz_max = std::max(nnz_max, p.nnz);
+    d.idx32 = nnz_max < ((int64_t)1 << 32) ? 1 : 0;
     return d;
 }
 
@@ -589,6 +593,7 @@ mgnn_status mgnn_graph_csr_load(mgnn_ctx ctx, const int64_t* indptr, const int32
     dfree(ctx->g_cols);
     CK(dalloc(&ctx->g_indptr, ctx->n_global + 1));
     CK(dalloc(&ctx->g_cols, nnz));
+    ctx->g_nnz = nnz;
     CK(cudaMemcpy(ctx->g_indptr, indptr, (ctx->n_global + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
     if (nnz) CK(cudaMemcpy(ctx->g_cols, cols, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
     return MGNN_OK;
@@ -615,6 +620,7 @@ mgnn_status mgnn_sampler_expand_remote(mgnn_ctx ctx, int32_t enable) {
         for (auto& p : ctx->parts) nnz += p.nnz;
         CK(dalloc(&ctx->g_indptr, ctx->n_global + 1));
         CK(dalloc(&ctx->g_cols, nnz));
+        ctx->g_nnz = nnz;
         mgnn_status st = upload_parts(ctx);
         if (st) return st;
         int64_t base = 0;
@@ -655,7 +661,7 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
     ctx->vp_max = 1;
     for (auto& p : ctx->parts) ctx->vp_max = std::max(ctx->vp_max, p.n_local + p.n_h);
     if (ctx->remote) ctx->vp_max = std::max<int64_t>(1, ctx->n_global);   // ranks are global ids (NEXT-1)
-    ctx->bm_words = ((ctx->vp_max + 31) / 32 + 3) / 4 * 4;   // multiple of 4: 16-byte bitmap loads
+    ctx->bm_words = ((ctx->vp_max + 31) / 32 + 15) / 16 * 16;   // multiple of 16: k_compact's vector loads
     const int64_t big = (int64_t)1 << 40;
     ctx->fcap[0] = std::min<int64_t>(batch, ctx->vp_max);
     for (int i = 0; i < n_layers; ++i) {

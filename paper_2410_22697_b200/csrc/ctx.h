@@ -110,6 +110,7 @@ struct mgnn_ctx_s {
     bool dense = false;                  // NEXT-1 dense S_A: every non-local node scorable
     int64_t* g_indptr = nullptr;
     int32_t* g_cols = nullptr;
+    int64_t g_nnz = 0;
     // sampler
     bool configured = false;
     int32_t L = 0, batch = 0, max_window = 0;

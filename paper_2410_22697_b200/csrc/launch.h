@@ -52,6 +52,7 @@ struct WinDev {
     int64_t n_global;
     const int64_t* g_indptr;             // [n_global+1]
     const int32_t* g_cols;               // [nnz] global ids
+    int32_t idx32;                       // every CSR index the sampler reads fits in 32 bits
 };
 
 // Segment of a radix sort (device array of these).

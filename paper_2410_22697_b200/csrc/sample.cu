@@ -30,7 +30,8 @@ namespace mgnn {
 
 constexpr int kThreads = 256;
 constexpr int kHopTileMin = 64;        // frontier nodes per k_hop tile: 64 or 256
-constexpr int kCWords = 4;             // bitmap words per k_compact thread (one 16-byte load)
+constexpr int kCWords = 4;             // bitmap words per k_compact thread (2 16-byte loads of pairs)
+constexpr int kColBatch = 8;           // neighbour-rank loads in flight per k_hop thread
 constexpr int kWordTile = kThreads * kCWords;   // bitmap words per k_compact tile
 
 int64_t scan_tiles_count(int64_t fcap) { return (fcap + kHopTileMin - 1) / kHopTileMin; }
@@ -99,7 +100,8 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
 // takes its whole neighbourhood, R#3; a node with deg > k is drawn by a group
 // of k lanes: Philox + Floyd, R#4-R#6); (3) all threads load the sampled
 // neighbours' ranks, write the columns (coalesced) and mark new nodes.
-__global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max, int T) {
+template <typename IdxT>   // CSR index staged per sample: uint32_t when every index fits (halves the tile)
+__global__ void __launch_bounds__(kThreads, 5) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max, int T) {
     pdl_enter();
     __shared__ long long sm[8];
     __shared__ int tslot, n_draw;
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
     __shared__ long long s_b0[kThreads];
     __shared__ int s_row[kThreads], s_d[kThreads], s_o[kThreads], s_draw[kThreads];
     extern __shared__ __align__(16) unsigned char dyn_smem[];
-    long long* sidx = reinterpret_cast<long long*>(dyn_smem);   // [T * k] CSR index of each sample of the tile
+    IdxT* sidx = reinterpret_cast<IdxT*>(dyn_smem);   // [T * k] CSR index of each sample of the tile
     const int m = blockIdx.y;
     const int lp = m / W.n_steps, w = m % W.n_steps;
     const PartDev& pd = W.parts[lp];
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
         if (threadIdx.x < T) s_o[threadIdx.x] = excl;
         const bool draw = cnt > 0 && d > k;
         if (cnt > 0 && !draw)                              // whole neighbourhood in CSR order (R#3)
-            for (int j = 0; j < cnt; ++j) sidx[excl + j] = b0 + j;
+            for (int j = 0; j < cnt; ++j) sidx[excl + j] = (IdxT)(b0 + j);
         const unsigned bal = __ballot_sync(kFull, draw);
         int dbase = 0;
         if (lane == 0 && bal) dbase = atomicAdd(&n_draw, __popc(bal));
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
                     const uint32_t pj = __shfl_sync(kFull, coll ? t : r, (gbase + jj) & 31);
                     if (gl > jj && r == pj) coll = true;
                 }
-                if (active) sidx[s_o[x] + gl] = s_b0[x] + (coll ? t : r);
+                if (active) sidx[s_o[x] + gl] = (IdxT)(s_b0[x] + (coll ? t : r));
             }
         }
         __syncthreads();
@@ -206,14 +208,28 @@ __global__ void __launch_bounds__(kThreads) k_hop(WinDev W, int hop, Scratch sc,
         const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
         uint32_t* nb = W.nb + ((int64_t)m * W.L + hop) * W.bm_words * 2;   // (bits, first position) pairs
         const int32_t* __restrict__ crank = W.remote ? W.g_cols : pd.cols_rank;
-    #pragma unroll 4
-        for (int e = threadIdx.x; e < (int)agg; e += kThreads) {
-            const int32_t c = crank[sidx[e]];
-            MGNN_CHECK(o_tile + e < W.col_stride[hop] && c < (W.remote ? W.n_global : pd.vp), "cols o=%lld c=%d",
-                       o_tile + e, c);
-            cols[e] = c;
-            const uint32_t bit = 1u << (c & 31);
-            if (!(fb[c >> 5] & bit)) atomicOr(&nb[2 * (c >> 5)], bit);
+        // batches of kColBatch samples per thread: all neighbour-rank loads in flight, then all
+        // membership loads, then the writes (the loads are independent; only the marks depend on them)
+        for (int e0 = threadIdx.x; e0 < (int)agg; e0 += kThreads * kColBatch) {
+            int32_t c[kColBatch];
+            uint32_t fw[kColBatch];
+#pragma unroll
+            for (int j = 0; j < kColBatch; ++j) {
+                const int e = e0 + j * kThreads;
+                c[j] = e < (int)agg ? __ldg(crank + sidx[e]) : -1;
+            }
+#pragma unroll
+            for (int j = 0; j < kColBatch; ++j) fw[j] = c[j] >= 0 ? __ldg(fb + (c[j] >> 5)) : ~0u;
+#pragma unroll
+            for (int j = 0; j < kColBatch; ++j) {
+                if (c[j] < 0) continue;
+                const int e = e0 + j * kThreads;
+                MGNN_CHECK(o_tile + e < W.col_stride[hop] && c[j] < (W.remote ? W.n_global : pd.vp),
+                           "cols o=%lld c=%d", o_tile + e, c[j]);
+                cols[e] = c[j];
+                const uint32_t bit = 1u << (c[j] & 31);
+                if (!(fw[j] & bit)) atomicOr(&nb[2 * (c[j] >> 5)], bit);
+            }
         }
         __syncthreads();
     }
@@ -234,14 +250,18 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
     uint32_t* nbp = W.nb + ((int64_t)m * W.L + hop) * W.bm_words * 2;   // word w: nbp[2w] bits, nbp[2w+1] position
     uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
     const int64_t wd0 = (int64_t)tile * kWordTile + (int64_t)threadIdx.x * kCWords;   // 4 consecutive words
-    uint32_t b[kCWords] = {0u, 0u, 0u, 0u};
-    if (wd0 + kCWords <= nwords) {       // 4 (bits, position) pairs: two 16-byte loads (bm_words % 4 == 0)
-        const uint4 v0 = *reinterpret_cast<const uint4*>(nbp + 2 * wd0);
-        const uint4 v1 = *reinterpret_cast<const uint4*>(nbp + 2 * wd0 + 4);
-        b[0] = v0.x; b[1] = v0.z; b[2] = v1.x; b[3] = v1.z;
+    uint32_t b[kCWords];
+    if (wd0 < nwords) {                  // kCWords (bits, position) pairs, 16-byte loads; bm_words % kCWords == 0,
+        const uint4* v = reinterpret_cast<const uint4*>(nbp + 2 * wd0);   // words >= nwords are never set
+#pragma unroll
+        for (int j = 0; j < kCWords / 2; ++j) {
+            const uint4 q = v[j];
+            b[2 * j] = q.x;
+            b[2 * j + 1] = q.z;
+        }
     } else {
 #pragma unroll
-        for (int j = 0; j < kCWords; ++j) b[j] = wd0 + j < nwords ? nbp[2 * (wd0 + j)] : 0u;
+        for (int j = 0; j < kCWords; ++j) b[j] = 0u;
     }
     int cnt = 0;
 #pragma unroll
@@ -264,8 +284,10 @@ __global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch
         uint32_t bb = b[j];
         // new_i keeps its bitmap; with the word's first position it gives every new node's frontier
         // position as wpre + popc(lower bits) (k_relabel), without a scattered rank -> position table
-        if (wd < nwords) nbp[2 * wd + 1] = (uint32_t)pos;
-        if (bb) fb[wd] |= bb;
+        if (bb) {                        // positions are only read where a bit is set
+            nbp[2 * wd + 1] = (uint32_t)pos;
+            fb[wd] |= bb;
+        }
         while (bb) {
             const int bi = __ffs(bb) - 1;
             bb &= bb - 1;
@@ -335,13 +357,18 @@ void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t
     if (tiles > target) tiles = target;
     if (tiles < 1) tiles = 1;
     dim3 grid((unsigned)tiles, w.n_inst);
-    const size_t smem = (size_t)T * w.k_hop[hop] * sizeof(long long);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_hop, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * MGNN_MAX_FANOUT * 8);
+        cudaFuncSetAttribute(k_hop<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * MGNN_MAX_FANOUT * 8);
+        cudaFuncSetAttribute(k_hop<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * MGNN_MAX_FANOUT * 4);
         attr_set = true;
     }
-    launch_k(k_hop, grid, dim3(kThreads), smem, s, w, hop, sc, (int64_t)(tiles_max < 1 ? 1 : tiles_max), T);
+    const int64_t tm = tiles_max < 1 ? 1 : tiles_max;
+    const char* f64 = getenv("MGNN_SAMPLE_IDX64");   // tests: force the 64-bit staging variant
+    if (w.idx32 && !(f64 && f64[0] == '1'))
+        launch_k(k_hop<uint32_t>, grid, dim3(kThreads), (size_t)T * w.k_hop[hop] * 4, s, w, hop, sc, tm, T);
+    else
+        launch_k(k_hop<uint64_t>, grid, dim3(kThreads), (size_t)T * w.k_hop[hop] * 8, s, w, hop, sc, tm, T);
     count_launches(1, __func__, s);
 }
 
