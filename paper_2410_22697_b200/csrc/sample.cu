@@ -31,6 +31,7 @@ namespace mgnn {
 constexpr int kThreads = 256;
 constexpr int kHopTileMin = 64;        // frontier nodes per k_hop tile: 64 or 256
 constexpr int kCWords = 4;             // bitmap words per k_compact thread (2 16-byte loads of pairs)
+constexpr int kRelabelBatch = 4;       // column lookups in flight per k_relabel thread (8: no gain)
 constexpr int kColBatch = 8;           // neighbour-rank loads in flight per k_hop thread
 constexpr int kWordTile = kThreads * kCWords;   // bitmap words per k_compact tile
 
@@ -326,15 +327,16 @@ __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
         const int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
         int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop];
         const int64_t E = off[hs[hop]];
-        // 4 independent lookups in flight per thread (bitmap / prefix words are L2 reads)
-        for (int64_t e0 = (int64_t)blockIdx.x * kThreads * 4 + threadIdx.x; e0 < E; e0 += stride * 4) {
-            int32_t c[4];
+        // kRelabelBatch independent lookups in flight per thread (bitmap / prefix words are L2 reads)
+        for (int64_t e0 = (int64_t)blockIdx.x * kThreads * kRelabelBatch + threadIdx.x; e0 < E;
+             e0 += stride * kRelabelBatch) {
+            int32_t c[kRelabelBatch];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) c[j] = e0 + j * kThreads < E ? cols[e0 + j * kThreads] : 0;
+            for (int j = 0; j < kRelabelBatch; ++j) c[j] = e0 + j * kThreads < E ? cols[e0 + j * kThreads] : 0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) c[j] = frontier_pos(W, m, hop, posof, c[j]);
+            for (int j = 0; j < kRelabelBatch; ++j) c[j] = frontier_pos(W, m, hop, posof, c[j]);
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < kRelabelBatch; ++j)
                 if (e0 + j * kThreads < E) cols[e0 + j * kThreads] = c[j];
         }
     }
@@ -382,7 +384,7 @@ void launch_compact(const WinDev& w, int hop, Scratch sc, cudaStream_t s) {
 void launch_relabel(const WinDev& w, cudaStream_t s) {
     int64_t e_max = 0;
     for (int i = 0; i < w.L; ++i) e_max = w.col_stride[i] > e_max ? w.col_stride[i] : e_max;
-    dim3 grid(grid_x_for(e_max, kThreads * 4, w.n_inst), w.n_inst);
+    dim3 grid(grid_x_for(e_max, kThreads * kRelabelBatch, w.n_inst), w.n_inst);
     launch_k(k_relabel, grid, dim3(kThreads), 0, s, w);
     count_launches(1, __func__, s);
 }
