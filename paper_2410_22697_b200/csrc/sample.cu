@@ -351,7 +351,8 @@ void launch_seeds(const WinDev& w, cudaStream_t s) {
 
 void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s) {
     // small hops (e.g. the seeds) use 64-node tiles so the launch still fills the GPU
-    const int T = (fcap * (int64_t)w.n_inst) / 256 < 148 * 4 ? 64 : 256;
+    const char* te = getenv("MGNN_HOP_TILE");          // experiment: force the tile size
+    const int T = te && atoi(te) == 64 ? 64 : ((fcap * (int64_t)w.n_inst) / 256 < 148 * 4 ? 64 : 256);
     const int64_t tiles_max = scan_tiles_count(fcap);          // scratch stride (64-node tiles)
     // persistent blocks (~5 resident per SM in total); each loops over claimed tiles
     int64_t tiles = (fcap + T - 1) / T;

@@ -147,6 +147,28 @@ def test_cfg1_remote_expansion(cfg1, wins):
     assert st["misses"] > 0 and st["evicted"] > 0
 
 
+@pytest.mark.parametrize("fanouts", [[1, 32], [3, 7], [32, 17, 9], [31, 2]])
+def test_cfg1_fanout_group_shapes(cfg1, fanouts):
+    """k_hop draws a node with k lanes, 32 // k nodes per warp step: k = 1, k = 32 (MGNN_MAX_FANOUT,
+    one node per warp), k not dividing 32 (idle lanes), mixed per hop."""
+    run_parity(cfg1, 2, 16, fanouts, 128, 2500, 0.9, 4, 1.0, [4, 4])
+
+
+@pytest.mark.parametrize("remote", [False, True])
+def test_cfg1_sampler_64bit_csr_index_staging(cfg1, monkeypatch, remote):
+    """k_hop stages 32-bit CSR indices when every index fits; the 64-bit variant (graphs with
+    >= 2^32 edges per partition, e.g. full papers100M under remote expansion) samples the same."""
+    monkeypatch.setenv("MGNN_SAMPLE_IDX64", "1")
+    run_parity(cfg1, 2, 64, [5, 10, 15], 256, 2500, 0.9, 4, 1.0, [4, 4, 4], remote=remote)
+
+
+@pytest.mark.parametrize("tile", ["64"])
+def test_cfg1_small_hop_tiles(cfg1, monkeypatch, tile):
+    """64-node k_hop tiles on every hop (the default picks them only for small frontiers)."""
+    monkeypatch.setenv("MGNN_HOP_TILE", tile)
+    run_parity(cfg1, 2, 64, [10, 25], 256, 2500, 0.9, 4, 1.0, [4, 4])
+
+
 def test_remote_expansion_three_hops_four_partitions(cfg1):
     run_parity(cfg1, 4, 64, [5, 10, 15], 128, 3500, 0.95, 4, 1.0, [4, 4], remote=True)
 
