@@ -3,7 +3,7 @@
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/randread tools/randread.cu && /tmp/randread
 //
-// Table of 2 GiB (>> the 126 MB L2); every thread issues `kBatch` independent loads per iteration at
+// Tables of 256 MB - 2 GiB (> the 126 MB L2); every thread issues `kBatch` independent loads per iteration at
 // hashed indices.  Reports loads/s and sector GB/s (32 B per load) -- the denominator DESIGN.md uses
 // for the random-gather kernels.
 #include <cstdio>
@@ -31,17 +31,17 @@ __global__ void k_rand(const int32_t* __restrict__ t, uint32_t mask, int iters, 
 }
 
 int main() {
-    const size_t n = (size_t)1 << 29;   // 2 GiB of int32
+    const size_t n_max = (size_t)1 << 29;   // up to 2 GiB of int32
     int32_t *t, *out;
-    cudaMalloc(&t, n * 4);
+    cudaMalloc(&t, n_max * 4);
     cudaMalloc(&out, 4);
-    cudaMemset(t, 1, n * 4);
+    cudaMemset(t, 1, n_max * 4);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    for (int bps : {4, 8}) {
-        for (int iters : {64}) {
-            const int blocks = 148 * bps, threads = 256;
+    for (size_t n : {(size_t)1 << 26, (size_t)1 << 27, (size_t)1 << 28, (size_t)1 << 29}) {   // 256 MB .. 2 GiB
+        for (int bps : {4, 8}) {
+            const int blocks = 148 * bps, threads = 256, iters = 64;
             k_rand<<<blocks, threads>>>(t, (uint32_t)(n - 1), iters, out);
             cudaEventRecord(a);
             const int reps = 5;
@@ -51,8 +51,8 @@ int main() {
             float ms;
             cudaEventElapsedTime(&ms, a, b);
             const double loads = (double)blocks * threads * iters * kBatch * reps;
-            printf("blocks/SM %d: %.2f G random loads/s, %.0f GB/s of 32-byte sectors\n", bps, loads / ms / 1e6,
-                   loads * 32 / ms / 1e6);
+            printf("table %4zu MB, blocks/SM %d: %.1f G random loads/s, %.0f GB/s of 32-byte sectors\n", n * 4 >> 20,
+                   bps, loads / ms / 1e6, loads * 32 / ms / 1e6);
         }
     }
     cudaError_t e = cudaGetLastError();
