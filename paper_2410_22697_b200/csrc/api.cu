@@ -243,7 +243,8 @@ mgnn_status mgnn_ctx_create(int32_t device, int32_t n_parts, int64_t n_global, c
     ctx->lp_of.assign(n_parts, -1);
     {
         const char* e = getenv("MGNN_EVICT_SORT");
-        ctx->force_sort_path = e && e[0] == '1';
+        ctx->force_sort_path = e && (e[0] == '1' || e[0] == '2');
+        ctx->sort_full_lists = e && e[0] == '2';
     }
     ctx->tables.assign(n_parts, nullptr);
     mgnn_status st = MGNN_OK;
@@ -289,6 +290,7 @@ void mgnn_destroy(mgnn_ctx ctx) {
     dfree(ctx->d_err);
     dfree(ctx->d_gathered);
     dfree(ctx->d_evsegs);
+    dfree(ctx->d_candsegs);
     dfree(ctx->d_initsegs);
     dfree(ctx->d_sel_n);
     dfree(ctx->ev_zero);
@@ -547,6 +549,21 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
         ctx->ev_ev.ticket = (unsigned*)(ctx->ev_zero + o_tk);
         ctx->ev_ev.thr = (long long*)(ctx->ev_zero + o_thr);
         ctx->ev_ev.n_cand = (unsigned long long*)(ctx->ev_zero + o_nc);
+    }
+    {   // large buffers: the K winners are sorted out of the compacted candidates (k_cand appends them
+        // unordered, so E sorts all 8 key bytes; R's schedule already covers every byte that differs)
+        std::vector<SortSeg> cs(2 * n_lp);
+        const long long* nc = reinterpret_cast<const long long*>(ctx->ev_ev.n_cand);
+        for (int lp = 0; lp < n_lp; ++lp) {
+            Part& p = ctx->parts[lp];
+            cs[2 * lp] = make_seg(p.ekt, p.evt, p.ek, p.ev, nc + 2 * lp, {0, 8, 16, 24, 32, 40, 48, 56});
+            SortSeg r = segs[2 * lp + 1];
+            r.keys = p.rkt; r.vals = p.rvt; r.keys_tmp = p.rk; r.vals_tmp = p.rv; r.n = nc + 2 * lp + 1;
+            cs[2 * lp + 1] = r;
+        }
+        dfree(ctx->d_candsegs);
+        CK(dalloc(&ctx->d_candsegs, cs.size()));
+        CK(cudaMemcpy(ctx->d_candsegs, cs.data(), cs.size() * sizeof(SortSeg), cudaMemcpyHostToDevice));
     }
     {
         mgnn_status st2 = ensure_scratch(ctx, &ctx->sort_scr, &ctx->sort_scr_bytes,
@@ -879,11 +896,19 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
         CK(cudaMemsetAsync(ctx->ev_zero, 0, ctx->ev_zero_bytes, s));
         launch_select(ctx->d_parts, n_lp, nmax, ctx->pol.alpha, ctx->pol.theta_r, ctx->d_evsegs, ctx->d_sel_n,
                       ctx->ev_sc, ctx->ev_ev, s);
-        if (cap_max <= kEvMax && !ctx->force_sort_path)
+        const SortSeg* pairs = ctx->d_evsegs;     // where the K winners of E and R end, in order
+        const long long* k_of = nullptr;           // K per segment (null: min(|E|, |R|) of the lists)
+        if (cap_max <= kEvMax && !ctx->force_sort_path) {
             launch_cand_rank(ctx->d_evsegs, n_lp, nmax, ctx->ev_ev, s);     // K winners in order, no sort
-        else
+        } else if (ctx->sort_full_lists) {
             radix_sort_pairs(ctx->d_evsegs, 2 * n_lp, nmax, ctx->ev_passes, ctx->sort_scr, s);
-        launch_swap_refill(ctx->d_parts, n_lp, cap_max, ctx->d_evsegs, world_of(ctx), w.counts, 8, w.n_steps, s);
+        } else {                                   // threshold candidates, then sort only those
+            launch_cand(ctx->d_evsegs, n_lp, nmax, ctx->ev_ev, s);
+            radix_sort_pairs(ctx->d_candsegs, 2 * n_lp, nmax, 8, ctx->sort_scr, s);
+            pairs = ctx->d_candsegs;
+            k_of = ctx->ev_ev.thr;
+        }
+        launch_swap_refill(ctx->d_parts, n_lp, cap_max, pairs, k_of, world_of(ctx), w.counts, 8, w.n_steps, s);
     }
     CKL();
     w.scored = true;

@@ -92,8 +92,10 @@ struct mgnn_ctx_s {
     mgnn_policy pol{};
     // eviction scratch
     SortSeg* d_evsegs = nullptr;
+    SortSeg* d_candsegs = nullptr;       // the compacted candidates (E: all 8 key bytes; R: as d_evsegs)
     SortSeg* d_initsegs = nullptr;
-    bool force_sort_path = false;        // MGNN_EVICT_SORT=1: always use the full radix-sort eviction path
+    bool force_sort_path = false;        // MGNN_EVICT_SORT=1: always use the radix-sort eviction path
+    bool sort_full_lists = false;        // MGNN_EVICT_SORT=2: sort the whole E / R lists, not the candidates
     int32_t ev_passes = 8;
     long long* d_sel_n = nullptr;
     char* ev_zero = nullptr;

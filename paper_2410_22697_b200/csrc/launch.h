@@ -124,7 +124,9 @@ void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, f
                    long long* n_out, Scratch sc, EvScratch ev, cudaStream_t s);
 // small-buffer path: candidates below the threshold digit, ranked by counting into sorted order
 void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, cudaStream_t s);
-void launch_swap_refill(const PartDev* parts, int n_lp, int64_t cap_max, const SortSeg* segs, const WorldDev& world,
+void launch_cand(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, cudaStream_t s);   // candidates only
+void launch_swap_refill(const PartDev* parts, int n_lp, int64_t cap_max, const SortSeg* segs, const long long* k_of,
+                        const WorldDev& world,
                         long long* counts, int64_t inst_stride_counts, int n_steps, cudaStream_t s);
 // |BUF| up to which the candidate-rank path (no sort) is used for eviction rounds
 constexpr int kEvMax = 65536;

@@ -16,7 +16,9 @@
 //   k_cand    compacts the candidates (digit <= T) -- typically a few hundred;
 //   k_rank    ranks every candidate by counting smaller candidate keys (keys are unique, so the
 //             rank IS the sorted position) and writes the K winners in order: no sort at all.
-//   large |BUF|: the onesweep radix sort of both lists (sort.cu).
+//   large |BUF|: k_hist2 + k_cand as above, then the onesweep radix sort (sort.cu) of the
+//             candidates only (all 8 key bytes: k_cand appends them unordered) -- K and a bucket
+//             instead of the whole lists; MGNN_EVICT_SORT=2 sorts the whole lists instead.
 //   k_swap_refill  pair i = (E[i], R[i]): swap of P:224, refill from the owner's table.
 #include <algorithm>
 
@@ -280,6 +282,13 @@ __global__ void __launch_bounds__(kSThreads) k_rank(const SortSeg* __restrict__ 
     }
 }
 
+void launch_cand(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, cudaStream_t s) {
+    dim3 g1(blocks_for(n_max, kSThreads) > 64 ? 64 : blocks_for(n_max, kSThreads), 2 * n_lp);
+    launch_k(k_hist2, g1, dim3(kSThreads), 0, s, segs, ev);
+    launch_k(k_cand, g1, dim3(kSThreads), 0, s, segs, ev);
+    count_launches(2, __func__, s);
+}
+
 void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, cudaStream_t s) {
     dim3 g1(blocks_for(n_max, kSThreads) > 64 ? 64 : blocks_for(n_max, kSThreads), 2 * n_lp);
     launch_k(k_hist2, g1, dim3(kSThreads), 0, s, segs, ev);
@@ -295,14 +304,15 @@ void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev
 // then the row of r is copied from its owner's table into the slot.
 // E and R are disjoint (buffered vs. not), so pairs never conflict.
 __global__ void __launch_bounds__(kSThreads) k_swap_refill(const PartDev* __restrict__ parts,
-                                                           const SortSeg* __restrict__ segs, WorldDev G,
+                                                           const SortSeg* __restrict__ segs,
+                                                           const long long* __restrict__ k_of, WorldDev G,
                                                            long long* counts, int64_t counts_stride, int n_steps) {
     pdl_enter();
     const int lp = blockIdx.y;
     const PartDev& pd = parts[lp];
     const SortSeg E = segs[2 * lp], R = segs[2 * lp + 1];
     const long long nE = *E.n, nR = *R.n;
-    const long long k = nE < nR ? nE : nR;
+    const long long k = k_of ? k_of[4 * lp] : (nE < nR ? nE : nR);   // k_of: {K, T} per segment
     const int lane = threadIdx.x & 31;
     const int pitch = G.pitch;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -339,10 +349,11 @@ __global__ void __launch_bounds__(kSThreads) k_swap_refill(const PartDev* __rest
     }
 }
 
-void launch_swap_refill(const PartDev* parts, int n_lp, int64_t cap_max, const SortSeg* segs, const WorldDev& world,
+void launch_swap_refill(const PartDev* parts, int n_lp, int64_t cap_max, const SortSeg* segs, const long long* k_of,
+                        const WorldDev& world,
                         long long* counts, int64_t counts_stride, int n_steps, cudaStream_t s) {
     dim3 grid(blocks_for(cap_max < 1 ? 1 : cap_max, kSThreads / 32), n_lp);
-    launch_k(k_swap_refill, grid, dim3(kSThreads), 0, s, parts, segs, world, counts, counts_stride, n_steps);
+    launch_k(k_swap_refill, grid, dim3(kSThreads), 0, s, parts, segs, k_of, world, counts, counts_stride, n_steps);
     count_launches(1, __func__, s);
 }
 
