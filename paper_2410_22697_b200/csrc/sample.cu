@@ -32,7 +32,13 @@ constexpr int kThreads = 256;
 constexpr int kHopTileMin = 64;        // frontier nodes per k_hop tile: 64 or 256
 constexpr int kCWords = 4;             // bitmap words per k_compact thread (2 16-byte loads of pairs)
 constexpr int kRelabelBatch = 4;       // column lookups in flight per k_relabel thread (8: no gain)
-constexpr int kColBatch = 8;           // neighbour-rank loads in flight per k_hop thread
+#ifndef MGNN_HOP_BLOCKS
+#define MGNN_HOP_BLOCKS 8                // resident k_hop blocks per SM (32 registers; 5 x 8 loads: +11 % hop time)
+#endif
+#ifndef MGNN_COL_BATCH
+#define MGNN_COL_BATCH 4
+#endif
+constexpr int kColBatch = MGNN_COL_BATCH;           // neighbour-rank loads in flight per k_hop thread
 constexpr int kWordTile = kThreads * kCWords;   // bitmap words per k_compact tile
 
 int64_t scan_tiles_count(int64_t fcap) { return (fcap + kHopTileMin - 1) / kHopTileMin; }
@@ -102,7 +108,7 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
 // of k lanes: Philox + Floyd, R#4-R#6); (3) all threads load the sampled
 // neighbours' ranks, write the columns (coalesced) and mark new nodes.
 template <typename IdxT>   // CSR index staged per sample: uint32_t when every index fits (halves the tile)
-__global__ void __launch_bounds__(kThreads, 5) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max, int T) {
+__global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max, int T) {
     pdl_enter();
     __shared__ long long sm[8];
     __shared__ int tslot, n_draw;
@@ -356,7 +362,7 @@ void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t
     const int64_t tiles_max = scan_tiles_count(fcap);          // scratch stride (64-node tiles)
     // persistent blocks (~5 resident per SM in total); each loops over claimed tiles
     int64_t tiles = (fcap + T - 1) / T;
-    const int64_t target = (148 * 5 + w.n_inst - 1) / w.n_inst;
+    const int64_t target = (148 * MGNN_HOP_BLOCKS + w.n_inst - 1) / w.n_inst;
     if (tiles > target) tiles = target;
     if (tiles < 1) tiles = 1;
     dim3 grid((unsigned)tiles, w.n_inst);
