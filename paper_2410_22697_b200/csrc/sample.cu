@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int
 }
 
 // ------------------------------------------------------------------ bitmap -> sorted new frontier nodes
-__global__ void __launch_bounds__(kThreads) k_compact(WinDev W, int hop, Scratch sc, int64_t tiles_max) {
+__global__ void __launch_bounds__(kThreads, 8) k_compact(WinDev W, int hop, Scratch sc, int64_t tiles_max) {
     pdl_enter();
     __shared__ long long sm[8];
     __shared__ int tslot;
