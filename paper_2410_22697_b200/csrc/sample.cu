@@ -24,6 +24,8 @@
 // After the last hop k_relabel rewrites the sampled columns as positions in
 // F_{i+1} (the DGL block layout the consumer indexes X with): a new node's
 // position is its word's position + popc of the lower bits of new_j.
+#include <cstdlib>
+
 #include "launch.h"
 
 namespace mgnn {
