@@ -1,0 +1,35 @@
+"""Launch-configuration variants that are fixed once per process (read from the environment at
+the first launch): each runs a cfg1 parity check in a fresh interpreter (-m gpu).
+
+* MGNN_GATHER=reg      -- register gather (k_gather<false> for narrow rows, <true> for >= 128 floats)
+* MGNN_PDL=0           -- plain launches instead of programmatic dependent launch
+* MGNN_GATHER_HINT=0/3 -- no L2 cache hints / table rows evict_last and X rows evict_first
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = """
+import sys
+sys.path.insert(0, {root!r})
+from inputs import synth
+from tests.parity_util import run_parity
+g = synth.generate(synth.CONFIGS["cfg1"])
+for D in (64, 200):
+    run_parity(g, 2, D, [10, 25], 256, 2500, 0.9, 4, 1.0, [4, 4])
+print("variant parity ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"MGNN_GATHER": "reg"}, {"MGNN_PDL": "0"}, {"MGNN_GATHER_HINT": "0"},
+                                 {"MGNN_GATHER_HINT": "3"}])
+def test_variant_parity(env):
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT)], cwd=ROOT, env=e, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "variant parity ok" in r.stdout, (env, r.stdout[-2000:], r.stderr[-4000:])
