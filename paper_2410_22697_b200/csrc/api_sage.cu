@@ -35,6 +35,8 @@ void free_sage(mgnn_ctx_s* ctx) {
         cudaStreamDestroy(S.side);
         for (auto& e : S.ev_fork) cudaEventDestroy(e);
         cudaEventDestroy(S.ev_join);
+        cudaEventDestroy(S.ev_start);
+        cudaEventDestroy(S.ev_zero);
         S.side = nullptr;
     }
     S.ready = S.train = false;
@@ -250,6 +252,8 @@ mgnn_status mgnn_sage_train_config(mgnn_ctx ctx, const int32_t* labels) {
         CK(cudaStreamCreateWithFlags(&S.side, cudaStreamNonBlocking));
         for (auto& e : S.ev_fork) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&S.ev_join, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&S.ev_start, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&S.ev_zero, cudaEventDisableTiming));
         S.rows64 = (ctx->batch + 63) / 64 * 64;
         const int64_t nl = M * S.rows64 * S.npad[L - 1];
         CK(dalloc(&S.logits, nl));
@@ -303,6 +307,28 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
     const int L = S.L;
     const int n_lp = (int)ctx->parts.size();
     const int i0 = step_in_window, is = w.n_steps;   // instances lp * n_steps + step_in_window
+    // The input-gradient buffers dH[l-1] (l >= 1) are cleared on the side stream beside the forward:
+    // nothing of this step touches them before the first dgrad, and every write of the previous
+    // step (dgrad, scatter, ReLU mask on `s`) precedes the fork of that step's last weight gradient,
+    // which the side stream already follows.
+    if (L > 1) {
+        CK(cudaEventRecord(S.ev_start, s));
+        CK(cudaStreamWaitEvent(S.side, S.ev_start, 0));
+        for (int l = 1; l < L; ++l) {
+            ZeroRowsArgs za;
+            memset(&za, 0, sizeof(za));
+            za.n_inst = n_lp;
+            za.inst0 = i0;
+            za.inst_step = is;
+            za.hop = L - l;
+            za.hop_size = w.hop_size;
+            za.buf = S.dh[l - 1];
+            za.rows = S.dh_rows[l - 1];
+            za.pitch = S.npad[l - 1];
+            launch_zero_rows(za, S.side);
+        }
+        CK(cudaEventRecord(S.ev_zero, S.side));
+    }
     // forward, keeping every layer's output and neighbour means
     for (int l = 0; l < L; ++l) {
         mgnn_status st = l < L - 1 ? sage_layer(ctx, w, slot, l, n_lp, i0, is, S.h[l], S.out_rows[l], S.npad[l],
@@ -386,17 +412,7 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
         CK(cudaStreamWaitEvent(S.side, S.ev_fork[l], 0));
         if (!launch_wgrad(wa, S.side)) return fail(ctx, MGNN_ECUDA, "train: wgrad launch configuration failed");
         if (l > 0) {
-            ZeroRowsArgs za;
-            memset(&za, 0, sizeof(za));
-            za.n_inst = n_lp;
-            za.inst0 = i0;
-            za.inst_step = is;
-            za.hop = hop + 1;
-            za.hop_size = w.hop_size;
-            za.buf = S.dh[l - 1];
-            za.rows = S.dh_rows[l - 1];
-            za.pitch = S.npad[l - 1];
-            launch_zero_rows(za, s);
+            if (l == L - 1) CK(cudaStreamWaitEvent(s, S.ev_zero, 0));
             DgradArgs da;
             memset(&da, 0, sizeof(da));
             da.n_inst = n_lp;

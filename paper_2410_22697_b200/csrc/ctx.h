@@ -152,7 +152,7 @@ struct mgnn_ctx_s {
         float* dmean = nullptr;                   // dZ W_neigh / deg of the current layer (dgrad -> scatter)
         float* loss = nullptr;                    // device scalar
         cudaStream_t side = nullptr;              // weight gradients run beside the input-gradient chain
-        cudaEvent_t ev_fork[kMaxLayers] = {}, ev_join = nullptr;
+        cudaEvent_t ev_fork[kMaxLayers] = {}, ev_join = nullptr, ev_start = nullptr, ev_zero = nullptr;
         int64_t rows64 = 0, dh_rows[kMaxLayers] = {};
         alignas(64) unsigned char map_dz128[kMaxLayers][128], map_wt[kMaxLayers][128], map_mean128[kMaxLayers][128];
     } sage;
