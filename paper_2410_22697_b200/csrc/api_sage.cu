@@ -307,6 +307,13 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
     const int L = S.L;
     const int n_lp = (int)ctx->parts.size();
     const int i0 = step_in_window, is = w.n_steps;   // instances lp * n_steps + step_in_window
+    // every early return after the side stream forked joins it back into `s` first, so a CUDA-graph
+    // capture of the caller's stream never ends with an un-joined fork
+    bool forked = false;
+    auto joined = [&](mgnn_status st) -> mgnn_status {
+        if (forked && cudaEventRecord(S.ev_join, S.side) == cudaSuccess) cudaStreamWaitEvent(s, S.ev_join, 0);
+        return st;
+    };
     // The input-gradient buffers dH[l-1] (l >= 1) are cleared on the side stream beside the forward:
     // nothing of this step touches them before the first dgrad, and every write of the previous
     // step (dgrad, scatter, ReLU mask on `s`) precedes the fork of that step's last weight gradient,
@@ -314,6 +321,7 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
     if (L > 1) {
         CK(cudaEventRecord(S.ev_start, s));
         CK(cudaStreamWaitEvent(S.side, S.ev_start, 0));
+        forked = true;
         for (int l = 1; l < L; ++l) {
             ZeroRowsArgs za;
             memset(&za, 0, sizeof(za));
@@ -335,7 +343,7 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
                                                 S.npad[l], S.mean[l], s, true)
                                    : sage_layer(ctx, w, slot, l, n_lp, i0, is, S.logits, S.rows64, S.npad[l],
                                                 S.npad[l], S.mean[l], s, true);
-        if (st) return st;
+        if (st) return joined(st);
     }
     // loss: mean cross-entropy per trainer, averaged over the n_trainers of the DDP step
     XentArgs xa;
@@ -410,7 +418,9 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
         // input gradient and the next layer's mask proceed on `s` (joined before returning)
         CK(cudaEventRecord(S.ev_fork[l], s));
         CK(cudaStreamWaitEvent(S.side, S.ev_fork[l], 0));
-        if (!launch_wgrad(wa, S.side)) return fail(ctx, MGNN_ECUDA, "train: wgrad launch configuration failed");
+        forked = true;
+        if (!launch_wgrad(wa, S.side))
+            return joined(fail(ctx, MGNN_ECUDA, "train: wgrad launch configuration failed"));
         if (l > 0) {
             if (l == L - 1) CK(cudaStreamWaitEvent(s, S.ev_zero, 0));
             DgradArgs da;
@@ -434,7 +444,7 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
             da.dmean = S.dmean;
             da.dmean_rows = S.out_rows[l];
             if (!launch_dgrad(S.map_dz128[l], S.map_wt[l], da, s))
-                return fail(ctx, MGNN_ECUDA, "train: dgrad launch configuration failed");
+                return joined(fail(ctx, MGNN_ECUDA, "train: dgrad launch configuration failed"));
             launch_scatter(da, s);
         }
     }

@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
 void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, cudaStream_t s) {
     // exactly one wave of 4 resident 256-thread blocks per SM in total (64 registers per thread):
     // floor, so no second, nearly empty wave leaves SMs idle at the tail
-    int64_t target = (148 * 4) / w.n_inst;
+    int64_t target = ((int64_t)num_sms() * 4) / w.n_inst;
     int64_t need = (w.ucap + kGWarps * 32 - 1) / (kGWarps * 32);
     unsigned gx = (unsigned)(need < target ? need : target);
     if (gx < 1) gx = 1;
@@ -363,12 +363,8 @@ void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, cud
     const int R = (int)std::min<int64_t>(32, std::max<int64_t>(1, stage / ((int64_t)w.pitch * 4)));
     if (use_tma && (int64_t)w.pitch * 4 <= stage) {
         const size_t smem = (size_t)kTWarps * 2 * stage;
-        static size_t attr = 0;
-        if (smem > attr) {
-            cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = smem;
-        }
-        int64_t tgt = (148 * bps) / w.n_inst;
+        ensure_smem_k(k_gather_tma, (int)smem);
+        int64_t tgt = ((int64_t)num_sms() * bps) / w.n_inst;
         int64_t nd = (w.ucap + kTWarps * R - 1) / (kTWarps * R);
         unsigned gxt = (unsigned)std::max<int64_t>(1, std::min(nd, tgt));
         // L2 hints: 2 (default) = X rows stored evict_first, so the once-written minibatch does not push

@@ -19,6 +19,18 @@ constexpr int kMaxLayers = MGNN_MAX_LAYERS;
 void count_launches(long long n, const char* who, cudaStream_t s);
 long long launches_total();
 
+// SM count of the current device (cudaDevAttrMultiProcessorCount, cached per device): every grid is
+// sized from it instead of assuming B200's 148.
+int num_sms();
+// Opt-in dynamic shared memory for `func` on the CURRENT device: raised to `bytes` once per
+// (device, kernel) -- the attribute is per device, so a second context on another GPU sets it again.
+// Thread-safe.  Returns the CUDA error of the attribute call (cudaSuccess if already set).
+cudaError_t ensure_smem(const void* func, int bytes);
+template <typename F>
+inline cudaError_t ensure_smem_k(F* func, int bytes) {
+    return ensure_smem(reinterpret_cast<const void*>(func), bytes);
+}
+
 // ------------------------------------------------------------------ window (device view)
 struct WinDev {
     int32_t n_inst, n_steps, L, batch, pitch, feat_dim;

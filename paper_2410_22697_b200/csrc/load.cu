@@ -15,7 +15,7 @@ constexpr int kLThreads = 256;
 
 static inline unsigned lblocks(int64_t n) {
     int64_t b = (n + kLThreads - 1) / kLThreads;
-    if (b > 148 * 16) b = 148 * 16;
+    if (b > (int64_t)num_sms() * 16) b = (int64_t)num_sms() * 16;
     return (unsigned)(b < 1 ? 1 : b);
 }
 

@@ -390,16 +390,13 @@ constexpr size_t kSmemPerCta = (228 * 1024) / kCtasPerSm - 2048;   // per CTA, m
 
 
 bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArgs& args_in, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
+    {   // per device (ensure_smem): the opt-in limit, and the whole unified L1/shared array as shared
+        // memory so two CTAs fit per SM (the carveout is a hint; setting it again is harmless)
         int optin = 0, dev0 = 0;
         cudaGetDevice(&dev0);
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev0);
-        if (cudaFuncSetAttribute(k_sage_layer, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024) != cudaSuccess)
-            return false;
-        // the whole unified L1/shared array as shared memory, so two CTAs fit per SM
+        if (ensure_smem_k(k_sage_layer, optin - 1024) != cudaSuccess) return false;
         cudaFuncSetAttribute(k_sage_layer, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        attr = true;
     }
     SageLayerArgs a = args_in;
     a.n_panels = (a.k_in + kPanelChunks * kChunkCols - 1) / (kPanelChunks * kChunkCols);
@@ -423,9 +420,7 @@ bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArg
     while ((int)a.tmem_cols < a.npad) a.tmem_cols <<= 1;
     // instruction descriptor: D fp32, A/B tf32, both K-major, N = npad, M = 128
     a.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(a.npad >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = num_sms();
     CUtensorMap mi = *(const CUtensorMap*)map_in, mw = *(const CUtensorMap*)map_w;
     launch_k(k_sage_layer, dim3(kCtasPerSm * sms), dim3(kSageThreads), smem, s, mi, mw, a);
     count_launches(1, __func__, s);
@@ -614,16 +609,11 @@ __global__ void __launch_bounds__(kGThreads, 1)
 
 bool launch_sage_gemm(const void* map_in, const void* map_w, const void* map_mean, const SageLayerArgs& args_in,
                       cudaStream_t s) {
-    static bool attr = false;
-    int optin = 0, dev = 0, sms = 148;
+    int optin = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_sage_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024) != cudaSuccess)
-            return false;
-        attr = true;
-    }
+    const int sms = num_sms();
+    if (ensure_smem_k(k_sage_gemm, optin - 1024) != cudaSuccess) return false;
     SageLayerArgs a = args_in;
     if (a.n_inst > kMaxInst || a.npad % 16 || a.npad < 16 || a.npad > 256 || !map_mean) return false;
     const int64_t nk = 2 * (int64_t)((a.k_in + kChunkCols - 1) / kChunkCols);

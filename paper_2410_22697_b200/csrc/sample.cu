@@ -49,7 +49,7 @@ int64_t scan_tiles_words(int64_t words) { return (words + kWordTile - 1) / kWord
 static inline unsigned grid_x_for(int64_t items_per_inst, int items_per_block, int n_inst) {
     // enough blocks to cover one instance, but about 16 resident blocks per SM overall
     int64_t need = (items_per_inst + items_per_block - 1) / items_per_block;
-    int64_t target = (148 * 16 + n_inst - 1) / n_inst;
+    int64_t target = ((int64_t)num_sms() * 16 + n_inst - 1) / n_inst;
     int64_t g = need < target ? need : target;
     return (unsigned)(g < 1 ? 1 : g);
 }
@@ -360,20 +360,16 @@ void launch_seeds(const WinDev& w, cudaStream_t s) {
 void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t s) {
     // small hops (e.g. the seeds) use 64-node tiles so the launch still fills the GPU
     const char* te = getenv("MGNN_HOP_TILE");          // experiment: force the tile size
-    const int T = te && atoi(te) == 64 ? 64 : ((fcap * (int64_t)w.n_inst) / 256 < 148 * 4 ? 64 : 256);
+    const int T = te && atoi(te) == 64 ? 64 : ((fcap * (int64_t)w.n_inst) / 256 < (int64_t)num_sms() * 4 ? 64 : 256);
     const int64_t tiles_max = scan_tiles_count(fcap);          // scratch stride (64-node tiles)
     // persistent blocks (~5 resident per SM in total); each loops over claimed tiles
     int64_t tiles = (fcap + T - 1) / T;
-    const int64_t target = (148 * MGNN_HOP_BLOCKS + w.n_inst - 1) / w.n_inst;
+    const int64_t target = ((int64_t)num_sms() * MGNN_HOP_BLOCKS + w.n_inst - 1) / w.n_inst;
     if (tiles > target) tiles = target;
     if (tiles < 1) tiles = 1;
     dim3 grid((unsigned)tiles, w.n_inst);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_hop<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * MGNN_MAX_FANOUT * 8);
-        cudaFuncSetAttribute(k_hop<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * MGNN_MAX_FANOUT * 4);
-        attr_set = true;
-    }
+    ensure_smem_k(k_hop<uint64_t>, 256 * MGNN_MAX_FANOUT * 8);
+    ensure_smem_k(k_hop<uint32_t>, 256 * MGNN_MAX_FANOUT * 4);
     const int64_t tm = tiles_max < 1 ? 1 : tiles_max;
     const char* f64 = getenv("MGNN_SAMPLE_IDX64");   // tests: force the 64-bit staging variant
     if (w.idx32 && !(f64 && f64[0] == '1'))

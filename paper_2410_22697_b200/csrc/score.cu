@@ -31,7 +31,7 @@ constexpr int kDig = 4096;            // 12-bit top-of-key histogram
 
 static inline unsigned blocks_for(int64_t n, int per_block) {
     int64_t b = (n + per_block - 1) / per_block;
-    if (b > 148 * 8) b = 148 * 8;
+    if (b > (int64_t)num_sms() * 8) b = (int64_t)num_sms() * 8;
     return (unsigned)(b < 1 ? 1 : b);
 }
 

@@ -525,18 +525,11 @@ void launch_zero_rows(const ZeroRowsArgs& a, cudaStream_t s) {
 }
 
 bool launch_wgrad(const WgradArgs& a_in, cudaStream_t s) {
-    static bool attr = false;
     const size_t smem = 1024 + 2 * kWStage;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return false;
-        attr = true;
-    }
+    if (ensure_smem_k(k_wgrad, (int)smem) != cudaSuccess) return false;
     WgradArgs a = a_in;
     if (a.n_inst > kWMaxInst || a.kp % 128 || a.npad > 256) return false;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = num_sms();
     const int tiles = ((a.npad + 127) / 128) * ((2 * a.kp) / 128);
     // split-K over every SM (measured: fewer CTAs with >= 8 chunks each was slower, 16 -> 26 us; the
     // chunk loads are latency-bound, the partial-tile atomics are not)
@@ -549,17 +542,10 @@ bool launch_wgrad(const WgradArgs& a_in, cudaStream_t s) {
 bool launch_dgrad(const void* map_dz, const void* map_wt, const DgradArgs& a, cudaStream_t s) {
     if (a.n_inst > kWMaxInst || a.kp % 32 || a.kp > 256 || a.npad_out > 256) return false;
     const size_t smem = 1024 + 2 * ((size_t)kDTile * 128 + (size_t)2 * a.kp * 128);
-    static size_t attr = 0;
-    if (smem > attr) {
-        if (cudaFuncSetAttribute(k_dgrad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return false;
-        attr = smem;
-    }
+    if (ensure_smem_k(k_dgrad, (int)smem) != cudaSuccess) return false;
     uint32_t cols = 32;
     while ((int)cols < 2 * a.kp) cols <<= 1;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = num_sms();
     launch_k(k_dgrad, dim3(sms), dim3(128), smem, s, *(const CUtensorMap*)map_dz, *(const CUtensorMap*)map_wt, a, cols);
     count_launches(1, __func__, s);
     return true;
@@ -576,7 +562,7 @@ void launch_mean(const SageLayerArgs& a, cudaStream_t s) {
 }
 
 void launch_sgd_layers(const SgdLayers& d, float lr, cudaStream_t s) {
-    launch_k(k_sgd_layers, dim3(148), dim3(kT), 0, s, d, lr);
+    launch_k(k_sgd_layers, dim3(num_sms()), dim3(kT), 0, s, d, lr);
     count_launches(1, __func__, s);
 }
 

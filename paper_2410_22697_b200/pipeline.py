@@ -335,13 +335,12 @@ def ddp_step(ctx: Context, slot: int, step_in_window: int, n_trainers: int, lr: 
     across ranks (NCCL through torch.distributed, on the same stream), then SGD."""
     import torch
     import torch.distributed as dist
+    if isinstance(stream, int):        # a raw cudaStream_t: the all-reduce must be ordered on it too
+        stream = torch.cuda.ExternalStream(stream)
     ctx.train_step(slot, step_in_window, n_trainers, stream)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         g = ctx.grads()
-        if stream is not None and not isinstance(stream, int):
-            with torch.cuda.stream(stream):
-                dist.all_reduce(g, group=group)
-        else:
+        with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
             dist.all_reduce(g, group=group)
     ctx.sgd(lr, stream)
 

@@ -428,6 +428,34 @@ def test_epoch_permutations():
     assert not np.array_equal(e0, e1) and np.array_equal(e0, p.epoch_perm(RUN_SEED, 0, 40))
 
 
+def test_epoch_permutation_order_is_ascending_philox_key():
+    """R#8 pins the ORDER, not just the permutation: epoch e of partition p lists the train ids by
+    ascending 64-bit key (out[0] << 32 | out[1]) of Philox(ctr = (id, e, 0, (p << 8) | 2), run_seed),
+    ties by ascending id.  The keys are recomputed through the KAT-pinned Philox (test above), so a
+    descending sort, a swapped key word, a wrong counter word or a dropped partition id all fail."""
+    n = 120
+    train = np.zeros(n, bool)
+    train[np.random.default_rng(3).choice(n, 70, replace=False)] = True
+    g = synth.Graph(n, np.zeros(n + 1, np.int64), np.zeros(0, np.int32), train)
+    W, parts = world_from(g, 2, D=0)
+    key = [RUN_SEED & 0xFFFFFFFF, RUN_SEED >> 32]
+    for pid in (0, 1):
+        ids = parts[pid].train_ids
+        for e in (0, 1, 7):
+            perm = W.parts[pid].epoch_perm(RUN_SEED, e, len(ids))
+            k = []
+            for v in perm.tolist():
+                o = O.philox([v, e, 0, (pid << 8) | 2], key)
+                k.append(((o[0] << 32) | o[1], v))
+            assert k == sorted(k), (pid, e)
+            assert sorted(perm.tolist()) == sorted(ids.tolist())
+        # seeds of step 1 = the first B ids of epoch 0 (R#8, O5)
+        p = W.parts[pid]
+        p.buffer_init(0.9, 0.5, 1.0, 0, 0)
+        p.step(RUN_SEED, 1, [1], 16)
+        assert p.frontier()[:p.hop_sizes()[0]].tolist() == p.epoch_perm(RUN_SEED, 0, len(ids))[:16].tolist()
+
+
 # ------------------------------------------------------------------ whole-step pins
 def _run_world(g, P, fanouts, B, f_bp, gamma, delta, theta, steps, D=4, bounds=None, check=None):
     W, parts = world_from(g, P, D=D, bounds=bounds)
