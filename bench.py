@@ -1,24 +1,25 @@
 """Benchmark: sampled+feature-ready minibatches/s of the halo feature pipeline
 (arXiv 2410.22697 prefetch + eviction) on B200, per BASELINE.json.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {mgnn,reference}]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {mgnn,reference}] [--config C]
     torchrun --nproc-per-node N bench.py --gpus N ...     (N > 1, one rank per GPU)
 
-Workload (BASELINE.json configs[1], fits one GPU): ogbn-arxiv-shaped synthetic
-graph (169,343 nodes, ~2.33M directed edges, 128-dim fp32 features), fanout
-[10, 25], batch 1000, P = 2 partitions per GPU (trainers), policy for P from
-the paper's GPU optima: P=2 (f=.25, gamma=.995, Delta=32), P=4
-(.50, .995, 32), P>=8 (.35, .995, 128); theta_R = 1.
-One bench "step" = one WINDOW of 32 consecutive minibatch steps for every
-partition on the GPU (sample, classify, gather, tally, decay, and the eviction
-round that ends the window when 32 | Delta): 32 x 2 minibatches per GPU.
-Software pipeline (the paper's prepare-ahead, Alg.1 l.9): in timed iteration i
-the sampling of window i+1 runs on a second stream concurrently with the
-classify/gather/score of window i; both streams join at the end of the
-iteration.  Timing: per-iteration CUDA events, L2 flushed (256 MB write)
-between timed iterations, max over ranks.  `e2e` drives the same pipeline
-through the C ABI with the seeds in pinned HOST memory (H2D inside mgnn_sample)
-and every window's per-minibatch counters read back to the host (D2H).
+Default workload (BASELINE.json configs[3], the largest config that fits one GPU with its own
+partitioning): ogbn-products-shaped synthetic graph (2,449,029 nodes, ~123.7M directed edges,
+100-dim fp32 features), fanout [5, 10, 15], batch 2000, 2 partitions (trainers) per GPU, policy
+for the total partition count P from the paper's GPU optima: P=2 (f=.50, gamma=.995,
+Delta=32), P=4 (.50, .995, 32), P=8 (.50, .9995, 16); theta_R = 1.  `--config arxiv` etc. select
+the other configs (arxiv's tables are L2-resident, so its line is not an HBM roofline).
+One bench "step" = one WINDOW of consecutive minibatch steps for every partition on the GPU
+(sample, classify, gather, tally, decay, and the eviction round that ends the window when the
+window length divides Delta): e.g. 32 x 2 minibatches per GPU for products at P = 2.
+Schedule (paper_2410_22697_b200/schedule.py, the paper's prepare-ahead, Alg.1 l.9): in timed
+iteration i the sampling of window i+1 runs on a second stream concurrently with the
+classify/gather/score of window i; both streams join at the end of the iteration.  Timing: per-
+iteration CUDA events, L2 flushed (256 MB write) between timed iterations, the K-iteration run
+repeated 3 times and the median reported, max over ranks.  `e2e` drives the same schedule through
+the C ABI with the seeds in pinned HOST memory (H2D inside mgnn_sample) and every window's
+per-minibatch counters read back to the host (D2H), same flush and per-iteration events.
 """
 from __future__ import annotations
 
@@ -26,6 +27,7 @@ import argparse
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -39,24 +41,23 @@ from inputs import synth  # noqa: E402
 
 METRIC = "sampled+feature-ready minibatches/sec"
 UNIT = "minibatches/s"
-WINDOW = 32
-PARTS_PER_GPU = 2
-CFG = synth.CONFIGS["arxiv"]
-REMOTE = False                     # NEXT-1 remote expansion (--remote)
-DENSE = False                      # NEXT-1 dense S_A (--dense)
+DEFAULT_CONFIG = "products"
 
 # Measurement policy (f_p in basis points, gamma, Delta) by config and total partitions P: the
-# paper's GPU optima; theta_R = 1.
+# paper's GPU optima; theta_R = 1.  Looked up for the P actually used.
 POLICY = {
     "cfg1": {2: (2500, 0.995, 64)},
     "arxiv": {2: (2500, 0.995, 32), 4: (5000, 0.995, 32), 8: (3500, 0.995, 128)},
     "reddit": {2: (3500, 0.995, 32), 4: (5000, 0.995, 256), 8: (5000, 0.95, 32)},
     "products": {2: (5000, 0.995, 32), 4: (5000, 0.995, 32), 8: (5000, 0.9995, 16)},
     "papers_s32": {8: (5000, 0.9995, 512)},
+    "papers": {8: (5000, 0.9995, 512)},
 }
-# partitions per GPU and window length per config (papers: all 8 partitions on one GPU at N=1,
-# short windows so the statically bounded window arenas fit in HBM)
-LAYOUT = {"cfg1": (2, 32), "arxiv": (2, 32), "reddit": (2, 32), "products": (2, 32), "papers_s32": (8, 8)}
+# default partitions per GPU (configs 1-4: 2 trainers per GPU, P = 2N; papers: P = 8 at every N,
+# 8/N per GPU) and the window length (steps per window; papers shorter: 8 trainers per GPU)
+LAYOUT = {"cfg1": (2, 32), "arxiv": (2, 32), "reddit": (2, 32), "products": (2, 32), "papers_s32": (8, 16),
+          "papers": (8, 16)}
+FIXED_P = {"papers_s32": 8, "papers": 8}
 WORKLOAD_TEXT = {
     "cfg1": "synthetic 10k-node graph, avg degree 10, 64-d fp32, fanout [10,25], batch 256 (BASELINE.json configs[0])",
     "arxiv": "ogbn-arxiv-shaped synthetic (169,343 nodes, ~2.33M directed edges, 128-d fp32), "
@@ -67,35 +68,45 @@ WORKLOAD_TEXT = {
                 "fanout [5,10,15], batch 2000 (BASELINE.json configs[3])",
     "papers_s32": "ogbn-papers100M-shaped synthetic at 1/32 scale (3.47M nodes, ~101M directed edges, 128-d fp32), "
                   "8 partitions, fanout [5,10,15], batch 2000 (BASELINE.json configs[4], scaled)",
+    "papers": "ogbn-papers100M-shaped synthetic (111,059,956 nodes, ~3.23B directed edges, 128-d fp32), "
+              "8 partitions, fanout [5,10,15], batch 2000 (BASELINE.json configs[4])",
 }
 
 
-def select_config(name: str) -> None:
-    global CFG, WINDOW, PARTS_PER_GPU
-    CFG = synth.CONFIGS[name]
-    PARTS_PER_GPU, WINDOW = LAYOUT[name]
+class Setup:
+    """Workload + layout chosen by the command line."""
 
+    def __init__(self, name: str, world: int, parts_per_gpu=None, parts=None, window=None):
+        self.name = name
+        self.cfg = synth.CONFIGS[name]
+        ppg, win = LAYOUT[name]
+        if parts is None and name in FIXED_P:
+            parts = FIXED_P[name]
+        if parts is not None:
+            if parts % world:
+                raise SystemExit(f"--parts {parts} is not a multiple of the {world} GPUs")
+            ppg = parts // world
+        elif parts_per_gpu is not None:
+            ppg = parts_per_gpu
+        self.ppg = ppg
+        self.P = ppg * world
+        table = POLICY[name]
+        k = min((q for q in table if q >= self.P), default=max(table))
+        self.policy_P = k
+        self.f_bp, self.gamma, self.delta = table[k]
+        w = window or win
+        self.window = min(w, self.delta) if self.delta > 0 else w
 
-def policy_for(P: int):
-    table = POLICY[CFG.name]
-    k = min((q for q in table if q >= P), default=max(table))
-    f_bp, gamma, delta = table[k]
-    return f_bp, gamma, delta
-
-
-def window_for(delta: int) -> int:
-    """Steps per window: a window may end on an eviction step but not contain one earlier."""
-    return min(WINDOW, delta) if delta > 0 else WINDOW
-
-
-def workload(P: int) -> dict:
-    f_bp, gamma, delta = policy_for(P)
-    return {
-        "workload": WORKLOAD_TEXT[CFG.name],
-        "partitions": P, "partitions_per_gpu": PARTS_PER_GPU, "f_p": f_bp / 10000, "gamma": gamma, "delta": delta,
-        "theta_r": 1.0, "window_steps": WINDOW, "minibatches_per_step_per_gpu": WINDOW * PARTS_PER_GPU,
-        "l2": "flushed (256 MB write) between timed windows",
-    }
+    def workload(self) -> dict:
+        return {
+            "workload": WORKLOAD_TEXT[self.name], "config_name": self.name,
+            "partitions": self.P, "partitions_per_gpu": self.ppg,
+            "layout": ("P = 2 trainers per GPU (P = 2N)" if self.ppg == 2 and self.name not in FIXED_P else
+                       f"P = {self.P} partitions, {self.ppg} per GPU"),
+            "policy_for_P": self.policy_P, "f_p": self.f_bp / 10000, "gamma": self.gamma, "delta": self.delta,
+            "theta_r": 1.0, "window_steps": self.window, "minibatches_per_step_per_gpu": self.window * self.ppg,
+            "l2": "flushed (256 MB write) between timed windows",
+        }
 
 
 # ---------------------------------------------------------------- clocks
@@ -186,20 +197,60 @@ def peer_copy_gbs(src: int, dst: int):
         return None
 
 
+def nvlink_counters(index: int):
+    """NVLink throughput counters of one GPU (NVML field values, KiB since driver load; None if the
+    driver does not expose them): read before and after the timed region, so the difference is the
+    bytes that crossed this GPU's links while it ran."""
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(index)
+        ids = [nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX]
+        vals = nv.nvmlDeviceGetFieldValues(h, ids)
+        out = []
+        for v in vals:
+            if v.nvmlReturn != 0:
+                return None
+            out.append(int(v.value.ullVal))
+        return out
+    except Exception:
+        return None
+
+
+def traffic_table(name: str):
+    """Per-config ncu DRAM bytes per launch (profiles/r02/traffic_<config>.json, written by
+    tools/ncu_traffic.py from a committed `ncu --set full` capture of this config); None if absent."""
+    p = os.path.join(ROOT, "profiles", "r02", f"traffic_{name}.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d if d.get("config") == name else None
+    except (OSError, ValueError):
+        return None
+
+
+def git_head():
+    try:
+        return subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], cwd=ROOT, capture_output=True,
+                              text=True, timeout=10).stdout.strip() or None
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------- oracle timings (test infrastructure)
-def oracle_rate(parts, P, f_bp, gamma, delta, budget_s: float, min_steps: int = 8):
+def oracle_rate(S: Setup, parts, budget_s: float, remote=False, dense=False, min_steps: int = 8):
     """Oracle (oracle/orc.c, single thread) on the same workload: minibatches/s over a bounded sample."""
     from oracle import oracle as O
-    W = O.World(parts, CFG.feat_dim, synth.FEAT_SEED, dense=DENSE)
-    alpha = O.alpha_default(gamma, delta)
+    W = O.World(parts, S.cfg.feat_dim, synth.FEAT_SEED, dense=dense)
+    alpha = O.alpha_default(S.gamma, S.delta)
     for p in W.parts:
-        p.buffer_init(gamma, alpha, 1.0, delta, f_bp)
-        p.set_expand_remote(REMOTE)
+        p.buffer_init(S.gamma, alpha, 1.0, S.delta, S.f_bp)
+        p.set_expand_remote(remote)
     t0 = time.perf_counter()
     n_mb, step = 0, 1
     while True:
         for p in W.parts:
-            p.step(synth.RUN_SEED, step, CFG.fanouts, CFG.batch)
+            p.step(synth.RUN_SEED, step, S.cfg.fanouts, S.cfg.batch)
             n_mb += 1
         step += 1
         el = time.perf_counter() - t0
@@ -209,23 +260,23 @@ def oracle_rate(parts, P, f_bp, gamma, delta, budget_s: float, min_steps: int = 
     return n_mb / el, n_mb, el
 
 
-def oracle_rate_threads(parts, P, f_bp, gamma, delta, budget_s: float):
+def oracle_rate_threads(S: Setup, parts, budget_s: float, remote=False, dense=False):
     """The same oracle with one host thread per partition (the C steps release the GIL; partitions
     are independent between eviction rounds of their own buffers): SURVEY §8(d)'s P-thread rate."""
     import threading as th
     from oracle import oracle as O
-    W = O.World(parts, CFG.feat_dim, synth.FEAT_SEED, dense=DENSE)
-    alpha = O.alpha_default(gamma, delta)
+    W = O.World(parts, S.cfg.feat_dim, synth.FEAT_SEED, dense=dense)
+    alpha = O.alpha_default(S.gamma, S.delta)
     for p in W.parts:
-        p.buffer_init(gamma, alpha, 1.0, delta, f_bp)
-        p.set_expand_remote(REMOTE)
+        p.buffer_init(S.gamma, alpha, 1.0, S.delta, S.f_bp)
+        p.set_expand_remote(remote)
     counts = [0] * len(W.parts)
     t0 = time.perf_counter()
 
     def run(i):
         step = 1
         while time.perf_counter() - t0 < budget_s or step <= 8:
-            W.parts[i].step(synth.RUN_SEED, step, CFG.fanouts, CFG.batch)
+            W.parts[i].step(synth.RUN_SEED, step, S.cfg.fanouts, S.cfg.batch)
             counts[i] += 1
             step += 1
 
@@ -250,45 +301,49 @@ def host_cpu():
     return "unknown"
 
 
-def run_reference(args):
+def run_reference(args, S: Setup):
+    """The reference arm: the oracle (no reference code exists; /root/reference holds only the paper)
+    on the same workload, the GPU's hosted partitions, steps in order from t = 1.  Each bench step is
+    a bounded sample of a window (`ref_steps` consecutive steps of every hosted partition) so the
+    whole --steps K --warmup W run stays within a few minutes."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    global WINDOW
-    P = PARTS_PER_GPU * args.gpus
-    f_bp, gamma, delta = policy_for(P)
-    WINDOW = window_for(delta)
-    g = synth.generate(CFG)
-    parts = synth.partition(g, P)
-    # each reference "step" = the same 32 x (partitions on one GPU) minibatches, bounded by time
-    per_step = WINDOW * PARTS_PER_GPU
+    g = synth.generate(S.cfg)
+    parts = synth.partition(g, S.P)
     from oracle import oracle as O
-    W = O.World(parts, CFG.feat_dim, synth.FEAT_SEED)
-    alpha = O.alpha_default(gamma, delta)
+    mine_ids = list(range(S.ppg))
+    W = O.World([parts[i] for i in range(S.P)], S.cfg.feat_dim, synth.FEAT_SEED)
+    alpha = O.alpha_default(S.gamma, S.delta)
     for p in W.parts:
-        p.buffer_init(gamma, alpha, 1.0, delta, f_bp)
-    mine = W.parts[:PARTS_PER_GPU]
+        p.buffer_init(S.gamma, alpha, 1.0, S.delta, S.f_bp)
+    mine = [W.parts[i] for i in mine_ids]
+    # steps per reference bench step: ~1 s of single-thread work at the oracle's rate on this config
+    per_mb_s = {"cfg1": 0.001, "arxiv": 0.006, "reddit": 0.035, "products": 0.075, "papers_s32": 0.04,
+                "papers": 0.1}.get(S.name, 0.05)
+    ref_steps = int(max(1, min(S.window, round(1.0 / (per_mb_s * S.ppg)))))
     t = 1
     times = []
     for k in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        for w in range(WINDOW):
+        for w in range(ref_steps):
             for p in mine:
-                p.step(synth.RUN_SEED, t + w, CFG.fanouts, CFG.batch)
+                p.step(synth.RUN_SEED, t + w, S.cfg.fanouts, S.cfg.batch)
         if k >= args.warmup:
             times.append(time.perf_counter() - t0)
-        t += WINDOW
+        t += ref_steps
     W.close()
     total = sum(times)
+    per_step = ref_steps * S.ppg
     value = per_step * args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": workload(P),
+        "config": S.workload(),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{args.steps} windows x {per_step} minibatches of partitions 0-1 (P={P}), "
-                                   "single-threaded C oracle"},
+                         "sample": f"{args.steps} bench steps x {ref_steps} consecutive steps x {S.ppg} hosted "
+                                   f"partitions (P={S.P}), steps 1..{t - 1} in order, single-threaded C oracle"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -300,32 +355,35 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--runs", type=int, default=3, help="timed runs of --steps iterations; the median is reported")
     ap.add_argument("--impl", default="mgnn", choices=["mgnn", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(LAYOUT),
+                    help=f"workload (default: {DEFAULT_CONFIG}-shaped, BASELINE.json configs[3])")
+    ap.add_argument("--parts-per-gpu", type=int, default=None, help="partitions (trainers) per GPU")
+    ap.add_argument("--parts", type=int, default=None, help="total partitions P (a multiple of the GPU count)")
+    ap.add_argument("--window", type=int, default=None, help="steps per window (default per config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-extras", action="store_true", help="skip the with_consumer / with_training lines")
     ap.add_argument("--no-train-graph", action="store_true", help="training steps as eager launches")
     ap.add_argument("--remote", action="store_true",
                     help="NEXT-1: sample non-local frontier nodes from their owner's CSR")
     ap.add_argument("--dense", action="store_true", help="NEXT-1: dense S_A (every non-local node scorable)")
     ap.add_argument("--hash-partition", action="store_true",
                     help="NEXT-4 stress: partitions of a randomly relabelled graph (hash partitioner)")
-    ap.add_argument("--config", default="arxiv", choices=sorted(LAYOUT),
-                    help="workload (default: arxiv-shaped, BASELINE.json configs[1])")
     args = ap.parse_args()
-    global WINDOW, REMOTE, DENSE
-    select_config(args.config)
-    REMOTE = args.remote
-    DENSE = args.dense
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    S = Setup(args.config, world if args.impl == "mgnn" else args.gpus, args.parts_per_gpu, args.parts, args.window)
     if args.impl == "reference":
-        return run_reference(args)
+        return run_reference(args, S)
 
     import torch
     import torch.distributed as dist
     from paper_2410_22697_b200 import pipeline as PL
+    from paper_2410_22697_b200.schedule import PrepareAhead
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
@@ -343,23 +401,22 @@ def main():
             sys.stdout.flush()
             os.dup2(saved, 1)
             os.close(saved)
-    P = PARTS_PER_GPU * world
-    f_bp, gamma, delta = policy_for(P)
-    WINDOW = window_for(delta)
-    g = synth.generate(CFG)
+    cfg = S.cfg
+    WINDOW = S.window
+    g = synth.generate(cfg)
     if args.hash_partition:
         g = synth.hash_relabel(g)
-    parts = synth.partition(g, P)
-    hosted = list(range(PARTS_PER_GPU * rank, PARTS_PER_GPU * (rank + 1)))
-    ctx = PL.build_context(local, parts, CFG.feat_dim, synth.FEAT_SEED, hosted, dense=args.dense)
+    parts = synth.partition(g, S.P)
+    hosted = list(range(S.ppg * rank, S.ppg * (rank + 1)))
+    ctx = PL.build_context(local, parts, cfg.feat_dim, synth.FEAT_SEED, hosted, dense=args.dense)
     if world > 1:
         PL.exchange_tables(ctx)
-    alpha = PL.alpha_default(gamma, delta)
+    alpha = PL.alpha_default(S.gamma, S.delta)
     # INITIALIZE_PREFETCHER cost ("<1% of overall training"), CUDA events on the init stream
     i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     i0.record()
-    ctx.buffer_init(gamma, alpha, 1.0, delta, f_bp)
+    ctx.buffer_init(S.gamma, alpha, 1.0, S.delta, S.f_bp)
     i1.record()
     torch.cuda.synchronize()
     init_ms = i0.elapsed_time(i1)
@@ -367,143 +424,234 @@ def main():
         if world > 1:
             ctx.load_global_csr(g.indptr, g.cols)       # replicated global CSR on every GPU
         ctx.expand_remote(True)
-    ctx.sampler_config(CFG.fanouts, CFG.batch, synth.RUN_SEED, WINDOW)
+    ctx.sampler_config(cfg.fanouts, cfg.batch, synth.RUN_SEED, WINDOW)
     stream = torch.cuda.current_stream()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
 
+    def max_over_ranks(x: float) -> float:
+        t_ = torch.tensor([x], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        return float(t_.item())
+
     # Two streams = the paper's prepare-ahead overlap (Alg.1 l.9): NeighborSampler of window w+1
-    # (needs no buffer state) runs on sA while window w is classified/gathered/scored on sB.
-    sA = torch.cuda.Stream()
-    sB = stream
-    ev_sampled = [torch.cuda.Event(), torch.cuda.Event()]
-    ev_done = [torch.cuda.Event(), torch.cuda.Event()]
-
-    def sample_async(sl, tt):
-        sA.wait_event(ev_done[sl])            # slot free once its previous window was gathered + scored
-        ctx.sample(sl, tt, WINDOW, stream=sA)
-        ev_sampled[sl].record(sA)
-
-    def consume(sl):
-        sB.wait_event(ev_sampled[sl])
-        ctx.lookup_gather(sl, sB)
-        ctx.score(sl, sB)
-        ev_done[sl].record(sB)
-
-    t = 1
-    slot = 0
-    sample_async(0, t)
+    # (needs no buffer state) runs on stream A while window w is classified/gathered/scored on B.
+    pipe = PrepareAhead(ctx, WINDOW, t0=1, stream_b=stream)
     for _ in range(args.warmup):
-        sample_async(slot ^ 1, t + WINDOW)
-        consume(slot)
-        t += WINDOW
-        slot ^= 1
-    # ---------------- timed region (device path: inputs resident in HBM)
+        pipe.iteration()
+    # ---------------- timed region (device path: inputs resident in HBM); R runs, median reported
     K = args.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    R = max(1, args.runs)
+    mb_total = WINDOW * S.ppg * world * K
+    nv0 = nvlink_counters(local) if world > 1 else None
     launches0 = ctx.launch_count()
     ctx.profile(True)
-    ctx.profile_read()
-    hits = misses = 0
-    barrier()
+    ctx.profile_stages()                         # reset
+    runs = []
+    prof = {}
+    wall = 0.0
     with ClockSampler(local) as clk:
-        wall0 = time.perf_counter()
-        for i in range(K):
-            flush.zero_()                      # L2 flush between timed iterations (not timed)
-            ev[i][0].record(sB)
-            sA.wait_event(ev[i][0])
-            sample_async(slot ^ 1, t + WINDOW)  # window i+1: sampling stream
-            consume(slot)                       # window i: buffer stream
-            sB.wait_stream(sA)
-            ev[i][1].record(sB)
-            t += WINDOW
-            slot ^= 1
-        barrier()
-        wall = time.perf_counter() - wall0
-    launches = ctx.launch_count() - launches0
-    gms, glaunch, gbytes = ctx.profile_read()
+        for r in range(R):
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+            barrier()
+            wall0 = time.perf_counter()
+            for i in range(K):
+                pipe.iteration(events=ev[i])
+            barrier()
+            wall += time.perf_counter() - wall0
+            tot_ms = sum(a.elapsed_time(b) for a, b in ev)
+            max_ms = max_over_ranks(tot_ms)
+            runs.append({"value": mb_total / (max_ms / 1e3), "ms_per_step": max_ms / K, "my_ms": tot_ms})
+            ps = ctx.profile_stages()
+            for k_, v_ in ps.items():
+                prof[k_] = prof.get(k_, 0.0) + v_
     ctx.profile(False)
-    c = ctx.counts(slot ^ 1, stream)            # the last consumed window
-    hits += int(c[:, 2].sum())
-    misses += int(c[:, 3].sum())
+    launches = ctx.launch_count() - launches0
+    nv1 = nvlink_counters(local) if world > 1 else None
+    clocks = clk.summary()
+    order = sorted(range(R), key=lambda j: runs[j]["value"])
+    med = runs[order[R // 2]]
+    value = med["value"]
+    c = ctx.counts(pipe.slot ^ 1, stream)       # the last consumed window
+    hits = int(c[:, 2].sum())
+    misses = int(c[:, 3].sum())
     peer_rows = int(c[:, 7].sum())              # rows read from another GPU's table over NVLink
-    ms = [a.elapsed_time(b) for a, b in ev]
-    tot_ms = sum(ms)
-    mine_ms = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(mine_ms, op=dist.ReduceOp.MAX)
-    max_ms = float(mine_ms.item())
-    mb_total = WINDOW * PARTS_PER_GPU * world * K
-    value = mb_total / (max_ms / 1e3)
 
-    # ---------------- e2e: host seeds (pinned) -> C ABI -> counts back to host, every window
-    # The seeds a user passes are this window's F_0; take them from the library's epoch order by
-    # sampling the same steps first (sampling reads no buffer state), outside the timed region.
-    n_inst = PARTS_PER_GPU * WINDOW
+    # ---------------- e2e: host seeds (pinned) -> C ABI -> counts back to host, every window, through the
+    # same schedule (flush between iterations, per-iteration events).  The seeds a user passes are the
+    # window's F_0; take them from the library's epoch order by sampling the same steps first (sampling
+    # reads no buffer state), outside the timed region.
+    n_inst = S.ppg * WINDOW
     E2E = max(3, K)
-    t_e2e = t
-    seeds_h, counts_h = [], []
+    pipe.iteration(prepare_next=False)          # consume the window the device run left prepared
+    t_e2e = pipe.t
+    seeds_h, counts_h = {}, {}
+    slot = pipe.slot
     for i in range(E2E):
-        ctx.sample(slot, t_e2e + i * WINDOW, WINDOW, stream=stream)
+        tt = t_e2e + i * WINDOW
+        ctx.sample(slot, tt, WINDOW, stream=stream)
         wv = ctx.window(slot)
         n0 = PL.device_view(wv.hop_size, (wv.n_inst, 9), "i8")[:, 0].to(torch.int32)
-        f0 = PL.device_view(wv.frontier, (wv.n_inst, wv.rows_stride), "i4")[:, :CFG.batch]
-        seeds_h.append(f0.cpu().pin_memory())
-        counts_h.append(n0.cpu().pin_memory())
-    h2d = n_inst * CFG.batch * 4 + n_inst * 4
+        f0 = PL.device_view(wv.frontier, (wv.n_inst, wv.rows_stride), "i4")[:, :cfg.batch]
+        seeds_h[tt] = f0.cpu().pin_memory()
+        counts_h[tt] = n0.cpu().pin_memory()
+    h2d = n_inst * cfg.batch * 4 + n_inst * 4
     d2h = n_inst * 8 * 8
     cbuf = [torch.zeros((n_inst, 8), dtype=torch.int64).pin_memory() for _ in range(2)]
     ev_cnt = [torch.cuda.Event(), torch.cuda.Event()]
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2e_hits = 0
+    state = {"i": 0, "hits": 0}
+    epipe = PrepareAhead(ctx, WINDOW, t0=t_e2e, stream_b=stream,
+                         host_seeds=lambda sl, tt: (seeds_h[tt].data_ptr(), counts_h[tt].data_ptr()))
+    epipe.sA = pipe.sA
+    epipe.flush = pipe.flush
 
-    def sample_host(sl, i):                    # H2D of window i's seeds inside mgnn_sample (stream A)
-        sA.wait_event(ev_done[sl])
-        ctx.sample_ptr(sl, t_e2e + i * WINDOW, WINDOW, seeds_h[i].data_ptr(), counts_h[i].data_ptr(), True, sA)
-        ev_sampled[sl].record(sA)
-
-    barrier()
-    ev0.record(sB)
-    sA.wait_event(ev0)
-    sample_host(slot, 0)
-    for i in range(E2E):                       # same two-stream pipeline, host buffers at both ends
-        if i + 1 < E2E:
-            sample_host(slot ^ 1, i + 1)
-        sB.wait_event(ev_sampled[slot])
-        ctx.lookup_gather(slot, sB)
-        ctx.score(slot, sB)
-        ctx.counts_async(slot, cbuf[i % 2].data_ptr(), sB)      # D2H of the window's counters
+    def read_counts(sl, t0_, sB):
+        i = state["i"]
+        ctx.counts_async(sl, cbuf[i % 2].data_ptr(), sB)      # D2H of the window's counters
         ev_cnt[i % 2].record(sB)
-        ev_done[slot].record(sB)
+
+    ev_e = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(E2E)]
+    barrier()
+    for i in range(E2E):
+        state["i"] = i
+        epipe.iteration(events=ev_e[i], after_consume=read_counts, prepare_next=i + 1 < E2E)
         if i >= 1:                             # read the previous window's counters on the host
             ev_cnt[(i - 1) % 2].synchronize()
-            e2e_hits += int(cbuf[(i - 1) % 2][:, 2].sum())
-        slot ^= 1
-    ev1.record(sB)
+            state["hits"] += int(cbuf[(i - 1) % 2][:, 2].sum())
     ev_cnt[(E2E - 1) % 2].synchronize()
-    e2e_hits += int(cbuf[(E2E - 1) % 2][:, 2].sum())
+    state["hits"] += int(cbuf[(E2E - 1) % 2][:, 2].sum())
     barrier()
-    e2e_ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = WINDOW * PARTS_PER_GPU * world * E2E / (float(e2e_ms.item()) / 1e3)
+    e2e_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev_e))
+    e2e_value = WINDOW * S.ppg * world * E2E / (e2e_ms / 1e3)
+    t_next = epipe.t
+    slot = epipe.slot
 
+    line_extra = {}
+    if not args.no_extras:
+        line_extra = extras(args, S, ctx, pipe, t_next, slot, world, barrier, max_over_ranks, mb_total, K,
+                            med["ms_per_step"], prof, R)
+
+    if rank == 0:
+        peaks = {}
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                peaks = json.load(f)
+        except OSError:
+            pass
+        hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+        peak_src = ("MEASURED_PEAKS.json hbm_gbs (measured copy, burst: each kernel is timed alone per launch)"
+                    if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)")
+        n_win = R * K
+        g_ms = prof["gather_ms"] / max(prof["gather_calls"], 1)
+        g_bytes = 2.0 * prof["gather_rows"] * cfg.feat_dim * 4 / max(prof["gather_calls"], 1)
+        achieved = g_bytes / (g_ms / 1e3) / 1e9 if g_ms > 0 else None
+        s_ms = prof["sample_ms"] / max(prof["sample_calls"], 1)
+        s_bytes = (8.0 * prof["edges"] + 24.0 * prof["frontier"] + 8.0 * prof["unique"]) / max(prof["sample_calls"], 1)
+        s_ach = s_bytes / (s_ms / 1e3) / 1e9 if s_ms > 0 else None
+        tt_ = traffic_table(S.name)
+        step_ms_sum = sum(r_["my_ms"] for r_ in runs)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": med["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (seeded planted-block R-MAT graph, Philox features)",
+            "config": dict(S.workload(), **({"sampling": "remote expansion (NEXT-1)"} if args.remote else {}),
+                           **({"scores": "dense S_A (NEXT-1)"} if args.dense else {}),
+                           **({"partitioner": "hash (random relabel)"} if args.hash_partition else {}),
+                           graph_stats=synth.describe(g, parts)),
+            "runs": [r_["value"] for r_ in runs], "median_of": R,
+            "buffer_init_ms": init_ms,
+            "hit_rate": hits / max(1, hits + misses),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "steps": E2E, "path": "schedule.PrepareAhead with host seeds: mgnn_sample(pinned host seeds, "
+                                          "H2D) | lookup_gather + score_evict_refill + counts_read_async (D2H); "
+                                          "host reads each window's counters; L2 flushed between windows"},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "kernel": "k_gather_tma (classify + feature-row gather)",
+                         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": (achieved / hbm_peak) if achieved else None,
+                         "traffic": (tt_ or {}).get("k_gather_tma"),
+                         "traffic_source": (tt_ or {}).get("source"),
+                         "peak_source": peak_src, "launch_ms": g_ms, "share_of_step": prof["gather_ms"] / step_ms_sum,
+                         "algorithmic_bytes_per_launch": g_bytes,
+                         "algorithmic": "2 * rows * D * 4 (row read + X write, SURVEY §8(d))"},
+            "sampler_roofline": {
+                "bound": "hbm", "kernels": "k_hop x L + k_compact x L + k_relabel (stream A, beside the gather)",
+                "achieved": s_ach, "peak": hbm_peak, "unit": "GB/s", "frac": (s_ach / hbm_peak) if s_ach else None,
+                "ms_per_window": s_ms, "share_of_step": prof["sample_ms"] / step_ms_sum,
+                "algorithmic_bytes_per_window": s_bytes,
+                "algorithmic": "8 E + 24 F + 8 U (SURVEY §8(d)): E sampled edges, F expanded frontier nodes, U = |F_L|",
+                "per_window": {"E": prof["edges"] / max(prof["sample_calls"], 1),
+                               "F": prof["frontier"] / max(prof["sample_calls"], 1),
+                               "U": prof["unique"] / max(prof["sample_calls"], 1)},
+                "traffic": {k_: v_ for k_, v_ in (tt_ or {}).items() if k_ in ("k_hop", "k_compact", "k_relabel")}
+                or None},
+            "stages_ms_per_window": {"sample": s_ms, "gather": g_ms,
+                                     "score": prof["score_ms"] / max(prof["score_calls"], 1),
+                                     "window_pipelined": med["ms_per_step"],
+                                     "note": "CUDA events per call on the stream it runs on, inside the timed runs"},
+            "clocks": clocks,
+            "wall_s_timed_region": wall,
+            "git_head": git_head(),
+        }
+        line.update(line_extra)
+        if world > 1:
+            nv_bytes = peer_rows * cfg.feat_dim * 4
+            gbs = nv_bytes / (g_ms / 1e3) / 1e9 if g_ms > 0 else None
+            peer = peer_copy_gbs(local, (local + 1) % torch.cuda.device_count())
+            cnt = None
+            if nv0 and nv1:
+                cnt = {"tx_bytes_per_window": (nv1[0] - nv0[0]) * 1024 / n_win,
+                       "rx_bytes_per_window": (nv1[1] - nv0[1]) * 1024 / n_win,
+                       "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX (KiB) of this GPU around the timed runs"}
+            line["nvlink"] = {"peer_rows_per_window": peer_rows, "bytes_per_window": nv_bytes,
+                              "gbs_during_gather": gbs,
+                              "peak_gbs": 900.0, "peak_source": "NVLink 5 nominal per direction per GPU",
+                              "frac": gbs / 900.0 if gbs else None,
+                              "achievable_peer_copy_gbs": peer,
+                              "frac_of_achievable": gbs / peer if (gbs and peer) else None,
+                              "counters": cnt,
+                              "note": "miss + refill rows whose owner is on another GPU, read by peer loads "
+                                      "inside k_gather / k_swap_refill (last timed window); achievable = "
+                                      "256 MB device-to-device copy to the next GPU, best of 5"}
+        if world == 1 and not args.no_cpu_baseline:
+            rate, n_mb, el = oracle_rate(S, parts, args.cpu_budget, args.remote, args.dense)
+            rate_p, n_thr = oracle_rate_threads(S, parts, min(args.cpu_budget, 6.0), args.remote, args.dense)
+            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                    "sample": f"{n_mb} minibatches (steps 1..{n_mb // S.P} of all {S.P} partitions), "
+                                              f"{el:.1f} s, single-threaded C oracle",
+                                    "value_one_thread_per_partition": rate_p, "threads": n_thr,
+                                    "host_cpu": host_cpu(), "host_nproc": os.cpu_count()}
+        print(json.dumps(line), flush=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()                 # peers read our feature tables until everyone is done
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def extras(args, S, ctx, pipe, t_start, slot, world, barrier, max_over_ranks, mb_total, K, prep_ms, prof, R):
+    """with_consumer (A14) and with_training (NEXT-3) lines, plus the Eq.4-5 stage report."""
+    import torch
+    from paper_2410_22697_b200 import pipeline as PL
+    cfg = S.cfg
+    WINDOW = S.window
+    sA, sB = pipe.sA, pipe.sB
+    ev_sampled = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_done = [torch.cuda.Event(), torch.cuda.Event()]
+    flush = pipe.flush
     # ---------------- with consumer (A14): the same pipeline plus the GraphSAGE-mean forward of every
-    # minibatch (mgnn_sage_forward, tcgen05 TF32) between gather and score on the buffer stream, with
-    # the sampling of the next window still overlapped on stream A (Alg.1 l.6-9).
-    dims = synth.sage_dims(CFG.feat_dim, len(CFG.fanouts), synth.N_CLASSES[CFG.name])
+    # minibatch (mgnn_sage_forward, tcgen05 TF32) on stream C, while stream B gathers and scores window
+    # w+1 and stream A samples window w+2; a slot is resampled only after its score (B) and forward (C).
+    dims = synth.sage_dims(cfg.feat_dim, len(cfg.fanouts), synth.N_CLASSES[cfg.name])
     wts = synth.sage_weights(dims)
     ctx.sage_config(dims, [w_[0] for w_ in wts], [w_[1] for w_ in wts], [w_[2] for w_ in wts])
-    logits = torch.empty((PARTS_PER_GPU * WINDOW, CFG.batch, dims[-1]), dtype=torch.float32, device="cuda")
+    logits = torch.empty((S.ppg * WINDOW, cfg.batch, dims[-1]), dtype=torch.float32, device="cuda")
     fwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-
-    # Alg.1 overlap: the consumer of window w runs on its own stream C while stream B gathers and
-    # scores window w+1 and stream A samples window w+2; a slot is resampled only after both its
-    # score (B) and its forward pass (C) are done.
     sC = torch.cuda.Stream()
     ev_gathered = [torch.cuda.Event(), torch.cuda.Event()]
     ev_fwd = [torch.cuda.Event(), torch.cuda.Event()]
@@ -529,7 +677,7 @@ def main():
             fwd_ev[i][1].record(sC)
         ev_fwd[sl].record(sC)
 
-    t_c = t_e2e + E2E * WINDOW
+    t_c = t_start
     barrier()
     sample_async_c(slot, t_c)
     for _ in range(args.warmup):
@@ -553,16 +701,14 @@ def main():
     sB.wait_stream(sC)
     c1.record(sB)
     barrier()
-    c_ms = torch.tensor([c0.elapsed_time(c1)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(c_ms, op=dist.ReduceOp.MAX)
-    c_value = mb_total / (float(c_ms.item()) / 1e3)
+    c_ms = max_over_ranks(c0.elapsed_time(c1))
+    c_value = mb_total / (c_ms / 1e3)
     fwd_ms = sum(a.elapsed_time(b) for a, b in fwd_ev) / K
     # algorithmic work of the last forward (window slot ^ 1): per layer 2 * n_dst * (2 d_in) * d_out
     # flops (dense part) and the neighbour rows it averages (4 * d_in bytes per sampled edge)
     wv = ctx.window(slot ^ 1)
     hs = PL.device_view(wv.hop_size, (wv.n_inst, 9), "i8").cpu().numpy()
-    L_ = len(CFG.fanouts)
+    L_ = len(cfg.fanouts)
     flops = 0.0
     agg_bytes = 0.0
     for l in range(L_):
@@ -577,9 +723,9 @@ def main():
     # backward, NCCL all-reduce of the gradients across ranks (N > 1), SGD -- on stream C, one
     # DDP step per window step (the steps of a window are sequential through the weights), while
     # streams A/B prepare the next windows (Alg.1: prepare(t+1) || train(t)).
-    labels = synth.node_labels(CFG.n_nodes, dims[-1])
+    labels = synth.node_labels(cfg.n_nodes, dims[-1])
     ctx.train_config(labels)
-    n_trainers = PARTS_PER_GPU * world
+    n_trainers = S.ppg * world
     lr = 0.01
     ev_trained = [torch.cuda.Event(), torch.cuda.Event()]
 
@@ -589,19 +735,17 @@ def main():
         ctx.sample(sl, tt, WINDOW, stream=sA)
         ev_sampled[sl].record(sA)
 
-    # The WINDOW DDP steps of a slot are one CUDA graph (captured once per slot, replayed every
-    # window): ~12 launches per step, all device-resident sizes, so the graph is static.
     graphs = {}
     # one rank: graph capture; N > 1 keeps eager launches (the step is GPU-bound either way, and a
     # graph holding captured NCCL work hung the process teardown)
     use_graph = [not args.no_train_graph and world == 1]
 
-    def train_window(sl):
+    def train_window(sl, stream_):
         if use_graph[0]:
             if sl not in graphs:
                 try:
                     g_ = torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(g_, stream=sC):
+                    with torch.cuda.graph(g_, stream=stream_):
                         for w_ in range(WINDOW):
                             PL.ddp_step(ctx, sl, w_, n_trainers, lr, stream=torch.cuda.current_stream())
                     graphs[sl] = g_
@@ -609,20 +753,28 @@ def main():
                     print(f"[bench] training graph capture failed ({e!r}); eager launches", file=sys.stderr)
                     use_graph[0] = False
             if use_graph[0]:
-                with torch.cuda.stream(sC):
+                with torch.cuda.stream(stream_):
                     graphs[sl].replay()
                 return
         for w_ in range(WINDOW):
-            PL.ddp_step(ctx, sl, w_, n_trainers, lr, stream=sC)
+            PL.ddp_step(ctx, sl, w_, n_trainers, lr, stream=stream_)
 
-    def consume_train(sl):
+    tw_ev = []
+
+    def consume_train(sl, timed=False):
         sB.wait_event(ev_sampled[sl])
         ctx.lookup_gather(sl, sB)
         ev_gathered[sl].record(sB)
         ctx.score(sl, sB)
         ev_done[sl].record(sB)
         sC.wait_event(ev_gathered[sl])
-        train_window(sl)
+        if timed:
+            e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            e[0].record(sC)
+        train_window(sl, sC)
+        if timed:
+            e[1].record(sC)
+            tw_ev.append(e)
         ev_trained[sl].record(sC)
 
     KT = max(3, min(K, 6))
@@ -643,113 +795,71 @@ def main():
     sC.wait_event(t0e)
     for i in range(KT):
         sample_async_t(slot ^ 1, t_t + WINDOW)
-        consume_train(slot)
+        consume_train(slot, timed=True)
         t_t += WINDOW
         slot ^= 1
     sB.wait_stream(sA)
     sB.wait_stream(sC)
     t1e.record(sB)
     barrier()
-    tr_ms = torch.tensor([t0e.elapsed_time(t1e)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(tr_ms, op=dist.ReduceOp.MAX)
-    tr_value = WINDOW * PARTS_PER_GPU * world * KT / (float(tr_ms.item()) / 1e3)
+    tr_ms = max_over_ranks(t0e.elapsed_time(t1e))
+    tr_value = WINDOW * S.ppg * world * KT / (tr_ms / 1e3)
     tr_loss_t = torch.tensor([ctx.loss(sC) / (KT * WINDOW)], dtype=torch.float64, device="cuda")
     if world > 1:                       # each rank holds its trainers' share of the mean loss
+        import torch.distributed as dist
         dist.all_reduce(tr_loss_t)
     tr_loss = float(tr_loss_t.item())
-
-    clocks = clk.summary()
-    if rank == 0:
-        peaks = {}
-        try:
-            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-                peaks = json.load(f)
-        except OSError:
-            pass
-        hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-        peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
-        g_avg_ms = gms / max(glaunch, 1)
-        g_bytes = gbytes / max(glaunch, 1)
-        achieved = g_bytes / (g_avg_ms / 1e3) / 1e9 if g_avg_ms > 0 else None
-        traffic = None
-        tpath = os.path.join(ROOT, "profiles", "gather_traffic.json")
-        if os.path.exists(tpath):
-            try:
-                traffic = json.load(open(tpath)).get("bytes_per_launch")
-            except (OSError, ValueError):
-                traffic = None
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic",
-            "config": dict(workload(P), **({"sampling": "remote expansion (NEXT-1)"} if args.remote else {}),
-                           **({"scores": "dense S_A (NEXT-1)"} if args.dense else {}),
-                           **({"partitioner": "hash (random relabel)"} if args.hash_partition else {})),
-            "buffer_init_ms": init_ms,
-            "hit_rate": hits / max(1, hits + misses),
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "steps": E2E, "path": "two-stream pipeline: mgnn_sample(host pinned seeds, H2D) | "
-                                          "lookup_gather + score_evict_refill + counts_read_async (D2H), "
-                                          "host reads each window's counters"},
-            "gpu_launches": int(launches),
-            "roofline": {"bound": "hbm", "kernel": "k_gather (classify + feature-row gather)",
-                         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
-                         "peak_source": peak_src, "launch_ms": g_avg_ms, "share_of_step": gms / max(tot_ms, 1e-9),
-                         "algorithmic_bytes_per_launch": g_bytes},
-            "clocks": clocks,
-            "wall_s_timed_region": wall,
-            "with_consumer": {
-                "value": c_value, "unit": UNIT, "ms_per_step": float(c_ms.item()) / K,
-                "model": f"GraphSAGE-mean {dims} (random init), forward of every minibatch",
-                "consumer_ms_per_step": fwd_ms, "consumer_launches_per_step": L_,
-                "pipeline": "3 streams: sample(w+2) | gather+score(w+1) | forward(w), timed as one span",
-                "kernel": "k_mean (neighbour means, all SMs) + k_sage_gemm (warp-specialised: TMA ring of self "
-                          "rows / means / weights -> tcgen05.mma kind::tf32 into 2 TMEM accumulators -> "
-                          "bias/ReLU epilogue warps)",
-                "tflops": flops / (fwd_ms / 1e3) / 1e12 if fwd_ms > 0 else None,
-                "agg_gbs": agg_bytes / (fwd_ms / 1e3) / 1e9 if fwd_ms > 0 else None,
-                "dtype": "tf32 x tf32 -> f32"},
-            "with_training": {
-                "value": tr_value, "unit": UNIT, "ms_per_step": float(tr_ms.item()) / KT, "steps": KT,
-                "model": f"GraphSAGE-mean {dims}, softmax cross-entropy, SGD lr {lr}",
-                "ddp": f"{n_trainers} trainers; gradient all-reduce " + ("NCCL (torch.distributed)" if world > 1
-                                                                          else "none (one rank)"),
-                "mean_loss_in_timed_steps": tr_loss,
-                "pipeline": "3 streams: sample(w+2) | gather+score(w+1) | DDP steps of window w",
-                "cuda_graph": bool(use_graph[0]),
-                "dtype": "tf32 x tf32 -> f32"},
-        }
-        if world > 1:
-            nv_bytes = peer_rows * CFG.feat_dim * 4
-            gbs = nv_bytes / (g_avg_ms / 1e3) / 1e9 if g_avg_ms > 0 else None
-            peer = peer_copy_gbs(local, (local + 1) % torch.cuda.device_count())
-            line["nvlink"] = {"peer_rows_per_window": peer_rows, "bytes_per_window": nv_bytes,
-                              "gbs_during_gather": gbs,
-                              "peak_gbs": 900.0, "peak_source": "NVLink 5 nominal per direction per GPU",
-                              "frac": gbs / 900.0 if gbs else None,
-                              "achievable_peer_copy_gbs": peer,
-                              "frac_of_achievable": gbs / peer if (gbs and peer) else None,
-                              "note": "miss + refill rows whose owner is on another GPU, read by peer loads "
-                                      "inside k_gather / k_swap_refill (last timed window); achievable = "
-                                      "256 MB device-to-device copy to the next GPU, best of 5"}
-        if world == 1 and not args.no_cpu_baseline:
-            rate, n_mb, el = oracle_rate(parts, P, f_bp, gamma, delta, args.cpu_budget)
-            rate_p, n_thr = oracle_rate_threads(parts, P, f_bp, gamma, delta, min(args.cpu_budget, 6.0))
-            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
-                                    "sample": f"{n_mb} minibatches (steps 1..{n_mb // P} of all {P} partitions), "
-                                              f"{el:.1f} s, single-threaded C oracle",
-                                    "value_one_thread_per_partition": rate_p, "threads": n_thr,
-                                    "host_cpu": host_cpu(), "host_nproc": os.cpu_count()}
-        print(json.dumps(line), flush=True)
+    t_ddp_overlapped = sum(a.elapsed_time(b) for a, b in tw_ev) / len(tw_ev)
+    # t_DDP alone: the training of one already-prepared window with nothing else running (the slot
+    # consumed last still holds its gathered window; training it again only moves the weights)
+    last = slot ^ 1
+    alone = []
+    for _ in range(3):
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(sC)
+        train_window(last, sC)
+        b.record(sC)
+        barrier()
+        alone.append(a.elapsed_time(b))
+    t_ddp = max_over_ranks(statistics.median(alone))
+    T_win = tr_ms / KT
+    t_prep = prep_ms
     graphs.clear()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()                 # peers read our feature tables until everyone is done
-    ctx.close()
-    if world > 1:
-        dist.destroy_process_group()
+    return {
+        "with_consumer": {
+            "value": c_value, "unit": UNIT, "ms_per_step": c_ms / K,
+            "model": f"GraphSAGE-mean {dims} (random init), forward of every minibatch",
+            "consumer_ms_per_step": fwd_ms, "consumer_launches_per_step": 2 * L_,
+            "pipeline": "3 streams: sample(w+2) | gather+score(w+1) | forward(w), timed as one span",
+            "kernel": "k_mean (neighbour means, all SMs) + k_sage_gemm (warp-specialised: TMA ring of self "
+                      "rows / means / weights -> tcgen05.mma kind::tf32 into 2 TMEM accumulators -> "
+                      "bias/ReLU epilogue warps)",
+            "tflops": flops / (fwd_ms / 1e3) / 1e12 if fwd_ms > 0 else None,
+            "agg_gbs": agg_bytes / (fwd_ms / 1e3) / 1e9 if fwd_ms > 0 else None,
+            "dtype": "tf32 x tf32 -> f32"},
+        "with_training": {
+            "value": tr_value, "unit": UNIT, "ms_per_step": T_win, "steps": KT,
+            "model": f"GraphSAGE-mean {dims}, softmax cross-entropy, SGD lr {lr}",
+            "ddp": f"{n_trainers} trainers; gradient all-reduce " + ("NCCL (torch.distributed)" if world > 1
+                                                                      else "none (one rank)"),
+            "mean_loss_in_timed_steps": tr_loss,
+            "pipeline": "3 streams: sample(w+2) | gather+score(w+1) | DDP steps of window w",
+            "cuda_graph": bool(use_graph[0]),
+            "dtype": "tf32 x tf32 -> f32",
+            # Eq.4-5 per window; overlap efficiency read as the trainer's busy
+            # fraction t_DDP / T (1 = the preparation is fully hidden; DESIGN R#31)
+            "stage_model": {
+                "t_prepare_ms": t_prep, "t_ddp_ms": t_ddp, "t_ddp_under_overlap_ms": t_ddp_overlapped,
+                "T_window_ms": T_win, "eq5_max_ms": max(t_prep, t_ddp),
+                "T_over_eq5": T_win / max(t_prep, t_ddp),
+                "overlap_efficiency": t_ddp / T_win,
+                "stall_ms_per_window": max(0.0, T_win - t_ddp),
+                "hidden_fraction_of_shorter_stage": max(0.0, min(1.0, (t_prep + t_ddp - T_win) /
+                                                                 max(1e-9, min(t_prep, t_ddp)))),
+                "t_prepare_source": "pipeline-only window time of the timed runs (sample || gather + score)",
+                "t_ddp_source": "training of one prepared window with nothing else running (median of 3)"}},
+    }
 
 
 if __name__ == "__main__":

@@ -280,6 +280,25 @@ MGNN_API int64_t mgnn_launch_count(mgnn_ctx ctx);
 MGNN_API mgnn_status mgnn_profile_enable(mgnn_ctx ctx, int32_t enable);
 MGNN_API mgnn_status mgnn_profile_read(mgnn_ctx ctx, double* ms, int64_t* launches, int64_t* bytes);
 
+/* Per-stage CUDA-event timing of the three calls of the path (with mgnn_profile_enable on; each
+ * call brackets its launches with events on the caller's stream, so under a two-stream schedule
+ * the spans are the stages' durations while they overlap).  Fills out[0..MGNN_PROF_N-1] (doubles)
+ * with the indices below, summed since the last read, then resets (synchronises the events):
+ *   sampler kernels of mgnn_sample (k_hop, k_compact x L, k_relabel; not the seeds / epoch orders)
+ *   and the sampled units the sampling roofline counts (8 E + 24 F + 8 U bytes),
+ *   the gather launch and the rows it copied (2 * rows * D * 4 algorithmic bytes), and
+ *   mgnn_score_evict_refill (decay + eviction round).  EINVAL if n_out < MGNN_PROF_N. */
+enum {
+    MGNN_PROF_SAMPLE_MS = 0, MGNN_PROF_SAMPLE_CALLS = 1,
+    MGNN_PROF_EDGES = 2,      /* E: sampled edges, all hops and instances */
+    MGNN_PROF_FRONTIER = 3,   /* F: expanded frontier nodes, sum over hops 0..L-1 of |F_i| */
+    MGNN_PROF_UNIQUE = 4,     /* U: |F_L| summed over instances */
+    MGNN_PROF_GATHER_MS = 5, MGNN_PROF_GATHER_CALLS = 6, MGNN_PROF_GATHER_ROWS = 7,
+    MGNN_PROF_SCORE_MS = 8, MGNN_PROF_SCORE_CALLS = 9,
+    MGNN_PROF_N = 12
+};
+MGNN_API mgnn_status mgnn_profile_stages(mgnn_ctx ctx, double* out, int32_t n_out);
+
 /* Process-wide per-launcher timing (diagnostics): enable = 1 clears and starts recording an
  * event after every kernel launcher (time since the previous event on the same stream is
  * attributed to it); enable = 0 stops, synchronises and writes a text table into report. */

@@ -247,10 +247,16 @@ def describe(g: Graph, parts: List[PartitionInput]) -> dict:
         c = pi.cols
         nl = c[(c < lo) | (c >= hi)]
         halo.append(int(np.unique(nl).shape[0]) / max(1, hi - lo))
+    # degree histogram in power-of-two buckets: bucket b counts nodes with 2^(b-1) <= deg < 2^b (b = 0: deg 0)
+    b = np.zeros(deg.shape, np.int64)
+    nz = deg > 0
+    b[nz] = np.floor(np.log2(deg[nz])).astype(np.int64) + 1
+    hist = np.bincount(b, minlength=1).tolist() if deg.size else []
     return {
         "n_nodes": g.n_nodes, "nnz": g.nnz, "avg_deg": g.nnz / max(1, g.n_nodes),
         "max_deg": int(deg.max()) if deg.size else 0, "median_deg": float(np.median(deg)) if deg.size else 0.0,
-        "n_train": int(g.train_mask.sum()), "halo_over_local": halo,
+        "n_train": int(g.train_mask.sum()), "halo_over_local": [round(h, 4) for h in halo],
+        "deg_hist_log2": hist, "deg_hist_note": "bucket 0: degree 0; bucket b >= 1: 2^(b-1) <= degree < 2^b",
     }
 
 

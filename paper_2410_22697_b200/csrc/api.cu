@@ -223,12 +223,15 @@ WinDev win_dev(mgnn_ctx ctx, Win& w) {
     d.hop_size = w.hop_size;
     d.X = w.X;
     d.counts = w.counts;
+    d.gctr = w.gctr;
     d.pos_of = w.pos_of;
     d.fb = w.fb;
+    d.fbp = w.fbp;
     d.nb = w.nb;
     d.parts = ctx->d_parts;
     d.err = ctx->d_err;
     d.gathered_rows = ctx->d_gathered;
+    d.sampled_units = ctx->prof ? ctx->d_sampled : nullptr;
     d.remote = ctx->remote ? 1 : 0;
     d.n_global = ctx->n_global;
     d.g_indptr = ctx->g_indptr;
@@ -289,6 +292,8 @@ mgnn_status mgnn_ctx_create(int32_t device, int32_t n_parts, int64_t n_global, c
     chk(cudaMemset(ctx->d_err, 0, sizeof(int32_t)));
     chk(dalloc(&ctx->d_gathered, 1));
     chk(cudaMemset(ctx->d_gathered, 0, sizeof(long long)));
+    chk(dalloc(&ctx->d_sampled, 3));
+    chk(cudaMemset(ctx->d_sampled, 0, 3 * sizeof(long long)));
     if (st != MGNN_OK) {
         mgnn_destroy(ctx);
         return st;
@@ -309,10 +314,12 @@ void mgnn_destroy(mgnn_ctx ctx) {
         dfree(p.indptr); dfree(p.cols_rank); dfree(p.halo); dfree(p.deg_in); dfree(p.train); dfree(p.table);
     }
     for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
-    for (auto& e : ctx->prof_ev) {
-        cudaEventDestroy(e.first);
-        cudaEventDestroy(e.second);
-    }
+    for (auto& v : ctx->prof_ev)
+        for (auto& e : v) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+    dfree(ctx->d_sampled);
     dfree(ctx->d_bounds);
     dfree(ctx->d_tables);
     dfree(ctx->d_on_peer);
@@ -731,8 +738,8 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
         CK(dalloc(&w.pos_of, M * ctx->vp_max));
         CK(dalloc(&w.ext_seeds, M * batch));
         CK(dalloc(&w.ext_counts, M));
-        // zero region: [tile counters | status words | counts | fb | per-hop new-node bitmaps]
-        size_t ctr_words = (size_t)(2 * n_layers) * M;                  // int32
+        // zero region: [tile counters | status words | counts | fb | fbp], then the per-hop pairs
+        size_t ctr_words = (size_t)(2 * n_layers + 1) * M;              // int32 (+ gather chunk counters)
         size_t st_words = 0;
         for (int i = 0; i < n_layers; ++i)
             st_words += (size_t)M * (scan_tiles_count(ctx->fcap[i]) + 1) + (size_t)M * (scan_tiles_words(ctx->bm_words) + 1);
@@ -740,15 +747,19 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
         size_t off_st = ((ctr_words * 4 + 255) / 256) * 256;
         size_t off_cnt = off_st + ((st_words * 8 + 255) / 256) * 256;
         size_t off_fb = off_cnt + (((size_t)M * 8 * 8 + 255) / 256) * 256;
-        size_t off_nb = off_fb + (((size_t)M * ctx->bm_words * 4 + 255) / 256) * 256;
-        size_t total = off_nb + (size_t)M * n_layers * ctx->bm_words * 8;   // (bits, position) pairs
+        size_t off_fbp = off_fb + (((size_t)M * ctx->bm_words * 4 + 255) / 256) * 256;
+        size_t off_nb = off_fbp + (((size_t)M * ctx->bm_words * 4 + 255) / 256) * 256;
+        // the (bits, position) pairs follow the zeroed prefix: k_compact writes every word of them
+        size_t total = off_nb + (size_t)M * n_layers * ctx->bm_words * 8;
         CK(dalloc(&w.zero, total));
         CK(cudaMemset(w.zero, 0, total));
-        w.zero_bytes = total;
+        w.zero_bytes = off_nb;
         w.tilectr = (int32_t*)(w.zero + off_ctr);
+        w.gctr = w.tilectr + (size_t)(2 * n_layers) * M;
         w.status = (unsigned long long*)(w.zero + off_st);
         w.counts = (long long*)(w.zero + off_cnt);
         w.fb = (uint32_t*)(w.zero + off_fb);
+        w.fbp = (uint32_t*)(w.zero + off_fbp);
         w.nb = (uint32_t*)(w.zero + off_nb);
         size_t so = 0;
         for (int i = 0; i < n_layers; ++i) {
@@ -859,6 +870,12 @@ mgnn_status mgnn_sample(mgnn_ctx ctx, int32_t slot, uint64_t t0, int32_t n_steps
         wd.ext_counts = w.ext_counts;
     }
     launch_seeds(wd, s);
+    cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+    if (ctx->prof) {
+        CK(cudaEventCreate(&pe0));
+        CK(cudaEventCreate(&pe1));
+        CK(cudaEventRecord(pe0, s));
+    }
     for (int i = 0; i < ctx->L; ++i) {
         // per-hop scratch strides follow the max window; scans index by instance < M
         Scratch scc = w.sc_count[i], scp = w.sc_compact[i];
@@ -867,6 +884,10 @@ mgnn_status mgnn_sample(mgnn_ctx ctx, int32_t slot, uint64_t t0, int32_t n_steps
     }
     launch_relabel(wd, s);
     CKL();
+    if (ctx->prof) {
+        CK(cudaEventRecord(pe1, s));
+        ctx->prof_ev[0].emplace_back(pe0, pe1);
+    }
     w.sampled = true;
     w.gathered = w.scored = false;
     return MGNN_OK;
@@ -899,7 +920,7 @@ mgnn_status mgnn_lookup_gather(mgnn_ctx ctx, int32_t slot, mgnn_stream stream) {
     CKL();
     if (ctx->prof) {
         CK(cudaEventRecord(e1, s));
-        ctx->prof_ev.emplace_back(e0, e1);
+        ctx->prof_ev[1].emplace_back(e0, e1);
     }
     w.gathered = true;
     ctx->seq_started = true;
@@ -919,6 +940,12 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
     for (auto& p : ctx->parts) {
         cap_max = std::max(cap_max, p.cap);
         nmax = std::max(nmax, std::max(p.cap, p.n_h));
+    }
+    cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+    if (ctx->prof) {
+        CK(cudaEventCreate(&pe0));
+        CK(cudaEventCreate(&pe1));
+        CK(cudaEventRecord(pe0, s));
     }
     launch_decay(ctx->d_parts, n_lp, cap_max, w.n_steps, ctx->pol.gamma, s);
     const uint64_t t_last = w.step0 + (uint64_t)w.n_steps - 1;
@@ -941,6 +968,10 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
         launch_swap_refill(ctx->d_parts, n_lp, cap_max, pairs, k_of, world_of(ctx), w.counts, 8, w.n_steps, s);
     }
     CKL();
+    if (ctx->prof) {
+        CK(cudaEventRecord(pe1, s));
+        ctx->prof_ev[2].emplace_back(pe0, pe1);
+    }
     w.scored = true;
     return MGNN_OK;
 }
@@ -1071,10 +1102,9 @@ mgnn_status mgnn_profile_enable(mgnn_ctx ctx, int32_t enable) {
     return MGNN_OK;
 }
 
-mgnn_status mgnn_profile_read(mgnn_ctx ctx, double* ms, int64_t* launches, int64_t* bytes) {
-    GUARD();
+static mgnn_status drain_events(mgnn_ctx ctx, int stage, double* ms, long long* n) {
     double tot = 0.0;
-    for (auto& e : ctx->prof_ev) {
+    for (auto& e : ctx->prof_ev[stage]) {
         CK(cudaEventSynchronize(e.second));
         float x = 0.0f;
         CK(cudaEventElapsedTime(&x, e.first, e.second));
@@ -1082,8 +1112,46 @@ mgnn_status mgnn_profile_read(mgnn_ctx ctx, double* ms, int64_t* launches, int64
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
     }
-    const long long n = (long long)ctx->prof_ev.size();
-    ctx->prof_ev.clear();
+    *n = (long long)ctx->prof_ev[stage].size();
+    ctx->prof_ev[stage].clear();
+    *ms = tot;
+    return MGNN_OK;
+}
+
+mgnn_status mgnn_profile_stages(mgnn_ctx ctx, double* out, int32_t n_out) {
+    GUARD();
+    if (!out || n_out < MGNN_PROF_N) return fail(ctx, MGNN_EINVAL, "profile_stages: need MGNN_PROF_N doubles");
+    double ms[3];
+    long long n[3];
+    for (int st = 0; st < 3; ++st) {
+        mgnn_status r = drain_events(ctx, st, &ms[st], &n[st]);
+        if (r) return r;
+    }
+    long long su[3] = {0, 0, 0}, rows = 0;
+    CK(cudaMemcpy(su, ctx->d_sampled, sizeof(su), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(ctx->d_sampled, 0, sizeof(su)));
+    CK(cudaMemcpy(&rows, ctx->d_gathered, sizeof(long long), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(ctx->d_gathered, 0, sizeof(long long)));
+    for (int i = 0; i < n_out; ++i) out[i] = 0.0;
+    out[MGNN_PROF_SAMPLE_MS] = ms[0];
+    out[MGNN_PROF_SAMPLE_CALLS] = (double)n[0];
+    out[MGNN_PROF_EDGES] = (double)su[0];
+    out[MGNN_PROF_FRONTIER] = (double)su[1];
+    out[MGNN_PROF_UNIQUE] = (double)su[2];
+    out[MGNN_PROF_GATHER_MS] = ms[1];
+    out[MGNN_PROF_GATHER_CALLS] = (double)n[1];
+    out[MGNN_PROF_GATHER_ROWS] = (double)rows;
+    out[MGNN_PROF_SCORE_MS] = ms[2];
+    out[MGNN_PROF_SCORE_CALLS] = (double)n[2];
+    return MGNN_OK;
+}
+
+mgnn_status mgnn_profile_read(mgnn_ctx ctx, double* ms, int64_t* launches, int64_t* bytes) {
+    GUARD();
+    double tot = 0.0;
+    long long n = 0;
+    mgnn_status r = drain_events(ctx, 1, &tot, &n);
+    if (r) return r;
     long long rows = 0;
     CK(cudaMemcpy(&rows, ctx->d_gathered, sizeof(long long), cudaMemcpyDeviceToHost));
     CK(cudaMemset(ctx->d_gathered, 0, sizeof(long long)));

@@ -57,8 +57,10 @@ struct Win {
     size_t zero_bytes = 0;
     unsigned long long* status = nullptr;
     int32_t* tilectr = nullptr;
+    int32_t* gctr = nullptr;        // [M] gather chunk counters (dynamic claiming)
     long long* counts = nullptr;
     uint32_t* fb = nullptr;
+    uint32_t* fbp = nullptr;        // [M][bm_words] frontier membership before the current hop
     int32_t* ext_seeds = nullptr;
     int32_t* ext_counts = nullptr;
     // scratch sub-regions
@@ -164,9 +166,10 @@ struct mgnn_ctx_s {
     std::string err;
     // profiling
     bool prof = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev;
-    double prof_ms = 0.0;
-    long long prof_launches = 0;
+    // event pairs per stage: 0 = sampler kernels (k_hop, k_compact, k_relabel) of mgnn_sample,
+    // 1 = the gather launch of mgnn_lookup_gather, 2 = all of mgnn_score_evict_refill
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[3];
+    long long* d_sampled = nullptr;      // [3] sampled edges E, expanded frontier F, |F_L| U (profiling)
 };
 
 namespace mgnn {

@@ -49,15 +49,19 @@ struct WinDev {
     int32_t* cols[kMaxLayers];
     float* X;                            // [M][ucap][pitch]
     long long* counts;                   // [M][8]
+    int32_t* gctr;                       // [M] gather chunk counters (zeroed per window)
     int32_t* pos_of;                     // [M][vp_stride]
-    uint32_t* fb;                        // [M][bm_words] frontier membership
+    uint32_t* fb;                        // [M][bm_words] frontier membership (cumulative: F_i, then F_{i+1})
+    uint32_t* fbp;                       // [M][bm_words] membership of F_i while hop i runs (new_i = fb & ~fbp)
     uint32_t* nb;                        // [M][L][bm_words][2]: new_i bits of hop i (R#7) and the position
-                                         // in F_{i+1} of the word's first new node (one 8-byte pair)
+                                         // in F_{i+1} of the word's first new node (one 8-byte pair);
+                                         // written in full by k_compact (never zeroed)
     const int32_t* ext_seeds;            // [M][batch] or nullptr
     const int32_t* ext_counts;           // [M]
     const PartDev* parts;                // [n_parts_local]
     int32_t* err;                        // device error word
     long long* gathered_rows;            // profiling counter
+    long long* sampled_units;            // profiling: [3] += E, F, U of every instance (k_relabel)
     // NEXT-1 remote expansion: ranks are global ids; every frontier node is sampled from the
     // global CSR (all partitions hosted by this context)
     int32_t remote;

@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
     int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
     int32_t* pos = W.pos_of + (int64_t)m * W.vp_stride;
     uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
+    uint32_t* fbp = W.fbp + (int64_t)m * W.bm_words;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n0; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t gid = src[j];
         int64_t row = gid - pd.lo;
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
         } else {                                            // epoch order: distinct by construction
             atomicOr(&fb[r >> 5], bit);
         }
+        atomicOr(&fbp[r >> 5], bit);                        // F_0 = the frontier before hop 0
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) W.hop_size[(int64_t)m * (kMaxLayers + 1)] = n0;
 }
@@ -110,7 +112,8 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
 // of k lanes: Philox + Floyd, R#4-R#6); (3) all threads load the sampled
 // neighbours' ranks, write the columns (coalesced) and mark new nodes.
 template <typename IdxT>   // CSR index staged per sample: uint32_t when every index fits (halves the tile)
-__global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max, int T) {
+__global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max, int T,
+                                                                     int mark_filter) {
     pdl_enter();
     __shared__ long long sm[8];
     __shared__ int tslot, n_draw;
@@ -214,11 +217,12 @@ __global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int
         }
         if (tile == 0 && threadIdx.x == 0) off[0] = 0;
         int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop] + o_tile;
-        const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
-        uint32_t* nb = W.nb + ((int64_t)m * W.L + hop) * W.bm_words * 2;   // (bits, first position) pairs
+        uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
         const int32_t* __restrict__ crank = W.remote ? W.g_cols : pd.cols_rank;
-        // batches of kColBatch samples per thread: all neighbour-rank loads in flight, then all
-        // membership loads, then the writes (the loads are independent; only the marks depend on them)
+        // batches of kColBatch samples per thread: all neighbour-rank loads in flight, then the column
+        // writes and the membership marks: every sampled rank is OR-ed into the cumulative frontier
+        // bitmap fb (a fire-and-forget reduction; k_compact finds new_i = fb & ~F_i).  mark_filter = 1
+        // loads the word first and skips ranks already present.
         for (int e0 = threadIdx.x; e0 < (int)agg; e0 += kThreads * kColBatch) {
             int32_t c[kColBatch];
             uint32_t fw[kColBatch];
@@ -227,8 +231,13 @@ __global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int
                 const int e = e0 + j * kThreads;
                 c[j] = e < (int)agg ? __ldg(crank + sidx[e]) : -1;
             }
+            if (mark_filter) {
 #pragma unroll
-            for (int j = 0; j < kColBatch; ++j) fw[j] = c[j] >= 0 ? __ldg(fb + (c[j] >> 5)) : ~0u;
+                for (int j = 0; j < kColBatch; ++j) fw[j] = c[j] >= 0 ? __ldg(fb + (c[j] >> 5)) : ~0u;
+            } else {
+#pragma unroll
+                for (int j = 0; j < kColBatch; ++j) fw[j] = 0u;
+            }
 #pragma unroll
             for (int j = 0; j < kColBatch; ++j) {
                 if (c[j] < 0) continue;
@@ -237,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int
                            "cols o=%lld c=%d", o_tile + e, c[j]);
                 cols[e] = c[j];
                 const uint32_t bit = 1u << (c[j] & 31);
-                if (!(fw[j] & bit)) atomicOr(&nb[2 * (c[j] >> 5)], bit);
+                if (!(fw[j] & bit)) atomicOr(&fb[c[j] >> 5], bit);
             }
         }
         __syncthreads();
@@ -245,6 +254,10 @@ __global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int
 }
 
 // ------------------------------------------------------------------ bitmap -> sorted new frontier nodes
+// new_i = fb & ~fbp word by word (fb: every rank sampled so far, fbp: F_i); the popcount scan over
+// words in rank order (= ascending id) appends new_i to the frontier (R#7) and writes, for EVERY
+// word, the pair (new_i bits, frontier position of the word's first new node) that k_relabel reads;
+// fbp catches up with fb for the next hop.
 __global__ void __launch_bounds__(kThreads, 8) k_compact(WinDev W, int hop, Scratch sc, int64_t tiles_max) {
     pdl_enter();
     __shared__ long long sm[8];
@@ -257,17 +270,18 @@ __global__ void __launch_bounds__(kThreads, 8) k_compact(WinDev W, int hop, Scra
     const int tile = claim_tile(sc.tilectr + m, &tslot);
     if (tile >= ntiles) return;
     uint32_t* nbp = W.nb + ((int64_t)m * W.L + hop) * W.bm_words * 2;   // word w: nbp[2w] bits, nbp[2w+1] position
-    uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
+    const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
+    uint32_t* fbp = W.fbp + (int64_t)m * W.bm_words;
     const int64_t wd0 = (int64_t)tile * kWordTile + (int64_t)threadIdx.x * kCWords;   // 4 consecutive words
     uint32_t b[kCWords];
-    if (wd0 < nwords) {                  // kCWords (bits, position) pairs, 16-byte loads; bm_words % kCWords == 0,
-        const uint4* v = reinterpret_cast<const uint4*>(nbp + 2 * wd0);   // words >= nwords are never set
-#pragma unroll
-        for (int j = 0; j < kCWords / 2; ++j) {
-            const uint4 q = v[j];
-            b[2 * j] = q.x;
-            b[2 * j + 1] = q.z;
-        }
+    uint4 now = make_uint4(0u, 0u, 0u, 0u);
+    if (wd0 < nwords) {                  // bm_words % kCWords == 0: one 16-byte load of each bitmap
+        now = *reinterpret_cast<const uint4*>(fb + wd0);
+        const uint4 was = *reinterpret_cast<const uint4*>(fbp + wd0);
+        b[0] = now.x & ~was.x;
+        b[1] = now.y & ~was.y;
+        b[2] = now.z & ~was.z;
+        b[3] = now.w & ~was.w;
     } else {
 #pragma unroll
         for (int j = 0; j < kCWords; ++j) b[j] = 0u;
@@ -287,16 +301,25 @@ __global__ void __launch_bounds__(kThreads, 8) k_compact(WinDev W, int hop, Scra
     const int64_t nF = hs[hop];
     int64_t pos = nF + prefix_sh + excl;
     int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
+    if (wd0 < nwords) {
+        // new_i keeps its bitmap; with the word's first position it gives every new node's frontier
+        // position as wpre + popc(lower bits) (k_relabel), without a scattered rank -> position table
+        uint32_t p[kCWords];
+        int64_t q = pos;
+#pragma unroll
+        for (int j = 0; j < kCWords; ++j) {
+            p[j] = (uint32_t)q;
+            q += __popc(b[j]);
+        }
+        uint4* v = reinterpret_cast<uint4*>(nbp + 2 * wd0);
+        v[0] = make_uint4(b[0], p[0], b[1], p[1]);
+        v[1] = make_uint4(b[2], p[2], b[3], p[3]);
+        if (cnt) *reinterpret_cast<uint4*>(fbp + wd0) = now;
+    }
 #pragma unroll
     for (int j = 0; j < kCWords; ++j) {
         const int64_t wd = wd0 + j;
         uint32_t bb = b[j];
-        // new_i keeps its bitmap; with the word's first position it gives every new node's frontier
-        // position as wpre + popc(lower bits) (k_relabel), without a scattered rank -> position table
-        if (bb) {                        // positions are only read where a bit is set
-            nbp[2 * wd + 1] = (uint32_t)pos;
-            fb[wd] |= bb;
-        }
         while (bb) {
             const int bi = __ffs(bb) - 1;
             bb &= bb - 1;
@@ -331,6 +354,16 @@ __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
     const int32_t* posof = W.pos_of + (int64_t)m * W.vp_stride;
     const int64_t* hs = W.hop_size + (int64_t)m * (kMaxLayers + 1);
     const int64_t stride = (int64_t)gridDim.x * kThreads;
+    if (W.sampled_units && blockIdx.x == 0 && threadIdx.x == 0) {   // roofline units (bench profiling)
+        long long e = 0, f = 0;
+        for (int hop = 0; hop < W.L; ++hop) {
+            e += W.off[hop][(int64_t)m * W.off_stride[hop] + hs[hop]];
+            f += hs[hop];
+        }
+        atomicAdd((unsigned long long*)&W.sampled_units[0], (unsigned long long)e);
+        atomicAdd((unsigned long long*)&W.sampled_units[1], (unsigned long long)f);
+        atomicAdd((unsigned long long*)&W.sampled_units[2], (unsigned long long)hs[W.L]);
+    }
     for (int hop = 0; hop < W.L; ++hop) {
         const int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
         int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop];
@@ -372,10 +405,14 @@ void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t
     ensure_smem_k(k_hop<uint32_t>, 256 * MGNN_MAX_FANOUT * 4);
     const int64_t tm = tiles_max < 1 ? 1 : tiles_max;
     const char* f64 = getenv("MGNN_SAMPLE_IDX64");   // tests: force the 64-bit staging variant
+    static const int mark_filter = [] {              // 1: load the membership word before marking
+        const char* e = getenv("MGNN_MARK_FILTER");  // (measured: products sampling 0.79 ms with 0,
+        return e ? atoi(e) : 0;                      // 0.82 ms with 1; arxiv equal)
+    }();
     if (w.idx32 && !(f64 && f64[0] == '1'))
-        launch_k(k_hop<uint32_t>, grid, dim3(kThreads), (size_t)T * w.k_hop[hop] * 4, s, w, hop, sc, tm, T);
+        launch_k(k_hop<uint32_t>, grid, dim3(kThreads), (size_t)T * w.k_hop[hop] * 4, s, w, hop, sc, tm, T, mark_filter);
     else
-        launch_k(k_hop<uint64_t>, grid, dim3(kThreads), (size_t)T * w.k_hop[hop] * 8, s, w, hop, sc, tm, T);
+        launch_k(k_hop<uint64_t>, grid, dim3(kThreads), (size_t)T * w.k_hop[hop] * 8, s, w, hop, sc, tm, T, mark_filter);
     count_launches(1, __func__, s);
 }
 

@@ -1,8 +1,12 @@
 // sort.cu -- segmented, stable LSD radix sort of (u64 key, u32 value) pairs
 // ("onesweep" structure: one upfront histogram of every digit, one bin scan,
 // then one scatter launch per 8-bit digit whose tiles find their global digit
-// offsets by a decoupled look-back -- 2 + passes launches per sort instead of
-// 3 per pass).
+// offsets by a decoupled look-back -- 3 + passes launches per sort instead of
+// 3 per pass).  The element count lives on the device; every kernel is
+// persistent and loops over the tiles that count needs, a digit that is the
+// same for every key is skipped (the identity for a stable sort), and a final
+// copy moves the result back to the primary buffers after an odd number of
+// executed passes.
 //
 // Used for every total order the method needs:
 //   * buffer init: halo by (deg_in desc, id asc)            (R#10)
@@ -26,22 +30,30 @@ static inline int64_t sort_tiles(int64_t n_max) {
     return t < 1 ? 1 : t;
 }
 
-// scratch layout (all zeroed by one memset per sort):
-//   bins   u32 [n_seg][passes][256]            digit histograms -> bin offsets
-//   ctr    i32 [n_seg][passes]                 dynamic tile ids
-//   status u32 [n_seg][passes][tiles][256]     look-back words: [31:30] flag, [29:0] count
+// scratch layout:
+//   bins   u32 [n_seg][passes][256]            digit histograms -> bin offsets      } zeroed by one
+//   ctr    i32 [n_seg][passes]                 dynamic tile ids                     } small memset
+//   plan   i32 [n_seg][passes + 1]             per pass: input parity, or -1 = the pass is trivial
+//                                              (one digit value holds every key); [passes] = final parity
+//   status u32 [n_seg][passes][tiles][256]     look-back words: [31:30] flag, [29:0] count -- zeroed by
+//                                              k_sort_hist for the tiles the device-side length uses, so
+//                                              the host never clears the worst-case size
+// Every kernel is persistent (grid <= a few blocks per SM) and loops over the tiles the device-side
+// length needs, so a sort sized for n_max but holding a few thousand keys costs a few microseconds.
+static size_t head_bytes(int n_seg, int passes) {
+    size_t b = (size_t)n_seg * passes * kRadix * 4 + (size_t)n_seg * passes * 4 + (size_t)n_seg * (passes + 1) * 4;
+    return (b + 255) / 256 * 256;
+}
+
 size_t radix_scratch_bytes(int n_seg, int64_t n_max, int max_passes) {
     const int64_t passes = max_passes, tiles = sort_tiles(n_max);
-    size_t b = (size_t)n_seg * passes * kRadix * 4;
-    b += (size_t)n_seg * passes * 4;
-    b = (b + 255) / 256 * 256;
-    b += (size_t)n_seg * passes * tiles * kRadix * 4;
-    return b;
+    return head_bytes(n_seg, (int)passes) + (size_t)n_seg * passes * tiles * kRadix * 4;
 }
 
 struct SortScr {
     uint32_t* bins;
     int32_t* ctr;
+    int32_t* plan;
     uint32_t* status;
 };
 
@@ -49,22 +61,24 @@ static SortScr carve(void* base, int n_seg, int passes) {
     SortScr s;
     s.bins = (uint32_t*)base;
     s.ctr = (int32_t*)(s.bins + (size_t)n_seg * passes * kRadix);
-    size_t off = (size_t)n_seg * passes * kRadix * 4 + (size_t)n_seg * passes * 4;
-    off = (off + 255) / 256 * 256;
-    s.status = (uint32_t*)((char*)base + off);
+    s.plan = s.ctr + (size_t)n_seg * passes;
+    s.status = (uint32_t*)((char*)base + head_bytes(n_seg, passes));
     return s;
 }
 
-// ---- 1. histogram of every digit position in one read of the keys
+// ---- 1. histogram of every digit position in one read of the keys; clears the look-back words
 __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const SortSeg* __restrict__ segs, int passes,
-                                                            SortScr scr) {
+                                                            int64_t tiles_max, SortScr scr) {
     __shared__ uint32_t h[8][kRadix];
     const SortSeg sg = segs[blockIdx.y];
     const int64_t n = *sg.n;
+    const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
     for (int p = 0; p < passes; ++p) h[p][threadIdx.x] = 0;
     __syncthreads();
-    const int64_t base = (int64_t)blockIdx.x * kSortTile;
-    if (base < n) {
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int p = 0; p < passes; ++p)
+            scr.status[((size_t)(blockIdx.y * passes + p) * tiles_max + t) * kRadix + threadIdx.x] = 0u;
+        const int64_t base = t * kSortTile;
 #pragma unroll
         for (int i = 0; i < kSortItems; ++i) {
             const int64_t idx = base + (int64_t)i * kSortThreads + threadIdx.x;
@@ -80,15 +94,30 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const SortSeg* __res
         if (h[p][threadIdx.x]) atomicAdd(&bins[p * kRadix + threadIdx.x], h[p][threadIdx.x]);
 }
 
-// ---- 2. exclusive scan of each digit histogram -> bin offsets
-__global__ void __launch_bounds__(kSortThreads) k_sort_binscan(int passes, SortScr scr) {
+// ---- 2. exclusive scan of each digit histogram -> bin offsets; the pass plan (trivial passes skipped)
+__global__ void __launch_bounds__(kSortThreads) k_sort_binscan(const SortSeg* __restrict__ segs, int passes,
+                                                               SortScr scr) {
     __shared__ long long sm[8];
+    __shared__ int trivial_sh;
+    const SortSeg sg = segs[blockIdx.y];
+    const long long n = *sg.n;
     uint32_t* bins = scr.bins + (size_t)blockIdx.y * passes * kRadix;
+    int32_t* plan = scr.plan + (size_t)blockIdx.y * (passes + 1);
+    int parity = 0;
     for (int p = 0; p < passes; ++p) {
+        if (threadIdx.x == 0) trivial_sh = 0;
+        __syncthreads();
+        const uint32_t c = bins[p * kRadix + threadIdx.x];
+        if ((long long)c == n) trivial_sh = 1;    // every key has this digit: the pass is the identity
         long long tot;
-        const long long ex = block_excl_scan256(bins[p * kRadix + threadIdx.x], sm, &tot);
+        const long long ex = block_excl_scan256(c, sm, &tot);
         bins[p * kRadix + threadIdx.x] = (uint32_t)ex;
+        const bool skip = p >= sg.npass || n == 0 || trivial_sh;
+        if (threadIdx.x == 0) plan[p] = skip ? -1 : parity;
+        if (!skip) parity ^= 1;
+        __syncthreads();
     }
+    if (threadIdx.x == 0) plan[passes] = parity;
 }
 
 __device__ __forceinline__ void st_rel32(uint32_t* p, uint32_t v) {
@@ -101,7 +130,7 @@ __device__ __forceinline__ uint32_t ld_acq32(const uint32_t* p) {
 }
 constexpr uint32_t kSAgg = 1u << 30, kSInc = 2u << 30, kSMask = (1u << 30) - 1;
 
-// ---- 3. one digit pass: local stable ranks, per-digit look-back, scatter
+// ---- 3. one digit pass: local stable ranks, per-digit look-back, scatter (persistent over tiles)
 __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortSeg* __restrict__ segs, int passes, int p,
                                                             int64_t tiles_max, SortScr scr) {
     __shared__ uint32_t run[kRadix];       // per-digit running count inside the tile
@@ -110,12 +139,10 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortSeg* __res
     __shared__ int tslot;
     const int s = blockIdx.y;
     const SortSeg sg = segs[s];
-    if (p >= sg.npass) return;                 // this segment's schedule has fewer digits
+    const int parity = scr.plan[(size_t)s * (passes + 1) + p];
+    if (parity < 0) return;                    // beyond this segment's schedule, or a trivial digit
     const int64_t n = *sg.n;
     const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
-    const int tile = claim_tile(scr.ctr + s * passes + p, &tslot);
-    if (tile >= ntiles) return;
-    const int parity = p & 1;
     const unsigned long long* kin = parity ? sg.keys_tmp : sg.keys;
     const uint32_t* vin = parity ? sg.vals_tmp : sg.vals;
     unsigned long long* kout = parity ? sg.keys : sg.keys_tmp;
@@ -123,69 +150,86 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortSeg* __res
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const int shift = sg.shift[p];
-    const int64_t base = (int64_t)tile * kSortTile;
-    run[threadIdx.x] = 0;
-    for (int w = 0; w < 8; ++w) wc[w][threadIdx.x] = 0;
-    __syncthreads();
-    unsigned long long key[kSortItems];
-    uint32_t val[kSortItems], rank[kSortItems];
-#pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
-        const int64_t idx = base + (int64_t)i * kSortThreads + threadIdx.x;
-        const bool valid = idx < n;
-        key[i] = valid ? kin[idx] : 0ull;
-        val[i] = valid ? vin[idx] : 0u;
-        const unsigned digit = valid ? ((unsigned)(key[i] >> shift) & 0xFF) : (0x100u | lane);
-        const unsigned peers = __match_any_sync(kFull, digit);
-        const unsigned r = __popc(peers & lt);
-        if (valid && r == 0) wc[warp][digit] = __popc(peers);
-        __syncthreads();
-        {   // per digit: exclusive prefix over warps of this round, advance the tile-local count
-            uint32_t acc = run[threadIdx.x];
-#pragma unroll
-            for (int w = 0; w < 8; ++w) {
-                const uint32_t c = wc[w][threadIdx.x];
-                wc[w][threadIdx.x] = acc;
-                acc += c;
-            }
-            run[threadIdx.x] = acc;
-        }
-        __syncthreads();
-        rank[i] = valid ? wc[warp][digit] + r : 0xFFFFFFFFu;
-        __syncthreads();
+    for (;;) {
+        const int tile = claim_tile(scr.ctr + s * passes + p, &tslot);
+        __syncthreads();                       // tslot is rewritten by the next claim
+        if (tile >= ntiles) return;
+        const int64_t base = (int64_t)tile * kSortTile;
+        run[threadIdx.x] = 0;
         for (int w = 0; w < 8; ++w) wc[w][threadIdx.x] = 0;
         __syncthreads();
-    }
-    {   // thread d: publish the tile's count of digit d, look back for its exclusive prefix
-        const int d = threadIdx.x;
-        const uint32_t cnt = run[d];
-        uint32_t* st = scr.status + ((size_t)(s * passes + p) * tiles_max) * kRadix;
-        uint32_t excl = 0;
-        if (tile == 0) {
-            st_rel32(&st[d], kSInc | cnt);
-        } else {
-            st_rel32(&st[(size_t)tile * kRadix + d], kSAgg | cnt);
-            for (int j = tile - 1; j >= 0; --j) {
-                uint32_t v;
-                do {
-                    v = ld_acq32(&st[(size_t)j * kRadix + d]);
-                } while ((v & ~kSMask) == 0);
-                excl += v & kSMask;
-                if ((v & ~kSMask) == kSInc) break;
-            }
-            st_rel32(&st[(size_t)tile * kRadix + d], kSInc | (excl + cnt));
-        }
-        gofs[d] = scr.bins[(size_t)(s * passes + p) * kRadix + d] + excl;
-    }
-    __syncthreads();
+        unsigned long long key[kSortItems];
+        uint32_t val[kSortItems], rank[kSortItems];
 #pragma unroll
-    for (int i = 0; i < kSortItems; ++i) {
-        if (rank[i] == 0xFFFFFFFFu) continue;
-        const unsigned digit = (unsigned)(key[i] >> shift) & 0xFF;
-        const uint32_t pos = gofs[digit] + rank[i];
-        MGNN_CHECK(pos < n, "scatter pos=%u n=%lld seg=%d", pos, (long long)n, s);
-        kout[pos] = key[i];
-        vout[pos] = val[i];
+        for (int i = 0; i < kSortItems; ++i) {
+            const int64_t idx = base + (int64_t)i * kSortThreads + threadIdx.x;
+            const bool valid = idx < n;
+            key[i] = valid ? kin[idx] : 0ull;
+            val[i] = valid ? vin[idx] : 0u;
+            const unsigned digit = valid ? ((unsigned)(key[i] >> shift) & 0xFF) : (0x100u | lane);
+            const unsigned peers = __match_any_sync(kFull, digit);
+            const unsigned r = __popc(peers & lt);
+            if (valid && r == 0) wc[warp][digit] = __popc(peers);
+            __syncthreads();
+            {   // per digit: exclusive prefix over warps of this round, advance the tile-local count
+                uint32_t acc = run[threadIdx.x];
+#pragma unroll
+                for (int w = 0; w < 8; ++w) {
+                    const uint32_t c = wc[w][threadIdx.x];
+                    wc[w][threadIdx.x] = acc;
+                    acc += c;
+                }
+                run[threadIdx.x] = acc;
+            }
+            __syncthreads();
+            rank[i] = valid ? wc[warp][digit] + r : 0xFFFFFFFFu;
+            __syncthreads();
+            for (int w = 0; w < 8; ++w) wc[w][threadIdx.x] = 0;
+            __syncthreads();
+        }
+        {   // thread d: publish the tile's count of digit d, look back for its exclusive prefix
+            const int d = threadIdx.x;
+            const uint32_t cnt = run[d];
+            uint32_t* st = scr.status + ((size_t)(s * passes + p) * tiles_max) * kRadix;
+            uint32_t excl = 0;
+            if (tile == 0) {
+                st_rel32(&st[d], kSInc | cnt);
+            } else {
+                st_rel32(&st[(size_t)tile * kRadix + d], kSAgg | cnt);
+                for (int j = tile - 1; j >= 0; --j) {
+                    uint32_t v;
+                    do {
+                        v = ld_acq32(&st[(size_t)j * kRadix + d]);
+                    } while ((v & ~kSMask) == 0);
+                    excl += v & kSMask;
+                    if ((v & ~kSMask) == kSInc) break;
+                }
+                st_rel32(&st[(size_t)tile * kRadix + d], kSInc | (excl + cnt));
+            }
+            gofs[d] = scr.bins[(size_t)(s * passes + p) * kRadix + d] + excl;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kSortItems; ++i) {
+            if (rank[i] == 0xFFFFFFFFu) continue;
+            const unsigned digit = (unsigned)(key[i] >> shift) & 0xFF;
+            const uint32_t pos = gofs[digit] + rank[i];
+            MGNN_CHECK(pos < n, "scatter pos=%u n=%lld seg=%d", pos, (long long)n, s);
+            kout[pos] = key[i];
+            vout[pos] = val[i];
+        }
+        __syncthreads();
+    }
+}
+
+// ---- 4. an odd number of executed passes left the result in the tmp buffers: copy it back
+__global__ void __launch_bounds__(kSortThreads) k_sort_fix(const SortSeg* __restrict__ segs, int passes, SortScr scr) {
+    const SortSeg sg = segs[blockIdx.y];
+    if (scr.plan[(size_t)blockIdx.y * (passes + 1) + passes] == 0) return;
+    const int64_t n = *sg.n;
+    for (int64_t i = (int64_t)blockIdx.x * kSortThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kSortThreads) {
+        sg.keys[i] = sg.keys_tmp[i];
+        sg.vals[i] = sg.vals_tmp[i];
     }
 }
 
@@ -194,13 +238,17 @@ void radix_sort_pairs(const SortSeg* segs_dev, int n_seg, int64_t n_max, int max
     if (n_seg < 1) return;
     const int passes = max_passes;
     const int64_t tiles = sort_tiles(n_max);
-    cudaMemsetAsync(scratch, 0, radix_scratch_bytes(n_seg, n_max, max_passes), s);
+    cudaMemsetAsync(scratch, 0, head_bytes(n_seg, passes), s);
     const SortScr scr = carve(scratch, n_seg, passes);
-    dim3 grid((unsigned)tiles, (unsigned)n_seg);
-    k_sort_hist<<<grid, kSortThreads, 0, s>>>(segs_dev, passes, scr);
-    k_sort_binscan<<<dim3(1, n_seg), kSortThreads, 0, s>>>(passes, scr);
+    // persistent grids: at most ~4 blocks per SM over all segments; tiles are looped / claimed
+    int64_t gx = ((int64_t)num_sms() * 4 + n_seg - 1) / n_seg;
+    if (gx > tiles) gx = tiles;
+    dim3 grid((unsigned)(gx < 1 ? 1 : gx), (unsigned)n_seg);
+    k_sort_hist<<<grid, kSortThreads, 0, s>>>(segs_dev, passes, tiles, scr);
+    k_sort_binscan<<<dim3(1, n_seg), kSortThreads, 0, s>>>(segs_dev, passes, scr);
     for (int p = 0; p < passes; ++p) k_sort_pass<<<grid, kSortThreads, 0, s>>>(segs_dev, passes, p, tiles, scr);
-    count_launches(2 + passes, __func__, s);
+    k_sort_fix<<<grid, kSortThreads, 0, s>>>(segs_dev, passes, scr);
+    count_launches(3 + passes, __func__, s);
 }
 
 }  // namespace mgnn

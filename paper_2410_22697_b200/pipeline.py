@@ -288,6 +288,14 @@ class Context:
     def profile(self, enable: bool):
         self._chk("mgnn_profile_enable", self.L.mgnn_profile_enable(self._h, 1 if enable else 0))
 
+    def profile_stages(self) -> Dict[str, float]:
+        """mgnn_profile_stages: per-stage event times and sampled units since the last read."""
+        out = np.zeros(_lib.PROF_N, np.float64)
+        self._chk("mgnn_profile_stages", self.L.mgnn_profile_stages(self._h, _ptr(out), _lib.PROF_N))
+        keys = ["sample_ms", "sample_calls", "edges", "frontier", "unique", "gather_ms", "gather_calls",
+                "gather_rows", "score_ms", "score_calls"]
+        return {k: float(out[i]) for i, k in enumerate(keys)}
+
     def profile_read(self):
         ms = C.c_double()
         n = C.c_int64()
@@ -340,7 +348,10 @@ def ddp_step(ctx: Context, slot: int, step_in_window: int, n_trainers: int, lr: 
     ctx.train_step(slot, step_in_window, n_trainers, stream)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         g = ctx.grads()
-        with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream()):
+        if stream is not None:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(g, group=group)
+        else:                          # the current stream, which train_step / sgd also use
             dist.all_reduce(g, group=group)
     ctx.sgd(lr, stream)
 

@@ -1,0 +1,46 @@
+"""The timed two-stream schedule (bench.py's loop) against the oracle -- bit-exact (-m gpu).
+
+Closes SURVEY §8(a) A13 (Alg.1 l.5-9; queue depth P:403) for the schedule the bench
+actually times: paper_2410_22697_b200.schedule.PrepareAhead with two streams, PDL (library
+default), the per-iteration L2 flush and events, at the bench's window length and partition
+layout (tests/schedule_util.py says what is compared).
+"""
+import pytest
+
+from inputs import synth
+from tests.schedule_util import run_schedule_parity
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def test_schedule_cfg1_windows_with_eviction_rounds():
+    """configs[0], 4-step windows ending in eviction rounds (Delta = 4), 8 windows back to back."""
+    g = synth.generate(synth.CONFIGS["cfg1"])
+    st = run_schedule_parity(g, 2, 64, [10, 25], 256, 2500, 0.9, 4, 4, 8, x_rows=4096)
+    assert st["evicted"] > 0 and st["hits"] > 0 and st["misses"] > 0
+
+
+def test_schedule_cfg1_bench_window():
+    """configs[0] at the bench's 32-step window and the paper's Delta = 64 for it."""
+    g = synth.generate(synth.CONFIGS["cfg1"])
+    st = run_schedule_parity(g, 2, 64, [10, 25], 256, 2500, 0.995, 64, 32, 6, x_rows=4096)
+    assert st["evicted"] > 0
+
+
+@pytest.mark.slow
+def test_schedule_arxiv_full_size_bench_config():
+    """configs[1] at full size in the bench's configuration: P = 2 on one GPU, 32-step windows,
+    f = 0.25, gamma = 0.995, Delta = 32 (every window ends in an eviction round)."""
+    g = synth.generate(synth.CONFIGS["arxiv"])
+    st = run_schedule_parity(g, 2, 128, [10, 25], 1000, 2500, 0.995, 32, 32, 6, x_rows=4096)
+    assert st["evicted"] > 0
+
+
+@pytest.mark.slow
+def test_schedule_products_full_size_bench_config():
+    """configs[3] (the bench default) at full size in the bench's configuration: P = 2 on one GPU,
+    32-step windows, f = 0.5, gamma = 0.995, Delta = 32, 3 hops [5, 10, 15], batch 2000."""
+    g = synth.generate(synth.CONFIGS["products"])
+    st = run_schedule_parity(g, 2, 100, [5, 10, 15], 2000, 5000, 0.995, 32, 32, 4, x_rows=2048)
+    assert st["evicted"] > 0 and st["misses"] > 0

@@ -24,15 +24,15 @@ def main():
     ap.add_argument("--config", default="arxiv")
     ap.add_argument("--parts", type=int, default=2)
     a = ap.parse_args()
-    bench.select_config(a.config)
-    cfg = synth.CONFIGS[a.config]
-    P = a.parts
-    f_bp, gamma, delta = bench.policy_for(P)
+    S = bench.Setup(a.config, 1, parts=a.parts)
+    cfg = S.cfg
+    P = S.P
+    f_bp, gamma, delta = S.f_bp, S.gamma, S.delta
     g = synth.generate(cfg)
     parts = synth.partition(g, P)
     ctx = PL.build_context(0, parts, cfg.feat_dim, synth.FEAT_SEED)
     ctx.buffer_init(gamma, PL.alpha_default(gamma, delta), 1.0, delta, f_bp)
-    W = min(bench.WINDOW, delta)
+    W = S.window
     ctx.sampler_config(cfg.fanouts, cfg.batch, synth.RUN_SEED, W)
     s = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -75,9 +75,9 @@ if __name__ == "__main__" and "--timeline" not in sys.argv:
 
 def timeline(windows=6):
     """Pipelined (two-stream) iterations: event timestamps after each call, relative to iteration start."""
-    cfg = synth.CONFIGS["arxiv"]
-    P = 2
-    f_bp, gamma, delta = bench.policy_for(P)
+    S = bench.Setup("arxiv", 1)
+    cfg, P = S.cfg, S.P
+    f_bp, gamma, delta = S.f_bp, S.gamma, S.delta
     g = synth.generate(cfg)
     parts = synth.partition(g, P)
     ctx = PL.build_context(0, parts, cfg.feat_dim, synth.FEAT_SEED)

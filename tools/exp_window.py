@@ -1,0 +1,58 @@
+"""Window time of one config under the bench schedule, pipelined (two streams) or serial, with the
+per-stage CUDA-event times (mgnn_profile_stages).  Experiments only (env knobs of the library).
+
+    python tools/exp_window.py --config products [--serial] [--windows 12]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from inputs import synth  # noqa: E402
+from paper_2410_22697_b200 import pipeline as PL  # noqa: E402
+from paper_2410_22697_b200.schedule import PrepareAhead  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="products")
+    ap.add_argument("--windows", type=int, default=12)
+    ap.add_argument("--serial", action="store_true")
+    ap.add_argument("--parts", type=int, default=None)
+    ap.add_argument("--tag", default="")
+    a = ap.parse_args()
+    S = bench.Setup(a.config, 1, parts=a.parts)
+    g = synth.generate(S.cfg)
+    parts = synth.partition(g, S.P)
+    ctx = PL.build_context(0, parts, S.cfg.feat_dim, synth.FEAT_SEED)
+    ctx.buffer_init(S.gamma, PL.alpha_default(S.gamma, S.delta), 1.0, S.delta, S.f_bp)
+    ctx.sampler_config(S.cfg.fanouts, S.cfg.batch, synth.RUN_SEED, S.window)
+    pipe = PrepareAhead(ctx, S.window, serial=a.serial)
+    for _ in range(4):
+        pipe.iteration()
+    torch.cuda.synchronize()
+    ctx.profile(True)
+    ctx.profile_stages()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.windows)]
+    for i in range(a.windows):
+        pipe.iteration(events=ev[i])
+    torch.cuda.synchronize()
+    ms = sorted(x.elapsed_time(y) for x, y in ev)
+    pr = ctx.profile_stages()
+    n = max(pr["sample_calls"], 1)
+    out = {"tag": a.tag, "config": a.config, "serial": a.serial, "env": {k: v for k, v in os.environ.items() if k.startswith("MGNN_")},
+           "ms_median": ms[len(ms) // 2], "ms_min": ms[0], "mb_per_s": S.window * S.ppg / (ms[len(ms) // 2] / 1e3),
+           "sample_ms": pr["sample_ms"] / n, "gather_ms": pr["gather_ms"] / max(pr["gather_calls"], 1),
+           "score_ms": pr["score_ms"] / max(pr["score_calls"], 1)}
+    print(json.dumps(out), flush=True)
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()

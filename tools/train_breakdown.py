@@ -21,15 +21,14 @@ def main():
     ap.add_argument("--config", default="arxiv")
     ap.add_argument("--steps", type=int, default=32)
     a = ap.parse_args()
-    bench.select_config(a.config)
-    cfg = synth.CONFIGS[a.config]
-    P = bench.PARTS_PER_GPU
-    f_bp, gamma, delta = bench.policy_for(P)
+    S = bench.Setup(a.config, 1)
+    cfg, P = S.cfg, S.P
+    f_bp, gamma, delta = S.f_bp, S.gamma, S.delta
     g = synth.generate(cfg)
     parts = synth.partition(g, P)
     ctx = PL.build_context(0, parts, cfg.feat_dim, synth.FEAT_SEED)
     ctx.buffer_init(gamma, PL.alpha_default(gamma, delta), 1.0, delta, f_bp)
-    W = min(bench.WINDOW, delta)
+    W = S.window
     ctx.sampler_config(cfg.fanouts, cfg.batch, synth.RUN_SEED, W)
     dims = synth.sage_dims(cfg.feat_dim, len(cfg.fanouts), synth.N_CLASSES[cfg.name])
     wts = synth.sage_weights(dims)
