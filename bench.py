@@ -362,6 +362,8 @@ def main():
     ap.add_argument("--parts-per-gpu", type=int, default=None, help="partitions (trainers) per GPU")
     ap.add_argument("--parts", type=int, default=None, help="total partitions P (a multiple of the GPU count)")
     ap.add_argument("--window", type=int, default=None, help="steps per window (default per config)")
+    ap.add_argument("--static-arenas", action="store_true",
+                    help="size window arenas for the static worst case instead of a pilot-measured bound")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-extras", action="store_true", help="skip the with_consumer / with_training lines")
@@ -424,7 +426,15 @@ def main():
         if world > 1:
             ctx.load_global_csr(g.indptr, g.cols)       # replicated global CSR on every GPU
         ctx.expand_remote(True)
-    ctx.sampler_config(cfg.fanouts, cfg.batch, synth.RUN_SEED, WINDOW)
+    # realistic window arenas (mgnn_sampler_config_bounded): the largest |F_L| of a one-step pilot x 1.25;
+    # a window that still overflows is skipped on the device and reported, and the run is redone with a
+    # doubled bound (resuming at the overflowed step)
+    rows_bound = 0 if args.static_arenas else PL.estimate_rows_bound(ctx, cfg.fanouts, cfg.batch, synth.RUN_SEED)
+    if world > 1:                                # one bound for every rank (the largest)
+        rb = torch.tensor([rows_bound], dtype=torch.int64, device="cuda")
+        dist.all_reduce(rb, op=dist.ReduceOp.MAX)
+        rows_bound = int(rb.item())
+    ctx.sampler_config(cfg.fanouts, cfg.batch, synth.RUN_SEED, WINDOW, rows_bound=rows_bound)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -440,36 +450,57 @@ def main():
 
     # Two streams = the paper's prepare-ahead overlap (Alg.1 l.9): NeighborSampler of window w+1
     # (needs no buffer state) runs on stream A while window w is classified/gathered/scored on B.
-    pipe = PrepareAhead(ctx, WINDOW, t0=1, stream_b=stream)
-    for _ in range(args.warmup):
-        pipe.iteration()
-    # ---------------- timed region (device path: inputs resident in HBM); R runs, median reported
+    from paper_2410_22697_b200._lib import MgnnError
     K = args.steps
     R = max(1, args.runs)
     mb_total = WINDOW * S.ppg * world * K
-    nv0 = nvlink_counters(local) if world > 1 else None
-    launches0 = ctx.launch_count()
-    ctx.profile(True)
-    ctx.profile_stages()                         # reset
-    runs = []
-    prof = {}
-    wall = 0.0
-    with ClockSampler(local) as clk:
-        for r in range(R):
-            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-            barrier()
-            wall0 = time.perf_counter()
-            for i in range(K):
-                pipe.iteration(events=ev[i])
-            barrier()
-            wall += time.perf_counter() - wall0
-            tot_ms = sum(a.elapsed_time(b) for a, b in ev)
-            max_ms = max_over_ranks(tot_ms)
-            runs.append({"value": mb_total / (max_ms / 1e3), "ms_per_step": max_ms / K, "my_ms": tot_ms})
-            ps = ctx.profile_stages()
-            for k_, v_ in ps.items():
-                prof[k_] = prof.get(k_, 0.0) + v_
-    ctx.profile(False)
+    t_first = 1
+    for attempt in range(4):
+        pipe = PrepareAhead(ctx, WINDOW, t0=t_first, stream_b=stream)
+        for _ in range(args.warmup):
+            pipe.iteration()
+        # ---------------- timed region (device path: inputs resident in HBM); R runs, median reported
+        nv0 = nvlink_counters(local) if world > 1 else None
+        launches0 = ctx.launch_count()
+        ctx.profile(True)
+        ctx.profile_stages()                     # reset
+        runs = []
+        prof = {}
+        wall = 0.0
+        with ClockSampler(local) as clk:
+            for r in range(R):
+                ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+                barrier()
+                wall0 = time.perf_counter()
+                for i in range(K):
+                    pipe.iteration(events=ev[i])
+                barrier()
+                wall += time.perf_counter() - wall0
+                tot_ms = sum(a.elapsed_time(b) for a, b in ev)
+                max_ms = max_over_ranks(tot_ms)
+                runs.append({"value": mb_total / (max_ms / 1e3), "ms_per_step": max_ms / K, "my_ms": tot_ms})
+                ps = ctx.profile_stages()
+                for k_, v_ in ps.items():
+                    prof[k_] = prof.get(k_, 0.0) + v_
+        ctx.profile(False)
+        ovf = 0
+        try:
+            ctx.counts(pipe.slot ^ 1, stream)    # EOVERFLOW if any window of the run overflowed its arena
+        except MgnnError as e:
+            if e.status != 6:
+                raise
+            ovf = 1
+        if world > 1:
+            ot = torch.tensor([ovf], dtype=torch.int64, device="cuda")
+            dist.all_reduce(ot, op=dist.ReduceOp.MAX)
+            ovf = int(ot.item())
+        if not ovf:
+            break
+        print(f"[bench] arena bound {rows_bound} rows overflowed; retrying with {2 * rows_bound}", file=sys.stderr)
+        barrier()
+        rows_bound *= 2
+        ctx.sampler_config(cfg.fanouts, cfg.batch, synth.RUN_SEED, WINDOW, rows_bound=rows_bound)
+        t_first = ctx.next_step()                # resume at the overflowed window
     launches = ctx.launch_count() - launches0
     nv1 = nvlink_counters(local) if world > 1 else None
     clocks = clk.summary()
@@ -564,6 +595,11 @@ def main():
                            graph_stats=synth.describe(g, parts)),
             "runs": [r_["value"] for r_ in runs], "median_of": R,
             "buffer_init_ms": init_ms,
+            "arenas": {"rows_bound_per_instance": rows_bound or "static worst case",
+                       "static_bound": static_ucap(S),
+                       "x_bytes_per_slot": (rows_bound or static_ucap(S)) * (((cfg.feat_dim + 3) // 4) * 4) * 4
+                       * S.ppg * WINDOW,
+                       "note": "mgnn_sampler_config_bounded: pilot max |F_L| x 1.25; overflow -> skipped + retried"},
             "hit_rate": hits / max(1, hits + misses),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": E2E, "path": "schedule.PrepareAhead with host seeds: mgnn_sample(pinned host seeds, "
@@ -632,6 +668,14 @@ def main():
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def static_ucap(S) -> int:
+    """min(B * prod(1 + k_i), |V|): the worst-case |F_L| the static arenas are sized for."""
+    u = S.cfg.batch
+    for k in S.cfg.fanouts:
+        u *= 1 + k
+    return int(min(u, S.cfg.n_nodes))
 
 
 def extras(args, S, ctx, pipe, t_start, slot, world, barrier, max_over_ranks, mb_total, K, prep_ms, prof, R):

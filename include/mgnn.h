@@ -54,7 +54,8 @@ typedef enum {
     MGNN_ENOMEM = 2,    /* device allocation failed */
     MGNN_ECUDA = 3,     /* CUDA error (sticky) */
     MGNN_ESTATE = 5,    /* call-order violation (e.g. gather before sample) */
-    MGNN_EOVERFLOW = 6  /* a device-side size exceeded its arena bound (sticky) */
+    MGNN_EOVERFLOW = 6  /* a frontier exceeded the arena bound of mgnn_sampler_config_bounded (not sticky:
+                           the window and later ones were skipped; reconfigure and resume) */
 } mgnn_status;
 
 #define MGNN_MAX_LAYERS 8
@@ -151,6 +152,20 @@ MGNN_API mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* policy, m
  * of the counter-based Philox streams (R#4), and the largest window. */
 MGNN_API mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_layers, int32_t batch,
                                 uint64_t run_seed, int32_t max_window);
+
+/* The same with REALISTIC window arenas: every frontier F_i (i >= 1) of an instance is given room
+ * for at most rows_bound nodes (0 = the static worst case min(B * prod(1 + k_i), |V_p|), which
+ * for ogbn-products-shaped graphs is ~12x the frontiers that occur and for papers100M does not fit
+ * a window of 16 steps x 8 trainers).  X, the frontier and the per-hop blocks are sized from it.
+ * A window whose frontier does not fit is detected on the device: its frontiers are truncated,
+ * and it and every later window are SKIPPED by every kernel that changes buffer state (gather /
+ * tally, decay, eviction swap), so the prefetcher state stays that of the last good window.  The
+ * next mgnn_counts_read of such a window returns MGNN_EOVERFLOW (not sticky; mgnn_last_error
+ * names the step).  Recovery: call this again with a larger bound -- it resumes the step order at
+ * the overflowed window -- and sample from that step on.  rows_bound must be 0 or >= batch. */
+MGNN_API mgnn_status mgnn_sampler_config_bounded(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_layers,
+                                                 int32_t batch, uint64_t run_seed, int32_t max_window,
+                                                 int64_t rows_bound);
 
 /* SURVEY §8(f) NEXT-1, the alternative to reading R#1 (call before mgnn_sampler_config): with
  * enable != 0 every non-local frontier node is sampled too, from its owner's CSR row, with the
@@ -268,6 +283,10 @@ MGNN_API mgnn_status mgnn_part_info(mgnn_ctx ctx, int32_t lp, int64_t* info5);
 MGNN_API mgnn_status mgnn_halo_get(mgnn_ctx ctx, int32_t lp, int32_t* halo_ids, int32_t* deg_in);
 /* Feature table row of a node hosted here (synchronous; tests). */
 MGNN_API mgnn_status mgnn_table_row(mgnn_ctx ctx, int64_t node, float* out);
+
+/* The first step of the next window mgnn_lookup_gather accepts (windows are gathered in step
+ * order); after mgnn_sampler_config_bounded resumed from an arena overflow, the overflowed step. */
+MGNN_API mgnn_status mgnn_next_step(mgnn_ctx ctx, uint64_t* next_step);
 
 /* Kernel launches issued by this ctx since creation (bench evidence). */
 MGNN_API int64_t mgnn_launch_count(mgnn_ctx ctx);

@@ -97,7 +97,7 @@ namespace host {
 mgnn_status fail(mgnn_ctx c, mgnn_status st, const std::string& msg) {
     if (c) {
         c->err = msg;
-        if (st == MGNN_ECUDA || st == MGNN_EOVERFLOW) c->sticky = st;
+        if (st == MGNN_ECUDA) c->sticky = st;
     }
     return st;
 }
@@ -168,7 +168,6 @@ void free_win(Win& w) {
         dfree(w.cols[i]);
     }
     dfree(w.X);
-    dfree(w.pos_of);
     dfree(w.zero);
     dfree(w.ext_seeds);
     dfree(w.ext_counts);
@@ -216,7 +215,7 @@ WinDev win_dev(mgnn_ctx ctx, Win& w) {
         d.cols[i] = w.cols[i];
     }
     d.ucap = ctx->ucap;
-    d.vp_stride = ctx->vp_max;
+    d.seed_hmask = ctx->seed_h - 1;
     d.bm_words = ctx->bm_words;
     d.fr_rank = w.fr_rank;
     d.fr_gid = w.fr_gid;
@@ -224,7 +223,8 @@ WinDev win_dev(mgnn_ctx ctx, Win& w) {
     d.X = w.X;
     d.counts = w.counts;
     d.gctr = w.gctr;
-    d.pos_of = w.pos_of;
+    d.seedpos = w.seedpos;
+    d.ovf = ctx->d_ovf;
     d.fb = w.fb;
     d.fbp = w.fbp;
     d.nb = w.nb;
@@ -290,6 +290,8 @@ mgnn_status mgnn_ctx_create(int32_t device, int32_t n_parts, int64_t n_global, c
     chk(cudaMemset(ctx->d_on_peer, 0, n_parts));
     chk(dalloc(&ctx->d_err, 1));
     chk(cudaMemset(ctx->d_err, 0, sizeof(int32_t)));
+    chk(dalloc(&ctx->d_ovf, 1));
+    chk(cudaMemset(ctx->d_ovf, 0xFF, sizeof(unsigned long long)));
     chk(dalloc(&ctx->d_gathered, 1));
     chk(cudaMemset(ctx->d_gathered, 0, sizeof(long long)));
     chk(dalloc(&ctx->d_sampled, 3));
@@ -325,6 +327,7 @@ void mgnn_destroy(mgnn_ctx ctx) {
     dfree(ctx->d_on_peer);
     dfree(ctx->d_parts);
     dfree(ctx->d_err);
+    dfree(ctx->d_ovf);
     dfree(ctx->d_gathered);
     dfree(ctx->d_evsegs);
     dfree(ctx->d_candsegs);
@@ -342,6 +345,12 @@ void mgnn_destroy(mgnn_ctx ctx) {
 }
 
 const char* mgnn_last_error(mgnn_ctx ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+mgnn_status mgnn_next_step(mgnn_ctx ctx, uint64_t* next_step) {
+    if (!ctx || !next_step) return MGNN_EINVAL;
+    *next_step = ctx->seq_started ? ctx->next_step : 1;
+    return MGNN_OK;
+}
 
 int64_t mgnn_launch_count(mgnn_ctx ctx) {
     (void)ctx;
@@ -693,17 +702,33 @@ mgnn_status mgnn_sampler_expand_remote(mgnn_ctx ctx, int32_t enable) {
 
 mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_layers, int32_t batch,
                                 uint64_t run_seed, int32_t max_window) {
+    return mgnn_sampler_config_bounded(ctx, fanouts, n_layers, batch, run_seed, max_window, 0);
+}
+
+mgnn_status mgnn_sampler_config_bounded(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_layers, int32_t batch,
+                                        uint64_t run_seed, int32_t max_window, int64_t rows_bound) {
     GUARD();
-    if (!fanouts || n_layers < 1 || n_layers > kMaxLayers || batch < 1 || max_window < 1 || max_window > 64)
+    if (!fanouts || n_layers < 1 || n_layers > kMaxLayers || batch < 1 || max_window < 1 || max_window > 64 ||
+        rows_bound < 0 || (rows_bound > 0 && rows_bound < batch))
         return fail(ctx, MGNN_EINVAL, "bad sampler config");
     for (int i = 0; i < n_layers; ++i)
         if (fanouts[i] < 1 || fanouts[i] > MGNN_MAX_FANOUT) return fail(ctx, MGNN_EINVAL, "fanout must be 1..32");
     if (ctx->parts.empty()) return fail(ctx, MGNN_ESTATE, "no partition loaded");
     CK(cudaDeviceSynchronize());
+    {   // resuming after an arena overflow: every window from the overflowed one on was skipped on the
+        // device (no buffer state changed), so the step order resumes there
+        unsigned long long ovf = ~0ull;
+        CK(cudaMemcpy(&ovf, ctx->d_ovf, sizeof(ovf), cudaMemcpyDeviceToHost));
+        if (ovf != ~0ull) {
+            ctx->next_step = ovf;
+            CK(cudaMemset(ctx->d_ovf, 0xFF, sizeof(unsigned long long)));
+        }
+    }
     for (auto& w : ctx->win) free_win(w);
     free_sage(ctx);
     for (auto& p : ctx->parts) free_perm(p);
     ctx->configured = false;
+    ctx->rows_bound = rows_bound;
     ctx->L = n_layers;
     ctx->batch = batch;
     ctx->run_seed = run_seed;
@@ -721,8 +746,11 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
     for (int i = 0; i < n_layers; ++i) {
         ctx->ecap[i] = std::max<int64_t>(sat_mul(ctx->fcap[i], ctx->k_hop[i], big), 1);
         ctx->fcap[i + 1] = std::min<int64_t>(sat_mul(ctx->fcap[i], 1 + ctx->k_hop[i], big), ctx->vp_max);
+        if (rows_bound > 0) ctx->fcap[i + 1] = std::min(ctx->fcap[i + 1], rows_bound);   // realistic bound
     }
     ctx->ucap = ctx->fcap[n_layers];
+    ctx->seed_h = 1;
+    while (ctx->seed_h < 2 * ctx->fcap[0]) ctx->seed_h <<= 1;
     const int n_lp = (int)ctx->parts.size();
     const int64_t M = (int64_t)n_lp * max_window;
     for (auto& w : ctx->win) {
@@ -735,10 +763,9 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
             CK(dalloc(&w.cols[i], M * ctx->ecap[i]));
         }
         CK(dalloc(&w.X, (size_t)M * ctx->ucap * ctx->pitch));
-        CK(dalloc(&w.pos_of, M * ctx->vp_max));
         CK(dalloc(&w.ext_seeds, M * batch));
         CK(dalloc(&w.ext_counts, M));
-        // zero region: [tile counters | status words | counts | fb | fbp], then the per-hop pairs
+        // zero region: [tile counters | status words | counts | fb | fbp | seed hash], then the per-hop pairs
         size_t ctr_words = (size_t)(2 * n_layers + 1) * M;              // int32 (+ gather chunk counters)
         size_t st_words = 0;
         for (int i = 0; i < n_layers; ++i)
@@ -748,7 +775,8 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
         size_t off_cnt = off_st + ((st_words * 8 + 255) / 256) * 256;
         size_t off_fb = off_cnt + (((size_t)M * 8 * 8 + 255) / 256) * 256;
         size_t off_fbp = off_fb + (((size_t)M * ctx->bm_words * 4 + 255) / 256) * 256;
-        size_t off_nb = off_fbp + (((size_t)M * ctx->bm_words * 4 + 255) / 256) * 256;
+        size_t off_sp = off_fbp + (((size_t)M * ctx->bm_words * 4 + 255) / 256) * 256;
+        size_t off_nb = off_sp + (((size_t)M * ctx->seed_h * 8 + 255) / 256) * 256;
         // the (bits, position) pairs follow the zeroed prefix: k_compact writes every word of them
         size_t total = off_nb + (size_t)M * n_layers * ctx->bm_words * 8;
         CK(dalloc(&w.zero, total));
@@ -760,6 +788,7 @@ mgnn_status mgnn_sampler_config(mgnn_ctx ctx, const int32_t* fanouts, int32_t n_
         w.counts = (long long*)(w.zero + off_cnt);
         w.fb = (uint32_t*)(w.zero + off_fb);
         w.fbp = (uint32_t*)(w.zero + off_fbp);
+        w.seedpos = (int2*)(w.zero + off_sp);
         w.nb = (uint32_t*)(w.zero + off_nb);
         size_t so = 0;
         for (int i = 0; i < n_layers; ++i) {
@@ -947,8 +976,8 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
         CK(cudaEventCreate(&pe1));
         CK(cudaEventRecord(pe0, s));
     }
-    launch_decay(ctx->d_parts, n_lp, cap_max, w.n_steps, ctx->pol.gamma, s);
     const uint64_t t_last = w.step0 + (uint64_t)w.n_steps - 1;
+    launch_decay(ctx->d_parts, n_lp, cap_max, w.n_steps, ctx->pol.gamma, ctx->d_ovf, t_last, s);
     if (ctx->pol.delta > 0 && t_last % (uint64_t)ctx->pol.delta == 0) {
         CK(cudaMemsetAsync(ctx->ev_zero, 0, ctx->ev_zero_bytes, s));
         launch_select(ctx->d_parts, n_lp, nmax, ctx->pol.alpha, ctx->pol.theta_r, ctx->d_evsegs, ctx->d_sel_n,
@@ -965,7 +994,8 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
             pairs = ctx->d_candsegs;
             k_of = ctx->ev_ev.thr;
         }
-        launch_swap_refill(ctx->d_parts, n_lp, cap_max, pairs, k_of, world_of(ctx), w.counts, 8, w.n_steps, s);
+        launch_swap_refill(ctx->d_parts, n_lp, cap_max, pairs, k_of, world_of(ctx), w.counts, 8, w.n_steps,
+                           ctx->d_ovf, t_last, s);
     }
     CKL();
     if (ctx->prof) {
@@ -1022,13 +1052,20 @@ mgnn_status mgnn_counts_read(mgnn_ctx ctx, int32_t slot, int64_t* host_counts, m
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t M = (int64_t)ctx->parts.size() * w.n_steps;
     int32_t err = 0;
+    unsigned long long ovf = ~0ull;
     CK(cudaMemcpyAsync(host_counts, w.counts, M * 8 * sizeof(long long), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&err, ctx->d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&ovf, ctx->d_ovf, sizeof(ovf), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (err) {
         ctx->sticky = MGNN_EINVAL;
         return fail(ctx, MGNN_EINVAL, "invalid external seeds (not local or duplicated)");
     }
+    if (ovf <= w.step0 + (uint64_t)w.n_steps - 1)
+        return fail(ctx, MGNN_EOVERFLOW,
+                    "a frontier exceeded the arena bound at the window starting at step " + std::to_string(ovf) +
+                        ": that window and every later one were skipped (buffer state unchanged); reconfigure "
+                        "with a larger bound (mgnn_sampler_config_bounded) and resume sampling at that step");
     return MGNN_OK;
 }
 

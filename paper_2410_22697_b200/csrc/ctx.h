@@ -51,7 +51,7 @@ struct Win {
     int64_t* off[kMaxLayers] = {};
     int32_t* cols[kMaxLayers] = {};
     float* X = nullptr;
-    int32_t* pos_of = nullptr;
+    int2* seedpos = nullptr;        // [M][H] seed positions (inside the zeroed region)
     uint32_t* nb = nullptr;         // [M][L][bm_words][2] new-node bits + word positions (zero region)
     char* zero = nullptr;           // [scan scratch | counts | fb], zeroed per window
     size_t zero_bytes = 0;
@@ -88,6 +88,7 @@ struct mgnn_ctx_s {
     uint8_t* d_on_peer = nullptr;        // [P]: table imported from another process (NVLink)
     PartDev* d_parts = nullptr;
     int32_t* d_err = nullptr;
+    unsigned long long* d_ovf = nullptr; // first step of the first window that overflowed its arena (~0: none)
     long long* d_gathered = nullptr;
     // policy
     bool buffer_ready = false;
@@ -121,6 +122,8 @@ struct mgnn_ctx_s {
     int32_t fan[kMaxLayers] = {}, k_hop[kMaxLayers] = {};
     uint64_t run_seed = 0;
     int64_t ucap = 0, vp_max = 0, bm_words = 0;
+    int64_t rows_bound = 0;              // arena bound on |F_i| per instance (0 = the static worst case)
+    int32_t seed_h = 1;                  // seed-position hash slots per instance
     int64_t fcap[kMaxLayers + 1] = {}, ecap[kMaxLayers] = {};
     mgnn::host::Win win[2];
     SortSeg* d_permsegs = nullptr;       // [n_lp][max perm slots]

@@ -40,7 +40,7 @@ struct WinDev {
     int64_t ucap;                        // rows per instance (X, frontier)
     int64_t off_stride[kMaxLayers];      // offsets row stride per hop (>= fcap_i + 1)
     int64_t col_stride[kMaxLayers];      // cols stride per hop (= ecap_i)
-    int64_t vp_stride;                   // pos_of stride (>= max vp)
+    int32_t seed_hmask;                  // seed-position hash: slots per instance - 1 (power of two >= 2 B)
     int64_t bm_words;                    // bitmap words per instance
     int32_t* fr_rank;                    // [M][ucap]
     int32_t* fr_gid;                     // [M][ucap]
@@ -50,7 +50,11 @@ struct WinDev {
     float* X;                            // [M][ucap][pitch]
     long long* counts;                   // [M][8]
     int32_t* gctr;                       // [M] gather chunk counters (zeroed per window)
-    int32_t* pos_of;                     // [M][vp_stride]
+    int2* seedpos;                       // [M][seed_hmask+1] (rank + 1, position in F_0): open addressing,
+                                         // zeroed per window -- the seeds' positions for k_relabel
+    unsigned long long* ovf;             // smallest first step of a window whose frontier exceeded its
+                                         // arena bound (~0 = none); that window and later ones are skipped
+                                         // by every kernel that changes buffer state
     uint32_t* fb;                        // [M][bm_words] frontier membership (cumulative: F_i, then F_{i+1})
     uint32_t* fbp;                       // [M][bm_words] membership of F_i while hop i runs (new_i = fb & ~fbp)
     uint32_t* nb;                        // [M][L][bm_words][2]: new_i bits of hop i (R#7) and the position
@@ -135,7 +139,9 @@ int64_t scan_tiles_words(int64_t words);  // tiles used by compact for `words`
 void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, cudaStream_t s);
 
 // score.cu
-void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, float gamma, cudaStream_t s);
+// ovf / t_last: the window is skipped when *ovf <= t_last (arena overflow, mgnn_sampler_config_bounded)
+void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, float gamma,
+                  const unsigned long long* ovf, uint64_t t_last, cudaStream_t s);
 void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, float theta_r, const SortSeg* segs,
                    long long* n_out, Scratch sc, EvScratch ev, cudaStream_t s);
 // small-buffer path: candidates below the threshold digit, ranked by counting into sorted order
@@ -143,7 +149,8 @@ void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev
 void launch_cand(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, cudaStream_t s);   // candidates only
 void launch_swap_refill(const PartDev* parts, int n_lp, int64_t cap_max, const SortSeg* segs, const long long* k_of,
                         const WorldDev& world,
-                        long long* counts, int64_t inst_stride_counts, int n_steps, cudaStream_t s);
+                        long long* counts, int64_t inst_stride_counts, int n_steps, const unsigned long long* ovf,
+                        uint64_t t_last, cudaStream_t s);
 // |BUF| up to which the candidate-rank path (no sort) is used for eviction rounds
 constexpr int kEvMax = 65536;
 void launch_init_keys(const PartDev* pd_dev, int64_t n_h, const SortSeg* seg, long long* n_dev, cudaStream_t s);

@@ -54,6 +54,8 @@ static inline unsigned grid_x_for(int64_t items_per_inst, int items_per_block, i
     return (unsigned)(g < 1 ? 1 : g);
 }
 
+__device__ __forceinline__ uint32_t seed_hash(int32_t r) { return (uint32_t)r * 0x9E3779B1u >> 7; }
+
 // ------------------------------------------------------------------ seeds: F_0 (R#8)
 __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
     pdl_enter();
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
         src = perm + s0;
     }
     int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
-    int32_t* pos = W.pos_of + (int64_t)m * W.vp_stride;
+    int2* sp = W.seedpos + (int64_t)m * (W.seed_hmask + 1);
     uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
     uint32_t* fbp = W.fbp + (int64_t)m * W.bm_words;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n0; j += (int64_t)gridDim.x * blockDim.x) {
@@ -91,7 +93,13 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
         const int32_t r = (int32_t)((W.remote ? pd.lo : pd.h_below) + row);   // rank (= global id when remote)
         fr[j] = r;
         W.fr_gid[(int64_t)m * W.ucap + j] = (int32_t)gid;   // F_0 readable right after sampling
-        pos[r] = (int32_t)j;
+        for (uint32_t h = seed_hash(r) & (uint32_t)W.seed_hmask;; h = (h + 1) & (uint32_t)W.seed_hmask) {
+            const int prev = atomicCAS(&sp[h].x, 0, r + 1);        // open addressing, key = rank + 1
+            if (prev == 0 || prev == r + 1) {
+                sp[h].y = (int32_t)j;
+                break;
+            }
+        }
         const uint32_t bit = 1u << (r & 31);
         if (W.ext_seeds) {                                  // user seeds: detect duplicates
             if (atomicOr(&fb[r >> 5], bit) & bit) atomicOr(W.err, 2);
@@ -301,6 +309,9 @@ __global__ void __launch_bounds__(kThreads, 8) k_compact(WinDev W, int hop, Scra
     const int64_t nF = hs[hop];
     int64_t pos = nF + prefix_sh + excl;
     int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
+    // arena bound of F_{hop+1} (mgnn_sampler_config_bounded): positions past it are not stored, the
+    // size is clamped and the window is marked overflowed (every buffer-state kernel then skips it)
+    const int64_t cap = hop + 1 < W.L ? W.off_stride[hop + 1] - 1 : W.ucap;
     if (wd0 < nwords) {
         // new_i keeps its bitmap; with the word's first position it gives every new node's frontier
         // position as wpre + popc(lower bits) (k_relabel), without a scattered rank -> position table
@@ -324,19 +335,23 @@ __global__ void __launch_bounds__(kThreads, 8) k_compact(WinDev W, int hop, Scra
             const int bi = __ffs(bb) - 1;
             bb &= bb - 1;
             const int32_t r = (int32_t)(wd * 32 + bi);
-            MGNN_CHECK(pos < W.ucap && r < (W.remote ? W.n_global : pd.vp), "compact pos=%lld r=%d", (long long)pos, r);
-            fr[pos] = r;
+            MGNN_CHECK(r < (W.remote ? W.n_global : pd.vp), "compact r=%d", r);
+            if (pos < cap) fr[pos] = r;
             ++pos;
         }
     }
-    if (tile == ntiles - 1 && threadIdx.x == 0) hs[hop + 1] = nF + prefix_sh + agg;
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+        const int64_t total = nF + prefix_sh + agg;
+        hs[hop + 1] = total < cap ? total : cap;
+        if (total > cap) atomicMin(W.ovf, (unsigned long long)W.step0);
+    }
 }
 
 // ------------------------------------------------------------------ cols: rank -> position in F_{i+1}
 // A sampled rank c of hop i is either a seed (position from k_seeds' table) or a new node of
 // exactly one hop j <= i; then its position is wpre_j[c/32] + popc(new_j[c/32] & lower bits),
 // since new_j is appended to the frontier in ascending rank order (R#7).
-__device__ __forceinline__ int32_t frontier_pos(const WinDev& W, int m, int hop, const int32_t* __restrict__ posof,
+__device__ __forceinline__ int32_t frontier_pos(const WinDev& W, int m, int hop, const int2* __restrict__ sp,
                                                 int32_t c) {
     const int64_t wd = c >> 5;
     const uint32_t bit = 1u << (c & 31);
@@ -345,13 +360,18 @@ __device__ __forceinline__ int32_t frontier_pos(const WinDev& W, int m, int hop,
         const uint2 bp = __ldg(reinterpret_cast<const uint2*>(W.nb) + o);   // bits and position: one load
         if (bp.x & bit) return (int32_t)bp.y + __popc(bp.x & (bit - 1u));
     }
-    return posof[c];
+    // a seed: its position in F_0 from the window's seed hash (k_seeds)
+    for (uint32_t h = seed_hash(c) & (uint32_t)W.seed_hmask;; h = (h + 1) & (uint32_t)W.seed_hmask) {
+        const int2 e = __ldg(sp + h);
+        if (e.x == c + 1) return e.y;
+        if (e.x == 0) return 0;                  // not reached for a sampled column (overflowed window only)
+    }
 }
 
 __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
     pdl_enter();
     const int m = blockIdx.y;
-    const int32_t* posof = W.pos_of + (int64_t)m * W.vp_stride;
+    const int2* sp = W.seedpos + (int64_t)m * (W.seed_hmask + 1);
     const int64_t* hs = W.hop_size + (int64_t)m * (kMaxLayers + 1);
     const int64_t stride = (int64_t)gridDim.x * kThreads;
     if (W.sampled_units && blockIdx.x == 0 && threadIdx.x == 0) {   // roofline units (bench profiling)
@@ -368,6 +388,7 @@ __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
         const int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
         int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop];
         const int64_t E = off[hs[hop]];
+        const int32_t cap = (int32_t)hs[hop + 1];      // positions stay inside F_{hop+1} (clamped on overflow)
         // kRelabelBatch independent lookups in flight per thread (bitmap / prefix words are L2 reads)
         for (int64_t e0 = (int64_t)blockIdx.x * kThreads * kRelabelBatch + threadIdx.x; e0 < E;
              e0 += stride * kRelabelBatch) {
@@ -375,7 +396,10 @@ __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
 #pragma unroll
             for (int j = 0; j < kRelabelBatch; ++j) c[j] = e0 + j * kThreads < E ? cols[e0 + j * kThreads] : 0;
 #pragma unroll
-            for (int j = 0; j < kRelabelBatch; ++j) c[j] = frontier_pos(W, m, hop, posof, c[j]);
+            for (int j = 0; j < kRelabelBatch; ++j) {
+                const int32_t p = frontier_pos(W, m, hop, sp, c[j]);
+                c[j] = p < cap ? p : cap - 1;
+            }
 #pragma unroll
             for (int j = 0; j < kRelabelBatch; ++j)
                 if (e0 + j * kThreads < E) cols[e0 + j * kThreads] = c[j];

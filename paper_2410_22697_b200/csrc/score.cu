@@ -39,8 +39,10 @@ static inline unsigned blocks_for(int64_t n, int per_block) {
 // Slot s was hit at popc(mask) of the window's n_steps steps; each other step
 // multiplies S_E by gamma once (the same sequence of RN products the paper's
 // per-step loop performs: only *gamma ever touches S_E between rounds).
-__global__ void __launch_bounds__(kSThreads) k_decay(const PartDev* __restrict__ parts, int n_steps, float gamma) {
+__global__ void __launch_bounds__(kSThreads) k_decay(const PartDev* __restrict__ parts, int n_steps, float gamma,
+                                                     const unsigned long long* ovf, uint64_t t_last) {
     pdl_enter();
+    if (*ovf <= t_last) return;                  // arena overflow: the window was skipped
     const PartDev& pd = parts[blockIdx.y];
     for (int64_t s = (int64_t)blockIdx.x * kSThreads + threadIdx.x; s < pd.cap; s += (int64_t)gridDim.x * kSThreads) {
         const unsigned long long mask = pd.hitmask[s];
@@ -52,10 +54,11 @@ __global__ void __launch_bounds__(kSThreads) k_decay(const PartDev* __restrict__
     }
 }
 
-void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, float gamma, cudaStream_t s) {
+void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, float gamma,
+                  const unsigned long long* ovf, uint64_t t_last, cudaStream_t s) {
     if (cap_max < 1) return;
     dim3 grid(blocks_for(cap_max, kSThreads), n_lp);
-    launch_k(k_decay, grid, dim3(kSThreads), 0, s, parts, n_steps, gamma);
+    launch_k(k_decay, grid, dim3(kSThreads), 0, s, parts, n_steps, gamma, ovf, t_last);
     count_launches(1, __func__, s);
 }
 
@@ -306,8 +309,10 @@ void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev
 __global__ void __launch_bounds__(kSThreads) k_swap_refill(const PartDev* __restrict__ parts,
                                                            const SortSeg* __restrict__ segs,
                                                            const long long* __restrict__ k_of, WorldDev G,
-                                                           long long* counts, int64_t counts_stride, int n_steps) {
+                                                           long long* counts, int64_t counts_stride, int n_steps,
+                                                           const unsigned long long* ovf, uint64_t t_last) {
     pdl_enter();
+    if (*ovf <= t_last) return;                  // arena overflow: the window was skipped
     const int lp = blockIdx.y;
     const PartDev& pd = parts[lp];
     const SortSeg E = segs[2 * lp], R = segs[2 * lp + 1];
@@ -351,9 +356,11 @@ __global__ void __launch_bounds__(kSThreads) k_swap_refill(const PartDev* __rest
 
 void launch_swap_refill(const PartDev* parts, int n_lp, int64_t cap_max, const SortSeg* segs, const long long* k_of,
                         const WorldDev& world,
-                        long long* counts, int64_t counts_stride, int n_steps, cudaStream_t s) {
+                        long long* counts, int64_t counts_stride, int n_steps, const unsigned long long* ovf,
+                        uint64_t t_last, cudaStream_t s) {
     dim3 grid(blocks_for(cap_max < 1 ? 1 : cap_max, kSThreads / 32), n_lp);
-    launch_k(k_swap_refill, grid, dim3(kSThreads), 0, s, parts, segs, k_of, world, counts, counts_stride, n_steps);
+    launch_k(k_swap_refill, grid, dim3(kSThreads), 0, s, parts, segs, k_of, world, counts, counts_stride, n_steps,
+             ovf, t_last);
     count_launches(1, __func__, s);
 }
 

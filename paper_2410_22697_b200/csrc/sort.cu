@@ -1,13 +1,13 @@
-// sort.cu -- segmented, stable LSD radix sort of (u64 key, u32 value) pairs
-// ("onesweep" structure: one upfront histogram of every digit, one bin scan,
-// then one scatter launch per 8-bit digit whose tiles find their global digit
-// offsets by a decoupled look-back -- 3 + passes launches per sort instead of
-// 3 per pass).  The element count lives on the device; every kernel is
-// persistent and loops over the tiles that count needs, a digit that is the
-// same for every key is skipped (the identity for a stable sort), and a final
-// copy moves the result back to the primary buffers after an odd number of
-// executed passes.
-//
+// sort.cu -- segmented, stable LSD radix sort of (u64 key, u32 value) pairs:
+// one upfront histogram of every digit, one bin scan that also plans the
+// passes, then per 8-bit digit a count launch (per-tile digit counts) and a
+// scatter launch (each tile sums the counts of the earlier tiles -- independent
+// loads, no tile-to-tile look-back chain -- ranks its keys stably and
+// scatters), and a final fix-up: 3 + 2 * passes launches.  The element count
+// lives on the device; every kernel loops over the tiles that count needs, a
+// digit that is the same for every key is skipped (the identity for a stable
+// sort), and the fix-up copies the result back to the primary buffers after an
+// odd number of executed passes.//
 // Used for every total order the method needs:
 //   * buffer init: halo by (deg_in desc, id asc)            (R#10)
 //   * epoch order: train ids by (Philox key asc, id asc)     (R#8)
@@ -32,16 +32,15 @@ static inline int64_t sort_tiles(int64_t n_max) {
 
 // scratch layout:
 //   bins   u32 [n_seg][passes][256]            digit histograms -> bin offsets      } zeroed by one
-//   ctr    i32 [n_seg][passes]                 dynamic tile ids                     } small memset
-//   plan   i32 [n_seg][passes + 1]             per pass: input parity, or -1 = the pass is trivial
-//                                              (one digit value holds every key); [passes] = final parity
-//   status u32 [n_seg][passes][tiles][256]     look-back words: [31:30] flag, [29:0] count -- zeroed by
-//                                              k_sort_hist for the tiles the device-side length uses, so
-//                                              the host never clears the worst-case size
-// Every kernel is persistent (grid <= a few blocks per SM) and loops over the tiles the device-side
-// length needs, so a sort sized for n_max but holding a few thousand keys costs a few microseconds.
+//   plan   i32 [n_seg][passes + 1]             per pass: input parity, or -1 = the  } small memset
+//                                              pass is trivial (one digit value holds every key);
+//                                              [passes] = parity of the result
+//   tcount u32 [n_seg][passes][tiles][256]     per-tile digit counts of each pass (written by
+//                                              k_sort_count for the tiles the device-side length uses)
+// Every kernel loops over the tiles the device-side length needs (grids of at most a few blocks per
+// SM), so a sort sized for n_max that holds a few thousand keys costs a few microseconds a launch.
 static size_t head_bytes(int n_seg, int passes) {
-    size_t b = (size_t)n_seg * passes * kRadix * 4 + (size_t)n_seg * passes * 4 + (size_t)n_seg * (passes + 1) * 4;
+    size_t b = (size_t)n_seg * passes * kRadix * 4 + (size_t)n_seg * (passes + 1) * 4;
     return (b + 255) / 256 * 256;
 }
 
@@ -52,7 +51,6 @@ size_t radix_scratch_bytes(int n_seg, int64_t n_max, int max_passes) {
 
 struct SortScr {
     uint32_t* bins;
-    int32_t* ctr;
     int32_t* plan;
     uint32_t* status;
 };
@@ -60,15 +58,15 @@ struct SortScr {
 static SortScr carve(void* base, int n_seg, int passes) {
     SortScr s;
     s.bins = (uint32_t*)base;
-    s.ctr = (int32_t*)(s.bins + (size_t)n_seg * passes * kRadix);
-    s.plan = s.ctr + (size_t)n_seg * passes;
+    s.plan = (int32_t*)(s.bins + (size_t)n_seg * passes * kRadix);
     s.status = (uint32_t*)((char*)base + head_bytes(n_seg, passes));
     return s;
 }
 
-// ---- 1. histogram of every digit position in one read of the keys; clears the look-back words
+// ---- 1. histogram of every digit position in one read of the keys
 __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const SortSeg* __restrict__ segs, int passes,
                                                             int64_t tiles_max, SortScr scr) {
+    pdl_enter();
     __shared__ uint32_t h[8][kRadix];
     const SortSeg sg = segs[blockIdx.y];
     const int64_t n = *sg.n;
@@ -76,8 +74,6 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const SortSeg* __res
     for (int p = 0; p < passes; ++p) h[p][threadIdx.x] = 0;
     __syncthreads();
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        for (int p = 0; p < passes; ++p)
-            scr.status[((size_t)(blockIdx.y * passes + p) * tiles_max + t) * kRadix + threadIdx.x] = 0u;
         const int64_t base = t * kSortTile;
 #pragma unroll
         for (int i = 0; i < kSortItems; ++i) {
@@ -97,6 +93,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const SortSeg* __res
 // ---- 2. exclusive scan of each digit histogram -> bin offsets; the pass plan (trivial passes skipped)
 __global__ void __launch_bounds__(kSortThreads) k_sort_binscan(const SortSeg* __restrict__ segs, int passes,
                                                                SortScr scr) {
+    pdl_enter();
     __shared__ long long sm[8];
     __shared__ int trivial_sh;
     const SortSeg sg = segs[blockIdx.y];
@@ -120,23 +117,47 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_binscan(const SortSeg* __
     if (threadIdx.x == 0) plan[passes] = parity;
 }
 
-__device__ __forceinline__ void st_rel32(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// ---- 3. one digit pass in two launches (no serial look-back chain: a pass sorts at most a few
+// hundred thousand keys, where a chain of tile-to-tile waits costs more than a second launch):
+//   k_sort_count   per tile: digit counts -> tcount[seg][tile][256]
+//   k_sort_scatter per tile: global offset of each digit = bin offset + counts of the earlier tiles
+//                  (independent loads, one column per thread), stable local ranks, scatter
+__global__ void __launch_bounds__(kSortThreads) k_sort_count(const SortSeg* __restrict__ segs, int passes, int p,
+                                                             int64_t tiles_max, SortScr scr) {
+    pdl_enter();
+    __shared__ uint32_t h[kRadix];
+    const int s = blockIdx.y;
+    const SortSeg sg = segs[s];
+    const int parity = scr.plan[(size_t)s * (passes + 1) + p];
+    if (parity < 0) return;
+    const int64_t n = *sg.n;
+    const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+    const unsigned long long* kin = parity ? sg.keys_tmp : sg.keys;
+    const int shift = sg.shift[p];
+    const int lane = threadIdx.x & 31;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        h[threadIdx.x] = 0;
+        __syncthreads();
+        const int64_t base = t * kSortTile;
+#pragma unroll
+        for (int i = 0; i < kSortItems; ++i) {
+            const int64_t idx = base + (int64_t)i * kSortThreads + threadIdx.x;
+            const unsigned digit = idx < n ? ((unsigned)(kin[idx] >> shift) & 0xFF) : (0x100u | lane);
+            const unsigned peers = __match_any_sync(kFull, digit);
+            if (digit < 0x100u && lane == __ffs(peers) - 1) atomicAdd(&h[digit], (unsigned)__popc(peers));
+        }
+        __syncthreads();
+        scr.status[((size_t)(s * passes + p) * tiles_max + t) * kRadix + threadIdx.x] = h[threadIdx.x];
+        __syncthreads();
+    }
 }
-__device__ __forceinline__ uint32_t ld_acq32(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-constexpr uint32_t kSAgg = 1u << 30, kSInc = 2u << 30, kSMask = (1u << 30) - 1;
 
-// ---- 3. one digit pass: local stable ranks, per-digit look-back, scatter (persistent over tiles)
-__global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortSeg* __restrict__ segs, int passes, int p,
-                                                            int64_t tiles_max, SortScr scr) {
+__global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const SortSeg* __restrict__ segs, int passes, int p,
+                                                               int64_t tiles_max, SortScr scr) {
+    pdl_enter();
     __shared__ uint32_t run[kRadix];       // per-digit running count inside the tile
     __shared__ uint32_t wc[8][kRadix];     // per-warp digit counts of the current round
     __shared__ uint32_t gofs[kRadix];      // global offset of the tile's first item of each digit
-    __shared__ int tslot;
     const int s = blockIdx.y;
     const SortSeg sg = segs[s];
     const int parity = scr.plan[(size_t)s * (passes + 1) + p];
@@ -150,14 +171,25 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortSeg* __res
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const int shift = sg.shift[p];
-    for (;;) {
-        const int tile = claim_tile(scr.ctr + s * passes + p, &tslot);
-        __syncthreads();                       // tslot is rewritten by the next claim
-        if (tile >= ntiles) return;
-        const int64_t base = (int64_t)tile * kSortTile;
-        run[threadIdx.x] = 0;
-        for (int w = 0; w < 8; ++w) wc[w][threadIdx.x] = 0;
+    const uint32_t* tc = scr.status + ((size_t)(s * passes + p) * tiles_max) * kRadix;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        {   // thread d: exclusive prefix of digit d over the earlier tiles (independent loads)
+            const int d = threadIdx.x;
+            uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+            int64_t j = 0;
+            for (; j + 4 <= tile; j += 4) {
+                a0 += tc[(size_t)j * kRadix + d];
+                a1 += tc[(size_t)(j + 1) * kRadix + d];
+                a2 += tc[(size_t)(j + 2) * kRadix + d];
+                a3 += tc[(size_t)(j + 3) * kRadix + d];
+            }
+            for (; j < tile; ++j) a0 += tc[(size_t)j * kRadix + d];
+            gofs[d] = scr.bins[(size_t)(s * passes + p) * kRadix + d] + a0 + a1 + a2 + a3;
+            run[d] = 0;
+            for (int w = 0; w < 8; ++w) wc[w][d] = 0;
+        }
         __syncthreads();
+        const int64_t base = tile * kSortTile;
         unsigned long long key[kSortItems];
         uint32_t val[kSortItems], rank[kSortItems];
 #pragma unroll
@@ -187,28 +219,6 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortSeg* __res
             for (int w = 0; w < 8; ++w) wc[w][threadIdx.x] = 0;
             __syncthreads();
         }
-        {   // thread d: publish the tile's count of digit d, look back for its exclusive prefix
-            const int d = threadIdx.x;
-            const uint32_t cnt = run[d];
-            uint32_t* st = scr.status + ((size_t)(s * passes + p) * tiles_max) * kRadix;
-            uint32_t excl = 0;
-            if (tile == 0) {
-                st_rel32(&st[d], kSInc | cnt);
-            } else {
-                st_rel32(&st[(size_t)tile * kRadix + d], kSAgg | cnt);
-                for (int j = tile - 1; j >= 0; --j) {
-                    uint32_t v;
-                    do {
-                        v = ld_acq32(&st[(size_t)j * kRadix + d]);
-                    } while ((v & ~kSMask) == 0);
-                    excl += v & kSMask;
-                    if ((v & ~kSMask) == kSInc) break;
-                }
-                st_rel32(&st[(size_t)tile * kRadix + d], kSInc | (excl + cnt));
-            }
-            gofs[d] = scr.bins[(size_t)(s * passes + p) * kRadix + d] + excl;
-        }
-        __syncthreads();
 #pragma unroll
         for (int i = 0; i < kSortItems; ++i) {
             if (rank[i] == 0xFFFFFFFFu) continue;
@@ -224,6 +234,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const SortSeg* __res
 
 // ---- 4. an odd number of executed passes left the result in the tmp buffers: copy it back
 __global__ void __launch_bounds__(kSortThreads) k_sort_fix(const SortSeg* __restrict__ segs, int passes, SortScr scr) {
+    pdl_enter();
     const SortSeg sg = segs[blockIdx.y];
     if (scr.plan[(size_t)blockIdx.y * (passes + 1) + passes] == 0) return;
     const int64_t n = *sg.n;
@@ -240,15 +251,18 @@ void radix_sort_pairs(const SortSeg* segs_dev, int n_seg, int64_t n_max, int max
     const int64_t tiles = sort_tiles(n_max);
     cudaMemsetAsync(scratch, 0, head_bytes(n_seg, passes), s);
     const SortScr scr = carve(scratch, n_seg, passes);
-    // persistent grids: at most ~4 blocks per SM over all segments; tiles are looped / claimed
+    // grids of at most ~4 blocks per SM over all segments; every kernel loops over its tiles
     int64_t gx = ((int64_t)num_sms() * 4 + n_seg - 1) / n_seg;
     if (gx > tiles) gx = tiles;
     dim3 grid((unsigned)(gx < 1 ? 1 : gx), (unsigned)n_seg);
-    k_sort_hist<<<grid, kSortThreads, 0, s>>>(segs_dev, passes, tiles, scr);
-    k_sort_binscan<<<dim3(1, n_seg), kSortThreads, 0, s>>>(segs_dev, passes, scr);
-    for (int p = 0; p < passes; ++p) k_sort_pass<<<grid, kSortThreads, 0, s>>>(segs_dev, passes, p, tiles, scr);
-    k_sort_fix<<<grid, kSortThreads, 0, s>>>(segs_dev, passes, scr);
-    count_launches(3 + passes, __func__, s);
+    launch_k(k_sort_hist, grid, dim3(kSortThreads), 0, s, segs_dev, passes, tiles, scr);
+    launch_k(k_sort_binscan, dim3(1, n_seg), dim3(kSortThreads), 0, s, segs_dev, passes, scr);
+    for (int p = 0; p < passes; ++p) {
+        launch_k(k_sort_count, grid, dim3(kSortThreads), 0, s, segs_dev, passes, p, tiles, scr);
+        launch_k(k_sort_scatter, grid, dim3(kSortThreads), 0, s, segs_dev, passes, p, tiles, scr);
+    }
+    launch_k(k_sort_fix, grid, dim3(kSortThreads), 0, s, segs_dev, passes, scr);
+    count_launches(3 + 2 * passes, __func__, s);
 }
 
 }  // namespace mgnn

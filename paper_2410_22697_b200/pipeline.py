@@ -116,10 +116,14 @@ class Context:
         """NEXT-1: sample non-local frontier nodes from their owner's CSR (before sampler_config)."""
         self._chk("mgnn_sampler_expand_remote", self.L.mgnn_sampler_expand_remote(self._h, 1 if enable else 0))
 
-    def sampler_config(self, fanouts: Sequence[int], batch: int, run_seed: int, max_window: int):
+    def sampler_config(self, fanouts: Sequence[int], batch: int, run_seed: int, max_window: int,
+                       rows_bound: int = 0):
+        """rows_bound > 0: realistic window arenas (mgnn_sampler_config_bounded); 0: static worst case."""
         fo = np.array(fanouts, dtype=np.int32)
-        self._chk("mgnn_sampler_config",
-                  self.L.mgnn_sampler_config(self._h, _ptr(fo), fo.shape[0], batch, run_seed, max_window))
+        self._chk("mgnn_sampler_config_bounded",
+                  self.L.mgnn_sampler_config_bounded(self._h, _ptr(fo), fo.shape[0], batch, run_seed, max_window,
+                                                     int(rows_bound)))
+        self.rows_bound = int(rows_bound)
         self.fanouts = list(fanouts)
         self.batch = batch
         self.max_window = max_window
@@ -282,6 +286,12 @@ class Context:
         self._chk("mgnn_table_row", self.L.mgnn_table_row(self._h, node, _ptr(out)))
         return out
 
+    def next_step(self) -> int:
+        """mgnn_next_step: first step of the next window the library will gather."""
+        out = C.c_uint64()
+        self._chk("mgnn_next_step", self.L.mgnn_next_step(self._h, C.byref(out)))
+        return int(out.value)
+
     def launch_count(self) -> int:
         return int(self.L.mgnn_launch_count(self._h))
 
@@ -302,6 +312,24 @@ class Context:
         b = C.c_int64()
         self._chk("mgnn_profile_read", self.L.mgnn_profile_read(self._h, C.byref(ms), C.byref(n), C.byref(b)))
         return ms.value, n.value, b.value
+
+
+def estimate_rows_bound(ctx: "Context", fanouts: Sequence[int], batch: int, run_seed: int, pilot_steps=(1, 2),
+                        slack: float = 1.25, stream=None) -> int:
+    """A realistic arena bound for mgnn_sampler_config_bounded: the largest |F_L| of a pilot
+    (one-step windows at `pilot_steps`, every hosted partition, static arenas for one step) times
+    `slack`, rounded up to 1024 rows.  Sampling reads no buffer state, so the pilot changes nothing
+    the run depends on; the caller reconfigures the sampler afterwards."""
+    import torch
+    ctx.sampler_config(fanouts, batch, run_seed, 1)
+    u_max = 0
+    for t in pilot_steps:
+        ctx.sample(0, int(t), 1, stream=stream)
+        w = ctx.window(0)
+        hs = device_view(w.hop_size, (w.n_inst, _lib.MAX_LAYERS + 1), "i8")[:, w.n_layers]
+        torch.cuda.synchronize()
+        u_max = max(u_max, int(hs.max().item()))
+    return int(-(-int(u_max * slack) // 1024) * 1024)
 
 
 def alpha_default(gamma: float, delta: int) -> float:

@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--windows", type=int, default=4)
     ap.add_argument("--train", action="store_true", help="DDP training-step parity (NEXT-3) instead")
     ap.add_argument("--remote", action="store_true", help="NEXT-1 remote expansion (replicated global CSR)")
+    ap.add_argument("--parts", type=int, default=0, help="total partitions P (default 2 per GPU)")
+    ap.add_argument("--digest-out", default="", help="write this rank's per-partition result digests (JSON)")
     a = ap.parse_args()
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -34,8 +36,10 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = synth.CONFIGS[a.config]
     g = synth.generate(cfg)
-    P = 2 * world
-    hosted = [2 * rank, 2 * rank + 1]
+    P = a.parts or 2 * world
+    assert P % world == 0
+    per = P // world
+    hosted = list(range(per * rank, per * (rank + 1)))
     ok = torch.ones(1, device="cuda")
     try:
         if a.train:
@@ -50,6 +54,10 @@ def main():
                         [a.delta] * a.windows, hosted=hosted, device=local, exchange=True, remote=a.remote,
                         sample_every=1 if a.config == "cfg1" else 9, check_x_rows=0 if a.config == "cfg1" else 2048)
         print(f"[rank {rank}] parity ok: {st}", flush=True)
+        if a.digest_out:
+            import json
+            with open(f"{a.digest_out}.rank{rank}", "w") as f:
+                json.dump(st["digest"], f)
         assert st["misses"] > 0 and st["evicted"] > 0 and st["peer_rows"] > 0
     except Exception as e:  # report, then fail the collective result
         print(f"[rank {rank}] FAILED: {e!r}", flush=True)

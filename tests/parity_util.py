@@ -13,6 +13,8 @@ per partition, element by element:
 """
 from __future__ import annotations
 
+import hashlib
+
 import numpy as np
 
 from inputs import synth
@@ -36,7 +38,8 @@ def assert_bits_equal(a, b, what):
 def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, gamma: float, delta: int,
                theta_r: float, windows, run_seed: int = synth.RUN_SEED, feat_seed: int = synth.FEAT_SEED,
                alpha=None, hosted=None, sample_every: int = 1, check_x_rows: int = 0, ext_seeds=None,
-               device: int = 0, exchange: bool = False, remote: bool = False, dense: bool = False):
+               device: int = 0, exchange: bool = False, remote: bool = False, dense: bool = False,
+               rows_bound: int = 0):
     """windows: list of window lengths run back to back from step 1."""
     from paper_2410_22697_b200 import pipeline as PL
 
@@ -55,7 +58,9 @@ def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, g
     if exchange:                      # multi-process: map the other ranks' tables (CUDA IPC, NVLink)
         PL.exchange_tables(ctx)
     ctx.buffer_init(gamma, alpha, theta_r, delta, f_bp)
-    ctx.sampler_config(fanouts, batch, run_seed, max(windows))
+    if rows_bound < 0:                # realistic arenas from a pilot (pipeline.estimate_rows_bound)
+        rows_bound = PL.estimate_rows_bound(ctx, fanouts, batch, run_seed)
+    ctx.sampler_config(fanouts, batch, run_seed, max(windows), rows_bound=rows_bound)
     lps = {pid: lp for lp, pid in enumerate(ctx.parts)}
     # static partition facts
     for pid, lp in lps.items():
@@ -68,6 +73,7 @@ def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, g
     t = 1
     slot = 0
     stats = {"steps": 0, "hits": 0, "misses": 0, "evicted": 0}
+    digests = {pid: hashlib.sha256() for pid in lps}     # per-partition digest of everything compared
     for wlen in windows:
         seeds_arr = cnt_arr = None
         if ext_seeds is not None:
@@ -95,6 +101,7 @@ def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, g
                 got = [gc[0], gc[1], gc[2], gc[3], gc[4], gc[6]]
                 want = [oc["n_nodes"], oc["n_local"], oc["n_hit"], oc["n_miss"], oc["n_evicted"], oc["rows_fetched"]]
                 assert got == want, (pid, step, got, want)      # counts: every step
+                digests[pid].update(np.asarray(got, np.int64).tobytes())
                 # NVLink rows (counts[7]): misses + refills owned by a partition on another GPU
                 refill = gc[5] if w == wlen - 1 else 0
                 assert 0 <= gc[7] <= gc[3] + refill, (pid, step, gc[7])
@@ -132,8 +139,11 @@ def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, g
             assert_bits_equal(gs["sa"], os_["sa"], f"S_A p{pid} after t{t + wlen - 1}")
             assert_bits_equal(gs["slot_of"], os_["slot_of"], f"slot_of p{pid} after t{t + wlen - 1}")
             assert_bits_equal(gs["rows"], os_["rows"], f"BUF rows p{pid} after t{t + wlen - 1}")
+            for k in ("node_of_slot", "se", "sa", "slot_of"):
+                digests[pid].update(np.ascontiguousarray(gs[k]).tobytes())
         t += wlen
         slot ^= 1
+    stats["digest"] = {int(pid): h.hexdigest() for pid, h in digests.items()}
     if exchange:                      # peers may still read our tables until every rank is done
         import torch
         import torch.distributed as dist

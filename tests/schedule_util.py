@@ -24,7 +24,7 @@ from tests.parity_util import assert_bits_equal
 
 def run_schedule_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, gamma: float, delta: int,
                         window: int, n_windows: int, x_rows: int = 2048, warm: int = 0, flush_bytes: int = 256 << 20,
-                        run_seed: int = synth.RUN_SEED, feat_seed: int = synth.FEAT_SEED):
+                        run_seed: int = synth.RUN_SEED, feat_seed: int = synth.FEAT_SEED, rows_bound: int = -1):
     import torch
     from paper_2410_22697_b200 import pipeline as PL
     from paper_2410_22697_b200.schedule import PrepareAhead
@@ -33,7 +33,9 @@ def run_schedule_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_b
     alpha = float(O.alpha_default(gamma, delta))
     ctx = PL.build_context(0, parts, D, feat_seed)
     ctx.buffer_init(gamma, alpha, 1.0, delta, f_bp)
-    ctx.sampler_config(fanouts, batch, run_seed, window)
+    if rows_bound < 0:                 # realistic arenas, as bench.py sizes them
+        rows_bound = PL.estimate_rows_bound(ctx, fanouts, batch, run_seed)
+    ctx.sampler_config(fanouts, batch, run_seed, window, rows_bound=rows_bound)
     L = len(fanouts)
     n_inst = P * window
     pipe = PrepareAhead(ctx, window, t0=1, flush_bytes=flush_bytes)
@@ -67,6 +69,7 @@ def run_schedule_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_b
     for i in range(n_windows):                   # the bench loop, no host sync inside
         pipe.iteration(events=ev[i], after_consume=grab, prepare_next=i + 1 < n_windows)
     torch.cuda.synchronize()
+    ctx.counts(pipe.slot ^ 1)                    # raises MGNN_EOVERFLOW if any window overflowed its arena
     ms = [a.elapsed_time(b) for a, b in ev]
     snaps = {pid: ctx.snapshot(lp, rows=True) for lp, pid in enumerate(ctx.parts)}
     lps = {pid: lp for lp, pid in enumerate(ctx.parts)}

@@ -211,3 +211,82 @@ def test_consumer_training_remote_call_order_and_arguments(graph):
         c2.expand_remote(True)
     assert _status(e) == ESTATE
     c2.close()
+
+
+def test_arena_overflow_skips_windows_and_resumes(graph):
+    """mgnn_sampler_config_bounded: a window whose frontier exceeds the arena bound is detected on the
+    device, it and every later window are skipped by the buffer-state kernels, counts_read reports
+    MGNN_EOVERFLOW (not sticky), and reconfiguring with a larger bound resumes at the overflowed
+    step -- the run then matches the oracle's uninterrupted run bit for bit."""
+    EOVERFLOW = 6
+    P, fan, B, f_bp, gamma, delta = 2, [10, 25], 256, 2500, 0.9, 4
+    parts = synth.partition(graph, P)
+    alpha = float(O.alpha_default(gamma, delta))
+    ctx = PL.build_context(0, parts, 64, synth.FEAT_SEED)
+    ctx.buffer_init(gamma, alpha, 1.0, delta, f_bp)
+    bound = PL.estimate_rows_bound(ctx, fan, B, synth.RUN_SEED)
+    assert B <= bound
+    ctx.sampler_config(fan, B, synth.RUN_SEED, 4, rows_bound=bound)
+    counts = []
+    t, slot = 1, 0
+    for _ in range(2):                                  # steps 1-8 fit
+        ctx.sample(slot, t, 4)
+        ctx.lookup_gather(slot)
+        ctx.score(slot)
+        counts.append(ctx.counts(slot))
+        t += 4
+        slot ^= 1
+    snap_before = [ctx.snapshot(lp, rows=True) for lp in range(P)]
+    ctx.sampler_config(fan, B, synth.RUN_SEED, 4, rows_bound=B + 1)   # far too small: overflows at step 9
+    for _ in range(2):                                  # steps 9-16: both windows skipped on the device
+        ctx.sample(slot, t, 4)
+        ctx.lookup_gather(slot)
+        ctx.score(slot)
+        with pytest.raises(MgnnError) as e:
+            ctx.counts(slot)
+        assert _status(e) == EOVERFLOW and "step 9" in str(e.value)
+        t += 4
+        slot ^= 1
+    for lp in range(P):                                 # buffer state untouched by the skipped windows
+        snap = ctx.snapshot(lp, rows=True)
+        for k in ("node_of_slot", "se", "sa", "slot_of", "rows"):
+            assert np.array_equal(np.asarray(snap[k]).view(np.uint8), np.asarray(snap_before[lp][k]).view(np.uint8))
+    ctx.sampler_config(fan, B, synth.RUN_SEED, 4, rows_bound=0)       # resume at step 9
+    t = 9
+    with pytest.raises(MgnnError) as e:                 # the step order now restarts at 9, not 17
+        ctx.sample(slot, 17, 4)
+        ctx.lookup_gather(slot)
+    assert _status(e) == ESTATE
+    for _ in range(2):
+        ctx.sample(slot, t, 4)
+        ctx.lookup_gather(slot)
+        ctx.score(slot)
+        counts.append(ctx.counts(slot))
+        t += 4
+        slot ^= 1
+    W = O.World(parts, 64, synth.FEAT_SEED)
+    for p in W.parts:
+        p.buffer_init(gamma, alpha, 1.0, delta, f_bp)
+    for wi in range(4):
+        for w in range(4):
+            step = 1 + 4 * wi + w
+            for pid in range(P):
+                op = W.parts[pid]
+                op.step(synth.RUN_SEED, step, fan, B)
+                oc = op.counts()
+                gc = counts[wi][pid * 4 + w]
+                assert [gc[0], gc[2], gc[3], gc[4]] == [oc["n_nodes"], oc["n_hit"], oc["n_miss"], oc["n_evicted"]]
+    for pid in range(P):
+        gs = ctx.snapshot(pid, rows=True)
+        os_ = W.parts[pid].buffer_state(rows=True)
+        for k in ("node_of_slot", "se", "sa", "slot_of", "rows"):
+            assert np.array_equal(np.asarray(gs[k]).view(np.uint8), np.asarray(os_[k]).view(np.uint8)), k
+    ctx.close()
+    W.close()
+
+
+def test_bounded_arenas_parity(graph):
+    """Realistic arenas from the pilot bound (the bench's sizing) give the oracle's results."""
+    from tests.parity_util import run_parity
+    st = run_parity(graph, 2, 64, [10, 25], 256, 2500, 0.9, 4, 1.0, [4, 4, 4], rows_bound=-1)
+    assert st["evicted"] > 0

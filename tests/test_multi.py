@@ -159,3 +159,40 @@ def test_nccl_two_gpus_remote_expansion_parity():
                        capture_output=True, text=True, timeout=900, cwd=ROOT)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
+
+
+def _digests(prefix, world):
+    import json
+    out = {}
+    for r in range(world):
+        with open(f"{prefix}.rank{r}") as f:
+            out.update({int(k): v for k, v in json.load(f).items()})
+    return out
+
+
+@pytest.mark.gpu
+def test_placement_invariance_p8(tmp_path):
+    """SURVEY §4 layer 4 / north_star's layout: P = 8 partitions give the SAME per-partition results
+    (counts of every step, final BUF / S_E / S_A / slot_of -- each run also checked against the oracle)
+    whether one GPU hosts all 8, two GPUs host 4 each or four GPUs host 2 each (miss and refill rows of
+    partitions on other GPUs then cross NVLink)."""
+    sys.path.insert(0, ROOT)
+    from inputs import synth
+    from tests.parity_util import run_parity
+    g = synth.generate(synth.CONFIGS["cfg1"])
+    one = run_parity(g, 8, 64, [10, 25], 256, 2500, 0.9, 4, 1.0, [4] * 4)["digest"]
+    assert sorted(one) == list(range(8))
+    n = torch.cuda.device_count()
+    for world in (2, 4):
+        if n < world:
+            continue
+        prefix = str(tmp_path / f"dig{world}")
+        port = _free_port()
+        r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+                            "--master-addr", "127.0.0.1", "--master-port", str(port),
+                            os.path.join(ROOT, "tests", "multi_gpu_parity.py"), "--parts", "8",
+                            "--digest-out", prefix],
+                           capture_output=True, text=True, timeout=900, cwd=ROOT)
+        print(r.stdout[-3000:], r.stderr[-3000:])
+        assert r.returncode == 0
+        assert _digests(prefix, world) == one, world
