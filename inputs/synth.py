@@ -242,11 +242,14 @@ def describe(g: Graph, parts: List[PartitionInput]) -> dict:
     """Achieved shape statistics reported beside every result."""
     deg = np.diff(g.indptr)
     halo = []
+    seen = np.zeros(g.n_nodes, dtype=bool)
     for pi in parts:
         lo, hi = int(pi.bounds[pi.part_id]), int(pi.bounds[pi.part_id + 1])
         c = pi.cols
-        nl = c[(c < lo) | (c >= hi)]
-        halo.append(int(np.unique(nl).shape[0]) / max(1, hi - lo))
+        seen[:] = False
+        seen[c] = True                      # distinct neighbours without a sort (papers: 400M per part)
+        n_h = int(seen[:lo].sum()) + int(seen[hi:].sum())
+        halo.append(n_h / max(1, hi - lo))
     # degree histogram in power-of-two buckets: bucket b counts nodes with 2^(b-1) <= deg < 2^b (b = 0: deg 0)
     b = np.zeros(deg.shape, np.int64)
     nz = deg > 0
