@@ -203,8 +203,18 @@ def nvlink_counters(index: int):
     bytes that crossed this GPU's links while it ran."""
     try:
         import pynvml as nv
+        import torch
         nv.nvmlInit()
-        h = nv.nvmlDeviceGetHandleByIndex(index)
+        pr = torch.cuda.get_device_properties(index)
+        want = (int(pr.pci_domain_id), int(pr.pci_bus_id), int(pr.pci_device_id))
+        h = None
+        for i in range(nv.nvmlDeviceGetCount()):              # the NVML device of this CUDA ordinal
+            hh = nv.nvmlDeviceGetHandleByIndex(i)
+            pci = nv.nvmlDeviceGetPciInfo(hh)
+            if (int(pci.domain), int(pci.bus), int(pci.device)) == want:
+                h = hh
+        if h is None:
+            return None
         ids = [nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX]
         vals = nv.nvmlDeviceGetFieldValues(h, ids)
         out = []

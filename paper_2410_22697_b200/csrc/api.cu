@@ -146,6 +146,9 @@ mgnn_status upload_tables(mgnn_ctx ctx) {
     std::vector<uint8_t> peer(ctx->P);
     for (int q = 0; q < ctx->P; ++q) peer[q] = (ctx->tables[q] && ctx->lp_of[q] < 0) ? 1 : 0;
     CK(cudaMemcpy(ctx->d_on_peer, peer.data(), ctx->P, cudaMemcpyHostToDevice));
+    std::vector<int8_t> lpo(ctx->P);
+    for (int q = 0; q < ctx->P; ++q) lpo[q] = (int8_t)(ctx->lp_of[q] < 128 ? ctx->lp_of[q] : -1);
+    CK(cudaMemcpy(ctx->d_lp_of, lpo.data(), ctx->P, cudaMemcpyHostToDevice));
     return MGNN_OK;
 }
 
@@ -156,6 +159,7 @@ WorldDev world_of(mgnn_ctx ctx) {
     w.bounds = ctx->d_bounds;
     w.tables = ctx->d_tables;
     w.on_peer = ctx->d_on_peer;
+    w.lp_of = ctx->d_lp_of;
     return w;
 }
 
@@ -288,6 +292,8 @@ mgnn_status mgnn_ctx_create(int32_t device, int32_t n_parts, int64_t n_global, c
     chk(cudaMemset((void*)ctx->d_tables, 0, n_parts * sizeof(float*)));
     chk(dalloc(&ctx->d_on_peer, n_parts));
     chk(cudaMemset(ctx->d_on_peer, 0, n_parts));
+    chk(dalloc(&ctx->d_lp_of, n_parts));
+    chk(cudaMemset(ctx->d_lp_of, 0xFF, n_parts));
     chk(dalloc(&ctx->d_err, 1));
     chk(cudaMemset(ctx->d_err, 0, sizeof(int32_t)));
     chk(dalloc(&ctx->d_ovf, 1));
@@ -325,6 +331,7 @@ void mgnn_destroy(mgnn_ctx ctx) {
     dfree(ctx->d_bounds);
     dfree(ctx->d_tables);
     dfree(ctx->d_on_peer);
+    dfree(ctx->d_lp_of);
     dfree(ctx->d_parts);
     dfree(ctx->d_err);
     dfree(ctx->d_ovf);
@@ -628,6 +635,18 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
         CKL();
     }
     CK(cudaStreamSynchronize(s));
+    {   // TMA row-gather descriptors of every source on this GPU (k_gather_g4)
+        ctx->g4_ok = n_lp <= kMaxGatherMaps / 2 && ctx->D == ctx->pitch;
+        memset(&ctx->gmaps, 0, sizeof(ctx->gmaps));
+        ctx->gmaps.n_lp = n_lp;
+        for (int lp = 0; lp < n_lp && ctx->g4_ok; ++lp) {
+            const Part& p = ctx->parts[lp];
+            ctx->g4_ok = encode_row_map(ctx->gmaps.maps[lp], p.table, std::max<int64_t>(p.n_local, 1), ctx->D,
+                                        ctx->pitch) &&
+                         encode_row_map(ctx->gmaps.maps[n_lp + lp], p.rows, std::max<int64_t>(p.cap, 1), ctx->D,
+                                        ctx->pitch);
+        }
+    }
     ctx->pol = *pol;
     ctx->buffer_ready = true;
     ctx->seq_started = false;
@@ -945,7 +964,7 @@ mgnn_status mgnn_lookup_gather(mgnn_ctx ctx, int32_t slot, mgnn_stream stream) {
     for (auto& p : ctx->parts) table_bytes += p.n_local * (int64_t)ctx->pitch * 4;
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device);
-    launch_gather(wd, world_of(ctx), table_bytes <= (int64_t)l2 * 3 / 4, s);
+    launch_gather(wd, world_of(ctx), table_bytes <= (int64_t)l2 * 3 / 4, ctx->g4_ok ? &ctx->gmaps : nullptr, s);
     CKL();
     if (ctx->prof) {
         CK(cudaEventRecord(e1, s));

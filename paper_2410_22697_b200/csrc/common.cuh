@@ -90,6 +90,7 @@ struct WorldDev {
     const int64_t* bounds;      // [P+1]
     const float* const* tables; // [P] device-accessible pointers (NVLink peer pointers for remote)
     const uint8_t* on_peer;     // [P] 1 if the table lives on another GPU (rows cross NVLink)
+    const int8_t* lp_of;        // [P] local index of partition q in this context, or -1
 };
 
 __device__ __forceinline__ int owner_of(const int64_t* __restrict__ bounds, int P, int64_t v) {

@@ -86,6 +86,11 @@ struct mgnn_ctx_s {
     int64_t* d_bounds = nullptr;
     const float** d_tables = nullptr;
     uint8_t* d_on_peer = nullptr;        // [P]: table imported from another process (NVLink)
+    int8_t* d_lp_of = nullptr;           // [P]: local index of each partition hosted here, else -1
+    // TMA row-gather descriptors (k_gather_g4): [0, n_lp) tables, [n_lp, 2 n_lp) BUF rows; built by
+    // mgnn_buffer_init (the BUF rows live there); g4_ok = every descriptor encoded
+    GatherMaps gmaps{};
+    bool g4_ok = false;
     PartDev* d_parts = nullptr;
     int32_t* d_err = nullptr;
     unsigned long long* d_ovf = nullptr; // first step of the first window that overflowed its arena (~0: none)

@@ -375,7 +375,161 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
     flush();
 }
 
-void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, cudaStream_t s) {
+// ------------------------------------------------------------------ TMA row-gather variant (gather4)
+// Same classification, but rows that come from a source on this GPU -- the partition's own table (local),
+// its BUF rows (hits), or the table of another partition hosted by this context (misses) -- are loaded
+// by the tensor-memory accelerator FOUR AT A TIME: a chunk of R rows (R % 4 == 0) is split into groups
+// of 4 consecutive frontier positions; a group whose 4 rows share one source descriptor is one
+// cp.async.bulk.tensor.2d...tile::gather4 (4 row indices, one instruction), any other row (mixed group,
+// a peer GPU's table, the tail) one cp.async.bulk row copy as in k_gather_tma.  Frontier segments are
+// sorted by rank (R#7), which keeps local rows and halo rows in runs, so most groups are pure.  Each
+// group occupies a 128-byte-aligned slot of the stage and leaves with one bulk store (4 rows).
+// Bulk copies take their operands from uniform registers, so a warp issues them one lane at a time:
+// one instruction per 4 rows instead of one per row is what this variant buys.
+__device__ __forceinline__ void g4_load(void* sdst, const void* map, int32_t r0, int32_t r1, int32_t r2, int32_t r3,
+                                        uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(sdst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kTWarps * 32) k_gather_g4(WinDev W, WorldDev G, const __grid_constant__ GatherMaps gm,
+                                                             int R, int gstride, int hint) {
+    pdl_enter();
+    if (*W.ovf <= W.step0 + (uint64_t)W.n_steps - 1) return;   // arena overflow: window skipped
+    extern __shared__ __align__(128) unsigned char tsm[];
+    __shared__ __align__(8) uint64_t bars[kTWarps][2];
+    __shared__ unsigned long long cnt_sh[4];
+    const int m = blockIdx.y;
+    const int lp = m / W.n_steps, w = m % W.n_steps;
+    const PartDev& pd = W.parts[lp];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x < 4) cnt_sh[threadIdx.x] = 0;
+    if (lane == 0) {
+        mbar_init(&bars[warp][0], 1);
+        mbar_init(&bars[warp][1], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    const int64_t U = W.hop_size[(int64_t)m * (kMaxLayers + 1) + W.L];
+    const int pitch = W.pitch;
+    const uint32_t rowb = (uint32_t)pitch * 4u;
+    const int groups = R >> 2;
+    const int stage_bytes = groups * gstride;
+    const int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
+    int32_t* fgid = W.fr_gid + (int64_t)m * W.ucap;
+    float* X = W.X + (int64_t)m * W.ucap * pitch;
+    unsigned char* base = tsm + ((128u - (smem_u32(tsm) & 127u)) & 127u);   // tensor copies: 128-B aligned
+    unsigned char* stage[2] = {base + (size_t)warp * 2 * stage_bytes, base + (size_t)warp * 2 * stage_bytes + stage_bytes};
+    const unsigned long long wbit = 1ull << w;
+    const int n_lp = gm.n_lp;
+    const int64_t rank_lo = W.remote ? pd.lo : pd.h_below;
+    unsigned n_loc = 0, n_hit = 0, n_miss = 0, n_peer = 0;
+    const int64_t stride = (int64_t)gridDim.x * kTWarps * R;
+    uint32_t phase[2] = {0u, 0u};
+    const uint64_t pol_stream = policy_evict_first();
+    auto issue = [&](int64_t f0, int st) -> int {
+        const int64_t f = f0 + lane;
+        const bool valid = lane < R && f < U;
+        const float* src = nullptr;
+        int cls = 3, mid = -1;
+        int32_t row = 0;
+        if (valid) {
+            int32_t gid;
+            const int32_t r = fr[f];
+            cls = classify(W, G, pd, r, wbit, src, gid);
+            fgid[f] = gid;
+            if (cls == 0) {                                   // own table
+                mid = lp;
+                row = (int32_t)(r - rank_lo);
+            } else if (cls == 1) {                            // BUF slot
+                mid = n_lp + lp;
+                row = (int32_t)((src - pd.rows) / pitch);
+            } else if (cls == 2) {                            // miss, owner on this GPU
+                const int qo = owner_of(G.bounds, G.n_parts, gid);
+                const int l2 = G.lp_of[qo];
+                if (l2 >= 0) {
+                    mid = l2;
+                    row = (int32_t)(gid - G.bounds[qo]);
+                }
+            }
+        }
+        n_loc += __popc(__ballot_sync(kFull, cls == 0));
+        n_hit += __popc(__ballot_sync(kFull, cls == 1));
+        n_miss += __popc(__ballot_sync(kFull, cls >= 2 && cls != 3));
+        n_peer += __popc(__ballot_sync(kFull, cls == 4));
+        const int nrows = (int)(U - f0 < R ? U - f0 : R);
+        // a group is pure when its 4 lanes are valid and share one descriptor
+        const int g = lane >> 2, j = lane & 3;
+        const int mid0 = __shfl_sync(kFull, mid, lane & ~3);
+        const unsigned same = __ballot_sync(kFull, valid && mid >= 0 && mid == mid0);
+        const bool pure = ((same >> (lane & ~3)) & 0xFu) == 0xFu;
+        const int32_t r1 = __shfl_down_sync(kFull, row, 1), r2 = __shfl_down_sync(kFull, row, 2),
+                      r3 = __shfl_down_sync(kFull, row, 3);
+        bulk_wait_read0();                       // stores that last read this stage are done
+        __syncwarp();
+        if (lane == 0) mbar_expect_tx(&bars[warp][st], (uint32_t)nrows * rowb);
+        __syncwarp();
+        unsigned char* slot = stage[st] + (size_t)g * gstride;
+        if (valid) {
+            if (pure) {
+                if (j == 0) g4_load(slot, &gm.maps[mid][0], row, r1, r2, r3, &bars[warp][st]);
+            } else {
+                bulk_load(slot + (size_t)j * rowb, src, rowb, &bars[warp][st]);
+            }
+        }
+        return nrows;
+    };
+    int64_t f0 = ((int64_t)blockIdx.x * kTWarps + warp) * R;
+    int st = 0;
+    int nrows = f0 < U ? issue(f0, st) : 0;
+    while (f0 < U) {
+        const int64_t fn = f0 + stride;
+        int nn = 0;
+        if (fn < U) nn = issue(fn, st ^ 1);      // next chunk's loads overlap this chunk's wait
+        mbar_wait(&bars[warp][st], phase[st]);
+        phase[st] ^= 1u;
+        const int gi = lane;                     // lane g stores group g (up to 4 rows)
+        if (gi < groups && 4 * gi < nrows) {
+            const int rows_g = nrows - 4 * gi < 4 ? nrows - 4 * gi : 4;
+            float* dst = X + (f0 + 4 * gi) * pitch;
+            const unsigned char* sg = stage[st] + (size_t)gi * gstride;
+            if (hint & 2)
+                bulk_store_hint(dst, sg, (uint32_t)rows_g * rowb, pol_stream);
+            else
+                bulk_store(dst, sg, (uint32_t)rows_g * rowb);
+        }
+        bulk_commit();
+        f0 = fn;
+        nrows = nn;
+        st ^= 1;
+    }
+    bulk_wait0();
+    if (lane == 0) {
+        if (n_loc) atomicAdd(&cnt_sh[0], (unsigned long long)n_loc);
+        if (n_hit) atomicAdd(&cnt_sh[1], (unsigned long long)n_hit);
+        if (n_miss) atomicAdd(&cnt_sh[2], (unsigned long long)n_miss);
+        if (n_peer) atomicAdd(&cnt_sh[3], (unsigned long long)n_peer);
+    }
+    __syncthreads();
+    long long* cn = W.counts + (int64_t)m * 8;
+    if (threadIdx.x == 0) {
+        if (cnt_sh[0]) atomicAdd((unsigned long long*)&cn[1], cnt_sh[0]);
+        if (cnt_sh[1]) atomicAdd((unsigned long long*)&cn[2], cnt_sh[1]);
+        if (cnt_sh[2]) {
+            atomicAdd((unsigned long long*)&cn[3], cnt_sh[2]);
+            atomicAdd((unsigned long long*)&cn[6], cnt_sh[2]);
+        }
+        if (cnt_sh[3]) atomicAdd((unsigned long long*)&cn[7], cnt_sh[3]);
+        const unsigned long long rows = cnt_sh[0] + cnt_sh[1] + cnt_sh[2];
+        if (rows && W.gathered_rows) atomicAdd((unsigned long long*)W.gathered_rows, rows);
+        if (blockIdx.x == 0) cn[0] = U;
+    }
+}
+
+void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, const GatherMaps* g4, cudaStream_t s) {
     // exactly one wave of 4 resident 256-thread blocks per SM in total (64 registers per thread):
     // floor, so no second, nearly empty wave leaves SMs idle at the tail
     int64_t target = ((int64_t)num_sms() * 4) / w.n_inst;
@@ -405,7 +559,30 @@ void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, cud
     const int stage = stage_env ? stage_env : (small ? kTStageBytes / 2 : kTStageBytes);
     const int bps = bps_env ? bps_env : (small ? 6 : 3);
     const int R = (int)std::min<int64_t>(32, std::max<int64_t>(1, stage / ((int64_t)w.pitch * 4)));
-    if (use_tma && (int64_t)w.pitch * 4 <= stage) {
+    // row gather (gather4): 1 = always, 0 = never, 2 (default) = when the hosted tables fit in L2.
+    // Measured: arxiv (L2-resident) 0.228 -> 0.214 ms per pipelined window; products (from DRAM) gather
+    // alone 1.256 -> 1.297 ms and the pipelined window 2.22 -> 2.63 ms, so DRAM-bound gathers keep the
+    // per-row copies.
+    static const int use_g4 = [] {
+        const char* e = getenv("MGNN_GATHER_G4");
+        return e ? atoi(e) : 2;
+    }();
+    if (use_tma && (use_g4 == 1 || (use_g4 == 2 && l2_resident)) && g4 && w.feat_dim == w.pitch && w.pitch <= 256) {
+        // R rows per chunk (a multiple of 4), each group of 4 in a 128-byte-aligned slot
+        const int gstride = (int)(((int64_t)4 * w.pitch * 4 + 127) / 128 * 128);
+        const int groups = std::max(1, std::min(8, (stage + gstride / 2) / gstride));
+        const int Rg = 4 * groups;
+        const size_t smem = (size_t)kTWarps * 2 * groups * gstride + 128;
+        ensure_smem_k(k_gather_g4, (int)smem);
+        int64_t tgt = ((int64_t)num_sms() * bps) / w.n_inst;
+        int64_t nd = (w.ucap + kTWarps * Rg - 1) / (kTWarps * Rg);
+        unsigned gxt = (unsigned)std::max<int64_t>(1, std::min(nd, tgt));
+        static const int hint = [] {
+            const char* e = getenv("MGNN_GATHER_HINT");
+            return e ? atoi(e) & 7 : 6;
+        }();
+        launch_k(k_gather_g4, dim3(gxt, w.n_inst), dim3(kTWarps * 32), smem, s, w, world, *g4, Rg, gstride, hint);
+    } else if (use_tma && (int64_t)w.pitch * 4 <= stage) {
         const size_t smem = (size_t)kTWarps * 2 * stage;
         ensure_smem_k(k_gather_tma, (int)smem);
         int64_t tgt = ((int64_t)num_sms() * bps) / w.n_inst;

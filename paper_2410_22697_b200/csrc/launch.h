@@ -136,7 +136,16 @@ int64_t scan_tiles_count(int64_t fcap);   // tiles used by count_scan for fcap i
 int64_t scan_tiles_words(int64_t words);  // tiles used by compact for `words`
 
 // gather.cu
-void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, cudaStream_t s);
+// TMA row-gather descriptors of the sources on this GPU: maps[lp] = table of local partition lp,
+// maps[n_lp + lp] = its BUF rows (2-D fp32 [rows][D], box {D, 1}, for cp.async.bulk.tensor gather4).
+constexpr int kMaxGatherMaps = 16;
+struct alignas(64) GatherMaps {
+    unsigned char maps[kMaxGatherMaps][128];
+    int32_t n_lp;
+};
+void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, const GatherMaps* g4, cudaStream_t s);
+// sage.cu: 2-D fp32 row map for the gather4 path (box = one whole row of `cols` floats)
+bool encode_row_map(void* map_out, const float* base, int64_t rows, int64_t cols, int64_t pitch);
 
 // score.cu
 // ovf / t_last: the window is skipped when *ovf <= t_last (arena overflow, mgnn_sampler_config_bounded)

@@ -381,6 +381,20 @@ bool sage_encode_map(void* map_out, const float* base, int64_t rows, int64_t col
     return r == CUDA_SUCCESS;
 }
 
+// 2-D fp32 [rows][cols] table with row pitch `pitch` floats for the TMA row gather (gather4): the box is
+// one whole row (cols <= 256 floats, cols * 4 a multiple of 16), no swizzle -- four rows land packed.
+bool encode_row_map(void* map_out, const float* base, int64_t rows, int64_t cols, int64_t pitch) {
+    if (!load_encode() || cols < 4 || cols > 256 || (cols * 4) % 16 || rows < 1) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)pitch * 4};
+    cuuint32_t box[2] = {(cuuint32_t)cols, 1};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode((CUtensorMap*)map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // dynamic shared memory of one CTA: alignment slack, A (self + neigh panels), weight ring,
 // tile prefix, the tile's neighbour lists
 static size_t smem_fixed(int n_inst, int k_hop) {

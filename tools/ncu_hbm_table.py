@@ -4,7 +4,11 @@ measured HBM peak (MEASURED_PEAKS.json hbm_gbs).  Launch times under ncu are ser
 cold-cache (ncu flushes caches before every launch), so this is each kernel's own roofline
 position, not its share of a pipelined step.
 
-    python tools/ncu_hbm_table.py LAUNCHES.csv [PEAK_GBS]
+    python tools/ncu_hbm_table.py LAUNCHES.csv [PEAK_GBS] [--json OUT --config NAME]
+
+--json writes the per-config traffic table bench.py reads (profiles/r02/traffic_<config>.json):
+per kernel the DRAM bytes per launch (the roofline line's `traffic`), the duration and the fraction
+of the peak.  Capture it with `--cache-control none` so the bytes are the kernel's in-situ traffic.
 """
 import csv
 import json
@@ -13,7 +17,7 @@ import sys
 from collections import defaultdict
 
 
-def table(path, peak):
+def aggregate(path):
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r and "Metric Name" in r)
     h = rows[hi]
@@ -27,7 +31,7 @@ def table(path, peak):
             continue
         v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
         per[r[ii]][r[mi]] = v
-        names[r[ii]] = r[ki].split("(")[0].replace("mgnn::", "")
+        names[r[ii]] = r[ki].split("(")[0].replace("mgnn::", "").replace("void ", "").split("<")[0]
     agg = defaultdict(lambda: [0, 0.0, 0.0, 0.0, 0.0])
     for i, m in per.items():
         a = agg[names[i]]
@@ -36,6 +40,11 @@ def table(path, peak):
         a[2] += m.get("dram__bytes_read.sum", 0.0)
         a[3] += m.get("dram__bytes_write.sum", 0.0)
         a[4] += m.get("lts__t_bytes.sum", 0.0)
+    return agg
+
+
+def table(path, peak):
+    agg = aggregate(path)
     out = [f"{'kernel':24s} {'n':>3s} {'avg us':>9s} {'DRAM MB/launch':>15s} {'DRAM GB/s':>10s} {'% HBM peak':>10s} {'L2 GB/s':>9s}"]
     for k, (n, t, rd, wr, l2) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         gbs = (rd + wr) / t / 1e9 if t else 0.0
@@ -44,8 +53,34 @@ def table(path, peak):
     return "\n".join(out)
 
 
+def traffic_json(path, peak, config, out):
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    head = subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], cwd=root, capture_output=True,
+                          text=True).stdout.strip()
+    d = {"config": config, "source": os.path.relpath(path, root), "git_head": head,
+         "note": "ncu --cache-control none --clock-control none launch list: dram__bytes_read.sum + "
+                 "dram__bytes_write.sum per launch (serialised launches), averaged per kernel",
+         "peak_gbs": peak, "kernels": {}}
+    for k, (n, t, rd, wr, _) in aggregate(path).items():
+        d["kernels"][k] = {"launches": n, "us_per_launch": 1e6 * t / n, "dram_bytes_per_launch": (rd + wr) / n,
+                           "frac_of_peak": (rd + wr) / t / 1e9 / peak if t else None}
+        if k.startswith("k_gather_tma") or k.startswith("k_hop") or k in ("k_compact", "k_relabel"):
+            d[k] = (rd + wr) / n
+    with open(out, "w") as f:
+        json.dump(d, f, indent=1)
+
+
 if __name__ == "__main__":
-    peak = float(sys.argv[2]) if len(sys.argv) > 2 else json.load(
+    args = [a for a in sys.argv[1:]]
+    js = cfg = None
+    if "--json" in args:
+        js = args[args.index("--json") + 1]
+        cfg = args[args.index("--config") + 1]
+        args = [a for a in args if a not in ("--json", js, "--config", cfg)]
+    peak = float(args[1]) if len(args) > 1 else json.load(
         open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
     print(f"peak {peak} GB/s (MEASURED_PEAKS.json hbm_gbs)")
-    print(table(sys.argv[1], peak))
+    print(table(args[0], peak))
+    if js:
+        traffic_json(args[0], peak, cfg, js)
