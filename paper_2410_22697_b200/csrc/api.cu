@@ -999,16 +999,30 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
     launch_decay(ctx->d_parts, n_lp, cap_max, w.n_steps, ctx->pol.gamma, ctx->d_ovf, t_last, s);
     if (ctx->pol.delta > 0 && t_last % (uint64_t)ctx->pol.delta == 0) {
         CK(cudaMemsetAsync(ctx->ev_zero, 0, ctx->ev_zero_bytes, s));
-        launch_select(ctx->d_parts, n_lp, nmax, ctx->pol.alpha, ctx->pol.theta_r, ctx->d_evsegs, ctx->d_sel_n,
-                      ctx->ev_sc, ctx->ev_ev, s);
+        // the ordered lists are built only for the whole-list sort (MGNN_EVICT_SORT=2) or on request
+        // (MGNN_EV_SELECT=1); otherwise counts and histograms come straight from the scoreboards and the
+        // candidates are re-derived from them (unordered; their ranks / the sort order them)
+        static const bool ordered_select = [] {
+            const char* e = getenv("MGNN_EV_SELECT");
+            return e && e[0] == '1';
+        }();
+        const bool compact = ctx->sort_full_lists || ordered_select;
+        const PartDev* scan = compact ? nullptr : ctx->d_parts;
+        if (compact) {
+            launch_select(ctx->d_parts, n_lp, nmax, ctx->pol.alpha, ctx->pol.theta_r, ctx->d_evsegs, ctx->d_sel_n,
+                          ctx->ev_sc, ctx->ev_ev, s);
+        } else {
+            CK(cudaMemsetAsync(ctx->d_sel_n, 0, 2 * n_lp * sizeof(long long), s));
+            launch_ev_count(ctx->d_parts, n_lp, nmax, ctx->pol.alpha, ctx->pol.theta_r, ctx->d_sel_n, ctx->ev_ev, s);
+        }
         const SortSeg* pairs = ctx->d_evsegs;     // where the K winners of E and R end, in order
         const long long* k_of = nullptr;           // K per segment (null: min(|E|, |R|) of the lists)
-        if (cap_max <= kEvMax && !ctx->force_sort_path) {
-            launch_cand_rank(ctx->d_evsegs, n_lp, nmax, ctx->ev_ev, s);     // K winners in order, no sort
+        if (cap_max <= kEvMax && !ctx->force_sort_path) {                   // K winners in order, no sort
+            launch_cand_rank(ctx->d_evsegs, n_lp, nmax, ctx->ev_ev, scan, ctx->pol.alpha, ctx->pol.theta_r, s);
         } else if (ctx->sort_full_lists) {
             radix_sort_pairs(ctx->d_evsegs, 2 * n_lp, nmax, ctx->ev_passes, ctx->sort_scr, s);
         } else {                                   // threshold candidates, then sort only those
-            launch_cand(ctx->d_evsegs, n_lp, nmax, ctx->ev_ev, s);
+            launch_cand(ctx->d_evsegs, n_lp, nmax, ctx->ev_ev, scan, ctx->pol.alpha, ctx->pol.theta_r, s);
             radix_sort_pairs(ctx->d_candsegs, 2 * n_lp, nmax, 8, ctx->sort_scr, s);
             pairs = ctx->d_candsegs;
             k_of = ctx->ev_ev.thr;

@@ -153,9 +153,16 @@ void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, 
                   const unsigned long long* ovf, uint64_t t_last, cudaStream_t s);
 void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, float theta_r, const SortSeg* segs,
                    long long* n_out, Scratch sc, EvScratch ev, cudaStream_t s);
-// small-buffer path: candidates below the threshold digit, ranked by counting into sorted order
-void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, cudaStream_t s);
-void launch_cand(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, cudaStream_t s);   // candidates only
+// |E|, |R| and the top-digit histograms straight from the scoreboards (no ordered lists)
+void launch_ev_count(const PartDev* parts, int n_lp, int64_t n_max, float alpha, float theta_r, long long* n_out,
+                     EvScratch ev, cudaStream_t s);
+// small-buffer path: candidates below the threshold digit, ranked by counting into sorted order.
+// scan_parts != nullptr: candidates are re-derived from the scoreboards (after launch_ev_count);
+// nullptr: from the compacted lists of launch_select.
+void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, const PartDev* scan_parts,
+                      float alpha, float theta_r, cudaStream_t s);
+void launch_cand(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, const PartDev* scan_parts, float alpha,
+                 float theta_r, cudaStream_t s);   // candidates only
 void launch_swap_refill(const PartDev* parts, int n_lp, int64_t cap_max, const SortSeg* segs, const long long* k_of,
                         const WorldDev& world,
                         long long* counts, int64_t inst_stride_counts, int n_steps, const unsigned long long* ovf,

@@ -266,6 +266,8 @@ __global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int
 // words in rank order (= ascending id) appends new_i to the frontier (R#7) and writes, for EVERY
 // word, the pair (new_i bits, frontier position of the word's first new node) that k_relabel reads;
 // fbp catches up with fb for the next hop.
+// Persistent: a block claims the instance's word tiles in order until they run out (kernel start-up
+// -- PDL wait, constant loads -- was ~40 % of the stall samples with one short-lived block per tile).
 __global__ void __launch_bounds__(kThreads, 8) k_compact(WinDev W, int hop, Scratch sc, int64_t tiles_max) {
     pdl_enter();
     __shared__ long long sm[8];
@@ -275,75 +277,78 @@ __global__ void __launch_bounds__(kThreads, 8) k_compact(WinDev W, int hop, Scra
     const PartDev& pd = W.parts[m / W.n_steps];
     const int64_t nwords = ((W.remote ? W.n_global : pd.vp) + 31) >> 5;   // rank space
     const int64_t ntiles = (nwords + kWordTile - 1) / kWordTile;
-    const int tile = claim_tile(sc.tilectr + m, &tslot);
-    if (tile >= ntiles) return;
     uint32_t* nbp = W.nb + ((int64_t)m * W.L + hop) * W.bm_words * 2;   // word w: nbp[2w] bits, nbp[2w+1] position
     const uint32_t* fb = W.fb + (int64_t)m * W.bm_words;
     uint32_t* fbp = W.fbp + (int64_t)m * W.bm_words;
-    const int64_t wd0 = (int64_t)tile * kWordTile + (int64_t)threadIdx.x * kCWords;   // 4 consecutive words
-    uint32_t b[kCWords];
-    uint4 now = make_uint4(0u, 0u, 0u, 0u);
-    if (wd0 < nwords) {                  // bm_words % kCWords == 0: one 16-byte load of each bitmap
-        now = *reinterpret_cast<const uint4*>(fb + wd0);
-        const uint4 was = *reinterpret_cast<const uint4*>(fbp + wd0);
-        b[0] = now.x & ~was.x;
-        b[1] = now.y & ~was.y;
-        b[2] = now.z & ~was.z;
-        b[3] = now.w & ~was.w;
-    } else {
-#pragma unroll
-        for (int j = 0; j < kCWords; ++j) b[j] = 0u;
-    }
-    int cnt = 0;
-#pragma unroll
-    for (int j = 0; j < kCWords; ++j) cnt += __popc(b[j]);
-    long long agg;
-    const long long excl = block_excl_scan256(cnt, sm, &agg);
     int64_t* hs = W.hop_size + (int64_t)m * (kMaxLayers + 1);
-    if (threadIdx.x < 32) {
-        const unsigned long long pv = lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
-                                                         (unsigned long long)agg);
-        if (threadIdx.x == 0) prefix_sh = (long long)pv;
-    }
-    __syncthreads();
-    const int64_t nF = hs[hop];
-    int64_t pos = nF + prefix_sh + excl;
     int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
     // arena bound of F_{hop+1} (mgnn_sampler_config_bounded): positions past it are not stored, the
     // size is clamped and the window is marked overflowed (every buffer-state kernel then skips it)
     const int64_t cap = hop + 1 < W.L ? W.off_stride[hop + 1] - 1 : W.ucap;
-    if (wd0 < nwords) {
-        // new_i keeps its bitmap; with the word's first position it gives every new node's frontier
-        // position as wpre + popc(lower bits) (k_relabel), without a scattered rank -> position table
-        uint32_t p[kCWords];
-        int64_t q = pos;
+    for (;;) {
+        const int tile = claim_tile(sc.tilectr + m, &tslot);
+        if (tile >= ntiles) break;
+        const int64_t wd0 = (int64_t)tile * kWordTile + (int64_t)threadIdx.x * kCWords;   // 4 consecutive words
+        uint32_t b[kCWords];
+        uint4 now = make_uint4(0u, 0u, 0u, 0u);
+        if (wd0 < nwords) {              // bm_words % kCWords == 0: one 16-byte load of each bitmap
+            now = *reinterpret_cast<const uint4*>(fb + wd0);
+            const uint4 was = *reinterpret_cast<const uint4*>(fbp + wd0);
+            b[0] = now.x & ~was.x;
+            b[1] = now.y & ~was.y;
+            b[2] = now.z & ~was.z;
+            b[3] = now.w & ~was.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < kCWords; ++j) b[j] = 0u;
+        }
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < kCWords; ++j) cnt += __popc(b[j]);
+        long long agg;
+        const long long excl = block_excl_scan256(cnt, sm, &agg);
+        if (threadIdx.x < 32) {
+            const unsigned long long pv = lookback_exclusive(sc.status + (int64_t)m * tiles_max, tile,
+                                                             (unsigned long long)agg);
+            if (threadIdx.x == 0) prefix_sh = (long long)pv;
+        }
+        __syncthreads();
+        const int64_t nF = hs[hop];
+        int64_t pos = nF + prefix_sh + excl;
+        if (wd0 < nwords) {
+            // new_i keeps its bitmap; with the word's first position it gives every new node's frontier
+            // position as wpre + popc(lower bits) (k_relabel), without a scattered rank -> position table
+            uint32_t p[kCWords];
+            int64_t q = pos;
+#pragma unroll
+            for (int j = 0; j < kCWords; ++j) {
+                p[j] = (uint32_t)q;
+                q += __popc(b[j]);
+            }
+            uint4* v = reinterpret_cast<uint4*>(nbp + 2 * wd0);
+            v[0] = make_uint4(b[0], p[0], b[1], p[1]);
+            v[1] = make_uint4(b[2], p[2], b[3], p[3]);
+            if (cnt) *reinterpret_cast<uint4*>(fbp + wd0) = now;
+        }
 #pragma unroll
         for (int j = 0; j < kCWords; ++j) {
-            p[j] = (uint32_t)q;
-            q += __popc(b[j]);
+            const int64_t wd = wd0 + j;
+            uint32_t bb = b[j];
+            while (bb) {
+                const int bi = __ffs(bb) - 1;
+                bb &= bb - 1;
+                const int32_t r = (int32_t)(wd * 32 + bi);
+                MGNN_CHECK(r < (W.remote ? W.n_global : pd.vp), "compact r=%d", r);
+                if (pos < cap) fr[pos] = r;
+                ++pos;
+            }
         }
-        uint4* v = reinterpret_cast<uint4*>(nbp + 2 * wd0);
-        v[0] = make_uint4(b[0], p[0], b[1], p[1]);
-        v[1] = make_uint4(b[2], p[2], b[3], p[3]);
-        if (cnt) *reinterpret_cast<uint4*>(fbp + wd0) = now;
-    }
-#pragma unroll
-    for (int j = 0; j < kCWords; ++j) {
-        const int64_t wd = wd0 + j;
-        uint32_t bb = b[j];
-        while (bb) {
-            const int bi = __ffs(bb) - 1;
-            bb &= bb - 1;
-            const int32_t r = (int32_t)(wd * 32 + bi);
-            MGNN_CHECK(r < (W.remote ? W.n_global : pd.vp), "compact r=%d", r);
-            if (pos < cap) fr[pos] = r;
-            ++pos;
+        if (tile == ntiles - 1 && threadIdx.x == 0) {
+            const int64_t total = nF + prefix_sh + agg;
+            hs[hop + 1] = total < cap ? total : cap;
+            if (total > cap) atomicMin(W.ovf, (unsigned long long)W.step0);
         }
-    }
-    if (tile == ntiles - 1 && threadIdx.x == 0) {
-        const int64_t total = nF + prefix_sh + agg;
-        hs[hop + 1] = total < cap ? total : cap;
-        if (total > cap) atomicMin(W.ovf, (unsigned long long)W.step0);
+        __syncthreads();                 // prefix_sh / sm are reused by the next tile
     }
 }
 
@@ -442,7 +447,15 @@ void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t
 
 void launch_compact(const WinDev& w, int hop, Scratch sc, cudaStream_t s) {
     const int64_t tiles = scan_tiles_words(w.bm_words);
-    dim3 grid((unsigned)(tiles < 1 ? 1 : tiles), w.n_inst);
+    // persistent blocks: ~8 resident per SM over all instances, each looping over claimed tiles
+    static const int per_sm = [] {
+        const char* e = getenv("MGNN_COMPACT_BPS");
+        const int v = e ? atoi(e) : 8;
+        return v >= 1 && v <= 64 ? v : 8;
+    }();
+    int64_t gx = ((int64_t)num_sms() * per_sm + w.n_inst - 1) / w.n_inst;
+    if (gx > tiles) gx = tiles;
+    dim3 grid((unsigned)(gx < 1 ? 1 : gx), w.n_inst);
     launch_k(k_compact, grid, dim3(kThreads), 0, s, w, hop, sc, (int64_t)(tiles < 1 ? 1 : tiles));
     count_launches(1, __func__, s);
 }

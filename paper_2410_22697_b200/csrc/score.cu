@@ -142,6 +142,71 @@ void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, f
     count_launches(1, __func__, s);
 }
 
+// ------------------------------------------------------------------ unordered scan (default paths)
+// The K winners of each list are found from histograms and a threshold, then ranked or sorted, so
+// the lists themselves never need to exist in order: k_ev_count computes |E|, |R| and the top-12-bit
+// histograms straight from the scoreboards (E over the slots: S_E coalesced, the node id loaded only
+// for keys that count; R over the halo), and k_ev_hist2 / k_ev_cand re-derive the same unique keys.
+// Saves k_select's order-preserving compaction (look-back chain + the lists' writes).
+__device__ __forceinline__ bool ev_key(const PartDev& pd, bool isE, int64_t x, float alpha, float theta_r,
+                                       unsigned long long& key, uint32_t& val) {
+    if (isE) {                                   // x = slot
+        const float se = pd.se[x];
+        if (!(se < alpha)) return false;
+        const int32_t h = pd.slot_h[x];
+        key = ((unsigned long long)__float_as_uint(se) << 32) | (uint32_t)pd.halo_ids[h];
+        val = (uint32_t)x;
+        return true;
+    }
+    if (pd.slot_of[x] >= 0) return false;        // x = halo index
+    const float sa = pd.sa[x];
+    if (!(sa >= theta_r)) return false;
+    key = ((unsigned long long)(~__float_as_uint(sa)) << 32) | (uint32_t)pd.rank_deg[x];
+    val = (uint32_t)x;
+    return true;
+}
+
+__global__ void __launch_bounds__(kSThreads) k_ev_count(const PartDev* __restrict__ parts, float alpha, float theta_r,
+                                                        long long* __restrict__ n_out, EvScratch ev) {
+    pdl_enter();
+    __shared__ unsigned long long cnt_sh;
+    const int sg = blockIdx.y;
+    const PartDev& pd = parts[sg >> 1];
+    const bool isE = (sg & 1) == 0;
+    const int64_t n = isE ? pd.cap : pd.n_h;
+    if (threadIdx.x == 0) cnt_sh = 0;
+    __syncthreads();
+    uint32_t* hist = ev.hist + (size_t)sg * kDig;
+    const int lane = threadIdx.x & 31;
+    unsigned mine = 0;
+    for (int64_t x0 = (int64_t)blockIdx.x * kSThreads; x0 < n; x0 += (int64_t)gridDim.x * kSThreads) {
+        const int64_t x = x0 + threadIdx.x;
+        unsigned d = 0xFFFFFFFFu;
+        if (x < n) {
+            bool c;
+            unsigned long long key = 0;
+            if (isE) {                           // the digit needs only S_E (no id load)
+                const float se = pd.se[x];
+                c = se < alpha;
+                key = (unsigned long long)__float_as_uint(se) << 32;
+            } else {
+                uint32_t v;
+                c = ev_key(pd, false, x, alpha, theta_r, key, v);
+            }
+            if (c) {
+                d = (unsigned)(key >> 52);
+                ++mine;
+            }
+        }
+        const unsigned peers = __match_any_sync(kFull, d);
+        if (d != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[d], (unsigned)__popc(peers));
+    }
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(kFull, mine, o);
+    if (lane == 0 && mine) atomicAdd(&cnt_sh, (unsigned long long)mine);
+    __syncthreads();
+    if (threadIdx.x == 0 && cnt_sh) atomicAdd((unsigned long long*)&n_out[sg], cnt_sh);
+}
+
 // ------------------------------------------------------------------ candidates
 // Smallest digit T with #(digit <= T) >= need (T = -1 if need <= 0); *below = #(digit < T).
 // Block-wide (256 threads, 16 digits each); every block of the launch derives the same answer.
@@ -175,13 +240,16 @@ constexpr long long kCandMax = 4096;   // refine the threshold with the next 12 
 
 // Second-level histogram (key bits [40, 52)) of the threshold bucket, only when the first level
 // would leave more than kCandMax candidates (e.g. many equal scores in an early round).
-__global__ void __launch_bounds__(kSThreads) k_hist2(const SortSeg* __restrict__ segs, EvScratch ev) {
+__global__ void __launch_bounds__(kSThreads) k_hist2(const SortSeg* __restrict__ segs, EvScratch ev,
+                                                     const PartDev* __restrict__ parts, float alpha, float theta_r) {
     pdl_enter();
     __shared__ long long sm[8];
     __shared__ long long T_sh, below_sh;
     const int sg = blockIdx.y;
     const SortSeg S = segs[sg];
-    const long long n = *S.n;
+    // parts != nullptr: the lists were never compacted; scan the scoreboards (E: slots, R: halo)
+    const PartDev* pd = parts ? parts + (sg >> 1) : nullptr;
+    const long long n = pd ? ((sg & 1) ? pd->n_h : pd->cap) : *S.n;
     const long long nE = *segs[sg & ~1].n, nR = *segs[sg | 1].n;
     const long long K = nE < nR ? nE : nR;
     const uint32_t* hist = ev.hist + (size_t)sg * kDig;
@@ -195,8 +263,10 @@ __global__ void __launch_bounds__(kSThreads) k_hist2(const SortSeg* __restrict__
         const long long i = i0 + lane;
         unsigned d = 0xFFFFFFFFu;
         if (i < n) {
-            const unsigned long long k = S.keys[i];
-            if ((long long)(k >> 52) == T) d = (unsigned)(k >> 40) & 0xFFFu;
+            unsigned long long k = 0;
+            uint32_t v;
+            const bool c = pd ? ev_key(*pd, (sg & 1) == 0, i, alpha, theta_r, k, v) : (k = S.keys[i], true);
+            if (c && (long long)(k >> 52) == T) d = (unsigned)(k >> 40) & 0xFFFu;
         }
         const unsigned peers = __match_any_sync(kFull, d);
         if (d != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist2[d], (unsigned)__popc(peers));
@@ -205,13 +275,15 @@ __global__ void __launch_bounds__(kSThreads) k_hist2(const SortSeg* __restrict__
 
 // Every block derives K = min(|E|, |R|) of its partition and the threshold(s) of its list from the
 // histograms; block 0 records {K, T} for k_rank.
-__global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ segs, EvScratch ev) {
+__global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ segs, EvScratch ev,
+                                                    const PartDev* __restrict__ parts, float alpha, float theta_r) {
     pdl_enter();
     __shared__ long long sm[8];
     __shared__ long long T_sh, below_sh, T2_sh, below2_sh;
     const int sg = blockIdx.y;
     const SortSeg S = segs[sg];
-    const long long n = *S.n;
+    const PartDev* pd = parts ? parts + (sg >> 1) : nullptr;      // see k_hist2
+    const long long n = pd ? ((sg & 1) ? pd->n_h : pd->cap) : *S.n;
     const long long nE = *segs[sg & ~1].n, nR = *segs[sg | 1].n;
     const long long K = nE < nR ? nE : nR;
     const uint32_t* hist = ev.hist + (size_t)sg * kDig;
@@ -233,11 +305,12 @@ __global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ 
     for (long long i0 = (long long)blockIdx.x * kSThreads + (threadIdx.x & ~31); i0 < n; i0 += stride) {
         const long long i = i0 + lane;
         unsigned long long k = 0;
+        uint32_t v = 0;
         bool c = false;
         if (i < n) {
-            k = S.keys[i];
+            const bool in = pd ? ev_key(*pd, (sg & 1) == 0, i, alpha, theta_r, k, v) : (k = S.keys[i], v = S.vals[i], true);
             const long long d1 = (long long)(k >> 52);
-            c = d1 < T || (d1 == T && (long long)((k >> 40) & 0xFFF) <= T2);
+            c = in && (d1 < T || (d1 == T && (long long)((k >> 40) & 0xFFF) <= T2));
         }
         const unsigned ball = __ballot_sync(kFull, c);
         if (!ball) continue;
@@ -249,7 +322,7 @@ __global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ 
         if (c) {
             const unsigned long long p = base + __popc(ball & ((1u << lane) - 1u));
             S.keys_tmp[p] = k;
-            S.vals_tmp[p] = S.vals[i];
+            S.vals_tmp[p] = v;
         }
     }
 }
@@ -285,17 +358,28 @@ __global__ void __launch_bounds__(kSThreads) k_rank(const SortSeg* __restrict__ 
     }
 }
 
-void launch_cand(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, cudaStream_t s) {
-    dim3 g1(blocks_for(n_max, kSThreads) > 64 ? 64 : blocks_for(n_max, kSThreads), 2 * n_lp);
-    launch_k(k_hist2, g1, dim3(kSThreads), 0, s, segs, ev);
-    launch_k(k_cand, g1, dim3(kSThreads), 0, s, segs, ev);
+void launch_ev_count(const PartDev* parts, int n_lp, int64_t n_max, float alpha, float theta_r, long long* n_out,
+                     EvScratch ev, cudaStream_t s) {
+    dim3 grid(blocks_for(n_max, kSThreads), 2 * n_lp);
+    launch_k(k_ev_count, grid, dim3(kSThreads), 0, s, parts, alpha, theta_r, n_out, ev);
+    count_launches(1, __func__, s);
+}
+
+void launch_cand(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, const PartDev* scan_parts, float alpha,
+                 float theta_r, cudaStream_t s) {
+    const unsigned cap_blocks = scan_parts ? 256u : 64u;     // the scoreboard scan covers all of n_h
+    dim3 g1(blocks_for(n_max, kSThreads) > cap_blocks ? cap_blocks : blocks_for(n_max, kSThreads), 2 * n_lp);
+    launch_k(k_hist2, g1, dim3(kSThreads), 0, s, segs, ev, scan_parts, alpha, theta_r);
+    launch_k(k_cand, g1, dim3(kSThreads), 0, s, segs, ev, scan_parts, alpha, theta_r);
     count_launches(2, __func__, s);
 }
 
-void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, cudaStream_t s) {
-    dim3 g1(blocks_for(n_max, kSThreads) > 64 ? 64 : blocks_for(n_max, kSThreads), 2 * n_lp);
-    launch_k(k_hist2, g1, dim3(kSThreads), 0, s, segs, ev);
-    launch_k(k_cand, g1, dim3(kSThreads), 0, s, segs, ev);
+void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, const PartDev* scan_parts,
+                      float alpha, float theta_r, cudaStream_t s) {
+    const unsigned cap_blocks = scan_parts ? 256u : 64u;
+    dim3 g1(blocks_for(n_max, kSThreads) > cap_blocks ? cap_blocks : blocks_for(n_max, kSThreads), 2 * n_lp);
+    launch_k(k_hist2, g1, dim3(kSThreads), 0, s, segs, ev, scan_parts, alpha, theta_r);
+    launch_k(k_cand, g1, dim3(kSThreads), 0, s, segs, ev, scan_parts, alpha, theta_r);
     dim3 g2((unsigned)((n_max + kSThreads - 1) / kSThreads), 2 * n_lp);
     launch_k(k_rank, g2, dim3(kSThreads), 0, s, segs, ev);
     count_launches(3, __func__, s);
