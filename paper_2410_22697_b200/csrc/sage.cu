@@ -389,9 +389,18 @@ bool encode_row_map(void* map_out, const float* base, int64_t rows, int64_t cols
     cuuint64_t strides[1] = {(cuuint64_t)pitch * 4};
     cuuint32_t box[2] = {(cuuint32_t)cols, 1};
     cuuint32_t estr[2] = {1, 1};
+    // L2 fill promotion of the row reads: rows are random, so promotion beyond a sector only over-fetches
+    // (MGNN_G4_PROMO = 0 | 64 | 128 | 256 bytes; default none)
+    static const CUtensorMapL2promotion promo = [] {
+        const char* e = getenv("MGNN_G4_PROMO");
+        const int v = e ? atoi(e) : 0;
+        return v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                        : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                   : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    }();
     CUresult r = g_encode((CUtensorMap*)map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box,
-                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
