@@ -28,3 +28,31 @@ def test_gpu_arm_rejects_short_warmup():
     r = subprocess.run([sys.executable, "bench.py", "--warmup", "2"], cwd=ROOT, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode != 0 and "warmup" in r.stderr
+
+
+def test_layouts_and_policy_lookup():
+    """bench.Setup: configs 1-4 default to 2 trainers per GPU (P = 2N), papers keeps P = 8 at every N
+    (8/N per GPU), --parts / --parts-per-gpu override, and the policy is the paper's GPU optimum for
+    the P actually used, windows never straddle an eviction step."""
+    import importlib
+    sys.path.insert(0, ROOT)
+    bench = importlib.import_module("bench")
+    s = bench.Setup("products", 1)
+    assert (s.P, s.ppg, s.f_bp, s.gamma, s.delta, s.window) == (2, 2, 5000, 0.995, 32, 32)
+    s = bench.Setup("products", 4)
+    assert (s.P, s.ppg, s.gamma, s.delta, s.window) == (8, 2, 0.9995, 16, 16)
+    s = bench.Setup("products", 2, parts_per_gpu=1)
+    assert (s.P, s.ppg, s.delta) == (2, 1, 32)
+    for world, ppg in ((1, 8), (2, 4), (4, 2), (8, 1)):
+        s = bench.Setup("papers", world)
+        assert (s.P, s.ppg, s.delta, s.window) == (8, ppg, 512, 16)
+    s = bench.Setup("arxiv", 4, parts=8)
+    assert (s.P, s.ppg, s.f_bp, s.delta, s.window) == (8, 2, 3500, 128, 32)
+    s = bench.Setup("cfg1", 1)
+    assert s.window == 32 and s.delta == 64
+    try:
+        bench.Setup("papers", 3)
+        raise AssertionError("8 partitions cannot be split over 3 GPUs")
+    except SystemExit:
+        pass
+    assert bench.static_ucap(bench.Setup("products", 1)) == 2000 * 6 * 11 * 16
