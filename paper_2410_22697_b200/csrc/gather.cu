@@ -274,10 +274,51 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
         }
         n_loc = n_hit = n_miss = n_peer = 0;
     };
-    // claim the next chunk: instance m (advanced past exhausted instances), first row f0; false = done
+    // claim the next chunk: instance m (advanced past exhausted instances), first row f0, its rows nr;
+    // false = done
     int m = blockIdx.y, visited = 0;
-    int64_t next_static = (int64_t)blockIdx.x * kTWarps + warp;      // dyn == 0: fixed chunk stride
+    int64_t next_static = (int64_t)blockIdx.x * kTWarps + warp;      // dyn == 0 / 2: fixed chunk stride
+    // dyn == 2 (segment-aligned chunks): F_L = F_0 ++ new_0 ++ ... ++ new_{L-1}, every segment sorted by
+    // rank (R#7).  Chunk c of segment s covers the same FRACTION c / C_s of that segment in every instance
+    // of the window (C_s = ceil(longest segment s / R)), so the instances, which the warps walk in lock
+    // step, read the same rank region of the tables at the same time (L2 reuse across minibatches).
+    __shared__ long long seg_c[kMaxLayers + 2];     // chunk prefix over segments (max over instances)
+    if (dyn == 2) {
+        if (threadIdx.x < kMaxLayers + 2) seg_c[threadIdx.x] = 0;
+        __syncthreads();
+        for (int mi = threadIdx.x; mi < W.n_inst; mi += blockDim.x) {
+            const int64_t* hsi = W.hop_size + (int64_t)mi * (kMaxLayers + 1);
+            for (int sgi = 0; sgi <= W.L; ++sgi) {
+                const long long len = sgi == 0 ? hsi[0] : hsi[sgi] - hsi[sgi - 1];
+                atomicMax(&seg_c[sgi + 1], (len + R - 1) / R);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int sgi = 1; sgi <= W.L + 1; ++sgi) seg_c[sgi] += seg_c[sgi - 1];
+        __syncthreads();
+    }
+    int chunk_rows = R;
     auto claim = [&](int& cm, int64_t& f0) -> bool {
+        if (dyn == 2) {
+            const int64_t* hsm = W.hop_size + (int64_t)m * (kMaxLayers + 1);
+            for (;;) {
+                const int64_t j = next_static;
+                next_static += (int64_t)gridDim.x * kTWarps;
+                if (j >= seg_c[W.L + 1]) return false;
+                int sgi = 0;
+                while (j >= seg_c[sgi + 1]) ++sgi;
+                const int64_t c = j - seg_c[sgi], C = seg_c[sgi + 1] - seg_c[sgi];
+                const int64_t s0 = sgi == 0 ? 0 : hsm[sgi - 1], len = sgi == 0 ? hsm[0] : hsm[sgi] - hsm[sgi - 1];
+                const int64_t a = s0 + c * len / C, b = s0 + (c + 1) * len / C;
+                if (j == 0 && lane == 0) W.counts[(int64_t)m * 8] = hsm[W.L];
+                if (b <= a) continue;
+                cm = m;
+                f0 = a;
+                chunk_rows = (int)(b - a);
+                return true;
+            }
+        }
         if (!dyn) {
             const int64_t U = W.hop_size[(int64_t)m * (kMaxLayers + 1) + W.L];
             const int64_t c = next_static;
@@ -312,7 +353,8 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
         }
         const int lp = cm / W.n_steps, w = cm % W.n_steps;
         const PartDev& pd = W.parts[lp];
-        const int64_t U = W.hop_size[(int64_t)cm * (kMaxLayers + 1) + W.L];
+        const int64_t U0 = W.hop_size[(int64_t)cm * (kMaxLayers + 1) + W.L];
+        const int64_t U = dyn == 2 ? f0 + chunk_rows : U0;   // aligned chunks end inside F_L
         const int64_t f = f0 + lane;
         const bool valid = lane < R && f < U;
         const float* src = nullptr;

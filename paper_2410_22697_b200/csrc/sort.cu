@@ -16,6 +16,9 @@
 // ascending-id order, which realises the "id asc" tie-break.
 // Segments (independent arrays with device-side lengths) run side by side
 // along gridDim.y.
+#include <algorithm>
+#include <cstdlib>
+
 #include "launch.h"
 
 namespace mgnn {
@@ -40,7 +43,7 @@ static inline int64_t sort_tiles(int64_t n_max) {
 // Every kernel loops over the tiles the device-side length needs (grids of at most a few blocks per
 // SM), so a sort sized for n_max that holds a few thousand keys costs a few microseconds a launch.
 static size_t head_bytes(int n_seg, int passes) {
-    size_t b = (size_t)n_seg * passes * kRadix * 4 + (size_t)n_seg * (passes + 1) * 4;
+    size_t b = (size_t)n_seg * passes * kRadix * 4 + (size_t)n_seg * (passes + 1) * 4 + 4;   // + barrier word
     return (b + 255) / 256 * 256;
 }
 
@@ -244,6 +247,207 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_fix(const SortSeg* __rest
     }
 }
 
+// ---- the whole sort in ONE cooperative launch (default): the same phases separated by grid-wide
+// barriers instead of kernel boundaries.  An eviction round sorts a few thousand to a few ten thousand
+// candidates, where the 3 + 2 * passes dependent launches cost more than their work (products: ~150 us
+// for ~70k keys); here every block takes (segment, tile) pairs in a fixed stride.
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& gen) {
+    // sense-reversal-free barrier on a monotone counter: block b waits until ctr >= (gen + 1) * nblocks
+    __syncthreads();
+    const unsigned nb = gridDim.x * gridDim.y;
+    ++gen;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1u);
+        while (true) {
+            unsigned v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+            if (v >= gen * nb) break;
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_coop(const SortSeg* __restrict__ segs, int n_seg, int passes,
+                                                            int64_t tiles_max, SortScr scr, unsigned* bar) {
+    pdl_enter();
+    __shared__ uint32_t run[kRadix];
+    __shared__ uint32_t wc[8][kRadix];
+    __shared__ uint32_t gofs[kRadix];
+    __shared__ uint32_t h8[8][kRadix];
+    __shared__ long long sm[8];
+    __shared__ int trivial_sh;
+    unsigned gen = 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t nblk = gridDim.x;
+    const int64_t work = (int64_t)n_seg * tiles_max;      // (segment, tile) pairs, segment-major
+    // ---- histogram of every digit position
+    for (int p = 0; p < passes; ++p) h8[p][threadIdx.x] = 0;
+    int cur_seg = -1;
+    auto flush_hist = [&]() {
+        __syncthreads();
+        if (cur_seg >= 0) {
+            uint32_t* bins = scr.bins + (size_t)cur_seg * passes * kRadix;
+            for (int p = 0; p < passes; ++p) {
+                if (h8[p][threadIdx.x]) atomicAdd(&bins[p * kRadix + threadIdx.x], h8[p][threadIdx.x]);
+                h8[p][threadIdx.x] = 0;
+            }
+        }
+        __syncthreads();
+    };
+    for (int64_t wi = blockIdx.x; wi < work; wi += nblk) {
+        const int sgi = (int)(wi / tiles_max);
+        const int64_t t = wi - (int64_t)sgi * tiles_max;
+        const SortSeg sg = segs[sgi];
+        const int64_t n = *sg.n;
+        if (t * kSortTile >= n) continue;
+        if (sgi != cur_seg) {
+            flush_hist();
+            cur_seg = sgi;
+        }
+#pragma unroll
+        for (int i = 0; i < kSortItems; ++i) {
+            const int64_t idx = t * kSortTile + (int64_t)i * kSortThreads + threadIdx.x;
+            if (idx < n) {
+                const unsigned long long k = sg.keys[idx];
+                for (int p = 0; p < sg.npass; ++p) atomicAdd(&h8[p][(unsigned)(k >> sg.shift[p]) & 0xFF], 1u);
+            }
+        }
+    }
+    flush_hist();
+    grid_barrier(bar, gen);
+    // ---- bin offsets and the pass plan (block sgi < n_seg)
+    for (int sgi = blockIdx.x; sgi < n_seg; sgi += nblk) {
+        const SortSeg sg = segs[sgi];
+        const long long n = *sg.n;
+        uint32_t* bins = scr.bins + (size_t)sgi * passes * kRadix;
+        int32_t* plan = scr.plan + (size_t)sgi * (passes + 1);
+        int parity = 0;
+        for (int p = 0; p < passes; ++p) {
+            if (threadIdx.x == 0) trivial_sh = 0;
+            __syncthreads();
+            const uint32_t c = bins[p * kRadix + threadIdx.x];
+            if ((long long)c == n) trivial_sh = 1;
+            long long tot;
+            const long long ex = block_excl_scan256(c, sm, &tot);
+            bins[p * kRadix + threadIdx.x] = (uint32_t)ex;
+            const bool skip = p >= sg.npass || n == 0 || trivial_sh;
+            if (threadIdx.x == 0) plan[p] = skip ? -1 : parity;
+            if (!skip) parity ^= 1;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) plan[passes] = parity;
+        __syncthreads();
+    }
+    grid_barrier(bar, gen);
+    // ---- passes: per-tile counts | barrier | prefix over earlier tiles, stable ranks, scatter | barrier
+    for (int p = 0; p < passes; ++p) {
+        for (int64_t wi = blockIdx.x; wi < work; wi += nblk) {
+            const int sgi = (int)(wi / tiles_max);
+            const int64_t t = wi - (int64_t)sgi * tiles_max;
+            const SortSeg sg = segs[sgi];
+            const int parity = scr.plan[(size_t)sgi * (passes + 1) + p];
+            const int64_t n = *sg.n;
+            if (parity < 0 || t * kSortTile >= n) continue;
+            const unsigned long long* kin = parity ? sg.keys_tmp : sg.keys;
+            const int shift = sg.shift[p];
+            run[threadIdx.x] = 0;
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < kSortItems; ++i) {
+                const int64_t idx = t * kSortTile + (int64_t)i * kSortThreads + threadIdx.x;
+                const unsigned digit = idx < n ? ((unsigned)(kin[idx] >> shift) & 0xFF) : (0x100u | lane);
+                const unsigned peers = __match_any_sync(kFull, digit);
+                if (digit < 0x100u && lane == __ffs(peers) - 1) atomicAdd(&run[digit], (unsigned)__popc(peers));
+            }
+            __syncthreads();
+            scr.status[((size_t)(sgi * passes + p) * tiles_max + t) * kRadix + threadIdx.x] = run[threadIdx.x];
+            __syncthreads();
+        }
+        grid_barrier(bar, gen);
+        for (int64_t wi = blockIdx.x; wi < work; wi += nblk) {
+            const int sgi = (int)(wi / tiles_max);
+            const int64_t tile = wi - (int64_t)sgi * tiles_max;
+            const SortSeg sg = segs[sgi];
+            const int parity = scr.plan[(size_t)sgi * (passes + 1) + p];
+            const int64_t n = *sg.n;
+            if (parity < 0 || tile * kSortTile >= n) continue;
+            const unsigned long long* kin = parity ? sg.keys_tmp : sg.keys;
+            const uint32_t* vin = parity ? sg.vals_tmp : sg.vals;
+            unsigned long long* kout = parity ? sg.keys : sg.keys_tmp;
+            uint32_t* vout = parity ? sg.vals : sg.vals_tmp;
+            const int shift = sg.shift[p];
+            const uint32_t* tc = scr.status + ((size_t)(sgi * passes + p) * tiles_max) * kRadix;
+            {
+                const int d = threadIdx.x;
+                uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+                int64_t j = 0;
+                for (; j + 4 <= tile; j += 4) {
+                    a0 += tc[(size_t)j * kRadix + d];
+                    a1 += tc[(size_t)(j + 1) * kRadix + d];
+                    a2 += tc[(size_t)(j + 2) * kRadix + d];
+                    a3 += tc[(size_t)(j + 3) * kRadix + d];
+                }
+                for (; j < tile; ++j) a0 += tc[(size_t)j * kRadix + d];
+                gofs[d] = scr.bins[(size_t)(sgi * passes + p) * kRadix + d] + a0 + a1 + a2 + a3;
+                run[d] = 0;
+                for (int w = 0; w < 8; ++w) wc[w][d] = 0;
+            }
+            __syncthreads();
+            unsigned long long key[kSortItems];
+            uint32_t val[kSortItems], rank[kSortItems];
+#pragma unroll
+            for (int i = 0; i < kSortItems; ++i) {
+                const int64_t idx = tile * kSortTile + (int64_t)i * kSortThreads + threadIdx.x;
+                const bool valid = idx < n;
+                key[i] = valid ? kin[idx] : 0ull;
+                val[i] = valid ? vin[idx] : 0u;
+                const unsigned digit = valid ? ((unsigned)(key[i] >> shift) & 0xFF) : (0x100u | lane);
+                const unsigned peers = __match_any_sync(kFull, digit);
+                const unsigned r = __popc(peers & lt);
+                if (valid && r == 0) wc[warp][digit] = __popc(peers);
+                __syncthreads();
+                {
+                    uint32_t acc = run[threadIdx.x];
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) {
+                        const uint32_t c = wc[w][threadIdx.x];
+                        wc[w][threadIdx.x] = acc;
+                        acc += c;
+                    }
+                    run[threadIdx.x] = acc;
+                }
+                __syncthreads();
+                rank[i] = valid ? wc[warp][digit] + r : 0xFFFFFFFFu;
+                __syncthreads();
+                for (int w = 0; w < 8; ++w) wc[w][threadIdx.x] = 0;
+                __syncthreads();
+            }
+#pragma unroll
+            for (int i = 0; i < kSortItems; ++i) {
+                if (rank[i] == 0xFFFFFFFFu) continue;
+                const unsigned digit = (unsigned)(key[i] >> shift) & 0xFF;
+                const uint32_t pos = gofs[digit] + rank[i];
+                kout[pos] = key[i];
+                vout[pos] = val[i];
+            }
+            __syncthreads();
+        }
+        grid_barrier(bar, gen);
+    }
+    // ---- fix-up: an odd number of executed passes left the result in the tmp buffers
+    for (int sgi = 0; sgi < n_seg; ++sgi) {
+        if (scr.plan[(size_t)sgi * (passes + 1) + passes] == 0) continue;
+        const SortSeg sg = segs[sgi];
+        const int64_t n = *sg.n;
+        for (int64_t i = (int64_t)blockIdx.x * kSortThreads + threadIdx.x; i < n; i += nblk * kSortThreads) {
+            sg.keys[i] = sg.keys_tmp[i];
+            sg.vals[i] = sg.vals_tmp[i];
+        }
+    }
+}
+
 void radix_sort_pairs(const SortSeg* segs_dev, int n_seg, int64_t n_max, int max_passes, void* scratch,
                       cudaStream_t s) {
     if (n_seg < 1) return;
@@ -255,6 +459,30 @@ void radix_sort_pairs(const SortSeg* segs_dev, int n_seg, int64_t n_max, int max
     int64_t gx = ((int64_t)num_sms() * 4 + n_seg - 1) / n_seg;
     if (gx > tiles) gx = tiles;
     dim3 grid((unsigned)(gx < 1 ? 1 : gx), (unsigned)n_seg);
+    static const int coop = [] {
+        const char* e = getenv("MGNN_SORT_COOP");
+        return e ? atoi(e) : 1;
+    }();
+    if (coop) {                               // one cooperative launch, 1 block per SM at most
+        int64_t nb = std::min<int64_t>((int64_t)num_sms(), (int64_t)n_seg * tiles);
+        if (nb < 1) nb = 1;
+        unsigned* bar = reinterpret_cast<unsigned*>(scr.plan + (size_t)n_seg * (passes + 1));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)nb);
+        cfg.blockDim = dim3(kSortThreads);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, k_sort_coop, segs_dev, n_seg, passes, tiles, scr, bar) == cudaSuccess) {
+            count_launches(1, __func__, s);
+            return;
+        }
+        cudaGetLastError();                   // fall back to the multi-launch sort below
+    }
     launch_k(k_sort_hist, grid, dim3(kSortThreads), 0, s, segs_dev, passes, tiles, scr);
     launch_k(k_sort_binscan, dim3(1, n_seg), dim3(kSortThreads), 0, s, segs_dev, passes, scr);
     for (int p = 0; p < passes; ++p) {
