@@ -196,11 +196,15 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const SortSeg* __
         unsigned long long key[kSortItems];
         uint32_t val[kSortItems], rank[kSortItems];
 #pragma unroll
+        for (int i = 0; i < kSortItems; ++i) {         // every load of the tile in flight at once
+            const int64_t idx = base + (int64_t)i * kSortThreads + threadIdx.x;
+            key[i] = idx < n ? kin[idx] : 0ull;
+            val[i] = idx < n ? vin[idx] : 0u;
+        }
+#pragma unroll
         for (int i = 0; i < kSortItems; ++i) {
             const int64_t idx = base + (int64_t)i * kSortThreads + threadIdx.x;
             const bool valid = idx < n;
-            key[i] = valid ? kin[idx] : 0ull;
-            val[i] = valid ? vin[idx] : 0u;
             const unsigned digit = valid ? ((unsigned)(key[i] >> shift) & 0xFF) : (0x100u | lane);
             const unsigned peers = __match_any_sync(kFull, digit);
             const unsigned r = __popc(peers & lt);
@@ -354,10 +358,16 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_coop(const SortSeg* __res
             const int shift = sg.shift[p];
             run[threadIdx.x] = 0;
             __syncthreads();
+            unsigned long long kk[kSortItems];
 #pragma unroll
             for (int i = 0; i < kSortItems; ++i) {
                 const int64_t idx = t * kSortTile + (int64_t)i * kSortThreads + threadIdx.x;
-                const unsigned digit = idx < n ? ((unsigned)(kin[idx] >> shift) & 0xFF) : (0x100u | lane);
+                kk[i] = idx < n ? kin[idx] : 0ull;
+            }
+#pragma unroll
+            for (int i = 0; i < kSortItems; ++i) {
+                const int64_t idx = t * kSortTile + (int64_t)i * kSortThreads + threadIdx.x;
+                const unsigned digit = idx < n ? ((unsigned)(kk[i] >> shift) & 0xFF) : (0x100u | lane);
                 const unsigned peers = __match_any_sync(kFull, digit);
                 if (digit < 0x100u && lane == __ffs(peers) - 1) atomicAdd(&run[digit], (unsigned)__popc(peers));
             }
@@ -398,11 +408,15 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_coop(const SortSeg* __res
             unsigned long long key[kSortItems];
             uint32_t val[kSortItems], rank[kSortItems];
 #pragma unroll
+            for (int i = 0; i < kSortItems; ++i) {     // every load of the tile in flight at once
+                const int64_t idx = tile * kSortTile + (int64_t)i * kSortThreads + threadIdx.x;
+                key[i] = idx < n ? kin[idx] : 0ull;
+                val[i] = idx < n ? vin[idx] : 0u;
+            }
+#pragma unroll
             for (int i = 0; i < kSortItems; ++i) {
                 const int64_t idx = tile * kSortTile + (int64_t)i * kSortThreads + threadIdx.x;
                 const bool valid = idx < n;
-                key[i] = valid ? kin[idx] : 0ull;
-                val[i] = valid ? vin[idx] : 0u;
                 const unsigned digit = valid ? ((unsigned)(key[i] >> shift) & 0xFF) : (0x100u | lane);
                 const unsigned peers = __match_any_sync(kFull, digit);
                 const unsigned r = __popc(peers & lt);
