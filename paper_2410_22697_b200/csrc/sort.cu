@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_fix(const SortSeg* __rest
     }
 }
 
-// ---- the whole sort in ONE cooperative launch (default): the same phases separated by grid-wide
+// ---- the whole sort in ONE cooperative launch (MGNN_SORT_COOP=1): the same phases separated by grid-wide
 // barriers instead of kernel boundaries.  An eviction round sorts a few thousand to a few ten thousand
 // candidates, where the 3 + 2 * passes dependent launches cost more than their work (products: ~150 us
 // for ~70k keys); here every block takes (segment, tile) pairs in a fixed stride.
@@ -473,9 +473,11 @@ void radix_sort_pairs(const SortSeg* segs_dev, int n_seg, int64_t n_max, int max
     int64_t gx = ((int64_t)num_sms() * 4 + n_seg - 1) / n_seg;
     if (gx > tiles) gx = tiles;
     dim3 grid((unsigned)(gx < 1 ? 1 : gx), (unsigned)n_seg);
+    // MGNN_SORT_COOP=1: the single cooperative launch below (measured slower on products' eviction
+    // rounds: 180 vs 150 us per sort -- the passes' work, not the launches, dominates)
     static const int coop = [] {
         const char* e = getenv("MGNN_SORT_COOP");
-        return e ? atoi(e) : 1;
+        return e ? atoi(e) : 0;
     }();
     if (coop) {                               // one cooperative launch, 1 block per SM at most
         int64_t nb = std::min<int64_t>((int64_t)num_sms(), (int64_t)n_seg * tiles);
