@@ -17,6 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libmgnn.so")
+LIB_CHECKED = os.path.join(HERE, "libmgnn_checked.so")
 UNITS = ["api.cu", "api_sage.cu", "sample.cu", "gather.cu", "score.cu", "sort.cu", "load.cu", "sage.cu", "train.cu"]
 HEADERS = ["common.cuh", "launch.h", "umma.cuh", "ctx.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -33,16 +34,20 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    objdir = os.path.join(HERE, "build")
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """checked=True builds libmgnn_checked.so with the device bounds checks (-DMGNN_CHECKS: every
+    MGNN_CHECK traps with a message) -- the debug library the test suite can load through MGNN_LIB."""
+    objdir = os.path.join(HERE, "build_checked" if checked else "build")
     os.makedirs(objdir, exist_ok=True)
+    lib = LIB_CHECKED if checked else LIB
+    flags = FLAGS + (["-DMGNN_CHECKS"] if checked else [])
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "mgnn.h")]
     jobs = []
     for u in UNITS:
         src = os.path.join(CSRC, u)
         obj = os.path.join(objdir, u.replace(".cu", ".o"))
         if force or _stale(obj, [src] + hdrs):
-            jobs.append([NVCC, *FLAGS, "-c", src, "-o", obj])
+            jobs.append([NVCC, *flags, "-c", src, "-o", obj])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -54,12 +59,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(6, os.cpu_count() or 1)) as ex:
         list(ex.map(run, jobs))
     objs = [os.path.join(objdir, u.replace(".cu", ".o")) for u in UNITS]
-    if force or jobs or _stale(LIB, objs):
-        tmp = LIB + f".tmp{os.getpid()}"
+    if force or jobs or _stale(lib, objs):
+        tmp = lib + f".tmp{os.getpid()}"
         run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp, "-lcudart"])
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

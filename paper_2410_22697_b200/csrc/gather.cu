@@ -52,8 +52,10 @@ __device__ __forceinline__ int classify(const WinDev& W, const WorldDev& G, cons
         h = r < pd.h_below ? r : r - pd.n_local;
         gid = pd.halo_ids[h];
     }
+    MGNN_CHECK(h < pd.n_h || W.remote, "classify h=%lld n_h=%lld", (long long)h, (long long)pd.n_h);
     if (h >= 0) {
         const int32_t s = pd.slot_of[h];
+        MGNN_CHECK(s < pd.cap, "classify slot=%d cap=%lld", s, (long long)pd.cap);
         if (s >= 0) {
             src = pd.rows + (int64_t)s * pitch;
             atomicOr(&pd.hitmask[s], wbit);
@@ -62,6 +64,8 @@ __device__ __forceinline__ int classify(const WinDev& W, const WorldDev& G, cons
         atomicAdd(&pd.sa[h], 1.0f);
     }
     const int qo = owner_of(G.bounds, G.n_parts, gid);
+    MGNN_CHECK(G.tables[qo] != nullptr && gid >= G.bounds[qo] && gid < G.bounds[qo + 1], "miss gid=%d owner=%d", gid,
+               qo);
     src = G.tables[qo] + ((int64_t)gid - G.bounds[qo]) * pitch;
     return G.on_peer[qo] ? 4 : 2;
 }

@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
             row = 0;
         }
         const int32_t r = (int32_t)((W.remote ? pd.lo : pd.h_below) + row);   // rank (= global id when remote)
+        MGNN_CHECK(j < W.ucap, "seed position %lld", (long long)j);
         fr[j] = r;
         W.fr_gid[(int64_t)m * W.ucap + j] = (int32_t)gid;   // F_0 readable right after sampling
         for (uint32_t h = seed_hash(r) & (uint32_t)W.seed_hmask;; h = (h + 1) & (uint32_t)W.seed_hmask) {
@@ -403,6 +404,9 @@ __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
 #pragma unroll
             for (int j = 0; j < kRelabelBatch; ++j) {
                 const int32_t p = frontier_pos(W, m, hop, sp, c[j]);
+                MGNN_CHECK(p >= 0 && (p < cap || *W.ovf <= W.step0 + (uint64_t)W.n_steps - 1 ||
+                                      e0 + j * kThreads >= E),
+                           "relabel pos=%d cap=%d", p, cap);
                 c[j] = p < cap ? p : cap - 1;
             }
 #pragma unroll

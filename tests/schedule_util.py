@@ -22,9 +22,46 @@ from oracle import oracle as O
 from tests.parity_util import assert_bits_equal
 
 
+class _Perturbed:
+    """Race probe: forwards to the context but first enqueues a random-length spin kernel on the stream
+    of every sample / lookup_gather / score call, so the two streams interleave differently on every
+    run (compute-sanitizer is closed on this pool; an ordering bug between the streams shows up here as
+    a mismatch with the oracle)."""
+
+    def __init__(self, ctx, seed: int, max_cycles: int = 400_000):
+        self._c = ctx
+        self._rng = np.random.default_rng(seed)
+        self._max = max_cycles
+
+    def __getattr__(self, k):
+        return getattr(self._c, k)
+
+    def _spin(self, stream):
+        import torch
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(int(self._rng.integers(0, self._max)))
+
+    def sample(self, sl, tt, n, stream=None, **kw):
+        self._spin(stream)
+        return self._c.sample(sl, tt, n, stream=stream, **kw)
+
+    def sample_ptr(self, sl, tt, n, sp, cp, on_host, stream=None):
+        self._spin(stream)
+        return self._c.sample_ptr(sl, tt, n, sp, cp, on_host, stream)
+
+    def lookup_gather(self, sl, stream=None):
+        self._spin(stream)
+        return self._c.lookup_gather(sl, stream)
+
+    def score(self, sl, stream=None):
+        self._spin(stream)
+        return self._c.score(sl, stream)
+
+
 def run_schedule_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, gamma: float, delta: int,
                         window: int, n_windows: int, x_rows: int = 2048, warm: int = 0, flush_bytes: int = 256 << 20,
-                        run_seed: int = synth.RUN_SEED, feat_seed: int = synth.FEAT_SEED, rows_bound: int = -1):
+                        run_seed: int = synth.RUN_SEED, feat_seed: int = synth.FEAT_SEED, rows_bound: int = -1,
+                        perturb=None):
     import torch
     from paper_2410_22697_b200 import pipeline as PL
     from paper_2410_22697_b200.schedule import PrepareAhead
@@ -38,7 +75,7 @@ def run_schedule_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_b
     ctx.sampler_config(fanouts, batch, run_seed, window, rows_bound=rows_bound)
     L = len(fanouts)
     n_inst = P * window
-    pipe = PrepareAhead(ctx, window, t0=1, flush_bytes=flush_bytes)
+    pipe = PrepareAhead(ctx if perturb is None else _Perturbed(ctx, perturb), window, t0=1, flush_bytes=flush_bytes)
     grabbed = []
     xpos_n = x_rows
 

@@ -44,3 +44,33 @@ def test_schedule_products_full_size_bench_config():
     g = synth.generate(synth.CONFIGS["products"])
     st = run_schedule_parity(g, 2, 100, [5, 10, 15], 2000, 5000, 0.995, 32, 32, 4, x_rows=2048)
     assert st["evicted"] > 0 and st["misses"] > 0
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_schedule_perturbed_interleavings(seed):
+    """Race probe of the two-stream schedule: random spin kernels before every call shift how the
+    sampling stream and the buffer stream interleave; every run must still equal the oracle."""
+    g = synth.generate(synth.CONFIGS["cfg1"])
+    st = run_schedule_parity(g, 2, 64, [10, 25], 256, 2500, 0.9, 4, 4, 6, x_rows=1024, perturb=seed)
+    assert st["evicted"] > 0
+
+
+def test_checked_library_schedule_and_parity():
+    """The device bounds checks (-DMGNN_CHECKS: every MGNN_CHECK traps) on the timed schedule, the
+    window-batching parity tests and the API tests, in a fresh interpreter that loads
+    libmgnn_checked.so (MGNN_LIB) with MGNN_DEBUG_SYNC=1 (every launch synchronised and checked)."""
+    import os
+    import subprocess
+    import sys
+    from paper_2410_22697_b200 import build
+    lib = build.build(checked=True)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MGNN_LIB=lib, MGNN_DEBUG_SYNC="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_gpu_schedule.py::test_schedule_cfg1_windows_with_eviction_rounds",
+                        "tests/test_gpu_parity.py::test_cfg1_windows", "tests/test_gpu_parity.py::test_cfg1_policy_grid",
+                        "tests/test_gpu_api.py::test_arena_overflow_skips_windows_and_resumes"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=1200)
+    print(r.stdout[-3000:], r.stderr[-2000:])
+    assert r.returncode == 0
+    assert "libmgnn_checked" in lib
