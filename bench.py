@@ -217,12 +217,19 @@ def nvlink_counters(index: int):
             return None
         ids = [nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX]
         vals = nv.nvmlDeviceGetFieldValues(h, ids)
-        out = []
-        for v in vals:
-            if v.nvmlReturn != 0:
-                return None
-            out.append(int(v.value.ullVal))
-        return out
+        if all(v.nvmlReturn == 0 for v in vals):
+            return [int(v.value.ullVal) * 1024 for v in vals] + ["NVLINK_THROUGHPUT_DATA_TX/RX (KiB)"]
+        # per-link byte counters, summed over the links (scopeId = link index)
+        tx = rx = 0
+        ok = False
+        for link in range(18):
+            vv = nv.nvmlDeviceGetFieldValues(h, [(nv.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES, link),
+                                                 (nv.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES, link)])
+            if vv[0].nvmlReturn == 0 and vv[1].nvmlReturn == 0:
+                tx += int(vv[0].value.ullVal)
+                rx += int(vv[1].value.ullVal)
+                ok = True
+        return [tx, rx, "NVLINK_COUNT_XMIT/RCV_BYTES summed over links"] if ok else None
     except Exception:
         return None
 
@@ -654,9 +661,12 @@ def main():
             peer = peer_copy_gbs(local, (local + 1) % torch.cuda.device_count())
             cnt = None
             if nv0 and nv1:
-                cnt = {"tx_bytes_per_window": (nv1[0] - nv0[0]) * 1024 / n_win,
-                       "rx_bytes_per_window": (nv1[1] - nv0[1]) * 1024 / n_win,
-                       "source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX (KiB) of this GPU around the timed runs"}
+                txw, rxw = (nv1[0] - nv0[0]) / n_win, (nv1[1] - nv0[1]) / n_win
+                cnt = {"tx_bytes_per_window": txw, "rx_bytes_per_window": rxw,
+                       "rx_gbs_over_window": rxw / (med["ms_per_step"] / 1e3) / 1e9,
+                       "source": f"NVML {nv0[2]} of this GPU around the timed runs"}
+            else:
+                cnt = {"unavailable": "NVML NVLink throughput / byte counters not exposed on this driver"}
             line["nvlink"] = {"peer_rows_per_window": peer_rows, "bytes_per_window": nv_bytes,
                               "gbs_during_gather": gbs,
                               "peak_gbs": 900.0, "peak_source": "NVLink 5 nominal per direction per GPU",
