@@ -621,7 +621,9 @@ def main():
                        "x_bytes_per_slot": (rows_bound or static_ucap(S)) * (((cfg.feat_dim + 3) // 4) * 4) * 4
                        * S.ppg * WINDOW,
                        "note": "mgnn_sampler_config_bounded: pilot max |F_L| x 1.25; overflow -> skipped + retried"},
-            "hit_rate": hits / max(1, hits + misses),
+            "hit_rate": prof["hits"] / max(1.0, prof["hits"] + prof["misses"]),
+            "hit_rate_note": "buffer hits / halo accesses over every timed window (R#23 unique nodes per minibatch)",
+            "hit_rate_last_window": hits / max(1, hits + misses),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": E2E, "path": "schedule.PrepareAhead with host seeds: mgnn_sample(pinned host seeds, "
                                           "H2D) | lookup_gather + score_evict_refill + counts_read_async (D2H); "

@@ -314,6 +314,7 @@ enum {
     MGNN_PROF_UNIQUE = 4,     /* U: |F_L| summed over instances */
     MGNN_PROF_GATHER_MS = 5, MGNN_PROF_GATHER_CALLS = 6, MGNN_PROF_GATHER_ROWS = 7,
     MGNN_PROF_SCORE_MS = 8, MGNN_PROF_SCORE_CALLS = 9,
+    MGNN_PROF_HITS = 10, MGNN_PROF_MISSES = 11,   /* buffer hits / misses of every gathered minibatch */
     MGNN_PROF_N = 12
 };
 MGNN_API mgnn_status mgnn_profile_stages(mgnn_ctx ctx, double* out, int32_t n_out);

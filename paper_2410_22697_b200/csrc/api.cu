@@ -236,6 +236,7 @@ WinDev win_dev(mgnn_ctx ctx, Win& w) {
     d.err = ctx->d_err;
     d.gathered_rows = ctx->d_gathered;
     d.sampled_units = ctx->prof ? ctx->d_sampled : nullptr;
+    d.prof_hm = ctx->prof ? ctx->d_sampled + 3 : nullptr;
     d.remote = ctx->remote ? 1 : 0;
     d.n_global = ctx->n_global;
     d.g_indptr = ctx->g_indptr;
@@ -300,8 +301,8 @@ mgnn_status mgnn_ctx_create(int32_t device, int32_t n_parts, int64_t n_global, c
     chk(cudaMemset(ctx->d_ovf, 0xFF, sizeof(unsigned long long)));
     chk(dalloc(&ctx->d_gathered, 1));
     chk(cudaMemset(ctx->d_gathered, 0, sizeof(long long)));
-    chk(dalloc(&ctx->d_sampled, 3));
-    chk(cudaMemset(ctx->d_sampled, 0, 3 * sizeof(long long)));
+    chk(dalloc(&ctx->d_sampled, 5));
+    chk(cudaMemset(ctx->d_sampled, 0, 5 * sizeof(long long)));
     if (st != MGNN_OK) {
         mgnn_destroy(ctx);
         return st;
@@ -1197,7 +1198,7 @@ mgnn_status mgnn_profile_stages(mgnn_ctx ctx, double* out, int32_t n_out) {
         mgnn_status r = drain_events(ctx, st, &ms[st], &n[st]);
         if (r) return r;
     }
-    long long su[3] = {0, 0, 0}, rows = 0;
+    long long su[5] = {0, 0, 0, 0, 0}, rows = 0;
     CK(cudaMemcpy(su, ctx->d_sampled, sizeof(su), cudaMemcpyDeviceToHost));
     CK(cudaMemset(ctx->d_sampled, 0, sizeof(su)));
     CK(cudaMemcpy(&rows, ctx->d_gathered, sizeof(long long), cudaMemcpyDeviceToHost));
@@ -1213,6 +1214,8 @@ mgnn_status mgnn_profile_stages(mgnn_ctx ctx, double* out, int32_t n_out) {
     out[MGNN_PROF_GATHER_ROWS] = (double)rows;
     out[MGNN_PROF_SCORE_MS] = ms[2];
     out[MGNN_PROF_SCORE_CALLS] = (double)n[2];
+    out[MGNN_PROF_HITS] = (double)su[3];
+    out[MGNN_PROF_MISSES] = (double)su[4];
     return MGNN_OK;
 }
 

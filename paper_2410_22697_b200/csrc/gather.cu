@@ -168,6 +168,10 @@ __global__ void __launch_bounds__(kGThreads, 4) k_gather(WinDev W, WorldDev G) {
         if (cnt_sh[3]) atomicAdd((unsigned long long*)&cn[7], cnt_sh[3]);
         const unsigned long long rows = cnt_sh[0] + cnt_sh[1] + cnt_sh[2];
         if (rows && W.gathered_rows) atomicAdd((unsigned long long*)W.gathered_rows, rows);
+        if (W.prof_hm) {
+            if (cnt_sh[1]) atomicAdd((unsigned long long*)&W.prof_hm[0], cnt_sh[1]);
+            if (cnt_sh[2]) atomicAdd((unsigned long long*)&W.prof_hm[1], cnt_sh[2]);
+        }
         if (blockIdx.x == 0) cn[0] = U;
     }
 }
@@ -275,6 +279,10 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
             if (n_peer) atomicAdd((unsigned long long*)&cn[7], (unsigned long long)n_peer);
             const unsigned long long rows = (unsigned long long)n_loc + n_hit + n_miss;
             if (rows && W.gathered_rows) atomicAdd((unsigned long long*)W.gathered_rows, rows);
+            if (W.prof_hm) {
+                if (n_hit) atomicAdd((unsigned long long*)&W.prof_hm[0], (unsigned long long)n_hit);
+                if (n_miss) atomicAdd((unsigned long long*)&W.prof_hm[1], (unsigned long long)n_miss);
+            }
         }
         n_loc = n_hit = n_miss = n_peer = 0;
     };
@@ -571,6 +579,10 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_g4(WinDev W, WorldDev G
         if (cnt_sh[3]) atomicAdd((unsigned long long*)&cn[7], cnt_sh[3]);
         const unsigned long long rows = cnt_sh[0] + cnt_sh[1] + cnt_sh[2];
         if (rows && W.gathered_rows) atomicAdd((unsigned long long*)W.gathered_rows, rows);
+        if (W.prof_hm) {
+            if (cnt_sh[1]) atomicAdd((unsigned long long*)&W.prof_hm[0], cnt_sh[1]);
+            if (cnt_sh[2]) atomicAdd((unsigned long long*)&W.prof_hm[1], cnt_sh[2]);
+        }
         if (blockIdx.x == 0) cn[0] = U;
     }
 }

@@ -66,6 +66,7 @@ struct WinDev {
     int32_t* err;                        // device error word
     long long* gathered_rows;            // profiling counter
     long long* sampled_units;            // profiling: [3] += E, F, U of every instance (k_relabel)
+    long long* prof_hm;                  // profiling: [2] += hits, misses of every gathered instance
     // NEXT-1 remote expansion: ranks are global ids; every frontier node is sampled from the
     // global CSR (all partitions hosted by this context)
     int32_t remote;

@@ -303,7 +303,7 @@ class Context:
         out = np.zeros(_lib.PROF_N, np.float64)
         self._chk("mgnn_profile_stages", self.L.mgnn_profile_stages(self._h, _ptr(out), _lib.PROF_N))
         keys = ["sample_ms", "sample_calls", "edges", "frontier", "unique", "gather_ms", "gather_calls",
-                "gather_rows", "score_ms", "score_calls"]
+                "gather_rows", "score_ms", "score_calls", "hits", "misses"]
         return {k: float(out[i]) for i, k in enumerate(keys)}
 
     def profile_read(self):
