@@ -429,8 +429,11 @@ static void ensure_F(orc_part* p, int64_t n) {
 int orc_step(orc_part* p, uint64_t run_seed, uint64_t step, const int32_t* fanouts, int32_t n_layers,
              int32_t batch, const int32_t* seeds, int32_t n_seeds) {
     if (!p->ready || step < 1 || n_layers < 1 || n_layers > 8) return -1;
-    for (int32_t l = 0; l < n_layers; l++)
-        if (fanouts[l] < 1 || fanouts[l] > 32) return -1;
+    int32_t k_max = 1;
+    for (int32_t l = 0; l < n_layers; l++) {
+        if (fanouts[l] < 1) return -1;
+        if (fanouts[l] > k_max) k_max = fanouts[l];
+    }
     orc_world* w = p->w;
     const int32_t D = w->D;
     free_step(p);
@@ -494,9 +497,9 @@ int orc_step(orc_part* p, uint64_t run_seed, uint64_t step, const int32_t* fanou
                 int64_t row = x - src->lo, b0 = src->indptr[row], d = src->indptr[row + 1] - b0;
                 if (d <= k) {                          /* d <= k: whole neighbourhood (R#3) */
                     for (int64_t j = 0; j < d; j++) col[ne++] = src->cols[b0 + j];
-                } else {
-                    uint32_t r[32];
-                    int64_t pos[32];
+                } else {                               /* any fanout (the GPU library caps it at 32) */
+                    uint32_t* r = malloc(sizeof(uint32_t) * (size_t)k_max);
+                    int64_t* pos = malloc(sizeof(int64_t) * (size_t)k_max);
                     for (int32_t j = 0; j < k; j++) {
                         uint32_t ctr[4] = {(uint32_t)x, ((uint32_t)i << 16) | (uint32_t)j, (uint32_t)step,
                                            ((uint32_t)p->p << 8) | 1u}, o[4];
@@ -505,6 +508,8 @@ int orc_step(orc_part* p, uint64_t run_seed, uint64_t step, const int32_t* fanou
                     }
                     orc_floyd(d, k, r, pos);
                     for (int32_t j = 0; j < k; j++) col[ne++] = src->cols[b0 + pos[j]];
+                    free(r);
+                    free(pos);
                 }
             }
             off[f + 1] = ne;

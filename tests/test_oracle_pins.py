@@ -347,6 +347,18 @@ def test_sampler_invariants_random_graphs(seed):
         _check_sampler_invariants(W.parts[0], g, lo, hi, [2, 3])
 
 
+def test_sampler_fanouts_above_the_gpu_cap():
+    """The oracle follows the paper for any fanout (the CUDA library caps k at 32, MGNN_MAX_FANOUT):
+    k = 40 and 64 on a dense graph (degrees ~50-90) keep every sampler invariant."""
+    g = synth.random_graph(120, 0.7, 11)
+    W, parts = world_from(g, 2)
+    for p in W.parts:
+        p.buffer_init(0.9, 0.5, 1.0, 3, 5000)
+    for t in range(1, 4):
+        W.parts[0].step(RUN_SEED, t, [40, 64], 4)
+        _check_sampler_invariants(W.parts[0], g, 0, 60, [40, 64])
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_sampler_full_fanout_is_local_bfs(seed):
     """fanout >= max degree -> F_L is exactly the L-hop neighbourhood expanded through local nodes."""
