@@ -264,6 +264,17 @@ MGNN_API mgnn_status mgnn_sage_params(mgnn_ctx ctx, int32_t l, float* w_self, fl
 /* Device view of a window slot (valid after mgnn_sample of that slot). */
 MGNN_API mgnn_status mgnn_window_get(mgnn_ctx ctx, int32_t slot, mgnn_window* out);
 
+/* Caller-owned X (SURVEY §8(b) allocates X on the caller's side, e.g. a torch tensor): the arena
+ * shape is n_inst_max x rows_stride rows of `pitch` floats (mgnn_window_shape, after
+ * mgnn_sampler_config[_bounded]); mgnn_window_bind_x makes window slot `slot` gather into the
+ * caller's DEVICE buffer X (16-byte aligned, >= n_inst_max * rows_stride * pitch floats, on this
+ * context's GPU) and frees the library's arena of that slot.  The binding lasts until the next
+ * sampler configuration (which allocates library arenas again); the caller keeps ownership and
+ * must keep X alive while the slot is in use.  Synchronises the device.  EINVAL: too small,
+ * misaligned, not device memory of this GPU; ESTATE: before the sampler configuration. */
+MGNN_API mgnn_status mgnn_window_shape(mgnn_ctx ctx, int64_t* rows_stride, int64_t* pitch, int64_t* n_inst_max);
+MGNN_API mgnn_status mgnn_window_bind_x(mgnn_ctx ctx, int32_t slot, float* X, int64_t capacity_floats);
+
 /* Copy the window's counters ([n_inst][MGNN_C_N] int64) to host memory and
  * synchronise `stream`. */
 MGNN_API mgnn_status mgnn_counts_read(mgnn_ctx ctx, int32_t slot, int64_t* host_counts, mgnn_stream stream);

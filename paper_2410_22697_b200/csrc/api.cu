@@ -171,7 +171,8 @@ void free_win(Win& w) {
         dfree(w.off[i]);
         dfree(w.cols[i]);
     }
-    dfree(w.X);
+    if (!w.x_user) dfree(w.X);              // a caller-owned X stays the caller's
+    w.X = nullptr;
     dfree(w.zero);
     dfree(w.ext_seeds);
     dfree(w.ext_counts);
@@ -1065,6 +1066,37 @@ mgnn_status mgnn_window_get(mgnn_ctx ctx, int32_t slot, mgnn_window* out) {
     }
     out->counts = (const int64_t*)w.counts;
     return MGNN_OK;
+}
+
+mgnn_status mgnn_window_shape(mgnn_ctx ctx, int64_t* rows_stride, int64_t* pitch, int64_t* max_inst) {
+    GUARD();
+    if (!ctx->configured) return fail(ctx, MGNN_ESTATE, "window_shape before sampler_config");
+    if (rows_stride) *rows_stride = ctx->ucap;
+    if (pitch) *pitch = ctx->pitch;
+    if (max_inst) *max_inst = (int64_t)ctx->parts.size() * ctx->max_window;
+    return MGNN_OK;
+}
+
+mgnn_status mgnn_window_bind_x(mgnn_ctx ctx, int32_t slot, float* X, int64_t capacity_floats) {
+    GUARD();
+    if (!ctx->configured) return fail(ctx, MGNN_ESTATE, "bind_x before sampler_config");
+    if (slot < 0 || slot > 1 || !X) return fail(ctx, MGNN_EINVAL, "bind_x: bad slot / null X");
+    const int64_t need = (int64_t)ctx->parts.size() * ctx->max_window * ctx->ucap * ctx->pitch;
+    if (capacity_floats < need)
+        return fail(ctx, MGNN_EINVAL, "bind_x: X holds " + std::to_string(capacity_floats) + " floats, the window needs " +
+                                          std::to_string(need));
+    if ((reinterpret_cast<uintptr_t>(X) & 15) != 0) return fail(ctx, MGNN_EINVAL, "bind_x: X must be 16-byte aligned");
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, X) != cudaSuccess || pa.type != cudaMemoryTypeDevice || pa.device != ctx->device) {
+        cudaGetLastError();
+        return fail(ctx, MGNN_EINVAL, "bind_x: X is not device memory of this context's GPU");
+    }
+    CK(cudaDeviceSynchronize());                 // the slot's previous X may still be read or written
+    Win& w = ctx->win[slot];
+    if (!w.x_user) dfree(w.X);
+    w.X = X;
+    w.x_user = true;
+    return rebind_sage_input(ctx, slot);         // the consumer's TMA descriptor of layer 0 reads X
 }
 
 mgnn_status mgnn_counts_read_async(mgnn_ctx ctx, int32_t slot, int64_t* host_counts, mgnn_stream stream) {

@@ -45,6 +45,19 @@ void free_sage(mgnn_ctx_s* ctx) {
 }  // namespace host
 }  // namespace mgnn
 
+namespace mgnn {
+namespace host {
+mgnn_status rebind_sage_input(mgnn_ctx ctx, int slot) {
+    auto& S = ctx->sage;
+    if (!S.ready) return MGNN_OK;
+    const int64_t M = (int64_t)ctx->parts.size() * ctx->max_window;
+    if (!sage_encode_map(S.map_in[slot][0], ctx->win[slot].X, M * ctx->ucap, ctx->pitch, ctx->pitch, 128))
+        return fail(ctx, MGNN_ECUDA, "bind_x: cuTensorMapEncodeTiled (layer 0 input) failed");
+    return MGNN_OK;
+}
+}  // namespace host
+}  // namespace mgnn
+
 extern "C" {
 
 // ------------------------------------------------------------------ A14: GraphSAGE-mean consumer

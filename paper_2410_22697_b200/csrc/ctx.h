@@ -43,6 +43,7 @@ struct Part {
 
 struct Win {
     bool alloc = false, sampled = false, gathered = false, scored = false;
+    bool x_user = false;            // X is a caller-owned buffer (mgnn_window_bind_x)
     int32_t n_steps = 0;
     uint64_t step0 = 0;
     int32_t* fr_rank = nullptr;
@@ -231,6 +232,7 @@ mgnn_status upload_tables(mgnn_ctx ctx);
 WorldDev world_of(mgnn_ctx ctx);
 void free_win(Win& w);
 void free_sage(mgnn_ctx_s* ctx);           // api_sage.cu
+mgnn_status rebind_sage_input(mgnn_ctx ctx, int slot);   // api_sage.cu: re-encode layer 0's X descriptor
 void free_buffer(Part& p);
 void free_perm(Part& p);
 mgnn_status ensure_scratch(mgnn_ctx ctx, void** p, size_t* have, size_t bytes);

@@ -286,6 +286,20 @@ class Context:
         self._chk("mgnn_table_row", self.L.mgnn_table_row(self._h, node, _ptr(out)))
         return out
 
+    def window_shape(self):
+        """(rows_stride, pitch, n_inst_max) of the window arenas (mgnn_window_shape)."""
+        r, p, m = C.c_int64(), C.c_int64(), C.c_int64()
+        self._chk("mgnn_window_shape", self.L.mgnn_window_shape(self._h, C.byref(r), C.byref(p), C.byref(m)))
+        return r.value, p.value, m.value
+
+    def bind_x(self, slot: int, X) -> None:
+        """Caller-owned X for window slot `slot` (mgnn_window_bind_x): a contiguous float32 CUDA tensor of
+        at least n_inst_max * rows_stride * pitch elements; the caller keeps it alive."""
+        assert X.is_cuda and X.dtype.itemsize == 4 and X.is_contiguous()
+        self._chk("mgnn_window_bind_x", self.L.mgnn_window_bind_x(self._h, slot, C.c_void_p(X.data_ptr()), X.numel()))
+        self._x_keep = getattr(self, "_x_keep", {})
+        self._x_keep[slot] = X
+
     def next_step(self) -> int:
         """mgnn_next_step: first step of the next window the library will gather."""
         out = C.c_uint64()

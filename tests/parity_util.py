@@ -39,7 +39,7 @@ def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, g
                theta_r: float, windows, run_seed: int = synth.RUN_SEED, feat_seed: int = synth.FEAT_SEED,
                alpha=None, hosted=None, sample_every: int = 1, check_x_rows: int = 0, ext_seeds=None,
                device: int = 0, exchange: bool = False, remote: bool = False, dense: bool = False,
-               rows_bound: int = 0):
+               rows_bound: int = 0, bind_x: bool = False):
     """windows: list of window lengths run back to back from step 1."""
     from paper_2410_22697_b200 import pipeline as PL
 
@@ -61,6 +61,13 @@ def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, g
     if rows_bound < 0:                # realistic arenas from a pilot (pipeline.estimate_rows_bound)
         rows_bound = PL.estimate_rows_bound(ctx, fanouts, batch, run_seed)
     ctx.sampler_config(fanouts, batch, run_seed, max(windows), rows_bound=rows_bound)
+    x_user = {}
+    if bind_x:                        # caller-owned X (mgnn_window_bind_x): torch tensors, NaN-filled
+        import torch
+        rs, pitch, mi = ctx.window_shape()
+        for sl in (0, 1):
+            x_user[sl] = torch.full((mi, rs, pitch), float("nan"), device="cuda", dtype=torch.float32)
+            ctx.bind_x(sl, x_user[sl])
     lps = {pid: lp for lp, pid in enumerate(ctx.parts)}
     # static partition facts
     for pid, lp in lps.items():
@@ -126,6 +133,8 @@ def run_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, g
                     assert_bits_equal(gcols.astype(np.int32), cols, f"cols hop{i} p{pid} t{step}")
                     assert np.all(inst[f"cols{i}"] < hs[i + 1])
                 X = op.features()
+                if bind_x:                    # the rows landed in the caller's tensor
+                    assert_bits_equal(x_user[slot][m, :X.shape[0], :D].cpu().numpy(), X, f"user X p{pid} t{step}")
                 if check_x_rows and X.shape[0] > check_x_rows:
                     sel = np.linspace(0, X.shape[0] - 1, check_x_rows).astype(np.int64)
                     assert_bits_equal(inst["X"][sel], X[sel], f"X p{pid} t{step}")

@@ -61,7 +61,7 @@ def oracle_instance(op, step, fanouts, batch, run_seed=synth.RUN_SEED):
 
 
 def run_sage_parity(g, P, D, fanouts, batch, dims, windows, f_bp=2500, gamma=0.95, delta=0,
-                    inst_every=1, weight_seed=synth.SAGE_SEED, device=0):
+                    inst_every=1, weight_seed=synth.SAGE_SEED, device=0, bind_x=False):
     """Sample/gather windows on the GPU, run the consumer, compare every checked instance's
     logits with the fp64 oracle within error_bound.  Returns max |err| / bound."""
     import torch
@@ -77,6 +77,10 @@ def run_sage_parity(g, P, D, fanouts, batch, dims, windows, f_bp=2500, gamma=0.9
     ctx.sampler_config(fanouts, batch, synth.RUN_SEED, max(windows))
     wts = synth.sage_weights(dims, seed=weight_seed)
     ctx.sage_config(dims, [w[0] for w in wts], [w[1] for w in wts], [w[2] for w in wts])
+    if bind_x:                        # caller-owned X (mgnn_window_bind_x) after the consumer exists
+        rs, pitch, mi = ctx.window_shape()
+        for sl in (0, 1):
+            ctx.bind_x(sl, torch.full((mi * rs * pitch,), float("nan"), device="cuda", dtype=torch.float32))
     C = dims[-1]
     worst = 0.0
     t, slot = 1, 0

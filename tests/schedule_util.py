@@ -10,7 +10,7 @@ columns, and sampled X rows), then compares everything with the oracle (PAPER.md
 step, oracle/orc.c) once the run is over:
   * counts (|F_L|, local, hits, misses, evicted, rows fetched) of every instance of every window,
   * hop sizes, F_L, offsets and columns of the captured instances, element by element,
-  * X rows of the captured instances at `x_rows` evenly spaced positions (all rows if fewer),
+  * X rows of the captured instances: every row (x_rows = 0) or `x_rows` evenly spaced positions,
   * BUF membership, S_E, S_A, slot_of and BUF rows after the last window (0 ULP).
 """
 from __future__ import annotations
@@ -93,10 +93,14 @@ def run_schedule_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_b
             for m in picks:
                 U = hs_all[m, L]
                 rec[f"fr{m}"] = fr[m].clone()
-                k = torch.arange(xpos_n, device="cuda", dtype=torch.int64)
-                pos = torch.minimum((k * (U - 1)) // max(1, xpos_n - 1), U - 1)
-                rec[f"xpos{m}"] = pos
-                rec[f"x{m}"] = X[m].index_select(0, pos)[:, :D].clone()
+                if xpos_n > 0:               # x_rows evenly spaced rows
+                    k = torch.arange(xpos_n, device="cuda", dtype=torch.int64)
+                    pos = torch.minimum((k * (U - 1)) // max(1, xpos_n - 1), U - 1)
+                    rec[f"xpos{m}"] = pos
+                    rec[f"x{m}"] = X[m].index_select(0, pos)[:, :D].clone()
+                else:                        # x_rows = 0: every row of the arena (compared up to |F_L|)
+                    rec[f"xpos{m}"] = None
+                    rec[f"x{m}"] = X[m][:, :D].clone()
                 for i in range(L):
                     rec[f"off{m}_{i}"] = PL.device_view(wv.offsets[i], (n_inst, wv.off_stride[i]), "i8")[m].clone()
                     rec[f"cols{m}_{i}"] = PL.device_view(wv.cols[i], (n_inst, wv.col_stride[i]), "i4")[m].clone()
@@ -152,9 +156,13 @@ def run_schedule_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_b
                     assert_bits_equal(gF[gc_].astype(np.int32) if len(gc_) else gc_, cols,
                                       f"cols hop{i} p{pid} t{step}")
                 X = op.features()
-                pos = rec[f"xpos{m}"].cpu().numpy()
-                assert_bits_equal(rec[f"x{m}"].cpu().numpy(), X[pos], f"X p{pid} t{step}")
-                stats["x_rows"] += len(pos)
+                if rec[f"xpos{m}"] is None:
+                    assert_bits_equal(rec[f"x{m}"][:U].cpu().numpy(), X, f"X p{pid} t{step}")
+                    stats["x_rows"] += U
+                else:
+                    pos = rec[f"xpos{m}"].cpu().numpy()
+                    assert_bits_equal(rec[f"x{m}"].cpu().numpy(), X[pos], f"X p{pid} t{step}")
+                    stats["x_rows"] += len(pos)
     for pid, lp in lps.items():
         gs = snaps[pid]
         os_ = W.parts[pid].buffer_state(rows=True)

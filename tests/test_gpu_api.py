@@ -290,3 +290,19 @@ def test_bounded_arenas_parity(graph):
     from tests.parity_util import run_parity
     st = run_parity(graph, 2, 64, [10, 25], 256, 2500, 0.9, 4, 1.0, [4, 4, 4], rows_bound=-1)
     assert st["evicted"] > 0
+
+
+def test_caller_owned_x(graph):
+    """SURVEY §8(b)'s caller-owned X: torch tensors bound with mgnn_window_bind_x receive every
+    gathered row (bit-exact against the oracle), also as the consumer's input."""
+    from tests.parity_util import run_parity
+    from tests.sage_util import run_sage_parity
+    run_parity(graph, 2, 64, [10, 25], 256, 2500, 0.9, 4, 1.0, [4, 4], bind_x=True)
+    assert run_sage_parity(graph, 2, 64, [10, 25], 256, synth.sage_dims(64, 2, 16), [4], bind_x=True) <= 1.0
+    ctx = _ctx(graph)
+    rs, pitch, mi = ctx.window_shape()
+    small = torch.zeros(mi * rs * pitch - 4, device="cuda")
+    with pytest.raises(MgnnError) as e:
+        ctx.bind_x(0, small)
+    assert _status(e) == EINVAL
+    ctx.close()
