@@ -264,6 +264,15 @@ MGNN_API mgnn_status mgnn_sage_params(mgnn_ctx ctx, int32_t l, float* w_self, fl
 /* Device view of a window slot (valid after mgnn_sample of that slot). */
 MGNN_API mgnn_status mgnn_window_get(mgnn_ctx ctx, int32_t slot, mgnn_window* out);
 
+/* Deferred relabelling: with enable != 0, mgnn_sample stops after the last compaction and leaves
+ * every hop's columns as LOCAL RANKS; mgnn_relabel(slot) then rewrites them as positions in
+ * F_{i+1} (the DGL block layout of mgnn_window) on the given stream.  The gather does not read the
+ * columns, so the relabel of window w can run on a third stream beside its gather (it is L2-bound,
+ * the gather HBM-bound); the consumer and the training step refuse (ESTATE) a window whose relabel
+ * is still pending.  mgnn_relabel: ESTATE unless the slot was sampled with the relabel deferred. */
+MGNN_API mgnn_status mgnn_sampler_defer_relabel(mgnn_ctx ctx, int32_t enable);
+MGNN_API mgnn_status mgnn_relabel(mgnn_ctx ctx, int32_t slot, mgnn_stream stream);
+
 /* Caller-owned X (SURVEY §8(b) allocates X on the caller's side, e.g. a torch tensor): the arena
  * shape is n_inst_max x rows_stride rows of `pitch` floats (mgnn_window_shape, after
  * mgnn_sampler_config[_bounded]); mgnn_window_bind_x makes window slot `slot` gather into the
@@ -326,7 +335,8 @@ enum {
     MGNN_PROF_GATHER_MS = 5, MGNN_PROF_GATHER_CALLS = 6, MGNN_PROF_GATHER_ROWS = 7,
     MGNN_PROF_SCORE_MS = 8, MGNN_PROF_SCORE_CALLS = 9,
     MGNN_PROF_HITS = 10, MGNN_PROF_MISSES = 11,   /* buffer hits / misses of every gathered minibatch */
-    MGNN_PROF_N = 12
+    MGNN_PROF_RELABEL_MS = 12, MGNN_PROF_RELABEL_CALLS = 13,   /* deferred k_relabel (mgnn_relabel) */
+    MGNN_PROF_N = 16
 };
 MGNN_API mgnn_status mgnn_profile_stages(mgnn_ctx ctx, double* out, int32_t n_out);
 

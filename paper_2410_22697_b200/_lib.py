@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MGNN_LIB", os.path.join(HERE, "libmgnn.so"))   # override: A/B builds
 
 MAX_LAYERS = 8
-PROF_N = 12                      # MGNN_PROF_N
+PROF_N = 16                      # MGNN_PROF_N
 IPC_HANDLE_BYTES = 64
 C_NODES, C_LOCAL, C_HIT, C_MISS, C_EVICTED, C_REFILLED, C_ROWS_FETCHED, C_PEER_ROWS, C_N = 0, 1, 2, 3, 4, 5, 6, 7, 8
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 5: "ESTATE", 6: "EOVERFLOW"}
@@ -19,7 +19,8 @@ SYMBOLS = [
     "mgnn_table_export", "mgnn_table_import", "mgnn_buffer_init", "mgnn_sampler_config", "mgnn_sample",
     "mgnn_lookup_gather", "mgnn_score_evict_refill", "mgnn_sampler_config_bounded", "mgnn_window_get", "mgnn_counts_read",
     "mgnn_counts_read_async",
-    "mgnn_buffer_snapshot", "mgnn_part_info", "mgnn_next_step", "mgnn_window_shape", "mgnn_window_bind_x", "mgnn_halo_get", "mgnn_table_row", "mgnn_launch_count",
+    "mgnn_buffer_snapshot", "mgnn_part_info", "mgnn_next_step", "mgnn_window_shape", "mgnn_window_bind_x",
+    "mgnn_sampler_defer_relabel", "mgnn_relabel", "mgnn_halo_get", "mgnn_table_row", "mgnn_launch_count",
     "mgnn_profile_enable", "mgnn_profile_read", "mgnn_profile_stages", "mgnn_profile_kernels",
     "mgnn_sage_config", "mgnn_sage_forward", "mgnn_sage_train_config", "mgnn_sage_train_step",
     "mgnn_sage_grads", "mgnn_sage_sgd", "mgnn_sage_loss", "mgnn_sage_params", "mgnn_sampler_expand_remote",
@@ -94,6 +95,8 @@ def load(path: str = LIB_PATH):
         "mgnn_launch_count": (I64, [P]),
         "mgnn_next_step": (S, [P, P]),
         "mgnn_window_shape": (S, [P, P, P, P]),
+        "mgnn_sampler_defer_relabel": (S, [P, I32]),
+        "mgnn_relabel": (S, [P, I32, P]),
         "mgnn_window_bind_x": (S, [P, I32, P, I64]),
         "mgnn_profile_enable": (S, [P, I32]),
         "mgnn_profile_read": (S, [P, P, P, P]),

@@ -932,14 +932,45 @@ mgnn_status mgnn_sample(mgnn_ctx ctx, int32_t slot, uint64_t t0, int32_t n_steps
         launch_hop(wd, i, ctx->fcap[i], scc, s);
         launch_compact(wd, i, scp, s);
     }
-    launch_relabel(wd, s);
+    if (!ctx->defer_relabel) launch_relabel(wd, s);
     CKL();
     if (ctx->prof) {
         CK(cudaEventRecord(pe1, s));
         ctx->prof_ev[0].emplace_back(pe0, pe1);
     }
     w.sampled = true;
+    w.relabel_pending = ctx->defer_relabel;
     w.gathered = w.scored = false;
+    return MGNN_OK;
+}
+
+mgnn_status mgnn_sampler_defer_relabel(mgnn_ctx ctx, int32_t enable) {
+    GUARD();
+    ctx->defer_relabel = enable != 0;
+    return MGNN_OK;
+}
+
+mgnn_status mgnn_relabel(mgnn_ctx ctx, int32_t slot, mgnn_stream stream) {
+    GUARD();
+    if (slot < 0 || slot > 1) return fail(ctx, MGNN_EINVAL, "bad slot");
+    Win& w = ctx->win[slot];
+    if (!w.sampled || !w.relabel_pending) return fail(ctx, MGNN_ESTATE, "relabel needs a window sampled with the relabel deferred");
+    cudaStream_t s = (cudaStream_t)stream;
+    WinDev wd = win_dev(ctx, w);
+    wd.n_inst = (int32_t)((int64_t)ctx->parts.size() * w.n_steps);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->prof) {
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, s));
+    }
+    launch_relabel(wd, s);
+    CKL();
+    if (ctx->prof) {
+        CK(cudaEventRecord(e1, s));
+        ctx->prof_ev[3].emplace_back(e0, e1);
+    }
+    w.relabel_pending = false;
     return MGNN_OK;
 }
 
@@ -1224,9 +1255,9 @@ static mgnn_status drain_events(mgnn_ctx ctx, int stage, double* ms, long long* 
 mgnn_status mgnn_profile_stages(mgnn_ctx ctx, double* out, int32_t n_out) {
     GUARD();
     if (!out || n_out < MGNN_PROF_N) return fail(ctx, MGNN_EINVAL, "profile_stages: need MGNN_PROF_N doubles");
-    double ms[3];
-    long long n[3];
-    for (int st = 0; st < 3; ++st) {
+    double ms[4];
+    long long n[4];
+    for (int st = 0; st < 4; ++st) {
         mgnn_status r = drain_events(ctx, st, &ms[st], &n[st]);
         if (r) return r;
     }
@@ -1248,6 +1279,8 @@ mgnn_status mgnn_profile_stages(mgnn_ctx ctx, double* out, int32_t n_out) {
     out[MGNN_PROF_SCORE_CALLS] = (double)n[2];
     out[MGNN_PROF_HITS] = (double)su[3];
     out[MGNN_PROF_MISSES] = (double)su[4];
+    out[MGNN_PROF_RELABEL_MS] = ms[3];
+    out[MGNN_PROF_RELABEL_CALLS] = (double)n[3];
     return MGNN_OK;
 }
 

@@ -223,6 +223,7 @@ mgnn_status mgnn_sage_forward(mgnn_ctx ctx, int32_t slot, float* logits, int64_t
     if (logits_pitch < S.dims[S.L]) return fail(ctx, MGNN_EINVAL, "logits_pitch < dims[L]");
     Win& w = ctx->win[slot];
     if (!w.gathered) return fail(ctx, MGNN_ESTATE, "sage_forward needs a gathered window");
+    if (w.relabel_pending) return fail(ctx, MGNN_ESTATE, "sage_forward: the window's columns are not relabelled (mgnn_relabel)");
     cudaStream_t s = (cudaStream_t)stream;
     const int L = S.L;
     const int n_inst = (int)ctx->parts.size() * w.n_steps;
@@ -315,6 +316,7 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
     if (slot < 0 || slot > 1 || n_trainers < 1) return fail(ctx, MGNN_EINVAL, "bad slot / n_trainers");
     Win& w = ctx->win[slot];
     if (!w.gathered) return fail(ctx, MGNN_ESTATE, "train_step needs a gathered window");
+    if (w.relabel_pending) return fail(ctx, MGNN_ESTATE, "train_step: the window's columns are not relabelled (mgnn_relabel)");
     if (step_in_window < 0 || step_in_window >= w.n_steps) return fail(ctx, MGNN_EINVAL, "step_in_window");
     cudaStream_t s = (cudaStream_t)stream;
     const int L = S.L;

@@ -44,6 +44,7 @@ struct Part {
 struct Win {
     bool alloc = false, sampled = false, gathered = false, scored = false;
     bool x_user = false;            // X is a caller-owned buffer (mgnn_window_bind_x)
+    bool relabel_pending = false;   // sampled with the relabel deferred (mgnn_relabel not yet called)
     int32_t n_steps = 0;
     uint64_t step0 = 0;
     int32_t* fr_rank = nullptr;
@@ -167,6 +168,7 @@ struct mgnn_ctx_s {
         int64_t rows64 = 0, dh_rows[kMaxLayers] = {};
         alignas(64) unsigned char map_dz128[kMaxLayers][128], map_wt[kMaxLayers][128], map_mean128[kMaxLayers][128];
     } sage;
+    bool defer_relabel = false;          // mgnn_sample leaves the columns in rank space (mgnn_relabel)
     // ordering of windows through the buffer
     bool seq_started = false;
     uint64_t next_step = 0;
@@ -177,7 +179,7 @@ struct mgnn_ctx_s {
     bool prof = false;
     // event pairs per stage: 0 = sampler kernels (k_hop, k_compact, k_relabel) of mgnn_sample,
     // 1 = the gather launch of mgnn_lookup_gather, 2 = all of mgnn_score_evict_refill
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[3];
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[4];   // [3] = deferred k_relabel
     long long* d_sampled = nullptr;      // [5] sampled edges E, expanded frontier F, |F_L| U, hits, misses
 };
 

@@ -149,6 +149,13 @@ class Context:
                                                     C.c_void_p(counts_ptr), 1 if on_host else 0, _stream(stream)))
         self.n_steps[slot] = n_steps
 
+    def defer_relabel(self, enable: bool = True):
+        """mgnn_sampler_defer_relabel: mgnn_sample leaves the columns in rank space until relabel()."""
+        self._chk("mgnn_sampler_defer_relabel", self.L.mgnn_sampler_defer_relabel(self._h, 1 if enable else 0))
+
+    def relabel(self, slot: int, stream=None):
+        self._chk("mgnn_relabel", self.L.mgnn_relabel(self._h, slot, _stream(stream)))
+
     def lookup_gather(self, slot: int, stream=None):
         self._chk("mgnn_lookup_gather", self.L.mgnn_lookup_gather(self._h, slot, _stream(stream)))
 
@@ -317,7 +324,7 @@ class Context:
         out = np.zeros(_lib.PROF_N, np.float64)
         self._chk("mgnn_profile_stages", self.L.mgnn_profile_stages(self._h, _ptr(out), _lib.PROF_N))
         keys = ["sample_ms", "sample_calls", "edges", "frontier", "unique", "gather_ms", "gather_calls",
-                "gather_rows", "score_ms", "score_calls", "hits", "misses"]
+                "gather_rows", "score_ms", "score_calls", "hits", "misses", "relabel_ms", "relabel_calls"]
         return {k: float(out[i]) for i, k in enumerate(keys)}
 
     def profile_read(self):

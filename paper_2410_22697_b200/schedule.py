@@ -30,12 +30,16 @@ class PrepareAhead:
 
     def __init__(self, ctx, window: int, t0: int = 1, stream_b: Optional[torch.cuda.Stream] = None,
                  flush_bytes: int = 256 << 20,
-                 host_seeds: Optional[Callable[[int, int], Tuple[int, int]]] = None, serial: bool = False):
+                 host_seeds: Optional[Callable[[int, int], Tuple[int, int]]] = None, serial: bool = False,
+                 relabel_stream: bool = False):
         """window: steps per window (a window may end on an eviction step, never contain one earlier);
         t0: first global step (1-based, R#8); flush_bytes: L2 flush buffer written before every
         iteration (0 = none; B200 L2 is 126 MB); host_seeds(slot, t) -> (seeds_ptr, counts_ptr) of
         pinned host buffers makes mgnn_sample copy the window's seeds host -> device (the e2e path);
-        serial=True runs everything on stream B: consume(w), then sample(w+1) (no overlap)."""
+        serial=True runs everything on stream B: consume(w), then sample(w+1) (no overlap);
+        relabel_stream=True defers the columns' relabelling (mgnn_sampler_defer_relabel): window w's
+        k_relabel runs on a third stream C beside its gather (L2-bound beside HBM-bound) and stream B
+        joins C before the iteration ends, so the window's blocks are final when its end event fires."""
         self.ctx = ctx
         self.W = int(window)
         self.t = int(t0)
@@ -48,10 +52,16 @@ class PrepareAhead:
         self.flush = torch.empty(flush_bytes, dtype=torch.uint8, device=self.sB.device) if flush_bytes else None
         self.host_seeds = host_seeds
         self.primed = False
+        self.relabel_stream = relabel_stream and not serial
+        self.sC = torch.cuda.Stream(device=self.sB.device) if self.relabel_stream else None
+        self.ev_relabeled = [torch.cuda.Event(), torch.cuda.Event()]
+        ctx.defer_relabel(self.relabel_stream)
 
     # ---------------------------------------------------------------- the two halves
     def _sample(self, sl: int, tt: int) -> None:
         self.sA.wait_event(self.ev_done[sl])          # slot free once its previous window was consumed
+        if self.relabel_stream:
+            self.sA.wait_event(self.ev_relabeled[sl])
         if self.host_seeds is None:
             self.ctx.sample(sl, tt, self.W, stream=self.sA)
         else:
@@ -98,7 +108,13 @@ class PrepareAhead:
         else:
             if prepare_next:
                 self._sample(self.slot ^ 1, self.t + self.W)  # window w+1: sampling stream
+            if self.relabel_stream:                           # window w's blocks: third stream
+                self.sC.wait_event(self.ev_sampled[self.slot])
+                self.ctx.relabel(self.slot, self.sC)
+                self.ev_relabeled[self.slot].record(self.sC)
             self._consume(self.slot)                          # window w: buffer stream
+            if self.relabel_stream:
+                sB.wait_event(self.ev_relabeled[self.slot])
         consumed = (self.slot, self.t)
         if after_consume is not None:
             after_consume(self.slot, self.t, sB)

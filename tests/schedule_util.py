@@ -53,6 +53,10 @@ class _Perturbed:
         self._spin(stream)
         return self._c.lookup_gather(sl, stream)
 
+    def relabel(self, sl, stream=None):
+        self._spin(stream)
+        return self._c.relabel(sl, stream)
+
     def score(self, sl, stream=None):
         self._spin(stream)
         return self._c.score(sl, stream)
@@ -61,7 +65,7 @@ class _Perturbed:
 def run_schedule_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, gamma: float, delta: int,
                         window: int, n_windows: int, x_rows: int = 2048, warm: int = 0, flush_bytes: int = 256 << 20,
                         run_seed: int = synth.RUN_SEED, feat_seed: int = synth.FEAT_SEED, rows_bound: int = -1,
-                        perturb=None):
+                        perturb=None, relabel_stream: bool = False):
     import torch
     from paper_2410_22697_b200 import pipeline as PL
     from paper_2410_22697_b200.schedule import PrepareAhead
@@ -75,7 +79,8 @@ def run_schedule_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_b
     ctx.sampler_config(fanouts, batch, run_seed, window, rows_bound=rows_bound)
     L = len(fanouts)
     n_inst = P * window
-    pipe = PrepareAhead(ctx if perturb is None else _Perturbed(ctx, perturb), window, t0=1, flush_bytes=flush_bytes)
+    pipe = PrepareAhead(ctx if perturb is None else _Perturbed(ctx, perturb), window, t0=1, flush_bytes=flush_bytes,
+                        relabel_stream=relabel_stream)
     grabbed = []
     xpos_n = x_rows
 

@@ -46,12 +46,20 @@ def test_schedule_products_full_size_bench_config():
     assert st["evicted"] > 0 and st["misses"] > 0
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3])
-def test_schedule_perturbed_interleavings(seed):
-    """Race probe of the two-stream schedule: random spin kernels before every call shift how the
-    sampling stream and the buffer stream interleave; every run must still equal the oracle."""
+@pytest.mark.parametrize("seed,relabel_stream", [(1, False), (2, False), (3, False), (4, True), (5, True)])
+def test_schedule_perturbed_interleavings(seed, relabel_stream):
+    """Race probe of the schedule: random spin kernels before every call shift how the sampling
+    stream, the buffer stream (and the relabel stream) interleave; every run must equal the oracle."""
     g = synth.generate(synth.CONFIGS["cfg1"])
-    st = run_schedule_parity(g, 2, 64, [10, 25], 256, 2500, 0.9, 4, 4, 6, x_rows=1024, perturb=seed)
+    st = run_schedule_parity(g, 2, 64, [10, 25], 256, 2500, 0.9, 4, 4, 6, x_rows=1024, perturb=seed,
+                             relabel_stream=relabel_stream)
+    assert st["evicted"] > 0
+
+
+def test_schedule_relabel_stream_bench_window():
+    """The deferred relabel on a third stream (mgnn_relabel beside the gather) at the bench window."""
+    g = synth.generate(synth.CONFIGS["cfg1"])
+    st = run_schedule_parity(g, 2, 64, [10, 25], 256, 2500, 0.995, 64, 32, 4, x_rows=0, relabel_stream=True)
     assert st["evicted"] > 0
 
 

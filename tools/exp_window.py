@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--config", default="products")
     ap.add_argument("--windows", type=int, default=12)
     ap.add_argument("--serial", action="store_true")
+    ap.add_argument("--relabel-stream", action="store_true")
     ap.add_argument("--parts", type=int, default=None)
     ap.add_argument("--tag", default="")
     a = ap.parse_args()
@@ -33,7 +34,7 @@ def main():
     ctx = PL.build_context(0, parts, S.cfg.feat_dim, synth.FEAT_SEED)
     ctx.buffer_init(S.gamma, PL.alpha_default(S.gamma, S.delta), 1.0, S.delta, S.f_bp)
     ctx.sampler_config(S.cfg.fanouts, S.cfg.batch, synth.RUN_SEED, S.window)
-    pipe = PrepareAhead(ctx, S.window, serial=a.serial)
+    pipe = PrepareAhead(ctx, S.window, serial=a.serial, relabel_stream=a.relabel_stream)
     for _ in range(4):
         pipe.iteration()
     torch.cuda.synchronize()
@@ -49,7 +50,8 @@ def main():
     out = {"tag": a.tag, "config": a.config, "serial": a.serial, "env": {k: v for k, v in os.environ.items() if k.startswith("MGNN_")},
            "ms_median": ms[len(ms) // 2], "ms_min": ms[0], "mb_per_s": S.window * S.ppg / (ms[len(ms) // 2] / 1e3),
            "sample_ms": pr["sample_ms"] / n, "gather_ms": pr["gather_ms"] / max(pr["gather_calls"], 1),
-           "score_ms": pr["score_ms"] / max(pr["score_calls"], 1)}
+           "score_ms": pr["score_ms"] / max(pr["score_calls"], 1),
+           "relabel_ms": pr["relabel_ms"] / max(pr["relabel_calls"], 1), "relabel_stream": a.relabel_stream}
     print(json.dumps(out), flush=True)
     ctx.close()
 
