@@ -33,7 +33,8 @@ def test_schedule_arxiv_full_size_bench_config():
     """configs[1] at full size in the bench's configuration: P = 2 on one GPU, 32-step windows,
     f = 0.25, gamma = 0.995, Delta = 32 (every window ends in an eviction round)."""
     g = synth.generate(synth.CONFIGS["arxiv"])
-    st = run_schedule_parity(g, 2, 128, [10, 25], 1000, 2500, 0.995, 32, 32, 6, x_rows=0)   # every X row
+    st = run_schedule_parity(g, 2, 128, [10, 25], 1000, 2500, 0.995, 32, 32, 6, x_rows=0,    # every X row
+                             relabel_stream=True)                                       # as bench.py
     assert st["evicted"] > 0
 
 
@@ -42,7 +43,8 @@ def test_schedule_products_full_size_bench_config():
     """configs[3] (the bench default) at full size in the bench's configuration: P = 2 on one GPU,
     32-step windows, f = 0.5, gamma = 0.995, Delta = 32, 3 hops [5, 10, 15], batch 2000."""
     g = synth.generate(synth.CONFIGS["products"])
-    st = run_schedule_parity(g, 2, 100, [5, 10, 15], 2000, 5000, 0.995, 32, 32, 4, x_rows=0)   # every X row
+    st = run_schedule_parity(g, 2, 100, [5, 10, 15], 2000, 5000, 0.995, 32, 32, 4, x_rows=0,  # every X row
+                             relabel_stream=True)                                         # as bench.py
     assert st["evicted"] > 0 and st["misses"] > 0
 
 
