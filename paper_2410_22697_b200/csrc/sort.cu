@@ -155,11 +155,14 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_count(const SortSeg* __re
     }
 }
 
+// Stable local ranks with two block barriers per tile: warp w owns the contiguous items
+// [w * 256, (w + 1) * 256) of the tile (8 rounds of 32), ranks them inside the warp against a
+// warp-private digit counter row (match_any + __syncwarp only), then one pass over (digit, warp)
+// turns the per-warp counts into each warp's offset inside the tile's digit run.
 __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const SortSeg* __restrict__ segs, int passes, int p,
                                                                int64_t tiles_max, SortScr scr) {
     pdl_enter();
-    __shared__ uint32_t run[kRadix];       // per-digit running count inside the tile
-    __shared__ uint32_t wc[8][kRadix];     // per-warp digit counts of the current round
+    __shared__ uint32_t wc[8][kRadix];     // per-warp digit counts, then the warp's offset in the digit run
     __shared__ uint32_t gofs[kRadix];      // global offset of the tile's first item of each digit
     const int s = blockIdx.y;
     const SortSeg sg = segs[s];
@@ -175,7 +178,17 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const SortSeg* __
     const unsigned lt = (1u << lane) - 1u;
     const int shift = sg.shift[p];
     const uint32_t* tc = scr.status + ((size_t)(s * passes + p) * tiles_max) * kRadix;
+    constexpr int kPerWarp = kSortTile / 8;    // 256 items per warp
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t base = tile * kSortTile + (int64_t)warp * kPerWarp;
+        unsigned long long key[kSortItems];
+        uint32_t val[kSortItems], rank[kSortItems];
+#pragma unroll
+        for (int i = 0; i < kSortItems; ++i) {         // every load of the tile in flight at once
+            const int64_t idx = base + i * 32 + lane;
+            key[i] = idx < n ? kin[idx] : 0ull;
+            val[i] = idx < n ? vin[idx] : 0u;
+        }
         {   // thread d: exclusive prefix of digit d over the earlier tiles (independent loads)
             const int d = threadIdx.x;
             uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
@@ -188,49 +201,37 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const SortSeg* __
             }
             for (; j < tile; ++j) a0 += tc[(size_t)j * kRadix + d];
             gofs[d] = scr.bins[(size_t)(s * passes + p) * kRadix + d] + a0 + a1 + a2 + a3;
-            run[d] = 0;
-            for (int w = 0; w < 8; ++w) wc[w][d] = 0;
         }
-        __syncthreads();
-        const int64_t base = tile * kSortTile;
-        unsigned long long key[kSortItems];
-        uint32_t val[kSortItems], rank[kSortItems];
-#pragma unroll
-        for (int i = 0; i < kSortItems; ++i) {         // every load of the tile in flight at once
-            const int64_t idx = base + (int64_t)i * kSortThreads + threadIdx.x;
-            key[i] = idx < n ? kin[idx] : 0ull;
-            val[i] = idx < n ? vin[idx] : 0u;
-        }
+        for (int d = lane; d < kRadix; d += 32) wc[warp][d] = 0;     // the warp's own counter row
+        __syncwarp();
 #pragma unroll
         for (int i = 0; i < kSortItems; ++i) {
-            const int64_t idx = base + (int64_t)i * kSortThreads + threadIdx.x;
-            const bool valid = idx < n;
+            const bool valid = base + i * 32 + lane < n;
             const unsigned digit = valid ? ((unsigned)(key[i] >> shift) & 0xFF) : (0x100u | lane);
             const unsigned peers = __match_any_sync(kFull, digit);
             const unsigned r = __popc(peers & lt);
-            if (valid && r == 0) wc[warp][digit] = __popc(peers);
-            __syncthreads();
-            {   // per digit: exclusive prefix over warps of this round, advance the tile-local count
-                uint32_t acc = run[threadIdx.x];
-#pragma unroll
-                for (int w = 0; w < 8; ++w) {
-                    const uint32_t c = wc[w][threadIdx.x];
-                    wc[w][threadIdx.x] = acc;
-                    acc += c;
-                }
-                run[threadIdx.x] = acc;
-            }
-            __syncthreads();
-            rank[i] = valid ? wc[warp][digit] + r : 0xFFFFFFFFu;
-            __syncthreads();
-            for (int w = 0; w < 8; ++w) wc[w][threadIdx.x] = 0;
-            __syncthreads();
+            rank[i] = valid ? wc[warp][digit & 0xFF] + r : 0xFFFFFFFFu;
+            __syncwarp();
+            if (valid && r == 0) wc[warp][digit] += __popc(peers);
+            __syncwarp();
         }
+        __syncthreads();
+        {   // thread d: each warp's offset inside the tile's run of digit d
+            const int d = threadIdx.x;
+            uint32_t acc = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                const uint32_t c = wc[w][d];
+                wc[w][d] = acc;
+                acc += c;
+            }
+        }
+        __syncthreads();
 #pragma unroll
         for (int i = 0; i < kSortItems; ++i) {
             if (rank[i] == 0xFFFFFFFFu) continue;
             const unsigned digit = (unsigned)(key[i] >> shift) & 0xFF;
-            const uint32_t pos = gofs[digit] + rank[i];
+            const uint32_t pos = gofs[digit] + wc[warp][digit] + rank[i];
             MGNN_CHECK(pos < n, "scatter pos=%u n=%lld seg=%d", pos, (long long)n, s);
             kout[pos] = key[i];
             vout[pos] = val[i];
