@@ -43,7 +43,8 @@ constexpr int kRelabelBatch = 4;       // column lookups in flight per k_relabel
 constexpr int kColBatch = MGNN_COL_BATCH;           // neighbour-rank loads in flight per k_hop thread
 constexpr int kWordTile = kThreads * kCWords;   // bitmap words per k_compact tile
 
-int64_t scan_tiles_count(int64_t fcap) { return (fcap + kHopTileMin - 1) / kHopTileMin; }
+// + kMaxLayers + 1: segment-aligned tiles (k_hop align) may leave one partial tile per segment
+int64_t scan_tiles_count(int64_t fcap) { return (fcap + kHopTileMin - 1) / kHopTileMin + kMaxLayers + 1; }
 int64_t scan_tiles_words(int64_t words) { return (words + kWordTile - 1) / kWordTile; }
 
 static inline unsigned grid_x_for(int64_t items_per_inst, int items_per_block, int n_inst) {
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
 // neighbours' ranks, write the columns (coalesced) and mark new nodes.
 template <typename IdxT>   // CSR index staged per sample: uint32_t when every index fits (halves the tile)
 __global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max, int T,
-                                                                     int mark_filter) {
+                                                                     int mark_filter, int align) {
     pdl_enter();
     __shared__ long long sm[8];
     __shared__ int tslot, n_draw;
@@ -134,8 +135,32 @@ __global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int
     const int m = blockIdx.y;
     const int lp = m / W.n_steps, w = m % W.n_steps;
     const PartDev& pd = W.parts[lp];
-    const int64_t nF = W.hop_size[(int64_t)m * (kMaxLayers + 1) + hop];
-    const int64_t ntiles = (nF + T - 1) / T;
+    const int64_t* hsm = W.hop_size + (int64_t)m * (kMaxLayers + 1);
+    const int64_t nF = hsm[hop];
+    // align != 0: segment-aligned tiles.  F_hop = F_0 ++ new_0 ++ ... ++ new_{hop-1}, each segment in rank
+    // order (R#7); tile c of segment s covers the fraction [c, c+1) / C_s of that segment in EVERY
+    // instance (C_s = ceil(longest segment s of the window / T)), so the instances, whose blocks claim
+    // their tiles in step, sample the same rank region -- the same CSR rows -- at the same time (L2
+    // reuse of rows that several minibatches of the window expand).  Tiles stay contiguous and in
+    // frontier order, as the decoupled look-back requires.
+    __shared__ long long seg_c[kMaxLayers + 2];
+    int64_t ntiles = (nF + T - 1) / T;
+    if (align) {
+        if (threadIdx.x < kMaxLayers + 2) seg_c[threadIdx.x] = 0;
+        __syncthreads();
+        for (int mi = threadIdx.x; mi < W.n_inst; mi += blockDim.x) {
+            const int64_t* hsi = W.hop_size + (int64_t)mi * (kMaxLayers + 1);
+            for (int sgi = 0; sgi <= hop; ++sgi) {
+                const long long len = sgi == 0 ? hsi[0] : hsi[sgi] - hsi[sgi - 1];
+                atomicMax(&seg_c[sgi + 1], (len + T - 1) / T);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int sgi = 1; sgi <= hop + 1; ++sgi) seg_c[sgi] += seg_c[sgi - 1];
+        __syncthreads();
+        ntiles = seg_c[hop + 1];
+    }
     int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
     const int k = W.k_hop[hop];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -153,8 +178,16 @@ __global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int
             if (tile == 0 && threadIdx.x == 0) off[0] = 0;   // empty F_i
             break;
         }
-        const int64_t f = (int64_t)tile * T + threadIdx.x;
-        const bool mine = threadIdx.x < T && f < nF;
+        int64_t f = (int64_t)tile * T + threadIdx.x, f_end = nF;
+        if (align) {                                       // the tile's slice of its segment
+            int sgi = 0;
+            while (tile >= seg_c[sgi + 1]) ++sgi;
+            const int64_t c = tile - seg_c[sgi], C = seg_c[sgi + 1] - seg_c[sgi];
+            const int64_t s0 = sgi == 0 ? 0 : hsm[sgi - 1], len = sgi == 0 ? hsm[0] : hsm[sgi] - hsm[sgi - 1];
+            f = s0 + c * len / C + threadIdx.x;
+            f_end = s0 + (c + 1) * len / C;
+        }
+        const bool mine = threadIdx.x < T && f < f_end;
         int64_t row = -1, b0 = 0, d = 0;
         if (mine) {
             const int64_t r = W.fr_rank[(int64_t)m * W.ucap + f];
@@ -438,14 +471,20 @@ void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t
     ensure_smem_k(k_hop<uint32_t>, 256 * MGNN_MAX_FANOUT * 4);
     const int64_t tm = tiles_max < 1 ? 1 : tiles_max;
     const char* f64 = getenv("MGNN_SAMPLE_IDX64");   // tests: force the 64-bit staging variant
+    static const int align = [] {                    // 1: segment-aligned tiles across the window's instances
+        const char* e = getenv("MGNN_HOP_ALIGN");
+        return e ? atoi(e) : 0;
+    }();
     static const int mark_filter = [] {              // 1: load the membership word before marking
         const char* e = getenv("MGNN_MARK_FILTER");  // (measured: products sampling 0.79 ms with 0,
         return e ? atoi(e) : 0;                      // 0.82 ms with 1; arxiv equal)
     }();
     if (w.idx32 && !(f64 && f64[0] == '1'))
-        launch_k(k_hop<uint32_t>, grid, dim3(kThreads), (size_t)T * w.k_hop[hop] * 4, s, w, hop, sc, tm, T, mark_filter);
+        launch_k(k_hop<uint32_t>, grid, dim3(kThreads), (size_t)T * w.k_hop[hop] * 4, s, w, hop, sc, tm, T, mark_filter,
+                 align);
     else
-        launch_k(k_hop<uint64_t>, grid, dim3(kThreads), (size_t)T * w.k_hop[hop] * 8, s, w, hop, sc, tm, T, mark_filter);
+        launch_k(k_hop<uint64_t>, grid, dim3(kThreads), (size_t)T * w.k_hop[hop] * 8, s, w, hop, sc, tm, T, mark_filter,
+                 align);
     count_launches(1, __func__, s);
 }
 
