@@ -233,9 +233,32 @@ def nvlink_counters(index: int):
                 tx += int(vv[0].value.ullVal)
                 rx += int(vv[1].value.ullVal)
                 ok = True
-        return [tx, rx, "NVLINK_COUNT_XMIT/RCV_BYTES summed over links"] if ok else None
+        if ok:
+            return [tx, rx, "NVLINK_COUNT_XMIT/RCV_BYTES summed over links"]
+        return nvidia_smi_nvlink(nv.nvmlDeviceGetIndex(h))
     except Exception:
         return None
+
+
+def nvidia_smi_nvlink(nvml_index: int):
+    """`nvidia-smi nvlink -gt d -i N`: per-link data Tx / Rx counters (KiB), summed; None if unavailable."""
+    import re
+    try:
+        out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(nvml_index)], capture_output=True,
+                             text=True, timeout=20).stdout
+    except Exception:
+        return None
+    tx = rx = 0
+    found = False
+    for line in out.splitlines():
+        m = re.search(r"(Tx|Rx)\s*:?\s*([0-9]+)\s*KiB", line)
+        if m:
+            found = True
+            if m.group(1) == "Tx":
+                tx += int(m.group(2)) * 1024
+            else:
+                rx += int(m.group(2)) * 1024
+    return [tx, rx, "nvidia-smi nvlink -gt d (KiB per link, summed)"] if found else None
 
 
 def traffic_table(name: str):
