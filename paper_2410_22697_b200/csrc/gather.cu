@@ -313,23 +313,19 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
     int chunk_rows = R;
     auto claim = [&](int& cm, int64_t& f0) -> bool {
         if (dyn == 2) {
-            // one chunk index space over (segment, fraction, instance), instances innermost: the grid is
-            // 1-D (every block serves every instance), so the work splits evenly over the whole grid
+            const int64_t* hsm = W.hop_size + (int64_t)m * (kMaxLayers + 1);
             for (;;) {
                 const int64_t j = next_static;
                 next_static += (int64_t)gridDim.x * kTWarps;
-                if (j >= seg_c[W.L + 1] * W.n_inst) return false;
+                if (j >= seg_c[W.L + 1]) return false;
                 int sgi = 0;
-                while (j >= seg_c[sgi + 1] * W.n_inst) ++sgi;
-                const int64_t q = j - seg_c[sgi] * W.n_inst;
-                const int mi = (int)(q % W.n_inst);
-                const int64_t c = q / W.n_inst, C = seg_c[sgi + 1] - seg_c[sgi];
-                const int64_t* hsm = W.hop_size + (int64_t)mi * (kMaxLayers + 1);
+                while (j >= seg_c[sgi + 1]) ++sgi;
+                const int64_t c = j - seg_c[sgi], C = seg_c[sgi + 1] - seg_c[sgi];
                 const int64_t s0 = sgi == 0 ? 0 : hsm[sgi - 1], len = sgi == 0 ? hsm[0] : hsm[sgi] - hsm[sgi - 1];
                 const int64_t a = s0 + c * len / C, b = s0 + (c + 1) * len / C;
-                if (sgi == 0 && c == 0 && lane == 0) W.counts[(int64_t)mi * 8] = hsm[W.L];
+                if (j == 0 && lane == 0) W.counts[(int64_t)m * 8] = hsm[W.L];
                 if (b <= a) continue;
-                cm = mi;
+                cm = m;
                 f0 = a;
                 chunk_rows = (int)(b - a);
                 return true;
@@ -667,11 +663,7 @@ void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, con
             const char* e = getenv("MGNN_GATHER_DYN");
             return e ? atoi(e) : 2;
         }();
-        // aligned chunks (dyn 2) use a 1-D grid of exactly one wave (bps blocks per SM) over all instances
-        const dim3 grid = dyn == 2 ? dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * bps,
-                                                                                       nd * w.n_inst)))
-                                   : dim3(gxt, w.n_inst);
-        launch_k(k_gather_tma, grid, dim3(kTWarps * 32), smem, s, w, world, R, stage, hint, dyn);
+        launch_k(k_gather_tma, dim3(gxt, w.n_inst), dim3(kTWarps * 32), smem, s, w, world, R, stage, hint, dyn);
     } else {
         dim3 grid(gx, w.n_inst);
         if (w.pitch >= 128)
