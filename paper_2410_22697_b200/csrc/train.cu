@@ -136,7 +136,8 @@ constexpr int kWRegion = 128 * 128;              // 128 operand rows x 32 K valu
 constexpr int kWStage = 4 * kWRegion;            // A and B, 2 K-regions each: 64 KB
 constexpr int kWMaxInst = 256;
 
-__global__ void __launch_bounds__(128, 1) k_wgrad(WgradArgs a) {
+constexpr int kWThreads = 512;                    // 4 threads per operand row: 4x the loads in flight
+__global__ void __launch_bounds__(kWThreads, 1) k_wgrad(WgradArgs a) {
     extern __shared__ __align__(1024) unsigned char dsm[];
     __shared__ __align__(8) uint64_t bar_empty[2], bar_done;
     __shared__ uint32_t tmem_sh;
@@ -202,14 +203,15 @@ __global__ void __launch_bounds__(128, 1) k_wgrad(WgradArgs a) {
         if (i >= 2) mb_wait(&bar_empty[st], ((i >> 1) - 1) & 1);   // MMAs of chunk c-2 read this stage
         unsigned char* sa = base + st * kWStage;
         unsigned char* sb = sa + 2 * kWRegion;
-        // thread = (operand row x = threadIdx.x, i.e. o or c within the tile); 4 K rows per float4
-        const int x = threadIdx.x;
+        // thread = (operand row x, quarter q of the chunk's K rows); 4 K rows per float4
+        const int x = threadIdx.x & 127, q = threadIdx.x >> 7;
         const int o = mt * 128 + x, cc = col0 + x;
         const float* pa = a.dz + ((int64_t)m * a.dz_rows + r0) * a.dz_pitch + o;
         const float* pb = src_b + ((int64_t)m * b_rows + r0) * b_pitch + cc;
         const bool oka = o < a.npad, okb = cc < b_cols;
-#pragma unroll 4
-        for (int k4 = 0; k4 < kWRows / 4; ++k4) {
+        constexpr int kQ = kWRows / 4 / (kWThreads / 128);    // K groups of 4 per thread
+#pragma unroll
+        for (int k4 = q * kQ; k4 < (q + 1) * kQ; ++k4) {
             float va[4], vb[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(128, 1) k_wgrad(WgradArgs a) {
             mma_commit(&bar_empty[st]);
         }
     }
-    if (c_lo < c_hi) {
+    if (c_lo < c_hi && warp < 4) {                   // TMEM lanes 0-127: warps 0-3 drain the accumulator
         if (threadIdx.x == 0) mma_commit(&bar_done);
         __syncwarp();
         mb_wait(&bar_done, 0);
@@ -534,7 +536,7 @@ bool launch_wgrad(const WgradArgs& a_in, cudaStream_t s) {
     // split-K over every SM (measured: fewer CTAs with >= 8 chunks each was slower, 16 -> 26 us; the
     // chunk loads are latency-bound, the partial-tile atomics are not)
     a.ksplit = std::max(1, sms / tiles);
-    launch_k(k_wgrad, dim3(tiles * a.ksplit), dim3(128), smem, s, a);
+    launch_k(k_wgrad, dim3(tiles * a.ksplit), dim3(kWThreads), smem, s, a);
     count_launches(1, __func__, s);
     return true;
 }
