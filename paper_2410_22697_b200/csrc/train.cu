@@ -136,7 +136,7 @@ constexpr int kWRegion = 128 * 128;              // 128 operand rows x 32 K valu
 constexpr int kWStage = 4 * kWRegion;            // A and B, 2 K-regions each: 64 KB
 constexpr int kWMaxInst = 256;
 
-constexpr int kWThreads = 512;                    // 4 threads per operand row: 4x the loads in flight
+constexpr int kWThreads = 1024;                   // 8 threads per operand row: 8x the loads in flight
 __global__ void __launch_bounds__(kWThreads, 1) k_wgrad(WgradArgs a) {
     extern __shared__ __align__(1024) unsigned char dsm[];
     __shared__ __align__(8) uint64_t bar_empty[2], bar_done;
@@ -512,16 +512,23 @@ void launch_xent(const XentArgs& a, cudaStream_t s) {
     count_launches(1, __func__, s);
 }
 
+// blocks per instance so the whole launch fills every SM (~8 resident 256-thread blocks per SM) even
+// when a training step has only its 2-8 instances, capped by the work
+static unsigned fill_x(int64_t work_blocks, int n_inst) {
+    const int64_t target = ((int64_t)num_sms() * 8 + n_inst - 1) / n_inst;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(work_blocks, std::max<int64_t>(target, 1)));
+}
+
 void launch_relu_mask(const MaskArgs& a, cudaStream_t s) {
     const int64_t work = ((a.rows + 63) / 64 * 64) * (a.ncols / 4);
-    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + kT - 1) / kT, 256));
+    const unsigned gx = fill_x((work + kT - 1) / kT, a.n_inst);
     launch_k(k_relu_mask, dim3(gx, a.n_inst), dim3(kT), 0, s, a);
     count_launches(1, __func__, s);
 }
 
 void launch_zero_rows(const ZeroRowsArgs& a, cudaStream_t s) {
     const int64_t work = a.rows * (a.pitch / 4);
-    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + kT - 1) / kT, 256));
+    const unsigned gx = fill_x((work + kT - 1) / kT, a.n_inst);
     launch_k(k_zero_rows, dim3(gx, a.n_inst), dim3(kT), 0, s, a);
     count_launches(1, __func__, s);
 }
@@ -554,12 +561,14 @@ bool launch_dgrad(const void* map_dz, const void* map_wt, const DgradArgs& a, cu
 }
 
 void launch_scatter(const DgradArgs& a, cudaStream_t s) {
-    launch_k(k_scatter, dim3(64, a.n_inst), dim3(kT), 0, s, a);
+    launch_k(k_scatter, dim3(fill_x((a.dz_rows + 7) / 8, a.n_inst), a.n_inst), dim3(kT), 0, s, a);
     count_launches(1, __func__, s);
 }
 
 void launch_mean(const SageLayerArgs& a, cudaStream_t s) {
-    launch_k(k_mean, dim3(128, a.n_inst), dim3(kT), 0, s, a);
+    // warp per dst row: enough blocks that every SM keeps ~8 of them (the training step's forward has
+    // only 2-8 instances; 128 blocks per instance left ~14 warps per SM and 1.7 TB/s on products)
+    launch_k(k_mean, dim3(std::max(128u, fill_x((a.out_rows + 7) / 8, a.n_inst)), a.n_inst), dim3(kT), 0, s, a);
     count_launches(1, __func__, s);
 }
 
