@@ -190,40 +190,51 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wgrad(WgradArgs a) {
     const int b_cols = neigh ? a.mean_cols : a.in_cols;  // columns carrying data
     // K-major tf32, M = 128, N = 128
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
-    for (int c = c_lo; c < c_hi; ++c) {
-        const int i = c - c_lo, st = i & 1;
-        int lo = 0, hi = a.n_inst;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (pref[mid] <= c) lo = mid; else hi = mid;
-        }
+    // thread = (operand row x, rows q*8 .. q*8+7 of the chunk).  Chunk c+1's loads are issued before
+    // chunk c's transposed stores (ping-pong registers, no copies), so they are in flight across the
+    // barrier and the MMA issue; a full chunk loads without per-row predicates (ncu: the round-1 loop
+    // spent ~400 instructions per thread per chunk on 64-bit row addressing and a per-chunk search).
+    const int x = threadIdx.x & 127, q = threadIdx.x >> 7;
+    constexpr int kQ = kWRows / 4 / (kWThreads / 128);    // K groups of 4 per thread
+    constexpr int kR = kQ * 4;                            // rows per thread
+    const int o_row = mt * 128 + x, cc = col0 + x;
+    const bool oka = o_row < a.npad, okb = cc < b_cols;
+    const int sa_p = (int)a.dz_pitch, sb_p = (int)b_pitch;
+    int lo = 0;                                           // instance of the chunk (chunks ascend)
+    auto load_chunk = [&](int c, float (&va)[kQ][4], float (&vb)[kQ][4]) {
+        while (lo + 1 < a.n_inst && pref[lo + 1] <= c) ++lo;
         const int m = inst_of(lo, a.inst0, a.inst_step);
-        const int64_t r0 = (int64_t)(c - pref[lo]) * kWRows;
-        const int64_t n_rows = a.hop_size[(int64_t)m * (kMaxLayers + 1) + a.hop] - r0;
+        const int64_t r0 = (int64_t)(c - pref[lo]) * kWRows + q * kR;
+        const int nk = (int)min(a.hop_size[(int64_t)m * (kMaxLayers + 1) + a.hop] - r0, (int64_t)kR);
+        const float* pa = a.dz + ((int64_t)m * a.dz_rows + r0) * a.dz_pitch + o_row;
+        const float* pb = src_b + ((int64_t)m * b_rows + r0) * b_pitch + cc;
+        if (nk >= kR) {
+#pragma unroll
+            for (int j = 0; j < kR; ++j) {
+                va[j >> 2][j & 3] = oka ? __ldg(pa + j * sa_p) : 0.0f;
+                vb[j >> 2][j & 3] = okb ? __ldg(pb + j * sb_p) : 0.0f;
+            }
+        } else {                                          // the instance's last chunk: rows past |F_h| are 0
+#pragma unroll
+            for (int j = 0; j < kR; ++j) {
+                va[j >> 2][j & 3] = (oka && j < nk) ? __ldg(pa + j * sa_p) : 0.0f;
+                vb[j >> 2][j & 3] = (okb && j < nk) ? __ldg(pb + j * sb_p) : 0.0f;
+            }
+        }
+    };
+    auto step = [&](int c, float (&ca)[kQ][4], float (&cb)[kQ][4], float (&na)[kQ][4], float (&nb)[kQ][4]) {
+        const int i = c - c_lo, st = i & 1;
         if (i >= 2) mb_wait(&bar_empty[st], ((i >> 1) - 1) & 1);   // MMAs of chunk c-2 read this stage
+        if (c + 1 < c_hi) load_chunk(c + 1, na, nb);
         unsigned char* sa = base + st * kWStage;
         unsigned char* sb = sa + 2 * kWRegion;
-        // thread = (operand row x, quarter q of the chunk's K rows); 4 K rows per float4
-        const int x = threadIdx.x & 127, q = threadIdx.x >> 7;
-        const int o = mt * 128 + x, cc = col0 + x;
-        const float* pa = a.dz + ((int64_t)m * a.dz_rows + r0) * a.dz_pitch + o;
-        const float* pb = src_b + ((int64_t)m * b_rows + r0) * b_pitch + cc;
-        const bool oka = o < a.npad, okb = cc < b_cols;
-        constexpr int kQ = kWRows / 4 / (kWThreads / 128);    // K groups of 4 per thread
 #pragma unroll
-        for (int k4 = q * kQ; k4 < (q + 1) * kQ; ++k4) {
-            float va[4], vb[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int k = k4 * 4 + e;
-                const bool rk = k < n_rows;
-                va[e] = (oka && rk) ? __ldg(pa + (int64_t)k * a.dz_pitch) : 0.0f;
-                vb[e] = (okb && rk) ? __ldg(pb + (int64_t)k * b_pitch) : 0.0f;
-            }
+        for (int g = 0; g < kQ; ++g) {
+            const int k4 = q * kQ + g;
             const int reg = k4 >> 3, u = k4 & 7;            // 32 K values per region, 8 units of 4
             const uint32_t off = (uint32_t)(reg * kWRegion + x * 128 + ((u ^ (x & 7)) << 4));
-            *reinterpret_cast<float4*>(sa + off) = make_float4(va[0], va[1], va[2], va[3]);
-            *reinterpret_cast<float4*>(sb + off) = make_float4(vb[0], vb[1], vb[2], vb[3]);
+            *reinterpret_cast<float4*>(sa + off) = make_float4(ca[g][0], ca[g][1], ca[g][2], ca[g][3]);
+            *reinterpret_cast<float4*>(sb + off) = make_float4(cb[g][0], cb[g][1], cb[g][2], cb[g][3]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
@@ -238,6 +249,12 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wgrad(WgradArgs a) {
             }
             mma_commit(&bar_empty[st]);
         }
+    };
+    float ra[2][kQ][4], rb[2][kQ][4];
+    if (c_lo < c_hi) load_chunk(c_lo, ra[0], rb[0]);
+    for (int c = c_lo; c < c_hi; c += 2) {
+        step(c, ra[0], rb[0], ra[1], rb[1]);
+        if (c + 1 < c_hi) step(c + 1, ra[1], rb[1], ra[0], rb[0]);
     }
     if (c_lo < c_hi && warp < 4) {                   // TMEM lanes 0-127: warps 0-3 drain the accumulator
         if (threadIdx.x == 0) mma_commit(&bar_done);
