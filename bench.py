@@ -408,6 +408,8 @@ def main():
     ap.add_argument("--window", type=int, default=None, help="steps per window (default per config)")
     ap.add_argument("--static-arenas", action="store_true",
                     help="size window arenas for the static worst case instead of a pilot-measured bound")
+    ap.add_argument("--sm-split", type=int, default=0,
+                    help="mgnn_sm_partition: gather + scoring on this many SMs, sampling on the rest (0 = whole GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-extras", action="store_true", help="skip the with_consumer / with_training lines")
@@ -479,6 +481,7 @@ def main():
         dist.all_reduce(rb, op=dist.ReduceOp.MAX)
         rows_bound = int(rb.item())
     ctx.sampler_config(cfg.fanouts, cfg.batch, synth.RUN_SEED, WINDOW, rows_bound=rows_bound)
+    sm_split = ctx.sm_partition(args.sm_split) if args.sm_split else None
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -641,6 +644,8 @@ def main():
             "config": dict(S.workload(), **({"sampling": "remote expansion (NEXT-1)"} if args.remote else {}),
                            **({"scores": "dense S_A (NEXT-1)"} if args.dense else {}),
                            **({"partitioner": "hash (random relabel)"} if args.hash_partition else {}),
+                           **({"sm_partition": {"gather_sms": sm_split[0], "prepare_sms": sm_split[1]}}
+                              if sm_split else {}),
                            graph_stats=synth.describe(g, parts)),
             "runs": [r_["value"] for r_ in runs], "median_of": R,
             "buffer_init_ms": init_ms,

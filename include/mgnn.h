@@ -264,6 +264,18 @@ MGNN_API mgnn_status mgnn_sage_params(mgnn_ctx ctx, int32_t l, float* w_self, fl
 /* Device view of a window slot (valid after mgnn_sample of that slot). */
 MGNN_API mgnn_status mgnn_window_get(mgnn_ctx ctx, int32_t slot, mgnn_window* out);
 
+/* SM partition of the prepare-ahead pipeline (Alg.1 l.5-9; the overlap of Eq.4-5,
+ * P:245-251).  gather_sms > 0 splits the device's SMs into two green contexts: gather_sms SMs
+ * (rounded by the driver's split granularity) run mgnn_lookup_gather and mgnn_score_evict_refill,
+ * the remaining SMs run mgnn_sample and mgnn_relabel; gather_sms = 0 removes the partition (every
+ * call runs on the whole GPU, the default).  Each call still takes the caller's stream: its kernels
+ * start after the work queued there and the stream continues after them (an event hand-off to and
+ * from an internal stream of the partition), so results and ordering are unchanged -- only where
+ * the kernels run.  The consumer and training calls always use the whole GPU.  sms_out (may be
+ * NULL) receives the SM counts of [gather side, prepare side] (0, 0 when off).  Synchronises the
+ * device.  EINVAL: gather_sms < 0 or not below the SM count; ECUDA: green contexts unavailable. */
+MGNN_API mgnn_status mgnn_sm_partition(mgnn_ctx ctx, int32_t gather_sms, int32_t* sms_out);
+
 /* Deferred relabelling: with enable != 0, mgnn_sample stops after the last compaction and leaves
  * every hop's columns as LOCAL RANKS; mgnn_relabel(slot) then rewrites them as positions in
  * F_{i+1} (the DGL block layout of mgnn_window) on the given stream.  The gather does not read the

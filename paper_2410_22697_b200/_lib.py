@@ -24,7 +24,7 @@ SYMBOLS = [
     "mgnn_profile_enable", "mgnn_profile_read", "mgnn_profile_stages", "mgnn_profile_kernels",
     "mgnn_sage_config", "mgnn_sage_forward", "mgnn_sage_train_config", "mgnn_sage_train_step",
     "mgnn_sage_grads", "mgnn_sage_sgd", "mgnn_sage_loss", "mgnn_sage_params", "mgnn_sampler_expand_remote",
-    "mgnn_graph_csr_load", "mgnn_ctx_set_dense_scores",
+    "mgnn_graph_csr_load", "mgnn_ctx_set_dense_scores", "mgnn_sm_partition",
 ]
 
 
@@ -97,6 +97,7 @@ def load(path: str = LIB_PATH):
         "mgnn_window_shape": (S, [P, P, P, P]),
         "mgnn_sampler_defer_relabel": (S, [P, I32]),
         "mgnn_relabel": (S, [P, I32, P]),
+        "mgnn_sm_partition": (S, [P, I32, P]),
         "mgnn_window_bind_x": (S, [P, I32, P, I64]),
         "mgnn_profile_enable": (S, [P, I32]),
         "mgnn_profile_read": (S, [P, P, P, P]),

@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libmgnn.so")
 LIB_CHECKED = os.path.join(HERE, "libmgnn_checked.so")
-UNITS = ["api.cu", "api_sage.cu", "sample.cu", "gather.cu", "score.cu", "sort.cu", "load.cu", "sage.cu", "train.cu"]
+UNITS = ["api.cu", "api_sage.cu", "partition.cu", "sample.cu", "gather.cu", "score.cu", "sort.cu", "load.cu", "sage.cu", "train.cu"]
 HEADERS = ["common.cuh", "launch.h", "umma.cuh", "ctx.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 EXTRA = os.environ.get("MGNN_NVCC_EXTRA", "").split()

@@ -51,7 +51,9 @@ void count_launches(long long n, const char* who, cudaStream_t s) {
 }
 long long launches_total() { return g_launches.load(); }
 
+extern thread_local int t_sm_limit;          // partition.cu: set while a call runs on an SM partition
 int num_sms() {
+    if (t_sm_limit > 0) return t_sm_limit;
     static std::atomic<int> cache[64];            // 0 = not yet queried
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return 148;
@@ -316,6 +318,7 @@ void mgnn_destroy(mgnn_ctx ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
+    partition_free(ctx);
     for (auto& w : ctx->win) free_win(w);
     free_sage(ctx);
     for (auto& p : ctx->parts) {
@@ -889,7 +892,9 @@ mgnn_status mgnn_sample(mgnn_ctx ctx, int32_t slot, uint64_t t0, int32_t n_steps
     if (!seeds)
         for (auto& p : ctx->parts)
             if (p.n_train < 1) return fail(ctx, MGNN_EINVAL, "partition without train ids needs external seeds");
-    cudaStream_t s = (cudaStream_t)stream;
+    PartScope ps(ctx, 0, (cudaStream_t)stream);
+    if (ps.err) return fail(ctx, MGNN_ECUDA, "sm partition: stream hand-off failed");
+    cudaStream_t s = ps.s;
     // epoch orders needed by this window (R#8)
     if (!seeds) {
         for (int lp = 0; lp < n_lp; ++lp) {
@@ -955,7 +960,9 @@ mgnn_status mgnn_relabel(mgnn_ctx ctx, int32_t slot, mgnn_stream stream) {
     if (slot < 0 || slot > 1) return fail(ctx, MGNN_EINVAL, "bad slot");
     Win& w = ctx->win[slot];
     if (!w.sampled || !w.relabel_pending) return fail(ctx, MGNN_ESTATE, "relabel needs a window sampled with the relabel deferred");
-    cudaStream_t s = (cudaStream_t)stream;
+    PartScope ps(ctx, 1, (cudaStream_t)stream);
+    if (ps.err) return fail(ctx, MGNN_ECUDA, "sm partition: stream hand-off failed");
+    cudaStream_t s = ps.s;
     WinDev wd = win_dev(ctx, w);
     wd.n_inst = (int32_t)((int64_t)ctx->parts.size() * w.n_steps);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -984,7 +991,9 @@ mgnn_status mgnn_lookup_gather(mgnn_ctx ctx, int32_t slot, mgnn_stream stream) {
     if (other.gathered && !other.scored) return fail(ctx, MGNN_ESTATE, "previous window not scored");
     if (ctx->seq_started && w.step0 != ctx->next_step)
         return fail(ctx, MGNN_ESTATE, "windows must be gathered in step order");
-    cudaStream_t s = (cudaStream_t)stream;
+    PartScope ps(ctx, 2, (cudaStream_t)stream);
+    if (ps.err) return fail(ctx, MGNN_ECUDA, "sm partition: stream hand-off failed");
+    cudaStream_t s = ps.s;
     WinDev wd = win_dev(ctx, w);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof) {
@@ -1015,7 +1024,9 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
     if (slot < 0 || slot > 1) return fail(ctx, MGNN_EINVAL, "bad slot");
     Win& w = ctx->win[slot];
     if (!w.gathered || w.scored) return fail(ctx, MGNN_ESTATE, "score needs a gathered window");
-    cudaStream_t s = (cudaStream_t)stream;
+    PartScope ps(ctx, 2, (cudaStream_t)stream);
+    if (ps.err) return fail(ctx, MGNN_ECUDA, "sm partition: stream hand-off failed");
+    cudaStream_t s = ps.s;
     const int n_lp = (int)ctx->parts.size();
     int64_t cap_max = 0, nmax = 1;
     for (auto& p : ctx->parts) {

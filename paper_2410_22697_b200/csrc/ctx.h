@@ -74,6 +74,22 @@ struct Win {
 
 using namespace mgnn;          // internal header: the context below is written in the library's types
 
+namespace mgnn {
+namespace host {
+// SM partition (partition.cu): green contexts [0] gather + scoring, [1] sampling + relabel, and one
+// stream per call kind: 0 = mgnn_sample, 1 = mgnn_relabel (both on [1]), 2 = gather / score (on [0])
+constexpr int kPartStreams = 3;
+inline int part_of_stream(int i) { return i == 2 ? 0 : 1; }
+struct SmPartition {
+    bool on = false;
+    void* gc[2] = {nullptr, nullptr};    // CUgreenCtx
+    int sms[2] = {0, 0};
+    cudaStream_t s[kPartStreams] = {};
+    cudaEvent_t ev_in[kPartStreams] = {}, ev_out[kPartStreams] = {};
+};
+}  // namespace host
+}  // namespace mgnn
+
 struct mgnn_ctx_s {
     int device = 0;
     int32_t P = 0;
@@ -181,12 +197,27 @@ struct mgnn_ctx_s {
     // 1 = the gather launch of mgnn_lookup_gather, 2 = all of mgnn_score_evict_refill
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[4];   // [3] = deferred k_relabel
     long long* d_sampled = nullptr;      // [5] sampled edges E, expanded frontier F, |F_L| U, hits, misses
+    mgnn::host::SmPartition smp;         // mgnn_sm_partition
 };
 
 namespace mgnn {
 namespace host {
 
 mgnn_status fail(mgnn_ctx c, mgnn_status st, const std::string& msg);
+
+// Runs one API call's kernels on its SM-partition stream when a partition is set (else on the
+// caller's stream): `s` is the stream to launch on; the destructor hands ordering back to the caller.
+struct PartScope {
+    mgnn_ctx ctx;
+    int idx;
+    cudaStream_t caller_s, s;
+    bool active = false, err = false;
+    PartScope(mgnn_ctx c, int which, cudaStream_t caller);
+    ~PartScope();
+    PartScope(const PartScope&) = delete;
+    PartScope& operator=(const PartScope&) = delete;
+};
+void partition_free(mgnn_ctx ctx);
 
 #define CK(call)                                                                                     \
     do {                                                                                             \

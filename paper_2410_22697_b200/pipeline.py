@@ -153,6 +153,13 @@ class Context:
         """mgnn_sampler_defer_relabel: mgnn_sample leaves the columns in rank space until relabel()."""
         self._chk("mgnn_sampler_defer_relabel", self.L.mgnn_sampler_defer_relabel(self._h, 1 if enable else 0))
 
+    def sm_partition(self, gather_sms: int):
+        """mgnn_sm_partition: gather + scoring on `gather_sms` SMs, sampling + relabel on the rest
+        (green contexts; 0 = whole GPU).  Returns (gather-side SMs, prepare-side SMs)."""
+        out = (C.c_int32 * 2)()
+        self._chk("mgnn_sm_partition", self.L.mgnn_sm_partition(self._h, int(gather_sms), out))
+        return int(out[0]), int(out[1])
+
     def relabel(self, slot: int, stream=None):
         self._chk("mgnn_relabel", self.L.mgnn_relabel(self._h, slot, _stream(stream)))
 

@@ -65,7 +65,7 @@ class _Perturbed:
 def run_schedule_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, gamma: float, delta: int,
                         window: int, n_windows: int, x_rows: int = 2048, warm: int = 0, flush_bytes: int = 256 << 20,
                         run_seed: int = synth.RUN_SEED, feat_seed: int = synth.FEAT_SEED, rows_bound: int = -1,
-                        perturb=None, relabel_stream: bool = False):
+                        perturb=None, relabel_stream: bool = False, sm_split: int = 0):
     import torch
     from paper_2410_22697_b200 import pipeline as PL
     from paper_2410_22697_b200.schedule import PrepareAhead
@@ -77,6 +77,9 @@ def run_schedule_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_b
     if rows_bound < 0:                 # realistic arenas, as bench.py sizes them
         rows_bound = PL.estimate_rows_bound(ctx, fanouts, batch, run_seed)
     ctx.sampler_config(fanouts, batch, run_seed, window, rows_bound=rows_bound)
+    if sm_split:                       # mgnn_sm_partition: the calls run on green-context SM subsets
+        g_sms, p_sms = ctx.sm_partition(sm_split)
+        assert g_sms >= 1 and p_sms >= 1 and g_sms + p_sms <= torch.cuda.get_device_properties(0).multi_processor_count
     L = len(fanouts)
     n_inst = P * window
     pipe = PrepareAhead(ctx if perturb is None else _Perturbed(ctx, perturb), window, t0=1, flush_bytes=flush_bytes,

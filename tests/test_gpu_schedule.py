@@ -65,6 +65,32 @@ def test_schedule_relabel_stream_bench_window():
     assert st["evicted"] > 0
 
 
+@pytest.mark.parametrize("sm_split,relabel_stream", [(40, False), (72, True)])
+def test_schedule_sm_partition(sm_split, relabel_stream):
+    """mgnn_sm_partition: gather + scoring and sampling (+ relabel) on disjoint green-context SM
+    subsets, ordered with the caller's streams by event hand-offs -- every window equals the oracle."""
+    g = synth.generate(synth.CONFIGS["cfg1"])
+    st = run_schedule_parity(g, 2, 64, [10, 25], 256, 2500, 0.9, 4, 4, 6, x_rows=0, relabel_stream=relabel_stream,
+                             sm_split=sm_split)
+    assert st["evicted"] > 0
+
+
+def test_sm_partition_api_contract():
+    """EINVAL for negative / too-large SM counts; 0 removes the partition; sizes reported."""
+    from paper_2410_22697_b200 import pipeline as PL
+    from paper_2410_22697_b200._lib import MgnnError
+    g = synth.generate(synth.CONFIGS["cfg1"])
+    ctx = PL.build_context(0, synth.partition(g, 2), 64, synth.FEAT_SEED)
+    n = torch.cuda.get_device_properties(0).multi_processor_count
+    for bad in (-1, n, n + 10):
+        with pytest.raises(MgnnError):
+            ctx.sm_partition(bad)
+    a, b = ctx.sm_partition(48)
+    assert a >= 48 and b >= 1 and a + b <= n
+    assert ctx.sm_partition(0) == (0, 0)
+    ctx.close()
+
+
 def test_checked_library_schedule_and_parity():
     """The device bounds checks (-DMGNN_CHECKS: every MGNN_CHECK traps) on the timed schedule, the
     window-batching parity tests and the API tests, in a fresh interpreter that loads

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--relabel-stream", action="store_true")
     ap.add_argument("--parts", type=int, default=None)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--sm-split", type=int, default=0, help="gather-side SMs of mgnn_sm_partition (0 = off)")
     a = ap.parse_args()
     S = bench.Setup(a.config, 1, parts=a.parts)
     g = synth.generate(S.cfg)
@@ -34,6 +35,7 @@ def main():
     ctx = PL.build_context(0, parts, S.cfg.feat_dim, synth.FEAT_SEED)
     ctx.buffer_init(S.gamma, PL.alpha_default(S.gamma, S.delta), 1.0, S.delta, S.f_bp)
     ctx.sampler_config(S.cfg.fanouts, S.cfg.batch, synth.RUN_SEED, S.window)
+    sms = ctx.sm_partition(a.sm_split) if a.sm_split else (0, 0)
     pipe = PrepareAhead(ctx, S.window, serial=a.serial, relabel_stream=a.relabel_stream)
     for _ in range(4):
         pipe.iteration()
@@ -51,7 +53,8 @@ def main():
            "ms_median": ms[len(ms) // 2], "ms_min": ms[0], "mb_per_s": S.window * S.ppg / (ms[len(ms) // 2] / 1e3),
            "sample_ms": pr["sample_ms"] / n, "gather_ms": pr["gather_ms"] / max(pr["gather_calls"], 1),
            "score_ms": pr["score_ms"] / max(pr["score_calls"], 1),
-           "relabel_ms": pr["relabel_ms"] / max(pr["relabel_calls"], 1), "relabel_stream": a.relabel_stream}
+           "relabel_ms": pr["relabel_ms"] / max(pr["relabel_calls"], 1), "relabel_stream": a.relabel_stream,
+           "sm_split": sms}
     print(json.dumps(out), flush=True)
     ctx.close()
 
