@@ -325,7 +325,10 @@ MGNN_API int64_t mgnn_launch_count(mgnn_ctx ctx);
 
 /* Optional CUDA-event timing of the gather kernel (the dominant HBM kernel):
  * when enabled, each mgnn_lookup_gather brackets its gather launch with events
- * on the caller's stream; read returns the summed milliseconds, the number of
+ * on the stream it runs on; enable = 1 also brackets mgnn_sample, mgnn_relabel and
+ * mgnn_score_evict_refill (mgnn_profile_stages), enable = 2 times the gather only
+ * (an event between two launches ends their programmatic overlap, so the other
+ * stages stay untouched); both levels count the sampled units and hits / misses; read returns the summed milliseconds, the number of
  * launches timed and the algorithmic bytes they moved (2 * rows * feat_dim * 4),
  * and resets them (synchronises the events). */
 MGNN_API mgnn_status mgnn_profile_enable(mgnn_ctx ctx, int32_t enable);

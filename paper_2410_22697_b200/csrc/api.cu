@@ -926,7 +926,7 @@ mgnn_status mgnn_sample(mgnn_ctx ctx, int32_t slot, uint64_t t0, int32_t n_steps
     }
     launch_seeds(wd, s);
     cudaEvent_t pe0 = nullptr, pe1 = nullptr;
-    if (ctx->prof) {
+    if (ctx->prof == 1) {
         CK(cudaEventCreate(&pe0));
         CK(cudaEventCreate(&pe1));
         CK(cudaEventRecord(pe0, s));
@@ -939,7 +939,7 @@ mgnn_status mgnn_sample(mgnn_ctx ctx, int32_t slot, uint64_t t0, int32_t n_steps
     }
     if (!ctx->defer_relabel) launch_relabel(wd, s);
     CKL();
-    if (ctx->prof) {
+    if (ctx->prof == 1) {
         CK(cudaEventRecord(pe1, s));
         ctx->prof_ev[0].emplace_back(pe0, pe1);
     }
@@ -966,14 +966,14 @@ mgnn_status mgnn_relabel(mgnn_ctx ctx, int32_t slot, mgnn_stream stream) {
     WinDev wd = win_dev(ctx, w);
     wd.n_inst = (int32_t)((int64_t)ctx->parts.size() * w.n_steps);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (ctx->prof) {
+    if (ctx->prof == 1) {
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
         CK(cudaEventRecord(e0, s));
     }
     launch_relabel(wd, s);
     CKL();
-    if (ctx->prof) {
+    if (ctx->prof == 1) {
         CK(cudaEventRecord(e1, s));
         ctx->prof_ev[3].emplace_back(e0, e1);
     }
@@ -1034,7 +1034,7 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
         nmax = std::max(nmax, std::max(p.cap, p.n_h));
     }
     cudaEvent_t pe0 = nullptr, pe1 = nullptr;
-    if (ctx->prof) {
+    if (ctx->prof == 1) {
         CK(cudaEventCreate(&pe0));
         CK(cudaEventCreate(&pe1));
         CK(cudaEventRecord(pe0, s));
@@ -1075,7 +1075,7 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
                            ctx->d_ovf, t_last, s);
     }
     CKL();
-    if (ctx->prof) {
+    if (ctx->prof == 1) {
         CK(cudaEventRecord(pe1, s));
         ctx->prof_ev[2].emplace_back(pe0, pe1);
     }
@@ -1243,7 +1243,7 @@ mgnn_status mgnn_profile_kernels(int32_t enable, char* report, int64_t report_le
 
 mgnn_status mgnn_profile_enable(mgnn_ctx ctx, int32_t enable) {
     if (!ctx) return MGNN_EINVAL;
-    ctx->prof = enable != 0;
+    ctx->prof = enable == 2 ? 2 : (enable != 0 ? 1 : 0);
     return MGNN_OK;
 }
 

@@ -192,7 +192,7 @@ struct mgnn_ctx_s {
     int sticky = MGNN_OK;
     std::string err;
     // profiling
-    bool prof = false;
+    int prof = 0;                        // 1: every stage timed by events, 2: only the gather launch
     // event pairs per stage: 0 = sampler kernels (k_hop, k_compact, k_relabel) of mgnn_sample,
     // 1 = the gather launch of mgnn_lookup_gather, 2 = all of mgnn_score_evict_refill
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[4];   // [3] = deferred k_relabel

@@ -323,8 +323,11 @@ class Context:
     def launch_count(self) -> int:
         return int(self.L.mgnn_launch_count(self._h))
 
-    def profile(self, enable: bool):
-        self._chk("mgnn_profile_enable", self.L.mgnn_profile_enable(self._h, 1 if enable else 0))
+    def profile(self, enable, gather_only: bool = False):
+        """mgnn_profile_enable: events around every stage (1), around the gather launch only (2,
+        gather_only=True: the other stages keep their programmatic launch overlap), or off."""
+        level = (2 if gather_only else 1) if enable else 0
+        self._chk("mgnn_profile_enable", self.L.mgnn_profile_enable(self._h, level))
 
     def profile_stages(self) -> Dict[str, float]:
         """mgnn_profile_stages: per-stage event times and sampled units since the last read."""
