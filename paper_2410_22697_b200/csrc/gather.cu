@@ -405,7 +405,16 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_tma(WinDev W, WorldDev 
         mbar_wait(&bars[warp][st], phase[st]);
         phase[st] ^= 1u;
         float* X = W.X + ((int64_t)cm * W.ucap + f0) * pitch;
-        if (hint & 4) {                          // the chunk's rows are contiguous in smem and in X:
+        if (hint & 8) {                          // stores through the LSU (smem -> registers -> X, streaming):
+            // the copy engine then carries only the row reads (it is the per-SM limit of this kernel)
+            const float4* s4 = reinterpret_cast<const float4*>(stage[st]);
+            float4* x4 = reinterpret_cast<float4*>(X);
+            const int n4 = (int)((uint32_t)nrows * rowb / 16u);
+#pragma unroll 4
+            for (int i = lane; i < n4; i += 32) __stcs(x4 + i, s4[i]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // reads done before the next TMA fill
+            __syncwarp();
+        } else if (hint & 4) {                   // the chunk's rows are contiguous in smem and in X:
             if (lane == 0) {                     // one bulk store of nrows rows
                 if (hint & 2)
                     bulk_store_hint(X, stage[st], (uint32_t)nrows * rowb, pol_stream);

@@ -4,6 +4,7 @@ the first launch): each runs a cfg1 parity check in a fresh interpreter (-m gpu)
 * MGNN_GATHER=reg      -- register gather (k_gather<false> for narrow rows, <true> for >= 128 floats)
 * MGNN_PDL=0           -- plain launches instead of programmatic dependent launch
 * MGNN_GATHER_HINT=0/3 -- no L2 cache hints / table rows evict_last and X rows evict_first
+* MGNN_GATHER_HINT=10/14 (with MGNN_GATHER_G4=0) -- X rows stored through the LSU instead of bulk stores
 """
 import os
 import subprocess
@@ -27,7 +28,8 @@ print("variant parity ok")
 
 
 @pytest.mark.parametrize("env", [{"MGNN_GATHER": "reg"}, {"MGNN_PDL": "0"}, {"MGNN_GATHER_HINT": "0"},
-                                 {"MGNN_GATHER_HINT": "3"}])
+                                 {"MGNN_GATHER_HINT": "3"}, {"MGNN_GATHER_HINT": "10", "MGNN_GATHER_G4": "0"},
+                                 {"MGNN_GATHER_HINT": "14", "MGNN_GATHER_G4": "0"}])
 def test_variant_parity(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT)], cwd=ROOT, env=e, capture_output=True,
