@@ -351,6 +351,7 @@ enum {
     MGNN_PROF_SCORE_MS = 8, MGNN_PROF_SCORE_CALLS = 9,
     MGNN_PROF_HITS = 10, MGNN_PROF_MISSES = 11,   /* buffer hits / misses of every gathered minibatch */
     MGNN_PROF_RELABEL_MS = 12, MGNN_PROF_RELABEL_CALLS = 13,   /* deferred k_relabel (mgnn_relabel) */
+    MGNN_PROF_RELABEL_PROBES = 14,   /* k_relabel's dependent probes (hop pairs + seed hash), all columns */
     MGNN_PROF_N = 16
 };
 MGNN_API mgnn_status mgnn_profile_stages(mgnn_ctx ctx, double* out, int32_t n_out);

@@ -304,8 +304,8 @@ mgnn_status mgnn_ctx_create(int32_t device, int32_t n_parts, int64_t n_global, c
     chk(cudaMemset(ctx->d_ovf, 0xFF, sizeof(unsigned long long)));
     chk(dalloc(&ctx->d_gathered, 1));
     chk(cudaMemset(ctx->d_gathered, 0, sizeof(long long)));
-    chk(dalloc(&ctx->d_sampled, 5));
-    chk(cudaMemset(ctx->d_sampled, 0, 5 * sizeof(long long)));
+    chk(dalloc(&ctx->d_sampled, 6));
+    chk(cudaMemset(ctx->d_sampled, 0, 6 * sizeof(long long)));
     if (st != MGNN_OK) {
         mgnn_destroy(ctx);
         return st;
@@ -1272,7 +1272,7 @@ mgnn_status mgnn_profile_stages(mgnn_ctx ctx, double* out, int32_t n_out) {
         mgnn_status r = drain_events(ctx, st, &ms[st], &n[st]);
         if (r) return r;
     }
-    long long su[5] = {0, 0, 0, 0, 0}, rows = 0;
+    long long su[6] = {0, 0, 0, 0, 0, 0}, rows = 0;
     CK(cudaMemcpy(su, ctx->d_sampled, sizeof(su), cudaMemcpyDeviceToHost));
     CK(cudaMemset(ctx->d_sampled, 0, sizeof(su)));
     CK(cudaMemcpy(&rows, ctx->d_gathered, sizeof(long long), cudaMemcpyDeviceToHost));
@@ -1292,6 +1292,7 @@ mgnn_status mgnn_profile_stages(mgnn_ctx ctx, double* out, int32_t n_out) {
     out[MGNN_PROF_MISSES] = (double)su[4];
     out[MGNN_PROF_RELABEL_MS] = ms[3];
     out[MGNN_PROF_RELABEL_CALLS] = (double)n[3];
+    out[MGNN_PROF_RELABEL_PROBES] = (double)su[5];
     return MGNN_OK;
 }
 

@@ -196,7 +196,8 @@ struct mgnn_ctx_s {
     // event pairs per stage: 0 = sampler kernels (k_hop, k_compact, k_relabel) of mgnn_sample,
     // 1 = the gather launch of mgnn_lookup_gather, 2 = all of mgnn_score_evict_refill
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[4];   // [3] = deferred k_relabel
-    long long* d_sampled = nullptr;      // [5] sampled edges E, expanded frontier F, |F_L| U, hits, misses
+    long long* d_sampled = nullptr;      // [6] sampled edges E, expanded frontier F, |F_L| U, hits, misses,
+                                         //     k_relabel's (bits, position) / seed-hash probes
     mgnn::host::SmPartition smp;         // mgnn_sm_partition
 };
 

@@ -42,6 +42,7 @@ constexpr int kRelabelBatch = 4;       // column lookups in flight per k_relabel
 #endif
 constexpr int kColBatch = MGNN_COL_BATCH;           // neighbour-rank loads in flight per k_hop thread
 constexpr int kWordTile = kThreads * kCWords;   // bitmap words per k_compact tile
+constexpr int kCompactStage = 4096;             // new ranks of a tile staged in shared memory (16 KB)
 
 // + kMaxLayers + 1: segment-aligned tiles (k_hop align) may leave one partial tile per segment
 int64_t scan_tiles_count(int64_t fcap) { return (fcap + kHopTileMin - 1) / kHopTileMin + kMaxLayers + 1; }
@@ -307,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 8) k_compact(WinDev W, int hop, Scra
     __shared__ long long sm[8];
     __shared__ int tslot;
     __shared__ long long prefix_sh;
+    __shared__ int32_t stage_sh[kCompactStage];  // the tile's new ranks in order (coalesced frontier writes)
     const int m = blockIdx.y;
     const PartDev& pd = W.parts[m / W.n_steps];
     const int64_t nwords = ((W.remote ? W.n_global : pd.vp) + 31) >> 5;   // rank space
@@ -364,17 +366,36 @@ __global__ void __launch_bounds__(kThreads, 8) k_compact(WinDev W, int hop, Scra
             v[1] = make_uint4(b[2], p[2], b[3], p[3]);
             if (cnt) *reinterpret_cast<uint4*>(fbp + wd0) = now;
         }
+        if (agg <= kCompactStage) {      // the tile's ranks go through shared memory, then out coalesced
+            int q = (int)excl;
 #pragma unroll
-        for (int j = 0; j < kCWords; ++j) {
-            const int64_t wd = wd0 + j;
-            uint32_t bb = b[j];
-            while (bb) {
-                const int bi = __ffs(bb) - 1;
-                bb &= bb - 1;
-                const int32_t r = (int32_t)(wd * 32 + bi);
-                MGNN_CHECK(r < (W.remote ? W.n_global : pd.vp), "compact r=%d", r);
-                if (pos < cap) fr[pos] = r;
-                ++pos;
+            for (int j = 0; j < kCWords; ++j) {
+                const int64_t wd = wd0 + j;
+                uint32_t bb = b[j];
+                while (bb) {
+                    const int bi = __ffs(bb) - 1;
+                    bb &= bb - 1;
+                    MGNN_CHECK(wd * 32 + bi < (W.remote ? W.n_global : pd.vp), "compact r=%lld", (long long)(wd * 32 + bi));
+                    stage_sh[q++] = (int32_t)(wd * 32 + bi);
+                }
+            }
+            __syncthreads();
+            const int64_t base = nF + prefix_sh;
+            for (int i = threadIdx.x; i < (int)agg; i += kThreads)
+                if (base + i < cap) fr[base + i] = stage_sh[i];
+        } else {
+#pragma unroll
+            for (int j = 0; j < kCWords; ++j) {
+                const int64_t wd = wd0 + j;
+                uint32_t bb = b[j];
+                while (bb) {
+                    const int bi = __ffs(bb) - 1;
+                    bb &= bb - 1;
+                    const int32_t r = (int32_t)(wd * 32 + bi);
+                    MGNN_CHECK(r < (W.remote ? W.n_global : pd.vp), "compact r=%d", r);
+                    if (pos < cap) fr[pos] = r;
+                    ++pos;
+                }
             }
         }
         if (tile == ntiles - 1 && threadIdx.x == 0) {
@@ -391,17 +412,19 @@ __global__ void __launch_bounds__(kThreads, 8) k_compact(WinDev W, int hop, Scra
 // exactly one hop j <= i; then its position is wpre_j[c/32] + popc(new_j[c/32] & lower bits),
 // since new_j is appended to the frontier in ascending rank order (R#7).
 __device__ __forceinline__ int32_t frontier_pos(const WinDev& W, int m, int hop, const int2* __restrict__ sp,
-                                                int32_t c) {
+                                                int32_t c, unsigned& probes) {
     const int64_t wd = c >> 5;
     const uint32_t bit = 1u << (c & 31);
     for (int j = hop; j >= 0; --j) {
         const int64_t o = ((int64_t)m * W.L + j) * W.bm_words + wd;
         const uint2 bp = __ldg(reinterpret_cast<const uint2*>(W.nb) + o);   // bits and position: one load
+        ++probes;
         if (bp.x & bit) return (int32_t)bp.y + __popc(bp.x & (bit - 1u));
     }
     // a seed: its position in F_0 from the window's seed hash (k_seeds)
     for (uint32_t h = seed_hash(c) & (uint32_t)W.seed_hmask;; h = (h + 1) & (uint32_t)W.seed_hmask) {
         const int2 e = __ldg(sp + h);
+        ++probes;
         if (e.x == c + 1) return e.y;
         if (e.x == 0) return 0;                  // not reached for a sampled column (overflowed window only)
     }
@@ -423,6 +446,7 @@ __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
         atomicAdd((unsigned long long*)&W.sampled_units[1], (unsigned long long)f);
         atomicAdd((unsigned long long*)&W.sampled_units[2], (unsigned long long)hs[W.L]);
     }
+    unsigned probes = 0;                         // dependent probes (roofline units, profiling only)
     for (int hop = 0; hop < W.L; ++hop) {
         const int64_t* off = W.off[hop] + (int64_t)m * W.off_stride[hop];
         int32_t* cols = W.cols[hop] + (int64_t)m * W.col_stride[hop];
@@ -436,7 +460,9 @@ __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
             for (int j = 0; j < kRelabelBatch; ++j) c[j] = e0 + j * kThreads < E ? cols[e0 + j * kThreads] : 0;
 #pragma unroll
             for (int j = 0; j < kRelabelBatch; ++j) {
-                const int32_t p = frontier_pos(W, m, hop, sp, c[j]);
+                unsigned pr = 0;
+                const int32_t p = frontier_pos(W, m, hop, sp, c[j], pr);
+                if (e0 + j * kThreads < E) probes += pr;
                 MGNN_CHECK(p >= 0 && (p < cap || *W.ovf <= W.step0 + (uint64_t)W.n_steps - 1 ||
                                       e0 + j * kThreads >= E),
                            "relabel pos=%d cap=%d", p, cap);
@@ -446,6 +472,10 @@ __global__ void __launch_bounds__(kThreads) k_relabel(WinDev W) {
             for (int j = 0; j < kRelabelBatch; ++j)
                 if (e0 + j * kThreads < E) cols[e0 + j * kThreads] = c[j];
         }
+    }
+    if (W.sampled_units) {
+        for (int o = 16; o > 0; o >>= 1) probes += __shfl_xor_sync(kFull, probes, o);
+        if ((threadIdx.x & 31) == 0 && probes) atomicAdd((unsigned long long*)&W.sampled_units[5], (unsigned long long)probes);
     }
 }
 

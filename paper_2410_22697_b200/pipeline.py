@@ -334,7 +334,8 @@ class Context:
         out = np.zeros(_lib.PROF_N, np.float64)
         self._chk("mgnn_profile_stages", self.L.mgnn_profile_stages(self._h, _ptr(out), _lib.PROF_N))
         keys = ["sample_ms", "sample_calls", "edges", "frontier", "unique", "gather_ms", "gather_calls",
-                "gather_rows", "score_ms", "score_calls", "hits", "misses", "relabel_ms", "relabel_calls"]
+                "gather_rows", "score_ms", "score_calls", "hits", "misses", "relabel_ms", "relabel_calls",
+                "relabel_probes"]
         return {k: float(out[i]) for i, k in enumerate(keys)}
 
     def profile_read(self):

@@ -54,6 +54,8 @@ def main():
            "sample_ms": pr["sample_ms"] / n, "gather_ms": pr["gather_ms"] / max(pr["gather_calls"], 1),
            "score_ms": pr["score_ms"] / max(pr["score_calls"], 1),
            "relabel_ms": pr["relabel_ms"] / max(pr["relabel_calls"], 1), "relabel_stream": a.relabel_stream,
+           "relabel_probes": pr["relabel_probes"] / max(pr["relabel_calls"], 1),
+           "edges": pr["edges"] / n, "frontier": pr["frontier"] / n, "unique": pr["unique"] / n,
            "sm_split": sms}
     print(json.dumps(out), flush=True)
     ctx.close()
