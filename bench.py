@@ -273,6 +273,22 @@ def traffic_table(name: str):
         return None
 
 
+def random_load_peak(table_bytes=None):
+    """Measured random-load ceiling (profiles/r02/randread.json, tools/randread.cu): of an L2-resident
+    table, or (table_bytes given) of the smallest measured table at least that large (DRAM-resident)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "randread.json")) as f:
+            d = json.load(f)
+        if table_bytes is None:
+            return float(d["l2_resident_random_loads_g_per_s"]), "L2-resident table"
+        rows = sorted((r for r in d["rows"] if (r["table_mb"] << 20) >= table_bytes), key=lambda r: r["table_mb"])
+        rows = rows or sorted(d["rows"], key=lambda r: -r["table_mb"])
+        best = max(r["g_loads_per_s"] for r in rows if r["table_mb"] == rows[0]["table_mb"])
+        return float(best), f"{rows[0]['table_mb']} MB table"
+    except (OSError, ValueError, KeyError, IndexError):
+        return None, None
+
+
 def git_head():
     try:
         return subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], cwd=ROOT, capture_output=True,
@@ -649,6 +665,32 @@ def main():
         s_bytes = (8.0 * sp_["edges"] + 24.0 * sp_["frontier"] + 8.0 * sp_["unique"]) / max(sp_["sample_calls"], 1)
         s_ach = s_bytes / (s_ms / 1e3) / 1e9 if s_ms > 0 else None
         tt_ = traffic_table(S.name)
+        cfg_layers = len(cfg.fanouts)
+        # k_relabel is bound by dependent random probes of L2-resident (bits, position) pairs, not bytes:
+        # probes per window (counted by the kernel) / its event time vs the measured L2 random-load ceiling
+        rl_ms = sp_["relabel_ms"] / max(sp_["relabel_calls"], 1)
+        rl_probes = sp_["relabel_probes"] / max(sp_["relabel_calls"], 1)
+        rl_peak, _ = random_load_peak()
+        rl_rate = rl_probes / (rl_ms / 1e3) / 1e9 if rl_ms > 0 and rl_probes > 0 else None
+        # k_hop: one random 4-byte column load per sampled edge from the hosted partitions' cols_rank
+        # (ncu per-launch time at HEAD from the committed traffic table) vs the random-load ceiling of a
+        # DRAM table of that size
+        cols_bytes = sum(int(parts[q].cols.nbytes) for q in hosted)
+        hop_peak, hop_tab = random_load_peak(cols_bytes)
+        hop_us = ((tt_ or {}).get("kernels", {}).get("k_hop", {}) or {}).get("us_per_launch")
+        e_win = sp_["edges"] / max(sp_["sample_calls"], 1)
+        hop_rate = e_win / (cfg_layers * hop_us * 1e-6) / 1e9 if hop_us else None
+        hop_roof = {"bound": "dram_random_loads", "edges_per_window": e_win, "launches_per_window": cfg_layers,
+                    "us_per_launch_ncu": hop_us, "achieved": hop_rate, "unit": "G loads/s", "peak": hop_peak,
+                    "frac": (hop_rate / hop_peak) if hop_rate and hop_peak else None,
+                    "peak_source": f"profiles/r02/randread.json ({hop_tab}: hosted cols_rank = {cols_bytes >> 20} MB)",
+                    "note": "k > 1 samples of a node share its CSR row, so the loads beat fully random ones"}
+        relabel_roof = {"bound": "l2_random_loads", "probes_per_window": rl_probes,
+                        "probes_per_edge": rl_probes / max(sp_["edges"] / max(sp_["sample_calls"], 1), 1.0),
+                        "ms_per_window": rl_ms, "achieved": rl_rate, "unit": "G loads/s", "peak": rl_peak,
+                        "frac": (rl_rate / rl_peak) if rl_rate and rl_peak else None,
+                        "peak_source": "profiles/r02/randread.json (tools/randread.cu, L2-resident random loads)",
+                        "note": "deferred k_relabel on its own stream beside the gather (time includes the sharing)"}
         step_ms_sum = sum(r_["my_ms"] for r_ in runs)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
@@ -694,7 +736,8 @@ def main():
                                "F": sp_["frontier"] / max(sp_["sample_calls"], 1),
                                "U": sp_["unique"] / max(sp_["sample_calls"], 1)},
                 "traffic": {k_: v_ for k_, v_ in (tt_ or {}).items() if k_ in ("k_hop", "k_compact", "k_relabel")}
-                or None},
+                or None,
+                "relabel": relabel_roof, "hop": hop_roof},
             "stages_ms_per_window": {"sample": s_ms,
                                      "gather": sp_["gather_ms"] / max(sp_["gather_calls"], 1),
                                      "score": sp_["score_ms"] / max(sp_["score_calls"], 1),
