@@ -18,8 +18,9 @@ namespace host {
 void free_sage(mgnn_ctx_s* ctx) {
     auto& S = ctx->sage;
     dfree(S.params);
+    dfree(S.w3);
     for (int l = 0; l < kMaxLayers; ++l) {
-        S.w[l] = S.b[l] = nullptr;
+        S.w[l] = S.b[l] = S.whi[l] = S.wlo[l] = nullptr;
         dfree(S.h[l]);
         dfree(S.wt[l]);
         dfree(S.mean[l]);
@@ -104,12 +105,33 @@ mgnn_status mgnn_sage_config(mgnn_ctx ctx, const mgnn_sage_desc* d) {
     }
     CK(dalloc(&S.params, off));
     CK(cudaMemcpy(S.params, hp.data(), off * sizeof(float), cudaMemcpyHostToDevice));
+    {
+        const char* e = getenv("MGNN_SAGE_TF32");
+        S.split3 = !(e && e[0] == '1');
+    }
+    if (S.split3) {
+        int64_t wn = 0;
+        for (int l = 0; l < L; ++l) wn += (int64_t)S.npad[l] * 2 * S.kp[l];
+        CK(dalloc(&S.w3, 2 * wn));
+        int64_t o = 0;
+        for (int l = 0; l < L; ++l) {
+            S.whi[l] = S.w3 + o;
+            S.wlo[l] = S.w3 + wn + o;
+            o += (int64_t)S.npad[l] * 2 * S.kp[l];
+        }
+    }
     for (int l = 0; l < L; ++l) {
         S.w[l] = S.params + S.w_off[l];
         S.b[l] = S.params + S.b_off[l];
         const int64_t wc = 2 * (int64_t)S.kp[l];
         if (!sage_encode_map(S.map_w[l], S.w[l], S.npad[l], wc, wc, S.npad[l]))
             return fail(ctx, MGNN_ECUDA, "sage: cuTensorMapEncodeTiled (weights) failed");
+        if (S.split3) {
+            launch_split_tf32(S.w[l], S.whi[l], S.wlo[l], (int64_t)S.npad[l] * wc, 0);
+            if (!sage_encode_map(S.map_whi[l], S.whi[l], S.npad[l], wc, wc, S.npad[l]) ||
+                !sage_encode_map(S.map_wlo[l], S.wlo[l], S.npad[l], wc, wc, S.npad[l]))
+                return fail(ctx, MGNN_ECUDA, "sage: cuTensorMapEncodeTiled (split weights) failed");
+        }
         S.out_rows[l] = ctx->fcap[L - 1 - l];
         if (l < L - 1) {
             const int64_t n = M * S.out_rows[l] * S.npad[l];
@@ -134,6 +156,7 @@ mgnn_status mgnn_sage_config(mgnn_ctx ctx, const mgnn_sage_desc* d) {
             if (!sage_encode_map(S.map_in[slot][l], base, rows, cols, pitch, 128))
                 return fail(ctx, MGNN_ECUDA, "sage: cuTensorMapEncodeTiled (activations) failed");
         }
+    CK(cudaDeviceSynchronize());                 // the weight split (legacy stream) precedes every forward
     S.ready = true;
     return MGNN_OK;
 }
@@ -180,7 +203,9 @@ mgnn_status sage_layer(mgnn_ctx ctx, Win& w, int slot, int l, int n_inst, int in
     a.mean_pitch = S.kp[l];
     if (mean_first) {          // means by k_mean over all SMs, then the warp-specialised TMA-fed GEMM
         launch_mean(a, s);
-        if (!launch_sage_gemm(S.map_in[slot][l], S.map_w[l], S.map_mean128[l], a, s))
+        a.split3 = S.split3 ? 1 : 0;
+        if (!launch_sage_gemm(S.map_in[slot][l], S.split3 ? S.map_whi[l] : S.map_w[l], S.map_wlo[l],
+                              S.map_mean128[l], a, s))
             return fail(ctx, MGNN_ECUDA, "sage: gemm launch configuration failed");
         return MGNN_OK;
     }
@@ -490,6 +515,8 @@ mgnn_status mgnn_sage_sgd(mgnn_ctx ctx, float lr, mgnn_stream stream) {
         d.w[l] = S.w[l];
         d.g[l] = S.grads + S.w_off[l];
         d.wt[l] = S.wt[l];
+        d.whi[l] = S.whi[l];
+        d.wlo[l] = S.wlo[l];
         d.rows[l] = S.npad[l];
         d.cols[l] = 2 * (int64_t)S.kp[l];
     }

@@ -167,6 +167,13 @@ struct mgnn_ctx_s {
         float* h[kMaxLayers] = {};                // hidden outputs H^{l+1}, l < L-1: [M][out_rows][npad]
         int64_t out_rows[kMaxLayers] = {};        // rows per instance of layer l's output buffer (= fcap[h])
         alignas(64) unsigned char map_w[kMaxLayers][128];
+        // 3xTF32 forward GEMM (default; MGNN_SAGE_TF32=1: one TF32 pass): Wcat = W_hi + W_lo, refreshed
+        // with every weight update (mgnn_sage_config, k_sgd_layers)
+        bool split3 = true;
+        float* w3 = nullptr;                      // [W_hi of every layer | W_lo of every layer]
+        float* whi[kMaxLayers] = {};
+        float* wlo[kMaxLayers] = {};
+        alignas(64) unsigned char map_whi[kMaxLayers][128], map_wlo[kMaxLayers][128];
         alignas(64) unsigned char map_in[2][kMaxLayers][128];   // [window slot][layer]
         // training (NEXT-3)
         bool train = false;

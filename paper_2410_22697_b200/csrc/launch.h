@@ -211,12 +211,16 @@ struct SageLayerArgs {
     float* mean_out;           // optional [M][mean_rows][mean_pitch]: neighbour means (training)
     int64_t mean_rows, mean_pitch;
     int32_t b_resident;        // k_sage_gemm: all weight chunks stay in shared memory (set by the launcher)
+    int32_t split3;            // k_sage_gemm: 3xTF32 (A_hi W_hi + A_hi W_lo + A_lo W_hi), fp32-grade products
 };
 bool sage_encode_map(void* map_out, const float* base, int64_t rows, int64_t cols, int64_t pitch, int box_rows);
 bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArgs& a, cudaStream_t s);
 // out = act([H_in | mean] Wcat^T + b) with the means precomputed (warp-specialised, TMA + tcgen05)
-bool launch_sage_gemm(const void* map_in, const void* map_w, const void* map_mean, const SageLayerArgs& a,
-                      cudaStream_t s);
+// map_w is W_hi (low 13 mantissa bits zero) and map_wlo W - W_hi when a.split3, else map_w = W, map_wlo unused
+bool launch_sage_gemm(const void* map_in, const void* map_w, const void* map_wlo, const void* map_mean,
+                      const SageLayerArgs& a, cudaStream_t s);
+// hi = w with the low 13 mantissa bits cleared (exactly a TF32 value), lo = w - hi (exact), n floats
+void launch_split_tf32(const float* w, float* hi, float* lo, int64_t n, cudaStream_t s);
 // neighbour means of a layer's dst rows into mean_out (warp per row, all SMs): the training step's
 // forward, whose per-step instance count is too small for the fused aggregation to fill the GPU
 void launch_mean(const SageLayerArgs& a, cudaStream_t s);
@@ -301,6 +305,8 @@ struct SgdLayers {             // per layer: Wcat [rows][cols] followed by the b
     float* w[kMaxLayers];
     float* g[kMaxLayers];
     float* wt[kMaxLayers];
+    float* whi[kMaxLayers];    // optional 3xTF32 split of the updated Wcat (k_sage_gemm operands)
+    float* wlo[kMaxLayers];
     int64_t rows[kMaxLayers], cols[kMaxLayers];
 };
 void launch_sgd_layers(const SgdLayers& d, float lr, cudaStream_t s);

@@ -458,30 +458,59 @@ bool launch_sage_layer(const void* map_in, const void* map_w, const SageLayerArg
 // TMEM accumulators; warps 2-17 drain the other accumulator (bias, ReLU, stores) meanwhile, so
 // loads, MMAs and the epilogue of consecutive tiles overlap.  One CTA per SM, persistent.
 constexpr int kGEpiWarps = 16;            // epilogue warps (4 per TMEM lane quarter)
-constexpr int kGThreads = (2 + kGEpiWarps) * 32;   // + TMA warp + MMA warp
+constexpr int kGConvWarps = 4;            // 3xTF32: split each A chunk into hi / lo in shared memory
+constexpr int kGThreads = (2 + kGEpiWarps + kGConvWarps) * 32;   // + TMA warp + MMA warp
 constexpr int kGMaxStages = 8;
+
+// 3xTF32 (a.split3): a = a_hi + a_lo and w = w_hi + w_lo exactly, a_hi / w_hi with the low 13 mantissa
+// bits cleared (TF32 values the tensor core reads exactly, whatever its own conversion of the rest);
+// a.w ~ a_hi w_hi + a_hi w_lo + a_lo w_hi with |error| <= 3 2^-20 |a||w| per product before the fp32
+// accumulation (the dropped a_lo w_lo and the TF32 conversion of the lo parts).  W_hi / W_lo come from
+// HBM (split once per weight update); the A chunk is split in shared memory by kGConvWarps warps
+// between its TMA arrival and its MMAs.
+__global__ void k_split_tf32(const float* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo, int64_t n) {
+    pdl_enter();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = w[i];
+        const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        hi[i] = h;
+        lo[i] = __fsub_rn(v, h);
+    }
+}
+
+void launch_split_tf32(const float* w, float* hi, float* lo, int64_t n, cudaStream_t s) {
+    int64_t b = (n + 255) / 256;
+    if (b > (int64_t)num_sms() * 8) b = (int64_t)num_sms() * 8;
+    launch_k(k_split_tf32, dim3((unsigned)(b < 1 ? 1 : b)), dim3(256), 0, s, w, hi, lo, n);
+    count_launches(1, __func__, s);
+}
 
 __global__ void __launch_bounds__(kGThreads, 1)
     k_sage_gemm(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_w,
-                const __grid_constant__ CUtensorMap map_mean, SageLayerArgs a) {
+                const __grid_constant__ CUtensorMap map_wlo, const __grid_constant__ CUtensorMap map_mean,
+                SageLayerArgs a) {
     extern __shared__ __align__(1024) unsigned char dsm[];
-    __shared__ __align__(8) uint64_t full[kGMaxStages], empty[kGMaxStages], tfull[2], tempty[2];
+    __shared__ __align__(8) uint64_t full[kGMaxStages], empty[kGMaxStages], conv[kGMaxStages], tfull[2], tempty[2];
     __shared__ uint32_t tmem_sh;
     unsigned char* base = dsm + ((1024u - (su32(dsm) & 1023u)) & 1023u);
     const uint32_t b_bytes = (uint32_t)a.npad * 128u;
     const int nch = (a.k_in + kChunkCols - 1) / kChunkCols;   // 32-column chunks per operand half
     const int nk = 2 * nch;
     // weights resident in shared memory for the whole kernel when they fit (a.b_resident), else
-    // streamed with each A chunk
-    const uint32_t stage_bytes = kChunkBytesA + (a.b_resident ? 0u : b_bytes);
+    // streamed with each A chunk.  Stage: [A | A_lo (split3)] [W (| W_lo)] ; resident: W chunks, W_lo chunks
+    const int nparts = a.split3 ? 2 : 1;
+    const uint32_t a_stage = kChunkBytesA * (uint32_t)nparts;
+    const uint32_t stage_bytes = a_stage + (a.b_resident ? 0u : b_bytes * (uint32_t)nparts);
+    const uint32_t tx_bytes = kChunkBytesA + (a.b_resident ? 0u : b_bytes * (uint32_t)nparts);
     unsigned char* b_res = base + (size_t)a.stages * stage_bytes;
-    int32_t* tile_pref = (int32_t*)(b_res + (a.b_resident ? (size_t)nk * b_bytes : 0));
+    int32_t* tile_pref = (int32_t*)(b_res + (a.b_resident ? (size_t)nparts * nk * b_bytes : 0));
     __shared__ __align__(8) uint64_t bfull;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < a.stages; ++i) {
             mb_init(&full[i], 1);
             mb_init(&empty[i], 1);
+            mb_init(&conv[i], kGConvWarps);
         }
         for (int i = 0; i < 2; ++i) {
             mb_init(&tfull[i], 1);
@@ -491,6 +520,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_in) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+        if (a.split3) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_wlo) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_mean) : "memory");
     }
     if (warp == 1) tmem_alloc(&tmem_sh, a.tmem_cols);    // 2 accumulators of npad columns
@@ -531,10 +561,12 @@ __global__ void __launch_bounds__(kGThreads, 1)
     if (warp == 0) {
         if (lane == 0) {                         // TMA producer
             if (a.b_resident && blockIdx.x < n_tiles) {
-                mb_expect_tx(&bfull, (uint32_t)nk * b_bytes);
-                for (int kc = 0; kc < nk; ++kc)
-                    tma_load_2d(b_res + (size_t)kc * b_bytes, &map_w,
-                                kc < nch ? kc * kChunkCols : a.kp + (kc - nch) * kChunkCols, 0, &bfull);
+                mb_expect_tx(&bfull, (uint32_t)(nparts * nk) * b_bytes);
+                for (int kc = 0; kc < nk; ++kc) {
+                    const int wcol = kc < nch ? kc * kChunkCols : a.kp + (kc - nch) * kChunkCols;
+                    tma_load_2d(b_res + (size_t)kc * b_bytes, &map_w, wcol, 0, &bfull);
+                    if (a.split3) tma_load_2d(b_res + (size_t)(nk + kc) * b_bytes, &map_wlo, wcol, 0, &bfull);
+                }
             }
             uint32_t g = 0;
             for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -545,7 +577,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
                     const uint32_t st = g % a.stages;
                     if (g >= (uint32_t)a.stages) mb_wait(&empty[st], ((g / a.stages) - 1) & 1);
                     unsigned char* sa = base + st * stage_bytes;
-                    mb_expect_tx(&full[st], stage_bytes);
+                    mb_expect_tx(&full[st], tx_bytes);
                     if (kc < nch)
                         tma_load_2d(sa, &map_in, kc * kChunkCols, (int)((int64_t)m * a.in_rows + row0), &full[st]);
                     else
@@ -553,7 +585,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
                                     &full[st]);
                     if (!a.b_resident) {
                         const int wcol = kc < nch ? kc * kChunkCols : a.kp + (kc - nch) * kChunkCols;
-                        tma_load_2d(sa + kChunkBytesA, &map_w, wcol, 0, &full[st]);
+                        tma_load_2d(sa + a_stage, &map_w, wcol, 0, &full[st]);
+                        if (a.split3) tma_load_2d(sa + a_stage + b_bytes, &map_wlo, wcol, 0, &full[st]);
                     }
                 }
             }
@@ -570,16 +603,54 @@ __global__ void __launch_bounds__(kGThreads, 1)
                 for (int kc = 0; kc < nk; ++kc, ++g) {
                     const uint32_t st = g % a.stages;
                     mb_wait(&full[st], (g / a.stages) & 1);
+                    if (a.split3) mb_wait(&conv[st], (g / a.stages) & 1);   // A split into hi / lo
                     tc_fence_after();
                     const uint32_t a0 = su32(base + st * stage_bytes);
-                    const uint32_t b0 = a.b_resident ? su32(b_res + (size_t)kc * b_bytes) : a0 + kChunkBytesA;
+                    const uint32_t b0 = a.b_resident ? su32(b_res + (size_t)kc * b_bytes) : a0 + a_stage;
+                    if (a.split3) {
+                        const uint32_t al = a0 + kChunkBytesA;
+                        const uint32_t bl = a.b_resident ? su32(b_res + (size_t)(nk + kc) * b_bytes) : b0 + b_bytes;
 #pragma unroll
-                    for (int k = 0; k < kChunkCols / 8; ++k)
-                        mma_tf32(d, sdesc(a0 + k * 32), sdesc(b0 + k * 32), a.idesc, (kc > 0 || k > 0) ? 1u : 0u);
+                        for (int k = 0; k < kChunkCols / 8; ++k) {
+                            mma_tf32(d, sdesc(al + k * 32), sdesc(b0 + k * 32), a.idesc, (kc > 0 || k > 0) ? 1u : 0u);
+                            mma_tf32(d, sdesc(a0 + k * 32), sdesc(bl + k * 32), a.idesc, 1u);
+                            mma_tf32(d, sdesc(a0 + k * 32), sdesc(b0 + k * 32), a.idesc, 1u);
+                        }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < kChunkCols / 8; ++k)
+                            mma_tf32(d, sdesc(a0 + k * 32), sdesc(b0 + k * 32), a.idesc, (kc > 0 || k > 0) ? 1u : 0u);
+                    }
                     mma_commit(&empty[st]);
                 }
                 mma_commit(&tfull[acc]);
             }
+        }
+    } else if (warp >= 2 + kGEpiWarps) {         // 3xTF32 converters: A chunk -> hi in place, lo beside it
+        if (a.split3) {
+            const int ct = threadIdx.x - (2 + kGEpiWarps) * 32;
+            uint32_t g = 0;
+            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x)
+                for (int kc = 0; kc < nk; ++kc, ++g) {
+                    const uint32_t st = g % a.stages;
+                    mb_wait(&full[st], (g / a.stages) & 1);
+                    uint4* hi4 = reinterpret_cast<uint4*>(base + st * stage_bytes);
+                    float4* lo4 = reinterpret_cast<float4*>(base + st * stage_bytes + kChunkBytesA);
+#pragma unroll 4
+                    for (int i = ct; i < kChunkBytesA / 16; i += kGConvWarps * 32) {
+                        const uint4 v = hi4[i];
+                        const uint4 h = make_uint4(v.x & 0xFFFFE000u, v.y & 0xFFFFE000u, v.z & 0xFFFFE000u,
+                                                   v.w & 0xFFFFE000u);
+                        lo4[i] = make_float4(__fsub_rn(__uint_as_float(v.x), __uint_as_float(h.x)),
+                                             __fsub_rn(__uint_as_float(v.y), __uint_as_float(h.y)),
+                                             __fsub_rn(__uint_as_float(v.z), __uint_as_float(h.z)),
+                                             __fsub_rn(__uint_as_float(v.w), __uint_as_float(h.w)));
+                        hi4[i] = h;
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> MMA reads
+                    __syncwarp();
+                    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&conv[st])) : "memory");
+                }
         }
     } else {                                     // epilogue warps: lane quarter warp % 4, column groups
         const int q = warp & 3;
@@ -630,8 +701,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
     if (warp == 1) tmem_dealloc(tmem, a.tmem_cols);
 }
 
-bool launch_sage_gemm(const void* map_in, const void* map_w, const void* map_mean, const SageLayerArgs& args_in,
-                      cudaStream_t s) {
+bool launch_sage_gemm(const void* map_in, const void* map_w, const void* map_wlo, const void* map_mean,
+                      const SageLayerArgs& args_in, cudaStream_t s) {
     int optin = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -639,17 +710,19 @@ bool launch_sage_gemm(const void* map_in, const void* map_w, const void* map_mea
     if (ensure_smem_k(k_sage_gemm, optin - 1024) != cudaSuccess) return false;
     SageLayerArgs a = args_in;
     if (a.n_inst > kMaxInst || a.npad % 16 || a.npad < 16 || a.npad > 256 || !map_mean) return false;
+    if (a.split3 && !map_wlo) return false;
+    const int64_t parts = a.split3 ? 2 : 1;                  // 3xTF32: A_lo beside A, W_lo beside W
     const int64_t nk = 2 * (int64_t)((a.k_in + kChunkCols - 1) / kChunkCols);
-    const int64_t w_all = nk * a.npad * 128;                  // every weight chunk of the layer
+    const int64_t w_all = parts * nk * a.npad * 128;          // every weight chunk of the layer
+    const int64_t a_st = parts * (int64_t)kChunkBytesA;
     const int64_t fixed = 1024 + (int64_t)((a.n_inst + 4) & ~3) * 4;
     const int64_t room = (int64_t)optin - 2048 - fixed;
     // keep the weights resident unless that leaves fewer A chunks in flight than streaming them
     // (A in flight is what the kernel's throughput follows: measured 132 vs 150 us at 7 vs 6 stages)
-    const int64_t st_res = w_all + 2 * (int64_t)kChunkBytesA <= room
-                               ? std::min<int64_t>(kGMaxStages, (room - w_all) / kChunkBytesA) : 0;
-    const int64_t st_str = std::min<int64_t>(kGMaxStages, room / (kChunkBytesA + (int64_t)a.npad * 128));
+    const int64_t st_res = w_all + 2 * a_st <= room ? std::min<int64_t>(kGMaxStages, (room - w_all) / a_st) : 0;
+    const int64_t st_str = std::min<int64_t>(kGMaxStages, room / (a_st + parts * (int64_t)a.npad * 128));
     a.b_resident = st_res >= st_str ? 1 : 0;
-    const int64_t stage = kChunkBytesA + (a.b_resident ? 0 : (int64_t)a.npad * 128);
+    const int64_t stage = a_st + (a.b_resident ? 0 : parts * (int64_t)a.npad * 128);
     const int64_t ring = room - (a.b_resident ? w_all : 0);
     a.stages = (int)std::max<int64_t>(2, std::min<int64_t>(kGMaxStages, ring / stage));
     const size_t smem = (size_t)fixed + (size_t)a.stages * stage + (a.b_resident ? (size_t)w_all : 0);
@@ -657,7 +730,8 @@ bool launch_sage_gemm(const void* map_in, const void* map_w, const void* map_mea
     while ((int)a.tmem_cols < 2 * a.npad) a.tmem_cols <<= 1;
     a.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(a.npad >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
     CUtensorMap mi = *(const CUtensorMap*)map_in, mw = *(const CUtensorMap*)map_w, mm = *(const CUtensorMap*)map_mean;
-    launch_k(k_sage_gemm, dim3(sms), dim3(kGThreads), smem, s, mi, mw, mm, a);
+    CUtensorMap ml = a.split3 ? *(const CUtensorMap*)map_wlo : mw;
+    launch_k(k_sage_gemm, dim3(sms), dim3(kGThreads), smem, s, mi, mw, ml, mm, a);
     count_launches(1, __func__, s);
     return true;
 }

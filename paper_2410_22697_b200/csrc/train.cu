@@ -500,6 +500,11 @@ __global__ void __launch_bounds__(kT) k_sgd_layers(SgdLayers d, float lr) {
             const float v = __fsub_rn(w[i], __fmul_rn(lr, g[i]));
             w[i] = v;
             g[i] = 0.0f;
+            if (i < rows * cols && d.whi[l]) {          // 3xTF32 operands of the forward GEMM
+                const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+                d.whi[l][i] = hi;
+                d.wlo[l][i] = __fsub_rn(v, hi);
+            }
             if (i < rows * cols && wt) {
                 const int64_t o = i / cols, c = i - o * cols;
                 wt[c * rows + o] = v;

@@ -23,8 +23,20 @@ U_TF32 = 2.0 ** -10
 U32 = 2.0 ** -24
 
 
-def error_bound(X, blocks, weights):
-    """Running elementwise bound on |GPU - exact| of every layer's output (see module doc)."""
+def gpu_precision() -> str:
+    """The forward GEMM's operand precision in this process: "3xtf32" (k_sage_gemm default), or "tf32"
+    (MGNN_SAGE_TF32=1, or the fused in-kernel aggregation MGNN_SAGE_SPLIT=0)."""
+    import os
+    if os.environ.get("MGNN_SAGE_TF32") == "1" or os.environ.get("MGNN_SAGE_SPLIT") == "0":
+        return "tf32"
+    return "3xtf32"
+
+
+def error_bound(X, blocks, weights, precision: str = "tf32"):
+    """Running elementwise bound on |GPU - exact| of every layer's output (see module doc).
+    precision "3xtf32": a = a_hi + a_lo, w = w_hi + w_lo exactly (TF32 hi parts), three TF32 products
+    a_hi w_hi + a_hi w_lo + a_lo w_hi, each within 3 u^2 |a||w| of a w (dropped a_lo w_lo, the TF32
+    conversion of the lo parts), accumulated in fp32 over 3K terms."""
     h = np.asarray(X, np.float64)
     e = np.zeros_like(h)
     L = len(weights)
@@ -33,7 +45,12 @@ def error_bound(X, blocks, weights):
         n = len(off) - 1
         ws, wn, b = (np.abs(np.asarray(a, np.float64)) for a in weights[l])
         K = 2 * h.shape[1]
-        c = 2 * U_TF32 + U_TF32 ** 2 + (K + 2) * U32
+        if precision == "3xtf32":
+            u_op = 3 * U_TF32 ** 2
+            c = u_op + (3 * K + 2) * U32
+        else:
+            u_op = 2 * U_TF32
+            c = 2 * U_TF32 + U_TF32 ** 2 + (K + 2) * U32
         mean_abs = np.zeros((n, h.shape[1]))
         mean_err = np.zeros((n, h.shape[1]))
         for i in range(n):
@@ -44,7 +61,7 @@ def error_bound(X, blocks, weights):
         mag = np.abs(h[:n]) @ ws.T + mean_abs @ wn.T
         ws_, wn_, b_ = (np.asarray(a, np.float64) for a in weights[l])
         z = S.sage_layer(h, n, np.asarray(off), np.asarray(nbr), ws_, wn_, b_, relu=False)
-        e = 2.0 * (c * mag + (e[:n] @ ws.T + mean_err @ wn.T) * (1 + 2 * U_TF32) + U32 * np.abs(z))
+        e = 2.0 * (c * mag + (e[:n] @ ws.T + mean_err @ wn.T) * (1 + u_op) + U32 * np.abs(z))
         h = np.maximum(z, 0.0) if l < L - 1 else z
     return e
 
@@ -61,7 +78,7 @@ def oracle_instance(op, step, fanouts, batch, run_seed=synth.RUN_SEED):
 
 
 def run_sage_parity(g, P, D, fanouts, batch, dims, windows, f_bp=2500, gamma=0.95, delta=0,
-                    inst_every=1, weight_seed=synth.SAGE_SEED, device=0, bind_x=False):
+                    inst_every=1, weight_seed=synth.SAGE_SEED, device=0, bind_x=False, precision=None):
     """Sample/gather windows on the GPU, run the consumer, compare every checked instance's
     logits with the fp64 oracle within error_bound.  Returns max |err| / bound."""
     import torch
@@ -102,7 +119,7 @@ def run_sage_parity(g, P, D, fanouts, batch, dims, windows, f_bp=2500, gamma=0.9
                 if (checked := checked + 1) % inst_every:
                     continue
                 ref = S.sage_forward(X, blocks, wts)[-1]
-                bound = error_bound(X, blocks, wts)
+                bound = error_bound(X, blocks, wts, precision or gpu_precision())
                 n0 = ref.shape[0]
                 got = got_all[m, :n0, :]
                 assert np.all(np.isfinite(got)), (pid, t + w)

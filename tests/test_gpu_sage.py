@@ -64,3 +64,14 @@ def test_reddit_width_features():
     last chunk), 41 classes, on a small graph."""
     g = synth.random_graph(700, 0.01, seed=41)
     run_sage_parity(g, 2, 602, [4, 8], 48, [602, 128, 41], [2])
+
+
+@pytest.mark.parametrize("tf32", ["0", "1"])
+def test_gemm_3xtf32_and_tf32(cfg1, tf32, monkeypatch):
+    """k_sage_gemm's operand precision: 3xTF32 (default: hi/lo split of A in shared memory and of W
+    in HBM, three TF32 products per term -- checked against the fp32-grade bound) and one TF32 pass
+    (MGNN_SAGE_TF32=1, the TF32 bound); wide layers (npad 256, streamed weights) included."""
+    monkeypatch.setenv("MGNN_SAGE_TF32", tf32)
+    run_sage_parity(cfg1, 2, 64, [10, 25], 256, synth.sage_dims(64, 2, 16), [3])
+    g = synth.random_graph(1200, 0.006, seed=77)
+    run_sage_parity(g, 2, 100, [5, 10, 15], 64, [100, 256, 256, 47], [2])
