@@ -28,8 +28,17 @@ constexpr int kSortItems = 8;
 constexpr int kSortTile = kSortThreads * kSortItems;  // 2048
 constexpr int kRadix = 256;
 
+// Small sorts (device-side n <= kSmallN, e.g. an eviction round's candidates) use 512-key tiles (2 keys
+// per thread): four times the blocks per pass, a quarter of the serial ranking rounds per block -- a
+// pass over a few ten thousand keys is bound by one tile's latency, not by bandwidth.
+constexpr int kSmallItems = 2;
+constexpr int kSmallTile = kSortThreads * kSmallItems;   // 512
+constexpr int64_t kSmallN = 65536;
+
 static inline int64_t sort_tiles(int64_t n_max) {
     int64_t t = (n_max + kSortTile - 1) / kSortTile;
+    const int64_t ts = (std::min<int64_t>(n_max, kSmallN) + kSmallTile - 1) / kSmallTile;   // small-mode tiles
+    t = std::max(t, ts);
     return t < 1 ? 1 : t;
 }
 
@@ -125,25 +134,20 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_binscan(const SortSeg* __
 //   k_sort_count   per tile: digit counts -> tcount[seg][tile][256]
 //   k_sort_scatter per tile: global offset of each digit = bin offset + counts of the earlier tiles
 //                  (independent loads, one column per thread), stable local ranks, scatter
-__global__ void __launch_bounds__(kSortThreads) k_sort_count(const SortSeg* __restrict__ segs, int passes, int p,
-                                                             int64_t tiles_max, SortScr scr) {
-    pdl_enter();
-    __shared__ uint32_t h[kRadix];
-    const int s = blockIdx.y;
-    const SortSeg sg = segs[s];
-    const int parity = scr.plan[(size_t)s * (passes + 1) + p];
-    if (parity < 0) return;
-    const int64_t n = *sg.n;
-    const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+template <int ITEMS>
+__device__ __forceinline__ void sort_count_body(const SortSeg& sg, int s, int passes, int p, int parity, int64_t n,
+                                                int64_t tiles_max, const SortScr& scr, uint32_t* h) {
+    constexpr int kTile = kSortThreads * ITEMS;
+    const int64_t ntiles = (n + kTile - 1) / kTile;
     const unsigned long long* kin = parity ? sg.keys_tmp : sg.keys;
     const int shift = sg.shift[p];
     const int lane = threadIdx.x & 31;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         h[threadIdx.x] = 0;
         __syncthreads();
-        const int64_t base = t * kSortTile;
+        const int64_t base = t * kTile;
 #pragma unroll
-        for (int i = 0; i < kSortItems; ++i) {
+        for (int i = 0; i < ITEMS; ++i) {
             const int64_t idx = base + (int64_t)i * kSortThreads + threadIdx.x;
             const unsigned digit = idx < n ? ((unsigned)(kin[idx] >> shift) & 0xFF) : (0x100u | lane);
             const unsigned peers = __match_any_sync(kFull, digit);
@@ -155,21 +159,31 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_count(const SortSeg* __re
     }
 }
 
+__global__ void __launch_bounds__(kSortThreads) k_sort_count(const SortSeg* __restrict__ segs, int passes, int p,
+                                                             int64_t tiles_max, SortScr scr) {
+    pdl_enter();
+    __shared__ uint32_t h[kRadix];
+    const int s = blockIdx.y;
+    const SortSeg sg = segs[s];
+    const int parity = scr.plan[(size_t)s * (passes + 1) + p];
+    if (parity < 0) return;
+    const int64_t n = *sg.n;
+    if (n <= kSmallN)
+        sort_count_body<kSmallItems>(sg, s, passes, p, parity, n, tiles_max, scr, h);
+    else
+        sort_count_body<kSortItems>(sg, s, passes, p, parity, n, tiles_max, scr, h);
+}
+
 // Stable local ranks with two block barriers per tile: warp w owns the contiguous items
 // [w * 256, (w + 1) * 256) of the tile (8 rounds of 32), ranks them inside the warp against a
 // warp-private digit counter row (match_any + __syncwarp only), then one pass over (digit, warp)
 // turns the per-warp counts into each warp's offset inside the tile's digit run.
-__global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const SortSeg* __restrict__ segs, int passes, int p,
-                                                               int64_t tiles_max, SortScr scr) {
-    pdl_enter();
-    __shared__ uint32_t wc[8][kRadix];     // per-warp digit counts, then the warp's offset in the digit run
-    __shared__ uint32_t gofs[kRadix];      // global offset of the tile's first item of each digit
-    const int s = blockIdx.y;
-    const SortSeg sg = segs[s];
-    const int parity = scr.plan[(size_t)s * (passes + 1) + p];
-    if (parity < 0) return;                    // beyond this segment's schedule, or a trivial digit
-    const int64_t n = *sg.n;
-    const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+template <int ITEMS>
+__device__ __forceinline__ void sort_scatter_body(const SortSeg& sg, int s, int passes, int p, int parity, int64_t n,
+                                                  int64_t tiles_max, const SortScr& scr, uint32_t (*wc)[kRadix],
+                                                  uint32_t* gofs) {
+    constexpr int kTile = kSortThreads * ITEMS;
+    const int64_t ntiles = (n + kTile - 1) / kTile;
     const unsigned long long* kin = parity ? sg.keys_tmp : sg.keys;
     const uint32_t* vin = parity ? sg.vals_tmp : sg.vals;
     unsigned long long* kout = parity ? sg.keys : sg.keys_tmp;
@@ -178,13 +192,13 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const SortSeg* __
     const unsigned lt = (1u << lane) - 1u;
     const int shift = sg.shift[p];
     const uint32_t* tc = scr.status + ((size_t)(s * passes + p) * tiles_max) * kRadix;
-    constexpr int kPerWarp = kSortTile / 8;    // 256 items per warp
+    constexpr int kPerWarp = kTile / 8;        // ITEMS * 32 items per warp
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t base = tile * kSortTile + (int64_t)warp * kPerWarp;
-        unsigned long long key[kSortItems];
-        uint32_t val[kSortItems], rank[kSortItems];
+        const int64_t base = tile * kTile + (int64_t)warp * kPerWarp;
+        unsigned long long key[ITEMS];
+        uint32_t val[ITEMS], rank[ITEMS];
 #pragma unroll
-        for (int i = 0; i < kSortItems; ++i) {         // every load of the tile in flight at once
+        for (int i = 0; i < ITEMS; ++i) {              // every load of the tile in flight at once
             const int64_t idx = base + i * 32 + lane;
             key[i] = idx < n ? kin[idx] : 0ull;
             val[i] = idx < n ? vin[idx] : 0u;
@@ -205,7 +219,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const SortSeg* __
         for (int d = lane; d < kRadix; d += 32) wc[warp][d] = 0;     // the warp's own counter row
         __syncwarp();
 #pragma unroll
-        for (int i = 0; i < kSortItems; ++i) {
+        for (int i = 0; i < ITEMS; ++i) {
             const bool valid = base + i * 32 + lane < n;
             const unsigned digit = valid ? ((unsigned)(key[i] >> shift) & 0xFF) : (0x100u | lane);
             const unsigned peers = __match_any_sync(kFull, digit);
@@ -228,7 +242,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const SortSeg* __
         }
         __syncthreads();
 #pragma unroll
-        for (int i = 0; i < kSortItems; ++i) {
+        for (int i = 0; i < ITEMS; ++i) {
             if (rank[i] == 0xFFFFFFFFu) continue;
             const unsigned digit = (unsigned)(key[i] >> shift) & 0xFF;
             const uint32_t pos = gofs[digit] + wc[warp][digit] + rank[i];
@@ -238,6 +252,22 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const SortSeg* __
         }
         __syncthreads();
     }
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_scatter(const SortSeg* __restrict__ segs, int passes, int p,
+                                                               int64_t tiles_max, SortScr scr) {
+    pdl_enter();
+    __shared__ uint32_t wc[8][kRadix];     // per-warp digit counts, then the warp's offset in the digit run
+    __shared__ uint32_t gofs[kRadix];      // global offset of the tile's first item of each digit
+    const int s = blockIdx.y;
+    const SortSeg sg = segs[s];
+    const int parity = scr.plan[(size_t)s * (passes + 1) + p];
+    if (parity < 0) return;                    // beyond this segment's schedule, or a trivial digit
+    const int64_t n = *sg.n;
+    if (n <= kSmallN)
+        sort_scatter_body<kSmallItems>(sg, s, passes, p, parity, n, tiles_max, scr, wc, gofs);
+    else
+        sort_scatter_body<kSortItems>(sg, s, passes, p, parity, n, tiles_max, scr, wc, gofs);
 }
 
 // ---- 4. an odd number of executed passes left the result in the tmp buffers: copy it back
