@@ -290,6 +290,8 @@ def random_load_peak(table_bytes=None):
 
 
 def git_head():
+    if os.environ.get("MGNN_GIT_HEAD"):          # the GPU box's copy has no .git: the caller passes it
+        return os.environ["MGNN_GIT_HEAD"]
     try:
         return subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], cwd=ROOT, capture_output=True,
                               text=True, timeout=10).stdout.strip() or None
@@ -666,6 +668,8 @@ def main():
         s_ach = s_bytes / (s_ms / 1e3) / 1e9 if s_ms > 0 else None
         tt_ = traffic_table(S.name)
         cfg_layers = len(cfg.fanouts)
+        # the gather variant that ran: the TMA row gather (gather4) when the hosted tables fit in L2
+        g_kernel = "k_gather_g4" if (tt_ or {}).get("k_gather_g4") else "k_gather_tma"
         # k_relabel is bound by dependent random probes of L2-resident (bits, position) pairs, not bytes:
         # probes per window (counted by the kernel) / its event time vs the measured L2 random-load ceiling
         rl_ms = sp_["relabel_ms"] / max(sp_["relabel_calls"], 1)
@@ -717,10 +721,10 @@ def main():
                                           "H2D) | lookup_gather + score_evict_refill + counts_read_async (D2H); "
                                           "host reads each window's counters; L2 flushed between windows"},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "hbm", "kernel": "k_gather_tma (classify + feature-row gather)",
+            "roofline": {"bound": "hbm", "kernel": f"{g_kernel} (classify + feature-row gather)",
                          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": (achieved / hbm_peak) if achieved else None,
-                         "traffic": (tt_ or {}).get("k_gather_tma"),
+                         "traffic": (tt_ or {}).get(g_kernel),
                          "traffic_source": (tt_ or {}).get("source"),
                          "peak_source": peak_src, "launch_ms": g_ms, "share_of_step": prof["gather_ms"] / step_ms_sum,
                          "algorithmic_bytes_per_launch": g_bytes,

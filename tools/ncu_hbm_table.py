@@ -56,8 +56,8 @@ def table(path, peak):
 def traffic_json(path, peak, config, out):
     import subprocess
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    head = subprocess.run(["git", "rev-parse", "--short=12", "HEAD"], cwd=root, capture_output=True,
-                          text=True).stdout.strip()
+    head = os.environ.get("MGNN_GIT_HEAD") or subprocess.run(   # the GPU box has no .git: passed in
+        ["git", "rev-parse", "--short=12", "HEAD"], cwd=root, capture_output=True, text=True).stdout.strip()
     d = {"config": config, "source": os.path.relpath(path, root), "git_head": head,
          "note": "ncu --cache-control none --clock-control none launch list: dram__bytes_read.sum + "
                  "dram__bytes_write.sum per launch (serialised launches), averaged per kernel",
@@ -65,7 +65,7 @@ def traffic_json(path, peak, config, out):
     for k, (n, t, rd, wr, _) in aggregate(path).items():
         d["kernels"][k] = {"launches": n, "us_per_launch": 1e6 * t / n, "dram_bytes_per_launch": (rd + wr) / n,
                            "frac_of_peak": (rd + wr) / t / 1e9 / peak if t else None}
-        if k.startswith("k_gather_tma") or k.startswith("k_hop") or k in ("k_compact", "k_relabel"):
+        if k.startswith("k_gather") or k.startswith("k_hop") or k in ("k_compact", "k_relabel"):
             d[k] = (rd + wr) / n
     with open(out, "w") as f:
         json.dump(d, f, indent=1)
