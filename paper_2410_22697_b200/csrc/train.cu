@@ -88,6 +88,39 @@ __global__ void __launch_bounds__(kT) k_relu_mask(MaskArgs a) {
     const int64_t n = a.hop_size[(int64_t)m * (kMaxLayers + 1) + a.hop];
     const int64_t n64 = (n + 63) / 64 * 64;
     const int q = a.ncols / 4;
+    if (kT % q == 0) {
+        // fixed column per thread (kT / q rows per block step): no per-element 64-bit division, and the
+        // bias gradient accumulates in registers with one shared atomic per thread and column
+        const int c4 = threadIdx.x % q;
+        const int rpi = kT / q;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t r = (int64_t)blockIdx.x * rpi + threadIdx.x / q; r < n64; r += (int64_t)gridDim.x * rpi) {
+            float4* dz = reinterpret_cast<float4*>(a.dz + ((int64_t)m * a.rows + r) * a.pitch) + c4;
+            if (r >= n) {
+                *dz = make_float4(0.f, 0.f, 0.f, 0.f);
+                continue;
+            }
+            const float4 h = *(reinterpret_cast<const float4*>(a.h + ((int64_t)m * a.h_rows + r) * a.h_pitch) + c4);
+            float4 g = *dz;
+            g.x = h.x > 0.0f ? g.x : 0.0f;
+            g.y = h.y > 0.0f ? g.y : 0.0f;
+            g.z = h.z > 0.0f ? g.z : 0.0f;
+            g.w = h.w > 0.0f ? g.w : 0.0f;
+            *dz = g;
+            acc.x += g.x;
+            acc.y += g.y;
+            acc.z += g.z;
+            acc.w += g.w;
+        }
+        if (acc.x != 0.0f) atomicAdd(&s_db[4 * c4], acc.x);
+        if (acc.y != 0.0f) atomicAdd(&s_db[4 * c4 + 1], acc.y);
+        if (acc.z != 0.0f) atomicAdd(&s_db[4 * c4 + 2], acc.z);
+        if (acc.w != 0.0f) atomicAdd(&s_db[4 * c4 + 3], acc.w);
+        __syncthreads();
+        for (int c = threadIdx.x; c < a.ncols; c += kT)
+            if (s_db[c] != 0.0f) atomicAdd(&a.db[c], s_db[c]);
+        return;
+    }
     for (int64_t e = (int64_t)blockIdx.x * kT + threadIdx.x; e < n64 * q; e += (int64_t)gridDim.x * kT) {
         const int64_t r = e / q;
         const int c4 = (int)(e - r * q);
