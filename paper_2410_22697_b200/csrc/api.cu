@@ -598,7 +598,8 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
         const size_t o_tk = o_hist2 + up(nseg * 4096 * 4);
         const size_t o_thr = o_tk + 256;
         const size_t o_nc = o_thr + up(nseg * 16);
-        ctx->ev_zero_bytes = o_nc + up(nseg * 8);
+        const size_t o_kth = o_nc + up(nseg * 8);
+        ctx->ev_zero_bytes = o_kth + up(nseg * 16);
         CK(dalloc((char**)&ctx->ev_zero, ctx->ev_zero_bytes));
         ctx->ev_sc.tilectr = (int32_t*)ctx->ev_zero;
         ctx->ev_sc.status = (unsigned long long*)(ctx->ev_zero + o_st);
@@ -607,6 +608,7 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
         ctx->ev_ev.ticket = (unsigned*)(ctx->ev_zero + o_tk);
         ctx->ev_ev.thr = (long long*)(ctx->ev_zero + o_thr);
         ctx->ev_ev.n_cand = (unsigned long long*)(ctx->ev_zero + o_nc);
+        ctx->ev_ev.kth = (unsigned long long*)(ctx->ev_zero + o_kth);
     }
     {   // large buffers: the K winners are sorted out of the compacted candidates (k_cand appends them
         // unordered, so E sorts all 8 key bytes; R's schedule already covers every byte that differs)

@@ -108,6 +108,7 @@ struct EvScratch {        // eviction-round scratch, zeroed per round
     unsigned* ticket;               // last-block detection of k_select
     long long* thr;                 // [2*n_lp][2] = {K, threshold digit T (-1: none)}
     unsigned long long* n_cand;     // [2*n_lp] candidates appended by k_cand
+    unsigned long long* kth;        // [2*n_lp][2] {1, exact K-th smallest key} when k_tie resolved ties, else 0
 };
 
 // Launch with programmatic stream serialization (PDL) unless MGNN_PDL=0; the kernel must call

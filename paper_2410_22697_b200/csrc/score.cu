@@ -273,6 +273,61 @@ __global__ void __launch_bounds__(kSThreads) k_hist2(const SortSeg* __restrict__
     }
 }
 
+// Ties beyond the two histogram levels: when the threshold bucket (the 24 key bits the histograms
+// see) still holds more than kCandMax keys beyond the K needed -- e.g. thousands of R nodes with the
+// same integer S_A at the threshold -- one block per list finds the exact K-th smallest key with four
+// more digit passes over the low 40 bits ([28,40), [16,28), [4,16), [0,4)); k_cand then keeps exactly
+// the K winners and k_rank's counting stays O(K^2).  Exits at once otherwise (one launch per round).
+// Rank path only (buffers <= kEvMax slots): the sort path is linear in its candidates.
+__global__ void __launch_bounds__(kSThreads) k_tie(const SortSeg* __restrict__ segs, EvScratch ev,
+                                                   const PartDev* __restrict__ parts, float alpha, float theta_r) {
+    pdl_enter();
+    __shared__ long long sm[8];
+    __shared__ long long T_sh, below_sh;
+    __shared__ uint32_t h[kDig];
+    const int sg = blockIdx.y;
+    const SortSeg S = segs[sg];
+    const PartDev* pd = parts ? parts + (sg >> 1) : nullptr;
+    const long long n = pd ? ((sg & 1) ? pd->n_h : pd->cap) : *S.n;
+    const long long nE = *segs[sg & ~1].n, nR = *segs[sg | 1].n;
+    const long long K = nE < nR ? nE : nR;
+    const uint32_t* hist = ev.hist + (size_t)sg * kDig;
+    find_threshold(hist, K, sm, &T_sh, &below_sh);
+    const long long T = T_sh;
+    long long below = below_sh;
+    if (T < 0 || below + (long long)hist[T] <= kCandMax) return;           // one level suffices
+    const uint32_t* hist2 = ev.hist2 + (size_t)sg * kDig;
+    find_threshold(hist2, K - below, sm, &T_sh, &below_sh);
+    const long long T2 = T_sh;
+    below += below_sh;
+    if (below + (long long)hist2[T2] - K <= kCandMax) return;              // two levels suffice
+    unsigned long long prefix = ((unsigned long long)T << 52) | ((unsigned long long)T2 << 40);
+    long long need = K - below;                                            // rank inside the bucket
+    const int lo_of[4] = {28, 16, 4, 0}, hi_of[4] = {40, 28, 16, 4};
+    for (int lv = 0; lv < 4; ++lv) {
+        const int lo = lo_of[lv], hi = hi_of[lv];
+        const unsigned mask = (1u << (hi - lo)) - 1u;
+        for (int d = threadIdx.x; d < kDig; d += kSThreads) h[d] = 0;
+        __syncthreads();
+        for (long long i = threadIdx.x; i < n; i += kSThreads) {
+            unsigned long long k = 0;
+            uint32_t v;
+            const bool c = pd ? ev_key(*pd, (sg & 1) == 0, i, alpha, theta_r, k, v) : (k = S.keys[i], true);
+            if (c && (k >> hi) == (prefix >> hi)) atomicAdd(&h[(unsigned)(k >> lo) & mask], 1u);
+        }
+        __syncthreads();
+        find_threshold(h, need, sm, &T_sh, &below_sh);
+        MGNN_CHECK(T_sh >= 0, "tie level %d: no threshold (need %lld)", lv, need);
+        prefix |= (unsigned long long)T_sh << lo;
+        need -= below_sh;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {                      // keys are unique: exactly K keys are <= prefix
+        ev.kth[2 * sg] = 1ull;
+        ev.kth[2 * sg + 1] = prefix;
+    }
+}
+
 // Every block derives K = min(|E|, |R|) of its partition and the threshold(s) of its list from the
 // histograms; block 0 records {K, T} for k_rank.
 __global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ segs, EvScratch ev,
@@ -302,6 +357,8 @@ __global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ 
     if (T < 0) return;
     const int lane = threadIdx.x & 31;
     const long long stride = (long long)gridDim.x * kSThreads;
+    const bool exact = ev.kth[2 * sg] != 0ull;   // k_tie resolved the K-th key exactly
+    const unsigned long long kth = ev.kth[2 * sg + 1];
     for (long long i0 = (long long)blockIdx.x * kSThreads + (threadIdx.x & ~31); i0 < n; i0 += stride) {
         const long long i = i0 + lane;
         unsigned long long k = 0;
@@ -310,7 +367,7 @@ __global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ 
         if (i < n) {
             const bool in = pd ? ev_key(*pd, (sg & 1) == 0, i, alpha, theta_r, k, v) : (k = S.keys[i], v = S.vals[i], true);
             const long long d1 = (long long)(k >> 52);
-            c = in && (d1 < T || (d1 == T && (long long)((k >> 40) & 0xFFF) <= T2));
+            c = in && (exact ? k <= kth : (d1 < T || (d1 == T && (long long)((k >> 40) & 0xFFF) <= T2)));
         }
         const unsigned ball = __ballot_sync(kFull, c);
         if (!ball) continue;
@@ -369,6 +426,7 @@ void launch_cand(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, con
                  float theta_r, cudaStream_t s) {
     const unsigned cap_blocks = scan_parts ? 256u : 64u;     // the scoreboard scan covers all of n_h
     dim3 g1(blocks_for(n_max, kSThreads) > cap_blocks ? cap_blocks : blocks_for(n_max, kSThreads), 2 * n_lp);
+    // (no k_tie here: the radix sort is linear in the candidates, ties only cost their sort passes)
     launch_k(k_hist2, g1, dim3(kSThreads), 0, s, segs, ev, scan_parts, alpha, theta_r);
     launch_k(k_cand, g1, dim3(kSThreads), 0, s, segs, ev, scan_parts, alpha, theta_r);
     count_launches(2, __func__, s);
@@ -379,10 +437,11 @@ void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev
     const unsigned cap_blocks = scan_parts ? 256u : 64u;
     dim3 g1(blocks_for(n_max, kSThreads) > cap_blocks ? cap_blocks : blocks_for(n_max, kSThreads), 2 * n_lp);
     launch_k(k_hist2, g1, dim3(kSThreads), 0, s, segs, ev, scan_parts, alpha, theta_r);
+    launch_k(k_tie, dim3(1, 2 * n_lp), dim3(kSThreads), 0, s, segs, ev, scan_parts, alpha, theta_r);
     launch_k(k_cand, g1, dim3(kSThreads), 0, s, segs, ev, scan_parts, alpha, theta_r);
     dim3 g2((unsigned)((n_max + kSThreads - 1) / kSThreads), 2 * n_lp);
     launch_k(k_rank, g2, dim3(kSThreads), 0, s, segs, ev);
-    count_launches(3, __func__, s);
+    count_launches(4, __func__, s);
 }
 
 // ------------------------------------------------------------------ swap + refill

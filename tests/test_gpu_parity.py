@@ -203,3 +203,33 @@ def test_products_remote_expansion_dense_scores_window():
     st = run_parity(g, 2, 100, [5, 10, 15], 2000, 5000, 0.995, 32, 1.0, [32], sample_every=16, check_x_rows=1024,
                     remote=True, dense=True)
     assert st["hits"] > 0 and st["misses"] > 0
+
+
+def test_eviction_ties_beyond_two_histogram_levels():
+    """thousands of replacement candidates tie at S_A = 1.0 (one miss each) at the K-th
+    key, beyond what the two 12-bit histogram levels can split (a 24-bit tie).  k_tie resolves the
+    exact K-th key (tie-break rank_deg, then id, R#18); the buffer after the round must equal the
+    oracle.  The oracle, run separately, shows that the condition held: the round admitted some
+    S_A = 1.0 nodes and left more than kCandMax (4096) tied ones out."""
+    from oracle import oracle as O
+    g = synth.generate(synth.CONFIGS["arxiv"])
+    P, D, fan, B, f_bp, gamma, delta = 2, 16, [10, 25], 1000, 1500, 0.5, 2
+    st = run_parity(g, P, D, fan, B, f_bp, gamma, delta, 1.0, [2, 2], check_x_rows=64)
+    assert st["evicted"] > 0
+    parts = synth.partition(g, P)
+    W = O.World(parts, D, synth.FEAT_SEED)
+    alpha = float(O.alpha_default(gamma, delta))
+    init = {}
+    for p in W.parts:
+        p.buffer_init(gamma, alpha, 1.0, delta, f_bp)
+        init[p] = p.buffer_state()["node_of_slot"].copy()
+    for t in range(1, 5):
+        for p in W.parts:
+            p.step(synth.RUN_SEED, t, fan, B)
+    for p in W.parts:
+        bs = p.buffer_state()
+        replaced = bs["node_of_slot"] != init[p]
+        admitted_tied = int(np.count_nonzero(bs["se"][replaced] == np.float32(1.0)))
+        left_tied = int(np.count_nonzero((bs["sa"] == np.float32(1.0)) & (bs["slot_of"] < 0)))
+        assert admitted_tied > 0 and left_tied > 4096, (admitted_tied, left_tied)
+    W.close()
