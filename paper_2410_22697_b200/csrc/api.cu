@@ -129,6 +129,7 @@ void fill_partdev(const mgnn_ctx_s* c, const Part& p, PartDev* d) {
     d->slot_h = p.slot_h;
     d->hitmask = p.hitmask;
     d->rank_deg = p.rank_deg;
+    d->deg_order = p.deg_order;
     d->perm = p.perm;
     d->halo_map = p.halo_map;
     (void)c;
@@ -182,7 +183,7 @@ void free_win(Win& w) {
 }
 
 void free_buffer(Part& p) {
-    dfree(p.rows); dfree(p.se); dfree(p.sa); dfree(p.slot_of); dfree(p.slot_h); dfree(p.hitmask); dfree(p.rank_deg);
+    dfree(p.rows); dfree(p.se); dfree(p.sa); dfree(p.slot_of); dfree(p.slot_h); dfree(p.hitmask); dfree(p.rank_deg); dfree(p.deg_order);
     dfree(p.ek); dfree(p.ekt); dfree(p.ev); dfree(p.evt); dfree(p.rk); dfree(p.rkt); dfree(p.rv); dfree(p.rvt);
 }
 
@@ -286,6 +287,8 @@ mgnn_status mgnn_ctx_create(int32_t device, int32_t n_parts, int64_t n_global, c
         const char* e = getenv("MGNN_EVICT_SORT");
         ctx->force_sort_path = e && (e[0] == '1' || e[0] == '2');
         ctx->sort_full_lists = e && e[0] == '2';
+        const char* e2 = getenv("MGNN_EV_SELECT");
+        ctx->ev_scan = e2 && e2[0] == '0';
     }
     ctx->tables.assign(n_parts, nullptr);
     mgnn_status st = MGNN_OK;
@@ -343,6 +346,7 @@ void mgnn_destroy(mgnn_ctx ctx) {
     dfree(ctx->d_gathered);
     dfree(ctx->d_evsegs);
     dfree(ctx->d_candsegs);
+    dfree(ctx->d_candsegs_hi);
     dfree(ctx->d_initsegs);
     dfree(ctx->d_sel_n);
     dfree(ctx->ev_zero);
@@ -552,6 +556,7 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
         CK(dalloc(&p.slot_h, p.cap));
         CK(dalloc(&p.hitmask, p.cap));
         CK(dalloc(&p.rank_deg, p.n_h));
+        CK(dalloc(&p.deg_order, p.n_h));
         CK(dalloc(&p.ek, p.cap)); CK(dalloc(&p.ekt, p.cap)); CK(dalloc(&p.ev, p.cap)); CK(dalloc(&p.evt, p.cap));
         CK(dalloc(&p.rk, p.n_h)); CK(dalloc(&p.rkt, p.n_h)); CK(dalloc(&p.rv, p.n_h)); CK(dalloc(&p.rvt, p.n_h));
         cap_max = std::max(cap_max, p.cap);
@@ -599,7 +604,9 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
         const size_t o_thr = o_tk + 256;
         const size_t o_nc = o_thr + up(nseg * 16);
         const size_t o_kth = o_nc + up(nseg * 8);
-        ctx->ev_zero_bytes = o_kth + up(nseg * 16);
+        const size_t o_tc2 = o_kth + up(nseg * 16);
+        const size_t o_st2 = o_tc2 + up(nseg * 4);
+        ctx->ev_zero_bytes = o_st2 + up(nseg * ctx->ev_tiles * 8);
         CK(dalloc((char**)&ctx->ev_zero, ctx->ev_zero_bytes));
         ctx->ev_sc.tilectr = (int32_t*)ctx->ev_zero;
         ctx->ev_sc.status = (unsigned long long*)(ctx->ev_zero + o_st);
@@ -609,6 +616,8 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
         ctx->ev_ev.thr = (long long*)(ctx->ev_zero + o_thr);
         ctx->ev_ev.n_cand = (unsigned long long*)(ctx->ev_zero + o_nc);
         ctx->ev_ev.kth = (unsigned long long*)(ctx->ev_zero + o_kth);
+        ctx->ev_sc2.tilectr = (int32_t*)(ctx->ev_zero + o_tc2);
+        ctx->ev_sc2.status = (unsigned long long*)(ctx->ev_zero + o_st2);
     }
     {   // large buffers: the K winners are sorted out of the compacted candidates (k_cand appends them
         // unordered, so E sorts all 8 key bytes; R's schedule already covers every byte that differs)
@@ -624,6 +633,16 @@ mgnn_status mgnn_buffer_init(mgnn_ctx ctx, const mgnn_policy* pol, mgnn_stream s
         dfree(ctx->d_candsegs);
         CK(dalloc(&ctx->d_candsegs, cs.size()));
         CK(cudaMemcpy(ctx->d_candsegs, cs.data(), cs.size() * sizeof(SortSeg), cudaMemcpyHostToDevice));
+        // candidates from the ordered lists (k_cand_ord keeps E in id order, R in rank_deg order): the
+        // stable sort needs the high word (the score) only
+        for (int lp = 0; lp < n_lp; ++lp) {
+            Part& p = ctx->parts[lp];
+            cs[2 * lp] = make_seg(p.ekt, p.evt, p.ek, p.ev, nc + 2 * lp, {32, 40, 48, 56});
+            cs[2 * lp + 1] = make_seg(p.rkt, p.rvt, p.rk, p.rv, nc + 2 * lp + 1, {32, 40, 48, 56});
+        }
+        dfree(ctx->d_candsegs_hi);
+        CK(dalloc(&ctx->d_candsegs_hi, cs.size()));
+        CK(cudaMemcpy(ctx->d_candsegs_hi, cs.data(), cs.size() * sizeof(SortSeg), cudaMemcpyHostToDevice));
     }
     {
         mgnn_status st2 = ensure_scratch(ctx, &ctx->sort_scr, &ctx->sort_scr_bytes,
@@ -1048,11 +1067,7 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
         // ordered E / R lists (k_select, default) or counts and histograms straight from the scoreboards
         // with the candidates re-derived from them (MGNN_EV_SELECT=0; measured slower on products:
         // count + candidate scans 97 us per round against 70 us for select + candidates on the lists)
-        static const bool ordered_select = [] {
-            const char* e = getenv("MGNN_EV_SELECT");
-            return !(e && e[0] == '0');
-        }();
-        const bool compact = ctx->sort_full_lists || ordered_select;
+        const bool compact = ctx->sort_full_lists || !ctx->ev_scan;
         const PartDev* scan = compact ? nullptr : ctx->d_parts;
         if (compact) {
             launch_select(ctx->d_parts, n_lp, nmax, ctx->pol.alpha, ctx->pol.theta_r, ctx->d_evsegs, ctx->d_sel_n,
@@ -1067,7 +1082,12 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
             launch_cand_rank(ctx->d_evsegs, n_lp, nmax, ctx->ev_ev, scan, ctx->pol.alpha, ctx->pol.theta_r, s);
         } else if (ctx->sort_full_lists) {
             radix_sort_pairs(ctx->d_evsegs, 2 * n_lp, nmax, ctx->ev_passes, ctx->sort_scr, s);
-        } else {                                   // threshold candidates, then sort only those
+        } else if (compact) {                      // threshold candidates in list order, sort their scores
+            launch_cand_ord(ctx->d_evsegs, n_lp, nmax, ctx->ev_ev, ctx->ev_sc2, ctx->ev_tiles, s);
+            radix_sort_pairs(ctx->d_candsegs_hi, 2 * n_lp, nmax, 4, ctx->sort_scr, s);
+            pairs = ctx->d_candsegs_hi;
+            k_of = ctx->ev_ev.thr;
+        } else {                                   // threshold candidates (unordered), sort all key bytes
             launch_cand(ctx->d_evsegs, n_lp, nmax, ctx->ev_ev, scan, ctx->pol.alpha, ctx->pol.theta_r, s);
             radix_sort_pairs(ctx->d_candsegs, 2 * n_lp, nmax, 8, ctx->sort_scr, s);
             pairs = ctx->d_candsegs;

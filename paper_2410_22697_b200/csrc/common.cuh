@@ -79,6 +79,7 @@ struct PartDev {
     int32_t* slot_h;           // [cap] halo index in slot
     unsigned long long* hitmask;  // [cap] bit w = hit at window step w
     int32_t* rank_deg;         // [n_h] position in the (deg_in desc, id asc) order (replacement tie-break)
+    int32_t* deg_order;        // [n_h] halo index at each position of that order (inverse of rank_deg)
     int32_t* perm;             // [perm_slots][n_train] epoch orders
     const int32_t* halo_map;   // [n_global] halo index or -1 (remote expansion only)
 };

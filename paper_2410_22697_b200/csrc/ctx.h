@@ -33,6 +33,7 @@ struct Part {
     int32_t* slot_h = nullptr;
     unsigned long long* hitmask = nullptr;
     int32_t* rank_deg = nullptr;
+    int32_t* deg_order = nullptr;        // inverse of rank_deg (R lists are compacted in this order)
     int32_t* perm = nullptr;
     int32_t perm_chunk = 1;              // G: epoch orders generated per sort call
     int64_t chunk_loaded[2] = {-1, -1};  // chunk id c (epochs [cG, cG+G)) held by ring half c % 2
@@ -119,14 +120,17 @@ struct mgnn_ctx_s {
     // eviction scratch
     SortSeg* d_evsegs = nullptr;
     SortSeg* d_candsegs = nullptr;       // the compacted candidates (E: all 8 key bytes; R: as d_evsegs)
+    SortSeg* d_candsegs_hi = nullptr;    // candidates in list order (k_cand_ord): the score digits only
     SortSeg* d_initsegs = nullptr;
     bool force_sort_path = false;        // MGNN_EVICT_SORT=1: always use the radix-sort eviction path
+    bool ev_scan = false;                // MGNN_EV_SELECT=0: no ordered lists, scoreboard scans
     bool sort_full_lists = false;        // MGNN_EVICT_SORT=2: sort the whole E / R lists, not the candidates
     int32_t ev_passes = 8;
     long long* d_sel_n = nullptr;
     char* ev_zero = nullptr;
     size_t ev_zero_bytes = 0;
     Scratch ev_sc{};
+    Scratch ev_sc2{};                  // k_cand_ord's look-back (same round as k_select's)
     EvScratch ev_ev{};
     int64_t ev_tiles = 1;
     void* sort_scr = nullptr;            // radix sort scratch of init / eviction (buffer stream)

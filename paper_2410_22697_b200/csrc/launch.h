@@ -163,6 +163,8 @@ void launch_ev_count(const PartDev* parts, int n_lp, int64_t n_max, float alpha,
 // nullptr: from the compacted lists of launch_select.
 void launch_cand_rank(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, const PartDev* scan_parts,
                       float alpha, float theta_r, cudaStream_t s);
+void launch_cand_ord(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, Scratch sc, int64_t tiles_max,
+                     cudaStream_t s);
 void launch_cand(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, const PartDev* scan_parts, float alpha,
                  float theta_r, cudaStream_t s);   // candidates only
 void launch_swap_refill(const PartDev* parts, int n_lp, int64_t cap_max, const SortSeg* segs, const long long* k_of,

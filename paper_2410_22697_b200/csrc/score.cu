@@ -63,7 +63,9 @@ void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, 
 }
 
 // ------------------------------------------------------------------ candidate selection
-// Segment 2*lp = E, 2*lp+1 = R; both scanned in halo (= id) order.  Scores here are >= +0, so
+// Segment 2*lp = E, 2*lp+1 = R; E scanned in halo (= id) order, R in the static (deg_in desc, id asc)
+// order of the buffer init, so each list is already in the order of its key's LOW word: a stable sort
+// of the high word (the score) alone yields the full key order (k_cand_ord + a 4-digit sort).  Scores here are >= +0, so
 // their IEEE bit patterns order like the values.  Order-preserving compaction by a decoupled
 // look-back scan, plus a warp-aggregated histogram of key >> 52 per list.
 __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict__ parts, float alpha, float theta_r,
@@ -88,8 +90,10 @@ __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict_
             const int64_t x = i0 + i;
             bool pf = false;
             if (x < n) {
-                const int32_t s = pd.slot_of[x];
-                pf = isE ? (s >= 0 && pd.se[s] < alpha) : (s < 0 && pd.sa[x] >= theta_r);
+                // E in halo (= id) order; R in the static (deg_in desc, id asc) order: x = rank_deg of h
+                const int64_t h = isE ? x : pd.deg_order[x];
+                const int32_t s = pd.slot_of[h];
+                pf = isE ? (s >= 0 && pd.se[s] < alpha) : (s < 0 && pd.sa[h] >= theta_r);
             }
             flags |= (unsigned)pf << i;
             cnt += pf;
@@ -115,8 +119,9 @@ __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict_
                     val = (uint32_t)pd.slot_of[x];
                     key = ((unsigned long long)__float_as_uint(pd.se[val]) << 32) | (uint32_t)pd.halo_ids[x];
                 } else {
-                    val = (uint32_t)x;
-                    key = ((unsigned long long)(~__float_as_uint(pd.sa[x])) << 32) | (uint32_t)pd.rank_deg[x];
+                    const int32_t h = pd.deg_order[x];
+                    val = (uint32_t)h;
+                    key = ((unsigned long long)(~__float_as_uint(pd.sa[h])) << 32) | (uint32_t)x;   // rank_deg[h] = x
                 }
                 MGNN_CHECK(pos < (isE ? pd.cap : n), "select pos=%lld n=%lld sg=%d", (long long)pos, (long long)n, sg);
                 out.keys[pos] = key;
@@ -384,6 +389,70 @@ __global__ void __launch_bounds__(kSThreads) k_cand(const SortSeg* __restrict__ 
     }
 }
 
+// Order-preserving variant for the compacted lists (k_select): tiles of 2048 list entries claimed in
+// order, block scan + decoupled look-back, so the candidates keep the list order -- E by id, R by
+// rank_deg, i.e. the order of each key's low word -- and the K winners need a stable sort of the HIGH
+// word only (4 digit passes instead of 8).  Same thresholds as k_cand.
+__global__ void __launch_bounds__(kSThreads) k_cand_ord(const SortSeg* __restrict__ segs, EvScratch ev, Scratch sc,
+                                                        int64_t tiles_max) {
+    pdl_enter();
+    __shared__ long long sm[8];
+    __shared__ long long T_sh, below_sh, T2_sh, below2_sh, prefix_sh;
+    __shared__ int tslot;
+    const int sg = blockIdx.y;
+    const SortSeg S = segs[sg];
+    const long long n = *S.n;
+    const long long nE = *segs[sg & ~1].n, nR = *segs[sg | 1].n;
+    const long long K = nE < nR ? nE : nR;
+    const uint32_t* hist = ev.hist + (size_t)sg * kDig;
+    find_threshold(hist, K, sm, &T_sh, &below_sh);
+    const long long T = T_sh;
+    const bool refined = T >= 0 && below_sh + (long long)hist[T] > kCandMax;
+    long long T2 = 0xFFF;
+    if (refined) {
+        find_threshold(ev.hist2 + (size_t)sg * kDig, K - below_sh, sm, &T2_sh, &below2_sh);
+        T2 = T2_sh;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ev.thr[2 * sg] = K;
+        ev.thr[2 * sg + 1] = T;
+    }
+    if (T < 0) return;                           // same answer in every block of the segment
+    const int64_t tile_items = kSThreads * 8;
+    const int64_t ntiles = (n + tile_items - 1) / tile_items;
+    const int tile = claim_tile(sc.tilectr + sg, &tslot);
+    if (tile >= ntiles) return;
+    const int64_t i0 = (int64_t)tile * tile_items + (int64_t)threadIdx.x * 8;
+    unsigned long long k[8];
+    unsigned flags = 0;
+    long long cnt = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        k[i] = i0 + i < n ? S.keys[i0 + i] : ~0ull;
+        const long long d1 = (long long)(k[i] >> 52);
+        const bool c = i0 + i < n && (d1 < T || (d1 == T && (long long)((k[i] >> 40) & 0xFFF) <= T2));
+        flags |= (unsigned)c << i;
+        cnt += c;
+    }
+    long long agg;
+    const long long excl = block_excl_scan256(cnt, sm, &agg);
+    if (threadIdx.x < 32) {
+        const unsigned long long pv = lookback_exclusive(sc.status + (int64_t)sg * tiles_max, tile,
+                                                         (unsigned long long)agg);
+        if (threadIdx.x == 0) prefix_sh = (long long)pv;
+    }
+    __syncthreads();
+    long long pos = prefix_sh + excl;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        if ((flags >> i) & 1u) {
+            S.keys_tmp[pos] = k[i];
+            S.vals_tmp[pos] = S.vals[i0 + i];
+            ++pos;
+        }
+    if (tile == ntiles - 1 && threadIdx.x == 0) ev.n_cand[sg] = (unsigned long long)(prefix_sh + agg);
+}
+
 // ------------------------------------------------------------------ rank by counting (unique keys)
 __global__ void __launch_bounds__(kSThreads) k_rank(const SortSeg* __restrict__ segs, EvScratch ev) {
     pdl_enter();
@@ -429,6 +498,17 @@ void launch_cand(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, con
     // (no k_tie here: the radix sort is linear in the candidates, ties only cost their sort passes)
     launch_k(k_hist2, g1, dim3(kSThreads), 0, s, segs, ev, scan_parts, alpha, theta_r);
     launch_k(k_cand, g1, dim3(kSThreads), 0, s, segs, ev, scan_parts, alpha, theta_r);
+    count_launches(2, __func__, s);
+}
+
+void launch_cand_ord(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev, Scratch sc, int64_t tiles_max,
+                     cudaStream_t s) {
+    const unsigned cap_blocks = 64u;
+    dim3 g1(blocks_for(n_max, kSThreads) > cap_blocks ? cap_blocks : blocks_for(n_max, kSThreads), 2 * n_lp);
+    launch_k(k_hist2, g1, dim3(kSThreads), 0, s, segs, ev, (const PartDev*)nullptr, 0.0f, 0.0f);
+    int64_t tiles = (n_max + kSThreads * 8 - 1) / (kSThreads * 8);
+    if (tiles < 1) tiles = 1;
+    launch_k(k_cand_ord, dim3((unsigned)tiles, 2 * n_lp), dim3(kSThreads), 0, s, segs, ev, sc, tiles_max);
     count_launches(2, __func__, s);
 }
 
@@ -532,6 +612,7 @@ __global__ void k_init_reset(const PartDev* __restrict__ pdp, const uint32_t* __
         pd.sa[h] = 0.0f;
         pd.slot_of[h] = -1;
         pd.rank_deg[order[h]] = (int32_t)h;
+        pd.deg_order[h] = (int32_t)order[h];
     }
 }
 

@@ -90,12 +90,16 @@ def test_arxiv_full_size_bench_config():
     assert st["evicted"] > 0
 
 
-@pytest.mark.parametrize("mode", ["1", "2"])
+@pytest.mark.parametrize("mode", ["1", "1s", "2"])
 @pytest.mark.parametrize("wins", [[4, 4, 4, 4], [8, 8, 8]])
 def test_cfg1_full_sort_eviction_path(cfg1, monkeypatch, wins, mode):
     """The large-buffer eviction paths give the same result: radix sort of the threshold
-    candidates only (1, the default above kEvMax slots) and of the whole E and R lists (2)."""
-    monkeypatch.setenv("MGNN_EVICT_SORT", mode)
+    candidates only (1, the default above kEvMax slots: candidates kept in list order, so only
+    the score digits are sorted), the same from unordered scoreboard scans (1s, all 8 key
+    bytes) and of the whole E and R lists (2)."""
+    monkeypatch.setenv("MGNN_EVICT_SORT", mode[0])
+    if mode == "1s":
+        monkeypatch.setenv("MGNN_EV_SELECT", "0")
     st = run_parity(cfg1, 2, 64, [10, 25], 256, 2500, 0.9, wins[0], 1.0, wins)
     assert st["evicted"] > 0
 
