@@ -273,6 +273,16 @@ def traffic_table(name: str):
         return None
 
 
+def gather_kernel_name(tt=None) -> str:
+    """The gather kernel the library launches (MGNN_GATHER, read once per process by libmgnn): flat
+    (default) -> k_gather_flat; tma -> k_gather_tma, or k_gather_g4 (TMA row gather) when the hosted
+    tables fit in L2 (named by the committed traffic table of the config); reg -> k_gather."""
+    e = os.environ.get("MGNN_GATHER", "flat")
+    if e.startswith("t"):
+        return "k_gather_g4" if (tt or {}).get("k_gather_g4") else "k_gather_tma"
+    return "k_gather" if e.startswith("r") else "k_gather_flat"
+
+
 def random_load_peak(table_bytes=None):
     """Measured random-load ceiling (profiles/r02/randread.json, tools/randread.cu): of an L2-resident
     table, or (table_bytes given) of the smallest measured table at least that large (DRAM-resident)."""
@@ -668,8 +678,7 @@ def main():
         s_ach = s_bytes / (s_ms / 1e3) / 1e9 if s_ms > 0 else None
         tt_ = traffic_table(S.name)
         cfg_layers = len(cfg.fanouts)
-        # the gather variant that ran: the TMA row gather (gather4) when the hosted tables fit in L2
-        g_kernel = "k_gather_g4" if (tt_ or {}).get("k_gather_g4") else "k_gather_tma"
+        g_kernel = gather_kernel_name(tt_)
         # k_relabel is bound by dependent random probes of L2-resident (bits, position) pairs, not bytes:
         # probes per window (counted by the kernel) / its event time vs the measured L2 random-load ceiling
         rl_ms = sp_["relabel_ms"] / max(sp_["relabel_calls"], 1)

@@ -596,6 +596,123 @@ __global__ void __launch_bounds__(kTWarps * 32) k_gather_g4(WinDev W, WorldDev G
     }
 }
 
+// ------------------------------------------------------------------ flat register variant
+// Same classification; a warp's chunk of R <= 32 consecutive frontier rows is copied as ONE flat run
+// of nrows * q float4 (q = pitch / 4): lane l moves elements l, l + 32, l + 64, ... so every load and
+// store instruction is fully active whatever q is (a 100-d row is 25 float4: the per-row loop of
+// k_gather leaves 7 of 32 lanes idle), UNR 16-byte loads are in flight per lane, and the X stores of
+// the chunk are contiguous.  No shared-memory staging: the sampling kernels of the next window can be
+// resident beside it.  Chunks are segment-aligned as in k_gather_tma (dyn == 2).
+constexpr int kFThreads = 256;
+constexpr int kFWarps = kFThreads / 32;
+template <int kFUnroll, int kMinBlocks>
+__global__ void __launch_bounds__(kFThreads, kMinBlocks) k_gather_flat(WinDev W, WorldDev G) {
+    pdl_enter();
+    if (*W.ovf <= W.step0 + (uint64_t)W.n_steps - 1) return;   // arena overflow: window skipped
+    __shared__ unsigned long long cnt_sh[4];
+    __shared__ long long seg_c[kMaxLayers + 2];
+    const int m = blockIdx.y;
+    const int lp = m / W.n_steps, w = m % W.n_steps;
+    const PartDev& pd = W.parts[lp];
+    const int64_t* hsm = W.hop_size + (int64_t)m * (kMaxLayers + 1);
+    const int R = 32;
+    if (threadIdx.x < 4) cnt_sh[threadIdx.x] = 0;
+    if (threadIdx.x < kMaxLayers + 2) seg_c[threadIdx.x] = 0;
+    __syncthreads();
+    // chunk c of segment s covers the same fraction of that segment in every instance (see k_gather_tma)
+    for (int mi = threadIdx.x; mi < W.n_inst; mi += blockDim.x) {
+        const int64_t* hsi = W.hop_size + (int64_t)mi * (kMaxLayers + 1);
+        for (int sgi = 0; sgi <= W.L; ++sgi) {
+            const long long len = sgi == 0 ? hsi[0] : hsi[sgi] - hsi[sgi - 1];
+            atomicMax(&seg_c[sgi + 1], (len + R - 1) / R);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int sgi = 1; sgi <= W.L + 1; ++sgi) seg_c[sgi] += seg_c[sgi - 1];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int pitch = W.pitch;
+    const int q = pitch >> 2;
+    const unsigned long long wbit = 1ull << w;
+    const int32_t* fr = W.fr_rank + (int64_t)m * W.ucap;
+    int32_t* fgid = W.fr_gid + (int64_t)m * W.ucap;
+    float4* X4 = reinterpret_cast<float4*>(W.X + (int64_t)m * W.ucap * pitch);
+    unsigned n_loc = 0, n_hit = 0, n_miss = 0, n_peer = 0;
+    const int64_t nchunks = seg_c[W.L + 1];
+    for (int64_t j = (int64_t)blockIdx.x * kFWarps + warp; j < nchunks; j += (int64_t)gridDim.x * kFWarps) {
+        int sgi = 0;
+        while (j >= seg_c[sgi + 1]) ++sgi;
+        const int64_t c = j - seg_c[sgi], C = seg_c[sgi + 1] - seg_c[sgi];
+        const int64_t s0 = sgi == 0 ? 0 : hsm[sgi - 1], len = sgi == 0 ? hsm[0] : hsm[sgi] - hsm[sgi - 1];
+        const int64_t a = s0 + c * len / C, b = s0 + (c + 1) * len / C;
+        if (b <= a) continue;
+        const int nrows = (int)(b - a);
+        // ---- classify the chunk's rows, one per lane
+        const float* src = nullptr;
+        int cls = 3;
+        if (lane < nrows) {
+            int32_t gid;
+            cls = classify(W, G, pd, fr[a + lane], wbit, src, gid);
+            fgid[a + lane] = gid;
+        }
+        n_loc += __popc(__ballot_sync(kFull, cls == 0));
+        n_hit += __popc(__ballot_sync(kFull, cls == 1));
+        n_miss += __popc(__ballot_sync(kFull, cls >= 2 && cls != 3));
+        n_peer += __popc(__ballot_sync(kFull, cls == 4));
+        // ---- flat copy: element e = row (e / q), column (e % q); rows of the chunk are contiguous in X
+        const int total = nrows * q;
+        float4* Xc = X4 + a * q;
+        int row = lane / q, col = lane - row * q;           // element `lane`, advanced by 32 per step
+        const int drow = 32 / q, dcol = 32 - drow * q;
+        for (int e0 = 0; e0 < total; e0 += 32 * kFUnroll) {
+            float4 v[kFUnroll];
+            int rr = row, cc = col;
+#pragma unroll
+            for (int u = 0; u < kFUnroll; ++u) {
+                const float4* sp = reinterpret_cast<const float4*>(
+                    __shfl_sync(kFull, (unsigned long long)src, rr & 31));
+                if (e0 + u * 32 + lane < total) v[u] = __ldg(sp + cc);
+                rr += drow;
+                cc += dcol;
+                if (cc >= q) {
+                    cc -= q;
+                    ++rr;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kFUnroll; ++u)
+                if (e0 + u * 32 + lane < total) __stcs(Xc + e0 + u * 32 + lane, v[u]);
+            row = rr;
+            col = cc;
+        }
+    }
+    if (lane == 0) {
+        if (n_loc) atomicAdd(&cnt_sh[0], (unsigned long long)n_loc);
+        if (n_hit) atomicAdd(&cnt_sh[1], (unsigned long long)n_hit);
+        if (n_miss) atomicAdd(&cnt_sh[2], (unsigned long long)n_miss);
+        if (n_peer) atomicAdd(&cnt_sh[3], (unsigned long long)n_peer);
+    }
+    __syncthreads();
+    long long* cn = W.counts + (int64_t)m * 8;
+    if (threadIdx.x == 0) {
+        if (cnt_sh[0]) atomicAdd((unsigned long long*)&cn[1], cnt_sh[0]);
+        if (cnt_sh[1]) atomicAdd((unsigned long long*)&cn[2], cnt_sh[1]);
+        if (cnt_sh[2]) {
+            atomicAdd((unsigned long long*)&cn[3], cnt_sh[2]);
+            atomicAdd((unsigned long long*)&cn[6], cnt_sh[2]);
+        }
+        if (cnt_sh[3]) atomicAdd((unsigned long long*)&cn[7], cnt_sh[3]);
+        const unsigned long long rows = cnt_sh[0] + cnt_sh[1] + cnt_sh[2];
+        if (rows && W.gathered_rows) atomicAdd((unsigned long long*)W.gathered_rows, rows);
+        if (W.prof_hm) {
+            if (cnt_sh[1]) atomicAdd((unsigned long long*)&W.prof_hm[0], cnt_sh[1]);
+            if (cnt_sh[2]) atomicAdd((unsigned long long*)&W.prof_hm[1], cnt_sh[2]);
+        }
+        if (blockIdx.x == 0) cn[0] = hsm[W.L];
+    }
+}
+
 void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, const GatherMaps* g4, cudaStream_t s) {
     // exactly one wave of 4 resident 256-thread blocks per SM in total (64 registers per thread):
     // floor, so no second, nearly empty wave leaves SMs idle at the tail
@@ -603,10 +720,49 @@ void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, con
     int64_t need = (w.ucap + kGWarps * 32 - 1) / (kGWarps * 32);
     unsigned gx = (unsigned)(need < target ? need : target);
     if (gx < 1) gx = 1;
-    static const int use_tma = [] {            // default: TMA bulk copies; MGNN_GATHER=reg forces registers
+    // MGNN_GATHER: flat (default) = k_gather_flat; tma = TMA bulk copies (k_gather_tma, or k_gather_g4 when
+    // the hosted tables fit in L2); reg = the per-row register gather of round 1.  Pipelined windows
+    // (tools/exp_window.py, sampling of the next window beside the gather, profiles/r02/gather_flat/):
+    // products 2.01 -> 1.91 ms, reddit 2.27 -> 2.03, papers_s32 2.05 -> 1.99, arxiv 0.220 -> 0.211, cfg1
+    // equal.  Alone the flat gather is slower on products (1.24 vs 1.14 ms) -- the TMA variants hold
+    // 192 KB of staging per SM, so the sampling kernels cannot be resident beside them.
+    static const int use_tma = [] {
         const char* e = getenv("MGNN_GATHER");
-        return e && e[0] == 'r' ? 0 : 1;
+        return e && e[0] == 't' ? 1 : 0;
     }();
+    static const bool use_flat = [] {
+        const char* e = getenv("MGNN_GATHER");
+        return !(e && (e[0] == 't' || e[0] == 'r'));
+    }();
+    static const int flat_bps = [] {
+        const char* e = getenv("MGNN_FLAT_BPS");
+        const int v = e ? atoi(e) : 0;
+        return v >= 1 && v <= 8 ? v : 4;
+    }();
+    if (use_flat) {
+        const int64_t tgt = std::max<int64_t>(1, ((int64_t)num_sms() * flat_bps) / w.n_inst);
+        const int64_t nd = (w.ucap + kFWarps * 32 - 1) / (kFWarps * 32);
+        const unsigned gxf = (unsigned)std::max<int64_t>(1, std::min(nd, tgt));
+        static const int flat_unr = [] {
+            const char* e = getenv("MGNN_FLAT_UNR");
+            return e ? atoi(e) : 4;
+        }();
+        const dim3 gf(gxf, w.n_inst), bf(kFThreads);
+        switch (flat_bps * 16 + flat_unr) {
+            case 3 * 16 + 8: launch_k(k_gather_flat<8, 3>, gf, bf, 0, s, w, world); break;
+            case 3 * 16 + 6: launch_k(k_gather_flat<6, 3>, gf, bf, 0, s, w, world); break;
+            case 4 * 16 + 6: launch_k(k_gather_flat<6, 4>, gf, bf, 0, s, w, world); break;
+            case 5 * 16 + 4: launch_k(k_gather_flat<4, 5>, gf, bf, 0, s, w, world); break;
+            case 5 * 16 + 2: launch_k(k_gather_flat<2, 5>, gf, bf, 0, s, w, world); break;
+            case 6 * 16 + 2: launch_k(k_gather_flat<2, 6>, gf, bf, 0, s, w, world); break;
+            case 4 * 16 + 2: launch_k(k_gather_flat<2, 4>, gf, bf, 0, s, w, world); break;
+            case 4 * 16 + 5: launch_k(k_gather_flat<5, 4>, gf, bf, 0, s, w, world); break;
+            case 4 * 16 + 8: launch_k(k_gather_flat<8, 4>, gf, bf, 0, s, w, world); break;
+            default: launch_k(k_gather_flat<4, 4>, gf, bf, 0, s, w, world); break;
+        }
+        count_launches(1, __func__, s);
+        return;
+    }
     // staging per warp: 2 stages of `stage` bytes; `bps` resident blocks per SM (one wave).  The
     // shared memory left on each SM is what the concurrently running sampling kernels can use.
     // 192 KB of staging per SM either way.  When the gathered tables fit in L2 (reads hit L2, the

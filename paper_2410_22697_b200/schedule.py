@@ -31,7 +31,7 @@ class PrepareAhead:
     def __init__(self, ctx, window: int, t0: int = 1, stream_b: Optional[torch.cuda.Stream] = None,
                  flush_bytes: int = 256 << 20,
                  host_seeds: Optional[Callable[[int, int], Tuple[int, int]]] = None, serial: bool = False,
-                 relabel_stream: bool = False):
+                 relabel_stream: bool = False, relabel_after_gather: bool = False):
         """window: steps per window (a window may end on an eviction step, never contain one earlier);
         t0: first global step (1-based, R#8); flush_bytes: L2 flush buffer written before every
         iteration (0 = none; B200 L2 is 126 MB); host_seeds(slot, t) -> (seeds_ptr, counts_ptr) of
@@ -39,7 +39,9 @@ class PrepareAhead:
         serial=True runs everything on stream B: consume(w), then sample(w+1) (no overlap);
         relabel_stream=True defers the columns' relabelling (mgnn_sampler_defer_relabel): window w's
         k_relabel runs on a third stream C beside its gather (L2-bound beside HBM-bound) and stream B
-        joins C before the iteration ends, so the window's blocks are final when its end event fires."""
+        joins C before the iteration ends, so the window's blocks are final when its end event fires;
+        relabel_after_gather=True starts that relabel only when window w's gather is done, i.e. beside its
+        scoring / eviction round (both latency-bound) instead of beside the HBM-bound gather."""
         self.ctx = ctx
         self.W = int(window)
         self.t = int(t0)
@@ -55,6 +57,8 @@ class PrepareAhead:
         self.relabel_stream = relabel_stream and not serial
         self.sC = torch.cuda.Stream(device=self.sB.device) if self.relabel_stream else None
         self.ev_relabeled = [torch.cuda.Event(), torch.cuda.Event()]
+        self.relabel_after_gather = relabel_after_gather and self.relabel_stream
+        self.ev_gathered = [torch.cuda.Event(), torch.cuda.Event()]
         ctx.defer_relabel(self.relabel_stream)
 
     # ---------------------------------------------------------------- the two halves
@@ -72,8 +76,17 @@ class PrepareAhead:
     def _consume(self, sl: int) -> None:
         self.sB.wait_event(self.ev_sampled[sl])
         self.ctx.lookup_gather(sl, self.sB)
+        if self.relabel_after_gather:
+            self.ev_gathered[sl].record(self.sB)
+            self.sC.wait_event(self.ev_gathered[sl])
+            self._relabel(sl)
         self.ctx.score(sl, self.sB)
         self.ev_done[sl].record(self.sB)
+
+    def _relabel(self, sl: int) -> None:
+        self.sC.wait_event(self.ev_sampled[sl])
+        self.ctx.relabel(sl, self.sC)
+        self.ev_relabeled[sl].record(self.sC)
 
     # ---------------------------------------------------------------- public
     def prime(self) -> None:
@@ -108,10 +121,8 @@ class PrepareAhead:
         else:
             if prepare_next:
                 self._sample(self.slot ^ 1, self.t + self.W)  # window w+1: sampling stream
-            if self.relabel_stream:                           # window w's blocks: third stream
-                self.sC.wait_event(self.ev_sampled[self.slot])
-                self.ctx.relabel(self.slot, self.sC)
-                self.ev_relabeled[self.slot].record(self.sC)
+            if self.relabel_stream and not self.relabel_after_gather:
+                self._relabel(self.slot)                      # window w's blocks: third stream
             self._consume(self.slot)                          # window w: buffer stream
             if self.relabel_stream:
                 sB.wait_event(self.ev_relabeled[self.slot])

@@ -2,9 +2,11 @@
 the first launch): each runs a cfg1 parity check in a fresh interpreter (-m gpu).
 
 * MGNN_GATHER=reg      -- register gather (k_gather<false> for narrow rows, <true> for >= 128 floats)
+* MGNN_GATHER=tma      -- TMA bulk copies (k_gather_g4 on these L2-resident tables; k_gather_tma with G4=0)
+* MGNN_FLAT_BPS / MGNN_FLAT_UNR -- other block counts / loads in flight of the default k_gather_flat
 * MGNN_PDL=0           -- plain launches instead of programmatic dependent launch
-* MGNN_GATHER_HINT=0/3 -- no L2 cache hints / table rows evict_last and X rows evict_first
-* MGNN_GATHER_HINT=10/14 (with MGNN_GATHER_G4=0) -- X rows stored through the LSU instead of bulk stores
+* MGNN_GATHER_HINT=0/3 -- (tma) no L2 cache hints / table rows evict_last and X rows evict_first
+* MGNN_GATHER_HINT=10/14 (tma, G4=0) -- X rows stored through the LSU instead of bulk stores
 """
 import os
 import subprocess
@@ -27,10 +29,17 @@ print("variant parity ok")
 """
 
 
-@pytest.mark.parametrize("env", [{"MGNN_GATHER": "reg"}, {"MGNN_PDL": "0"}, {"MGNN_GATHER_HINT": "0"},
-                                 {"MGNN_GATHER_HINT": "3"}, {"MGNN_GATHER_HINT": "10", "MGNN_GATHER_G4": "0"},
-                                 {"MGNN_GATHER_HINT": "14", "MGNN_GATHER_G4": "0"}])
+@pytest.mark.parametrize("env", [{"MGNN_GATHER": "reg"}, {"MGNN_GATHER": "tma"},
+                                 {"MGNN_GATHER": "tma", "MGNN_GATHER_G4": "0"},
+                                 {"MGNN_FLAT_BPS": "3", "MGNN_FLAT_UNR": "8"}, {"MGNN_FLAT_UNR": "6"},
+                                 {"MGNN_FLAT_BPS": "5", "MGNN_FLAT_UNR": "2"}, {"MGNN_PDL": "0"},
+                                 {"MGNN_GATHER": "tma", "MGNN_GATHER_HINT": "0"},
+                                 {"MGNN_GATHER": "tma", "MGNN_GATHER_HINT": "3"},
+                                 {"MGNN_GATHER": "tma", "MGNN_GATHER_HINT": "10", "MGNN_GATHER_G4": "0"},
+                                 {"MGNN_GATHER": "tma", "MGNN_GATHER_HINT": "14", "MGNN_GATHER_G4": "0"}],
+                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_variant_parity(env):
+    """cfg1 parity under one environment variant (ids: the variables, e.g. MGNN_GATHER=flat)."""
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT)], cwd=ROOT, env=e, capture_output=True,
                        text=True, timeout=600)

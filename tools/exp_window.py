@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--windows", type=int, default=12)
     ap.add_argument("--serial", action="store_true")
     ap.add_argument("--relabel-stream", action="store_true")
+    ap.add_argument("--relabel-after-gather", action="store_true")
+    ap.add_argument("--prio-b", action="store_true", help="buffer stream (gather + score) at high priority")
     ap.add_argument("--parts", type=int, default=None)
     ap.add_argument("--tag", default="")
     ap.add_argument("--sm-split", type=int, default=0, help="gather-side SMs of mgnn_sm_partition (0 = off)")
@@ -36,27 +38,39 @@ def main():
     ctx.buffer_init(S.gamma, PL.alpha_default(S.gamma, S.delta), 1.0, S.delta, S.f_bp)
     ctx.sampler_config(S.cfg.fanouts, S.cfg.batch, synth.RUN_SEED, S.window)
     sms = ctx.sm_partition(a.sm_split) if a.sm_split else (0, 0)
-    pipe = PrepareAhead(ctx, S.window, serial=a.serial, relabel_stream=a.relabel_stream)
+    sb = torch.cuda.Stream(priority=-1) if a.prio_b else None
+    pipe = PrepareAhead(ctx, S.window, serial=a.serial, stream_b=sb, relabel_stream=a.relabel_stream,
+                        relabel_after_gather=a.relabel_after_gather)
     for _ in range(4):
         pipe.iteration()
     torch.cuda.synchronize()
-    ctx.profile(True)
-    ctx.profile_stages()
+    # window times without per-stage events (those end the launches' programmatic overlap) ...
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.windows)]
     for i in range(a.windows):
         pipe.iteration(events=ev[i])
     torch.cuda.synchronize()
     ms = sorted(x.elapsed_time(y) for x, y in ev)
+    # ... then the stages of as many windows with them
+    ctx.profile(True)
+    ctx.profile_stages()
+    evp = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.windows)]
+    for i in range(a.windows):
+        pipe.iteration(events=evp[i])
+    torch.cuda.synchronize()
+    msp = sorted(x.elapsed_time(y) for x, y in evp)
     pr = ctx.profile_stages()
     n = max(pr["sample_calls"], 1)
     out = {"tag": a.tag, "config": a.config, "serial": a.serial, "env": {k: v for k, v in os.environ.items() if k.startswith("MGNN_")},
-           "ms_median": ms[len(ms) // 2], "ms_min": ms[0], "mb_per_s": S.window * S.ppg / (ms[len(ms) // 2] / 1e3),
+           "ms_median": ms[len(ms) // 2], "ms_min": ms[0], "ms_median_staged": msp[len(msp) // 2], "mb_per_s": S.window * S.ppg / (ms[len(ms) // 2] / 1e3),
            "sample_ms": pr["sample_ms"] / n, "gather_ms": pr["gather_ms"] / max(pr["gather_calls"], 1),
            "score_ms": pr["score_ms"] / max(pr["score_calls"], 1),
            "relabel_ms": pr["relabel_ms"] / max(pr["relabel_calls"], 1), "relabel_stream": a.relabel_stream,
            "relabel_probes": pr["relabel_probes"] / max(pr["relabel_calls"], 1),
            "edges": pr["edges"] / n, "frontier": pr["frontier"] / n, "unique": pr["unique"] / n,
-           "sm_split": sms}
+           "sm_split": sms, "prio_b": a.prio_b}
+    cn = ctx.counts(pipe.slot ^ 1)                  # the last consumed window: evictions per instance (col 4)
+    out["evicted_last_window"] = int(cn[:, 4].sum())
+    out["parts"] = [ctx.part_info(lp) for lp in range(S.ppg)]
     print(json.dumps(out), flush=True)
     ctx.close()
 
