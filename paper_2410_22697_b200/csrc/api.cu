@@ -25,6 +25,7 @@ static const bool g_debug_sync = [] {
 struct ProfRec {
     const char* who;
     cudaEvent_t a, b;
+    cudaStream_t s;
 };
 static bool g_kprof = false;
 static std::vector<ProfRec> g_kprof_recs;
@@ -42,7 +43,7 @@ void count_launches(long long n, const char* who, cudaStream_t s) {
         cudaEventRecord(e, s);
         for (auto& pl : g_kprof_last)
             if (pl.first == s) {
-                g_kprof_recs.push_back(ProfRec{who, pl.second, e});
+                g_kprof_recs.push_back(ProfRec{who, pl.second, e, s});
                 pl.second = e;
                 return;
             }
@@ -1242,6 +1243,24 @@ mgnn_status mgnn_profile_kernels(int32_t enable, char* report, int64_t report_le
             snprintf(line, sizeof(line), "%-28s %10.3f ms %8lld calls %9.2f us/call\n", a.first.c_str(), a.second.first,
                      a.second.second, 1e3 * a.second.first / (double)a.second.second);
             out += line;
+        }
+        if (getenv("MGNN_KPROF_TIMELINE") && !g_kprof_recs.empty()) {   // end time of every launch (us) on
+            out += "timeline (launcher stream end_us):\n";                 // one clock, base = first event
+            std::vector<cudaStream_t> ss;
+            for (auto& r : g_kprof_recs) {
+                float ms = 0.0f;
+                if (cudaEventElapsedTime(&ms, g_kprof_recs.front().a, r.b) != cudaSuccess) continue;
+                int si = -1;
+                for (size_t i = 0; i < ss.size(); ++i)
+                    if (ss[i] == r.s) si = (int)i;
+                if (si < 0) {
+                    si = (int)ss.size();
+                    ss.push_back(r.s);
+                }
+                char line[128];
+                snprintf(line, sizeof(line), "%s %d %.1f\n", r.who, si, 1e3 * ms);
+                out += line;
+            }
         }
         snprintf(report, (size_t)report_len, "%s", out.c_str());
     }

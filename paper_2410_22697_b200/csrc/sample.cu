@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kThreads) k_seeds(WinDev W) {
 // neighbours' ranks, write the columns (coalesced) and mark new nodes.
 template <typename IdxT>   // CSR index staged per sample: uint32_t when every index fits (halves the tile)
 __global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int hop, Scratch sc, int64_t tiles_max, int T,
-                                                                     int mark_filter, int align) {
+                                                                     int mark_filter, int align, int one_tile) {
     pdl_enter();
     __shared__ long long sm[8];
     __shared__ int tslot, n_draw;
@@ -171,8 +171,10 @@ __global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int
     const uint32_t c3 = ((uint32_t)pd.part_id << 8) | kStreamSample;
     const uint32_t step = (uint32_t)(W.step0 + (uint64_t)w);
     const int64_t h_below = pd.h_below, n_local = pd.n_local, lo = pd.lo;
-    // persistent: blocks claim tiles in order until the instance's frontier is exhausted
-    for (;;) {
+    // persistent: blocks claim tiles in order until the instance's frontier is exhausted (one_tile: a
+    // block takes one tile and exits, so blocks of other streams' kernels get SM slots as it runs)
+    for (int done = 0;; ++done) {
+        if (one_tile && done) break;
         if (threadIdx.x == 0) n_draw = 0;
         const int tile = claim_tile(sc.tilectr + m, &tslot);
         if (tile >= ntiles) {
@@ -303,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, MGNN_HOP_BLOCKS) k_hop(WinDev W, int
 // fbp catches up with fb for the next hop.
 // Persistent: a block claims the instance's word tiles in order until they run out (kernel start-up
 // -- PDL wait, constant loads -- was ~40 % of the stall samples with one short-lived block per tile).
-__global__ void __launch_bounds__(kThreads, 8) k_compact(WinDev W, int hop, Scratch sc, int64_t tiles_max) {
+__global__ void __launch_bounds__(kThreads, 8) k_compact(WinDev W, int hop, Scratch sc, int64_t tiles_max, int one_tile) {
     pdl_enter();
     __shared__ long long sm[8];
     __shared__ int tslot;
@@ -321,7 +323,8 @@ __global__ void __launch_bounds__(kThreads, 8) k_compact(WinDev W, int hop, Scra
     // arena bound of F_{hop+1} (mgnn_sampler_config_bounded): positions past it are not stored, the
     // size is clamped and the window is marked overflowed (every buffer-state kernel then skips it)
     const int64_t cap = hop + 1 < W.L ? W.off_stride[hop + 1] - 1 : W.ucap;
-    for (;;) {
+    for (int done = 0;; ++done) {
+        if (one_tile && done) break;
         const int tile = claim_tile(sc.tilectr + m, &tslot);
         if (tile >= ntiles) break;
         const int64_t wd0 = (int64_t)tile * kWordTile + (int64_t)threadIdx.x * kCWords;   // 4 consecutive words
@@ -493,8 +496,13 @@ void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t
     const int64_t tiles_max = scan_tiles_count(fcap);          // scratch stride (64-node tiles)
     // persistent blocks (~5 resident per SM in total); each loops over claimed tiles
     int64_t tiles = (fcap + T - 1) / T;
-    const int64_t target = ((int64_t)num_sms() * MGNN_HOP_BLOCKS + w.n_inst - 1) / w.n_inst;
-    if (tiles > target) tiles = target;
+    static const int grid_bps = [] {                 // resident-block cap of the persistent grid per SM
+        const char* e = getenv("MGNN_HOP_GRID_BPS");  // (0 = one block per tile, not persistent)
+        const int v = e ? atoi(e) : MGNN_HOP_BLOCKS;
+        return v >= 0 && v <= 64 ? v : MGNN_HOP_BLOCKS;
+    }();
+    const int64_t target = ((int64_t)num_sms() * grid_bps + w.n_inst - 1) / w.n_inst;
+    if (grid_bps > 0 && tiles > target) tiles = target;
     if (tiles < 1) tiles = 1;
     dim3 grid((unsigned)tiles, w.n_inst);
     ensure_smem_k(k_hop<uint64_t>, 256 * MGNN_MAX_FANOUT * 8);
@@ -511,10 +519,10 @@ void launch_hop(const WinDev& w, int hop, int64_t fcap, Scratch sc, cudaStream_t
     }();
     if (w.idx32 && !(f64 && f64[0] == '1'))
         launch_k(k_hop<uint32_t>, grid, dim3(kThreads), (size_t)T * w.k_hop[hop] * 4, s, w, hop, sc, tm, T, mark_filter,
-                 align);
+                 align, grid_bps == 0 && !align ? 1 : 0);
     else
         launch_k(k_hop<uint64_t>, grid, dim3(kThreads), (size_t)T * w.k_hop[hop] * 8, s, w, hop, sc, tm, T, mark_filter,
-                 align);
+                 align, grid_bps == 0 && !align ? 1 : 0);
     count_launches(1, __func__, s);
 }
 
@@ -524,12 +532,12 @@ void launch_compact(const WinDev& w, int hop, Scratch sc, cudaStream_t s) {
     static const int per_sm = [] {
         const char* e = getenv("MGNN_COMPACT_BPS");
         const int v = e ? atoi(e) : 8;
-        return v >= 1 && v <= 64 ? v : 8;
+        return v >= 0 && v <= 64 ? v : 8;            // 0: one block per tile (not persistent)
     }();
     int64_t gx = ((int64_t)num_sms() * per_sm + w.n_inst - 1) / w.n_inst;
-    if (gx > tiles) gx = tiles;
+    if (per_sm == 0 || gx > tiles) gx = tiles;
     dim3 grid((unsigned)(gx < 1 ? 1 : gx), w.n_inst);
-    launch_k(k_compact, grid, dim3(kThreads), 0, s, w, hop, sc, (int64_t)(tiles < 1 ? 1 : tiles));
+    launch_k(k_compact, grid, dim3(kThreads), 0, s, w, hop, sc, (int64_t)(tiles < 1 ? 1 : tiles), per_sm == 0 ? 1 : 0);
     count_launches(1, __func__, s);
 }
 

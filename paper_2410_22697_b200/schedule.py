@@ -31,7 +31,7 @@ class PrepareAhead:
     def __init__(self, ctx, window: int, t0: int = 1, stream_b: Optional[torch.cuda.Stream] = None,
                  flush_bytes: int = 256 << 20,
                  host_seeds: Optional[Callable[[int, int], Tuple[int, int]]] = None, serial: bool = False,
-                 relabel_stream: bool = False, relabel_after_gather: bool = False):
+                 relabel_stream: bool = False, relabel_after_gather: bool = False, score_after_sample: bool = False):
         """window: steps per window (a window may end on an eviction step, never contain one earlier);
         t0: first global step (1-based, R#8); flush_bytes: L2 flush buffer written before every
         iteration (0 = none; B200 L2 is 126 MB); host_seeds(slot, t) -> (seeds_ptr, counts_ptr) of
@@ -55,10 +55,15 @@ class PrepareAhead:
         self.host_seeds = host_seeds
         self.primed = False
         self.relabel_stream = relabel_stream and not serial
-        self.sC = torch.cuda.Stream(device=self.sB.device) if self.relabel_stream else None
+        # the relabel stream takes stream B's priority: both carry window w, which the iteration waits for;
+        # stream A (the next window's sampling) has the slack
+        self.sC = (torch.cuda.Stream(device=self.sB.device, priority=self.sB.priority) if self.relabel_stream
+                   else None)
         self.ev_relabeled = [torch.cuda.Event(), torch.cuda.Event()]
         self.relabel_after_gather = relabel_after_gather and self.relabel_stream
         self.ev_gathered = [torch.cuda.Event(), torch.cuda.Event()]
+        self.score_after_sample = score_after_sample and not serial
+        self._next_sampled = False
         ctx.defer_relabel(self.relabel_stream)
 
     # ---------------------------------------------------------------- the two halves
@@ -80,6 +85,8 @@ class PrepareAhead:
             self.ev_gathered[sl].record(self.sB)
             self.sC.wait_event(self.ev_gathered[sl])
             self._relabel(sl)
+        if self.score_after_sample and self._next_sampled:
+            self.sB.wait_event(self.ev_sampled[sl ^ 1])   # the eviction round after the next window's sampling
         self.ctx.score(sl, self.sB)
         self.ev_done[sl].record(self.sB)
 
@@ -119,6 +126,7 @@ class PrepareAhead:
             if prepare_next:
                 self._sample(self.slot ^ 1, self.t + self.W)
         else:
+            self._next_sampled = prepare_next
             if prepare_next:
                 self._sample(self.slot ^ 1, self.t + self.W)  # window w+1: sampling stream
             if self.relabel_stream and not self.relabel_after_gather:

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--relabel-stream", action="store_true")
     ap.add_argument("--relabel-after-gather", action="store_true")
     ap.add_argument("--prio-b", action="store_true", help="buffer stream (gather + score) at high priority")
+    ap.add_argument("--score-after-sample", action="store_true")
+    ap.add_argument("--kprof", action="store_true", help="per-launch event times on each stream (stderr)")
     ap.add_argument("--parts", type=int, default=None)
     ap.add_argument("--tag", default="")
     ap.add_argument("--sm-split", type=int, default=0, help="gather-side SMs of mgnn_sm_partition (0 = off)")
@@ -40,7 +42,7 @@ def main():
     sms = ctx.sm_partition(a.sm_split) if a.sm_split else (0, 0)
     sb = torch.cuda.Stream(priority=-1) if a.prio_b else None
     pipe = PrepareAhead(ctx, S.window, serial=a.serial, stream_b=sb, relabel_stream=a.relabel_stream,
-                        relabel_after_gather=a.relabel_after_gather)
+                        relabel_after_gather=a.relabel_after_gather, score_after_sample=a.score_after_sample)
     for _ in range(4):
         pipe.iteration()
     torch.cuda.synchronize()
@@ -67,7 +69,19 @@ def main():
            "relabel_ms": pr["relabel_ms"] / max(pr["relabel_calls"], 1), "relabel_stream": a.relabel_stream,
            "relabel_probes": pr["relabel_probes"] / max(pr["relabel_calls"], 1),
            "edges": pr["edges"] / n, "frontier": pr["frontier"] / n, "unique": pr["unique"] / n,
-           "sm_split": sms, "prio_b": a.prio_b}
+           "sm_split": sms, "prio_b": a.prio_b, "score_after_sample": a.score_after_sample}
+    if a.kprof:
+        import ctypes as C
+        from paper_2410_22697_b200 import _lib
+        L = _lib.load()
+        torch.cuda.synchronize()
+        L.mgnn_profile_kernels(1, None, 0)
+        for i in range(a.windows):
+            pipe.iteration()
+        torch.cuda.synchronize()
+        buf = C.create_string_buffer(1 << 22)
+        L.mgnn_profile_kernels(0, buf, len(buf))
+        print(f"[kprof {a.config} {a.tag}] per launcher, {a.windows} windows:\n" + buf.value.decode(), file=sys.stderr)
     cn = ctx.counts(pipe.slot ^ 1)                  # the last consumed window: evictions per instance (col 4)
     out["evicted_last_window"] = int(cn[:, 4].sum())
     out["parts"] = [ctx.part_info(lp) for lp in range(S.ppg)]
