@@ -3,6 +3,7 @@
 # HEAD, the bench command's launch list, and (part "multi") the 2- / 4-GPU tests and scaling lines.
 #
 #   tools/evidence_r02.sh single    # 1 GPU: bench lines, ncu tables
+#   tools/evidence_r02.sh traffic   # 1 GPU: only the per-config ncu DRAM tables
 #   tools/evidence_r02.sh multi N   # N GPUs: test_multi + bench at N for products (P=2N) and papers_s32 (P=8)
 # Output under gpurun_out/evidence/ (copied into profiles/r02/ by hand after review).
 set -u
@@ -10,7 +11,7 @@ OUT=gpurun_out/evidence
 mkdir -p $OUT
 part=${1:-single}
 
-if [ "$part" = single ]; then
+if [ "$part" = single ] || [ "$part" = traffic ]; then
     # 1. per-config DRAM traffic of every library kernel (cache-control none: in-situ bytes); the tables
     #    also go to profiles/r02/ on this box so the bench lines below read the HEAD numbers
     for c in cfg1 arxiv reddit products papers_s32; do
@@ -21,6 +22,7 @@ if [ "$part" = single ]; then
         python tools/ncu_hbm_table.py $OUT/launches_$c.csv --json $OUT/traffic_$c.json --config $c \
             > $OUT/table_$c.txt 2>&1 && cp $OUT/traffic_$c.json profiles/r02/traffic_$c.json
     done
+    [ "$part" = traffic ] && exit 0
     # 2. bench lines (the driver's default command first), each under its own timeout
     timeout 900 python bench.py > $OUT/bench_products.json 2> $OUT/bench_products.err
     for c in cfg1 arxiv reddit papers_s32; do
