@@ -903,11 +903,12 @@ def extras(args, S, ctx, pipe, t_start, slot, world, barrier, max_over_ranks, mb
             "consumer_ms_per_step": fwd_ms, "consumer_launches_per_step": 2 * L_,
             "pipeline": "3 streams: sample(w+2) | gather+score(w+1) | forward(w), timed as one span",
             "kernel": "k_mean (neighbour means, all SMs) + k_sage_gemm (warp-specialised: TMA ring of self "
-                      "rows / means / weights -> tcgen05.mma kind::tf32 into 2 TMEM accumulators -> "
+                      "rows / means / weights -> tcgen05.mma kind::tf32, 3 products per term (3xTF32), into 2 TMEM accumulators -> "
                       "bias/ReLU epilogue warps)",
             "tflops": flops / (fwd_ms / 1e3) / 1e12 if fwd_ms > 0 else None,
             "agg_gbs": agg_bytes / (fwd_ms / 1e3) / 1e9 if fwd_ms > 0 else None,
-            "dtype": "tf32 x tf32 -> f32"}}
+            "dtype": ("tf32 x tf32 -> f32" if os.environ.get("MGNN_SAGE_TF32") == "1"
+                      else "3xtf32 (hi/lo split, fp32-grade products) -> f32")}}
     try:
         out.update(_train_extras(args, S, ctx, WINDOW, world, barrier, max_over_ranks, K, prep_ms, sA, sB, sC,
                                  ev_sampled, ev_done, ev_gathered, flush, slot, t_c, dims, lr_=0.01))
@@ -1038,7 +1039,8 @@ def _train_extras(args, S, ctx, WINDOW, world, barrier, max_over_ranks, K, prep_
             "mean_loss_in_timed_steps": tr_loss,
             "pipeline": "3 streams: sample(w+2) | gather+score(w+1) | DDP steps of window w",
             "cuda_graph": bool(use_graph[0]),
-            "dtype": "tf32 x tf32 -> f32",
+            "dtype": ("tf32 x tf32 -> f32" if os.environ.get("MGNN_SAGE_TF32") == "1"
+                      else "3xtf32 (forward and backward GEMMs) -> f32"),
             # Eq.4-5 per window; overlap efficiency read as the trainer's busy
             # fraction t_DDP / T (1 = the preparation is fully hidden; DESIGN R#31)
             "stage_model": {

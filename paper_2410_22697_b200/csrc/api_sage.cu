@@ -454,6 +454,7 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
         wa.npad = S.npad[l];
         wa.dw = S.grads + S.w_off[l];
         wa.max_chunks = (int64_t)n_lp * ((S.out_rows[l] + 63) / 64);
+        wa.split3 = S.split3 ? 1 : 0;
         // the weight gradient only reads dZ, H and the means: it runs on the side stream while the
         // input gradient and the next layer's mask proceed on `s` (joined before returning)
         CK(cudaEventRecord(S.ev_fork[l], s));
@@ -483,6 +484,7 @@ mgnn_status mgnn_sage_train_step(mgnn_ctx ctx, int32_t slot, int32_t step_in_win
             da.dh_pitch = S.npad[l - 1];
             da.dmean = S.dmean;
             da.dmean_rows = S.out_rows[l];
+            da.split3 = S.split3 ? 1 : 0;
             if (!launch_dgrad(S.map_dz128[l], S.map_wt[l], da, s))
                 return joined(fail(ctx, MGNN_ECUDA, "train: dgrad launch configuration failed"));
             launch_scatter(da, s);

@@ -279,6 +279,7 @@ struct WgradArgs {             // dW[npad][2 kp] += dZ^T [H | mean] over the ste
     float* dw;                 // [npad][2 kp]
     int64_t max_chunks;        // upper bound of the step's 64-row chunks (host hint for the K split)
     int32_t ksplit;            // CTAs per (M-tile, N-tile), set by the launcher
+    int32_t split3;            // 3xTF32 (fp32-grade products), else one TF32 pass
 };
 bool launch_wgrad(const WgradArgs& a, cudaStream_t s);
 
@@ -297,6 +298,7 @@ struct DgradArgs {             // dH[i] += dZ_i W_self; dH[j] += dZ_i W_neigh / 
     int64_t dh_rows, dh_pitch;
     float* dmean;              // [M][dmean_rows][kp]: dZ_i W_neigh / deg(i), scattered by k_scatter
     int64_t dmean_rows;
+    int32_t split3;            // 3xTF32: dZ and Wt tiles split into hi / lo in shared memory
 };
 bool launch_dgrad(const void* map_dz, const void* map_wt, const DgradArgs& a, cudaStream_t s);
 // dH[j] += dmean[i] for every sampled neighbour j of dst row i (warp per row, vector atomics)

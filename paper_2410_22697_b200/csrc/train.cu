@@ -164,13 +164,20 @@ __global__ void __launch_bounds__(kT) k_zero_rows(ZeroRowsArgs a) {
 // CTA's threads load each 64-row chunk and store it TRANSPOSED into the K-major SWIZZLE_128B
 // layout (operand row = o or c, 128-byte rows of 32 consecutive K values, 16-byte unit u of
 // row x at u ^ (x % 8)); rows past |F_h| and columns past the data read as zero.
-constexpr int kWRows = 64;                       // K rows per chunk
+// 3xTF32 (SPLIT, DESIGN R#29): the threads split every value into hi (low 13 mantissa bits cleared) and
+// lo = v - hi while transposing, so a stage holds A_hi | A_lo | B_hi | B_lo of a 32-row chunk (the same
+// 64 KB as the TF32 stage's A | B of 64 rows), and each K step issues a_lo b_hi + a_hi b_lo + a_hi b_hi.
 constexpr int kWRegion = 128 * 128;              // 128 operand rows x 32 K values (fp32): 16 KB
-constexpr int kWStage = 4 * kWRegion;            // A and B, 2 K-regions each: 64 KB
+constexpr int kWStage = 4 * kWRegion;            // 4 regions: A and B x 2 K-regions, or A/B x hi/lo
 constexpr int kWMaxInst = 256;
 
+__device__ __forceinline__ float tf32_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
+
 constexpr int kWThreads = 1024;                   // 8 threads per operand row: 8x the loads in flight
+template <bool SPLIT>
 __global__ void __launch_bounds__(kWThreads, 1) k_wgrad(WgradArgs a) {
+    constexpr int kWRows = SPLIT ? 32 : 64;      // K rows per chunk
+    constexpr int kNReg = kWRows / 32;           // K-regions per operand part
     extern __shared__ __align__(1024) unsigned char dsm[];
     __shared__ __align__(8) uint64_t bar_empty[2], bar_done;
     __shared__ uint32_t tmem_sh;
@@ -259,15 +266,29 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wgrad(WgradArgs a) {
         const int i = c - c_lo, st = i & 1;
         if (i >= 2) mb_wait(&bar_empty[st], ((i >> 1) - 1) & 1);   // MMAs of chunk c-2 read this stage
         if (c + 1 < c_hi) load_chunk(c + 1, na, nb);
-        unsigned char* sa = base + st * kWStage;
-        unsigned char* sb = sa + 2 * kWRegion;
+        unsigned char* sa = base + st * kWStage;                      // A (hi)
+        unsigned char* sb = sa + (SPLIT ? 2 : 1) * kNReg * kWRegion;   // B (hi)
 #pragma unroll
         for (int g = 0; g < kQ; ++g) {
             const int k4 = q * kQ + g;
             const int reg = k4 >> 3, u = k4 & 7;            // 32 K values per region, 8 units of 4
             const uint32_t off = (uint32_t)(reg * kWRegion + x * 128 + ((u ^ (x & 7)) << 4));
-            *reinterpret_cast<float4*>(sa + off) = make_float4(ca[g][0], ca[g][1], ca[g][2], ca[g][3]);
-            *reinterpret_cast<float4*>(sb + off) = make_float4(cb[g][0], cb[g][1], cb[g][2], cb[g][3]);
+            if (SPLIT) {
+                float4 ah, bh;
+                ah.x = tf32_hi(ca[g][0]); ah.y = tf32_hi(ca[g][1]); ah.z = tf32_hi(ca[g][2]); ah.w = tf32_hi(ca[g][3]);
+                bh.x = tf32_hi(cb[g][0]); bh.y = tf32_hi(cb[g][1]); bh.z = tf32_hi(cb[g][2]); bh.w = tf32_hi(cb[g][3]);
+                *reinterpret_cast<float4*>(sa + off) = ah;
+                *reinterpret_cast<float4*>(sb + off) = bh;
+                *reinterpret_cast<float4*>(sa + kNReg * kWRegion + off) =
+                    make_float4(__fsub_rn(ca[g][0], ah.x), __fsub_rn(ca[g][1], ah.y), __fsub_rn(ca[g][2], ah.z),
+                                __fsub_rn(ca[g][3], ah.w));
+                *reinterpret_cast<float4*>(sb + kNReg * kWRegion + off) =
+                    make_float4(__fsub_rn(cb[g][0], bh.x), __fsub_rn(cb[g][1], bh.y), __fsub_rn(cb[g][2], bh.z),
+                                __fsub_rn(cb[g][3], bh.w));
+            } else {
+                *reinterpret_cast<float4*>(sa + off) = make_float4(ca[g][0], ca[g][1], ca[g][2], ca[g][3]);
+                *reinterpret_cast<float4*>(sb + off) = make_float4(cb[g][0], cb[g][1], cb[g][2], cb[g][3]);
+            }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
@@ -278,7 +299,14 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wgrad(WgradArgs a) {
 #pragma unroll
             for (int kk = 0; kk < kWRows / 8; ++kk) {      // UMMA K = 8: region kk/4, 32-byte step kk%4
                 const uint32_t ko = (uint32_t)((kk >> 2) * kWRegion + (kk & 3) * 32);
-                mma_tf32(tmem, sdesc(a0 + ko), sdesc(b0 + ko), idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                if (SPLIT) {                                // small terms first
+                    const uint32_t lo = (uint32_t)(kNReg * kWRegion);
+                    mma_tf32(tmem, sdesc(a0 + lo + ko), sdesc(b0 + ko), idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                    mma_tf32(tmem, sdesc(a0 + ko), sdesc(b0 + lo + ko), idesc, 1u);
+                    mma_tf32(tmem, sdesc(a0 + ko), sdesc(b0 + ko), idesc, 1u);
+                } else {
+                    mma_tf32(tmem, sdesc(a0 + ko), sdesc(b0 + ko), idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                }
             }
             mma_commit(&bar_empty[st]);
         }
@@ -314,21 +342,27 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wgrad(WgradArgs a) {
 // ------------------------------------------------------------------ input gradient (tcgen05, K-major)
 constexpr int kDTile = 128;
 
+// 3xTF32 (SPLIT): warps 1-3 split each landed stage (dZ tile and Wt chunk) into hi in place and lo in a
+// second copy of the stage, then arrive on bar_conv; the MMA thread issues a_lo b_hi + a_hi b_lo + a_hi b_hi.
+template <bool SPLIT>
 __global__ void __launch_bounds__(128, 1)
     k_dgrad(const __grid_constant__ CUtensorMap map_dz, const __grid_constant__ CUtensorMap map_wt, DgradArgs a,
             uint32_t tmem_cols) {
     extern __shared__ __align__(1024) unsigned char dsm[];
-    __shared__ __align__(8) uint64_t bar_full[2], bar_empty[2], bar_done;
+    __shared__ __align__(8) uint64_t bar_full[2], bar_empty[2], bar_done, bar_conv[2];
     __shared__ uint32_t tmem_sh;
     __shared__ int32_t pref[kWMaxInst + 1];
     unsigned char* base = dsm + ((1024u - (su32(dsm) & 1023u)) & 1023u);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t a_bytes = kDTile * 128, b_bytes = (uint32_t)(2 * a.kp) * 128;
-    const uint32_t stage_bytes = a_bytes + b_bytes;
+    const uint32_t plain_bytes = a_bytes + b_bytes;                 // [A | B] (hi in place when SPLIT)
+    const uint32_t stage_bytes = SPLIT ? 2 * plain_bytes : plain_bytes;   // + [A_lo | B_lo]
     if (warp == 0) {
         if (lane == 0) {
             mb_init(&bar_full[0], 1);
             mb_init(&bar_full[1], 1);
+            mb_init(&bar_conv[0], 3);
+            mb_init(&bar_conv[1], 3);
             mb_init(&bar_empty[0], 1);
             mb_init(&bar_empty[1], 1);
             mb_init(&bar_done, 1);
@@ -381,7 +415,7 @@ __global__ void __launch_bounds__(128, 1)
                 const int st = gg & 1;
                 if (gg >= 2) mb_wait(&bar_empty[st], ((gg >> 1) - 1) & 1);
                 unsigned char* sa = base + st * stage_bytes;
-                mb_expect_tx(&bar_full[st], stage_bytes);
+                mb_expect_tx(&bar_full[st], plain_bytes);
                 tma_load_2d(sa, &map_dz, j * 32, (int)((int64_t)m * a.dz_rows + row0), &bar_full[st]);
                 tma_load_2d(sa + a_bytes, &map_wt, j * 32, 0, &bar_full[st]);
                 if (a.kp > 128) tma_load_2d(sa + a_bytes + a.kp * 128, &map_wt, j * 32, a.kp, &bar_full[st]);
@@ -391,18 +425,50 @@ __global__ void __launch_bounds__(128, 1)
                 const uint32_t gg = g + j;
                 if (j + 1 < nk) issue(j + 1, gg + 1);
                 const int st = gg & 1;
-                mb_wait(&bar_full[st], (gg >> 1) & 1);
+                mb_wait(SPLIT ? &bar_conv[st] : &bar_full[st], (gg >> 1) & 1);
                 tc_fence_after();
                 const uint32_t sa = su32(base + st * stage_bytes), sb = sa + a_bytes;
+                const uint32_t nb = (uint32_t)a.kp * 128;             // neighbour half of the Wt chunk
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    mma_tf32(tmem, sdesc(sa + k * 32), sdesc(sb + k * 32), idesc, (j > 0 || k > 0) ? 1u : 0u);
-                    mma_tf32(tmem + (uint32_t)a.kp, sdesc(sa + k * 32), sdesc(sb + a.kp * 128 + k * 32), idesc,
-                             (j > 0 || k > 0) ? 1u : 0u);
+                    const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
+                    if (SPLIT) {
+                        const uint32_t al = sa + plain_bytes, bl = sb + plain_bytes;
+                        mma_tf32(tmem, sdesc(al + k * 32), sdesc(sb + k * 32), idesc, acc);
+                        mma_tf32(tmem, sdesc(sa + k * 32), sdesc(bl + k * 32), idesc, 1u);
+                        mma_tf32(tmem, sdesc(sa + k * 32), sdesc(sb + k * 32), idesc, 1u);
+                        mma_tf32(tmem + (uint32_t)a.kp, sdesc(al + k * 32), sdesc(sb + nb + k * 32), idesc, acc);
+                        mma_tf32(tmem + (uint32_t)a.kp, sdesc(sa + k * 32), sdesc(bl + nb + k * 32), idesc, 1u);
+                        mma_tf32(tmem + (uint32_t)a.kp, sdesc(sa + k * 32), sdesc(sb + nb + k * 32), idesc, 1u);
+                    } else {
+                        mma_tf32(tmem, sdesc(sa + k * 32), sdesc(sb + k * 32), idesc, acc);
+                        mma_tf32(tmem + (uint32_t)a.kp, sdesc(sa + k * 32), sdesc(sb + nb + k * 32), idesc, acc);
+                    }
                 }
                 mma_commit(&bar_empty[st]);
             }
             mma_commit(&bar_done);
+        }
+        if (SPLIT && warp >= 1) {            // converters: hi in place, lo into the stage's second half
+            const int t = threadIdx.x - 32;
+            const uint32_t n4 = plain_bytes / 16;
+            for (int j = 0; j < nk; ++j) {
+                const uint32_t gg = g + j;
+                const int st = gg & 1;
+                mb_wait(&bar_full[st], (gg >> 1) & 1);
+                float4* p = reinterpret_cast<float4*>(base + st * stage_bytes);
+                float4* pl = reinterpret_cast<float4*>(base + st * stage_bytes + plain_bytes);
+                for (uint32_t i = t; i < n4; i += 96) {
+                    const float4 v = p[i];
+                    float4 h;
+                    h.x = tf32_hi(v.x); h.y = tf32_hi(v.y); h.z = tf32_hi(v.z); h.w = tf32_hi(v.w);
+                    p[i] = h;
+                    pl[i] = make_float4(__fsub_rn(v.x, h.x), __fsub_rn(v.y, h.y), __fsub_rn(v.z, h.z), __fsub_rn(v.w, h.w));
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mb_arrive(&bar_conv[st]);
+            }
         }
         __syncwarp();
         g += nk;
@@ -590,7 +656,8 @@ void launch_zero_rows(const ZeroRowsArgs& a, cudaStream_t s) {
 
 bool launch_wgrad(const WgradArgs& a_in, cudaStream_t s) {
     const size_t smem = 1024 + 2 * kWStage;
-    if (ensure_smem_k(k_wgrad, (int)smem) != cudaSuccess) return false;
+    if (ensure_smem_k(k_wgrad<false>, (int)smem) != cudaSuccess) return false;
+    if (ensure_smem_k(k_wgrad<true>, (int)smem) != cudaSuccess) return false;
     WgradArgs a = a_in;
     if (a.n_inst > kWMaxInst || a.kp % 128 || a.npad > 256) return false;
     const int sms = num_sms();
@@ -598,19 +665,30 @@ bool launch_wgrad(const WgradArgs& a_in, cudaStream_t s) {
     // split-K over every SM (measured: fewer CTAs with >= 8 chunks each was slower, 16 -> 26 us; the
     // chunk loads are latency-bound, the partial-tile atomics are not)
     a.ksplit = std::max(1, sms / tiles);
-    launch_k(k_wgrad, dim3(tiles * a.ksplit), dim3(kWThreads), smem, s, a);
+    if (a.split3)
+        launch_k(k_wgrad<true>, dim3(tiles * a.ksplit), dim3(kWThreads), smem, s, a);
+    else
+        launch_k(k_wgrad<false>, dim3(tiles * a.ksplit), dim3(kWThreads), smem, s, a);
     count_launches(1, __func__, s);
     return true;
 }
 
 bool launch_dgrad(const void* map_dz, const void* map_wt, const DgradArgs& a, cudaStream_t s) {
     if (a.n_inst > kWMaxInst || a.kp % 32 || a.kp > 256 || a.npad_out > 256) return false;
-    const size_t smem = 1024 + 2 * ((size_t)kDTile * 128 + (size_t)2 * a.kp * 128);
-    if (ensure_smem_k(k_dgrad, (int)smem) != cudaSuccess) return false;
+    const size_t plain = (size_t)kDTile * 128 + (size_t)2 * a.kp * 128;
+    const bool split = a.split3 && 1024 + 4 * plain <= 227 * 1024;     // kp <= 128 (hidden layers)
+    const size_t smem = 1024 + 2 * (split ? 2 : 1) * plain;
+    if (ensure_smem_k(k_dgrad<false>, 1024 + 2 * (int)plain) != cudaSuccess) return false;
+    if (split && ensure_smem_k(k_dgrad<true>, (int)smem) != cudaSuccess) return false;
     uint32_t cols = 32;
     while ((int)cols < 2 * a.kp) cols <<= 1;
     const int sms = num_sms();
-    launch_k(k_dgrad, dim3(sms), dim3(128), smem, s, *(const CUtensorMap*)map_dz, *(const CUtensorMap*)map_wt, a, cols);
+    if (split)
+        launch_k(k_dgrad<true>, dim3(sms), dim3(128), smem, s, *(const CUtensorMap*)map_dz,
+                 *(const CUtensorMap*)map_wt, a, cols);
+    else
+        launch_k(k_dgrad<false>, dim3(sms), dim3(128), smem, s, *(const CUtensorMap*)map_dz,
+                 *(const CUtensorMap*)map_wt, a, cols);
     count_launches(1, __func__, s);
     return true;
 }

@@ -15,6 +15,9 @@ __device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
 __device__ __forceinline__ void mb_expect_tx(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
 __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
         "{\n .reg .pred p;\n SW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra SW_%=;\n}\n" ::"r"(

@@ -261,3 +261,51 @@ def test_sgd_step_decreases_loss():
     loss0, grads = S.sage_loss_grads(X, blocks, wts, labels)
     loss1, _ = S.sage_loss_grads(X, blocks, S.sgd(wts, grads, 0.05), labels)
     assert loss1 < loss0
+
+
+@pytest.mark.filterwarnings("ignore::UserWarning")
+def test_gradient_bounds_hold_for_fp32_and_catch_one_percent():
+    """tests/train_util.grad_bounds (the first DDP step's elementwise tolerance) against an independent
+    fp32 implementation: torch autograd in float32 on CPU through sparse row-mean matrices (products
+    no worse than 3xTF32's) lands inside the 3xTF32 bound, and a 1 % error on the largest-magnitude
+    element of every gradient tensor does not."""
+    import torch
+    from tests.train_util import grad_bounds
+    g = synth.random_graph(600, 0.02, seed=11)
+    parts = synth.partition(g, 2)
+    D = 12
+    W = O.World(parts, D, synth.FEAT_SEED)
+    p = W.parts[1]
+    p.buffer_init(0.9, float(O.alpha_default(0.9, 4)), 1.0, 4, 2500)
+    dims = synth.sage_dims(D, 2, 7, hidden=9)
+    w32 = synth.sage_weights(dims, seed=5)
+    wts = [tuple(np.asarray(a, np.float64) for a in w) for w in w32]
+    p.step(synth.RUN_SEED, 1, [10, 25], 32)
+    F = p.frontier()
+    blocks = [(off, S.positions(F, cols)) for off, cols in (p.hop_block(h) for h in range(2))]
+    X = p.features().astype(np.float64)
+    labels = np.random.default_rng(2).integers(0, 7, size=p.hop_sizes()[0])
+    _, ref = S.sage_loss_grads(X, blocks, wts, labels)
+    n_acc = [len(blocks[1 - l][0]) - 1 for l in range(2)]
+    bnd = grad_bounds(X, blocks, wts, labels, 1.0, n_acc, "3xtf32")
+    tw = [[torch.tensor(np.asarray(a, np.float32), requires_grad=True) for a in w] for w in w32]
+    h = torch.as_tensor(X.astype(np.float32))
+    for l in range(2):
+        off, nbr = blocks[1 - l]
+        n = len(off) - 1
+        deg = np.diff(off).astype(np.float32)
+        vals = np.repeat(np.where(deg > 0, 1.0 / np.maximum(deg, 1.0), 0.0).astype(np.float32),
+                         np.diff(off).astype(np.int64))
+        A = torch.sparse_csr_tensor(torch.as_tensor(np.asarray(off, np.int64)), torch.as_tensor(np.asarray(nbr, np.int64)),
+                                    torch.as_tensor(vals), size=(n, h.shape[0]), dtype=torch.float32)
+        z = h[:n] @ tw[l][0].T + (A @ h) @ tw[l][1].T + tw[l][2]
+        h = torch.relu(z) if l == 0 else z
+    torch.nn.functional.cross_entropy(h, torch.as_tensor(labels)).backward()
+    for l in range(2):
+        for t in range(3):
+            got = tw[l][t].grad.numpy().astype(np.float64)
+            err = np.abs(got - ref[l][t])
+            assert np.all(err <= bnd[l][t]), (l, t, float(np.max(err / (bnd[l][t] + 1e-30))))
+            k = np.unravel_index(np.argmax(np.abs(ref[l][t])), ref[l][t].shape)
+            assert 0.01 * abs(ref[l][t][k]) > bnd[l][t][k], (l, t, ref[l][t][k], bnd[l][t][k])
+    W.close()
