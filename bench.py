@@ -46,6 +46,15 @@ DEFAULT_CONFIG = "products"
 # the columns' relabel on a third stream beside the gather (schedule.PrepareAhead relabel_stream):
 # products window 2.207 -> 2.162 ms, arxiv 0.214 -> 0.206 ms
 RELABEL_STREAM = True
+# Launch tuning by config (libmgnn reads these once per process, before its first launch; every variant
+# is parity-tested in tests/test_gpu_variants.py): on products the next window's sampling stream runs at
+# high priority with the persistent k_hop / k_compact grids capped at 5 blocks per SM, so its kernels
+# are dispatched beside the gather instead of queueing behind the gather's blocks (products window
+# 1.90 -> 1.80 ms, profiles/r02/gather_flat/exp_s29*); neutral on arxiv / cfg1, 1-4 % slower on reddit /
+# papers_s32, which keep the defaults.
+TUNING = {
+    "products": {"env": {"MGNN_HOP_GRID_BPS": "5", "MGNN_COMPACT_BPS": "5"}, "sampling_priority": -1},
+}
 
 # Measurement policy (f_p in basis points, gamma, Delta) by config and total partitions P: the
 # paper's GPU optima; theta_R = 1.  Looked up for the P actually used.
@@ -100,6 +109,7 @@ class Setup:
         self.f_bp, self.gamma, self.delta = table[k]
         w = window or win
         self.window = min(w, self.delta) if self.delta > 0 else w
+        self.sampling_priority = 0
 
     def workload(self) -> dict:
         return {
@@ -110,6 +120,9 @@ class Setup:
             "policy_for_P": self.policy_P, "f_p": self.f_bp / 10000, "gamma": self.gamma, "delta": self.delta,
             "theta_r": 1.0, "window_steps": self.window, "minibatches_per_step_per_gpu": self.window * self.ppg,
             "l2": "flushed (256 MB write) between timed windows",
+            "launch": {"gather": os.environ.get("MGNN_GATHER", "flat"),
+                       **{k: v for k, v in os.environ.items() if k.startswith("MGNN_")},
+                       "sampling_stream_priority": self.sampling_priority},
         }
 
 
@@ -441,6 +454,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-extras", action="store_true", help="skip the with_consumer / with_training lines")
+    ap.add_argument("--no-tuning", action="store_true", help="library launch defaults (ignore TUNING)")
     ap.add_argument("--no-train-graph", action="store_true", help="training steps as eager launches")
     ap.add_argument("--remote", action="store_true",
                     help="NEXT-1: sample non-local frontier nodes from their owner's CSR")
@@ -455,6 +469,10 @@ def main():
     if args.impl == "reference":
         return run_reference(args, S)
 
+    tune = {} if args.no_tuning else TUNING.get(S.name, {})
+    for k_, v_ in tune.get("env", {}).items():
+        os.environ.setdefault(k_, v_)
+    S.sampling_priority = tune.get("sampling_priority", 0)
     import torch
     import torch.distributed as dist
     from paper_2410_22697_b200 import pipeline as PL
@@ -531,7 +549,8 @@ def main():
     mb_total = WINDOW * S.ppg * world * K
     t_first = 1
     for attempt in range(4):
-        pipe = PrepareAhead(ctx, WINDOW, t0=t_first, stream_b=stream, relabel_stream=RELABEL_STREAM)
+        pipe = PrepareAhead(ctx, WINDOW, t0=t_first, stream_b=stream, relabel_stream=RELABEL_STREAM,
+                            sampling_priority=tune.get("sampling_priority", 0))
         for _ in range(args.warmup):
             pipe.iteration()
         # ---------------- timed region (device path: inputs resident in HBM); R runs, median reported

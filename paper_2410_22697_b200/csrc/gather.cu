@@ -737,7 +737,7 @@ void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, con
     static const int flat_bps = [] {
         const char* e = getenv("MGNN_FLAT_BPS");
         const int v = e ? atoi(e) : 0;
-        return v >= 1 && v <= 8 ? v : 4;
+        return v >= 1 && v <= 256 ? v : 4;
     }();
     if (use_flat) {
         const int64_t tgt = std::max<int64_t>(1, ((int64_t)num_sms() * flat_bps) / w.n_inst);
@@ -748,7 +748,7 @@ void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, con
             return e ? atoi(e) : 4;
         }();
         const dim3 gf(gxf, w.n_inst), bf(kFThreads);
-        switch (flat_bps * 16 + flat_unr) {
+        switch ((flat_bps > 6 ? 4 : flat_bps) * 16 + flat_unr) {   // > 6: more, shorter blocks of <4, 4>
             case 3 * 16 + 8: launch_k(k_gather_flat<8, 3>, gf, bf, 0, s, w, world); break;
             case 3 * 16 + 6: launch_k(k_gather_flat<6, 3>, gf, bf, 0, s, w, world); break;
             case 4 * 16 + 6: launch_k(k_gather_flat<6, 4>, gf, bf, 0, s, w, world); break;

@@ -31,7 +31,8 @@ class PrepareAhead:
     def __init__(self, ctx, window: int, t0: int = 1, stream_b: Optional[torch.cuda.Stream] = None,
                  flush_bytes: int = 256 << 20,
                  host_seeds: Optional[Callable[[int, int], Tuple[int, int]]] = None, serial: bool = False,
-                 relabel_stream: bool = False, relabel_after_gather: bool = False, score_after_sample: bool = False):
+                 relabel_stream: bool = False, relabel_after_gather: bool = False, score_after_sample: bool = False,
+                 sampling_priority: int = 0):
         """window: steps per window (a window may end on an eviction step, never contain one earlier);
         t0: first global step (1-based, R#8); flush_bytes: L2 flush buffer written before every
         iteration (0 = none; B200 L2 is 126 MB); host_seeds(slot, t) -> (seeds_ptr, counts_ptr) of
@@ -48,7 +49,7 @@ class PrepareAhead:
         self.slot = 0
         self.sB = stream_b if stream_b is not None else torch.cuda.current_stream()
         self.serial = serial
-        self.sA = self.sB if serial else torch.cuda.Stream(device=self.sB.device)
+        self.sA = self.sB if serial else torch.cuda.Stream(device=self.sB.device, priority=sampling_priority)
         self.ev_sampled = [torch.cuda.Event(), torch.cuda.Event()]
         self.ev_done = [torch.cuda.Event(), torch.cuda.Event()]
         self.flush = torch.empty(flush_bytes, dtype=torch.uint8, device=self.sB.device) if flush_bytes else None

@@ -65,7 +65,7 @@ class _Perturbed:
 def run_schedule_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_bp: int, gamma: float, delta: int,
                         window: int, n_windows: int, x_rows: int = 2048, warm: int = 0, flush_bytes: int = 256 << 20,
                         run_seed: int = synth.RUN_SEED, feat_seed: int = synth.FEAT_SEED, rows_bound: int = -1,
-                        perturb=None, relabel_stream: bool = False, sm_split: int = 0):
+                        perturb=None, relabel_stream: bool = False, sm_split: int = 0, sampling_priority: int = 0):
     import torch
     from paper_2410_22697_b200 import pipeline as PL
     from paper_2410_22697_b200.schedule import PrepareAhead
@@ -83,7 +83,7 @@ def run_schedule_parity(g: synth.Graph, P: int, D: int, fanouts, batch: int, f_b
     L = len(fanouts)
     n_inst = P * window
     pipe = PrepareAhead(ctx if perturb is None else _Perturbed(ctx, perturb), window, t0=1, flush_bytes=flush_bytes,
-                        relabel_stream=relabel_stream)
+                        relabel_stream=relabel_stream, sampling_priority=sampling_priority)
     grabbed = []
     xpos_n = x_rows
 

@@ -38,14 +38,35 @@ def test_schedule_arxiv_full_size_bench_config():
     assert st["evicted"] > 0
 
 
+PRODUCTS_SCRIPT = """
+import sys
+sys.path.insert(0, {root!r})
+from inputs import synth
+from tests.schedule_util import run_schedule_parity
+g = synth.generate(synth.CONFIGS["products"])
+st = run_schedule_parity(g, 2, 100, [5, 10, 15], 2000, 5000, 0.995, 32, 32, 4, x_rows=0,   # every X row
+                         relabel_stream=True, sampling_priority={prio})                   # as bench.py
+assert st["evicted"] > 0 and st["misses"] > 0, st
+print("products schedule parity ok", st)
+"""
+
+
 @pytest.mark.slow
 def test_schedule_products_full_size_bench_config():
     """configs[3] (the bench default) at full size in the bench's configuration: P = 2 on one GPU,
-    32-step windows, f = 0.5, gamma = 0.995, Delta = 32, 3 hops [5, 10, 15], batch 2000."""
-    g = synth.generate(synth.CONFIGS["products"])
-    st = run_schedule_parity(g, 2, 100, [5, 10, 15], 2000, 5000, 0.995, 32, 32, 4, x_rows=0,  # every X row
-                             relabel_stream=True)                                         # as bench.py
-    assert st["evicted"] > 0 and st["misses"] > 0
+    32-step windows, f = 0.5, gamma = 0.995, Delta = 32, 3 hops [5, 10, 15], batch 2000, with
+    bench.py's launch tuning for products (sampling stream priority, sampler grid caps: environment read
+    once per process, so a fresh interpreter)."""
+    import os
+    import subprocess
+    import sys
+    import bench
+    tune = bench.TUNING.get("products", {})
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, **tune.get("env", {}))
+    r = subprocess.run([sys.executable, "-c", PRODUCTS_SCRIPT.format(root=root, prio=tune.get("sampling_priority", 0))],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0 and "products schedule parity ok" in r.stdout, (r.stdout[-2000:], r.stderr[-4000:])
 
 
 @pytest.mark.parametrize("seed,relabel_stream", [(1, False), (2, False), (3, False), (4, True), (5, True)])

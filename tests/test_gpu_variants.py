@@ -34,6 +34,7 @@ print("variant parity ok")
                                  {"MGNN_FLAT_BPS": "3", "MGNN_FLAT_UNR": "8"}, {"MGNN_FLAT_UNR": "6"},
                                  {"MGNN_FLAT_BPS": "5", "MGNN_FLAT_UNR": "2"}, {"MGNN_PDL": "0"},
                                  {"MGNN_HOP_GRID_BPS": "0", "MGNN_COMPACT_BPS": "0"},
+                                 {"MGNN_HOP_GRID_BPS": "5", "MGNN_COMPACT_BPS": "5"},
                                  {"MGNN_GATHER": "tma", "MGNN_GATHER_HINT": "0"},
                                  {"MGNN_GATHER": "tma", "MGNN_GATHER_HINT": "3"},
                                  {"MGNN_GATHER": "tma", "MGNN_GATHER_HINT": "10", "MGNN_GATHER_G4": "0"},

@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--relabel-after-gather", action="store_true")
     ap.add_argument("--prio-b", action="store_true", help="buffer stream (gather + score) at high priority")
     ap.add_argument("--score-after-sample", action="store_true")
+    ap.add_argument("--prio-a", action="store_true", help="sampling stream at high priority")
+    ap.add_argument("--gather-events", action="store_true", help="events around the gather launch in the timed run")
     ap.add_argument("--kprof", action="store_true", help="per-launch event times on each stream (stderr)")
     ap.add_argument("--parts", type=int, default=None)
     ap.add_argument("--tag", default="")
@@ -42,11 +44,14 @@ def main():
     sms = ctx.sm_partition(a.sm_split) if a.sm_split else (0, 0)
     sb = torch.cuda.Stream(priority=-1) if a.prio_b else None
     pipe = PrepareAhead(ctx, S.window, serial=a.serial, stream_b=sb, relabel_stream=a.relabel_stream,
-                        relabel_after_gather=a.relabel_after_gather, score_after_sample=a.score_after_sample)
+                        relabel_after_gather=a.relabel_after_gather, score_after_sample=a.score_after_sample,
+                        sampling_priority=-1 if a.prio_a else 0)
     for _ in range(4):
         pipe.iteration()
     torch.cuda.synchronize()
     # window times without per-stage events (those end the launches' programmatic overlap) ...
+    if a.gather_events:
+        ctx.profile(True, gather_only=True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.windows)]
     for i in range(a.windows):
         pipe.iteration(events=ev[i])
@@ -63,13 +68,13 @@ def main():
     pr = ctx.profile_stages()
     n = max(pr["sample_calls"], 1)
     out = {"tag": a.tag, "config": a.config, "serial": a.serial, "env": {k: v for k, v in os.environ.items() if k.startswith("MGNN_")},
-           "ms_median": ms[len(ms) // 2], "ms_min": ms[0], "ms_median_staged": msp[len(msp) // 2], "mb_per_s": S.window * S.ppg / (ms[len(ms) // 2] / 1e3),
+           "ms_median": ms[len(ms) // 2], "ms_mean": sum(ms) / len(ms), "ms_min": ms[0], "ms_median_staged": msp[len(msp) // 2], "mb_per_s": S.window * S.ppg / (ms[len(ms) // 2] / 1e3),
            "sample_ms": pr["sample_ms"] / n, "gather_ms": pr["gather_ms"] / max(pr["gather_calls"], 1),
            "score_ms": pr["score_ms"] / max(pr["score_calls"], 1),
            "relabel_ms": pr["relabel_ms"] / max(pr["relabel_calls"], 1), "relabel_stream": a.relabel_stream,
            "relabel_probes": pr["relabel_probes"] / max(pr["relabel_calls"], 1),
            "edges": pr["edges"] / n, "frontier": pr["frontier"] / n, "unique": pr["unique"] / n,
-           "sm_split": sms, "prio_b": a.prio_b, "score_after_sample": a.score_after_sample}
+           "sm_split": sms, "prio_b": a.prio_b, "score_after_sample": a.score_after_sample, "prio_a": a.prio_a}
     if a.kprof:
         import ctypes as C
         from paper_2410_22697_b200 import _lib
