@@ -32,7 +32,7 @@ class PrepareAhead:
                  flush_bytes: int = 256 << 20,
                  host_seeds: Optional[Callable[[int, int], Tuple[int, int]]] = None, serial: bool = False,
                  relabel_stream: bool = False, relabel_after_gather: bool = False, score_after_sample: bool = False,
-                 sampling_priority: int = 0):
+                 sampling_priority: int = 0, score_priority: Optional[int] = None):
         """window: steps per window (a window may end on an eviction step, never contain one earlier);
         t0: first global step (1-based, R#8); flush_bytes: L2 flush buffer written before every
         iteration (0 = none; B200 L2 is 126 MB); host_seeds(slot, t) -> (seeds_ptr, counts_ptr) of
@@ -64,6 +64,12 @@ class PrepareAhead:
         self.relabel_after_gather = relabel_after_gather and self.relabel_stream
         self.ev_gathered = [torch.cuda.Event(), torch.cuda.Event()]
         self.score_after_sample = score_after_sample and not serial
+        # score_priority: the eviction round of window w on its own stream D at this priority (a chain of
+        # short latency-bound launches that would otherwise queue behind the next window's sampling)
+        self.sD = (torch.cuda.Stream(device=self.sB.device, priority=score_priority)
+                   if score_priority is not None and not serial else None)
+        self.ev_gdone = [torch.cuda.Event(), torch.cuda.Event()]
+        self.ev_sdone = [torch.cuda.Event(), torch.cuda.Event()]
         self._next_sampled = False
         ctx.defer_relabel(self.relabel_stream)
 
@@ -88,7 +94,14 @@ class PrepareAhead:
             self._relabel(sl)
         if self.score_after_sample and self._next_sampled:
             self.sB.wait_event(self.ev_sampled[sl ^ 1])   # the eviction round after the next window's sampling
-        self.ctx.score(sl, self.sB)
+        if self.sD is not None:
+            self.ev_gdone[sl].record(self.sB)
+            self.sD.wait_event(self.ev_gdone[sl])
+            self.ctx.score(sl, self.sD)
+            self.ev_sdone[sl].record(self.sD)
+            self.sB.wait_event(self.ev_sdone[sl])
+        else:
+            self.ctx.score(sl, self.sB)
         self.ev_done[sl].record(self.sB)
 
     def _relabel(self, sl: int) -> None:

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--score-after-sample", action="store_true")
     ap.add_argument("--prio-a", action="store_true", help="sampling stream at high priority")
     ap.add_argument("--gather-events", action="store_true", help="events around the gather launch in the timed run")
+    ap.add_argument("--score-prio", type=int, default=None, help="eviction round on its own stream at this priority")
     ap.add_argument("--kprof", action="store_true", help="per-launch event times on each stream (stderr)")
     ap.add_argument("--parts", type=int, default=None)
     ap.add_argument("--tag", default="")
@@ -45,7 +46,7 @@ def main():
     sb = torch.cuda.Stream(priority=-1) if a.prio_b else None
     pipe = PrepareAhead(ctx, S.window, serial=a.serial, stream_b=sb, relabel_stream=a.relabel_stream,
                         relabel_after_gather=a.relabel_after_gather, score_after_sample=a.score_after_sample,
-                        sampling_priority=-1 if a.prio_a else 0)
+                        sampling_priority=-1 if a.prio_a else 0, score_priority=a.score_prio)
     for _ in range(4):
         pipe.iteration()
     torch.cuda.synchronize()
@@ -74,7 +75,7 @@ def main():
            "relabel_ms": pr["relabel_ms"] / max(pr["relabel_calls"], 1), "relabel_stream": a.relabel_stream,
            "relabel_probes": pr["relabel_probes"] / max(pr["relabel_calls"], 1),
            "edges": pr["edges"] / n, "frontier": pr["frontier"] / n, "unique": pr["unique"] / n,
-           "sm_split": sms, "prio_b": a.prio_b, "score_after_sample": a.score_after_sample, "prio_a": a.prio_a}
+           "sm_split": sms, "prio_b": a.prio_b, "score_after_sample": a.score_after_sample, "prio_a": a.prio_a, "score_prio": a.score_prio}
     if a.kprof:
         import ctypes as C
         from paper_2410_22697_b200 import _lib
