@@ -4,6 +4,7 @@
 #
 #   tools/evidence_r02.sh single    # 1 GPU: bench lines, ncu tables
 #   tools/evidence_r02.sh traffic   # 1 GPU: only the per-config ncu DRAM tables
+#   tools/evidence_r02.sh final     # 1 GPU: GPU suite, smoke, bench lines of every config, launch list
 #   tools/evidence_r02.sh multi N   # N GPUs: test_multi + bench at N for products (P=2N) and papers_s32 (P=8)
 # Output under gpurun_out/evidence/ (copied into profiles/r02/ by hand after review).
 set -u
@@ -31,6 +32,24 @@ if [ "$part" = single ] || [ "$part" = traffic ]; then
     timeout 1500 python bench.py --config papers --no-cpu-baseline --steps 10 --warmup 3 --runs 1 \
         > $OUT/bench_papers.json 2> $OUT/bench_papers.err
     # 3. launch list of the bench's own default command (the gpu__time_duration pass of B200_PROFILING.md)
+    timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -s 60 -c 400 --csv \
+        --log-file $OUT/bench_launches.csv python bench.py --steps 3 --warmup 3 --runs 1 --no-extras \
+        --no-cpu-baseline > $OUT/bench_under_ncu.log 2>&1
+    python tools/launch_summary.py $OUT/bench_launches.csv > $OUT/bench_launches_summary.txt 2>&1
+    exit 0
+fi
+
+if [ "$part" = final ]; then
+    # end-of-round lines at HEAD: GPU suite, smoke, every config's bench line, full papers, the bench
+    # command's launch list (traffic tables: part "traffic")
+    timeout 1800 python -m pytest tests -m gpu -q > $OUT/gpu_tests.log 2>&1; echo "gpu tests rc=$?" >> $OUT/status
+    python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/status
+    timeout 900 python bench.py > $OUT/bench_products.json 2> $OUT/bench_products.err
+    for c in cfg1 arxiv reddit papers_s32; do
+        timeout 900 python bench.py --config $c > $OUT/bench_$c.json 2> $OUT/bench_$c.err
+    done
+    timeout 1500 python bench.py --config papers --no-cpu-baseline --steps 10 --warmup 3 --runs 1 \
+        > $OUT/bench_papers.json 2> $OUT/bench_papers.err
     timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -s 60 -c 400 --csv \
         --log-file $OUT/bench_launches.csv python bench.py --steps 3 --warmup 3 --runs 1 --no-extras \
         --no-cpu-baseline > $OUT/bench_under_ncu.log 2>&1
