@@ -54,6 +54,9 @@ RELABEL_STREAM = True
 # papers_s32, which keep the defaults.
 TUNING = {
     "products": {"env": {"MGNN_HOP_GRID_BPS": "5", "MGNN_COMPACT_BPS": "5"}, "sampling_priority": -1},
+    # cfg1's ~2 MB tables: the TMA row gather (k_gather_g4) beats the flat gather by 4 % in the bench loop
+    # (profiles/r02/tuning/exp_s37: 832-835k vs 796-799k minibatches/s); arxiv is equal or better flat
+    "cfg1": {"env": {"MGNN_GATHER": "tma"}},
 }
 
 # Measurement policy (f_p in basis points, gamma, Delta) by config and total partitions P: the

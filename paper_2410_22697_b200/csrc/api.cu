@@ -290,6 +290,8 @@ mgnn_status mgnn_ctx_create(int32_t device, int32_t n_parts, int64_t n_global, c
         ctx->sort_full_lists = e && e[0] == '2';
         const char* e2 = getenv("MGNN_EV_SELECT");
         ctx->ev_scan = e2 && e2[0] == '0';
+        const char* e3 = getenv("MGNN_FUSED_DECAY");
+        ctx->no_fused_decay = e3 && e3[0] == '0';
     }
     ctx->tables.assign(n_parts, nullptr);
     mgnn_status st = MGNN_OK;
@@ -1062,17 +1064,20 @@ mgnn_status mgnn_score_evict_refill(mgnn_ctx ctx, int32_t slot, mgnn_stream stre
         CK(cudaEventRecord(pe0, s));
     }
     const uint64_t t_last = w.step0 + (uint64_t)w.n_steps - 1;
-    launch_decay(ctx->d_parts, n_lp, cap_max, w.n_steps, ctx->pol.gamma, ctx->d_ovf, t_last, s);
-    if (ctx->pol.delta > 0 && t_last % (uint64_t)ctx->pol.delta == 0) {
+    const bool round = ctx->pol.delta > 0 && t_last % (uint64_t)ctx->pol.delta == 0;
+    // ordered E / R lists (k_select, default) or counts and histograms straight from the scoreboards
+    // with the candidates re-derived from them (MGNN_EV_SELECT=0; measured slower on products:
+    // count + candidate scans 97 us per round against 70 us for select + candidates on the lists)
+    const bool compact = ctx->sort_full_lists || !ctx->ev_scan;
+    // on an eviction window with ordered lists the decay runs inside k_select (one launch less)
+    const bool fused_decay = round && compact && !ctx->no_fused_decay;
+    if (!fused_decay) launch_decay(ctx->d_parts, n_lp, cap_max, w.n_steps, ctx->pol.gamma, ctx->d_ovf, t_last, s);
+    if (round) {
         CK(cudaMemsetAsync(ctx->ev_zero, 0, ctx->ev_zero_bytes, s));
-        // ordered E / R lists (k_select, default) or counts and histograms straight from the scoreboards
-        // with the candidates re-derived from them (MGNN_EV_SELECT=0; measured slower on products:
-        // count + candidate scans 97 us per round against 70 us for select + candidates on the lists)
-        const bool compact = ctx->sort_full_lists || !ctx->ev_scan;
         const PartDev* scan = compact ? nullptr : ctx->d_parts;
         if (compact) {
             launch_select(ctx->d_parts, n_lp, nmax, ctx->pol.alpha, ctx->pol.theta_r, ctx->d_evsegs, ctx->d_sel_n,
-                          ctx->ev_sc, ctx->ev_ev, s);
+                          ctx->ev_sc, ctx->ev_ev, s, fused_decay ? w.n_steps : 0, ctx->pol.gamma, ctx->d_ovf, t_last);
         } else {
             CK(cudaMemsetAsync(ctx->d_sel_n, 0, 2 * n_lp * sizeof(long long), s));
             launch_ev_count(ctx->d_parts, n_lp, nmax, ctx->pol.alpha, ctx->pol.theta_r, ctx->d_sel_n, ctx->ev_ev, s);

@@ -123,7 +123,8 @@ struct mgnn_ctx_s {
     SortSeg* d_candsegs_hi = nullptr;    // candidates in list order (k_cand_ord): the score digits only
     SortSeg* d_initsegs = nullptr;
     bool force_sort_path = false;        // MGNN_EVICT_SORT=1: always use the radix-sort eviction path
-    bool ev_scan = false;                // MGNN_EV_SELECT=0: no ordered lists, scoreboard scans
+    bool ev_scan = false;
+    bool no_fused_decay = false;         // MGNN_FUSED_DECAY=0: k_decay stays a launch of its own on eviction windows                // MGNN_EV_SELECT=0: no ordered lists, scoreboard scans
     bool sort_full_lists = false;        // MGNN_EVICT_SORT=2: sort the whole E / R lists, not the candidates
     int32_t ev_passes = 8;
     long long* d_sel_n = nullptr;

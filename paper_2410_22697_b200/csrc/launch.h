@@ -154,7 +154,8 @@ bool encode_row_map(void* map_out, const float* base, int64_t rows, int64_t cols
 void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, float gamma,
                   const unsigned long long* ovf, uint64_t t_last, cudaStream_t s);
 void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, float theta_r, const SortSeg* segs,
-                   long long* n_out, Scratch sc, EvScratch ev, cudaStream_t s);
+                   long long* n_out, Scratch sc, EvScratch ev, cudaStream_t s, int decay_steps = 0, float gamma = 1.0f,
+                   const unsigned long long* ovf = nullptr, uint64_t t_last = 0);
 // |E|, |R| and the top-digit histograms straight from the scoreboards (no ordered lists)
 void launch_ev_count(const PartDev* parts, int n_lp, int64_t n_max, float alpha, float theta_r, long long* n_out,
                      EvScratch ev, cudaStream_t s);

@@ -68,10 +68,15 @@ void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, 
 // of the high word (the score) alone yields the full key order (k_cand_ord + a 4-digit sort).  Scores here are >= +0, so
 // their IEEE bit patterns order like the values.  Order-preserving compaction by a decoupled
 // look-back scan, plus a warp-aggregated histogram of key >> 52 per list.
+// decay_steps > 0: the window's decay (k_decay) is folded in -- the E scan visits every slot exactly once
+// (through its halo node), so it applies the slot's pending gamma products before reading S_E; one
+// dependent launch less in the eviction round.
 __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict__ parts, float alpha, float theta_r,
                                                       const SortSeg* __restrict__ segs, long long* __restrict__ n_out,
-                                                      Scratch sc, int64_t tiles_max, EvScratch ev) {
+                                                      Scratch sc, int64_t tiles_max, EvScratch ev, int decay_steps,
+                                                      float gamma, const unsigned long long* ovf, uint64_t t_last) {
     pdl_enter();
+    const bool decay = decay_steps > 0 && !(*ovf <= t_last);   // an overflowed window is not decayed
     __shared__ long long sm[8];
     __shared__ int tslot;
     __shared__ long long prefix_sh;
@@ -93,6 +98,14 @@ __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict_
                 // E in halo (= id) order; R in the static (deg_in desc, id asc) order: x = rank_deg of h
                 const int64_t h = isE ? x : pd.deg_order[x];
                 const int32_t s = pd.slot_of[h];
+                if (isE && s >= 0 && decay) {            // the same RN products as k_decay
+                    const unsigned long long mask = pd.hitmask[s];
+                    const int unused = decay_steps - __popcll(mask);
+                    float v = pd.se[s];
+                    for (int k = 0; k < unused; ++k) v = __fmul_rn(v, gamma);
+                    pd.se[s] = v;
+                    if (mask) pd.hitmask[s] = 0ull;
+                }
                 pf = isE ? (s >= 0 && pd.se[s] < alpha) : (s < 0 && pd.sa[h] >= theta_r);
             }
             flags |= (unsigned)pf << i;
@@ -139,11 +152,13 @@ __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict_
 }
 
 void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, float theta_r, const SortSeg* segs,
-                   long long* n_out, Scratch sc, EvScratch ev, cudaStream_t s) {
+                   long long* n_out, Scratch sc, EvScratch ev, cudaStream_t s, int decay_steps, float gamma,
+                   const unsigned long long* ovf, uint64_t t_last) {
     int64_t tiles = (n_max + kSThreads * 8 - 1) / (kSThreads * 8);
     if (tiles < 1) tiles = 1;
     dim3 grid((unsigned)tiles, 2 * n_lp);
-    launch_k(k_select, grid, dim3(kSThreads), 0, s, parts, alpha, theta_r, segs, n_out, sc, tiles, ev);
+    launch_k(k_select, grid, dim3(kSThreads), 0, s, parts, alpha, theta_r, segs, n_out, sc, tiles, ev, decay_steps,
+             gamma, ovf, t_last);
     count_launches(1, __func__, s);
 }
 

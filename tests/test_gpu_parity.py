@@ -90,7 +90,7 @@ def test_arxiv_full_size_bench_config():
     assert st["evicted"] > 0
 
 
-@pytest.mark.parametrize("mode", ["1", "1s", "2"])
+@pytest.mark.parametrize("mode", ["1", "1d", "1s", "2"])
 @pytest.mark.parametrize("wins", [[4, 4, 4, 4], [8, 8, 8]])
 def test_cfg1_full_sort_eviction_path(cfg1, monkeypatch, wins, mode):
     """The large-buffer eviction paths give the same result: radix sort of the threshold
@@ -100,6 +100,8 @@ def test_cfg1_full_sort_eviction_path(cfg1, monkeypatch, wins, mode):
     monkeypatch.setenv("MGNN_EVICT_SORT", mode[0])
     if mode == "1s":
         monkeypatch.setenv("MGNN_EV_SELECT", "0")
+    if mode == "1d":                                   # the window's decay as its own launch (k_decay)
+        monkeypatch.setenv("MGNN_FUSED_DECAY", "0")
     st = run_parity(cfg1, 2, 64, [10, 25], 256, 2500, 0.9, wins[0], 1.0, wins)
     assert st["evicted"] > 0
 
