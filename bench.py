@@ -458,6 +458,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-extras", action="store_true", help="skip the with_consumer / with_training lines")
     ap.add_argument("--no-tuning", action="store_true", help="library launch defaults (ignore TUNING)")
+    ap.add_argument("--no-gather-events", action="store_true",
+                    help="experiment: no events around the gather in the timed runs (roofline then unavailable)")
     ap.add_argument("--no-train-graph", action="store_true", help="training steps as eager launches")
     ap.add_argument("--remote", action="store_true",
                     help="NEXT-1: sample non-local frontier nodes from their owner's CSR")
@@ -561,7 +563,7 @@ def main():
         launches0 = ctx.launch_count()
         # events around the gather launch only (its roofline); events between the other launches
         # would end their programmatic overlap (PDL) and lengthen the step (cfg1: 72 -> 85 us)
-        ctx.profile(True, gather_only=True)
+        ctx.profile(not args.no_gather_events, gather_only=True)
         ctx.profile_stages()                     # reset
         runs = []
         prof = {}
@@ -757,7 +759,7 @@ def main():
                          "frac": (achieved / hbm_peak) if achieved else None,
                          "traffic": (tt_ or {}).get(g_kernel),
                          "traffic_source": (tt_ or {}).get("source"),
-                         "peak_source": peak_src, "launch_ms": g_ms, "share_of_step": prof["gather_ms"] / step_ms_sum,
+                         "peak_source": peak_src, "launch_ms": g_ms, "share_of_step": prof["gather_ms"] / max(step_ms_sum, 1e-9),
                          "algorithmic_bytes_per_launch": g_bytes,
                          "algorithmic": "2 * rows * D * 4 (row read + X write, SURVEY §8(d))"},
             "sampler_roofline": {
