@@ -289,13 +289,15 @@ def traffic_table(name: str):
         return None
 
 
-def gather_kernel_name(tt=None) -> str:
+def gather_kernel_name(g4_eligible: bool = False) -> str:
     """The gather kernel the library launches (MGNN_GATHER, read once per process by libmgnn): flat
-    (default) -> k_gather_flat; tma -> k_gather_tma, or k_gather_g4 (TMA row gather) when the hosted
-    tables fit in L2 (named by the committed traffic table of the config); reg -> k_gather."""
+    (default) -> k_gather_flat; tma -> k_gather_g4 (TMA row gather) when the hosted tables fit in 3/4 of
+    L2 and the rows are unpadded and at most 256 floats (the library's rule, api.cu / gather.cu; also
+    MGNN_GATHER_G4), else k_gather_tma; reg -> k_gather."""
     e = os.environ.get("MGNN_GATHER", "flat")
     if e.startswith("t"):
-        return "k_gather_g4" if (tt or {}).get("k_gather_g4") else "k_gather_tma"
+        g4 = os.environ.get("MGNN_GATHER_G4", "2")
+        return "k_gather_g4" if (g4 == "1" or (g4 == "2" and g4_eligible)) else "k_gather_tma"
     return "k_gather" if e.startswith("r") else "k_gather_flat"
 
 
@@ -702,7 +704,10 @@ def main():
         s_ach = s_bytes / (s_ms / 1e3) / 1e9 if s_ms > 0 else None
         tt_ = traffic_table(S.name)
         cfg_layers = len(cfg.fanouts)
-        g_kernel = gather_kernel_name(tt_)
+        pitch_ = (cfg.feat_dim + 3) // 4 * 4
+        l2_res = (sum(len(parts[q].indptr) - 1 for q in hosted) * pitch_ * 4
+                  <= torch.cuda.get_device_properties(local).L2_cache_size * 3 // 4)
+        g_kernel = gather_kernel_name(l2_res and pitch_ == cfg.feat_dim and pitch_ <= 256 and S.ppg <= 8)
         # k_relabel is bound by dependent random probes of L2-resident (bits, position) pairs, not bytes:
         # probes per window (counted by the kernel) / its event time vs the measured L2 random-load ceiling
         rl_ms = sp_["relabel_ms"] / max(sp_["relabel_calls"], 1)

@@ -19,7 +19,7 @@ if [ "$part" = single ] || [ "$part" = traffic ]; then
         timeout 900 ncu --cache-control none --clock-control none --kernel-name regex:"k_" \
             --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_bytes.sum \
             -s $([ $c = papers_s32 ] && echo 250 || echo 100) -c 100 --csv --log-file $OUT/launches_$c.csv \
-            python tools/exp_window.py --config $c --relabel-stream --windows 12 > $OUT/ncu_$c.log 2>&1
+            python tools/exp_window.py --config $c --relabel-stream --tuned --windows 12 > $OUT/ncu_$c.log 2>&1
         python tools/ncu_hbm_table.py $OUT/launches_$c.csv --json $OUT/traffic_$c.json --config $c \
             > $OUT/table_$c.txt 2>&1 && cp $OUT/traffic_$c.json profiles/r02/traffic_$c.json
     done

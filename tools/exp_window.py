@@ -35,7 +35,12 @@ def main():
     ap.add_argument("--parts", type=int, default=None)
     ap.add_argument("--tag", default="")
     ap.add_argument("--sm-split", type=int, default=0, help="gather-side SMs of mgnn_sm_partition (0 = off)")
+    ap.add_argument("--tuned", action="store_true", help="bench.py's launch tuning for the config (TUNING)")
     a = ap.parse_args()
+    if a.tuned:                                  # before the library's first launch reads them
+        for k_, v_ in bench.TUNING.get(a.config, {}).get("env", {}).items():
+            os.environ.setdefault(k_, v_)
+        a.prio_a = a.prio_a or bench.TUNING.get(a.config, {}).get("sampling_priority", 0) < 0
     S = bench.Setup(a.config, 1, parts=a.parts)
     g = synth.generate(S.cfg)
     parts = synth.partition(g, S.P)
