@@ -9,16 +9,19 @@
 //             R = {not buffered, S_A >= theta_r} with UNIQUE 64-bit keys
 //               E: S_E bits << 32 | node id             -> ascending = (S_E asc, id asc)      (R#16)
 //               R: ~S_A bits << 32 | rank_deg            -> ascending = (S_A desc, deg_in desc, id asc) (R#18)
-//             (rank_deg = position in the static (deg_in desc, id asc) order of the buffer init),
-//             plus a histogram of the top 12 key bits; the last block computes K = min(|E|, |R|)
-//             (R#19) and, per list, the threshold digit T below which the K smallest keys lie.
+//             (rank_deg = position in the static (deg_in desc, id asc) order of the buffer init;
+//             E is scanned in id order, R in that degree order, so each list is in its low word's
+//             order), plus a histogram of the top 12 key bits; on eviction windows it also applies
+//             the window's decay (k_decay folded in).  K = min(|E|, |R|) (R#19) and, per list, the
+//             threshold digit T below which the K smallest keys lie follow from the histograms.
 //   small |BUF| (<= kEvMax):
 //   k_cand    compacts the candidates (digit <= T) -- typically a few hundred;
 //   k_rank    ranks every candidate by counting smaller candidate keys (keys are unique, so the
 //             rank IS the sorted position) and writes the K winners in order: no sort at all.
-//   large |BUF|: k_hist2 + k_cand as above, then the onesweep radix sort (sort.cu) of the
-//             candidates only (all 8 key bytes: k_cand appends them unordered) -- K and a bucket
-//             instead of the whole lists; MGNN_EVICT_SORT=2 sorts the whole lists instead.
+//   large |BUF|: k_hist2 + k_cand_ord (order-preserving), then a stable radix sort (sort.cu) of the
+//             candidates' score word only (4 digits) -- K and a bucket instead of the whole lists;
+//             MGNN_EV_SELECT=0: unordered candidates from scoreboard scans, all 8 key bytes sorted;
+//             MGNN_EVICT_SORT=2 sorts the whole lists instead.
 //   k_swap_refill  pair i = (E[i], R[i]): swap of P:224, refill from the owner's table.
 #include <algorithm>
 
