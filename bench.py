@@ -144,6 +144,7 @@ class ClockSampler:
         self.stop = threading.Event()
         self.h = None
         self.max_mhz = None
+        self.period = float(os.environ.get("BENCH_CLOCK_PERIOD_MS", "1")) / 1e3
 
     def __enter__(self):
         try:
@@ -176,7 +177,7 @@ class ClockSampler:
                                   nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
             except Exception:
                 pass
-            time.sleep(0.001)
+            time.sleep(self.period)
 
     def __exit__(self, *a):
         self.stop.set()
