@@ -56,3 +56,34 @@ def test_layouts_and_policy_lookup():
     except SystemExit:
         pass
     assert bench.static_ucap(bench.Setup("products", 1)) == 2000 * 6 * 11 * 16
+
+
+def test_gather_kernel_name_follows_the_library_rule(monkeypatch):
+    """The roofline names the gather the library launches: flat by default, the TMA row gather only
+    under MGNN_GATHER=tma for L2-resident, unpadded rows (or MGNN_GATHER_G4=1), reg -> k_gather."""
+    import bench
+    monkeypatch.delenv("MGNN_GATHER", raising=False)
+    monkeypatch.delenv("MGNN_GATHER_G4", raising=False)
+    assert bench.gather_kernel_name(True) == "k_gather_flat"
+    monkeypatch.setenv("MGNN_GATHER", "tma")
+    assert bench.gather_kernel_name(True) == "k_gather_g4"
+    assert bench.gather_kernel_name(False) == "k_gather_tma"
+    monkeypatch.setenv("MGNN_GATHER_G4", "0")
+    assert bench.gather_kernel_name(True) == "k_gather_tma"
+    monkeypatch.setenv("MGNN_GATHER_G4", "1")
+    assert bench.gather_kernel_name(False) == "k_gather_g4"
+    monkeypatch.setenv("MGNN_GATHER", "reg")
+    assert bench.gather_kernel_name(True) == "k_gather"
+
+
+def test_launch_tuning_is_per_config_and_known():
+    """bench.TUNING only names configs bench.py knows and library variables the parity suite covers
+    (tests/test_gpu_variants.py runs each of these settings against the oracle)."""
+    import bench
+    known_env = {"MGNN_HOP_GRID_BPS", "MGNN_COMPACT_BPS", "MGNN_GATHER"}
+    for name, t in bench.TUNING.items():
+        assert name in bench.POLICY
+        assert set(t.get("env", {})) <= known_env
+        assert t.get("sampling_priority", 0) in (0, -1)
+    src = open(bench.__file__.replace("bench.py", "tests/test_gpu_variants.py")).read()
+    assert '"MGNN_HOP_GRID_BPS": "5", "MGNN_COMPACT_BPS": "5"' in src and '"MGNN_GATHER": "tma"' in src
