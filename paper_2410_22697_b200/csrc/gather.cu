@@ -748,16 +748,14 @@ void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, con
             return e ? atoi(e) : 4;
         }();
         const dim3 gf(gxf, w.n_inst), bf(kFThreads);
-        switch ((flat_bps > 6 ? 4 : flat_bps) * 16 + flat_unr) {   // > 6: more, shorter blocks of <4, 4>
+        // the variants measured without register spills (profiles/r02/gather_flat/exp_s10*); > 6 blocks per
+        // SM: more, shorter blocks of <4, 4>
+        switch ((flat_bps > 6 ? 4 : flat_bps) * 16 + flat_unr) {
             case 3 * 16 + 8: launch_k(k_gather_flat<8, 3>, gf, bf, 0, s, w, world); break;
             case 3 * 16 + 6: launch_k(k_gather_flat<6, 3>, gf, bf, 0, s, w, world); break;
             case 4 * 16 + 6: launch_k(k_gather_flat<6, 4>, gf, bf, 0, s, w, world); break;
-            case 5 * 16 + 4: launch_k(k_gather_flat<4, 5>, gf, bf, 0, s, w, world); break;
             case 5 * 16 + 2: launch_k(k_gather_flat<2, 5>, gf, bf, 0, s, w, world); break;
-            case 6 * 16 + 2: launch_k(k_gather_flat<2, 6>, gf, bf, 0, s, w, world); break;
             case 4 * 16 + 2: launch_k(k_gather_flat<2, 4>, gf, bf, 0, s, w, world); break;
-            case 4 * 16 + 5: launch_k(k_gather_flat<5, 4>, gf, bf, 0, s, w, world); break;
-            case 4 * 16 + 8: launch_k(k_gather_flat<8, 4>, gf, bf, 0, s, w, world); break;
             default: launch_k(k_gather_flat<4, 4>, gf, bf, 0, s, w, world); break;
         }
         count_launches(1, __func__, s);
