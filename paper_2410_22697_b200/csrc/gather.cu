@@ -748,7 +748,7 @@ void launch_gather(const WinDev& w, const WorldDev& world, bool l2_resident, con
             return e ? atoi(e) : 4;
         }();
         const dim3 gf(gxf, w.n_inst), bf(kFThreads);
-        // the variants measured without register spills (profiles/r02/gather_flat/exp_s10*); > 6 blocks per
+        // the measured variants (profiles/r02/gather_flat/exp_s10*, all parity-tested); > 6 blocks per
         // SM: more, shorter blocks of <4, 4>
         switch ((flat_bps > 6 ? 4 : flat_bps) * 16 + flat_unr) {
             case 3 * 16 + 8: launch_k(k_gather_flat<8, 3>, gf, bf, 0, s, w, world); break;
