@@ -4,10 +4,11 @@
 Tolerance.  The forward GEMMs and the backward GEMMs (k_wgrad, k_dgrad) multiply in
 3xTF32 by default (fp32-grade products, per-product error 3 u_tf32^2 ~ 2.9e-6), MGNN_SAGE_TF32=1 in one
 TF32 pass (u_tf32 = 2^-10); gradients are reduced with fp32 atomics in a data-dependent order.
-  * First DDP step (identical weights on both sides): ELEMENTWISE, |g - g_ref| <= the running bound of
-    grad_bounds() (rigorous worst case: operand errors propagated from the forward's running bound,
-    product errors, fp32 accumulation over the step's rows in any order, and ReLU units whose
-    pre-activation lies within its forward bound of 0 counted as masked either way).
+  * Every DDP step (one process): ELEMENTWISE, |g - g_ref| <= the running bound of grad_bounds()
+    (rigorous worst case: operand errors propagated from the forward's running bound, product errors,
+    fp32 accumulation over the step's rows in any order, ReLU units whose pre-activation lies within its
+    forward bound of 0 counted as masked either way, and the weights' drift from earlier SGD steps,
+    e_W <- (e_W + lr B_g)(1 + 2 u32) + 2 u32 (|W| + lr |g|)); the weights after SGD within e_W.
   * Every step, NORMWISE per tensor: ||g - g_ref|| <= REL_l ||g_ref||, and for the last layer per output
     row o ||g_o - g_ref_o|| <= REL_l (||g_ref_o|| + ||g_ref|| / sqrt(rows)), REL_l = REL 2^(L-1-l):
     REL = 16 u_tf32 = 1/64 for one TF32 pass (two TF32 products per layer forward and backward, times the
@@ -31,10 +32,12 @@ U32 = 2.0 ** -24
 U_TF32 = 2.0 ** -10
 
 
-def forward_bounds(X, blocks, weights, precision):
+def forward_bounds(X, blocks, weights, precision, e_w=None):
     """Per layer (h, e_h, mean, e_mean, z, e_z): the oracle's fp64 quantities and the running elementwise
     bounds on |GPU - exact| of the layer's input, neighbour means and pre-activation -- the recurrence of
-    tests/sage_util.error_bound (module doc there), kept layer by layer."""
+    tests/sage_util.error_bound (module doc there), kept layer by layer.  e_w: per layer elementwise
+    bounds (e_Ws, e_Wn, e_b) on |W_gpu - W_ref| after earlier SGD steps (None: identical weights); their
+    products with |input| + e_input join e_z."""
     h = np.asarray(X, np.float64)
     e = np.zeros_like(h)
     L = len(weights)
@@ -63,13 +66,16 @@ def forward_bounds(X, blocks, weights, precision):
         ws_, wn_, b_ = (np.asarray(a, np.float64) for a in weights[l])
         z = S.sage_layer(h, n, np.asarray(off), np.asarray(nbr), ws_, wn_, b_, relu=False)
         ez = 2.0 * (c * mag + (e[:n] @ ws.T + mean_err @ wn.T) * (1 + u_op) + U32 * np.abs(z))
+        if e_w is not None:                      # the GPU's weights differ from the oracle's by e_w
+            ews, ewn, eb = e_w[l]
+            ez += 2.0 * (((np.abs(h[:n]) + e[:n]) @ ews.T + (mean_abs + mean_err) @ ewn.T) * (1 + u_op) + eb)
         out.append((h, e, mean, mean_err, z, ez))
         h = np.maximum(z, 0.0) if l < L - 1 else z
         e = ez
     return out
 
 
-def grad_bounds(X, blocks, weights, labels, scale, n_acc, precision):
+def grad_bounds(X, blocks, weights, labels, scale, n_acc, precision, e_w=None):
     """Elementwise bounds on |GPU - exact| of one trainer's gradient contribution (scaled by `scale` =
     1 / n_trainers, as the GPU scales dlogits) per layer: [(dW_self, dW_neigh, db)].  A running bound
     through the backward, evaluated in fp64 from the oracle's own quantities (nothing from the CUDA path):
@@ -82,7 +88,7 @@ def grad_bounds(X, blocks, weights, labels, scale, n_acc, precision):
         for 3xTF32 products, 2 u_tf32 + u_tf32^2 for one TF32 pass, K the rows the step accumulates
         (n_acc[l], every trainer of the step: split-K partial sums and atomics in any order);
       * the neighbour scatter dH[j] += dZ_i W_neigh / deg(i) by fp32 atomics adds (count_j + 1) u32 sum |.|."""
-    fw = forward_bounds(X, blocks, weights, precision)
+    fw = forward_bounds(X, blocks, weights, precision, e_w)
     u_op = 3 * U_TF32 ** 2 if precision == "3xtf32" else 2 * U_TF32 + U_TF32 ** 2
     L = len(weights)
     zL, ezL = fw[-1][4], fw[-1][5]
@@ -132,11 +138,15 @@ def grad_bounds(X, blocks, weights, labels, scale, n_acc, precision):
             mag_s = adz @ aws
             dh_in[:n] += dz @ ws
             e_in[:n] += edz @ aws * (1 + u_op) + cK * mag_s
+            if e_w is not None:                  # dZ W with the GPU's weights
+                e_in[:n] += (adz + edz) @ e_w[l][0] * (1 + u_op)
             acc[:n] += mag_s
             cnt[:n] += 1
             dm = (dz @ wn) * inv
             mag_n = (adz @ awn) * inv
             e_n = (edz @ awn * (1 + u_op) + cK * (adz @ awn)) * inv + U32 * mag_n
+            if e_w is not None:
+                e_n += ((adz + edz) @ e_w[l][1] * (1 + u_op)) * inv
             for i in range(n):
                 nb = nbr[off[i]:off[i + 1]]
                 if len(nb):
@@ -207,6 +217,7 @@ def run_train_parity(g, P, D, fanouts, batch, dims, n_steps, lr=0.05, window=Non
     from tests.sage_util import gpu_precision
     precision = gpu_precision()
     REL = REL_3XTF32 if precision == "3xtf32" else REL_TF32
+    e_w = [tuple(np.zeros_like(np.asarray(a, np.float64)) for a in layer) for layer in ref_w]
     gsum = {}
     t = 1
     slot = 0
@@ -229,7 +240,7 @@ def run_train_parity(g, P, D, fanouts, batch, dims, n_steps, lr=0.05, window=Non
                 gpu_loss = float(lt.item())
             ref_g = None
             ref_loss = 0.0
-            first = done == 0 and not multi       # weights still identical on both sides: elementwise bounds
+            first = not multi                     # elementwise bounds at every step (weight drift in e_w)
             inst = []
             for pid in range(P):
                 _, blocks, X = oracle_instance(W.parts[pid], t + w, fanouts, batch)
@@ -245,7 +256,7 @@ def run_train_parity(g, P, D, fanouts, batch, dims, n_steps, lr=0.05, window=Non
                 n_acc = [sum(len(b[Ld - 1 - l][0]) - 1 for _, b, _ in inst) for l in range(Ld)]
                 bsum = None
                 for X_, b_, y_ in inst:
-                    bd = grad_bounds(X_, b_, ref_w, y_, 1.0 / P, n_acc, precision)
+                    bd = grad_bounds(X_, b_, ref_w, y_, 1.0 / P, n_acc, precision, e_w)
                     bsum = bd if bsum is None else [tuple(a + c for a, c in zip(x, y)) for x, y in zip(bsum, bd)]
                 for l in range(Ld):
                     for k, name in enumerate(("W_self", "W_neigh", "b")):
@@ -264,8 +275,18 @@ def run_train_parity(g, P, D, fanouts, batch, dims, n_steps, lr=0.05, window=Non
                                              rows=l == L - 1, rel=rel) / rel)
             ctx.sgd(lr)
             ref_w = S.sgd(ref_w, ref_g, lr)
+            if first:                             # W_gpu = fl(W - lr g_gpu): drift bound of the next step
+                Ld = len(dims) - 1
+                e_w = [tuple((ew + lr * bsum[l][k]) * (1 + 2 * U32)
+                             + 2 * U32 * (np.abs(ref_w[l][k]) + lr * np.abs(ref_g[l][k]))
+                             for k, ew in enumerate(e_w[l])) for l in range(Ld)]
             for l in range(len(dims) - 1):
                 got = ctx.params(l)
+                if first:                         # weights elementwise within the drift bound
+                    for k in range(3):
+                        errw = np.abs(np.asarray(got[k], np.float64) - ref_w[l][k])
+                        assert np.all(errw <= e_w[l][k] + 1e-30), ("weights elementwise", t + w, l, k,
+                                                                  float(np.max(errw / (e_w[l][k] + 1e-30))))
                 for k, name in enumerate(("W_self", "W_neigh", "b")):
                     gsum[(l, k)] = gsum.get((l, k), 0.0) + np.linalg.norm(ref_g[l][k])
                     err = np.linalg.norm(np.asarray(got[k], np.float64) - ref_w[l][k])
@@ -281,5 +302,5 @@ def run_train_parity(g, P, D, fanouts, batch, dims, n_steps, lr=0.05, window=Non
     ctx.close()
     W.close()
     print(f"[train parity] worst gradient error / tolerance {worst:.3f} (normwise, every step); "
-          f"first step elementwise worst |err| / bound {elem_worst:.3e} ({precision})")
+          f"elementwise (every step) worst |err| / bound {elem_worst:.3e} ({precision})")
     return worst
