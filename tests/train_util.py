@@ -4,7 +4,7 @@
 Tolerance.  The forward GEMMs and the backward GEMMs (k_wgrad, k_dgrad) multiply in
 3xTF32 by default (fp32-grade products, per-product error 3 u_tf32^2 ~ 2.9e-6), MGNN_SAGE_TF32=1 in one
 TF32 pass (u_tf32 = 2^-10); gradients are reduced with fp32 atomics in a data-dependent order.
-  * Every DDP step (one process): ELEMENTWISE, |g - g_ref| <= the running bound of grad_bounds()
+  * Every DDP step (one process or several ranks, the all-reduce's fp32 sum added): ELEMENTWISE, |g - g_ref| <= the running bound of grad_bounds()
     (rigorous worst case: operand errors propagated from the forward's running bound, product errors,
     fp32 accumulation over the step's rows in any order, ReLU units whose pre-activation lies within its
     forward bound of 0 counted as masked either way, and the weights' drift from earlier SGD steps,
@@ -240,8 +240,9 @@ def run_train_parity(g, P, D, fanouts, batch, dims, n_steps, lr=0.05, window=Non
                 gpu_loss = float(lt.item())
             ref_g = None
             ref_loss = 0.0
-            first = not multi                     # elementwise bounds at every step (weight drift in e_w)
+            first = True                          # elementwise bounds at every step (weight drift in e_w)
             inst = []
+            gabs = None                           # sum over trainers of |g_p| (the all-reduce's rounding)
             for pid in range(P):
                 _, blocks, X = oracle_instance(W.parts[pid], t + w, fanouts, batch)
                 F0 = W.parts[pid].frontier()[:W.parts[pid].hop_sizes()[0]]
@@ -251,6 +252,8 @@ def run_train_parity(g, P, D, fanouts, batch, dims, n_steps, lr=0.05, window=Non
                 ref_g = gr if ref_g is None else [tuple(a + b for a, b in zip(x, y)) for x, y in zip(ref_g, gr)]
                 if first:
                     inst.append((X, blocks, labels[F0]))
+                    ga = [tuple(np.abs(x) for x in layer) for layer in gr]
+                    gabs = ga if gabs is None else [tuple(a + b for a, b in zip(x, y)) for x, y in zip(gabs, ga)]
             if first:
                 Ld = len(dims) - 1
                 n_acc = [sum(len(b[Ld - 1 - l][0]) - 1 for _, b, _ in inst) for l in range(Ld)]
@@ -258,6 +261,11 @@ def run_train_parity(g, P, D, fanouts, batch, dims, n_steps, lr=0.05, window=Non
                 for X_, b_, y_ in inst:
                     bd = grad_bounds(X_, b_, ref_w, y_, 1.0 / P, n_acc, precision, e_w)
                     bsum = bd if bsum is None else [tuple(a + c for a, c in zip(x, y)) for x, y in zip(bsum, bd)]
+                if multi:                         # NCCL sum over the ranks' gradient buffers in fp32
+                    import torch.distributed as dist
+                    nr = dist.get_world_size()
+                    bsum = [tuple(b + (nr + 1) * U32 * (a + b) for a, b in zip(ga_, bs_))
+                            for ga_, bs_ in zip(gabs, bsum)]
                 for l in range(Ld):
                     for k, name in enumerate(("W_self", "W_neigh", "b")):
                         err = np.abs(np.asarray(gpu_g[l][k], np.float64) - ref_g[l][k])
