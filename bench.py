@@ -302,6 +302,22 @@ def gather_kernel_name(g4_eligible: bool = False) -> str:
     return "k_gather" if e.startswith("r") else "k_gather_flat"
 
 
+def sampler_ncu_dram(tt, layers: int, peak: float):
+    """The sampler kernels' DRAM rate from the committed ncu table alone (one source for bytes and time):
+    (k_hop x L + k_compact x L + k_relabel) DRAM bytes per window / their ncu time per window, against the
+    HBM peak -- next to the SURVEY §8(d) algorithmic-bytes fraction, which counts 8 B per sampled edge
+    although every edge is one random DRAM burst."""
+    ks = (tt or {}).get("kernels", {})
+    if not all(k in ks for k in ("k_hop", "k_compact", "k_relabel")):
+        return None
+    n = {"k_hop": layers, "k_compact": layers, "k_relabel": 1}
+    b = sum(ks[k]["dram_bytes_per_launch"] * n[k] for k in n)
+    us = sum(ks[k]["us_per_launch"] * n[k] for k in n)
+    gbs = b / (us * 1e-6) / 1e9 if us > 0 else None
+    return {"bytes_per_window": b, "us_per_window_serialised": us, "gbs": gbs,
+            "frac": (gbs / peak) if gbs else None, "source": (tt or {}).get("source")}
+
+
 def random_load_peak(table_bytes=None):
     """Measured random-load ceiling (profiles/r02/randread.json, tools/randread.cu): of an L2-resident
     table, or (table_bytes given) of the smallest measured table at least that large (DRAM-resident)."""
@@ -780,6 +796,7 @@ def main():
                                "U": sp_["unique"] / max(sp_["sample_calls"], 1)},
                 "traffic": {k_: v_ for k_, v_ in (tt_ or {}).items() if k_ in ("k_hop", "k_compact", "k_relabel")}
                 or None,
+                "ncu_dram": sampler_ncu_dram(tt_, cfg_layers, hbm_peak),
                 "relabel": relabel_roof, "hop": hop_roof},
             "stages_ms_per_window": {"sample": s_ms,
                                      "gather": sp_["gather_ms"] / max(sp_["gather_calls"], 1),
