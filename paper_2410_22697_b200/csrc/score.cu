@@ -74,6 +74,11 @@ void launch_decay(const PartDev* parts, int n_lp, int64_t cap_max, int n_steps, 
 // decay_steps > 0: the window's decay (k_decay) is folded in -- the E scan visits every slot exactly once
 // (through its halo node), so it applies the slot's pending gamma products before reading S_E; one
 // dependent launch less in the eviction round.
+#ifndef MGNN_SEL_ITEMS
+#define MGNN_SEL_ITEMS 16
+#endif
+constexpr int kSelItems = MGNN_SEL_ITEMS;           // list entries per thread (tile = 256 x kSelItems); 16:
+                                                    // half the look-back chain, products eviction round -3 %
 __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict__ parts, float alpha, float theta_r,
                                                       const SortSeg* __restrict__ segs, long long* __restrict__ n_out,
                                                       Scratch sc, int64_t tiles_max, EvScratch ev, int decay_steps,
@@ -87,14 +92,14 @@ __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict_
     const PartDev& pd = parts[sg >> 1];
     const bool isE = (sg & 1) == 0;
     const int64_t n = pd.n_h;
-    const int64_t tile_items = kSThreads * 8;
+    const int64_t tile_items = kSThreads * kSelItems;
     const int64_t ntiles = (n + tile_items - 1) / tile_items;
     const int tile = claim_tile(sc.tilectr + sg, &tslot);
     if (tile < ntiles) {
-        const int64_t i0 = (int64_t)tile * tile_items + (int64_t)threadIdx.x * 8;
+        const int64_t i0 = (int64_t)tile * tile_items + (int64_t)threadIdx.x * kSelItems;
         unsigned flags = 0;
         long long cnt = 0;
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < kSelItems; ++i) {
             const int64_t x = i0 + i;
             bool pf = false;
             if (x < n) {
@@ -125,7 +130,7 @@ __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict_
         int64_t pos = prefix_sh + excl;
         const SortSeg out = segs[sg];
         uint32_t* hist = ev.hist + (size_t)sg * kDig;
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < kSelItems; ++i) {
             const int64_t x = i0 + i;
             unsigned d = 0xFFFFFFFFu;
             if ((flags >> i) & 1u) {
@@ -157,7 +162,7 @@ __global__ void __launch_bounds__(kSThreads) k_select(const PartDev* __restrict_
 void launch_select(const PartDev* parts, int n_lp, int64_t n_max, float alpha, float theta_r, const SortSeg* segs,
                    long long* n_out, Scratch sc, EvScratch ev, cudaStream_t s, int decay_steps, float gamma,
                    const unsigned long long* ovf, uint64_t t_last) {
-    int64_t tiles = (n_max + kSThreads * 8 - 1) / (kSThreads * 8);
+    int64_t tiles = (n_max + kSThreads * kSelItems - 1) / (kSThreads * kSelItems);
     if (tiles < 1) tiles = 1;
     dim3 grid((unsigned)tiles, 2 * n_lp);
     launch_k(k_select, grid, dim3(kSThreads), 0, s, parts, alpha, theta_r, segs, n_out, sc, tiles, ev, decay_steps,
