@@ -441,16 +441,16 @@ __global__ void __launch_bounds__(kSThreads) k_cand_ord(const SortSeg* __restric
         ev.thr[2 * sg + 1] = T;
     }
     if (T < 0) return;                           // same answer in every block of the segment
-    const int64_t tile_items = kSThreads * 8;
+    const int64_t tile_items = kSThreads * kSelItems;
     const int64_t ntiles = (n + tile_items - 1) / tile_items;
     const int tile = claim_tile(sc.tilectr + sg, &tslot);
     if (tile >= ntiles) return;
-    const int64_t i0 = (int64_t)tile * tile_items + (int64_t)threadIdx.x * 8;
-    unsigned long long k[8];
+    const int64_t i0 = (int64_t)tile * tile_items + (int64_t)threadIdx.x * kSelItems;
+    unsigned long long k[kSelItems];
     unsigned flags = 0;
     long long cnt = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kSelItems; ++i) {
         k[i] = i0 + i < n ? S.keys[i0 + i] : ~0ull;
         const long long d1 = (long long)(k[i] >> 52);
         const bool c = i0 + i < n && (d1 < T || (d1 == T && (long long)((k[i] >> 40) & 0xFFF) <= T2));
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(kSThreads) k_cand_ord(const SortSeg* __restric
     __syncthreads();
     long long pos = prefix_sh + excl;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < kSelItems; ++i)
         if ((flags >> i) & 1u) {
             S.keys_tmp[pos] = k[i];
             S.vals_tmp[pos] = S.vals[i0 + i];
@@ -529,7 +529,7 @@ void launch_cand_ord(const SortSeg* segs, int n_lp, int64_t n_max, EvScratch ev,
     const unsigned cap_blocks = 64u;
     dim3 g1(blocks_for(n_max, kSThreads) > cap_blocks ? cap_blocks : blocks_for(n_max, kSThreads), 2 * n_lp);
     launch_k(k_hist2, g1, dim3(kSThreads), 0, s, segs, ev, (const PartDev*)nullptr, 0.0f, 0.0f);
-    int64_t tiles = (n_max + kSThreads * 8 - 1) / (kSThreads * 8);
+    int64_t tiles = (n_max + kSThreads * kSelItems - 1) / (kSThreads * kSelItems);
     if (tiles < 1) tiles = 1;
     launch_k(k_cand_ord, dim3((unsigned)tiles, 2 * n_lp), dim3(kSThreads), 0, s, segs, ev, sc, tiles_max);
     count_launches(2, __func__, s);
